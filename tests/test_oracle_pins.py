@@ -1,0 +1,348 @@
+"""Pins for the CPU oracle (O1 map, S1 structural LSM) -- CPU only.
+
+Each test pins the oracle to something other than itself: the paper's and
+SPEC's worked examples (tests/golden/*.lsm, each with its citation), closed
+forms of the merge work, structural invariants
+(PAPER.md:377-382, 417-429), and brute force O0 (oracle/brute.py) on
+exhaustive tiny schedules.
+"""
+import itertools
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests import lsm_script
+
+
+class OracleAdapter:
+    """Structure from S1; every query answered by S1 (paper pipeline) AND O1
+    (definition), asserted equal."""
+
+    def __init__(self, b):
+        self.s1 = oracle.ShadowLSM(b)
+        self.o1 = oracle.OracleDict(b)
+
+    def update(self, k, v, d):
+        self.s1.update(k, v, d)
+        self.o1.apply_batch(k, v, d)
+
+    def lookup(self, q):
+        a = self.s1.lookup(q)
+        b = self.o1.lookup(q)
+        assert np.array_equal(a[1], b[1]) and np.array_equal(a[0], b[0])
+        return a
+
+    def count(self, k1, k2):
+        a = self.s1.count(k1, k2)
+        assert np.array_equal(a, self.o1.count(k1, k2))
+        return a
+
+    def range(self, k1, k2):
+        a = self.s1.range(k1, k2)
+        b = self.o1.range(k1, k2)
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
+        return a
+
+    def cleanup(self):
+        self.s1.cleanup()
+        self.o1.cleanup()
+        assert self.s1.r == self.o1.r
+
+    @property
+    def r(self):
+        return self.s1.r
+
+    @property
+    def merged_records(self):
+        return self.s1.merged_records
+
+    def level(self, i):
+        return self.s1.level(i)
+
+    def num_levels(self):
+        return self.s1.num_levels()
+
+
+@pytest.mark.parametrize("path", lsm_script.golden_files(), ids=lambda p: p.split("/")[-1])
+def test_golden_scripts(path):
+    lsm_script.run(path, OracleAdapter)
+
+
+def test_text_dump_matches_script_dump():
+    s = oracle.ShadowLSM(4)
+    s.update(np.array([3, 7], np.uint32), np.array([1, 2], np.uint32), np.array([0, 1], np.uint8))
+    assert oracle.dump_text(s) == "lsm b=4 r=1\nlevel 0: 3:R:1 7:T:0 " \
+        "2147483647:T:0 2147483647:T:0"
+
+
+def test_bounds_spec_examples():
+    # keys [2,4,4,9] (original keys; packed = k<<1|1)
+    packed = [(k << 1) | 1 for k in (2, 4, 4, 9)]
+    assert oracle.lower_bound(packed, 4) == 1
+    assert oracle.lower_bound(packed, 10) == 4
+    assert oracle.upper_bound(packed, 4) == 3
+    assert oracle.upper_bound(packed, 1) == 0
+    # status bit ignored: a tombstone 4 is still "equal" to 4
+    packed2 = [(2 << 1) | 1, (4 << 1), (4 << 1) | 1, (9 << 1)]
+    assert oracle.lower_bound(packed2, 4) == 1 and oracle.upper_bound(packed2, 4) == 3
+    # query keys >= 2^31 compared unshifted (R8): never equal to a stored key
+    assert oracle.lower_bound(packed, 0xFFFFFFFF) == 4
+
+
+def test_bounds_vs_linear_scan_exhaustive():
+    # bounds match linear scans on sorted inputs (brute force)
+    rng = np.random.default_rng(1)
+    for n in range(0, 20):
+        for _ in range(20):
+            ks = np.sort(rng.integers(0, 6, n)) if n else np.zeros(0, np.int64)
+            st = rng.integers(0, 2, n)
+            packed = [(int(k) << 1) | int(s) for k, s in zip(ks, st)]
+            for q in range(-0, 8):
+                lb = next((i for i, k in enumerate(ks) if k >= q), n)
+                ub = next((i for i, k in enumerate(ks) if k > q), n)
+                assert oracle.lower_bound(packed, q) == lb
+                assert oracle.upper_bound(packed, q) == ub
+
+
+def _ffz(r):
+    t = 0
+    while (r >> t) & 1:
+        t += 1
+    return t
+
+
+@pytest.mark.parametrize("b", [1, 3, 8])
+def test_merge_work_closed_form_and_occupancy(b):
+    # T_ins(r) = T_sort + (2^ffz(r)-1) T_merge  =>  each insert
+    # at r writes exactly 2b(2^ffz(r)-1) merged records.
+    # occupied levels are the set bits of r.
+    s = oracle.ShadowLSM(b)
+    total = 0
+    for r in range(0, 70):
+        before = s.merged_records
+        k, v, d = synth.updates(7, r * b, b, delete_frac4=1)
+        s.update(k, v, d)
+        delta = s.merged_records - before
+        assert delta == 2 * b * (2 ** _ffz(r) - 1)
+        total += delta
+        R = r + 1
+        occ = [i for i in range(s.num_levels()) if len(s.level(i)[0]) > 0]
+        assert occ == [i for i in range(R.bit_length()) if (R >> i) & 1]
+        for i in occ:
+            assert len(s.level(i)[0]) == b << i
+        # amortized bound
+        assert s.merged_records <= 2 * b * R * math.ceil(math.log2(R + 1))
+        # exact closed form at R = 2^m (derived): b * R * log2 R
+        if R & (R - 1) == 0:
+            assert s.merged_records == b * R * int(math.log2(R))
+
+
+def test_building_invariants_random():
+    # (1) each level sorted by key; (2) within a segment,
+    # newest first; (3) within one batch, tombstones before regulars (R3).
+    b = 16
+    s = oracle.ShadowLSM(b)
+    for j in range(40):
+        k, v, d = synth.updates(11, j * b, b, delete_frac4=2, alphabet=24)
+        s.update(k, v, d)
+        for i in range(s.num_levels()):
+            keys, vals, tags = s.level(i, with_tags=True)
+            if len(keys) == 0:
+                continue
+            orig = keys >> 1
+            assert np.all(orig[1:] >= orig[:-1])
+            same = orig[1:] == orig[:-1]
+            assert np.all(tags[1:][same] <= tags[:-1][same])          # (2)
+            same_batch = same & (tags[1:] == tags[:-1])
+            assert np.all((keys[1:] & 1)[same_batch] >= (keys[:-1] & 1)[same_batch])  # (3)
+            assert np.all(vals[(keys & 1) == 0] == 0)  # R6
+
+
+def _sorted_by_definition(recs):
+    # stable sort by packed key: explicit (key, input index)
+    return [r for _, _, r in sorted((r[0], i, r) for i, r in enumerate(recs))]
+
+
+def test_sort_and_merge_exhaustive_tiny():
+    # merge == stable sort keyed on (original key, source
+    # newer=0/older=1, index), exhaustive over a 3-key alphabet with ops {I,D},
+    # b = 2 (combined merge size 4) plus all single batches of b = 3.
+    ops = [(k, d) for k in range(3) for d in (0, 1)]
+    for b, nb in ((3, 1), (2, 2)):
+        for combo in itertools.product(ops, repeat=b * nb):
+            s = oracle.ShadowLSM(b)
+            sorted_batches = []
+            for j in range(nb):
+                part = combo[j * b:(j + 1) * b]
+                keys = np.array([k for k, _ in part], np.uint32)
+                dels = np.array([d for _, d in part], np.uint8)
+                vals = np.arange(j * b + 1, (j + 1) * b + 1, dtype=np.uint32)
+                s.update(keys, vals, dels)
+                recs = [((int(k) << 1) | (0 if d else 1), 0 if d else int(v))
+                        for k, d, v in zip(keys, dels, vals)]
+                sorted_batches.append(_sorted_by_definition(recs))
+            if nb == 1:
+                exp = sorted_batches[0]
+                lvl = 0
+            else:
+                newer, older = sorted_batches[1], sorted_batches[0]
+                tagged = [(r[0] >> 1, 0, i, r) for i, r in enumerate(newer)] + \
+                         [(r[0] >> 1, 1, i, r) for i, r in enumerate(older)]
+                exp = [t[3] for t in sorted(tagged)]
+                lvl = 1
+            k, v = s.level(lvl)
+            assert list(zip(k.tolist(), v.tolist())) == exp, combo
+
+
+def _random_schedule_check(b, nbatch, alphabet, seed, frac4, brute=False):
+    s = oracle.ShadowLSM(b)
+    o = oracle.OracleDict(b)
+    o0 = oracle.BruteDict() if brute else None
+    dom = alphabet + 2
+    for j in range(nbatch):
+        k, v, d = synth.updates(seed, j * b, b, delete_frac4=frac4, alphabet=alphabet)
+        s.update(k, v, d)
+        o.apply_batch(k, v, d)
+        if o0 is not None:
+            o0.apply_batch(k, v, d)
+        q = np.arange(dom, dtype=np.uint32)
+        sv, sf = s.lookup(q)
+        ov, of = o.lookup(q)
+        assert np.array_equal(sf, of) and np.array_equal(sv[sf == 1], ov[of == 1])
+        k1 = synth.uniform_u32(seed + j, 6, 40) % np.uint32(dom)
+        k2 = synth.uniform_u32(seed + j, 7, 40) % np.uint32(dom)
+        assert np.array_equal(s.count(k1, k2), o.count(k1, k2))
+        for x, y in zip(s.range(k1, k2), o.range(k1, k2)):
+            assert np.array_equal(x, y)
+        if o0 is not None:
+            for qq in range(dom):
+                bv = o0.lookup(qq)
+                assert (bv is None) == (of[qq] == 0)
+                if bv is not None:
+                    assert bv == ov[qq]
+            for a1, a2 in zip(k1[:10], k2[:10]):
+                assert o0.count(a1, a2) == int(o.count([a1], [a2])[0])
+                off, ks, vs = o.range([a1], [a2])
+                assert o0.range(a1, a2) == list(zip(ks.tolist(), vs.tolist()))
+    return s, o
+
+
+def test_o1_vs_brute_exhaustive_tiny():
+    # Whole-pipeline brute force: b = 2, 3-key alphabet,
+    # ops {I, D}, all schedules of 2 batches; O0 vs O1 vs S1.
+    ops = [(k, d) for k in range(3) for d in (0, 1)]
+    b = 2
+    for combo in itertools.product(ops, repeat=2 * b):
+        s = oracle.ShadowLSM(b)
+        o = oracle.OracleDict(b)
+        o0 = oracle.BruteDict()
+        for j in range(2):
+            part = combo[j * b:(j + 1) * b]
+            keys = np.array([k for k, _ in part], np.uint32)
+            dels = np.array([d for _, d in part], np.uint8)
+            vals = np.arange(j * b + 1, (j + 1) * b + 1, dtype=np.uint32)
+            for m in (s.update, o.apply_batch, o0.apply_batch):
+                m(keys, vals, dels)
+            q = np.arange(4, dtype=np.uint32)
+            sv, sf = s.lookup(q)
+            ov, of = o.lookup(q)
+            for qq in range(4):
+                bv = o0.lookup(qq)
+                assert (bv is None) == (of[qq] == 0) == (sf[qq] == 0), combo
+                if bv is not None:
+                    assert bv == ov[qq] == sv[qq], combo
+            assert o0.count(0, 3) == int(o.count([0], [3])[0]) == int(s.count([0], [3])[0])
+        s.cleanup()
+        sv2, sf2 = s.lookup(np.arange(4, dtype=np.uint32))
+        assert np.array_equal(sf2, of) and np.array_equal(sv2[sf2 == 1], ov[of == 1])
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_schedules_with_brute(seed):
+    _random_schedule_check(b=4, nbatch=12, alphabet=10, seed=seed, frac4=2, brute=True)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_schedules_s1_vs_o1(seed):
+    # SPEC.md:499 acceptance 1 (scaled): duplicate-heavy alphabets, mixed
+    s, o = _random_schedule_check(b=64, nbatch=33, alphabet=300, seed=100 + seed, frac4=1)
+    # cleanup transparency + idempotence
+    q = np.arange(302, dtype=np.uint32)
+    before = s.lookup(q)
+    k1 = np.array([0, 5, 100], np.uint32)
+    k2 = np.array([301, 50, 99], np.uint32)
+    rb = s.range(k1, k2)
+    s.cleanup()
+    o.cleanup()
+    after = s.lookup(q)
+    assert np.array_equal(before[1], after[1]) and np.array_equal(before[0], after[0])
+    for x, y in zip(rb, s.range(k1, k2)):
+        assert np.array_equal(x, y)
+    assert s.r == o.r == -(-len(o) // 64)
+    imgs = [s.level(i) for i in range(s.num_levels())]
+    s.cleanup()
+    for i, (k, v) in enumerate(imgs):
+        k2_, v2_ = s.level(i)
+        assert np.array_equal(k, k2_) and np.array_equal(v, v2_)
+    # only placebo tombstones remain; no duplicate original keys
+    allk = np.concatenate([s.level(i)[0] for i in range(s.num_levels())])
+    tomb = allk[(allk & 1) == 0]
+    assert np.all(tomb == 0xFFFFFFFE)
+    live = allk[(allk & 1) == 1] >> 1
+    assert len(np.unique(live)) == len(live) == len(o)
+
+
+def test_cleanup_image_derivable_from_o1():
+    # post-cleanup image = sorted live pairs of O1 encoded
+    # (k<<1)|1, then r'b-|S| placebos, sliced into the set bits of r' ascending.
+    b = 8
+    s, o = _random_schedule_check(b=b, nbatch=21, alphabet=60, seed=5, frac4=2)
+    s.cleanup()
+    o.cleanup()
+    k, v = o.items()
+    img_k = np.concatenate([(k.astype(np.uint64) << 1 | 1).astype(np.uint32),
+                            np.full(o.r * b - len(k), 0xFFFFFFFE, np.uint32)])
+    img_v = np.concatenate([v, np.zeros(o.r * b - len(k), np.uint32)])
+    off = 0
+    for i in range(64):
+        if (o.r >> i) & 1:
+            sk, sv = s.level(i)
+            n = b << i
+            assert np.array_equal(sk, img_k[off:off + n]) and np.array_equal(sv, img_v[off:off + n])
+            off += n
+    assert off == len(img_k)
+
+
+def test_count_candidates_scale_with_L():
+    # SPEC.md:506 (acceptance 8): mean candidates for L=1024 is 128x L=8 (±20%)
+    b = 1 << 12
+    s = oracle.ShadowLSM(b)
+    for j in range(16):
+        k, v, d = synth.updates(3, j * b, b, delete_frac4=0)
+        s.update(k, v, d)
+    n = 16 * b
+    cands = []
+    for L in (8, 1024):
+        k1, k2 = synth.range_queries(3, 400, n, L)
+        _, c = s.count(k1, k2, return_candidates=True)
+        cands.append(c / 400)
+    assert 0.8 * 128 <= cands[1] / cands[0] <= 1.2 * 128
+
+
+def test_out_of_domain_key_dropped_with_flag():
+    # R5: keys >= 2^31-1 become placebos (S1) / are dropped (O1)
+    s = oracle.ShadowLSM(4)
+    o = oracle.OracleDict(4)
+    k = np.array([5, 0x7FFFFFFF, 0xFFFFFFFF, 6], np.uint32)
+    v = np.array([1, 2, 3, 4], np.uint32)
+    d = np.zeros(4, np.uint8)
+    s.update(k, v, d)
+    o.apply_batch(k, v, d)
+    assert s.domain_error
+    assert len(o) == 2
+    kk, vv = s.level(0)
+    assert kk.tolist() == [11, 13, 0xFFFFFFFE, 0xFFFFFFFE]
