@@ -1,0 +1,371 @@
+#!/usr/bin/env python3
+"""bench.py -- GPU LSM hot path on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
+
+Workload (N=1): BASELINE.json configs[2] ("C3"): b = 2^20, 64 mixed batches
+(75% insert / 25% delete) from empty -> 2^26 resident records, then 2^24
+lookups (50% hit), 2^24 counts and 2^24 ranges at expected length L = 8,
+cleanup, and the same queries again. One STEP = that whole cycle (every row of
+SURVEY.md §8(a)). `value` = M updates/s over the update phase of the timed
+steps (device time, CUDA events); the query and cleanup rates are reported in
+`queries` / `cleanup`. Inputs (600 MB of updates, 512 MB structure) exceed
+the 126 MB L2, so no explicit flush is needed.
+
+N > 1: the key-range sharded LSM (paper_1707_05354_b200.sharded): the global
+batch b_global = N * 2^20 is generated across ranks, routed to key owners by
+the bucket kernel + NCCL all-to-all, and inserted into each rank's LSM.
+Weak scaling; timing is the max over ranks.
+
+--impl reference: the CPU oracle (oracle/, std::map) on the same config,
+bounded samples per step (the reference arm of this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+B = 1 << 20
+R = 64
+NQ = 1 << 24
+L_RANGE = 8
+METRIC = "M updates/s at batch b; M lookup/count/range queries/s; HBM GB/s vs peak"
+UNIT = "M updates/s"
+WORKLOAD = ("C3: b=2^20, 64 mixed batches (75% insert/25% delete) from empty -> 2^26 "
+            "resident; 2^24 lookups (50% hit), 2^24 count + 2^24 range at L=8, before "
+            "and after lsm_cleanup")
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """Samples SM clocks + throttle reasons with NVML during the timed region."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x2: "applications_clocks_setting"}
+
+    def __init__(self, index=0):
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.hdl = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.hdl, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.hdl, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.hdl)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def cpu_baseline_oracle(seconds_budget=15.0):
+    """The oracle O1 (std::map, 1 thread) on a bounded sample of C3."""
+    import oracle
+    seed = synth.SEED_BASE + 2
+    o = oracle.OracleDict(B)
+    nb = 0
+    t0 = time.perf_counter()
+    batches = []
+    for j in range(8):
+        batches.append(synth.updates(seed, j * B, B, delete_frac4=1))
+    t0 = time.perf_counter()
+    for j, (k, v, d) in enumerate(batches):
+        o.apply_batch(k, v, d)
+        nb += 1
+        if time.perf_counter() - t0 > seconds_budget * 0.6:
+            break
+    t_upd = time.perf_counter() - t0
+    q = synth.lookup_queries(seed, 1 << 20, nb * B)
+    t1 = time.perf_counter()
+    o.lookup(q)
+    t_lk = time.perf_counter() - t1
+    return {"value": nb * B / t_upd / 1e6, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"first {nb} of 64 C3 batches ({nb}x2^20 mixed updates into a std::map), "
+                      f"then 2^20 lookups",
+            "lookup_mqps": (1 << 20) / t_lk / 1e6}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle on this arm's config (bounded samples)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    seed = synth.SEED_BASE + 2
+    per_step = 2  # batches of 2^20 per step (bounded sample)
+    data = [synth.updates(seed, j * B, B, delete_frac4=1) for j in range(per_step)]
+    times = []
+    for it in range(args.warmup + args.steps):
+        o = oracle.OracleDict(B)
+        t0 = time.perf_counter()
+        for k, v, d in data:
+            o.apply_batch(k, v, d)
+        dt = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    value = args.steps * per_step * B / tot / 1e6
+    sample = f"{per_step} C3 batches (2x2^20 mixed updates) into a fresh std::map per step"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "b": B, "batches": R},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_native(args):
+    import torch
+    import paper_1707_05354_b200 as pkg
+    from paper_1707_05354_b200 import to_device
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        from paper_1707_05354_b200.sharded import run_sharded_bench
+        return run_sharded_bench(args, dist, rank, world, local_rank)
+
+    seed = synth.SEED_BASE + 2
+    dev = torch.device("cuda", local_rank)
+    # ---- inputs resident in HBM before timing ----
+    t0 = time.time()
+    keys_d, vals_d, ops_d = [], [], []
+    host_batches = []
+    for j in range(R):
+        k, v, d = synth.updates(seed, j * B, B, delete_frac4=1)
+        keys_d.append(to_device(k, dev))
+        vals_d.append(to_device(v, dev))
+        ops_d.append(to_device(d, dev))
+        if args.e2e:
+            host_batches.append((torch.from_numpy(k.view(np.int32)).pin_memory(),
+                                 torch.from_numpy(v.view(np.int32)).pin_memory(),
+                                 torch.from_numpy(d).pin_memory()))
+    n_res = R * B
+    q_look = to_device(synth.lookup_queries(seed, NQ, n_res), dev)
+    k1, k2 = synth.range_queries(seed, NQ, n_res, L_RANGE)
+    k1_d, k2_d = to_device(k1, dev), to_device(k2, dev)
+    gen_s = time.time() - t0
+    lv = torch.empty(NQ, dtype=torch.int32, device=dev)
+    lf = torch.empty(NQ, dtype=torch.uint8, device=dev)
+    cnt = torch.empty(NQ, dtype=torch.int32, device=dev)
+    roff = torch.empty(NQ + 1, dtype=torch.int64, device=dev)
+    rcap = 16 * NQ
+    rk = torch.empty(rcap, dtype=torch.int32, device=dev)
+    rv = torch.empty(rcap, dtype=torch.int32, device=dev)
+
+    lsm = pkg.GpuLSM(B, reserve_batches=R)
+    stream = torch.cuda.current_stream()
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def step(record):
+        e = [ev() for _ in range(10)]
+        lsm.clear()
+        e[0].record(stream)
+        for j in range(R):
+            lsm.update(keys_d[j], vals_d[j], ops_d[j])
+        e[1].record(stream)
+        lsm.lookup_into(q_look, lv, lf)
+        e[2].record(stream)
+        lsm.count_into(k1_d, k2_d, cnt)
+        e[3].record(stream)
+        tot_pre = lsm.range_into(k1_d, k2_d, roff, rk, rv)
+        e[4].record(stream)
+        lsm.cleanup()
+        e[5].record(stream)
+        lsm.lookup_into(q_look, lv, lf)
+        e[6].record(stream)
+        lsm.count_into(k1_d, k2_d, cnt)
+        e[7].record(stream)
+        tot_post = lsm.range_into(k1_d, k2_d, roff, rk, rv)
+        e[8].record(stream)
+        if record is not None:
+            record.append((e, tot_pre, tot_post))
+
+    # warm-up
+    for _ in range(args.warmup):
+        step(None)
+    torch.cuda.synchronize()
+    levels_before = bin(R).count("1")
+    recs = []
+    l0 = lsm.launch_count
+    lsm.profile_enable(True)
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize()
+        start, stop = ev(), ev()
+        start.record(stream)
+        for _ in range(args.steps):
+            step(recs)
+        stop.record(stream)
+        torch.cuda.synchronize()
+    prof = lsm.profile_read()
+    lsm.profile_enable(False)
+    launches = lsm.launch_count - l0
+    total_ms = start.elapsed_time(stop)
+    ph = np.zeros(8)
+    for e, _, _ in recs:
+        for i in range(8):
+            ph[i] += e[i].elapsed_time(e[i + 1])
+    ph /= args.steps
+    r_after = lsm.r
+    upd_ms = ph[0]
+    value = R * B / (upd_ms * 1e-3) / 1e6
+
+    # ---- roofline of the dominant kernel class ----
+    peak, peak_src = measured_peaks()
+    dom = max(prof, key=lambda c: prof[c]["ms"])
+    ach = prof[dom]["alg_bytes"] / (prof[dom]["ms"] * 1e-3) / 1e9 if prof[dom]["ms"] else 0.0
+    step_kernel_ms = sum(p["ms"] for p in prof.values())
+    traffic = None
+    summ = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(summ):
+        with open(summ) as f:
+            tr = json.load(f)
+        if dom in tr:
+            traffic = tr[dom].get("dram_bytes_per_launch_model_scaled")
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak,
+                "peak_source": peak_src, "unit": "GB/s", "frac": ach / peak,
+                "traffic": traffic,
+                "share_of_step_kernel_time": prof[dom]["ms"] / step_kernel_ms if step_kernel_ms else None}
+    per_class = {c: {"ms_per_step": p["ms"] / args.steps,
+                     "launches_per_step": p["launches"] / args.steps,
+                     "alg_GBps": (p["alg_bytes"] / (p["ms"] * 1e-3) / 1e9) if p["ms"] else None,
+                     "frac_of_peak": ((p["alg_bytes"] / (p["ms"] * 1e-3) / 1e9) / peak) if p["ms"] else None}
+                 for c, p in prof.items() if p["launches"]}
+    queries = {
+        "nq": NQ, "L": L_RANGE,
+        "lookup_mqps_before_cleanup": NQ / (ph[1] * 1e-3) / 1e6,
+        "count_mqps_before_cleanup": NQ / (ph[2] * 1e-3) / 1e6,
+        "range_mqps_before_cleanup": NQ / (ph[3] * 1e-3) / 1e6,
+        "lookup_mqps_after_cleanup": NQ / (ph[5] * 1e-3) / 1e6,
+        "count_mqps_after_cleanup": NQ / (ph[6] * 1e-3) / 1e6,
+        "range_mqps_after_cleanup": NQ / (ph[7] * 1e-3) / 1e6,
+        "levels_before_cleanup": levels_before,
+        "levels_after_cleanup": bin(r_after).count("1"),
+        "range_pairs_before": recs[-1][1], "range_pairs_after": recs[-1][2],
+    }
+    cleanup = {"ms": ph[4], "melem_per_s": n_res / (ph[4] * 1e-3) / 1e6,
+               "r_after": r_after}
+
+    # ---- e2e: updates through the public API from pinned host buffers ----
+    e2e = None
+    if args.e2e:
+        def e2e_step():
+            lsm.clear()
+            for (hk, hv, hd) in host_batches:
+                lsm.update_host(hk, hv, hd)
+            lsm.sync()  # D2H of the sticky status word: the step's result
+        for _ in range(1):
+            e2e_step()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / args.steps
+        e2e = {"value": R * B / dt / 1e6, "unit": UNIT,
+               "h2d_bytes_per_step": R * B * 9, "d2h_bytes_per_step": 4,
+               "note": "lsm_update_host x64 (pinned H2D inside) + lsm_sync, wall clock"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u32", "data": "synthetic (splitmix64 uniform 31-bit keys)",
+        "config": {"workload": WORKLOAD, "b": B, "batches": R, "resident": n_res,
+                   "mix": "75% insert / 25% delete", "nq": NQ, "L": L_RANGE,
+                   "l2": "inputs larger than L2 (600 MB updates, 512 MB levels) -- no flush"},
+        "update_ms_per_step": upd_ms,
+        "phase_ms": {"update": ph[0], "lookup": ph[1], "count": ph[2], "range": ph[3],
+                     "cleanup": ph[4], "lookup_post": ph[5], "count_post": ph[6],
+                     "range_post": ph[7]},
+        "queries": queries, "cleanup": cleanup,
+        "roofline": roofline, "kernels": per_class,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "input_gen_s": gen_s,
+    }
+    if args.cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_oracle()
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_native(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,218 @@
+/*
+ * gpulsm.h -- C ABI of the B200-native GPU LSM batched-update hot path.
+ *
+ * The GPU LSM (Ashkiani et al., arXiv 1707.05354; /root/reference/PAPER.md) is
+ * a dynamic dictionary of 32-bit keys and 32-bit values kept as
+ * levels of sizes b*2^i, each completely full or completely empty; the full
+ * levels are the set bits of the resident batch count r (PAPER.md:289-291,
+ * 377-382). Updates arrive in batches of b; queries in
+ * batches of any size.
+ *
+ * Conventions for every entry point
+ *  - All data pointers named d_* are DEVICE pointers owned by the caller; the
+ *    library reads/writes them stream-ordered on `stream` (a cudaStream_t
+ *    passed as void*, NULL = legacy default stream). Inputs must stay live
+ *    until the stream reaches the operation. h_* pointers are HOST pointers.
+ *  - The handle owns the level storage and all scratch. It is bound to the
+ *    device current at lsm_create. Mutations (insert/delete/update/cleanup)
+ *    need exclusive access ("updates and queries are performed in separate
+ *    phases"); queries may run concurrently with each other.
+ *  - Host-detectable errors (NULL pointers, n == 0 or n > b, ...) return
+ *    immediately and enqueue nothing. Device-detected errors are STICKY and
+ *    reported by lsm_sync / lsm_range / lsm_cleanup. Nothing is thrown.
+ *  - Keys: user ("original") keys lie in [0, LSM_MAX_KEY] (31-bit domain of
+ *    PAPER.md:609 minus the reserved placebo key 2^31-1).
+ *    Query keys may be any 32-bit word; keys outside the domain are absent.
+ *  - Values are arbitrary 32-bit words. A lookup miss writes LSM_NOT_FOUND
+ *    into the value slot; use d_found_out to tell it from a stored 0xFFFFFFFF.
+ *  - Readings of silent/ambiguous passages: DESIGN.md §3 (R1..R22).
+ */
+#ifndef GPULSM_H
+#define GPULSM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default) /* exported even under -fvisibility=hidden */
+#endif
+
+typedef struct lsm lsm_t;
+
+typedef enum {
+  LSM_OK = 0,
+  LSM_ERR_INVALID_ARG = 1,  /* NULL handle/pointer, bad b, bad level index   */
+  LSM_ERR_BATCH_SIZE = 2,   /* update with n == 0 or n > b                   */
+  LSM_ERR_KEY_DOMAIN = 3,   /* sticky: an update key > LSM_MAX_KEY was seen;
+                               that record was stored as a placebo (dropped)  */
+  LSM_ERR_CAPACITY = 4,     /* lsm_range output larger than `capacity`       */
+  LSM_ERR_OOM = 5,          /* device allocation failed                      */
+  LSM_ERR_CUDA = 6,         /* CUDA runtime error (launch/sync)              */
+  LSM_ERR_NO_DEVICE = 7     /* no CUDA device / not an sm_100 device         */
+} lsm_status;
+
+#define LSM_MAX_KEY 0x7FFFFFFEu   /* user keys in [0, 2^31-2]                 */
+#define LSM_PLACEBO 0xFFFFFFFEu   /* key variable of a placebo: key 2^31-1,
+                                     tombstone status      */
+#define LSM_NOT_FOUND 0xFFFFFFFFu /* value written for ⊥       */
+#define LSM_MAX_LEVELS 40
+
+/* ------------------------------------------------------------------------ */
+/* Lifetime                                                                  */
+/* ------------------------------------------------------------------------ */
+
+/* Create an empty LSM with batch size b >= 1 (rule 1) on
+ * the current CUDA device. r = 0, all levels empty. *out receives the
+ * handle. Errors: LSM_ERR_INVALID_ARG (b == 0, out NULL), LSM_ERR_NO_DEVICE. */
+lsm_status lsm_create(uint64_t b, lsm_t** out);
+
+/* Free all device memory owned by h (synchronises the device first). */
+lsm_status lsm_destroy(lsm_t* h);
+
+/* Pre-allocate level storage and scratch for up to max_batches resident
+ * batches so that no allocation happens inside later calls. Optional. */
+lsm_status lsm_reserve(lsm_t* h, uint64_t max_batches, void* stream);
+
+/* Drop every element (r = 0) without freeing memory. Stream-ordered. */
+lsm_status lsm_clear(lsm_t* h, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Updates: batch insertion with status-bit encoding, stable radix sort and   */
+/* the binary-counter merge cascade (§3.2-3.3, §4.1, Fig. 2a, Fig. 4)*/
+/* ------------------------------------------------------------------------ */
+
+/* Mixed batch of n updates, 1 <= n <= b (rule 2).
+ * d_keys[n]      original keys (u32, any alignment)
+ * d_vals[n]      values (u32); ignored for deletes; may be NULL (= all 0)
+ * d_is_delete[n] u8, nonzero = delete(k) (a tombstone),
+ *                zero = insert(k, v); NULL = all inserts.
+ * Semantics (rules 3-6, readings R4, R6, R7): the batch
+ * is newer than every resident batch; within the batch a delete of k wins
+ * over inserts of k, and among inserts of k the first one (lowest index)
+ * wins. n < b is padded with invisible placebos (R7). Increments r.
+ * Device work: encode + 4-pass onesweep LSD radix sort on the 32-bit key
+ * variable (status bit included), then for i = 0..ffz(r)-1 a
+ * merge-path merge on key>>1, batch first on ties (R1),
+ * the last merge writing straight into level ffz(r).
+ * Errors: LSM_ERR_BATCH_SIZE, LSM_ERR_INVALID_ARG, LSM_ERR_OOM,
+ * LSM_ERR_CUDA; out-of-domain keys set the sticky LSM_ERR_KEY_DOMAIN.      */
+lsm_status lsm_update(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals,
+                      const uint8_t* d_is_delete, uint64_t n, void* stream);
+
+/* All-insert batch (lsm_update with d_is_delete = NULL). */
+lsm_status lsm_insert(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals,
+                      uint64_t n, void* stream);
+
+/* All-delete batch: Delete(batch) = Insert(tombed(batch)). */
+lsm_status lsm_delete(lsm_t* h, const uint32_t* d_keys, uint64_t n, void* stream);
+
+/* lsm_update from HOST buffers: copies the batch (9 B/update) into internal
+ * device staging on `stream`, then runs lsm_update. h_* must stay valid until
+ * the stream reaches the copy (use pinned memory for async overlap).       */
+lsm_status lsm_update_host(lsm_t* h, const uint32_t* h_keys, const uint32_t* h_vals,
+                           const uint8_t* h_is_delete, uint64_t n, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Retrieval (§3.4-3.5, §4.2-4.4, Fig. 2b-d)                        */
+/* ------------------------------------------------------------------------ */
+
+/* lookup(k) for nq query keys: search the
+ * full levels from the smallest; at each, lower_bound on the original key;
+ * a matching regular element returns its value, a matching tombstone
+ * returns ⊥, else continue.
+ * d_q[nq] u32 query keys; d_vals_out[nq] u32 (LSM_NOT_FOUND on ⊥);
+ * d_found_out[nq] u8 (1 found / 0 ⊥), may be NULL. nq == 0 is a no-op.    */
+lsm_status lsm_lookup(lsm_t* h, const uint32_t* d_q, uint64_t nq,
+                      uint32_t* d_vals_out, uint8_t* d_found_out, void* stream);
+
+/* Host-buffer variant of lsm_lookup (copies in, runs, copies out; h_found_out
+ * may be NULL). Synchronises `stream` before returning.                    */
+lsm_status lsm_lookup_host(lsm_t* h, const uint32_t* h_q, uint64_t nq,
+                           uint32_t* h_vals_out, uint8_t* h_found_out, void* stream);
+
+/* count(k1,k2): number of live pairs with k1 <= k <= k2 (PAPER.md:105-106,
+ * §4.3); 0 when k1 > k2 (R9). Per query, per full level:
+ * lower/upper bounds, then a validation that keeps a candidate iff it is
+ * regular, first of its key run in its level, and its key is absent from
+ * every newer level (equivalent to stages 3-5 of §4.3).
+ * d_k1[nq], d_k2[nq] u32; d_counts_out[nq] u32.                            */
+lsm_status lsm_count(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2, uint64_t nq,
+                     uint32_t* d_counts_out, void* stream);
+
+/* range(k1,k2): all live pairs with k1 <= k <= k2 (§4.4
+ * PAPER.md:728-736). Output: d_offsets_out[nq+1] (u64, exclusive scan of the
+ * per-query counts), then the pairs of query q at [offsets[q], offsets[q+1])
+ * in d_keys_out (original keys) / d_vals_out, ascending by key.
+ * *total_out (HOST) receives the total number of pairs. If total > capacity
+ * the offsets are written, no pairs are, and LSM_ERR_CAPACITY is returned
+ * (retry with a larger buffer). Synchronises `stream`.                      */
+lsm_status lsm_range(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2, uint64_t nq,
+                     uint64_t* d_offsets_out, uint32_t* d_keys_out, uint32_t* d_vals_out,
+                     uint64_t capacity, uint64_t* total_out, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Cleanup (§3.6, §4.5)                            */
+/* ------------------------------------------------------------------------ */
+
+/* Merge all full levels (newer wins ties), drop tombstones and stale
+ * elements, pad with r'b - V < b placebos, and re-slice ascending keys into
+ * the set bits of r' = ceil(V/b) ascending (R10-R13). Query results are
+ * unchanged. Synchronises `stream` (the host needs V to set r').           */
+lsm_status lsm_cleanup(lsm_t* h, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Introspection                                                             */
+/* ------------------------------------------------------------------------ */
+
+lsm_status lsm_batch_size(const lsm_t* h, uint64_t* b_out);
+/* r: the number of resident batches; level i is full iff bit i of r is set. */
+lsm_status lsm_num_batches(const lsm_t* h, uint64_t* r_out);
+/* Device view of level i: key variables ((k<<1)|status) and values, n =
+ * b*2^i if full else 0 (pointers NULL). Valid until the next mutation.     */
+lsm_status lsm_level_view(const lsm_t* h, uint32_t i, const uint32_t** d_keys,
+                          const uint32_t** d_vals, uint64_t* n);
+/* Synchronise `stream` and return (then clear) any sticky device error.    */
+lsm_status lsm_sync(lsm_t* h, void* stream);
+/* Number of kernels this handle has launched so far (monotone).            */
+uint64_t lsm_launch_count(const lsm_t* h);
+const char* lsm_status_string(lsm_status s);
+
+/* ------------------------------------------------------------------------ */
+/* Per-kernel profiling with CUDA events on the launching stream             */
+/* ------------------------------------------------------------------------ */
+typedef enum {
+  LSM_K_SORT_HIST = 0, /* encode + all-digit histograms                     */
+  LSM_K_SORT_PASS = 1, /* onesweep scatter passes                           */
+  LSM_K_MERGE = 2,     /* merge-path merges (cascade and cleanup)           */
+  LSM_K_LOOKUP = 3,
+  LSM_K_COUNT = 4,     /* count kernel and range's counting pass            */
+  LSM_K_RANGE = 5,     /* range write pass                                  */
+  LSM_K_SCAN = 6,      /* offset scans                                      */
+  LSM_K_CLEANUP = 7,   /* cleanup mark+compact and placebo fill             */
+  LSM_K_OTHER = 8,
+  LSM_K_NUM = 9
+} lsm_kernel_class;
+
+typedef struct {
+  uint64_t launches[LSM_K_NUM];
+  double ms[LSM_K_NUM];           /* summed CUDA-event durations            */
+  double alg_bytes[LSM_K_NUM];    /* algorithmic bytes        */
+} lsm_profile;
+
+/* Enable/disable event bracketing of every launch (enable resets totals).  */
+lsm_status lsm_profile_enable(lsm_t* h, int on);
+/* Synchronise the recorded events and return the per-class totals.        */
+lsm_status lsm_profile_read(lsm_t* h, lsm_profile* out);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GPULSM_H */

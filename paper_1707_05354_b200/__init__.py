@@ -1,0 +1,310 @@
+"""paper_1707_05354_b200 -- B200-native GPU LSM batched-update hot path.
+
+Thin ctypes binding over the C ABI in include/gpulsm.h (libgpulsm.so, built
+in-tree for sm_100a by paper_1707_05354_b200.build). Every step of the path
+runs in the library's CUDA kernels; this module only marshals pointers,
+sizes and the current torch CUDA stream. PyTorch provides device memory,
+streams and process groups. There is no CPU fallback: if the library is
+missing or no CUDA device is present, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgpulsm.so")
+
+LSM_OK = 0
+LSM_ERR_CAPACITY = 4
+LSM_ERR_KEY_DOMAIN = 3
+LSM_NOT_FOUND = 0xFFFFFFFF
+LSM_PLACEBO = 0xFFFFFFFE
+MAX_KEY = 0x7FFFFFFE
+LSM_MAX_LEVELS = 40
+KERNEL_CLASSES = ["sort_hist", "sort_pass", "merge", "lookup", "count", "range",
+                  "scan", "cleanup", "other"]
+
+_vp = ctypes.c_void_p
+_u64 = ctypes.c_uint64
+_st = ctypes.c_int
+
+# name -> (argtypes, restype); the exact entry points of include/gpulsm.h
+SIGNATURES = {
+    "lsm_create": ([_u64, ctypes.POINTER(_vp)], _st),
+    "lsm_destroy": ([_vp], _st),
+    "lsm_reserve": ([_vp, _u64, _vp], _st),
+    "lsm_clear": ([_vp, _vp], _st),
+    "lsm_update": ([_vp, _vp, _vp, _vp, _u64, _vp], _st),
+    "lsm_insert": ([_vp, _vp, _vp, _u64, _vp], _st),
+    "lsm_delete": ([_vp, _vp, _u64, _vp], _st),
+    "lsm_update_host": ([_vp, _vp, _vp, _vp, _u64, _vp], _st),
+    "lsm_lookup": ([_vp, _vp, _u64, _vp, _vp, _vp], _st),
+    "lsm_lookup_host": ([_vp, _vp, _u64, _vp, _vp, _vp], _st),
+    "lsm_count": ([_vp, _vp, _vp, _u64, _vp, _vp], _st),
+    "lsm_range": ([_vp, _vp, _vp, _u64, _vp, _vp, _vp, _u64, ctypes.POINTER(_u64), _vp], _st),
+    "lsm_cleanup": ([_vp, _vp], _st),
+    "lsm_batch_size": ([_vp, ctypes.POINTER(_u64)], _st),
+    "lsm_num_batches": ([_vp, ctypes.POINTER(_u64)], _st),
+    "lsm_level_view": ([_vp, ctypes.c_uint32, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                        ctypes.POINTER(_u64)], _st),
+    "lsm_sync": ([_vp, _vp], _st),
+    "lsm_launch_count": ([_vp], _u64),
+    "lsm_status_string": ([_st], ctypes.c_char_p),
+    "lsm_profile_enable": ([_vp, ctypes.c_int], _st),
+    "lsm_profile_read": ([_vp, _vp], _st),
+}
+
+
+class LsmProfile(ctypes.Structure):
+    _fields_ = [("launches", _u64 * 9), ("ms", ctypes.c_double * 9),
+                ("alg_bytes", ctypes.c_double * 9)]
+
+
+class LsmError(RuntimeError):
+    def __init__(self, code, what):
+        self.code = code
+        super().__init__(f"{what}: {status_string(code)} ({code})")
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libgpulsm.so (raises if absent -- no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise ImportError(f"libgpulsm.so not built at {path}; run "
+                              "`python -m paper_1707_05354_b200.build`")
+        L = ctypes.CDLL(path)
+        for name, (args, res) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def status_string(code: int) -> str:
+    return load_library().lsm_status_string(code).decode()
+
+
+def _check(code, what):
+    if code != LSM_OK:
+        raise LsmError(code, what)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream_ptr(stream=None):
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _dev(t, nbytes_per=4, name="tensor"):
+    """Device pointer of a contiguous CUDA tensor with 4-byte (or 1-byte) items."""
+    torch = _torch()
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if t.element_size() != nbytes_per:
+        raise TypeError(f"{name} must have {nbytes_per}-byte elements, got {t.dtype}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class _CudaView:
+    def __init__(self, ptr, n, typestr):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3}
+
+
+def to_device(a, device="cuda"):
+    """numpy u32/u8 array -> CUDA tensor of the same bytes (int32 / uint8)."""
+    torch = _torch()
+    a = np.ascontiguousarray(a)
+    if a.dtype == np.uint32:
+        a = a.view(np.int32)
+    return torch.from_numpy(a).to(device)
+
+
+def to_numpy_u32(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+class GpuLSM:
+    """A GPU LSM dictionary with batch size b on the current CUDA device."""
+
+    def __init__(self, b: int, reserve_batches: int = 0):
+        self._lib = load_library()
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise RuntimeError("GpuLSM needs a CUDA device (no CPU fallback)")
+        h = ctypes.c_void_p()
+        _check(self._lib.lsm_create(int(b), ctypes.byref(h)), "lsm_create")
+        self.h = h
+        self.b = int(b)
+        if reserve_batches:
+            _check(self._lib.lsm_reserve(self.h, int(reserve_batches), _stream_ptr()),
+                   "lsm_reserve")
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._lib.lsm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- updates ----
+    def update(self, keys, vals=None, is_delete=None, stream=None):
+        n = keys.numel()
+        _check(self._lib.lsm_update(self.h, _dev(keys, 4, "keys"), _dev(vals, 4, "vals"),
+                                    _dev(is_delete, 1, "is_delete"), n, _stream_ptr(stream)),
+               "lsm_update")
+
+    def insert(self, keys, vals, stream=None):
+        _check(self._lib.lsm_insert(self.h, _dev(keys, 4, "keys"), _dev(vals, 4, "vals"),
+                                    keys.numel(), _stream_ptr(stream)), "lsm_insert")
+
+    def delete(self, keys, stream=None):
+        _check(self._lib.lsm_delete(self.h, _dev(keys, 4, "keys"), keys.numel(),
+                                    _stream_ptr(stream)), "lsm_delete")
+
+    def update_host(self, keys: np.ndarray, vals=None, is_delete=None, stream=None):
+        """lsm_update_host from (ideally pinned) host numpy/tensor buffers."""
+        def hp(a):
+            if a is None:
+                return None
+            if isinstance(a, np.ndarray):
+                return ctypes.c_void_p(a.ctypes.data)
+            return ctypes.c_void_p(a.data_ptr())
+        n = len(keys)
+        _check(self._lib.lsm_update_host(self.h, hp(keys), hp(vals), hp(is_delete), n,
+                                         _stream_ptr(stream)), "lsm_update_host")
+
+    # ---- queries ----
+    def lookup(self, q, stream=None):
+        torch = _torch()
+        nq = q.numel()
+        vals = torch.empty(nq, dtype=torch.int32, device=q.device)
+        found = torch.empty(nq, dtype=torch.uint8, device=q.device)
+        self.lookup_into(q, vals, found, stream)
+        return vals, found
+
+    def lookup_into(self, q, vals, found=None, stream=None):
+        _check(self._lib.lsm_lookup(self.h, _dev(q, 4, "q"), q.numel(), _dev(vals, 4, "vals"),
+                                    _dev(found, 1, "found"), _stream_ptr(stream)), "lsm_lookup")
+
+    def lookup_host(self, q: np.ndarray, stream=None):
+        q = np.ascontiguousarray(q, dtype=np.uint32)
+        v = np.empty(len(q), np.uint32)
+        f = np.empty(len(q), np.uint8)
+        _check(self._lib.lsm_lookup_host(self.h, ctypes.c_void_p(q.ctypes.data), len(q),
+                                         ctypes.c_void_p(v.ctypes.data),
+                                         ctypes.c_void_p(f.ctypes.data), _stream_ptr(stream)),
+               "lsm_lookup_host")
+        return v, f
+
+    def count(self, k1, k2, stream=None):
+        torch = _torch()
+        out = torch.empty(k1.numel(), dtype=torch.int32, device=k1.device)
+        self.count_into(k1, k2, out, stream)
+        return out
+
+    def count_into(self, k1, k2, out, stream=None):
+        if k1.numel() != k2.numel():
+            raise ValueError("k1 and k2 differ in length")
+        _check(self._lib.lsm_count(self.h, _dev(k1, 4, "k1"), _dev(k2, 4, "k2"), k1.numel(),
+                                   _dev(out, 4, "out"), _stream_ptr(stream)), "lsm_count")
+
+    def range(self, k1, k2, capacity: int | None = None, stream=None):
+        """Returns (offsets[nq+1] int64, keys int32-bits, vals int32-bits)."""
+        torch = _torch()
+        nq = k1.numel()
+        if k2.numel() != nq:
+            raise ValueError("k1 and k2 differ in length")
+        offsets = torch.empty(nq + 1, dtype=torch.int64, device=k1.device)
+        cap = int(capacity) if capacity is not None else max(16, 16 * nq)
+        while True:
+            keys = torch.empty(max(cap, 1), dtype=torch.int32, device=k1.device)
+            vals = torch.empty(max(cap, 1), dtype=torch.int32, device=k1.device)
+            total = _u64(0)
+            code = self._lib.lsm_range(self.h, _dev(k1, 4, "k1"), _dev(k2, 4, "k2"), nq,
+                                       _dev(offsets, 8, "offsets"), _dev(keys, 4, "keys"),
+                                       _dev(vals, 4, "vals"), cap, ctypes.byref(total),
+                                       _stream_ptr(stream))
+            if code == LSM_ERR_CAPACITY:
+                cap = int(total.value)
+                continue
+            _check(code, "lsm_range")
+            t = int(total.value)
+            return offsets, keys[:t], vals[:t]
+
+    def range_into(self, k1, k2, offsets, keys, vals, stream=None) -> int:
+        total = _u64(0)
+        _check(self._lib.lsm_range(self.h, _dev(k1, 4, "k1"), _dev(k2, 4, "k2"), k1.numel(),
+                                   _dev(offsets, 8, "offsets"), _dev(keys, 4, "keys"),
+                                   _dev(vals, 4, "vals"), keys.numel(), ctypes.byref(total),
+                                   _stream_ptr(stream)), "lsm_range")
+        return int(total.value)
+
+    def cleanup(self, stream=None):
+        _check(self._lib.lsm_cleanup(self.h, _stream_ptr(stream)), "lsm_cleanup")
+
+    # ---- introspection ----
+    @property
+    def r(self) -> int:
+        v = _u64(0)
+        _check(self._lib.lsm_num_batches(self.h, ctypes.byref(v)), "lsm_num_batches")
+        return int(v.value)
+
+    def level(self, i: int):
+        """(keys, vals) of level i as int32 CUDA tensors (copies; empty if level empty)."""
+        torch = _torch()
+        kp, vp, n = ctypes.c_void_p(), ctypes.c_void_p(), _u64(0)
+        _check(self._lib.lsm_level_view(self.h, i, ctypes.byref(kp), ctypes.byref(vp),
+                                        ctypes.byref(n)), "lsm_level_view")
+        n = int(n.value)
+        if n == 0:
+            e = torch.empty(0, dtype=torch.int32, device="cuda")
+            return e, e.clone()
+        k = torch.as_tensor(_CudaView(kp.value, n, "<i4"), device="cuda").clone()
+        v = torch.as_tensor(_CudaView(vp.value, n, "<i4"), device="cuda").clone()
+        return k, v
+
+    def sync(self, stream=None):
+        _check(self._lib.lsm_sync(self.h, _stream_ptr(stream)), "lsm_sync")
+
+    def clear(self, stream=None):
+        _check(self._lib.lsm_clear(self.h, _stream_ptr(stream)), "lsm_clear")
+
+    def reserve(self, max_batches: int, stream=None):
+        _check(self._lib.lsm_reserve(self.h, int(max_batches), _stream_ptr(stream)),
+               "lsm_reserve")
+
+    @property
+    def launch_count(self) -> int:
+        return int(self._lib.lsm_launch_count(self.h))
+
+    def profile_enable(self, on: bool = True):
+        _check(self._lib.lsm_profile_enable(self.h, 1 if on else 0), "lsm_profile_enable")
+
+    def profile_read(self) -> dict:
+        p = LsmProfile()
+        _check(self._lib.lsm_profile_read(self.h, ctypes.byref(p)), "lsm_profile_read")
+        return {name: {"launches": int(p.launches[i]), "ms": float(p.ms[i]),
+                       "alg_bytes": float(p.alg_bytes[i])}
+                for i, name in enumerate(KERNEL_CLASSES)}

@@ -1,0 +1,198 @@
+// common.cuh -- device helpers and internal launcher declarations for the
+// B200 GPU LSM (sm_100a). Internal to the library; the public boundary is
+// include/gpulsm.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gpulsm.h"
+
+namespace gpulsm {
+
+constexpr uint32_t kMaxKey = LSM_MAX_KEY;
+constexpr uint32_t kPlacebo = LSM_PLACEBO;
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+
+// Level table passed by value in kernel parameters (occupied levels only,
+// ascending index = newest first).
+struct LevelTable {
+  const uint32_t* keys[LSM_MAX_LEVELS];
+  const uint32_t* vals[LSM_MAX_LEVELS];
+  uint64_t n[LSM_MAX_LEVELS];
+  int count;
+};
+
+__device__ __forceinline__ uint32_t lane_id() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%laneid;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void stg_v4(void* p, uint4 v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+// lower_bound over the original key (key variable >> 1) of a sorted level:
+// first index p with (K[p] >> 1) >= q; the query word is compared unshifted
+// (reading R8), so q >= 2^31 is past every stored key.
+__device__ __forceinline__ uint64_t lower_bound_orig(const uint32_t* __restrict__ K, uint64_t n,
+                                                     uint32_t q) {
+  uint64_t lo = 0;
+  while (n > 0) {
+    uint64_t half = n >> 1;
+    uint32_t k = __ldg(K + lo + half) >> 1;
+    if (k < q) {
+      lo += half + 1;
+      n -= half + 1;
+    } else {
+      n = half;
+    }
+  }
+  return lo;
+}
+// upper_bound: first index p with (K[p] >> 1) > q.
+__device__ __forceinline__ uint64_t upper_bound_orig(const uint32_t* __restrict__ K, uint64_t n,
+                                                     uint32_t q) {
+  uint64_t lo = 0;
+  while (n > 0) {
+    uint64_t half = n >> 1;
+    uint32_t k = __ldg(K + lo + half) >> 1;
+    if (k <= q) {
+      lo += half + 1;
+      n -= half + 1;
+    } else {
+      n = half;
+    }
+  }
+  return lo;
+}
+
+// Exclusive scan of one value per thread across a block of NT threads
+// (NT multiple of 32, <= 1024). `tmp` needs NT/32 + 1 words. Returns the
+// exclusive prefix; *total receives the block sum. Contains __syncthreads.
+template <int NT, typename T>
+__device__ __forceinline__ T block_exclusive_scan(T v, T* tmp, T* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) tmp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    constexpr int NW = NT / 32;
+    T w = lane < NW ? tmp[lane] : T(0);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      T y = __shfl_up_sync(kFull, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < NW) tmp[lane] = w;  // inclusive warp totals
+    if (lane == NW - 1) tmp[NW] = w;
+  }
+  __syncthreads();
+  T excl = x - v + (warp > 0 ? tmp[warp - 1] : T(0));
+  *total = tmp[NT / 32];
+  __syncthreads();  // tmp may be reused right away
+  return excl;
+}
+
+// ---------------------------------------------------------------------------
+// Launchers (host side). Each returns cudaGetLastError() after the launch.
+// ---------------------------------------------------------------------------
+
+enum UpdateMode { kModeInsert = 0, kModeDelete = 1, kModeMixed = 2 };
+
+struct SortScratch {
+  uint32_t* hist;         // [2][4][256] double-buffered digit histograms
+  uint32_t* status;       // [4][tiles][256] decoupled look-back words
+  uint32_t* tile_ctr;     // [4] dynamic tile counters
+  uint32_t* err;          // sticky domain-error flag
+  uint32_t* tmp_keys[2];  // b-sized ping-pong for the passes
+  uint32_t* tmp_vals[2];
+  uint64_t tiles_cap;     // status capacity in tiles
+  int parity;             // which hist half this sort uses
+};
+
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;
+constexpr int kSortTile = kSortThreads * kSortItems;
+constexpr int kRadixBits = 8;
+constexpr int kRadix = 1 << kRadixBits;
+constexpr int kPasses = 4;
+
+inline uint64_t sort_tiles(uint64_t b) { return (b + kSortTile - 1) / kSortTile; }
+
+// Encode + stable LSD radix sort of one batch (status bit included) into
+// (out_keys, out_vals). Launches 1 histogram kernel + 4 onesweep passes.
+// `launch_cb(cls, bytes)` brackets each launch for profiling/counting.
+struct LaunchHooks {
+  void (*begin)(void* ctx, int cls, cudaStream_t s);
+  void (*end)(void* ctx, int cls, double bytes, cudaStream_t s, int nkernels);
+  void* ctx;
+};
+
+cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals,
+                              const uint8_t* ops, int mode, uint64_t n, uint64_t b,
+                              SortScratch& S, uint32_t* out_keys, uint32_t* out_vals,
+                              cudaStream_t s, const LaunchHooks& hk);
+
+// Stable merge on key>>1, A (newer) first on ties, into out[na+nb].
+cudaError_t launch_merge(const uint32_t* ak, const uint32_t* av, uint64_t na,
+                         const uint32_t* bk, const uint32_t* bv, uint64_t nb, uint32_t* ok,
+                         uint32_t* ov, cudaStream_t s, const LaunchHooks& hk);
+
+cudaError_t launch_lookup(const LevelTable& T, const uint32_t* q, uint64_t nq,
+                          uint32_t* vals_out, uint8_t* found_out, cudaStream_t s,
+                          const LaunchHooks& hk);
+
+cudaError_t launch_count(const LevelTable& T, const uint32_t* k1, const uint32_t* k2,
+                         uint64_t nq, uint32_t* counts_out, cudaStream_t s,
+                         const LaunchHooks& hk, int cls);
+
+// Exclusive scan of u32 counts into u64 offsets[n+1]; block_sums needs
+// scan_scratch_words(n) u64 words.
+uint64_t scan_scratch_words(uint64_t n);
+cudaError_t launch_scan(const uint32_t* counts, uint64_t n, uint64_t* offsets,
+                        uint64_t* block_sums, cudaStream_t s, const LaunchHooks& hk);
+
+cudaError_t launch_range_write(const LevelTable& T, const uint32_t* k1, const uint32_t* k2,
+                               uint64_t nq, const uint64_t* offsets, uint32_t* keys_out,
+                               uint32_t* vals_out, cudaStream_t s, const LaunchHooks& hk);
+
+// Cleanup: valid = regular && first of its key run in M; compact into C.
+// tile_counts: cleanup_tiles(n) u32; offsets: cleanup_tiles(n)+1 u64.
+uint64_t cleanup_tiles(uint64_t n);
+cudaError_t launch_cleanup_count(const uint32_t* mk, uint64_t n, uint32_t* tile_counts,
+                                 cudaStream_t s, const LaunchHooks& hk);
+cudaError_t launch_cleanup_write(const uint32_t* mk, const uint32_t* mv, uint64_t n,
+                                 const uint64_t* tile_offsets, uint32_t* ck, uint32_t* cv,
+                                 cudaStream_t s, const LaunchHooks& hk);
+cudaError_t launch_fill_placebo(uint32_t* ck, uint32_t* cv, uint64_t from, uint64_t to,
+                                cudaStream_t s, const LaunchHooks& hk);
+
+}  // namespace gpulsm

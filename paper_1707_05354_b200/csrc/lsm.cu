@@ -1,0 +1,638 @@
+// lsm.cu -- the GPU LSM engine behind include/gpulsm.h.
+//
+// Host-side state: b, r (the binary counter of
+// PAPER.md:377-382, kept on the host so that t = ffz(r), is
+// known without a device sync), a level table of (keys, vals, owner) views,
+// one "home" buffer per level, ping-pong merge scratch, sort
+// scratch, query scratch, and a stream-ordered memory pool. Nothing on the
+// update path synchronises the device.
+//
+// Storage differs from Fig. 4, which keeps all levels in
+// one array and memsets/copies levels: here level i lives in its own buffer,
+// the last merge of a cascade writes straight into level t (no
+// gpu_memory_copy), emptied levels are not zeroed (emptiness is a bit of r,
+// no gpu_memory_set), and after a cleanup the new levels are views into the
+// compacted buffer (no redistribution copy).
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "common.cuh"
+
+using namespace gpulsm;
+
+namespace {
+
+struct Buffer {
+  uint32_t* keys = nullptr;
+  uint32_t* vals = nullptr;
+  uint64_t cap = 0;
+  int refs = 0;  // number of levels viewing it (cleanup buffers only)
+};
+
+struct Level {
+  const uint32_t* keys = nullptr;
+  const uint32_t* vals = nullptr;
+  Buffer* owner = nullptr;  // non-null: view into a shared cleanup buffer
+};
+
+struct ProfRec {
+  int cls;
+  cudaEvent_t e0, e1;
+  double bytes;
+};
+
+}  // namespace
+
+struct lsm {
+  int device = 0;
+  uint64_t b = 0;
+  uint64_t r = 0;
+  Level level[LSM_MAX_LEVELS];
+  Buffer home[LSM_MAX_LEVELS];
+  Buffer ping[2];         // merge ping-pong scratch
+  Buffer sortout;         // sorted batch when t >= 1
+  SortScratch sort{};
+  uint32_t* sort_meta = nullptr;
+  uint64_t sort_meta_words = 0;
+  // host-update staging
+  uint32_t* st_keys = nullptr;
+  uint32_t* st_vals = nullptr;
+  uint8_t* st_ops = nullptr;
+  // query scratch
+  void* qbuf = nullptr;
+  uint64_t qbuf_bytes = 0;
+  uint64_t* h_pinned = nullptr;  // host readback words
+  cudaMemPool_t pool = nullptr;
+  uint64_t launches = 0;
+  lsm_status sticky = LSM_OK;
+  // profiling
+  bool prof_on = false;
+  std::vector<ProfRec> prof;
+  std::vector<cudaEvent_t> ev_free;
+  cudaEvent_t pending = nullptr;
+  lsm_profile totals{};
+};
+
+namespace {
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+cudaEvent_t ev_get(lsm* h) {
+  if (!h->ev_free.empty()) {
+    cudaEvent_t e = h->ev_free.back();
+    h->ev_free.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void hook_begin(void* ctx, int cls, cudaStream_t s) {
+  lsm* h = static_cast<lsm*>(ctx);
+  if (!h->prof_on) return;
+  h->pending = ev_get(h);
+  cudaEventRecord(h->pending, s);
+  (void)cls;
+}
+
+void hook_end(void* ctx, int cls, double bytes, cudaStream_t s, int nk) {
+  lsm* h = static_cast<lsm*>(ctx);
+  h->launches += (uint64_t)nk;
+  if (!h->prof_on) return;
+  cudaEvent_t e1 = ev_get(h);
+  cudaEventRecord(e1, s);
+  h->prof.push_back(ProfRec{cls, h->pending, e1, bytes});
+  h->totals.launches[cls] += (uint64_t)nk;
+}
+
+LaunchHooks hooks(lsm* h) { return LaunchHooks{hook_begin, hook_end, h}; }
+
+lsm_status cuda_err(cudaError_t e) {
+  if (e == cudaSuccess) return LSM_OK;
+  if (e == cudaErrorMemoryAllocation) return LSM_ERR_OOM;
+  std::fprintf(stderr, "gpulsm: CUDA error %s\n", cudaGetErrorString(e));
+  return LSM_ERR_CUDA;
+}
+
+#define CK(expr)                                  \
+  do {                                            \
+    cudaError_t _e = (expr);                      \
+    if (_e != cudaSuccess) return cuda_err(_e);   \
+  } while (0)
+
+cudaError_t pool_alloc(lsm* h, void** p, uint64_t bytes, cudaStream_t s) {
+  if (bytes == 0) bytes = 16;
+  return cudaMallocFromPoolAsync(p, bytes, h->pool, s);
+}
+
+cudaError_t buf_ensure(lsm* h, Buffer& B, uint64_t n, cudaStream_t s) {
+  if (B.cap >= n) return cudaSuccess;
+  if (B.keys) cudaFreeAsync(B.keys, s);
+  if (B.vals) cudaFreeAsync(B.vals, s);
+  B.keys = B.vals = nullptr;
+  B.cap = 0;
+  cudaError_t e = pool_alloc(h, (void**)&B.keys, n * 4, s);
+  if (e != cudaSuccess) return e;
+  e = pool_alloc(h, (void**)&B.vals, n * 4, s);
+  if (e != cudaSuccess) return e;
+  B.cap = n;
+  return cudaSuccess;
+}
+
+void buf_free(Buffer& B, cudaStream_t s) {
+  if (B.keys) cudaFreeAsync(B.keys, s);
+  if (B.vals) cudaFreeAsync(B.vals, s);
+  B.keys = B.vals = nullptr;
+  B.cap = 0;
+}
+
+// release level i's storage (it becomes empty); frees a cleanup buffer when
+// its last view goes
+void level_release(lsm* h, int i, cudaStream_t s) {
+  Level& L = h->level[i];
+  if (L.owner) {
+    if (--L.owner->refs == 0) {
+      buf_free(*L.owner, s);
+      delete L.owner;
+    }
+  }
+  L = Level{};
+}
+
+cudaError_t ensure_sort_scratch(lsm* h, cudaStream_t s) {
+  const uint64_t tiles = sort_tiles(h->b);
+  if (h->sort_meta == nullptr) {
+    // hist[2][4][256] | tile_ctr[4] | err[1] | pad | status[4][tiles][256]
+    const uint64_t head = 2 * kPasses * kRadix + 8;
+    h->sort_meta_words = head + (uint64_t)kPasses * tiles * kRadix;
+    cudaError_t e = pool_alloc(h, (void**)&h->sort_meta, h->sort_meta_words * 4, s);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(h->sort_meta, 0, h->sort_meta_words * 4, s);
+    if (e != cudaSuccess) return e;
+    h->sort.hist = h->sort_meta;
+    h->sort.tile_ctr = h->sort_meta + 2 * kPasses * kRadix;
+    h->sort.err = h->sort.tile_ctr + 4;
+    h->sort.status = h->sort_meta + head;
+    h->sort.tiles_cap = tiles;
+    for (int k = 0; k < 2; ++k) {
+      e = pool_alloc(h, (void**)&h->sort.tmp_keys[k], h->b * 4, s);
+      if (e != cudaSuccess) return e;
+      e = pool_alloc(h, (void**)&h->sort.tmp_vals[k], h->b * 4, s);
+      if (e != cudaSuccess) return e;
+    }
+  }
+  return cudaSuccess;
+}
+
+cudaError_t ensure_qbuf(lsm* h, uint64_t bytes, cudaStream_t s) {
+  if (h->qbuf_bytes >= bytes) return cudaSuccess;
+  if (h->qbuf) cudaFreeAsync(h->qbuf, s);
+  h->qbuf = nullptr;
+  h->qbuf_bytes = 0;
+  uint64_t nb = std::max<uint64_t>(bytes, 1 << 20);
+  cudaError_t e = pool_alloc(h, &h->qbuf, nb, s);
+  if (e != cudaSuccess) return e;
+  h->qbuf_bytes = nb;
+  return cudaSuccess;
+}
+
+LevelTable level_table(const lsm* h) {
+  LevelTable T;
+  std::memset(&T, 0, sizeof(T));
+  int c = 0;
+  for (int i = 0; i < LSM_MAX_LEVELS; ++i) {
+    if ((h->r >> i) & 1ull) {
+      T.keys[c] = h->level[i].keys;
+      T.vals[c] = h->level[i].vals;
+      T.n[c] = h->b << i;
+      ++c;
+    }
+  }
+  T.count = c;
+  return T;
+}
+
+int ffz(uint64_t r) {
+  int t = 0;
+  while ((r >> t) & 1ull) ++t;
+  return t;
+}
+
+uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+extern "C" {
+
+const char* lsm_status_string(lsm_status s) {
+  switch (s) {
+    case LSM_OK: return "ok";
+    case LSM_ERR_INVALID_ARG: return "invalid argument";
+    case LSM_ERR_BATCH_SIZE: return "batch size must satisfy 1 <= n <= b";
+    case LSM_ERR_KEY_DOMAIN: return "update key outside [0, 2^31-2] (stored as placebo)";
+    case LSM_ERR_CAPACITY: return "range output larger than capacity";
+    case LSM_ERR_OOM: return "device out of memory";
+    case LSM_ERR_CUDA: return "CUDA error";
+    case LSM_ERR_NO_DEVICE: return "no CUDA device";
+  }
+  return "unknown";
+}
+
+lsm_status lsm_create(uint64_t b, lsm_t** out) {
+  if (!out || b == 0 || b > (1ull << 30)) return LSM_ERR_INVALID_ARG;
+  *out = nullptr;
+  int dev = 0, ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return LSM_ERR_NO_DEVICE;
+  }
+  CK(cudaGetDevice(&dev));
+  lsm* h = new (std::nothrow) lsm;
+  if (!h) return LSM_ERR_OOM;
+  h->device = dev;
+  h->b = b;
+  cudaMemPoolProps props{};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  cudaError_t e = cudaMemPoolCreate(&h->pool, &props);
+  if (e != cudaSuccess) {
+    delete h;
+    return cuda_err(e);
+  }
+  uint64_t thr = ~0ull;
+  cudaMemPoolSetAttribute(h->pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  e = cudaMallocHost((void**)&h->h_pinned, 64);
+  if (e != cudaSuccess) {
+    cudaMemPoolDestroy(h->pool);
+    delete h;
+    return cuda_err(e);
+  }
+  *out = h;
+  return LSM_OK;
+}
+
+lsm_status lsm_destroy(lsm_t* h) {
+  if (!h) return LSM_ERR_INVALID_ARG;
+  cudaSetDevice(h->device);
+  cudaDeviceSynchronize();
+  for (int i = 0; i < LSM_MAX_LEVELS; ++i) {
+    level_release(h, i, nullptr);
+    buf_free(h->home[i], nullptr);
+  }
+  buf_free(h->ping[0], nullptr);
+  buf_free(h->ping[1], nullptr);
+  buf_free(h->sortout, nullptr);
+  if (h->sort_meta) cudaFreeAsync(h->sort_meta, nullptr);
+  for (int k = 0; k < 2; ++k) {
+    if (h->sort.tmp_keys[k]) cudaFreeAsync(h->sort.tmp_keys[k], nullptr);
+    if (h->sort.tmp_vals[k]) cudaFreeAsync(h->sort.tmp_vals[k], nullptr);
+  }
+  if (h->st_keys) cudaFreeAsync(h->st_keys, nullptr);
+  if (h->st_vals) cudaFreeAsync(h->st_vals, nullptr);
+  if (h->st_ops) cudaFreeAsync(h->st_ops, nullptr);
+  if (h->qbuf) cudaFreeAsync(h->qbuf, nullptr);
+  cudaDeviceSynchronize();
+  for (auto& p : h->prof) {
+    cudaEventDestroy(p.e0);
+    cudaEventDestroy(p.e1);
+  }
+  for (auto e : h->ev_free) cudaEventDestroy(e);
+  if (h->h_pinned) cudaFreeHost(h->h_pinned);
+  cudaMemPoolDestroy(h->pool);
+  delete h;
+  return LSM_OK;
+}
+
+lsm_status lsm_reserve(lsm_t* h, uint64_t max_batches, void* stream) {
+  if (!h) return LSM_ERR_INVALID_ARG;
+  cudaStream_t s = S(stream);
+  CK(ensure_sort_scratch(h, s));
+  int top = 0;
+  while (top + 1 < LSM_MAX_LEVELS && (1ull << (top + 1)) <= max_batches) ++top;
+  for (int i = 0; i <= top; ++i) CK(buf_ensure(h, h->home[i], h->b << i, s));
+  CK(buf_ensure(h, h->sortout, h->b, s));
+  if (top >= 1) {
+    CK(buf_ensure(h, h->ping[0], h->b << (top - 1), s));
+    CK(buf_ensure(h, h->ping[1], h->b << (top - 1), s));
+  }
+  return LSM_OK;
+}
+
+lsm_status lsm_clear(lsm_t* h, void* stream) {
+  if (!h) return LSM_ERR_INVALID_ARG;
+  for (int i = 0; i < LSM_MAX_LEVELS; ++i)
+    if ((h->r >> i) & 1ull) level_release(h, i, S(stream));
+  h->r = 0;
+  return LSM_OK;
+}
+
+// Insert(batch), PAPER.md:462-473 / Fig. 4 PAPER.md:662-677.
+static lsm_status do_update(lsm_t* h, const uint32_t* keys, const uint32_t* vals,
+                            const uint8_t* ops, int mode, uint64_t n, cudaStream_t s) {
+  if (!h || !keys) return LSM_ERR_INVALID_ARG;
+  if (n == 0 || n > h->b) return LSM_ERR_BATCH_SIZE;
+  if (mode == kModeMixed && ops == nullptr) mode = kModeInsert;
+  const uint64_t b = h->b;
+  const int t = ffz(h->r);  // first empty level
+  if (t >= LSM_MAX_LEVELS) return LSM_ERR_INVALID_ARG;
+  LaunchHooks hk = hooks(h);
+  CK(ensure_sort_scratch(h, s));
+  CK(buf_ensure(h, h->home[t], b << t, s));
+  // sort (A1+A2): straight into level 0 when t == 0
+  uint32_t* sk = (t == 0) ? h->home[0].keys : nullptr;
+  uint32_t* sv = (t == 0) ? h->home[0].vals : nullptr;
+  if (t > 0) {
+    CK(buf_ensure(h, h->sortout, b, s));
+    sk = h->sortout.keys;
+    sv = h->sortout.vals;
+    if (t >= 2) {
+      CK(buf_ensure(h, h->ping[0], b << (t - 1), s));
+      CK(buf_ensure(h, h->ping[1], b << (t - 1), s));
+    }
+  }
+  CK(launch_sort_batch(keys, vals, ops, mode, n, b, h->sort, sk, sv, s, hk));
+  // cascade (A3): while level i is full, buffer <- merge(buffer, level i)
+  const uint32_t* ck = sk;
+  const uint32_t* cv = sv;
+  for (int i = 0; i < t; ++i) {
+    uint32_t* ok = (i == t - 1) ? h->home[t].keys : h->ping[i & 1].keys;
+    uint32_t* ov = (i == t - 1) ? h->home[t].vals : h->ping[i & 1].vals;
+    const uint64_t ni = b << i;
+    CK(launch_merge(ck, cv, ni, h->level[i].keys, h->level[i].vals, ni, ok, ov, s, hk));
+    level_release(h, i, s);  // level i <- empty
+    ck = ok;
+    cv = ov;
+  }
+  h->level[t].keys = h->home[t].keys;  // level t <- buffer
+  h->level[t].vals = h->home[t].vals;
+  h->level[t].owner = nullptr;
+  h->r += 1;  // num_batch++ 
+  return LSM_OK;
+}
+
+lsm_status lsm_update(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals,
+                      const uint8_t* d_is_delete, uint64_t n, void* stream) {
+  return do_update(h, d_keys, d_vals, d_is_delete, kModeMixed, n, S(stream));
+}
+
+lsm_status lsm_insert(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals, uint64_t n,
+                      void* stream) {
+  return do_update(h, d_keys, d_vals, nullptr, kModeInsert, n, S(stream));
+}
+
+lsm_status lsm_delete(lsm_t* h, const uint32_t* d_keys, uint64_t n, void* stream) {
+  return do_update(h, d_keys, nullptr, nullptr, kModeDelete, n, S(stream));
+}
+
+lsm_status lsm_update_host(lsm_t* h, const uint32_t* h_keys, const uint32_t* h_vals,
+                           const uint8_t* h_is_delete, uint64_t n, void* stream) {
+  if (!h || !h_keys) return LSM_ERR_INVALID_ARG;
+  if (n == 0 || n > h->b) return LSM_ERR_BATCH_SIZE;
+  cudaStream_t s = S(stream);
+  if (!h->st_keys) {
+    CK(pool_alloc(h, (void**)&h->st_keys, h->b * 4, s));
+    CK(pool_alloc(h, (void**)&h->st_vals, h->b * 4, s));
+    CK(pool_alloc(h, (void**)&h->st_ops, h->b, s));
+  }
+  CK(cudaMemcpyAsync(h->st_keys, h_keys, n * 4, cudaMemcpyHostToDevice, s));
+  if (h_vals) CK(cudaMemcpyAsync(h->st_vals, h_vals, n * 4, cudaMemcpyHostToDevice, s));
+  if (h_is_delete) CK(cudaMemcpyAsync(h->st_ops, h_is_delete, n, cudaMemcpyHostToDevice, s));
+  return do_update(h, h->st_keys, h_vals ? h->st_vals : nullptr,
+                   h_is_delete ? h->st_ops : nullptr, kModeMixed, n, s);
+}
+
+lsm_status lsm_lookup(lsm_t* h, const uint32_t* d_q, uint64_t nq, uint32_t* d_vals_out,
+                      uint8_t* d_found_out, void* stream) {
+  if (!h) return LSM_ERR_INVALID_ARG;
+  if (nq == 0) return LSM_OK;
+  if (!d_q || !d_vals_out) return LSM_ERR_INVALID_ARG;
+  LevelTable T = level_table(h);
+  CK(launch_lookup(T, d_q, nq, d_vals_out, d_found_out, S(stream), hooks(h)));
+  return LSM_OK;
+}
+
+lsm_status lsm_lookup_host(lsm_t* h, const uint32_t* h_q, uint64_t nq, uint32_t* h_vals_out,
+                           uint8_t* h_found_out, void* stream) {
+  if (!h) return LSM_ERR_INVALID_ARG;
+  if (nq == 0) return LSM_OK;
+  if (!h_q || !h_vals_out) return LSM_ERR_INVALID_ARG;
+  cudaStream_t s = S(stream);
+  const uint64_t need = align_up(nq * 4, 256) * 2 + align_up(nq, 256);
+  CK(ensure_qbuf(h, need, s));
+  uint8_t* base = static_cast<uint8_t*>(h->qbuf);
+  uint32_t* dq = reinterpret_cast<uint32_t*>(base);
+  uint32_t* dv = reinterpret_cast<uint32_t*>(base + align_up(nq * 4, 256));
+  uint8_t* df = base + 2 * align_up(nq * 4, 256);
+  CK(cudaMemcpyAsync(dq, h_q, nq * 4, cudaMemcpyHostToDevice, s));
+  LevelTable T = level_table(h);
+  CK(launch_lookup(T, dq, nq, dv, df, s, hooks(h)));
+  CK(cudaMemcpyAsync(h_vals_out, dv, nq * 4, cudaMemcpyDeviceToHost, s));
+  if (h_found_out) CK(cudaMemcpyAsync(h_found_out, df, nq, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return LSM_OK;
+}
+
+lsm_status lsm_count(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2, uint64_t nq,
+                     uint32_t* d_counts_out, void* stream) {
+  if (!h) return LSM_ERR_INVALID_ARG;
+  if (nq == 0) return LSM_OK;
+  if (!d_k1 || !d_k2 || !d_counts_out) return LSM_ERR_INVALID_ARG;
+  LevelTable T = level_table(h);
+  CK(launch_count(T, d_k1, d_k2, nq, d_counts_out, S(stream), hooks(h), LSM_K_COUNT));
+  return LSM_OK;
+}
+
+lsm_status lsm_range(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2, uint64_t nq,
+                     uint64_t* d_offsets_out, uint32_t* d_keys_out, uint32_t* d_vals_out,
+                     uint64_t capacity, uint64_t* total_out, void* stream) {
+  if (!h || !total_out) return LSM_ERR_INVALID_ARG;
+  cudaStream_t s = S(stream);
+  if (!d_offsets_out) return LSM_ERR_INVALID_ARG;
+  if (nq == 0) {
+    CK(cudaMemsetAsync(d_offsets_out, 0, 8, s));
+    *total_out = 0;
+    return LSM_OK;
+  }
+  if (!d_k1 || !d_k2) return LSM_ERR_INVALID_ARG;
+  LaunchHooks hk = hooks(h);
+  const uint64_t cbytes = align_up(nq * 4, 256);
+  const uint64_t sbytes = scan_scratch_words(nq) * 8;
+  CK(ensure_qbuf(h, cbytes + sbytes, s));
+  uint32_t* counts = static_cast<uint32_t*>(h->qbuf);
+  uint64_t* sums = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(h->qbuf) + cbytes);
+  LevelTable T = level_table(h);
+  CK(launch_count(T, d_k1, d_k2, nq, counts, s, hk, LSM_K_COUNT));
+  CK(launch_scan(counts, nq, d_offsets_out, sums, s, hk));
+  CK(cudaMemcpyAsync(h->h_pinned, d_offsets_out + nq, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const uint64_t total = h->h_pinned[0];
+  *total_out = total;
+  if (total > capacity) return LSM_ERR_CAPACITY;
+  if (total > 0 && (!d_keys_out || !d_vals_out)) return LSM_ERR_INVALID_ARG;
+  if (total > 0)
+    CK(launch_range_write(T, d_k1, d_k2, nq, d_offsets_out, d_keys_out, d_vals_out, s, hk));
+  return LSM_OK;
+}
+
+// Cleanup: 1) merge all occupied levels smallest to largest;
+// 2) mark stale; 3) compact; 4) pad with placebos; 5) redistribute.
+lsm_status lsm_cleanup(lsm_t* h, void* stream) {
+  if (!h) return LSM_ERR_INVALID_ARG;
+  cudaStream_t s = S(stream);
+  LaunchHooks hk = hooks(h);
+  const uint64_t b = h->b;
+  std::vector<int> occ;
+  for (int i = 0; i < LSM_MAX_LEVELS; ++i)
+    if ((h->r >> i) & 1ull) occ.push_back(i);
+  if (occ.empty()) return LSM_OK;
+  const uint64_t n = h->r * b;
+  // 1) iterative merges, newer (lower index) first on ties
+  const uint32_t* mk = h->level[occ[0]].keys;
+  const uint32_t* mv = h->level[occ[0]].vals;
+  uint64_t mn = b << occ[0];
+  int pp = 0;
+  if (occ.size() > 1) {
+    CK(buf_ensure(h, h->ping[0], n, s));
+    CK(buf_ensure(h, h->ping[1], n, s));
+  }
+  for (size_t j = 1; j < occ.size(); ++j) {
+    const int i = occ[j];
+    const uint64_t ni = b << i;
+    CK(launch_merge(mk, mv, mn, h->level[i].keys, h->level[i].vals, ni, h->ping[pp].keys,
+                    h->ping[pp].vals, s, hk));
+    mk = h->ping[pp].keys;
+    mv = h->ping[pp].vals;
+    mn += ni;
+    pp ^= 1;
+  }
+  // 2+3) mark + compact into a fresh buffer C
+  Buffer* C = new Buffer;
+  cudaError_t e = buf_ensure(h, *C, n, s);
+  if (e != cudaSuccess) {
+    delete C;
+    return cuda_err(e);
+  }
+  const uint64_t tiles = cleanup_tiles(n);
+  const uint64_t cbytes = align_up(tiles * 4, 256);
+  const uint64_t obytes = align_up((tiles + 1) * 8, 256);
+  const uint64_t sbytes = scan_scratch_words(tiles) * 8;
+  CK(ensure_qbuf(h, cbytes + obytes + sbytes, s));
+  uint8_t* qb = static_cast<uint8_t*>(h->qbuf);
+  uint32_t* tcounts = reinterpret_cast<uint32_t*>(qb);
+  uint64_t* toffs = reinterpret_cast<uint64_t*>(qb + cbytes);
+  uint64_t* tsums = reinterpret_cast<uint64_t*>(qb + cbytes + obytes);
+  CK(launch_cleanup_count(mk, mn, tcounts, s, hk));
+  CK(launch_scan(tcounts, tiles, toffs, tsums, s, hk));
+  CK(launch_cleanup_write(mk, mv, mn, toffs, C->keys, C->vals, s, hk));
+  CK(cudaMemcpyAsync(h->h_pinned, toffs + tiles, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const uint64_t V = h->h_pinned[0];
+  const uint64_t r2 = (V + b - 1) / b;  // R10
+  // 4) placebos fill [V, r'b) (R11)
+  CK(launch_fill_placebo(C->keys, C->vals, V, r2 * b, s, hk));
+  // 5) new levels are views of C: ascending keys into ascending set bits of
+  //    r' (R12), no copy
+  for (int i : occ) level_release(h, i, s);
+  uint64_t off = 0;
+  int refs = 0;
+  for (int i = 0; i < LSM_MAX_LEVELS; ++i) {
+    if (!((r2 >> i) & 1ull)) continue;
+    h->level[i].keys = C->keys + off;
+    h->level[i].vals = C->vals + off;
+    h->level[i].owner = C;
+    off += b << i;
+    ++refs;
+  }
+  C->refs = refs;
+  if (refs == 0) {
+    buf_free(*C, s);
+    delete C;
+  }
+  h->r = r2;
+  return LSM_OK;
+}
+
+lsm_status lsm_batch_size(const lsm_t* h, uint64_t* b_out) {
+  if (!h || !b_out) return LSM_ERR_INVALID_ARG;
+  *b_out = h->b;
+  return LSM_OK;
+}
+
+lsm_status lsm_num_batches(const lsm_t* h, uint64_t* r_out) {
+  if (!h || !r_out) return LSM_ERR_INVALID_ARG;
+  *r_out = h->r;
+  return LSM_OK;
+}
+
+lsm_status lsm_level_view(const lsm_t* h, uint32_t i, const uint32_t** d_keys,
+                          const uint32_t** d_vals, uint64_t* n) {
+  if (!h || !d_keys || !d_vals || !n || i >= LSM_MAX_LEVELS) return LSM_ERR_INVALID_ARG;
+  if ((h->r >> i) & 1ull) {
+    *d_keys = h->level[i].keys;
+    *d_vals = h->level[i].vals;
+    *n = h->b << i;
+  } else {
+    *d_keys = nullptr;
+    *d_vals = nullptr;
+    *n = 0;
+  }
+  return LSM_OK;
+}
+
+lsm_status lsm_sync(lsm_t* h, void* stream) {
+  if (!h) return LSM_ERR_INVALID_ARG;
+  cudaStream_t s = S(stream);
+  if (h->sort.err) {
+    CK(cudaMemcpyAsync(h->h_pinned + 1, h->sort.err, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    uint32_t v = (uint32_t)(h->h_pinned[1] & 0xFFFFFFFFu);
+    if (v) {
+      CK(cudaMemsetAsync(h->sort.err, 0, 4, s));
+      CK(cudaStreamSynchronize(s));
+      return LSM_ERR_KEY_DOMAIN;
+    }
+  } else {
+    CK(cudaStreamSynchronize(s));
+  }
+  CK(cudaGetLastError());
+  return LSM_OK;
+}
+
+uint64_t lsm_launch_count(const lsm_t* h) { return h ? h->launches : 0; }
+
+lsm_status lsm_profile_enable(lsm_t* h, int on) {
+  if (!h) return LSM_ERR_INVALID_ARG;
+  cudaDeviceSynchronize();
+  for (auto& p : h->prof) {
+    h->ev_free.push_back(p.e0);
+    h->ev_free.push_back(p.e1);
+  }
+  h->prof.clear();
+  h->totals = lsm_profile{};
+  h->prof_on = on != 0;
+  return LSM_OK;
+}
+
+lsm_status lsm_profile_read(lsm_t* h, lsm_profile* out) {
+  if (!h || !out) return LSM_ERR_INVALID_ARG;
+  for (auto& p : h->prof) {
+    CK(cudaEventSynchronize(p.e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, p.e0, p.e1));
+    h->totals.ms[p.cls] += ms;
+    h->totals.alg_bytes[p.cls] += p.bytes;
+    h->ev_free.push_back(p.e0);
+    h->ev_free.push_back(p.e1);
+  }
+  h->prof.clear();
+  *out = h->totals;
+  return LSM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,344 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle.
+
+Structure: level key/value arrays bit-exact vs S1 after every mutation.
+Queries: lookup / count / range results exactly equal to O1 (range compared
+per query as the sorted pair list, which is unique). All integer work, so
+the tolerance is zero (BASELINE.json north_star).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests import lsm_script
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+import paper_1707_05354_b200 as pkg  # noqa: E402
+from paper_1707_05354_b200 import to_device, to_numpy_u32  # noqa: E402
+
+
+class GpuAdapter:
+    def __init__(self, b):
+        self.lsm = pkg.GpuLSM(b)
+
+    def update(self, k, v, d):
+        self.lsm.update(to_device(k), to_device(v), to_device(d.astype(np.uint8)))
+
+    def lookup(self, q):
+        v, f = self.lsm.lookup(to_device(q))
+        return to_numpy_u32(v), f.cpu().numpy()
+
+    def count(self, k1, k2):
+        return to_numpy_u32(self.lsm.count(to_device(k1), to_device(k2)))
+
+    def range(self, k1, k2):
+        off, ks, vs = self.lsm.range(to_device(k1), to_device(k2))
+        return off.cpu().numpy().astype(np.uint64), to_numpy_u32(ks), to_numpy_u32(vs)
+
+    def cleanup(self):
+        self.lsm.cleanup()
+
+    @property
+    def r(self):
+        return self.lsm.r
+
+    def level(self, i):
+        k, v = self.lsm.level(i)
+        return to_numpy_u32(k), to_numpy_u32(v)
+
+    def num_levels(self):
+        return max(self.r.bit_length(), 1)
+
+
+def assert_levels_equal(gpu, s1, where=""):
+    assert gpu.r == s1.r, where
+    for i in range(max(gpu.r.bit_length(), s1.num_levels())):
+        gk, gv = gpu.level(i)
+        sk, sv = s1.level(i) if i < s1.num_levels() else (np.zeros(0, np.uint32),) * 2
+        assert len(gk) == len(sk), f"{where} level {i}: {len(gk)} vs {len(sk)}"
+        if not np.array_equal(gk, sk):
+            bad = np.nonzero(gk != sk)[0]
+            raise AssertionError(f"{where} level {i} keys differ at {bad[:10]} "
+                                 f"gpu={gk[bad[:10]]} s1={sk[bad[:10]]}")
+        assert np.array_equal(gv, sv), f"{where} level {i} vals differ"
+
+
+def assert_queries_equal(gpu, o1, lookups, k1, k2, where=""):
+    gv, gf = gpu.lookup(lookups)
+    ov, of = o1.lookup(lookups)
+    assert np.array_equal(gf, of), f"{where} lookup found mismatch"
+    assert np.array_equal(gv, ov), f"{where} lookup value mismatch"
+    gc = gpu.count(k1, k2)
+    oc = o1.count(k1, k2)
+    assert np.array_equal(gc, oc), f"{where} count mismatch at {np.nonzero(gc != oc)[0][:10]}"
+    goff, gk, gvv = gpu.range(k1, k2)
+    ooff, ok, ovv = o1.range(k1, k2)
+    assert np.array_equal(goff, ooff), f"{where} range offsets mismatch"
+    assert np.array_equal(gk, ok) and np.array_equal(gvv, ovv), f"{where} range pairs mismatch"
+    assert np.array_equal(np.diff(goff).astype(np.uint32), gc)  # count == len(range)
+
+
+@pytest.mark.parametrize("path", lsm_script.golden_files(), ids=lambda p: p.split("/")[-1])
+def test_golden_scripts_gpu(path):
+    lsm_script.run(path, GpuAdapter)
+
+
+def _run_schedule(b, nbatch, seed, frac4=1, alphabet=None, nlook=2000, nrange=300,
+                  Ls=(8, 64), cleanup_every=None, check_levels=True):
+    g = GpuAdapter(b)
+    s1 = oracle.ShadowLSM(b)
+    o1 = oracle.OracleDict(b)
+    dom = synth.D if alphabet is None else alphabet + 2
+    for j in range(nbatch):
+        k, v, d = synth.updates(seed, j * b, b, delete_frac4=frac4, alphabet=alphabet)
+        g.update(k, v, d)
+        s1.update(k, v, d)
+        o1.apply_batch(k, v, d)
+        if check_levels:
+            assert_levels_equal(g, s1, f"b={b} batch {j}")
+        q = synth.lookup_queries(seed + j, nlook, (j + 1) * b, alphabet)
+        L = Ls[j % len(Ls)]
+        k1, k2 = synth.range_queries(seed + j, nrange, (j + 1) * b, L, domain=dom)
+        assert_queries_equal(g, o1, q, k1, k2, f"b={b} batch {j}")
+        if cleanup_every and (j + 1) % cleanup_every == 0:
+            g.cleanup()
+            s1.cleanup()
+            o1.cleanup()
+            assert_levels_equal(g, s1, f"b={b} cleanup after {j}")
+            assert_queries_equal(g, o1, q, k1, k2, f"b={b} after cleanup {j}")
+    return g, s1, o1
+
+
+def test_config_c1():
+    # BASELINE.json configs[0]: b=1024, r=15 batches, 75% insert / 25% delete,
+    # 10^4 lookups + 10^3 count/range queries; then cleanup and repeat.
+    b = 1024
+    g, s1, o1 = _run_schedule(b, 15, synth.SEED_BASE + 0, frac4=1, nlook=10_000, nrange=1000)
+    g.cleanup()
+    s1.cleanup()
+    o1.cleanup()
+    assert_levels_equal(g, s1, "C1 cleanup")
+    q = synth.lookup_queries(synth.SEED_BASE, 10_000, 15 * b)
+    k1, k2 = synth.range_queries(synth.SEED_BASE, 1000, 15 * b, 8)
+    assert_queries_equal(g, o1, q, k1, k2, "C1 after cleanup")
+    # idempotence
+    g.cleanup()
+    s1.cleanup()
+    assert_levels_equal(g, s1, "C1 second cleanup")
+
+
+def test_config_c1_duplicates():
+    # C1-dup: keys mod 4096 force duplicates, in-batch insert+delete, re-inserts
+    _run_schedule(1024, 15, synth.SEED_BASE + 10, frac4=1, alphabet=4096, nlook=5000,
+                  nrange=500, cleanup_every=5)
+
+
+@pytest.mark.parametrize("b", [1, 2, 3, 5, 33, 100, 4095, 4096, 4097, 10_000])
+def test_ragged_batch_sizes(b):
+    nb = 9 if b < 5000 else 5
+    _run_schedule(b, nb, 77 + b, frac4=2, alphabet=3 * b + 7, nlook=500, nrange=100,
+                  cleanup_every=4)
+
+
+@pytest.mark.parametrize("b", [1 << 16, (1 << 17) + 123])
+def test_multi_tile_sort_and_merge(b):
+    # several sort tiles (4096) with a ragged tail; merges of 2b and 4b over
+    # many merge tiles; uniform 31-bit keys
+    _run_schedule(b, 4, 4242, frac4=1, nlook=20_000, nrange=2000)
+
+
+def test_partial_batches():
+    b = 1000
+    g = GpuAdapter(b)
+    s1 = oracle.ShadowLSM(b)
+    o1 = oracle.OracleDict(b)
+    rng = np.random.default_rng(5)
+    for j in range(12):
+        n = int(rng.integers(1, b + 1))
+        k, v, d = synth.updates(9, j * b, n, delete_frac4=1, alphabet=2000)
+        g.update(k, v, d)
+        s1.update(k, v, d)
+        o1.apply_batch(k, v, d)
+        assert_levels_equal(g, s1, f"partial {j}")
+    q = np.arange(2002, dtype=np.uint32)
+    k1, k2 = synth.range_queries(1, 200, 12 * b, 20, domain=2002)
+    assert_queries_equal(g, o1, q, k1, k2, "partial")
+
+
+def test_edge_queries():
+    b = 64
+    g = GpuAdapter(b)
+    o1 = oracle.OracleDict(b)
+    # queries on an empty LSM (R22)
+    q = np.array([0, 1, 0x7FFFFFFE, 0x7FFFFFFF, 0xFFFFFFFF], np.uint32)
+    v, f = g.lookup(q)
+    assert not f.any() and np.all(v == pkg.LSM_NOT_FOUND)
+    assert g.count(np.array([0], np.uint32), np.array([0xFFFFFFFF], np.uint32))[0] == 0
+    off, ks, vs = g.range(np.array([0], np.uint32), np.array([0xFFFFFFFF], np.uint32))
+    assert off.tolist() == [0, 0] and len(ks) == 0
+    # empty query batch (nq == 0)
+    e = torch.empty(0, dtype=torch.int32, device="cuda")
+    vv, ff = g.lsm.lookup(e)
+    assert vv.numel() == 0
+    assert g.lsm.count(e, e).numel() == 0
+    off, ks, vs = g.lsm.range(e, e)
+    assert off.cpu().tolist() == [0]
+    # max key and boundary keys; k1 > k2 (R9); a stored value 0xFFFFFFFF
+    k = np.array([0, 0x7FFFFFFE, 5, 6], np.uint32)
+    v = np.array([7, 8, 0xFFFFFFFF, 9], np.uint32)
+    d = np.zeros(4, np.uint8)
+    g.update(k, v, d)
+    o1.apply_batch(k, v, d)
+    q = np.array([0, 0x7FFFFFFE, 0x7FFFFFFF, 0xFFFFFFFF, 5, 6, 4], np.uint32)
+    k1 = np.array([0, 6, 0x7FFFFFFE, 0, 10, 0xFFFFFFFF], np.uint32)
+    k2 = np.array([0xFFFFFFFF, 5, 0xFFFFFFFF, 0x7FFFFFFE, 9, 0xFFFFFFFF], np.uint32)
+    assert_queries_equal(g, o1, q, k1, k2, "edge")
+    gv, gf = g.lookup(np.array([5], np.uint32))
+    assert gf[0] == 1 and gv[0] == 0xFFFFFFFF
+
+
+def test_out_of_domain_key_is_sticky_error():
+    b = 8
+    g = GpuAdapter(b)
+    s1 = oracle.ShadowLSM(b)
+    k = np.array([1, 0x7FFFFFFF, 2, 0xFFFFFFFF], np.uint32)
+    v = np.arange(4, dtype=np.uint32)
+    d = np.zeros(4, np.uint8)
+    g.update(k, v, d)
+    s1.update(k, v, d)
+    with pytest.raises(pkg.LsmError) as ei:
+        g.lsm.sync()
+    assert ei.value.code == pkg.LSM_ERR_KEY_DOMAIN
+    g.lsm.sync()  # cleared
+    assert_levels_equal(g, s1, "domain")
+
+
+def test_batch_size_errors():
+    g = pkg.GpuLSM(4)
+    with pytest.raises(pkg.LsmError):
+        g.update(to_device(np.arange(5, dtype=np.uint32)))
+    with pytest.raises(pkg.LsmError):
+        g.update(to_device(np.zeros(0, dtype=np.uint32)))
+    assert g.r == 0
+
+
+def test_insert_delete_entry_points():
+    b = 256
+    g = pkg.GpuLSM(b)
+    s1 = oracle.ShadowLSM(b)
+    k, v, _ = synth.updates(3, 0, b, delete_frac4=0, alphabet=500)
+    g.insert(to_device(k), to_device(v))
+    s1.update(k, v, np.zeros(b, np.uint8))
+    kd = k[: b // 2].copy()
+    g.delete(to_device(kd))
+    s1.update(kd, np.zeros(len(kd), np.uint32), np.ones(len(kd), np.uint8))
+    ad = GpuAdapter.__new__(GpuAdapter)
+    ad.lsm = g
+    assert_levels_equal(ad, s1, "insert/delete")
+
+
+def test_host_buffer_entry_points():
+    b = 512
+    g = pkg.GpuLSM(b)
+    o1 = oracle.OracleDict(b)
+    for j in range(6):
+        k, v, d = synth.updates(21, j * b, b, delete_frac4=1, alphabet=900)
+        g.update_host(k, v, d)
+        o1.apply_batch(k, v, d)
+    q = np.arange(902, dtype=np.uint32)
+    hv, hf = g.lookup_host(q)
+    ov, of = o1.lookup(q)
+    assert np.array_equal(hf, of) and np.array_equal(hv, ov)
+
+
+def test_determinism():
+    b = 3000
+    imgs = []
+    for _ in range(2):
+        g = GpuAdapter(b)
+        for j in range(7):
+            k, v, d = synth.updates(99, j * b, b, delete_frac4=1, alphabet=5000)
+            g.update(k, v, d)
+        imgs.append([g.level(i) for i in range(3)])
+    for (a, b_), (c, d_) in zip(*imgs):
+        assert np.array_equal(a, c) and np.array_equal(b_, d_)
+
+
+def test_launch_counter_counts_kernels():
+    g = pkg.GpuLSM(4096)
+    k, v, d = synth.updates(1, 0, 4096)
+    n0 = g.launch_count
+    g.update(to_device(k), to_device(v), to_device(d))
+    assert g.launch_count - n0 == 5  # histogram + 4 onesweep passes
+    g.update(to_device(k), to_device(v), to_device(d))
+    assert g.launch_count - n0 == 11  # + 5 + one merge
+
+
+@pytest.mark.slow
+def test_full_size_c3_sampled():
+    """BASELINE configs[2] at full size in bench.py's launch configuration:
+    b = 2^20, 64 mixed batches (n = 2^26). The oracle O1 is fed only updates
+    whose key lies in a sampled sub-range (keys never interact, so the
+    restriction is exact); lookups / counts / ranges inside that sub-range
+    are compared exactly, before and after cleanup. Structure is checked by
+    properties that hold at any size."""
+    b = 1 << 20
+    R = 64
+    seed = synth.SEED_BASE + 2
+    lo_key, hi_key = 1 << 24, (1 << 24) + (1 << 25)  # 1/64 of the domain
+    g = pkg.GpuLSM(b, reserve_batches=R)
+    o1 = oracle.OracleDict(b)
+    for j in range(R):
+        k, v, d = synth.updates(seed, j * b, b, delete_frac4=1)
+        g.update(to_device(k), to_device(v), to_device(d))
+        sel = (k >= lo_key) & (k < hi_key)
+        o1.apply_batch(k[sel], v[sel], d[sel])
+    g.sync()
+    assert g.r == R
+
+    def check(tag):
+        rng = np.random.default_rng(7)
+        q = np.concatenate([o1.items()[0][:20000],
+                            rng.integers(lo_key, hi_key, 20000).astype(np.uint32)])
+        gv, gf = g.lookup(to_device(q))
+        ov, of = o1.lookup(q)
+        assert np.array_equal(gf.cpu().numpy(), of), tag
+        assert np.array_equal(to_numpy_u32(gv), ov), tag
+        w = 8 * synth.D // (R * b)
+        k1 = rng.integers(lo_key, hi_key - w, 5000).astype(np.uint32)
+        k2 = (k1 + w).astype(np.uint32)
+        gc = to_numpy_u32(g.count(to_device(k1), to_device(k2)))
+        assert np.array_equal(gc, o1.count(k1, k2)), tag
+        off, ks, vs = g.range(to_device(k1), to_device(k2))
+        ooff, oks, ovs = o1.range(k1, k2)
+        assert np.array_equal(off.cpu().numpy().astype(np.uint64), ooff), tag
+        assert np.array_equal(to_numpy_u32(ks), oks) and np.array_equal(to_numpy_u32(vs), ovs)
+
+    def props():
+        for i in range(g.r.bit_length()):
+            k, _ = g.level(i)
+            kk = to_numpy_u32(k)
+            if (g.r >> i) & 1:
+                assert len(kk) == b << i
+                assert np.all((kk[1:] >> 1) >= (kk[:-1] >> 1))
+            else:
+                assert len(kk) == 0
+
+    props()
+    check("before cleanup")
+    g.cleanup()
+    assert g.r == -(-len_live(g) // b)
+    props()
+    check("after cleanup")
+
+
+def len_live(g):
+    tot = 0
+    for i in range(g.r.bit_length()):
+        k, _ = g.level(i)
+        kk = to_numpy_u32(k)
+        tot += int(np.count_nonzero(kk & 1))
+    return tot
