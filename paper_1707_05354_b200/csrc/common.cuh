@@ -41,6 +41,17 @@ __device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
 __device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// L2-coherent weak accesses (cache-global, bypass L1) for look-back status
+// words: a flag and its count share one aligned 32-bit word, so a reader
+// never sees a torn value; unlike strong relaxed accesses these coalesce.
+__device__ __forceinline__ uint32_t ld_cg(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_cg(uint32_t* p, uint32_t v) {
+  asm volatile("st.global.cg.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
   uint4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -129,23 +140,55 @@ enum UpdateMode { kModeInsert = 0, kModeDelete = 1, kModeMixed = 2 };
 
 struct SortScratch {
   uint32_t* hist;         // [2][4][256] double-buffered digit histograms
-  uint32_t* status;       // [4][tiles][256] decoupled look-back words
+  uint32_t* bases;        // [4][256] exclusive digit bases (last hist CTA)
+  uint32_t* done_ctr;     // hist CTAs finished (self-resetting)
+  uint32_t* status;       // [4][tiles][256] tile words + [4][groups][256] group words
   uint32_t* tile_ctr;     // [4] dynamic tile counters
   uint32_t* err;          // sticky domain-error flag
   uint32_t* tmp_keys[2];  // b-sized ping-pong for the passes
   uint32_t* tmp_vals[2];
   uint64_t tiles_cap;     // status capacity in tiles
   int parity;             // which hist half this sort uses
+  uint32_t epoch;         // sort counter -> look-back word epochs
 };
 
-constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;
+// one fat tile per SM: 1024 threads x 7 records (b = 2^20 -> 147 tiles)
+constexpr int kSortThreads = 1024;
+constexpr int kSortItems = 7;
 constexpr int kSortTile = kSortThreads * kSortItems;
 constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;
 constexpr int kPasses = 4;
 
 inline uint64_t sort_tiles(uint64_t b) { return (b + kSortTile - 1) / kSortTile; }
+inline uint64_t sort_groups(uint64_t b) { return (sort_tiles(b) + 31) / 32; }
+inline uint64_t sort_status_words(uint64_t b) {
+  return (uint64_t)kPasses * (sort_tiles(b) + sort_groups(b)) * kRadix;
+}
+
+// Programmatic dependent launch: every kernel on the update path waits for
+// its predecessor's results with griddepcontrol.wait (after a prologue that
+// touches no predecessor data) and lets its successor start launching.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                              cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 
 // Encode + stable LSD radix sort of one batch (status bit included) into
 // (out_keys, out_vals). Launches 1 histogram kernel + 4 onesweep passes.

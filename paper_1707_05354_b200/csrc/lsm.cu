@@ -136,9 +136,10 @@ cudaError_t buf_ensure(lsm* h, Buffer& B, uint64_t n, cudaStream_t s) {
   if (B.vals) cudaFreeAsync(B.vals, s);
   B.keys = B.vals = nullptr;
   B.cap = 0;
-  cudaError_t e = pool_alloc(h, (void**)&B.keys, n * 4, s);
+  // +16 elements: the merge's bulk copies read 16-byte-aligned supersets
+  cudaError_t e = pool_alloc(h, (void**)&B.keys, (n + 16) * 4, s);
   if (e != cudaSuccess) return e;
-  e = pool_alloc(h, (void**)&B.vals, n * 4, s);
+  e = pool_alloc(h, (void**)&B.vals, (n + 16) * 4, s);
   if (e != cudaSuccess) return e;
   B.cap = n;
   return cudaSuccess;
@@ -165,20 +166,21 @@ void level_release(lsm* h, int i, cudaStream_t s) {
 }
 
 cudaError_t ensure_sort_scratch(lsm* h, cudaStream_t s) {
-  const uint64_t tiles = sort_tiles(h->b);
   if (h->sort_meta == nullptr) {
-    // hist[2][4][256] | tile_ctr[4] | err[1] | pad | status[4][tiles][256]
-    const uint64_t head = 2 * kPasses * kRadix + 8;
-    h->sort_meta_words = head + (uint64_t)kPasses * tiles * kRadix;
+    // hist[2][4][256] | bases[4][256] | tile_ctr[4] | err | done | pad | status
+    const uint64_t head = 3 * kPasses * kRadix + 16;
+    h->sort_meta_words = head + sort_status_words(h->b);
     cudaError_t e = pool_alloc(h, (void**)&h->sort_meta, h->sort_meta_words * 4, s);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(h->sort_meta, 0, h->sort_meta_words * 4, s);
     if (e != cudaSuccess) return e;
     h->sort.hist = h->sort_meta;
-    h->sort.tile_ctr = h->sort_meta + 2 * kPasses * kRadix;
+    h->sort.bases = h->sort_meta + 2 * kPasses * kRadix;
+    h->sort.tile_ctr = h->sort_meta + 3 * kPasses * kRadix;
     h->sort.err = h->sort.tile_ctr + 4;
+    h->sort.done_ctr = h->sort.tile_ctr + 5;
     h->sort.status = h->sort_meta + head;
-    h->sort.tiles_cap = tiles;
+    h->sort.tiles_cap = sort_tiles(h->b);
     for (int k = 0; k < 2; ++k) {
       e = pool_alloc(h, (void**)&h->sort.tmp_keys[k], h->b * 4, s);
       if (e != cudaSuccess) return e;

@@ -7,14 +7,23 @@
 // (comparator (x >> 1) < (y >> 1)); reading R1 (the text, not Fig. 4's
 // argument order, fixes the tie rule).
 //
-// Design: merge-path partitioning inside the kernel, no
-// separate partition launch. Each CTA owns 4096 consecutive outputs; warp 0
-// and warp 1 find the CTA's two diagonal splits with a 32-ary cooperative
-// search (one ballot per round, ~log32(n) dependent round trips instead of
-// log2(n)). The CTA stages its A and B windows (keys and values) in shared
-// memory with coalesced loads, every thread finds its own 16-output split in
-// shared memory, merges 16 records into registers and writes them with
-// 128-bit stores.
+// Design: a persistent, warp-specialised merge-path kernel.
+//  * grid = 2 CTAs per SM; CTA c owns a contiguous run of 4096-output tiles.
+//  * warp 0 (producer) finds the merge-path split of every tile boundary:
+//    a full 32-ary cooperative search (one ballot per round) for the CTA's
+//    first diagonal, then a search HINTED by the previous split (the next
+//    split lies within 4096 of it: 3 rounds). It then moves the tile's A and
+//    B windows (keys and values) into a 3-stage shared-memory ring with
+//    cp.async.bulk (TMA bulk copies, 16-byte aligned supersets of the
+//    windows) completing on an mbarrier (expect_tx).
+//  * warps 1..8 (consumers) wait on the stage's mbarrier, each thread finds
+//    its own 16-output split inside the stage by binary search, merges 16
+//    records into registers and stores them with 128-bit writes, then
+//    releases the stage.
+// The search latency and the loads of tiles k+1, k+2 overlap the merge of
+// tile k; there is no partition launch and no block-wide barrier in the loop.
+
+#include <algorithm>
 
 #include "common.cuh"
 
@@ -22,19 +31,67 @@ namespace gpulsm {
 
 namespace {
 
-constexpr int kMergeThreads = 256;
+constexpr int kConsumerWarps = 8;
+constexpr int kMergeThreads = (kConsumerWarps + 1) * 32;
 constexpr int kMergeItems = 16;
-constexpr int kMergeTile = kMergeThreads * kMergeItems;
+constexpr int kMergeTile = kConsumerWarps * 32 * kMergeItems;  // 4096
+constexpr int kStages = 3;
+constexpr int kBufElems = kMergeTile + 16;  // A + B windows incl. alignment slack
 
-// Number of A elements among the first d outputs of merge(A, B) with A taken
-// first on ties: the first i in [max(0,d-nb), min(d,na)] with
-// !((A[i]>>1) <= (B[d-1-i]>>1)). Whole warp participates.
-__device__ __forceinline__ uint64_t warp_merge_path(const uint32_t* __restrict__ ak, uint64_t na,
-                                                    const uint32_t* __restrict__ bk, uint64_t nb,
-                                                    uint64_t d) {
+struct StageInfo {
+  uint64_t d0;
+  uint32_t na, nb;          // window lengths (elements)
+  uint32_t ka, kb, va, vb;  // element offsets of A/B data in the key/val buffers
+};
+
+struct MergeSmem {
+  uint32_t keys[kStages][kBufElems];
+  uint32_t vals[kStages][kBufElems];
+  StageInfo info[kStages];
+  unsigned long long full[kStages];
+  unsigned long long empty[kStages];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* b, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(tx)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// First i in [lo, hi] with !((A[i]>>1) <= (B[d-1-i]>>1)): the number of A
+// records among the first d outputs (A first on ties). Whole warp.
+__device__ __forceinline__ uint64_t warp_merge_path(const uint32_t* __restrict__ ak,
+                                                    const uint32_t* __restrict__ bk, uint64_t d,
+                                                    uint64_t lo, uint64_t hi) {
   const uint32_t lane = lane_id();
-  uint64_t lo = d > nb ? d - nb : 0;
-  uint64_t hi = d < na ? d : na;
   while (hi - lo > 32) {
     const uint64_t span = hi - lo;
     const uint64_t p = lo + ((uint64_t)(lane + 1) * span) / 33;
@@ -46,9 +103,8 @@ __device__ __forceinline__ uint64_t warp_merge_path(const uint32_t* __restrict__
     if (c > 0) lo = plo + 1;
     if (c < 32) hi = phi;
   }
-  const uint64_t span = hi - lo;
   bool t = false;
-  if (lane < span) {
+  if (lane < hi - lo) {
     const uint64_t p = lo + lane;
     t = (__ldg(ak + p) >> 1) <= (__ldg(bk + (d - 1 - p)) >> 1);
   }
@@ -58,78 +114,143 @@ __device__ __forceinline__ uint64_t warp_merge_path(const uint32_t* __restrict__
 __global__ void __launch_bounds__(kMergeThreads) merge_kernel(
     const uint32_t* __restrict__ ak, const uint32_t* __restrict__ av, uint64_t na,
     const uint32_t* __restrict__ bk, const uint32_t* __restrict__ bv, uint64_t nb,
-    uint32_t* __restrict__ ok, uint32_t* __restrict__ ov) {
-  __shared__ uint32_t sk[kMergeTile];
-  __shared__ uint32_t sv[kMergeTile];
-  __shared__ uint64_t s_split[2];
-  const int tid = threadIdx.x, warp = tid >> 5;
+    uint32_t* __restrict__ ok, uint32_t* __restrict__ ov, uint64_t ntiles) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  MergeSmem& S = *reinterpret_cast<MergeSmem*>(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint64_t total = na + nb;
-  const uint64_t d0 = (uint64_t)blockIdx.x * kMergeTile;
-  const uint64_t d1 = min(d0 + kMergeTile, total);
-  if (warp < 2) {
-    const uint64_t i = warp_merge_path(ak, na, bk, nb, warp == 0 ? d0 : d1);
-    if (lane_id() == 0) s_split[warp] = i;
-  }
-  __syncthreads();
-  const uint64_t a0 = s_split[0], a1 = s_split[1];
-  const uint64_t b0 = d0 - a0;
-  const uint32_t na_t = (uint32_t)(a1 - a0);
-  const uint32_t tile_n = (uint32_t)(d1 - d0);
-  const uint32_t nb_t = tile_n - na_t;
+  const uint64_t t_begin = (uint64_t)blockIdx.x * ntiles / gridDim.x;
+  const uint64_t t_end = (uint64_t)(blockIdx.x + 1) * ntiles / gridDim.x;
 
-  for (uint32_t idx = tid; idx < tile_n; idx += kMergeThreads) {
-    if (idx < na_t) {
-      sk[idx] = __ldg(ak + a0 + idx);
-      sv[idx] = __ldg(av + a0 + idx);
-    } else {
-      sk[idx] = __ldg(bk + b0 + (idx - na_t));
-      sv[idx] = __ldg(bv + b0 + (idx - na_t));
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&S.full[s], 1);
+      mbar_init(&S.empty[s], kConsumerWarps);
     }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  pdl_wait();  // inputs are the predecessor's outputs
+  pdl_trigger();
 
-  // per-thread split at diagonal dt inside the tile
-  const uint32_t dt = min((uint32_t)(tid * kMergeItems), tile_n);
-  uint32_t lo = dt > nb_t ? dt - nb_t : 0;
-  uint32_t hi = min(dt, na_t);
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if ((sk[mid] >> 1) <= (sk[na_t + dt - 1 - mid] >> 1))
-      lo = mid + 1;
-    else
-      hi = mid;
-  }
-  uint32_t ai = lo, bi = dt - lo;
-  uint32_t rk[kMergeItems], rv[kMergeItems];
+  if (warp == 0) {
+    // ---------------- producer ----------------
+    uint64_t d = t_begin * kMergeTile;
+    uint64_t a = warp_merge_path(ak, bk, d, d > nb ? d - nb : 0, d < na ? d : na);
+    for (uint64_t t = t_begin, k = 0; t < t_end; ++t, ++k) {
+      const uint64_t d_end = min(d + (uint64_t)kMergeTile, total);
+      uint64_t lo = d_end > nb ? d_end - nb : 0;
+      lo = max(lo, a);
+      uint64_t hi = min(a + (d_end - d), na);
+      const uint64_t a_end = warp_merge_path(ak, bk, d_end, lo, hi);
+      const int s = (int)(k % kStages);
+      const uint32_t ph = (uint32_t)((k / kStages) & 1);
+      mbar_wait(&S.empty[s], ph ^ 1u);
+      if (lane == 0) {
+        const uint64_t b0 = d - a, b1 = d_end - a_end;
+        StageInfo info;
+        info.d0 = d;
+        info.na = (uint32_t)(a_end - a);
+        info.nb = (uint32_t)(b1 - b0);
+        // 16-byte-aligned supersets of the four windows (A then B per array)
+        const void* src[4];
+        uint32_t bytes[4];
+        uint32_t* dst[4];
+        uint32_t off[4];
+        const uint32_t* arr[4] = {ak + a, bk + b0, av + a, bv + b0};
+        const uint32_t* arr_end[4] = {ak + a_end, bk + b1, av + a_end, bv + b1};
+        const uint32_t cnt[4] = {info.na, info.nb, info.na, info.nb};
+        uint32_t tx = 0;
 #pragma unroll
-  for (int k = 0; k < kMergeItems; ++k) {
-    const bool takeA = (bi >= nb_t) || (ai < na_t && (sk[ai] >> 1) <= (sk[na_t + bi] >> 1));
-    uint32_t idx = takeA ? ai : na_t + bi;
-    idx = min(idx, (uint32_t)(kMergeTile - 1));
-    rk[k] = sk[idx];
-    rv[k] = sv[idx];
-    ai += takeA ? 1u : 0u;
-    bi += takeA ? 0u : 1u;
-  }
-
-  const uint64_t base = d0 + dt;
-  const bool full = dt + kMergeItems <= tile_n;
-  if (full && ((reinterpret_cast<uintptr_t>(ok + base) | reinterpret_cast<uintptr_t>(ov + base)) & 15) == 0) {
+        for (int w = 0; w < 4; ++w) {
+          const uintptr_t s0 = reinterpret_cast<uintptr_t>(arr[w]) & ~(uintptr_t)15;
+          const uintptr_t e0 = (reinterpret_cast<uintptr_t>(arr_end[w]) + 15) & ~(uintptr_t)15;
+          bytes[w] = cnt[w] ? (uint32_t)(e0 - s0) : 0u;
+          src[w] = reinterpret_cast<const void*>(s0);
+          off[w] = (uint32_t)((reinterpret_cast<uintptr_t>(arr[w]) - s0) >> 2);
+          tx += bytes[w];
+        }
+        dst[0] = &S.keys[s][0];
+        dst[1] = &S.keys[s][bytes[0] >> 2];
+        dst[2] = &S.vals[s][0];
+        dst[3] = &S.vals[s][bytes[2] >> 2];
+        info.ka = off[0];
+        info.kb = (bytes[0] >> 2) + off[1];
+        info.va = off[2];
+        info.vb = (bytes[2] >> 2) + off[3];
+        S.info[s] = info;
+        mbar_arrive_expect_tx(&S.full[s], tx);  // release: info visible to consumers
 #pragma unroll
-    for (int q = 0; q < kMergeItems / 4; ++q) {
-      stg_v4(ok + base + 4 * q, make_uint4(rk[4 * q], rk[4 * q + 1], rk[4 * q + 2], rk[4 * q + 3]));
-      stg_v4(ov + base + 4 * q, make_uint4(rv[4 * q], rv[4 * q + 1], rv[4 * q + 2], rv[4 * q + 3]));
+        for (int w = 0; w < 4; ++w)
+          if (bytes[w]) bulk_g2s(dst[w], src[w], bytes[w], &S.full[s]);
+      }
+      __syncwarp();
+      a = a_end;
+      d = d_end;
     }
   } else {
+    // ---------------- consumers ----------------
+    const uint32_t ct = tid - 32;
+    for (uint64_t t = t_begin, k = 0; t < t_end; ++t, ++k) {
+      const int s = (int)(k % kStages);
+      const uint32_t ph = (uint32_t)((k / kStages) & 1);
+      mbar_wait(&S.full[s], ph);
+      const StageInfo info = S.info[s];
+      const uint32_t* K = S.keys[s];
+      const uint32_t* V = S.vals[s];
+      const uint32_t na_t = info.na, nb_t = info.nb, tile_n = na_t + nb_t;
+      const uint32_t dt = min(ct * kMergeItems, tile_n);
+      uint32_t lo = dt > nb_t ? dt - nb_t : 0;
+      uint32_t hi = min(dt, na_t);
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if ((K[info.ka + mid] >> 1) <= (K[info.kb + dt - 1 - mid] >> 1))
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      uint32_t ai = lo, bi = dt - lo;
+      uint32_t ka = ai < na_t ? K[info.ka + ai] : 0u;
+      uint32_t kb = bi < nb_t ? K[info.kb + bi] : 0u;
+      uint32_t rk[kMergeItems], rv[kMergeItems];
 #pragma unroll
-    for (int k = 0; k < kMergeItems; ++k) {
-      if (dt + k < tile_n) {
-        ok[base + k] = rk[k];
-        ov[base + k] = rv[k];
+      for (int q = 0; q < kMergeItems; ++q) {
+        const bool takeA = (bi >= nb_t) || (ai < na_t && (ka >> 1) <= (kb >> 1));
+        if (takeA) {
+          rk[q] = ka;
+          rv[q] = V[min(info.va + ai, (uint32_t)kBufElems - 1)];
+          ++ai;
+          ka = ai < na_t ? K[info.ka + ai] : 0u;
+        } else {
+          rk[q] = kb;
+          rv[q] = V[min(info.vb + bi, (uint32_t)kBufElems - 1)];
+          ++bi;
+          kb = bi < nb_t ? K[info.kb + bi] : 0u;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.empty[s]);  // smem no longer needed
+      const uint64_t base = info.d0 + dt;
+      if (dt + kMergeItems <= tile_n) {
+#pragma unroll
+        for (int q = 0; q < kMergeItems / 4; ++q) {
+          stg_v4(ok + base + 4 * q, make_uint4(rk[4 * q], rk[4 * q + 1], rk[4 * q + 2], rk[4 * q + 3]));
+          stg_v4(ov + base + 4 * q, make_uint4(rv[4 * q], rv[4 * q + 1], rv[4 * q + 2], rv[4 * q + 3]));
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < kMergeItems; ++q) {
+          if (dt + q < tile_n) {
+            ok[base + q] = rk[q];
+            ov[base + q] = rv[q];
+          }
+        }
       }
     }
   }
 }
+
+int g_num_sms = 0;
 
 }  // namespace
 
@@ -138,12 +259,27 @@ cudaError_t launch_merge(const uint32_t* ak, const uint32_t* av, uint64_t na,
                          uint32_t* ov, cudaStream_t s, const LaunchHooks& hk) {
   const uint64_t total = na + nb;
   if (total == 0) return cudaSuccess;
-  const uint64_t grid = (total + kMergeTile - 1) / kMergeTile;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(MergeSmem));
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    attr_set = true;
+  }
+  // outputs must be 16-byte aligned for the vector stores
+  if ((reinterpret_cast<uintptr_t>(ok) | reinterpret_cast<uintptr_t>(ov)) & 15)
+    return cudaErrorMisalignedAddress;
+  const uint64_t ntiles = (total + kMergeTile - 1) / kMergeTile;
+  const uint64_t grid = std::min<uint64_t>(ntiles, (uint64_t)g_num_sms * 2);
   hk.begin(hk.ctx, LSM_K_MERGE, s);
-  merge_kernel<<<(unsigned)grid, kMergeThreads, 0, s>>>(ak, av, na, bk, bv, nb, ok, ov);
+  cudaError_t e = launch_pdl(merge_kernel, (unsigned)grid, kMergeThreads, sizeof(MergeSmem), s, ak,
+                             av, na, bk, bv, nb, ok, ov, ntiles);
   // algorithmic bytes: each output record is read once (8 B) and written once
   hk.end(hk.ctx, LSM_K_MERGE, (double)total * 16.0, s, 1);
-  return cudaGetLastError();
+  return e;
 }
 
 }  // namespace gpulsm

@@ -60,45 +60,60 @@ __global__ void __launch_bounds__(kQThreads) lookup_kernel(LevelTable T,
 }
 
 // Per-query multi-way walk over the candidate slices [l_j, u_j) of the
-// occupied levels. Calls emit(key, val) for each valid key in ascending
-// order; returns the number of valid keys.
-template <typename Emit>
+// occupied levels. Calls emit(idx, key, val) for each valid key in ascending
+// order; returns the number of valid keys. NL > 0: exactly NL levels, state
+// in registers (fully unrolled); NL == 0: generic (T.count levels, local
+// memory), used only beyond kMaxUnrolledLevels occupied levels.
+constexpr int kMaxUnrolledLevels = 16;
+
+template <int NL, typename Emit>
 __device__ __forceinline__ uint32_t walk_range(const LevelTable& T, uint32_t a, uint32_t z,
                                                Emit emit) {
   if (a > z) return 0;  // R9: the empty range
-  uint64_t pos[LSM_MAX_LEVELS], end[LSM_MAX_LEVELS];
-  uint32_t head[LSM_MAX_LEVELS];
-  const int L = T.count;
-  for (int j = 0; j < L; ++j) {  // stage 1: per-level bounds
-    const uint32_t* K = T.keys[j];
-    const uint64_t l = lower_bound_orig(K, T.n[j], a);
-    const uint64_t u = upper_bound_orig(K, T.n[j], z);
-    pos[j] = l;
-    end[j] = u;
-    head[j] = l < u ? (__ldg(K + l) >> 1) : kSent;
+  constexpr int CAP = NL > 0 ? NL : LSM_MAX_LEVELS;
+  const int L = NL > 0 ? NL : T.count;
+  uint64_t pos[CAP], end[CAP];
+  uint32_t head[CAP];
+#pragma unroll
+  for (int j = 0; j < CAP; ++j) {  // stage 1: per-level bounds
+    if (j < L) {
+      const uint32_t* K = T.keys[j];
+      const uint64_t l = lower_bound_orig(K, T.n[j], a);
+      const uint64_t u = upper_bound_orig(K, T.n[j], z);
+      pos[j] = l;
+      end[j] = u;
+      head[j] = l < u ? (__ldg(K + l) >> 1) : kSent;
+    }
   }
   uint32_t cnt = 0;
   while (true) {
     uint32_t m = kSent;
-    for (int j = 0; j < L; ++j) m = min(m, head[j]);
+#pragma unroll
+    for (int j = 0; j < CAP; ++j)
+      if (j < L) m = min(m, head[j]);
     if (m == kSent) break;
     bool first = true, valid = false;
     uint32_t val = 0;
-    for (int j = 0; j < L; ++j) {
-      if (head[j] != m) continue;
-      const uint32_t* K = T.keys[j];
-      uint64_t p = pos[j];
-      if (first) {  // newest record of key m: run head in the lowest level
-        first = false;
-        valid = (__ldg(K + p) & 1u) != 0;
-        if (valid) val = __ldg(T.vals[j] + p);
+#pragma unroll
+    for (int j = 0; j < CAP; ++j) {
+      if (j < L && head[j] == m) {
+        const uint32_t* K = T.keys[j];
+        uint64_t p = pos[j];
+        if (first) {  // newest record of key m: run head in the lowest level
+          first = false;
+          valid = (__ldg(K + p) & 1u) != 0;
+          if (valid) val = __ldg(T.vals[j] + p);
+        }
+        // skip the rest of this level's run of key m (stale copies)
+        uint32_t nk = kSent;
+        while (++p < end[j]) {
+          nk = __ldg(K + p) >> 1;
+          if (nk != m) break;
+          nk = kSent;
+        }
+        pos[j] = p;
+        head[j] = p < end[j] ? nk : kSent;
       }
-      // skip the rest of this level's run of key m (stale copies)
-      do {
-        ++p;
-      } while (p < end[j] && (__ldg(K + p) >> 1) == m);
-      pos[j] = p;
-      head[j] = p < end[j] ? (__ldg(K + p) >> 1) : kSent;
     }
     if (valid) {
       emit(cnt, m, val);
@@ -108,6 +123,7 @@ __device__ __forceinline__ uint32_t walk_range(const LevelTable& T, uint32_t a, 
   return cnt;
 }
 
+template <int NL>
 __global__ void __launch_bounds__(kQThreads) count_kernel(LevelTable T,
                                                           const uint32_t* __restrict__ k1,
                                                           const uint32_t* __restrict__ k2,
@@ -115,9 +131,10 @@ __global__ void __launch_bounds__(kQThreads) count_kernel(LevelTable T,
                                                           uint32_t* __restrict__ counts) {
   const uint64_t i = (uint64_t)blockIdx.x * kQThreads + threadIdx.x;
   if (i >= nq) return;
-  counts[i] = walk_range(T, __ldg(k1 + i), __ldg(k2 + i), [](uint32_t, uint32_t, uint32_t) {});
+  counts[i] = walk_range<NL>(T, __ldg(k1 + i), __ldg(k2 + i), [](uint32_t, uint32_t, uint32_t) {});
 }
 
+template <int NL>
 __global__ void __launch_bounds__(kQThreads) range_write_kernel(
     LevelTable T, const uint32_t* __restrict__ k1, const uint32_t* __restrict__ k2, uint64_t nq,
     const uint64_t* __restrict__ offsets, uint32_t* __restrict__ keys_out,
@@ -125,10 +142,42 @@ __global__ void __launch_bounds__(kQThreads) range_write_kernel(
   const uint64_t i = (uint64_t)blockIdx.x * kQThreads + threadIdx.x;
   if (i >= nq) return;
   const uint64_t base = offsets[i];
-  walk_range(T, __ldg(k1 + i), __ldg(k2 + i), [&](uint32_t c, uint32_t key, uint32_t val) {
+  walk_range<NL>(T, __ldg(k1 + i), __ldg(k2 + i), [&](uint32_t c, uint32_t key, uint32_t val) {
     keys_out[base + c] = key;
     vals_out[base + c] = val;
   });
+}
+
+// dispatch on the number of occupied levels
+#define GPULSM_NL_CASES(M) \
+  M(1) M(2) M(3) M(4) M(5) M(6) M(7) M(8) M(9) M(10) M(11) M(12) M(13) M(14) M(15) M(16)
+
+template <typename... Args>
+void launch_count_nl(int nl, dim3 g, dim3 b, cudaStream_t s, Args... args) {
+  switch (nl) {
+#define GPULSM_C(N) \
+  case N:          \
+    count_kernel<N><<<g, b, 0, s>>>(args...); \
+    return;
+    GPULSM_NL_CASES(GPULSM_C)
+#undef GPULSM_C
+    default:
+      count_kernel<0><<<g, b, 0, s>>>(args...);
+  }
+}
+
+template <typename... Args>
+void launch_range_nl(int nl, dim3 g, dim3 b, cudaStream_t s, Args... args) {
+  switch (nl) {
+#define GPULSM_R(N) \
+  case N:          \
+    range_write_kernel<N><<<g, b, 0, s>>>(args...); \
+    return;
+    GPULSM_NL_CASES(GPULSM_R)
+#undef GPULSM_R
+    default:
+      range_write_kernel<0><<<g, b, 0, s>>>(args...);
+  }
 }
 
 // ---------------------------- exclusive scan -------------------------------
@@ -210,7 +259,11 @@ cudaError_t launch_count(const LevelTable& T, const uint32_t* k1, const uint32_t
                          const LaunchHooks& hk, int cls) {
   if (nq == 0) return cudaSuccess;
   hk.begin(hk.ctx, cls, s);
-  count_kernel<<<grid_for(nq, kQThreads), kQThreads, 0, s>>>(T, k1, k2, nq, counts_out);
+  if (T.count == 0) {
+    cudaMemsetAsync(counts_out, 0, nq * 4, s);
+  } else {
+    launch_count_nl(T.count, grid_for(nq, kQThreads), kQThreads, s, T, k1, k2, nq, counts_out);
+  }
   hk.end(hk.ctx, cls, (double)nq * (12.0 + 64.0 * T.count), s, 1);
   return cudaGetLastError();
 }
@@ -233,8 +286,9 @@ cudaError_t launch_range_write(const LevelTable& T, const uint32_t* k1, const ui
                                uint32_t* vals_out, cudaStream_t s, const LaunchHooks& hk) {
   if (nq == 0) return cudaSuccess;
   hk.begin(hk.ctx, LSM_K_RANGE, s);
-  range_write_kernel<<<grid_for(nq, kQThreads), kQThreads, 0, s>>>(T, k1, k2, nq, offsets,
-                                                                    keys_out, vals_out);
+  if (T.count > 0)
+    launch_range_nl(T.count, grid_for(nq, kQThreads), kQThreads, s, T, k1, k2, nq, offsets,
+                    keys_out, vals_out);
   hk.end(hk.ctx, LSM_K_RANGE, (double)nq * (16.0 + 64.0 * T.count), s, 1);
   return cudaGetLastError();
 }

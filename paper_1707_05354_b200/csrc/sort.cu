@@ -6,24 +6,36 @@
 // same key), reading R4 (stability: equal key variables keep input order, so
 // the first of duplicate inserts wins).
 //
-// Design: a onesweep-style LSD radix sort, 4 passes of 8
-// bits over the 32-bit key variable.
-//   * sort_hist_kernel: reads the raw batch once, encodes on the fly, and
-//     builds all four digit histograms (smem atomics, one global atomic per
-//     bin per CTA). It also zeroes the look-back status words and tile
-//     counters of this sort and the other half of the double-buffered
-//     histogram (for the next sort), so no memset launch is needed.
-//   * onesweep_pass_kernel<FIRST>: one kernel per digit. Tiles of 4096
-//     records (256 threads x 16) are claimed in launch order from an atomic
-//     counter; ranks inside a tile come from warp match_any + per-warp digit
-//     counters (stable: order = (warp, item, lane) = input order); the
-//     tile's digit counts are published to a decoupled look-back array so
-//     the global offset of every digit is known after one pass; records are
-//     then staged in shared memory in digit order and written out so that
-//     consecutive threads store consecutive addresses.
-//   * pass 0 (FIRST) reads the raw user arrays and encodes on the fly
-//     (fused A1): status bit, tombstone value 0 (R6), placebo padding of a
-//     partial batch (R7), domain check -> placebo + sticky error (R5).
+// Design: onesweep-style LSD radix sort, 4 passes of 8 bits
+// over the 32-bit key variable. Every kernel is launched with programmatic
+// dependent launch (griddepcontrol) so its prologue overlaps the tail of its
+// predecessor. Measured on B200 with a %globaltimer probe
+// (scripts/sort_probe.cu), the batch sizes of the paper (2^15..2^27) are far
+// too small to hide per-tile latency with many resident tiles, so the design
+// minimises the per-tile critical path instead:
+//  * one fat tile per SM: 1024 threads x 7 records (b = 2^20 -> 147 tiles,
+//    one wave, tile = blockIdx; a tile counter is used only for multi-wave
+//    sizes);
+//  * ranks from 8 warp ballots per record (the peers with the same digit)
+//    plus per-warp digit counters: order (warp, item, lane) = input order, so
+//    the sort is stable. No __match_any_sync and no shared atomics (both are
+//    slow on this part);
+//  * records are staged in shared memory in digit order BEFORE the global
+//    offsets are known (only the tile-local digit starts are needed), which
+//    frees their registers for the look-back window;
+//  * two-level decoupled look-back: counts are published with an L2 atomic
+//    (plain stores became visible microseconds late), the prefix inside a
+//    group of 32 tiles is one window of loads, earlier groups come from group
+//    totals published by each group's last tile, and every round re-polls all
+//    pending words at once;
+//  * sort_hist_kernel builds all four digit histograms in one read (batched
+//    independent loads, ballots, per-warp counters), and its last CTA turns
+//    them into exclusive digit bases for all passes. It also zeroes this
+//    sort's look-back words and the other half of the double-buffered
+//    histogram, so no memset launch exists;
+//  * pass 0 reads the raw user arrays and encodes on the fly (fused A1):
+//    status bit, tombstone value 0 (R6), placebo padding of a partial batch
+//    (R7), domain check -> placebo + sticky error (R5).
 
 #include "common.cuh"
 
@@ -31,10 +43,24 @@ namespace gpulsm {
 
 namespace {
 
-constexpr uint32_t kFlagAgg = 1u << 30;
-constexpr uint32_t kFlagPrefix = 2u << 30;
-constexpr uint32_t kValMask = (1u << 30) - 1;
+// look-back status word: [31] ready | [30:24] epoch of the sort | [23:0]
+// count. Epoch tagging means the words never need zeroing: a word left by an
+// earlier sort carries a different epoch and reads as "not ready".
+constexpr uint32_t kValMask = (1u << 24) - 1;
+__device__ __forceinline__ uint32_t st_word(uint32_t epoch, uint32_t v) {
+  return 0x80000000u | (epoch << 24) | v;
+}
+__device__ __forceinline__ bool st_ready(uint32_t w, uint32_t epoch) {
+  return (w >> 24) == (0x80u | epoch);
+}
 constexpr int kWarps = kSortThreads / 32;
+constexpr int kGroup = 32;  // tiles per look-back group (= window)
+constexpr int kHistThreads = 1024;
+constexpr int kHistWarps = kHistThreads / 32;
+constexpr int kHistBatch = 8;  // independent loads per thread per round
+#ifndef LB_SLEEP
+#define LB_SLEEP 32
+#endif
 
 struct RawBatch {
   const uint32_t* keys;
@@ -44,176 +70,361 @@ struct RawBatch {
   uint64_t n;  // real updates; [n, b) are placebo padding
 };
 
-// A1: the key variable of update `pos`.
-__device__ __forceinline__ void encode(const RawBatch& in, uint64_t pos, uint32_t& key,
-                                       uint32_t& val, bool& bad) {
+#ifdef GPULSM_PROBE
+__device__ unsigned long long* g_probe = nullptr;  // [pass][tile][8] globaltimer stamps
+__device__ unsigned int g_repolls[8];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define PROBE(k)                                                               \
+  do {                                                                         \
+    __syncthreads();                                                           \
+    if (threadIdx.x == 0 && g_probe)                                           \
+      g_probe[((uint64_t)(shift / 8) * 4096 + tile) * 8 + (k)] = gtimer();     \
+  } while (0)
+#else
+#define PROBE(k) \
+  do {           \
+  } while (0)
+#endif
+
+// A1: key variable and value of update `pos` from already-loaded raw words.
+__device__ __forceinline__ void encode_loaded(const RawBatch& in, uint64_t pos, uint32_t k,
+                                              uint32_t v, uint32_t op, uint32_t& key,
+                                              uint32_t& val, bool& bad) {
   bad = false;
-  if (pos >= in.n) {  // R7: placebo padding
+  const bool del = in.mode == kModeDelete || (in.mode == kModeMixed && op != 0);
+  if (pos >= in.n || k > kMaxKey) {  // R7 padding / R5 out of domain
+    bad = pos < in.n;
     key = kPlacebo;
     val = 0;
-    return;
-  }
-  uint32_t k = __ldg(in.keys + pos);
-  bool del = in.mode == kModeDelete || (in.mode == kModeMixed && __ldg(in.ops + pos) != 0);
-  if (k > kMaxKey) {  // R5: out of domain -> placebo, sticky error
-    key = kPlacebo;
-    val = 0;
-    bad = true;
     return;
   }
   key = (k << 1) | (del ? 0u : 1u);
-  val = (del || in.vals == nullptr) ? 0u : __ldg(in.vals + pos);
+  val = del ? 0u : v;
 }
 
-__global__ void __launch_bounds__(kSortThreads) sort_hist_kernel(
+// Mask of lanes whose 8-bit digit equals mine (8 ballots), restricted to
+// lanes with valid == true.
+__device__ __forceinline__ uint32_t digit_peers(uint32_t d, bool valid) {
+  uint32_t m = __ballot_sync(kFull, valid);
+#pragma unroll
+  for (int bit = 0; bit < kRadixBits; ++bit) {
+    const uint32_t bb = __ballot_sync(kFull, (d >> bit) & 1u);
+    m &= ((d >> bit) & 1u) ? bb : ~bb;
+  }
+  return m;
+}
+
+struct HistSmem {
+  uint32_t wh[kHistWarps][kPasses][kRadix];  // per-warp counters (128 KB)
+  uint32_t scan[kHistWarps + 1];
+  uint32_t last;
+};
+
+__global__ void __launch_bounds__(kHistThreads, 1) sort_hist_kernel(
     RawBatch in, uint64_t b, uint32_t* __restrict__ hist, uint32_t* __restrict__ hist_next,
-    uint32_t* __restrict__ status, uint64_t status_words, uint32_t* __restrict__ tile_ctr) {
-  __shared__ uint32_t sh[kPasses][kRadix];
-  for (int i = threadIdx.x; i < kPasses * kRadix; i += kSortThreads) (&sh[0][0])[i] = 0;
-  // zero this sort's look-back words and the next sort's histogram half
-  const uint64_t gtid = (uint64_t)blockIdx.x * kSortThreads + threadIdx.x;
-  const uint64_t gsz = (uint64_t)gridDim.x * kSortThreads;
-  for (uint64_t i = gtid; i < status_words; i += gsz) status[i] = 0;
+    uint32_t* __restrict__ bases, uint32_t* __restrict__ done_ctr, uint32_t* __restrict__ status,
+    uint64_t status_words, uint32_t* __restrict__ tile_ctr) {
+  extern __shared__ __align__(16) uint8_t hist_smem[];
+  HistSmem& S = *reinterpret_cast<HistSmem*>(hist_smem);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < kHistWarps * kPasses * kRadix; i += kHistThreads) (&S.wh[0][0][0])[i] = 0;
+  pdl_wait();
+  pdl_trigger();
+#ifdef GPULSM_PROBE
+  if (tid == 0 && g_probe) g_probe[4ull * 4096 * 8 + blockIdx.x * 4 + 0] = gtimer();
+#endif
+  const uint64_t gtid = (uint64_t)blockIdx.x * kHistThreads + tid;
+  const uint64_t gsz = (uint64_t)gridDim.x * kHistThreads;
+  (void)status;
+  (void)status_words;
   for (uint64_t i = gtid; i < kPasses * kRadix; i += gsz) hist_next[i] = 0;
   if (gtid < kPasses) tile_ctr[gtid] = 0;
   __syncthreads();
-  for (uint64_t pos = gtid; pos < b; pos += gsz) {
-    uint32_t key, val;
-    bool bad;
-    encode(in, pos, key, val, bad);
+  // each warp owns a contiguous chunk; rounds of kHistBatch x 32 records
+  // whose loads are all issued before any is used
+  const uint64_t nwarps = gsz / 32;
+  const uint64_t gw = gtid / 32;
+  const uint64_t per = ((b + nwarps - 1) / nwarps + 31) / 32 * 32;
+  const uint64_t w0 = gw * per, w1 = min(b, w0 + per);
+  for (uint64_t base = w0; base < w1; base += 32 * kHistBatch) {
+    uint32_t k[kHistBatch], op[kHistBatch];
 #pragma unroll
-    for (int p = 0; p < kPasses; ++p) atomicAdd(&sh[p][(key >> (p * kRadixBits)) & (kRadix - 1)], 1u);
+    for (int j = 0; j < kHistBatch; ++j) {
+      const uint64_t pos = base + j * 32 + lane;
+      const bool ld = pos < w1 && pos < in.n;
+      k[j] = ld ? __ldg(in.keys + pos) : 0u;
+      op[j] = (ld && in.mode == kModeMixed) ? (uint32_t)__ldg(in.ops + pos) : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < kHistBatch; ++j) {
+      const uint64_t pos = base + j * 32 + lane;
+      const bool valid = pos < w1;
+      if (__ballot_sync(kFull, valid) == 0) break;
+      uint32_t key, val;
+      bool bad;
+      encode_loaded(in, pos, k[j], 0u, op[j], key, val, bad);
+      uint32_t peers[kPasses];
+#pragma unroll
+      for (int p = 0; p < kPasses; ++p)
+        peers[p] = digit_peers((key >> (p * kRadixBits)) & (kRadix - 1), valid);
+#pragma unroll
+      for (int p = 0; p < kPasses; ++p) {
+        const uint32_t d = (key >> (p * kRadixBits)) & (kRadix - 1);
+        if (valid && lane == __ffs(peers[p]) - 1) S.wh[warp][p][d] += __popc(peers[p]);
+      }
+      __syncwarp();
+    }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < kPasses * kRadix; i += kSortThreads) {
-    uint32_t c = (&sh[0][0])[i];
+#ifdef GPULSM_PROBE
+  if (tid == 0 && g_probe) g_probe[4ull * 4096 * 8 + blockIdx.x * 4 + 1] = gtimer();
+#endif
+  for (int i = tid; i < kPasses * kRadix; i += kHistThreads) {
+    uint32_t c = 0;
+#pragma unroll 8
+    for (int w = 0; w < kHistWarps; ++w) c += (&S.wh[w][0][0])[i];
     if (c) atomicAdd(hist + i, c);
   }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) S.last = atomicAdd(done_ctr, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (S.last) {  // last CTA: exclusive digit bases for all passes
+    __threadfence();
+    const uint32_t c = ld_cg(hist + tid);  // tid = pass * 256 + digit
+    // exclusive scan within each 256-digit segment: warp scans + segment sums
+    uint32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) S.scan[warp] = x;
+    __syncthreads();
+    uint32_t before = 0;  // warps of the same segment before mine
+    const int seg_w0 = (warp / (kRadix / 32)) * (kRadix / 32);
+    for (int w = seg_w0; w < warp; ++w) before += S.scan[w];
+    bases[tid] = before + x - c;
+    if (tid == 0) *done_ctr = 0;
+  }
+#ifdef GPULSM_PROBE
+  if (tid == 0 && g_probe) g_probe[4ull * 4096 * 8 + blockIdx.x * 4 + 2] = gtimer();
+#endif
 }
+
+struct PassSmem {
+  uint32_t keys[kSortTile];
+  uint32_t vals[kSortTile];
+  uint32_t whist[kWarps][kRadix];  // per-warp digit counters -> warp offsets
+  uint32_t goff[kRadix];           // global offset - tile start, per digit
+  uint32_t tstart[kRadix];         // tile-local start of each digit
+  uint32_t scan[kWarps + 1];
+  uint32_t tile;
+};
 
 template <bool FIRST>
-__global__ void __launch_bounds__(kSortThreads) onesweep_pass_kernel(
+__global__ void __launch_bounds__(kSortThreads, 1) onesweep_pass_kernel(
     RawBatch in, const uint32_t* __restrict__ in_keys, const uint32_t* __restrict__ in_vals,
     uint32_t* __restrict__ out_keys, uint32_t* __restrict__ out_vals, uint64_t b,
-    const uint32_t* __restrict__ hist_pass, uint32_t* __restrict__ status,
-    uint32_t* __restrict__ tile_ctr, int shift, uint32_t* __restrict__ err) {
-  __shared__ uint32_t s_keys[kSortTile];
-  __shared__ uint32_t s_vals[kSortTile];
-  __shared__ uint32_t s_whist[kWarps][kRadix];
-  __shared__ uint32_t s_goff[kRadix];   // global offset - tile start, per digit
-  __shared__ uint32_t s_tstart[kRadix]; // tile-local start of each digit
-  __shared__ uint32_t s_scan[kWarps + 1];
-  __shared__ uint32_t s_tile;
-
+    const uint32_t* __restrict__ dbase, uint32_t* __restrict__ tile_st,
+    uint32_t* __restrict__ group_st, uint32_t* __restrict__ tile_ctr, int use_ctr, int shift,
+    uint32_t* __restrict__ err, uint32_t epoch) {
+  // use_ctr == 0 <=> all tiles are co-resident (one wave): the digit bases
+  // then come from the totals of ALL groups (no histogram kernel)
+  extern __shared__ __align__(16) uint8_t pass_smem[];
+  PassSmem& S = *reinterpret_cast<PassSmem*>(pass_smem);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < kWarps * kRadix; i += kSortThreads) (&s_whist[0][0])[i] = 0;
-  if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
-  __syncthreads();
-  const uint32_t tile = s_tile;
+#ifdef GPULSM_PROBE
+  const unsigned long long t_entry = gtimer();
+#endif
+  for (int i = tid; i < kWarps * kRadix; i += kSortThreads) (&S.whist[0][0])[i] = 0;
+  pdl_wait();
+  pdl_trigger();
+  if (use_ctr) {
+    if (tid == 0) S.tile = atomicAdd(tile_ctr, 1u);
+    __syncthreads();
+  }
+  const uint32_t tile = use_ctr ? S.tile : blockIdx.x;
+#ifdef GPULSM_PROBE
+  if (threadIdx.x == 0 && g_probe) g_probe[((uint64_t)(shift / 8) * 4096 + tile) * 8 + 0] = t_entry;
+#endif
+  PROBE(1);
   const uint64_t tile_base = (uint64_t)tile * kSortTile;
-  const uint32_t tile_n = (uint32_t)((b - tile_base) < (uint64_t)kSortTile ? (b - tile_base) : (uint64_t)kSortTile);
+  const uint32_t tile_n =
+      (uint32_t)((b - tile_base) < (uint64_t)kSortTile ? (b - tile_base) : (uint64_t)kSortTile);
+  const uint32_t wbase = warp * (32 * kSortItems);  // warp-striped segment
 
-  // ---- load (warp-striped: item i of warp w at w*512 + i*32 + lane) ----
+  // ---- load: item i of warp w at w*224 + i*32 + lane ----
   uint32_t k[kSortItems], v[kSortItems];
-  bool any_bad = false;
+  if (FIRST) {
+    uint32_t op[kSortItems];
 #pragma unroll
-  for (int i = 0; i < kSortItems; ++i) {
-    const uint32_t off = warp * (32 * kSortItems) + i * 32 + lane;
-    if (off < tile_n) {
-      if (FIRST) {
-        bool bad;
-        encode(in, tile_base + off, k[i], v[i], bad);
-        any_bad |= bad;
-      } else {
-        k[i] = __ldg(in_keys + tile_base + off);
-        v[i] = __ldg(in_vals + tile_base + off);
-      }
-    } else {
-      k[i] = 0;
-      v[i] = 0;
+    for (int i = 0; i < kSortItems; ++i) {  // independent loads first
+      const uint64_t pos = tile_base + wbase + i * 32 + lane;
+      const bool in_batch = pos < in.n;
+      k[i] = in_batch ? __ldg(in.keys + pos) : 0u;
+      v[i] = (in_batch && in.vals) ? __ldg(in.vals + pos) : 0u;
+      op[i] = (in_batch && in.mode == kModeMixed) ? (uint32_t)__ldg(in.ops + pos) : 0u;
+    }
+    bool any_bad = false;
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+      const uint64_t pos = tile_base + wbase + i * 32 + lane;
+      bool bad;
+      encode_loaded(in, pos, k[i], v[i], op[i], k[i], v[i], bad);
+      any_bad |= bad;
+    }
+    if (any_bad) atomicOr(err, 1u);
+  } else {
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+      const uint32_t off = wbase + i * 32 + lane;
+      const bool ok = off < tile_n;
+      k[i] = ok ? __ldg(in_keys + tile_base + off) : 0u;
+      v[i] = ok ? __ldg(in_vals + tile_base + off) : 0u;
     }
   }
-  if (FIRST && any_bad) atomicOr(err, 1u);
+  PROBE(2);
 
-  // ---- rank within the tile: match_any + per-warp digit counters ----
+  // ---- rank within the tile: ballot peers + per-warp digit counters ----
   uint32_t rk[kSortItems];
   const uint32_t lt = lanemask_lt();
+  {
+    uint32_t peers[kSortItems];
 #pragma unroll
-  for (int i = 0; i < kSortItems; ++i) {
-    const uint32_t off = warp * (32 * kSortItems) + i * 32 + lane;
-    const uint32_t d = off < tile_n ? (k[i] >> shift) & (kRadix - 1) : kRadix;
-    const uint32_t peers = __match_any_sync(kFull, d);
-    const int leader = __ffs(peers) - 1;
-    uint32_t old = 0;
-    if (lane == leader && d < kRadix) {
-      old = s_whist[warp][d];
-      s_whist[warp][d] = old + __popc(peers);
+    for (int i = 0; i < kSortItems; ++i)  // independent: all ballots first
+      peers[i] = digit_peers((k[i] >> shift) & (kRadix - 1), wbase + i * 32 + lane < tile_n);
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+      const bool valid = wbase + i * 32 + lane < tile_n;
+      const uint32_t d = (k[i] >> shift) & (kRadix - 1);
+      const int leader = __ffs(peers[i]) - 1;
+      uint32_t old = 0;
+      if (valid && lane == leader) {
+        old = S.whist[warp][d];
+        S.whist[warp][d] = old + __popc(peers[i]);
+      }
+      old = __shfl_sync(kFull, old, leader < 0 ? 0 : leader);
+      rk[i] = old + __popc(peers[i] & lt);
+      __syncwarp();
     }
-    old = __shfl_sync(kFull, old, leader);
-    rk[i] = old + __popc(peers & lt);
-    __syncwarp();
   }
   __syncthreads();
+  PROBE(3);
 
   // ---- per digit (thread = digit): warp exclusive offsets, tile count ----
-  const uint32_t dgt = tid;  // kSortThreads == kRadix
-  uint32_t run = 0;
-#pragma unroll
-  for (int w = 0; w < kWarps; ++w) {
-    uint32_t c = s_whist[w][dgt];
-    s_whist[w][dgt] = run;
-    run += c;
-  }
-  const uint32_t tile_cnt = run;
-
-  // decoupled look-back over earlier tiles for this digit
-  uint32_t* my = status + (uint64_t)tile * kRadix + dgt;
-  uint32_t excl = 0;
-  if (tile == 0) {
-    st_volatile(my, kFlagPrefix | tile_cnt);
-  } else {
-    st_volatile(my, kFlagAgg | tile_cnt);
-    int64_t j = (int64_t)tile - 1;
-    while (true) {
-      uint32_t sw = ld_volatile(status + (uint64_t)j * kRadix + dgt);
-      uint32_t flag = sw & ~kValMask;
-      if (flag == 0) continue;
-      excl += sw & kValMask;
-      if (flag == kFlagPrefix) break;
-      --j;
+  uint32_t tile_cnt = 0;
+  if (tid < kRadix) {
+#pragma unroll 8
+    for (int w = 0; w < kWarps; ++w) {
+      const uint32_t c = S.whist[w][tid];
+      S.whist[w][tid] = tile_cnt;
+      tile_cnt += c;
     }
-    st_volatile(my, kFlagPrefix | (excl + tile_cnt));
+    // publish through an L2 atomic: performed at L2 at once
+    atomicExch(tile_st + (uint64_t)tile * kRadix + tid, st_word(epoch, tile_cnt));
   }
   uint32_t tot;
-  const uint32_t dbase = block_exclusive_scan<kSortThreads, uint32_t>(hist_pass[dgt], s_scan, &tot);
-  const uint32_t tstart = block_exclusive_scan<kSortThreads, uint32_t>(tile_cnt, s_scan, &tot);
-  s_tstart[dgt] = tstart;
-  s_goff[dgt] = dbase + excl - tstart;
+  const uint32_t tstart = block_exclusive_scan<kSortThreads, uint32_t>(tile_cnt, S.scan, &tot);
+  if (tid < kRadix) S.tstart[tid] = tstart;
   __syncthreads();
 
-  // ---- stage in smem in digit order ----
+  // ---- stage in smem in digit order (needs only tile-local offsets) ----
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
-    const uint32_t off = warp * (32 * kSortItems) + i * 32 + lane;
+    const uint32_t off = wbase + i * 32 + lane;
     if (off < tile_n) {
       const uint32_t d = (k[i] >> shift) & (kRadix - 1);
-      const uint32_t p = s_tstart[d] + s_whist[warp][d] + rk[i];
-      s_keys[p] = k[i];
-      s_vals[p] = v[i];
+      const uint32_t p = S.tstart[d] + S.whist[warp][d] + rk[i];
+      S.keys[p] = k[i];
+      S.vals[p] = v[i];
     }
   }
+
+  // ---- two-level decoupled look-back (threads 0..255 = digits) ----
+  uint32_t gp = 0, wp = 0, total = 0;
+  const uint32_t ntiles = (uint32_t)((b + kSortTile - 1) / kSortTile);
+  if (tid < kRadix) {
+    const uint32_t dgt = tid;
+    const uint32_t g = tile / kGroup, g0 = g * kGroup;
+    // prefix inside the group: one window; every round re-polls ALL
+    // pending words, so the wait is one round trip after the last publish
+    {
+      const uint32_t npred = tile - g0;
+      uint32_t pending = npred >= 32 ? 0xFFFFFFFFu : ((1u << npred) - 1u);
+      while (pending) {
+        uint32_t sw[kGroup];
+#pragma unroll
+        for (int w = 0; w < kGroup; ++w)
+          sw[w] = (pending >> w) & 1u ? ld_cg(tile_st + (uint64_t)(g0 + w) * kRadix + dgt) : 0u;
+#pragma unroll
+        for (int w = 0; w < kGroup; ++w) {
+          if (((pending >> w) & 1u) && st_ready(sw[w], epoch)) {
+            wp += sw[w] & kValMask;
+            pending &= ~(1u << w);
+          }
+        }
+        if (pending && LB_SLEEP) __nanosleep(LB_SLEEP);
+      }
+    }
+    // the last tile of each group (incl. a partial last group) publishes
+    // the group total
+    if (tile == g0 + kGroup - 1 || tile == ntiles - 1)
+      atomicExch(group_st + (uint64_t)g * kRadix + dgt, st_word(epoch, wp + tile_cnt));
+    // earlier groups (multi-wave) or all groups (one wave: also the totals)
+    const uint32_t ng = use_ctr ? g : (ntiles + kGroup - 1) / kGroup;
+    for (uint32_t G0 = 0; G0 < ng; G0 += kGroup) {
+      const uint32_t cnt = min(ng - G0, (uint32_t)kGroup);
+      uint32_t pending = cnt >= 32 ? 0xFFFFFFFFu : ((1u << cnt) - 1u);
+      while (pending) {
+        uint32_t sw[kGroup];
+#pragma unroll
+        for (int w = 0; w < kGroup; ++w)
+          sw[w] = (pending >> w) & 1u ? ld_cg(group_st + (uint64_t)(G0 + w) * kRadix + dgt) : 0u;
+#pragma unroll
+        for (int w = 0; w < kGroup; ++w) {
+          if (((pending >> w) & 1u) && st_ready(sw[w], epoch)) {
+            const uint32_t x = sw[w] & kValMask;
+            total += x;
+            if (G0 + w < g) gp += x;
+            pending &= ~(1u << w);
+          }
+        }
+        if (pending && LB_SLEEP) __nanosleep(LB_SLEEP);
+      }
+    }
+  }
+  uint32_t base;
+  if (use_ctr) {
+    base = tid < kRadix ? __ldg(dbase + tid) : 0u;
+  } else {  // exclusive scan of the global digit totals
+    uint32_t t2;
+    base = block_exclusive_scan<kSortThreads, uint32_t>(total, S.scan, &t2);
+  }
+  if (tid < kRadix) S.goff[tid] = base + gp + wp - tstart;
   __syncthreads();
+  PROBE(5);
 
   // ---- write out: consecutive threads -> consecutive addresses per digit ----
-#pragma unroll 4
-  for (uint32_t idx = tid; idx < tile_n; idx += kSortThreads) {
-    const uint32_t key = s_keys[idx];
-    const uint32_t d = (key >> shift) & (kRadix - 1);
-    const uint32_t pos = s_goff[d] + idx;
-    out_keys[pos] = key;
-    out_vals[pos] = s_vals[idx];
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const uint32_t idx = i * kSortThreads + tid;
+    if (idx < tile_n) {
+      const uint32_t key = S.keys[idx];
+      const uint32_t pos = S.goff[(key >> shift) & (kRadix - 1)] + idx;
+      out_keys[pos] = key;
+      out_vals[pos] = S.vals[idx];
+    }
   }
+  PROBE(7);
 }
+
+int g_sms = 0;
+bool g_attr = false;
 
 }  // namespace
 
@@ -221,40 +432,66 @@ cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals
                               const uint8_t* ops, int mode, uint64_t n, uint64_t b,
                               SortScratch& S, uint32_t* out_keys, uint32_t* out_vals,
                               cudaStream_t s, const LaunchHooks& hk) {
+  if (!g_attr) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaFuncSetAttribute(sort_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(HistSmem));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(onesweep_pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(PassSmem));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(onesweep_pass_kernel<false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PassSmem));
+    if (e != cudaSuccess) return e;
+    g_attr = true;
+  }
   RawBatch in{raw_keys, raw_vals, ops, mode, n};
+  const uint32_t epoch = (uint32_t)(S.epoch++ % 127u) + 1u;  // 1..127
   const uint64_t tiles = sort_tiles(b);
+  const uint64_t groups = sort_groups(b);
   uint32_t* hist = S.hist + (S.parity ? kPasses * kRadix : 0);
   uint32_t* hist_next = S.hist + (S.parity ? 0 : kPasses * kRadix);
   S.parity ^= 1;
-  const uint64_t status_words = (uint64_t)kPasses * tiles * kRadix;
+  // status layout: [pass][tiles][256] tile words, then [pass][groups][256]
+  uint32_t* tile_st = S.status;
+  uint32_t* group_st = S.status + (uint64_t)kPasses * tiles * kRadix;
+  const uint64_t status_words = (uint64_t)kPasses * (tiles + groups) * kRadix;
+  // one wave (1 CTA per SM) -> tile = blockIdx, no counter round trip
+  const int use_ctr = tiles > (uint64_t)g_sms ? 1 : 0;
 
-  // histogram grid: enough CTAs to read the batch at full bandwidth
-  uint64_t hgrid = (b + kSortTile - 1) / kSortTile;
-  if (hgrid < 1) hgrid = 1;
-  if (hgrid > 148 * 4) hgrid = 148 * 4;
-  hk.begin(hk.ctx, LSM_K_SORT_HIST, s);
-  sort_hist_kernel<<<(unsigned)hgrid, kSortThreads, 0, s>>>(in, b, hist, hist_next, S.status,
-                                                             status_words, S.tile_ctr);
-  hk.end(hk.ctx, LSM_K_SORT_HIST, (double)b * 9.0, s, 1);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  cudaError_t e = cudaSuccess;
+  if (use_ctr) {  // multi-wave: digit bases from an upfront histogram
+    uint64_t hgrid = (b + 4 * kHistThreads - 1) / (4 * kHistThreads);
+    if (hgrid < 1) hgrid = 1;
+    if (hgrid > (uint64_t)g_sms) hgrid = g_sms;
+    hk.begin(hk.ctx, LSM_K_SORT_HIST, s);
+    e = launch_pdl(sort_hist_kernel, (unsigned)hgrid, kHistThreads, sizeof(HistSmem), s, in, b,
+                   hist, hist_next, S.bases, S.done_ctr, S.status, status_words, S.tile_ctr);
+    // bytes: keys (4 B) + op (1 B) per update
+    hk.end(hk.ctx, LSM_K_SORT_HIST, (double)b * 5.0, s, 1);
+    if (e != cudaSuccess) return e;
+  }
 
   const uint32_t* ik = nullptr;
   const uint32_t* iv = nullptr;
   for (int p = 0; p < kPasses; ++p) {
     uint32_t* ok = (p == kPasses - 1) ? out_keys : S.tmp_keys[p & 1];
     uint32_t* ov = (p == kPasses - 1) ? out_vals : S.tmp_vals[p & 1];
-    uint32_t* st = S.status + (uint64_t)p * tiles * kRadix;
+    uint32_t* ts = tile_st + (uint64_t)p * tiles * kRadix;
+    uint32_t* gs = group_st + (uint64_t)p * groups * kRadix;
     hk.begin(hk.ctx, LSM_K_SORT_PASS, s);
     if (p == 0)
-      onesweep_pass_kernel<true><<<(unsigned)tiles, kSortThreads, 0, s>>>(
-          in, nullptr, nullptr, ok, ov, b, hist, st, S.tile_ctr + p, 0, S.err);
+      e = launch_pdl(onesweep_pass_kernel<true>, (unsigned)tiles, kSortThreads, sizeof(PassSmem), s,
+                     in, (const uint32_t*)nullptr, (const uint32_t*)nullptr, ok, ov, b,
+                     (const uint32_t*)S.bases, ts, gs, S.tile_ctr + p, use_ctr, 0, S.err, epoch);
     else
-      onesweep_pass_kernel<false><<<(unsigned)tiles, kSortThreads, 0, s>>>(
-          in, ik, iv, ok, ov, b, hist + p * kRadix, st, S.tile_ctr + p, p * kRadixBits, S.err);
+      e = launch_pdl(onesweep_pass_kernel<false>, (unsigned)tiles, kSortThreads, sizeof(PassSmem),
+                     s, in, ik, iv, ok, ov, b, (const uint32_t*)(S.bases + p * kRadix), ts, gs,
+                     S.tile_ctr + p, use_ctr, p * kRadixBits, S.err, epoch);
     // bytes: pass 0 reads raw (k,v,op = 9 B) writes 8 B; others 16 B
     hk.end(hk.ctx, LSM_K_SORT_PASS, (double)b * (p == 0 ? 17.0 : 16.0), s, 1);
-    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     ik = ok;
     iv = ov;

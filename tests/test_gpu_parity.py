@@ -145,9 +145,21 @@ def test_ragged_batch_sizes(b):
 
 @pytest.mark.parametrize("b", [1 << 16, (1 << 17) + 123])
 def test_multi_tile_sort_and_merge(b):
-    # several sort tiles (4096) with a ragged tail; merges of 2b and 4b over
+    # several sort tiles (7168) with a ragged tail; merges of 2b and 4b over
     # many merge tiles; uniform 31-bit keys
     _run_schedule(b, 4, 4242, frac4=1, nlook=20_000, nrange=2000)
+
+
+def test_multi_wave_sort():
+    # b > 148 sort tiles: histogram kernel + tile counter + group look-back
+    # over more than one window of groups
+    _run_schedule((1 << 21) + 4097, 3, 99, frac4=1, nlook=20_000, nrange=1000)
+
+
+def test_one_wave_boundary_sort():
+    # exactly 148 tiles (largest one-wave batch) and one record more
+    for b in (148 * 7168, 148 * 7168 + 1):
+        _run_schedule(b, 2, 5 + b % 7, frac4=1, nlook=5000, nrange=500)
 
 
 def test_partial_batches():
@@ -272,9 +284,16 @@ def test_launch_counter_counts_kernels():
     k, v, d = synth.updates(1, 0, 4096)
     n0 = g.launch_count
     g.update(to_device(k), to_device(v), to_device(d))
-    assert g.launch_count - n0 == 5  # histogram + 4 onesweep passes
+    # one-wave batch (b <= 148 tiles): 4 onesweep passes, no histogram kernel
+    assert g.launch_count - n0 == 4
     g.update(to_device(k), to_device(v), to_device(d))
-    assert g.launch_count - n0 == 11  # + 5 + one merge
+    assert g.launch_count - n0 == 9  # + 4 + one merge
+    # multi-wave batch: histogram kernel + 4 passes
+    big = pkg.GpuLSM(2_000_000)
+    kb, vb, db = synth.updates(2, 0, 2_000_000)
+    n1 = big.launch_count
+    big.update(to_device(kb), to_device(vb), to_device(db))
+    assert big.launch_count - n1 == 5
 
 
 @pytest.mark.slow
