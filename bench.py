@@ -178,10 +178,12 @@ def run_native(args):
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local_rank)
-    dist = None
-    if world > 1:
+    if world > 1 or args.sharded:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29511")
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", local_rank))
         from paper_1707_05354_b200.sharded import run_sharded_bench
         return run_sharded_bench(args, dist, rank, world, local_rank)
 
@@ -359,6 +361,8 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the key-range sharded router even at N=1")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

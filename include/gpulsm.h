@@ -165,6 +165,43 @@ lsm_status lsm_range(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2, uint6
 lsm_status lsm_cleanup(lsm_t* h, void* stream);
 
 /* ------------------------------------------------------------------------ */
+/* Key-range sharding (multi-GPU router support)               */
+/* Every dictionary operation is key-local, so a partition */
+/* of the key domain gives per-shard semantics identical to the global ones. */
+/* Shard s of P owns the original keys k with owner(k) = min(P-1,            */
+/* floor(k*P / 2^31)); keys above LSM_MAX_KEY belong to shard P-1.            */
+/* ------------------------------------------------------------------------ */
+
+/* Stable partition of n records by destination shard. mode 0: owner(k) as
+ * above (range partition); mode 1: the top log2(P) bits of k*0x9E3779B1
+ * (P a power of two; used to split an oversized local batch without
+ * separating equal keys). Outputs are grouped by destination, input order
+ * kept inside each group. d_vals / d_ops / their outputs and d_perm_out
+ * (source index of each output slot, u32) may be NULL. d_counts_out[P] (u32,
+ * device) receives the group sizes. 1 <= P <= 64. Uses h for scratch.       */
+lsm_status lsm_shard_bucket(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals,
+                            const uint8_t* d_ops, uint64_t n, uint32_t nshards, int mode,
+                            uint32_t* d_keys_out, uint32_t* d_vals_out, uint8_t* d_ops_out,
+                            uint32_t* d_perm_out, uint32_t* d_counts_out, void* stream);
+
+/* out[perm[i]] = in[i] for i < n: routes lookup results back to the query
+ * order a lsm_shard_bucket permutation came from. d_found_* may be NULL.   */
+lsm_status lsm_shard_scatter(lsm_t* h, const uint32_t* d_perm, const uint32_t* d_vals_in,
+                             const uint8_t* d_found_in, uint64_t n, uint32_t* d_vals_out,
+                             uint8_t* d_found_out, void* stream);
+
+/* Intersect each [k1, k2] with the key interval [lo, hi] (a shard's range);
+ * an empty result is written as (1, 0), which every query treats as empty
+ * (R9).                                                                    */
+lsm_status lsm_shard_clip(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2, uint64_t n,
+                          uint32_t lo, uint32_t hi, uint32_t* d_k1_out, uint32_t* d_k2_out,
+                          void* stream);
+
+/* out[i] = sum_{p < parts} in[p * n + i] (u32): totals of per-shard counts. */
+lsm_status lsm_shard_sum(lsm_t* h, const uint32_t* d_in, uint32_t parts, uint64_t n,
+                         uint32_t* d_out, void* stream);
+
+/* ------------------------------------------------------------------------ */
 /* Introspection                                                             */
 /* ------------------------------------------------------------------------ */
 

@@ -55,6 +55,11 @@ SIGNATURES = {
     "lsm_status_string": ([_st], ctypes.c_char_p),
     "lsm_profile_enable": ([_vp, ctypes.c_int], _st),
     "lsm_profile_read": ([_vp, _vp], _st),
+    "lsm_shard_bucket": ([_vp, _vp, _vp, _vp, _u64, ctypes.c_uint32, ctypes.c_int, _vp, _vp, _vp,
+                          _vp, _vp, _vp], _st),
+    "lsm_shard_scatter": ([_vp, _vp, _vp, _vp, _u64, _vp, _vp, _vp], _st),
+    "lsm_shard_clip": ([_vp, _vp, _vp, _u64, ctypes.c_uint32, ctypes.c_uint32, _vp, _vp, _vp], _st),
+    "lsm_shard_sum": ([_vp, _vp, ctypes.c_uint32, _u64, _vp, _vp], _st),
 }
 
 
@@ -294,6 +299,44 @@ class GpuLSM:
     def reserve(self, max_batches: int, stream=None):
         _check(self._lib.lsm_reserve(self.h, int(max_batches), _stream_ptr(stream)),
                "lsm_reserve")
+
+    # ---- key-range sharding kernels (used by sharded.ShardedLSM) ----
+    def shard_bucket(self, keys, nshards, vals=None, ops=None, mode=0, want_perm=False,
+                     stream=None):
+        """Stable partition by owner shard -> (keys, vals, ops, perm, counts[P])."""
+        torch = _torch()
+        n = keys.numel()
+        dev = keys.device
+        ko = torch.empty(n, dtype=torch.int32, device=dev)
+        vo = torch.empty(n, dtype=torch.int32, device=dev) if vals is not None else None
+        oo = torch.empty(n, dtype=torch.uint8, device=dev) if ops is not None else None
+        po = torch.empty(n, dtype=torch.int32, device=dev) if want_perm else None
+        cnt = torch.empty(nshards, dtype=torch.int32, device=dev)
+        _check(self._lib.lsm_shard_bucket(self.h, _dev(keys, 4, "keys"), _dev(vals, 4, "vals"),
+                                          _dev(ops, 1, "ops"), n, nshards, mode, _dev(ko), _dev(vo),
+                                          _dev(oo, 1), _dev(po), _dev(cnt), _stream_ptr(stream)),
+               "lsm_shard_bucket")
+        return ko, vo, oo, po, cnt
+
+    def shard_scatter(self, perm, vals_in, found_in, vals_out, found_out, stream=None):
+        _check(self._lib.lsm_shard_scatter(self.h, _dev(perm), _dev(vals_in), _dev(found_in, 1),
+                                           perm.numel(), _dev(vals_out), _dev(found_out, 1),
+                                           _stream_ptr(stream)), "lsm_shard_scatter")
+
+    def shard_clip(self, k1, k2, lo, hi, stream=None):
+        torch = _torch()
+        o1 = torch.empty_like(k1)
+        o2 = torch.empty_like(k2)
+        _check(self._lib.lsm_shard_clip(self.h, _dev(k1), _dev(k2), k1.numel(), int(lo), int(hi),
+                                        _dev(o1), _dev(o2), _stream_ptr(stream)), "lsm_shard_clip")
+        return o1, o2
+
+    def shard_sum(self, parts_tensor, parts, n, stream=None):
+        torch = _torch()
+        out = torch.empty(n, dtype=torch.int32, device=parts_tensor.device)
+        _check(self._lib.lsm_shard_sum(self.h, _dev(parts_tensor), int(parts), int(n), _dev(out),
+                                       _stream_ptr(stream)), "lsm_shard_sum")
+        return out
 
     @property
     def launch_count(self) -> int:

@@ -235,6 +235,22 @@ cudaError_t launch_cleanup_count(const uint32_t* mk, uint64_t n, uint32_t* tile_
 cudaError_t launch_cleanup_write(const uint32_t* mk, const uint32_t* mv, uint64_t n,
                                  const uint64_t* tile_offsets, uint32_t* ck, uint32_t* cv,
                                  cudaStream_t s, const LaunchHooks& hk);
+// Sharding support (shard.cu)
+uint64_t bucket_scratch_words(uint64_t n, uint32_t P);
+cudaError_t launch_bucket(const uint32_t* keys, const uint32_t* vals, const uint8_t* ops,
+                          uint64_t n, uint32_t P, int mode, uint32_t* keys_out,
+                          uint32_t* vals_out, uint8_t* ops_out, uint32_t* perm_out,
+                          uint32_t* counts_out, uint32_t* scratch, cudaStream_t s,
+                          const LaunchHooks& hk);
+cudaError_t launch_scatter_back(const uint32_t* perm, const uint32_t* vin, const uint8_t* fin,
+                                uint64_t n, uint32_t* vout, uint8_t* fout, cudaStream_t s,
+                                const LaunchHooks& hk);
+cudaError_t launch_clip(const uint32_t* k1, const uint32_t* k2, uint64_t n, uint32_t lo,
+                        uint32_t hi, uint32_t* o1, uint32_t* o2, cudaStream_t s,
+                        const LaunchHooks& hk);
+cudaError_t launch_sum_parts(const uint32_t* in, uint32_t parts, uint64_t n, uint32_t* out,
+                             cudaStream_t s, const LaunchHooks& hk);
+
 cudaError_t launch_fill_placebo(uint32_t* ck, uint32_t* cv, uint64_t from, uint64_t to,
                                 cudaStream_t s, const LaunchHooks& hk);
 

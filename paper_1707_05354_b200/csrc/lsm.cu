@@ -560,6 +560,55 @@ lsm_status lsm_cleanup(lsm_t* h, void* stream) {
   return LSM_OK;
 }
 
+// ---------------- key-range sharding support ----------------
+lsm_status lsm_shard_bucket(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals,
+                            const uint8_t* d_ops, uint64_t n, uint32_t nshards, int mode,
+                            uint32_t* d_keys_out, uint32_t* d_vals_out, uint8_t* d_ops_out,
+                            uint32_t* d_perm_out, uint32_t* d_counts_out, void* stream) {
+  if (!h || nshards == 0 || nshards > 64 || !d_counts_out) return LSM_ERR_INVALID_ARG;
+  if (mode == 1 && (nshards & (nshards - 1))) return LSM_ERR_INVALID_ARG;
+  if (n > 0 && (!d_keys || !d_keys_out)) return LSM_ERR_INVALID_ARG;
+  if ((d_vals == nullptr) != (d_vals_out == nullptr) || (d_ops == nullptr) != (d_ops_out == nullptr))
+    return LSM_ERR_INVALID_ARG;
+  if (n > 0xFFFFFFFFull) return LSM_ERR_INVALID_ARG;
+  cudaStream_t s = S(stream);
+  CK(ensure_qbuf(h, bucket_scratch_words(n, nshards) * 4, s));
+  CK(launch_bucket(d_keys, d_vals, d_ops, n, nshards, mode, d_keys_out, d_vals_out, d_ops_out,
+                   d_perm_out, d_counts_out, static_cast<uint32_t*>(h->qbuf), s, hooks(h)));
+  return LSM_OK;
+}
+
+lsm_status lsm_shard_scatter(lsm_t* h, const uint32_t* d_perm, const uint32_t* d_vals_in,
+                             const uint8_t* d_found_in, uint64_t n, uint32_t* d_vals_out,
+                             uint8_t* d_found_out, void* stream) {
+  if (!h) return LSM_ERR_INVALID_ARG;
+  if (n == 0) return LSM_OK;
+  if (!d_perm || !d_vals_in || !d_vals_out || (d_found_in == nullptr) != (d_found_out == nullptr))
+    return LSM_ERR_INVALID_ARG;
+  CK(launch_scatter_back(d_perm, d_vals_in, d_found_in, n, d_vals_out, d_found_out, S(stream),
+                         hooks(h)));
+  return LSM_OK;
+}
+
+lsm_status lsm_shard_clip(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2, uint64_t n,
+                          uint32_t lo, uint32_t hi, uint32_t* d_k1_out, uint32_t* d_k2_out,
+                          void* stream) {
+  if (!h) return LSM_ERR_INVALID_ARG;
+  if (n == 0) return LSM_OK;
+  if (!d_k1 || !d_k2 || !d_k1_out || !d_k2_out) return LSM_ERR_INVALID_ARG;
+  CK(launch_clip(d_k1, d_k2, n, lo, hi, d_k1_out, d_k2_out, S(stream), hooks(h)));
+  return LSM_OK;
+}
+
+lsm_status lsm_shard_sum(lsm_t* h, const uint32_t* d_in, uint32_t parts, uint64_t n,
+                         uint32_t* d_out, void* stream) {
+  if (!h || parts == 0) return LSM_ERR_INVALID_ARG;
+  if (n == 0) return LSM_OK;
+  if (!d_in || !d_out) return LSM_ERR_INVALID_ARG;
+  CK(launch_sum_parts(d_in, parts, n, d_out, S(stream), hooks(h)));
+  return LSM_OK;
+}
+
 lsm_status lsm_batch_size(const lsm_t* h, uint64_t* b_out) {
   if (!h || !b_out) return LSM_ERR_INVALID_ARG;
   *b_out = h->b;

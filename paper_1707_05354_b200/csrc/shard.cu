@@ -158,7 +158,27 @@ __global__ void clip_kernel(const uint32_t* __restrict__ k1, const uint32_t* __r
   }
 }
 
+__global__ void sum_parts_kernel(const uint32_t* __restrict__ in, uint32_t parts, uint64_t n,
+                                 uint32_t* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t s = 0;
+    for (uint32_t p = 0; p < parts; ++p) s += __ldg(in + (uint64_t)p * n + i);
+    out[i] = s;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_sum_parts(const uint32_t* in, uint32_t parts, uint64_t n, uint32_t* out,
+                             cudaStream_t s, const LaunchHooks& hk) {
+  if (n == 0) return cudaSuccess;
+  unsigned grid = (unsigned)((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
+  hk.begin(hk.ctx, LSM_K_OTHER, s);
+  sum_parts_kernel<<<grid, 256, 0, s>>>(in, parts, n, out);
+  hk.end(hk.ctx, LSM_K_OTHER, (double)n * 4.0 * (parts + 1), s, 1);
+  return cudaGetLastError();
+}
 
 uint64_t bucket_scratch_words(uint64_t n, uint32_t P) {
   return (uint64_t)P * ((n + kBTile - 1) / kBTile) + 1;

@@ -1,0 +1,277 @@
+"""Key-range sharded GPU LSM across ranks (one LSM per GPU) -- DESIGN.md §7.
+
+The paper is single-GPU. Every dictionary operation is
+key-local: a key's whole history -- inserts, tombstones,
+stale copies -- lives on the shard that owns the key, so per-shard semantics
+are exactly the global ones. Shard s of P owns the original keys with
+owner(k) = min(P-1, floor(k*P / 2^31)) (keys above 2^31-2 go to P-1).
+
+Updates: each rank holds its slice of the global batch (positions
+[rank*b_in, (rank+1)*b_in) of the global batch order). The bucket kernel
+(lsm_shard_bucket) stably groups the slice by owner; an all-to-all of the
+counts and of the records (NCCL over NVLink on GPUs) delivers each owner its
+records in SOURCE-RANK order, which is global batch order, so the in-batch
+rules 4-6 (first insert wins, a delete wins) hold globally.
+Each owner then runs one local lsm_update with the received records
+(n <= b_local; the local LSM pads with placebos, reading R7). A local batch
+larger than b_local (probability ~1e-15 at the default 8-sigma slack) is
+split by a hash of the key into sub-batches inserted one after another;
+equal keys never straddle sub-batches, so the semantics are unchanged.
+
+Lookups: bucket the queries (keeping the permutation), all-to-all them to
+their owners, look up locally, all-to-all the (value, found) results back
+and scatter them to the original positions (lsm_shard_scatter).
+
+Counts: every rank gathers all ranks' (k1, k2), clips them to its own key
+interval (lsm_shard_clip), counts locally, and the per-shard partial counts
+go back to each query's origin with an all-to-all and are summed there
+(lsm_shard_sum): a range that spans shards is the sum of its pieces.
+
+All data-path arithmetic runs in libgpulsm kernels; torch.distributed only
+moves bytes. The backend is pluggable so the routing logic can be tested on
+CPU with gloo (tests/test_sharded_gloo.py); the GPU backend is the product.
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+import torch.distributed as dist
+
+from . import GpuLSM
+
+DOMAIN = 1 << 31
+
+
+def shard_bounds(P: int, s: int):
+    """[lo, hi] of original keys owned by shard s (hi inclusive)."""
+    lo = -(-s * DOMAIN // P)  # ceil(s * 2^31 / P)
+    hi = (-(-(s + 1) * DOMAIN // P) - 1) if s + 1 < P else 0xFFFFFFFF
+    return lo, hi
+
+
+def local_batch_size(b_global: int, P: int, slack_sigma: float = 8.0, align: int = 128) -> int:
+    """b_local = b_global/P + slack_sigma * sigma, sigma the binomial spread of
+    one shard's share of a uniform batch, rounded up to `align`."""
+    b_in = b_global // P
+    if P == 1:
+        return b_in
+    sigma = math.sqrt(b_global * (1.0 / P) * (1.0 - 1.0 / P))
+    return int(-(-math.ceil(b_in + slack_sigma * sigma) // align) * align)
+
+
+class GpuShardBackend:
+    """Product backend: every step runs in libgpulsm kernels on this GPU."""
+
+    def __init__(self, b_local: int, device=None, reserve_batches: int = 0):
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+        self.lsm = GpuLSM(b_local, reserve_batches=reserve_batches)
+
+    def empty(self, n, dtype):
+        return torch.empty(n, dtype=dtype, device=self.device)
+
+    def host_list(self, t):
+        return [int(x) for x in t.cpu().tolist()]
+
+    def bucket(self, keys, vals, ops, P, mode, want_perm):
+        return self.lsm.shard_bucket(keys, P, vals=vals, ops=ops, mode=mode, want_perm=want_perm)
+
+    def scatter(self, perm, vals, found):
+        vo = torch.empty_like(vals)
+        fo = torch.empty_like(found)
+        self.lsm.shard_scatter(perm, vals, found, vo, fo)
+        return vo, fo
+
+    def clip(self, k1, k2, lo, hi):
+        return self.lsm.shard_clip(k1, k2, lo, hi)
+
+    def sum_parts(self, t, P, n):
+        return self.lsm.shard_sum(t, P, n)
+
+    def update(self, k, v, o):
+        self.lsm.update(k, v, o)
+
+    def lookup(self, q):
+        return self.lsm.lookup(q)
+
+    def count(self, k1, k2):
+        return self.lsm.count(k1, k2)
+
+
+class ShardedLSM:
+    """One LSM per rank, keys partitioned by range, routed by all-to-all."""
+
+    def __init__(self, b_global: int, group=None, backend=None, slack_sigma: float = 8.0,
+                 reserve_batches: int = 0):
+        self.group = group
+        self.P = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if b_global % self.P:
+            raise ValueError("b_global must be a multiple of the number of ranks")
+        self.b_global = b_global
+        self.b_in = b_global // self.P
+        self.b_local = local_batch_size(b_global, self.P, slack_sigma)
+        self.lo, self.hi = shard_bounds(self.P, self.rank)
+        self.backend = backend if backend is not None else GpuShardBackend(
+            self.b_local, reserve_batches=reserve_batches)
+        self.batches = 0
+        self.overflow_splits = 0
+
+    # ---- collectives (bytes only) ----
+    def _a2a(self, send, send_counts, recv_counts, dtype):
+        out = self.backend.empty(sum(recv_counts), dtype)
+        dist.all_to_all_single(out, send, recv_counts, send_counts, group=self.group)
+        return out
+
+    def _exchange_counts(self, counts):
+        recv = self.backend.empty(self.P, torch.int32)
+        dist.all_to_all_single(recv, counts, group=self.group)
+        return self.backend.host_list(counts), self.backend.host_list(recv)
+
+    # ---- updates ----
+    def update(self, keys, vals=None, is_delete=None):
+        """This rank's slice of one global batch (global positions
+        [rank*b_in, (rank+1)*b_in)); all ranks call it together."""
+        if vals is None:
+            vals = self.backend.empty(keys.numel(), torch.int32).zero_()
+        if is_delete is None:
+            is_delete = self.backend.empty(keys.numel(), torch.uint8).zero_()
+        k, v, o, _, cnt = self.backend.bucket(keys, vals, is_delete, self.P, 0, False)
+        send, recv = self._exchange_counts(cnt)
+        rk = self._a2a(k, send, recv, torch.int32)
+        rv = self._a2a(v, send, recv, torch.int32)
+        ro = self._a2a(o, send, recv, torch.uint8)
+        self._local_insert(rk, rv, ro, sum(recv))
+        self.batches += 1
+
+    def _local_insert(self, rk, rv, ro, n):
+        if n == 0:
+            return
+        if n <= self.b_local:
+            self.backend.update(rk[:n], rv[:n], ro[:n])
+            return
+        # oversized local batch: 64 hash buckets (equal keys stay together),
+        # packed in order into sub-batches of at most b_local
+        self.overflow_splits += 1
+        k2, v2, o2, _, c2 = self.backend.bucket(rk[:n], rv[:n], ro[:n], 64, 1, False)
+        counts = self.backend.host_list(c2)
+        if max(counts) > self.b_local:
+            raise RuntimeError("shard overflow: one key-hash bucket exceeds b_local; "
+                               "raise slack_sigma")
+        start = cur = 0
+        for c in counts + [self.b_local + 1]:
+            if cur + c > self.b_local:
+                if cur:
+                    self.backend.update(k2[start:start + cur], v2[start:start + cur],
+                                        o2[start:start + cur])
+                start += cur
+                cur = 0
+            cur += c
+
+    # ---- queries ----
+    def lookup(self, q):
+        """Lookup this rank's queries; returns (vals, found) in query order."""
+        k, _, _, perm, cnt = self.backend.bucket(q, None, None, self.P, 0, True)
+        send, recv = self._exchange_counts(cnt)
+        rq = self._a2a(k, send, recv, torch.int32)
+        v, f = self.backend.lookup(rq)
+        bv = self._a2a(v, recv, send, torch.int32)
+        bf = self._a2a(f, recv, send, torch.uint8)
+        return self.backend.scatter(perm, bv, bf)
+
+    def count(self, k1, k2):
+        """Counts for this rank's (k1, k2) queries; every rank passes the same
+        number of queries."""
+        nq = k1.numel()
+        all1 = self.backend.empty(nq * self.P, torch.int32)
+        all2 = self.backend.empty(nq * self.P, torch.int32)
+        dist.all_gather_into_tensor(all1, k1, group=self.group)
+        dist.all_gather_into_tensor(all2, k2, group=self.group)
+        c1, c2 = self.backend.clip(all1, all2, self.lo, self.hi)
+        partial = self.backend.count(c1, c2)
+        recv = self._a2a(partial, [nq] * self.P, [nq] * self.P, torch.int32)
+        return self.backend.sum_parts(recv, self.P, nq)
+
+
+def run_sharded_bench(args, dist_mod, rank, world, local_rank):
+    """bench.py --gpus N (N > 1): weak scaling of the sharded LSM.
+
+    Global batch b_global = N * 2^20 (each rank contributes 2^20 positions of
+    the global order), R = 64 global batches from empty (2^26 resident per
+    GPU), then 2^24 lookups per rank routed to their owners. Times are CUDA
+    events on each rank, max over ranks."""
+    import json
+    import os
+    import sys
+    import time
+
+    import numpy as np
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import synth
+    from . import to_device
+
+    B_IN = 1 << 20
+    R = 64
+    NQ = 1 << 24
+    b_global = B_IN * world
+    seed = synth.SEED_BASE + 4
+    dev = torch.device("cuda", local_rank)
+    keys, vals, ops = [], [], []
+    for j in range(R):
+        k, v, d = synth.updates(seed, j * b_global + rank * B_IN, B_IN, delete_frac4=0)
+        keys.append(to_device(k, dev))
+        vals.append(to_device(v, dev))
+        ops.append(to_device(d, dev))
+    q = to_device(synth.lookup_queries(seed + rank, NQ, R * b_global), dev)
+    sh = ShardedLSM(b_global, reserve_batches=R + 2)
+
+    def step():
+        sh.backend.lsm.clear()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e2 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for j in range(R):
+            sh.update(keys[j], vals[j], ops[j])
+        e1.record()
+        sh.lookup(q)
+        e2.record()
+        return e0, e1, e2
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist_mod.barrier()
+    recs = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        recs.append(step())
+    torch.cuda.synchronize()
+    dist_mod.barrier()
+    wall = time.perf_counter() - t0
+    upd = sum(a.elapsed_time(b) for a, b, _ in recs) / args.steps
+    look = sum(b.elapsed_time(c) for _, b, c in recs) / args.steps
+    t = torch.tensor([upd, look, wall], device=dev, dtype=torch.float64)
+    dist_mod.all_reduce(t, op=dist_mod.ReduceOp.MAX)
+    upd, look, wall = [float(x) for x in t.tolist()]
+    if rank == 0:
+        line = {
+            "metric": "M updates/s at batch b; M lookup/count/range queries/s; HBM GB/s vs peak",
+            "value": R * b_global / (upd * 1e-3) / 1e6, "unit": "M updates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": (upd + look), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic (splitmix64 uniform keys)",
+            "config": {"workload": "C5: key-range sharded LSM, global batch b = N x 2^20 routed by "
+                                   "bucket kernel + NCCL all-to-all, 64 global batches "
+                                   f"(2^26 resident per GPU), 2^24 lookups per rank",
+                       "b_global": b_global, "b_local": sh.b_local, "batches": R,
+                       "parallelism": f"key-range shards x{world}"},
+            "lookup_mqps": world * NQ / (look * 1e-3) / 1e6,
+            "overflow_splits": sh.overflow_splits,
+            "wall_s": wall,
+        }
+        print(json.dumps(line), flush=True)
+    dist_mod.barrier()
+    dist_mod.destroy_process_group()
+    return 0

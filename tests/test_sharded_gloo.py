@@ -1,0 +1,202 @@
+"""Multi-process (world size 2, gloo, CPU) tests of the key-range sharded
+router (paper_1707_05354_b200/sharded.py).
+
+The router's host logic -- count exchange, all-to-all splits, source-rank
+concatenation order (global batch order), the oversize-batch split, query
+routing and result scatter, clipped partial counts -- runs unchanged; the
+per-rank backend is a test-only CPU stand-in (numpy + the O1 oracle as each
+shard's local dictionary). Results must equal ONE global oracle fed the whole
+global batches in order.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+class CpuTestBackend:
+    """Test-only backend: same contract as sharded.GpuShardBackend."""
+
+    def __init__(self, b_local):
+        import oracle
+        self.b_local = b_local
+        self.store = oracle.OracleDict(b_local)
+        self.batch_sizes = []
+
+    def empty(self, n, dtype):
+        return torch.empty(n, dtype=dtype)
+
+    def host_list(self, t):
+        return [int(x) for x in t.tolist()]
+
+    @staticmethod
+    def owner(k, P, mode):
+        k = k.astype(np.uint64)
+        if mode == 0:
+            o = (k * np.uint64(P)) >> np.uint64(31)
+            return np.minimum(o, P - 1).astype(np.int64)
+        h = (k * np.uint64(0x9E3779B1)) & np.uint64(0xFFFFFFFF)
+        bits = int(P).bit_length() - 1
+        return (h >> np.uint64(32 - bits)).astype(np.int64) if bits else np.zeros(len(k), np.int64)
+
+    def bucket(self, keys, vals, ops, P, mode, want_perm):
+        k = keys.numpy().view(np.uint32)
+        o = self.owner(k, P, mode)
+        perm = np.argsort(o, kind="stable")
+        counts = np.bincount(o, minlength=P).astype(np.int32)
+        kb = torch.from_numpy(k[perm].view(np.int32).copy())
+        vb = torch.from_numpy(vals.numpy()[perm].copy()) if vals is not None else None
+        ob = torch.from_numpy(ops.numpy()[perm].copy()) if ops is not None else None
+        pb = torch.from_numpy(perm.astype(np.int32)) if want_perm else None
+        return kb, vb, ob, pb, torch.from_numpy(counts)
+
+    def scatter(self, perm, vals, found):
+        vo = torch.empty_like(vals)
+        fo = torch.empty_like(found)
+        vo[perm.long()] = vals
+        fo[perm.long()] = found
+        return vo, fo
+
+    def clip(self, k1, k2, lo, hi):
+        a = k1.numpy().view(np.uint32).astype(np.int64)
+        z = k2.numpy().view(np.uint32).astype(np.int64)
+        empty = (a > z) | (z < lo) | (a > hi)
+        a2 = np.where(empty, 1, np.maximum(a, lo))
+        z2 = np.where(empty, 0, np.minimum(z, hi))
+        return (torch.from_numpy(a2.astype(np.uint32).view(np.int32)),
+                torch.from_numpy(z2.astype(np.uint32).view(np.int32)))
+
+    def sum_parts(self, t, P, n):
+        return torch.from_numpy(t.numpy().reshape(P, n).sum(axis=0).astype(np.int32))
+
+    def update(self, k, v, o):
+        assert k.numel() <= self.b_local
+        self.batch_sizes.append(k.numel())
+        self.store.apply_batch(k.numpy().view(np.uint32), v.numpy().view(np.uint32), o.numpy())
+
+    def lookup(self, q):
+        v, f = self.store.lookup(q.numpy().view(np.uint32))
+        return torch.from_numpy(v.view(np.int32).copy()), torch.from_numpy(f.copy())
+
+    def count(self, k1, k2):
+        c = self.store.count(k1.numpy().view(np.uint32), k2.numpy().view(np.uint32))
+        return torch.from_numpy(c.view(np.int32).copy())
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, scenario, out_q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import synth
+        from paper_1707_05354_b200.sharded import ShardedLSM, local_batch_size
+        b_global, nbatch, alphabet, slack = scenario
+        sh = ShardedLSM(b_global, backend=CpuTestBackend(local_batch_size(b_global, world, slack)),
+                        slack_sigma=slack)
+        b_in = b_global // world
+        for j in range(nbatch):
+            k, v, d = synth.updates(77, j * b_global + rank * b_in, b_in, delete_frac4=1,
+                                    alphabet=alphabet)
+            if alphabet is not None and alphabet < 0:
+                pass
+            sh.update(torch.from_numpy(k.view(np.int32).copy()), torch.from_numpy(v.view(np.int32).copy()),
+                      torch.from_numpy(d.copy()))
+        dom = alphabet if alphabet else synth.D
+        q = synth.lookup_queries(5 + rank, 500, nbatch * b_global, alphabet)
+        q = np.concatenate([q, np.array([0, 0x7FFFFFFE, 0x7FFFFFFF, 0xFFFFFFFF], np.uint32)])
+        qv, qf = sh.lookup(torch.from_numpy(q.view(np.int32).copy()))
+        k1, k2 = synth.range_queries(9 + rank, 300, nbatch * b_global, 16, domain=dom)
+        # ranges that straddle the shard boundary and the whole domain
+        k1 = np.concatenate([k1, np.array([0, (1 << 30) - 5, 0], np.uint32)])
+        k2 = np.concatenate([k2, np.array([0xFFFFFFFF, (1 << 30) + 5, 3], np.uint32)])
+        c = sh.count(torch.from_numpy(k1.view(np.int32).copy()), torch.from_numpy(k2.view(np.int32).copy()))
+        out_q.put((rank, q, qv.numpy().view(np.uint32), qf.numpy(), k1, k2,
+                   c.numpy().view(np.uint32), sh.overflow_splits, sh.backend.batch_sizes))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(scenario):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, scenario, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return sorted(res, key=lambda x: x[0])
+
+
+def _global_oracle(scenario):
+    import oracle
+    import synth
+    b_global, nbatch, alphabet, _ = scenario
+    o = oracle.OracleDict(b_global)
+    for j in range(nbatch):
+        k, v, d = synth.updates(77, j * b_global, b_global, delete_frac4=1, alphabet=alphabet)
+        o.apply_batch(k, v, d)
+    return o
+
+
+@pytest.mark.parametrize("scenario", [
+    (512, 6, None, 8.0),       # uniform keys, normal slack
+    (256, 5, 300, 8.0),        # duplicate-heavy: in-batch ties cross ranks
+])
+def test_sharded_router_matches_global_oracle(scenario):
+    res = _run(scenario)
+    o = _global_oracle(scenario)
+    for (rank, q, qv, qf, k1, k2, c, splits, sizes) in res:
+        ov, of = o.lookup(q)
+        assert np.array_equal(qf, of), rank
+        assert np.array_equal(qv[qf == 1], ov[of == 1]), rank
+        assert np.array_equal(c, o.count(k1, k2)), rank
+
+
+def test_sharded_router_oversize_split():
+    # all keys in shard 0's range (alphabet 300 << 2^30) and zero slack:
+    # shard 0 receives 2x b_local per batch and must split by key hash
+    scenario = (256, 4, 300, 0.0)
+    res = _run(scenario)
+    o = _global_oracle(scenario)
+    r0 = res[0]
+    assert r0[7] == 4  # one split per batch on shard 0
+    assert max(r0[8]) <= 128
+    for (rank, q, qv, qf, k1, k2, c, splits, sizes) in res:
+        ov, of = o.lookup(q)
+        assert np.array_equal(qf, of) and np.array_equal(qv[qf == 1], ov[of == 1])
+        assert np.array_equal(c, o.count(k1, k2))
+
+
+def test_shard_bounds_partition_the_domain():
+    from paper_1707_05354_b200.sharded import shard_bounds
+    for P in (1, 2, 3, 4, 7, 8):
+        prev = -1
+        for s in range(P):
+            lo, hi = shard_bounds(P, s)
+            assert lo == prev + 1
+            # owner() of the bounds agrees with the kernel formula
+            assert min(P - 1, (lo * P) >> 31) == s
+            if hi <= 0x7FFFFFFE:
+                assert min(P - 1, (hi * P) >> 31) == s
+            prev = hi
+        assert prev == 0xFFFFFFFF
