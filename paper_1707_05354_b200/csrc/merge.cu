@@ -32,9 +32,13 @@ namespace gpulsm {
 namespace {
 
 constexpr int kConsumerWarps = 8;
-constexpr int kMergeThreads = (kConsumerWarps + 1) * 32;
-constexpr int kMergeItems = 16;
-constexpr int kMergeTile = kConsumerWarps * 32 * kMergeItems;  // 4096
+constexpr int kConsumers = kConsumerWarps * 32;
+constexpr int kMergeThreads = kConsumers + 32;
+// 15 (odd) records per thread: neighbouring lanes then read the staged
+// windows ~7.5 words apart, spread over all 32 banks (16 gave 8-way
+// conflicts, measured: the merge was shared-memory bound)
+constexpr int kMergeItems = 15;
+constexpr int kMergeTile = kConsumers * kMergeItems;  // 3840
 constexpr int kStages = 3;
 constexpr int kBufElems = kMergeTile + 16;  // A + B windows incl. alignment slack
 
@@ -86,6 +90,27 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void consumers_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+}
+
 // First i in [lo, hi] with !((A[i]>>1) <= (B[d-1-i]>>1)): the number of A
 // records among the first d outputs (A first on ties). Whole warp.
 __device__ __forceinline__ uint64_t warp_merge_path(const uint32_t* __restrict__ ak,
@@ -111,6 +136,21 @@ __device__ __forceinline__ uint64_t warp_merge_path(const uint32_t* __restrict__
   return lo + __popc(__ballot_sync(kFull, t));
 }
 
+#ifdef GPULSM_PROBE
+__device__ unsigned long long* g_mprobe = nullptr;  // [cta][8] globaltimer stamps
+__device__ __forceinline__ unsigned long long mtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define MPROBE(k) \
+  do { if (g_mprobe) g_mprobe[blockIdx.x * 8 + (k)] = mtimer(); } while (0)
+#else
+#define MPROBE(k) \
+  do {            \
+  } while (0)
+#endif
+
 __global__ void __launch_bounds__(kMergeThreads) merge_kernel(
     const uint32_t* __restrict__ ak, const uint32_t* __restrict__ av, uint64_t na,
     const uint32_t* __restrict__ bk, const uint32_t* __restrict__ bv, uint64_t nb,
@@ -122,27 +162,31 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(
   const uint64_t t_begin = (uint64_t)blockIdx.x * ntiles / gridDim.x;
   const uint64_t t_end = (uint64_t)(blockIdx.x + 1) * ntiles / gridDim.x;
 
+  if (tid == 0) MPROBE(0);
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&S.full[s], 1);
-      mbar_init(&S.empty[s], kConsumerWarps);
+      mbar_init(&S.empty[s], 1);  // the consumer that issues the tile's bulk store
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   pdl_wait();  // inputs are the predecessor's outputs
   pdl_trigger();
+  if (tid == 0) MPROBE(1);
 
   if (warp == 0) {
     // ---------------- producer ----------------
     uint64_t d = t_begin * kMergeTile;
     uint64_t a = warp_merge_path(ak, bk, d, d > nb ? d - nb : 0, d < na ? d : na);
+    if (lane == 0) MPROBE(2);
     for (uint64_t t = t_begin, k = 0; t < t_end; ++t, ++k) {
       const uint64_t d_end = min(d + (uint64_t)kMergeTile, total);
       uint64_t lo = d_end > nb ? d_end - nb : 0;
       lo = max(lo, a);
       uint64_t hi = min(a + (d_end - d), na);
       const uint64_t a_end = warp_merge_path(ak, bk, d_end, lo, hi);
+      if (lane == 0 && k == 0) MPROBE(3);
       const int s = (int)(k % kStages);
       const uint32_t ph = (uint32_t)((k / kStages) & 1);
       mbar_wait(&S.empty[s], ph ^ 1u);
@@ -195,9 +239,10 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(
       const int s = (int)(k % kStages);
       const uint32_t ph = (uint32_t)((k / kStages) & 1);
       mbar_wait(&S.full[s], ph);
+      if (tid == 32 && k == 0) MPROBE(4);
       const StageInfo info = S.info[s];
-      const uint32_t* K = S.keys[s];
-      const uint32_t* V = S.vals[s];
+      uint32_t* K = S.keys[s];
+      uint32_t* V = S.vals[s];
       const uint32_t na_t = info.na, nb_t = info.nb, tile_n = na_t + nb_t;
       const uint32_t dt = min(ct * kMergeItems, tile_n);
       uint32_t lo = dt > nb_t ? dt - nb_t : 0;
@@ -212,41 +257,55 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(
       uint32_t ai = lo, bi = dt - lo;
       uint32_t ka = ai < na_t ? K[info.ka + ai] : 0u;
       uint32_t kb = bi < nb_t ? K[info.kb + bi] : 0u;
-      uint32_t rk[kMergeItems], rv[kMergeItems];
+      // serial merge: only the key loads sit on the dependency chain; the
+      // value of each output is gathered afterwards from its recorded slot
+      uint32_t rk[kMergeItems], src[kMergeItems];
 #pragma unroll
       for (int q = 0; q < kMergeItems; ++q) {
         const bool takeA = (bi >= nb_t) || (ai < na_t && (ka >> 1) <= (kb >> 1));
+        rk[q] = takeA ? ka : kb;
+        src[q] = takeA ? info.va + ai : info.vb + bi;
         if (takeA) {
-          rk[q] = ka;
-          rv[q] = V[min(info.va + ai, (uint32_t)kBufElems - 1)];
           ++ai;
           ka = ai < na_t ? K[info.ka + ai] : 0u;
         } else {
-          rk[q] = kb;
-          rv[q] = V[min(info.vb + bi, (uint32_t)kBufElems - 1)];
           ++bi;
           kb = bi < nb_t ? K[info.kb + bi] : 0u;
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&S.empty[s]);  // smem no longer needed
-      const uint64_t base = info.d0 + dt;
-      if (dt + kMergeItems <= tile_n) {
+      uint32_t rv[kMergeItems];
 #pragma unroll
-        for (int q = 0; q < kMergeItems / 4; ++q) {
-          stg_v4(ok + base + 4 * q, make_uint4(rk[4 * q], rk[4 * q + 1], rk[4 * q + 2], rk[4 * q + 3]));
-          stg_v4(ov + base + 4 * q, make_uint4(rv[4 * q], rv[4 * q + 1], rv[4 * q + 2], rv[4 * q + 3]));
-        }
-      } else {
+      for (int q = 0; q < kMergeItems; ++q) rv[q] = V[min(src[q], (uint32_t)kBufElems - 1)];
+      consumers_sync();  // every consumer is done reading this stage
+      // stage the merged tile in place (lane stride 15 words: conflict-free)
 #pragma unroll
-        for (int q = 0; q < kMergeItems; ++q) {
-          if (dt + q < tile_n) {
-            ok[base + q] = rk[q];
-            ov[base + q] = rv[q];
-          }
+      for (int q = 0; q < kMergeItems; ++q) {
+        if (dt + q < tile_n) {
+          K[dt + q] = rk[q];
+          V[dt + q] = rv[q];
         }
       }
+      fence_proxy_async_smem();  // generic smem writes -> visible to the bulk copy
+      consumers_sync();
+      if (ct == 0) {
+        // one TMA bulk store per array, then free the stage once read
+        const uint32_t n16 = tile_n & ~3u;
+        if (n16) {
+          bulk_s2g(ok + info.d0, K, n16 * 4);
+          bulk_s2g(ov + info.d0, V, n16 * 4);
+          bulk_commit();
+        }
+        for (uint32_t i = n16; i < tile_n; ++i) {  // ragged tail (< 4 records)
+          ok[info.d0 + i] = K[i];
+          ov[info.d0 + i] = V[i];
+        }
+        bulk_wait_read();
+        mbar_arrive(&S.empty[s]);
+      }
+      if (tid == 32 && k == 0) MPROBE(5);
     }
+    if (ct == 0) bulk_wait_all();  // writes complete before the grid retires
+    if (tid == 32) MPROBE(6);
   }
 }
 
