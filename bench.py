@@ -277,16 +277,19 @@ def run_native(args):
     dom = max(prof, key=lambda c: prof[c]["ms"])
     ach = prof[dom]["alg_bytes"] / (prof[dom]["ms"] * 1e-3) / 1e9 if prof[dom]["ms"] else 0.0
     step_kernel_ms = sum(p["ms"] for p in prof.values())
-    traffic = None
+    traffic, traffic_src = None, None
     summ = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(summ):
         with open(summ) as f:
             tr = json.load(f)
-        if dom in tr:
-            traffic = tr[dom].get("dram_bytes_per_launch_model_scaled")
+        if dom in tr:  # DRAM bytes of one captured launch of this kernel (ncu --set full)
+            traffic = tr[dom].get("dram_bytes_per_launch")
+            traffic_src = f"profiles/ncu_traffic.json ({tr[dom].get('kernel')}, {tr[dom].get('rep')})"
+    alg_per_launch = prof[dom]["alg_bytes"] / max(prof[dom]["launches"], 1)
     roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak,
                 "peak_source": peak_src, "unit": "GB/s", "frac": ach / peak,
-                "traffic": traffic,
+                "traffic": traffic, "traffic_source": traffic_src,
+                "alg_bytes_per_launch": alg_per_launch,
                 "share_of_step_kernel_time": prof[dom]["ms"] / step_kernel_ms if step_kernel_ms else None}
     per_class = {c: {"ms_per_step": p["ms"] / args.steps,
                      "launches_per_step": p["launches"] / args.steps,

@@ -108,7 +108,24 @@ __device__ __forceinline__ void encode_loaded(const RawBatch& in, uint64_t pos, 
 
 // Mask of lanes whose 8-bit digit equals mine (8 ballots), restricted to
 // lanes with valid == true.
+#ifndef RANK_VARIANT
+#define RANK_VARIANT 1
+#endif
 __device__ __forceinline__ uint32_t digit_peers(uint32_t d, bool valid) {
+#if RANK_VARIANT == 2
+  const uint32_t m = __match_any_sync(kFull, valid ? d : 0xFFFFFFFFu);
+  return valid ? m : 0u;
+#elif RANK_VARIANT == 1
+  // 8 independent ballots, combined by a balanced AND tree (depth 3)
+  uint32_t t[kRadixBits];
+#pragma unroll
+  for (int bit = 0; bit < kRadixBits; ++bit) {
+    const uint32_t bb = __ballot_sync(kFull, (d >> bit) & 1u);
+    t[bit] = ((d >> bit) & 1u) ? bb : ~bb;
+  }
+  const uint32_t m = ((t[0] & t[1]) & (t[2] & t[3])) & ((t[4] & t[5]) & (t[6] & t[7]));
+  return m & __ballot_sync(kFull, valid);
+#else
   uint32_t m = __ballot_sync(kFull, valid);
 #pragma unroll
   for (int bit = 0; bit < kRadixBits; ++bit) {
@@ -116,6 +133,7 @@ __device__ __forceinline__ uint32_t digit_peers(uint32_t d, bool valid) {
     m &= ((d >> bit) & 1u) ? bb : ~bb;
   }
   return m;
+#endif
 }
 
 struct HistSmem {

@@ -43,6 +43,7 @@ int main(int argc, char** argv) {
   cudaEventRecord(e1); cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1);
   printf("b=%llu tiles=%llu sort avg %.2f us (%.2f G pairs/s)\n", (unsigned long long)b, (unsigned long long)tiles, ms * 10, b / (ms * 1e-2) / 1e9 * 1e-3 * 1e3 / 1e3);
+#ifdef GPULSM_PROBE
   unsigned int zero8[8] = {0};
   cudaMemcpyToSymbol(g_repolls, zero8, sizeof(zero8));
   unsigned long long* probe; size_t pn = 4ull * 4096 * 8 + 4096 * 4;
@@ -97,6 +98,7 @@ int main(int argc, char** argv) {
   unsigned int rp[8];
   cudaMemcpyFromSymbol(rp, g_repolls, sizeof(rp));
   for (int i = 0; i < 8; ++i) printf("repolls[%d]=%u\n", i, rp[i]);
+#endif
   printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
