@@ -4,6 +4,8 @@
 #pragma once
 
 #include <cuda_runtime.h>
+
+#include <algorithm>
 #include <stdint.h>
 
 #include "gpulsm.h"
@@ -14,14 +16,39 @@ constexpr uint32_t kMaxKey = LSM_MAX_KEY;
 constexpr uint32_t kPlacebo = LSM_PLACEBO;
 constexpr uint32_t kFull = 0xFFFFFFFFu;
 
+// Fence-key index of a level (the
+// paper's future-work direction PAPER.md:1043-1046 without COLA's
+// inter-level pointers): F1[j] = K[8j], F2[j] = F1[32j] = K[256j],
+// F3[j] = F2[32j] = K[8192j] (full key variables). A lower_bound then reads
+// F3 (shared memory), one 128-byte line of F2, one of F1 and one 32-byte
+// sector of K instead of log2(n) dependent probes.
+constexpr int kF1Step = 8;
+constexpr int kFanout = 32;
+inline __host__ __device__ uint64_t idx_f1_len(uint64_t n) { return (n + kF1Step - 1) / kF1Step; }
+inline __host__ __device__ uint64_t idx_f2_len(uint64_t n) { return (idx_f1_len(n) + kFanout - 1) / kFanout; }
+inline __host__ __device__ uint64_t idx_f3_len(uint64_t n) { return (idx_f2_len(n) + kFanout - 1) / kFanout; }
+// words of one index allocation: F1 | F2 | F3, each padded to 32 words
+inline __host__ __device__ uint64_t idx_words(uint64_t n) {
+  auto r = [](uint64_t x) { return (x + 31) / 32 * 32; };
+  return r(idx_f1_len(n)) + r(idx_f2_len(n)) + r(idx_f3_len(n));
+}
+inline __host__ __device__ uint64_t idx_f2_off(uint64_t n) { return (idx_f1_len(n) + 31) / 32 * 32; }
+inline __host__ __device__ uint64_t idx_f3_off(uint64_t n) {
+  return idx_f2_off(n) + (idx_f2_len(n) + 31) / 32 * 32;
+}
+
 // Level table passed by value in kernel parameters (occupied levels only,
 // ascending index = newest first).
 struct LevelTable {
   const uint32_t* keys[LSM_MAX_LEVELS];
   const uint32_t* vals[LSM_MAX_LEVELS];
+  const uint32_t* idx[LSM_MAX_LEVELS];   // F1 | F2 | F3 (see idx_f*_off)
   uint64_t n[LSM_MAX_LEVELS];
+  uint32_t f3_smem_off[LSM_MAX_LEVELS];  // offset of the level's F3 in smem
+  uint32_t f3_smem_total;                // words of F3 staged in smem
   int count;
 };
+constexpr uint32_t kF3SmemMax = 24 * 1024;  // words (96 KB); larger indexes use global F3
 
 __device__ __forceinline__ uint32_t lane_id() {
   uint32_t r;
@@ -199,19 +226,33 @@ struct LaunchHooks {
   void* ctx;
 };
 
+// out_f1 (nullable): F1 of the output level (every 8th sorted key).
 cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals,
                               const uint8_t* ops, int mode, uint64_t n, uint64_t b,
                               SortScratch& S, uint32_t* out_keys, uint32_t* out_vals,
-                              cudaStream_t s, const LaunchHooks& hk);
+                              uint32_t* out_f1, cudaStream_t s, const LaunchHooks& hk);
 
-// Stable merge on key>>1, A (newer) first on ties, into out[na+nb].
+// Stable merge on key>>1, A (newer) first on ties, into out[na+nb];
+// out_f1 (nullable) receives F1 of the output.
 cudaError_t launch_merge(const uint32_t* ak, const uint32_t* av, uint64_t na,
                          const uint32_t* bk, const uint32_t* bv, uint64_t nb, uint32_t* ok,
-                         uint32_t* ov, cudaStream_t s, const LaunchHooks& hk);
+                         uint32_t* ov, uint32_t* out_f1, cudaStream_t s, const LaunchHooks& hk);
+
+// Index maintenance (index.cu): F1 from a level's keys (cleanup views), and
+// F2/F3 from F1 for up to LSM_MAX_LEVELS levels in one launch.
+cudaError_t launch_build_f1(const uint32_t* keys, uint64_t n, uint32_t* f1, cudaStream_t s,
+                            const LaunchHooks& hk);
+struct IndexJobs {
+  uint32_t* idx[LSM_MAX_LEVELS];
+  uint64_t n[LSM_MAX_LEVELS];
+  int count;
+};
+cudaError_t launch_finalize_index(const IndexJobs& J, cudaStream_t s, const LaunchHooks& hk);
 
 cudaError_t launch_lookup(const LevelTable& T, const uint32_t* q, uint64_t nq,
                           uint32_t* vals_out, uint8_t* found_out, cudaStream_t s,
                           const LaunchHooks& hk);
+int device_sms();
 
 cudaError_t launch_count(const LevelTable& T, const uint32_t* k1, const uint32_t* k2,
                          uint64_t nq, uint32_t* counts_out, cudaStream_t s,

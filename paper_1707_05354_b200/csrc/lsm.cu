@@ -37,6 +37,9 @@ struct Level {
   const uint32_t* keys = nullptr;
   const uint32_t* vals = nullptr;
   Buffer* owner = nullptr;  // non-null: view into a shared cleanup buffer
+  uint32_t* idx = nullptr;  // fence-key index F1 | F2 | F3
+  bool idx_owned = false;   // allocated for a view (freed with the level)
+  bool idx_ready = false;   // F2/F3 derived from F1
 };
 
 struct ProfRec {
@@ -53,6 +56,7 @@ struct lsm {
   uint64_t r = 0;
   Level level[LSM_MAX_LEVELS];
   Buffer home[LSM_MAX_LEVELS];
+  uint32_t* home_idx[LSM_MAX_LEVELS] = {};  // index storage of each home level
   Buffer ping[2];         // merge ping-pong scratch
   Buffer sortout;         // sorted batch when t >= 1
   SortScratch sort{};
@@ -162,7 +166,14 @@ void level_release(lsm* h, int i, cudaStream_t s) {
       delete L.owner;
     }
   }
+  if (L.idx_owned && L.idx) cudaFreeAsync(L.idx, s);
   L = Level{};
+}
+
+// index storage of home level i (F1 | F2 | F3 for b*2^i records)
+cudaError_t home_idx_ensure(lsm* h, int i, cudaStream_t s) {
+  if (h->home_idx[i]) return cudaSuccess;
+  return pool_alloc(h, (void**)&h->home_idx[i], idx_words(h->b << i) * 4, s);
 }
 
 cudaError_t ensure_sort_scratch(lsm* h, cudaStream_t s) {
@@ -203,20 +214,47 @@ cudaError_t ensure_qbuf(lsm* h, uint64_t bytes, cudaStream_t s) {
   return cudaSuccess;
 }
 
+// Level table of the occupied levels, newest first; F3 of as many levels as
+// fit in kF3SmemMax words is staged in shared memory by the query kernels.
 LevelTable level_table(const lsm* h) {
   LevelTable T;
   std::memset(&T, 0, sizeof(T));
   int c = 0;
+  uint32_t off = 0;
   for (int i = 0; i < LSM_MAX_LEVELS; ++i) {
     if ((h->r >> i) & 1ull) {
       T.keys[c] = h->level[i].keys;
       T.vals[c] = h->level[i].vals;
+      T.idx[c] = h->level[i].idx;
       T.n[c] = h->b << i;
+      const uint64_t n3 = (idx_f3_len(T.n[c]) + 3) / 4 * 4;
+      if (off + n3 <= kF3SmemMax) {
+        T.f3_smem_off[c] = off;
+        off += (uint32_t)n3;
+      } else {
+        T.f3_smem_off[c] = 0xFFFFFFFFu;  // searched in global memory
+      }
       ++c;
     }
   }
+  T.f3_smem_total = off;
   T.count = c;
   return T;
+}
+
+// Derive F2/F3 of every occupied level whose index is stale (one launch).
+cudaError_t ensure_index(lsm* h, cudaStream_t s, const LaunchHooks& hk) {
+  IndexJobs J;
+  std::memset(&J, 0, sizeof(J));
+  for (int i = 0; i < LSM_MAX_LEVELS; ++i) {
+    if (((h->r >> i) & 1ull) && !h->level[i].idx_ready) {
+      J.idx[J.count] = h->level[i].idx;
+      J.n[J.count] = h->b << i;
+      ++J.count;
+      h->level[i].idx_ready = true;
+    }
+  }
+  return launch_finalize_index(J, s, hk);
 }
 
 int ffz(uint64_t r) {
@@ -286,6 +324,7 @@ lsm_status lsm_destroy(lsm_t* h) {
   for (int i = 0; i < LSM_MAX_LEVELS; ++i) {
     level_release(h, i, nullptr);
     buf_free(h->home[i], nullptr);
+    if (h->home_idx[i]) cudaFreeAsync(h->home_idx[i], nullptr);
   }
   buf_free(h->ping[0], nullptr);
   buf_free(h->ping[1], nullptr);
@@ -317,7 +356,10 @@ lsm_status lsm_reserve(lsm_t* h, uint64_t max_batches, void* stream) {
   CK(ensure_sort_scratch(h, s));
   int top = 0;
   while (top + 1 < LSM_MAX_LEVELS && (1ull << (top + 1)) <= max_batches) ++top;
-  for (int i = 0; i <= top; ++i) CK(buf_ensure(h, h->home[i], h->b << i, s));
+  for (int i = 0; i <= top; ++i) {
+    CK(buf_ensure(h, h->home[i], h->b << i, s));
+    CK(home_idx_ensure(h, i, s));
+  }
   CK(buf_ensure(h, h->sortout, h->b, s));
   if (top >= 1) {
     CK(buf_ensure(h, h->ping[0], h->b << (top - 1), s));
@@ -346,6 +388,7 @@ static lsm_status do_update(lsm_t* h, const uint32_t* keys, const uint32_t* vals
   LaunchHooks hk = hooks(h);
   CK(ensure_sort_scratch(h, s));
   CK(buf_ensure(h, h->home[t], b << t, s));
+  CK(home_idx_ensure(h, t, s));
   // sort (A1+A2): straight into level 0 when t == 0
   uint32_t* sk = (t == 0) ? h->home[0].keys : nullptr;
   uint32_t* sv = (t == 0) ? h->home[0].vals : nullptr;
@@ -358,7 +401,9 @@ static lsm_status do_update(lsm_t* h, const uint32_t* keys, const uint32_t* vals
       CK(buf_ensure(h, h->ping[1], b << (t - 1), s));
     }
   }
-  CK(launch_sort_batch(keys, vals, ops, mode, n, b, h->sort, sk, sv, s, hk));
+  // the producer of level t also writes its fence keys F1 (t == 0: the sort)
+  CK(launch_sort_batch(keys, vals, ops, mode, n, b, h->sort, sk, sv,
+                       t == 0 ? h->home_idx[0] : nullptr, s, hk));
   // cascade (A3): while level i is full, buffer <- merge(buffer, level i)
   const uint32_t* ck = sk;
   const uint32_t* cv = sv;
@@ -366,7 +411,8 @@ static lsm_status do_update(lsm_t* h, const uint32_t* keys, const uint32_t* vals
     uint32_t* ok = (i == t - 1) ? h->home[t].keys : h->ping[i & 1].keys;
     uint32_t* ov = (i == t - 1) ? h->home[t].vals : h->ping[i & 1].vals;
     const uint64_t ni = b << i;
-    CK(launch_merge(ck, cv, ni, h->level[i].keys, h->level[i].vals, ni, ok, ov, s, hk));
+    CK(launch_merge(ck, cv, ni, h->level[i].keys, h->level[i].vals, ni, ok, ov,
+                    i == t - 1 ? h->home_idx[t] : nullptr, s, hk));
     level_release(h, i, s);  // level i <- empty
     ck = ok;
     cv = ov;
@@ -374,6 +420,9 @@ static lsm_status do_update(lsm_t* h, const uint32_t* keys, const uint32_t* vals
   h->level[t].keys = h->home[t].keys;  // level t <- buffer
   h->level[t].vals = h->home[t].vals;
   h->level[t].owner = nullptr;
+  h->level[t].idx = h->home_idx[t];
+  h->level[t].idx_owned = false;
+  h->level[t].idx_ready = false;  // F2/F3 derived before the next query
   h->r += 1;  // num_batch++ 
   return LSM_OK;
 }
@@ -414,6 +463,7 @@ lsm_status lsm_lookup(lsm_t* h, const uint32_t* d_q, uint64_t nq, uint32_t* d_va
   if (!h) return LSM_ERR_INVALID_ARG;
   if (nq == 0) return LSM_OK;
   if (!d_q || !d_vals_out) return LSM_ERR_INVALID_ARG;
+  CK(ensure_index(h, S(stream), hooks(h)));
   LevelTable T = level_table(h);
   CK(launch_lookup(T, d_q, nq, d_vals_out, d_found_out, S(stream), hooks(h)));
   return LSM_OK;
@@ -432,6 +482,7 @@ lsm_status lsm_lookup_host(lsm_t* h, const uint32_t* h_q, uint64_t nq, uint32_t*
   uint32_t* dv = reinterpret_cast<uint32_t*>(base + align_up(nq * 4, 256));
   uint8_t* df = base + 2 * align_up(nq * 4, 256);
   CK(cudaMemcpyAsync(dq, h_q, nq * 4, cudaMemcpyHostToDevice, s));
+  CK(ensure_index(h, s, hooks(h)));
   LevelTable T = level_table(h);
   CK(launch_lookup(T, dq, nq, dv, df, s, hooks(h)));
   CK(cudaMemcpyAsync(h_vals_out, dv, nq * 4, cudaMemcpyDeviceToHost, s));
@@ -445,6 +496,7 @@ lsm_status lsm_count(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2, uint6
   if (!h) return LSM_ERR_INVALID_ARG;
   if (nq == 0) return LSM_OK;
   if (!d_k1 || !d_k2 || !d_counts_out) return LSM_ERR_INVALID_ARG;
+  CK(ensure_index(h, S(stream), hooks(h)));
   LevelTable T = level_table(h);
   CK(launch_count(T, d_k1, d_k2, nq, d_counts_out, S(stream), hooks(h), LSM_K_COUNT));
   return LSM_OK;
@@ -468,6 +520,7 @@ lsm_status lsm_range(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2, uint6
   CK(ensure_qbuf(h, cbytes + sbytes, s));
   uint32_t* counts = static_cast<uint32_t*>(h->qbuf);
   uint64_t* sums = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(h->qbuf) + cbytes);
+  CK(ensure_index(h, s, hk));
   LevelTable T = level_table(h);
   CK(launch_count(T, d_k1, d_k2, nq, counts, s, hk, LSM_K_COUNT));
   CK(launch_scan(counts, nq, d_offsets_out, sums, s, hk));
@@ -507,7 +560,7 @@ lsm_status lsm_cleanup(lsm_t* h, void* stream) {
     const int i = occ[j];
     const uint64_t ni = b << i;
     CK(launch_merge(mk, mv, mn, h->level[i].keys, h->level[i].vals, ni, h->ping[pp].keys,
-                    h->ping[pp].vals, s, hk));
+                    h->ping[pp].vals, nullptr, s, hk));
     mk = h->ping[pp].keys;
     mv = h->ping[pp].vals;
     mn += ni;
@@ -548,6 +601,11 @@ lsm_status lsm_cleanup(lsm_t* h, void* stream) {
     h->level[i].keys = C->keys + off;
     h->level[i].vals = C->vals + off;
     h->level[i].owner = C;
+    // the view's fence keys (F1) come from its keys; F2/F3 lazily
+    CK(pool_alloc(h, (void**)&h->level[i].idx, idx_words(b << i) * 4, s));
+    h->level[i].idx_owned = true;
+    h->level[i].idx_ready = false;
+    CK(launch_build_f1(h->level[i].keys, b << i, h->level[i].idx, s, hk));
     off += b << i;
     ++refs;
   }

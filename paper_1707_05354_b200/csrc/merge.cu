@@ -154,7 +154,8 @@ __device__ __forceinline__ unsigned long long mtimer() {
 __global__ void __launch_bounds__(kMergeThreads) merge_kernel(
     const uint32_t* __restrict__ ak, const uint32_t* __restrict__ av, uint64_t na,
     const uint32_t* __restrict__ bk, const uint32_t* __restrict__ bv, uint64_t nb,
-    uint32_t* __restrict__ ok, uint32_t* __restrict__ ov, uint64_t ntiles) {
+    uint32_t* __restrict__ ok, uint32_t* __restrict__ ov, uint64_t ntiles,
+    uint32_t* __restrict__ out_f1) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   MergeSmem& S = *reinterpret_cast<MergeSmem*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -276,6 +277,13 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(
       uint32_t rv[kMergeItems];
 #pragma unroll
       for (int q = 0; q < kMergeItems; ++q) rv[q] = V[min(src[q], (uint32_t)kBufElems - 1)];
+      if (out_f1 != nullptr) {  // fence keys of the new level: every 8th output
+#pragma unroll
+        for (int q = 0; q < kMergeItems; ++q) {
+          const uint64_t g = info.d0 + dt + q;
+          if (dt + q < tile_n && (g & (kF1Step - 1)) == 0) out_f1[g / kF1Step] = rk[q];
+        }
+      }
       consumers_sync();  // every consumer is done reading this stage
       // stage the merged tile in place (lane stride 15 words: conflict-free)
 #pragma unroll
@@ -315,7 +323,7 @@ int g_num_sms = 0;
 
 cudaError_t launch_merge(const uint32_t* ak, const uint32_t* av, uint64_t na,
                          const uint32_t* bk, const uint32_t* bv, uint64_t nb, uint32_t* ok,
-                         uint32_t* ov, cudaStream_t s, const LaunchHooks& hk) {
+                         uint32_t* ov, uint32_t* out_f1, cudaStream_t s, const LaunchHooks& hk) {
   const uint64_t total = na + nb;
   if (total == 0) return cudaSuccess;
   static bool attr_set = false;
@@ -335,7 +343,7 @@ cudaError_t launch_merge(const uint32_t* ak, const uint32_t* av, uint64_t na,
   const uint64_t grid = std::min<uint64_t>(ntiles, (uint64_t)g_num_sms * 2);
   hk.begin(hk.ctx, LSM_K_MERGE, s);
   cudaError_t e = launch_pdl(merge_kernel, (unsigned)grid, kMergeThreads, sizeof(MergeSmem), s, ak,
-                             av, na, bk, bv, nb, ok, ov, ntiles);
+                             av, na, bk, bv, nb, ok, ov, ntiles, out_f1);
   // algorithmic bytes: each output record is read once (8 B) and written once
   hk.end(hk.ctx, LSM_K_MERGE, (double)total * 16.0, s, 1);
   return e;

@@ -1,4 +1,4 @@
-// query.cu -- A4 lookup, A5 count, A6 range (sm_100a), plus the offset scan.
+// query.cu -- A4 lookup, A5 count, A6 range (sm_100a).
 //
 // Lookup: PAPER.md:413-437 (§3.4), Fig. 2b, §4.2
 // per query, search the full levels from the smallest
@@ -7,19 +7,26 @@
 // stops; otherwise continue.
 //
 // Count / range: PAPER.md:444-454 (§3.5), Fig. 2c/2d, §4.3-4.4
-// PAPER.md:693-736. Stage 1 (per-level lower/upper bounds) is kept as in
-// the paper. Stages 2-5 (scan, gather, segmented sort ignoring the status
-// bit, keep the first of each key run if regular) are replaced by an
-// equivalent per-query multi-way walk over the per-level candidate slices
-// (DESIGN.md §4.5): every record of a lower-index level is newer than every
-// record of a higher one and within a level a key run is
-// newest-first (invariant 2), so the newest record of a
-// key is the run head in the lowest level holding the key. Walking the
-// slices in key order visits exactly the paper's segments in order; the
-// walk emits each key once, valid iff that newest record is regular. For
-// range, a count pass, an exclusive scan of the counts (stage 2 on valid
-// counts instead of candidate counts) and a write pass give per-query
-// offsets and pairs sorted by key.
+// PAPER.md:693-736. Stage 1 (per-level lower/upper bounds) as in the paper.
+// Stages 2-5 (scan, gather, segmented sort ignoring the status bit, keep the
+// first of each key run if regular) are replaced by an equivalent per-query
+// multi-way walk over the per-level candidate slices: every
+// record of a lower-index level is newer than every record of a higher one
+// and within a level a key run is newest-first (invariant
+// 2), so the newest record of a key is the run head in the
+// lowest level holding the key; the walk visits the paper's segments in key
+// order and keeps a key iff that head is regular. For range, a count pass, an
+// exclusive scan of the valid counts (scan.cu) and a write pass give
+// per-query offsets and pairs sorted by key.
+//
+// Searches: the paper's bottleneck is "the random memory
+// accesses required in all binary searches". Every lower_bound
+// here goes through the level's fence-key index (common.cuh): a binary search
+// of F3 in shared memory, then one 128-byte line of F2, one of F1 and one
+// 32-byte sector of K. Each warp serves 32 queries and searches
+// cooperatively: for each of its 32 queries the warp loads the whole line in
+// one coalesced load and a ballot counts the fences below the query, so a
+// step issues 32 independent line loads per warp.
 
 #include "common.cuh"
 
@@ -27,64 +34,231 @@ namespace gpulsm {
 
 namespace {
 
-constexpr int kQThreads = 256;
+constexpr int kQThreads = 512;
+constexpr int kQCtasPerSm = 2;
 constexpr uint32_t kSent = 0xFFFFFFFFu;  // > any original key (<= 2^31-1)
 
-__global__ void __launch_bounds__(kQThreads) lookup_kernel(LevelTable T,
-                                                           const uint32_t* __restrict__ q,
-                                                           uint64_t nq,
-                                                           uint32_t* __restrict__ vals_out,
-                                                           uint8_t* __restrict__ found_out) {
-  const uint64_t i = (uint64_t)blockIdx.x * kQThreads + threadIdx.x;
-  if (i >= nq) return;
-  const uint32_t key = __ldg(q + i);
-  uint32_t v = LSM_NOT_FOUND;
-  uint8_t f = 0;
-  for (int j = 0; j < T.count; ++j) {
-    const uint32_t* K = T.keys[j];
-    const uint64_t n = T.n[j];
-    const uint64_t p = lower_bound_orig(K, n, key);
-    if (p < n) {
-      const uint32_t kk = __ldg(K + p);
-      if ((kk >> 1) == key) {
-        if (kk & 1u) {
-          v = __ldg(T.vals[j] + p);
-          f = 1;
-        }
-        break;  // a tombstone: deleted
-      }
-    }
-  }
-  vals_out[i] = v;
-  if (found_out) found_out[i] = f;
+struct LvView {
+  const uint32_t* K;
+  const uint32_t* V;
+  const uint32_t* f1;
+  const uint32_t* f2;
+  const uint32_t* f3;  // shared memory when staged, else global
+  uint64_t n;
+  uint32_t n1, n2, n3;
+};
+
+__device__ __forceinline__ LvView level_view(const LevelTable& T, int j, const uint32_t* sF3) {
+  LvView L;
+  L.K = T.keys[j];
+  L.V = T.vals[j];
+  L.n = T.n[j];
+  const uint32_t* idx = T.idx[j];
+  L.f1 = idx;
+  L.f2 = idx + idx_f2_off(L.n);
+  L.f3 = T.f3_smem_off[j] != 0xFFFFFFFFu ? sF3 + T.f3_smem_off[j] : idx + idx_f3_off(L.n);
+  L.n1 = (uint32_t)idx_f1_len(L.n);
+  L.n2 = (uint32_t)idx_f2_len(L.n);
+  L.n3 = (uint32_t)idx_f3_len(L.n);
+  return L;
 }
 
-// Per-query multi-way walk over the candidate slices [l_j, u_j) of the
-// occupied levels. Calls emit(idx, key, val) for each valid key in ascending
-// order; returns the number of valid keys. NL > 0: exactly NL levels, state
-// in registers (fully unrolled); NL == 0: generic (T.count levels, local
-// memory), used only beyond kMaxUnrolledLevels occupied levels.
-constexpr int kMaxUnrolledLevels = 16;
+// Stage the F3 arrays that fit into shared memory (kF3SmemMax words).
+__device__ __forceinline__ void stage_f3(const LevelTable& T, uint32_t* sF3) {
+  for (int j = 0; j < T.count; ++j) {
+    if (T.f3_smem_off[j] == 0xFFFFFFFFu) continue;
+    const uint32_t* g = T.idx[j] + idx_f3_off(T.n[j]);
+    const uint32_t n3 = (uint32_t)idx_f3_len(T.n[j]);
+    for (uint32_t i = threadIdx.x; i < n3; i += blockDim.x) sF3[T.f3_smem_off[j] + i] = __ldg(g + i);
+  }
+  __syncthreads();
+}
 
-template <int NL, typename Emit>
-__device__ __forceinline__ uint32_t walk_range(const LevelTable& T, uint32_t a, uint32_t z,
-                                               Emit emit) {
-  if (a > z) return 0;  // R9: the empty range
-  constexpr int CAP = NL > 0 ? NL : LSM_MAX_LEVELS;
-  const int L = NL > 0 ? NL : T.count;
-  uint64_t pos[CAP], end[CAP];
-  uint32_t head[CAP];
-#pragma unroll
-  for (int j = 0; j < CAP; ++j) {  // stage 1: per-level bounds
-    if (j < L) {
-      const uint32_t* K = T.keys[j];
-      const uint64_t l = lower_bound_orig(K, T.n[j], a);
-      const uint64_t u = upper_bound_orig(K, T.n[j], z);
-      pos[j] = l;
-      end[j] = u;
-      head[j] = l < u ? (__ldg(K + l) >> 1) : kSent;
+// number of entries of a sorted array with (entry >> 1) < x (lane-private)
+__device__ __forceinline__ uint32_t count_below(const uint32_t* a, uint32_t len, uint32_t x) {
+  uint32_t lo = 0;
+  while (len > 0) {
+    const uint32_t half = len >> 1;
+    if ((a[lo + half] >> 1) < x) {
+      lo += half + 1;
+      len -= half + 1;
+    } else {
+      len = half;
     }
   }
+  return lo;
+}
+
+// For every lane: entries of a[32*ln .. 32*ln+32) (within [0, len)) with
+// (entry >> 1) < x, where ln and x are the lane's own. The warp loads each
+// lane's line with one coalesced 128-byte load, then counts with a ballot.
+__device__ __forceinline__ uint32_t coop_line_count(const uint32_t* __restrict__ a, uint32_t len,
+                                                    uint32_t ln, uint32_t x) {
+  const uint32_t lane = lane_id();
+  uint32_t res = 0;
+#pragma unroll
+  for (int h = 0; h < 32; h += 16) {  // two rounds of 16 independent line loads
+    uint32_t v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t lj = __shfl_sync(kFull, ln, h + j);
+      const uint64_t i = (uint64_t)lj * 32 + lane;
+      v[j] = i < len ? __ldg(a + i) : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t lj = __shfl_sync(kFull, ln, h + j);
+      const uint32_t xj = __shfl_sync(kFull, x, h + j);
+      const bool below = ((uint64_t)lj * 32 + lane < len) && ((v[j] >> 1) < xj);
+      const uint32_t m = __ballot_sync(kFull, below);
+      if (lane == (uint32_t)(h + j)) res = __popc(m);
+    }
+  }
+  return res;
+}
+
+// Same for 8-record groups of K: four queries per warp load (lanes 8s..8s+7
+// read query 4i+s's group).
+__device__ __forceinline__ uint32_t coop_group_count(const uint32_t* __restrict__ K, uint64_t n,
+                                                     uint32_t g, uint32_t x) {
+  const uint32_t lane = lane_id();
+  const uint32_t sub = lane >> 3, e = lane & 7;
+  uint32_t v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t gj = __shfl_sync(kFull, g, 4 * i + sub);
+    const uint64_t idx = (uint64_t)gj * kF1Step + e;
+    v[i] = idx < n ? __ldg(K + idx) : 0u;
+  }
+  uint32_t res = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t gj = __shfl_sync(kFull, g, 4 * i + sub);
+    const uint32_t xj = __shfl_sync(kFull, x, 4 * i + sub);
+    const bool below = ((uint64_t)gj * kF1Step + e < n) && ((v[i] >> 1) < xj);
+    const uint32_t m = __ballot_sync(kFull, below);
+    const uint32_t cg = __popc((m >> (8 * sub)) & 0xFFu);
+    const uint32_t t = __shfl_sync(kFull, cg, 8 * (lane & 3));
+    if ((lane >> 2) == (uint32_t)i) res = t;
+  }
+  return res;
+}
+
+// lower_bound on the original key for every lane's x: the first position p
+// with (K[p] >> 1) >= x. Whole warp; each lane may have a different x.
+// F3[c3-1] < x <= F3[c3] brackets 8192 records; the F2 line below it, the F1
+// line below that and the 8-record group below that narrow it to p.
+__device__ __noinline__ uint64_t coop_lower_bound(const LvView L, uint32_t x) {
+  const uint32_t c3 = count_below(L.f3, L.n3, x);
+  const bool zero = c3 == 0;  // K[0] >= x
+  const uint32_t l2 = zero ? 0u : c3 - 1;
+  const uint32_t c2 = l2 * kFanout + coop_line_count(L.f2, L.n2, l2, x);
+  const uint32_t l1 = zero ? 0u : c2 - 1;
+  const uint32_t c1 = l1 * kFanout + coop_line_count(L.f1, L.n1, l1, x);
+  const uint32_t g = zero ? 0u : c1 - 1;
+  const uint64_t p = (uint64_t)g * kF1Step + coop_group_count(L.K, L.n, g, x);
+  return zero ? 0ull : p;
+}
+
+// Entries of a[base .. base+len_run) below x (orig < x), given a[base] < x:
+// a binary search over the (len_run - 1) entries after base, lane-private.
+__device__ __forceinline__ uint32_t run_count(const uint32_t* __restrict__ a, uint64_t base,
+                                              uint32_t len_run, uint32_t x) {
+  uint32_t lo = 1, n = len_run - 1;  // entry 0 is known to be below x
+  while (n > 0) {
+    const uint32_t half = n >> 1;
+    if ((__ldg(a + base + lo + half) >> 1) < x) {
+      lo += half + 1;
+      n -= half + 1;
+    } else {
+      n = half;
+    }
+  }
+  return lo;
+}
+
+// Entries of the 32-entry line a[32*ln ..) (within len) below x, given that
+// its first entry is below x. One round trip loads the three other sector
+// heads (the whole line lands in L1), then a search inside the chosen
+// 8-entry sector hits L1.
+__device__ __forceinline__ uint32_t line_count(const uint32_t* __restrict__ a, uint64_t len,
+                                               uint32_t ln, uint32_t x) {
+  const uint64_t base = (uint64_t)ln * kFanout;
+  const uint32_t e1 = base + 8 < len ? __ldg(a + base + 8) : 0xFFFFFFFFu;
+  const uint32_t e2 = base + 16 < len ? __ldg(a + base + 16) : 0xFFFFFFFFu;
+  const uint32_t e3 = base + 24 < len ? __ldg(a + base + 24) : 0xFFFFFFFFu;
+  const uint32_t t = (base + 8 < len && (e1 >> 1) < x) + (base + 16 < len && (e2 >> 1) < x) +
+                     (base + 24 < len && (e3 >> 1) < x);
+  const uint64_t s0 = base + 8 * t;
+  const uint32_t run = (uint32_t)(len - s0 < 8 ? len - s0 : 8);
+  return 8 * t + run_count(a, s0, run, x);
+}
+
+// Lane-private lower_bound on the original key through the fence index:
+// F3 (shared memory) -> F2 line -> F1 line -> 8-record group of K.
+__device__ __forceinline__ uint64_t idx_lower_bound(const LvView& L, uint32_t x) {
+  if (x > 0x7FFFFFFFu) return L.n;  // above every original key (R8)
+  const uint32_t c3 = count_below(L.f3, L.n3, x);
+  if (c3 == 0) return 0;  // K[0] >= x
+  const uint32_t c2 = (c3 - 1) * kFanout + line_count(L.f2, L.n2, c3 - 1, x);
+  const uint32_t c1 = (c2 - 1) * kFanout + line_count(L.f1, L.n1, c2 - 1, x);
+  const uint64_t g = (uint64_t)(c1 - 1) * kF1Step;
+  return g + run_count(L.K, g, (uint32_t)(L.n - g < kF1Step ? L.n - g : kF1Step), x);
+}
+
+// x for an upper bound: (K[p] >> 1) <= z  <=>  (K[p] >> 1) < z + 1
+__device__ __forceinline__ uint32_t ub_arg(uint32_t z) {
+  return z >= 0x7FFFFFFFu ? 0x80000000u : z + 1u;
+}
+
+__global__ void __launch_bounds__(kQThreads, kQCtasPerSm) lookup_kernel(
+    LevelTable T, const uint32_t* __restrict__ q, uint64_t nq, uint32_t* __restrict__ vals_out,
+    uint8_t* __restrict__ found_out) {
+  extern __shared__ uint32_t sF3[];
+  stage_f3(T, sF3);
+  const uint32_t lane = lane_id();
+  const uint64_t gw = ((uint64_t)blockIdx.x * kQThreads + threadIdx.x) / 32;
+  const uint64_t nw = (uint64_t)gridDim.x * kQThreads / 32;
+  for (uint64_t base = gw * 32; base < nq; base += nw * 32) {
+    const uint64_t i = base + lane;
+    const bool act = i < nq;
+    const uint32_t x = act ? __ldg(q + i) : 0u;
+    bool done = !act;
+    uint32_t v = LSM_NOT_FOUND;
+    uint8_t f = 0;
+    for (int j = 0; j < T.count; ++j) {
+      if (__all_sync(kFull, done)) break;
+      const LvView L = level_view(T, j, sF3);
+      const uint64_t p = done ? L.n : idx_lower_bound(L, x);
+      if (!done && p < L.n) {
+        const uint32_t kk = __ldg(L.K + p);
+        if ((kk >> 1) == x) {
+          done = true;
+          if (kk & 1u) {  // regular: its value; a tombstone: ⊥
+            v = __ldg(L.V + p);
+            f = 1;
+          }
+        }
+      }
+    }
+    if (act) {
+      vals_out[i] = v;
+      if (found_out) found_out[i] = f;
+    }
+  }
+}
+
+// Per-query walk over the candidate slices [pos_j, end_j) of the occupied
+// levels (state in registers for NL > 0). emit(idx, key, val) is called for
+// each valid key in ascending order; returns the number of valid keys.
+template <int NL, typename Emit>
+__device__ __forceinline__ uint32_t walk_slices(const LevelTable& T, uint64_t* pos, uint64_t* end,
+                                                int L, Emit emit) {
+  constexpr int CAP = NL > 0 ? NL : LSM_MAX_LEVELS;
+  uint32_t head[CAP];
+#pragma unroll
+  for (int j = 0; j < CAP; ++j)
+    if (j < L) head[j] = pos[j] < end[j] ? (__ldg(T.keys[j] + pos[j]) >> 1) : kSent;
   uint32_t cnt = 0;
   while (true) {
     uint32_t m = kSent;
@@ -123,133 +297,182 @@ __device__ __forceinline__ uint32_t walk_range(const LevelTable& T, uint32_t a, 
   return cnt;
 }
 
+// Stage 1 for all occupied levels: [l_j, u_j) = [lower_bound(k1),
+// upper_bound(k2)) per level, cooperative across the warp; empty when k1 > k2
+// (R9).
 template <int NL>
-__global__ void __launch_bounds__(kQThreads) count_kernel(LevelTable T,
-                                                          const uint32_t* __restrict__ k1,
-                                                          const uint32_t* __restrict__ k2,
-                                                          uint64_t nq,
-                                                          uint32_t* __restrict__ counts) {
-  const uint64_t i = (uint64_t)blockIdx.x * kQThreads + threadIdx.x;
-  if (i >= nq) return;
-  counts[i] = walk_range<NL>(T, __ldg(k1 + i), __ldg(k2 + i), [](uint32_t, uint32_t, uint32_t) {});
+__device__ __forceinline__ void bounds(const LevelTable& T, const uint32_t* sF3, uint32_t a,
+                                       uint32_t z, bool empty, uint64_t* pos, uint64_t* end,
+                                       int L) {
+  constexpr int CAP = NL > 0 ? NL : LSM_MAX_LEVELS;
+  const uint32_t xz = ub_arg(z);
+#pragma unroll
+  for (int j = 0; j < CAP; ++j) {
+    if (j < L) {
+      const LvView V = level_view(T, j, sF3);
+      pos[j] = empty ? 0 : idx_lower_bound(V, a);
+      end[j] = empty ? 0 : idx_lower_bound(V, xz);
+    }
+  }
 }
 
 template <int NL>
-__global__ void __launch_bounds__(kQThreads) range_write_kernel(
+__global__ void __launch_bounds__(kQThreads, 1) count_kernel(
+    LevelTable T, const uint32_t* __restrict__ k1, const uint32_t* __restrict__ k2, uint64_t nq,
+    uint32_t* __restrict__ counts) {
+  extern __shared__ uint32_t sF3[];
+  stage_f3(T, sF3);
+  constexpr int CAP = NL > 0 ? NL : LSM_MAX_LEVELS;
+  const int L = NL > 0 ? NL : T.count;
+  const uint32_t lane = lane_id();
+  const uint64_t gw = ((uint64_t)blockIdx.x * kQThreads + threadIdx.x) / 32;
+  const uint64_t nw = (uint64_t)gridDim.x * kQThreads / 32;
+  for (uint64_t base = gw * 32; base < nq; base += nw * 32) {
+    const uint64_t i = base + lane;
+    const bool act = i < nq;
+    const uint32_t a = act ? __ldg(k1 + i) : 1u, z = act ? __ldg(k2 + i) : 0u;
+    uint64_t pos[CAP], end[CAP];
+    bounds<NL>(T, sF3, a, z, a > z, pos, end, L);
+    const uint32_t c = walk_slices<NL>(T, pos, end, L, [](uint32_t, uint32_t, uint32_t) {});
+    if (act) counts[i] = c;
+  }
+}
+
+template <int NL>
+__global__ void __launch_bounds__(kQThreads, 1) range_write_kernel(
     LevelTable T, const uint32_t* __restrict__ k1, const uint32_t* __restrict__ k2, uint64_t nq,
     const uint64_t* __restrict__ offsets, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out) {
-  const uint64_t i = (uint64_t)blockIdx.x * kQThreads + threadIdx.x;
-  if (i >= nq) return;
-  const uint64_t base = offsets[i];
-  walk_range<NL>(T, __ldg(k1 + i), __ldg(k2 + i), [&](uint32_t c, uint32_t key, uint32_t val) {
-    keys_out[base + c] = key;
-    vals_out[base + c] = val;
-  });
-}
-
-// dispatch on the number of occupied levels
-#define GPULSM_NL_CASES(M) \
-  M(1) M(2) M(3) M(4) M(5) M(6) M(7) M(8) M(9) M(10) M(11) M(12) M(13) M(14) M(15) M(16)
-
-template <typename... Args>
-void launch_count_nl(int nl, dim3 g, dim3 b, cudaStream_t s, Args... args) {
-  switch (nl) {
-#define GPULSM_C(N) \
-  case N:          \
-    count_kernel<N><<<g, b, 0, s>>>(args...); \
-    return;
-    GPULSM_NL_CASES(GPULSM_C)
-#undef GPULSM_C
-    default:
-      count_kernel<0><<<g, b, 0, s>>>(args...);
+  extern __shared__ uint32_t sF3[];
+  stage_f3(T, sF3);
+  constexpr int CAP = NL > 0 ? NL : LSM_MAX_LEVELS;
+  const int L = NL > 0 ? NL : T.count;
+  const uint32_t lane = lane_id();
+  const uint64_t gw = ((uint64_t)blockIdx.x * kQThreads + threadIdx.x) / 32;
+  const uint64_t nw = (uint64_t)gridDim.x * kQThreads / 32;
+  for (uint64_t base = gw * 32; base < nq; base += nw * 32) {
+    const uint64_t i = base + lane;
+    const bool act = i < nq;
+    const uint32_t a = act ? __ldg(k1 + i) : 1u, z = act ? __ldg(k2 + i) : 0u;
+    uint64_t pos[CAP], end[CAP];
+    bounds<NL>(T, sF3, a, z, a > z, pos, end, L);
+    const uint64_t o = act ? offsets[i] : 0;
+    walk_slices<NL>(T, pos, end, L, [&](uint32_t c, uint32_t key, uint32_t val) {
+      keys_out[o + c] = key;
+      vals_out[o + c] = val;
+    });
   }
 }
 
-template <typename... Args>
-void launch_range_nl(int nl, dim3 g, dim3 b, cudaStream_t s, Args... args) {
-  switch (nl) {
-#define GPULSM_R(N) \
-  case N:          \
-    range_write_kernel<N><<<g, b, 0, s>>>(args...); \
-    return;
-    GPULSM_NL_CASES(GPULSM_R)
-#undef GPULSM_R
-    default:
-      range_write_kernel<0><<<g, b, 0, s>>>(args...);
+int g_sms = 0;
+
+unsigned query_grid(uint64_t nq) {
+  if (g_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
   }
+  const uint64_t warps = (nq + 31) / 32;
+  const uint64_t want = (warps + kQThreads / 32 - 1) / (kQThreads / 32);
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)g_sms * kQCtasPerSm));
 }
 
-// ---------------------------- exclusive scan -------------------------------
-constexpr int kScanThreads = 256;
-constexpr int kScanItems = 16;
-constexpr int kScanTile = kScanThreads * kScanItems;
-
-__global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(const uint32_t* __restrict__ c,
-                                                                   uint64_t n,
-                                                                   uint64_t* __restrict__ sums) {
-  __shared__ uint64_t tmp[kScanThreads / 32 + 1];
-  const uint64_t base = (uint64_t)blockIdx.x * kScanTile + threadIdx.x * kScanItems;
-  uint64_t s = 0;
-#pragma unroll
-  for (int k = 0; k < kScanItems; ++k)
-    if (base + k < n) s += c[base + k];
-  uint64_t tot;
-  block_exclusive_scan<kScanThreads, uint64_t>(s, tmp, &tot);
-  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+template <typename K>
+cudaError_t set_smem(K kern) {
+  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(kF3SmemMax * 4));
 }
 
-__global__ void __launch_bounds__(1024) scan_top_kernel(uint64_t* __restrict__ sums, uint64_t nb,
-                                                        uint64_t* __restrict__ total_out) {
-  __shared__ uint64_t tmp[1024 / 32 + 1];
-  uint64_t carry = 0;
-  for (uint64_t base = 0; base < nb; base += 1024) {
-    const uint64_t i = base + threadIdx.x;
-    const uint64_t v = i < nb ? sums[i] : 0;
-    uint64_t tot;
-    const uint64_t ex = block_exclusive_scan<1024, uint64_t>(v, tmp, &tot);
-    if (i < nb) sums[i] = carry + ex;
-    carry += tot;
+constexpr int kMaxUnrolled = 8;
+
+template <int N>
+struct CountLauncher {
+  static cudaError_t go(int nl, unsigned g, cudaStream_t s, size_t smem, const LevelTable& T,
+                        const uint32_t* k1, const uint32_t* k2, uint64_t nq, uint32_t* out) {
+    if (nl == N) {
+      static bool attr = false;
+      if (!attr) {
+        cudaError_t e = set_smem(count_kernel<N>);
+        if (e != cudaSuccess) return e;
+        attr = true;
+      }
+      count_kernel<N><<<g, kQThreads, smem, s>>>(T, k1, k2, nq, out);
+      return cudaGetLastError();
+    }
+    return CountLauncher<N - 1>::go(nl, g, s, smem, T, k1, k2, nq, out);
   }
-  if (threadIdx.x == 0) *total_out = carry;
-}
-
-__global__ void __launch_bounds__(kScanThreads) scan_down_kernel(const uint32_t* __restrict__ c,
-                                                                 uint64_t n,
-                                                                 const uint64_t* __restrict__ sums,
-                                                                 uint64_t* __restrict__ off) {
-  __shared__ uint64_t tmp[kScanThreads / 32 + 1];
-  const uint64_t base = (uint64_t)blockIdx.x * kScanTile + threadIdx.x * kScanItems;
-  uint32_t v[kScanItems];
-  uint64_t s = 0;
-#pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    v[k] = base + k < n ? c[base + k] : 0u;
-    s += v[k];
+};
+template <>
+struct CountLauncher<0> {
+  static cudaError_t go(int, unsigned g, cudaStream_t s, size_t smem, const LevelTable& T,
+                        const uint32_t* k1, const uint32_t* k2, uint64_t nq, uint32_t* out) {
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = set_smem(count_kernel<0>);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    count_kernel<0><<<g, kQThreads, smem, s>>>(T, k1, k2, nq, out);
+    return cudaGetLastError();
   }
-  uint64_t tot;
-  uint64_t ex = block_exclusive_scan<kScanThreads, uint64_t>(s, tmp, &tot) + sums[blockIdx.x];
-#pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    if (base + k < n) off[base + k] = ex;
-    ex += v[k];
-  }
-}
+};
 
-inline unsigned grid_for(uint64_t n, int per_block) {
-  return (unsigned)((n + per_block - 1) / per_block);
-}
+template <int N>
+struct RangeLauncher {
+  static cudaError_t go(int nl, unsigned g, cudaStream_t s, size_t smem, const LevelTable& T,
+                        const uint32_t* k1, const uint32_t* k2, uint64_t nq, const uint64_t* off,
+                        uint32_t* ko, uint32_t* vo) {
+    if (nl == N) {
+      static bool attr = false;
+      if (!attr) {
+        cudaError_t e = set_smem(range_write_kernel<N>);
+        if (e != cudaSuccess) return e;
+        attr = true;
+      }
+      range_write_kernel<N><<<g, kQThreads, smem, s>>>(T, k1, k2, nq, off, ko, vo);
+      return cudaGetLastError();
+    }
+    return RangeLauncher<N - 1>::go(nl, g, s, smem, T, k1, k2, nq, off, ko, vo);
+  }
+};
+template <>
+struct RangeLauncher<0> {
+  static cudaError_t go(int, unsigned g, cudaStream_t s, size_t smem, const LevelTable& T,
+                        const uint32_t* k1, const uint32_t* k2, uint64_t nq, const uint64_t* off,
+                        uint32_t* ko, uint32_t* vo) {
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = set_smem(range_write_kernel<0>);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    range_write_kernel<0><<<g, kQThreads, smem, s>>>(T, k1, k2, nq, off, ko, vo);
+    return cudaGetLastError();
+  }
+};
 
 }  // namespace
+
+int device_sms() {
+  query_grid(1);
+  return g_sms;
+}
 
 cudaError_t launch_lookup(const LevelTable& T, const uint32_t* q, uint64_t nq,
                           uint32_t* vals_out, uint8_t* found_out, cudaStream_t s,
                           const LaunchHooks& hk) {
   if (nq == 0) return cudaSuccess;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = set_smem(lookup_kernel);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
   hk.begin(hk.ctx, LSM_K_LOOKUP, s);
-  lookup_kernel<<<grid_for(nq, kQThreads), kQThreads, 0, s>>>(T, q, nq, vals_out, found_out);
-  // algorithmic bytes per query: 4 B in, 5 B out, one 32 B
-  // sector per searched level is accounted by the caller's level count.
+  lookup_kernel<<<query_grid(nq), kQThreads, T.f3_smem_total * 4, s>>>(T, q, nq, vals_out,
+                                                                       found_out);
+  // algorithmic bytes per query: 4 B in + 5 B out, and per
+  // searched level one 32 B sector of keys (the fence lines are L2-resident)
   hk.end(hk.ctx, LSM_K_LOOKUP, (double)nq * (9.0 + 32.0 * T.count), s, 1);
   return cudaGetLastError();
 }
@@ -259,38 +482,29 @@ cudaError_t launch_count(const LevelTable& T, const uint32_t* k1, const uint32_t
                          const LaunchHooks& hk, int cls) {
   if (nq == 0) return cudaSuccess;
   hk.begin(hk.ctx, cls, s);
+  cudaError_t e;
   if (T.count == 0) {
-    cudaMemsetAsync(counts_out, 0, nq * 4, s);
+    e = cudaMemsetAsync(counts_out, 0, nq * 4, s);
   } else {
-    launch_count_nl(T.count, grid_for(nq, kQThreads), kQThreads, s, T, k1, k2, nq, counts_out);
+    const int nl = T.count <= kMaxUnrolled ? T.count : 0;
+    e = CountLauncher<kMaxUnrolled>::go(nl, query_grid(nq), s, T.f3_smem_total * 4, T, k1, k2, nq,
+                                        counts_out);
   }
+  // 8 B in, 4 B out, two 32 B key sectors per level
   hk.end(hk.ctx, cls, (double)nq * (12.0 + 64.0 * T.count), s, 1);
-  return cudaGetLastError();
-}
-
-uint64_t scan_scratch_words(uint64_t n) { return (n + kScanTile - 1) / kScanTile + 1; }
-
-cudaError_t launch_scan(const uint32_t* counts, uint64_t n, uint64_t* offsets,
-                        uint64_t* block_sums, cudaStream_t s, const LaunchHooks& hk) {
-  const uint64_t nb = (n + kScanTile - 1) / kScanTile;
-  hk.begin(hk.ctx, LSM_K_SCAN, s);
-  if (nb > 0) scan_reduce_kernel<<<(unsigned)nb, kScanThreads, 0, s>>>(counts, n, block_sums);
-  scan_top_kernel<<<1, 1024, 0, s>>>(block_sums, nb, offsets + n);
-  if (nb > 0) scan_down_kernel<<<(unsigned)nb, kScanThreads, 0, s>>>(counts, n, block_sums, offsets);
-  hk.end(hk.ctx, LSM_K_SCAN, (double)n * 16.0, s, 3);
-  return cudaGetLastError();
+  return e;
 }
 
 cudaError_t launch_range_write(const LevelTable& T, const uint32_t* k1, const uint32_t* k2,
                                uint64_t nq, const uint64_t* offsets, uint32_t* keys_out,
                                uint32_t* vals_out, cudaStream_t s, const LaunchHooks& hk) {
-  if (nq == 0) return cudaSuccess;
+  if (nq == 0 || T.count == 0) return cudaSuccess;
   hk.begin(hk.ctx, LSM_K_RANGE, s);
-  if (T.count > 0)
-    launch_range_nl(T.count, grid_for(nq, kQThreads), kQThreads, s, T, k1, k2, nq, offsets,
-                    keys_out, vals_out);
+  const int nl = T.count <= kMaxUnrolled ? T.count : 0;
+  cudaError_t e = RangeLauncher<kMaxUnrolled>::go(nl, query_grid(nq), s, T.f3_smem_total * 4, T,
+                                                  k1, k2, nq, offsets, keys_out, vals_out);
   hk.end(hk.ctx, LSM_K_RANGE, (double)nq * (16.0 + 64.0 * T.count), s, 1);
-  return cudaGetLastError();
+  return e;
 }
 
 }  // namespace gpulsm

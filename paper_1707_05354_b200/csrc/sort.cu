@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(kSortThreads, 1) onesweep_pass_kernel(
     uint32_t* __restrict__ out_keys, uint32_t* __restrict__ out_vals, uint64_t b,
     const uint32_t* __restrict__ dbase, uint32_t* __restrict__ tile_st,
     uint32_t* __restrict__ group_st, uint32_t* __restrict__ tile_ctr, int use_ctr, int shift,
-    uint32_t* __restrict__ err, uint32_t epoch) {
+    uint32_t* __restrict__ err, uint32_t epoch, uint32_t* __restrict__ out_f1) {
   // use_ctr == 0 <=> all tiles are co-resident (one wave): the digit bases
   // then come from the totals of ALL groups (no histogram kernel)
   extern __shared__ __align__(16) uint8_t pass_smem[];
@@ -436,6 +436,7 @@ __global__ void __launch_bounds__(kSortThreads, 1) onesweep_pass_kernel(
       const uint32_t pos = S.goff[(key >> shift) & (kRadix - 1)] + idx;
       out_keys[pos] = key;
       out_vals[pos] = S.vals[idx];
+      if (out_f1 != nullptr && (pos & (kF1Step - 1)) == 0) out_f1[pos / kF1Step] = key;
     }
   }
   PROBE(7);
@@ -449,7 +450,7 @@ bool g_attr = false;
 cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals,
                               const uint8_t* ops, int mode, uint64_t n, uint64_t b,
                               SortScratch& S, uint32_t* out_keys, uint32_t* out_vals,
-                              cudaStream_t s, const LaunchHooks& hk) {
+                              uint32_t* out_f1, cudaStream_t s, const LaunchHooks& hk) {
   if (!g_attr) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -503,11 +504,13 @@ cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals
     if (p == 0)
       e = launch_pdl(onesweep_pass_kernel<true>, (unsigned)tiles, kSortThreads, sizeof(PassSmem), s,
                      in, (const uint32_t*)nullptr, (const uint32_t*)nullptr, ok, ov, b,
-                     (const uint32_t*)S.bases, ts, gs, S.tile_ctr + p, use_ctr, 0, S.err, epoch);
+                     (const uint32_t*)S.bases, ts, gs, S.tile_ctr + p, use_ctr, 0, S.err, epoch,
+                     (uint32_t*)(p == kPasses - 1 ? out_f1 : nullptr));
     else
       e = launch_pdl(onesweep_pass_kernel<false>, (unsigned)tiles, kSortThreads, sizeof(PassSmem),
                      s, in, ik, iv, ok, ov, b, (const uint32_t*)(S.bases + p * kRadix), ts, gs,
-                     S.tile_ctr + p, use_ctr, p * kRadixBits, S.err, epoch);
+                     S.tile_ctr + p, use_ctr, p * kRadixBits, S.err, epoch,
+                     (uint32_t*)(p == kPasses - 1 ? out_f1 : nullptr));
     // bytes: pass 0 reads raw (k,v,op = 9 B) writes 8 B; others 16 B
     hk.end(hk.ctx, LSM_K_SORT_PASS, (double)b * (p == 0 ? 17.0 : 16.0), s, 1);
     if (e != cudaSuccess) return e;
