@@ -148,8 +148,10 @@ lsm_status lsm_count(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2, uint6
  * per-query counts), then the pairs of query q at [offsets[q], offsets[q+1])
  * in d_keys_out (original keys) / d_vals_out, ascending by key.
  * *total_out (HOST) receives the total number of pairs. If total > capacity
- * the offsets are written, no pairs are, and LSM_ERR_CAPACITY is returned
- * (retry with a larger buffer). Synchronises `stream`.                      */
+ * the offsets are written, only pairs at positions < capacity are, and
+ * LSM_ERR_CAPACITY is returned (retry with a larger buffer). One kernel:
+ * per-level bounds, a counting walk, offsets by a warp scan + decoupled
+ * look-back, a writing walk. Synchronises `stream`.                         */
 lsm_status lsm_range(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2, uint64_t nq,
                      uint64_t* d_offsets_out, uint32_t* d_keys_out, uint32_t* d_vals_out,
                      uint64_t capacity, uint64_t* total_out, void* stream);

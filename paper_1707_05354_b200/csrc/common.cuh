@@ -264,9 +264,13 @@ uint64_t scan_scratch_words(uint64_t n);
 cudaError_t launch_scan(const uint32_t* counts, uint64_t n, uint64_t* offsets,
                         uint64_t* block_sums, cudaStream_t s, const LaunchHooks& hk);
 
-cudaError_t launch_range_write(const LevelTable& T, const uint32_t* k1, const uint32_t* k2,
-                               uint64_t nq, const uint64_t* offsets, uint32_t* keys_out,
-                               uint32_t* vals_out, cudaStream_t s, const LaunchHooks& hk);
+// Single-pass range: offsets[nq+1] and the pairs (written while < capacity);
+// scratch: range_scratch_words(nq) u64 (zeroed by the launcher).
+uint64_t range_scratch_words(uint64_t nq);
+cudaError_t launch_range(const LevelTable& T, const uint32_t* k1, const uint32_t* k2,
+                         uint64_t nq, uint64_t* offsets, uint32_t* keys_out, uint32_t* vals_out,
+                         uint64_t capacity, unsigned long long* scratch, cudaStream_t s,
+                         const LaunchHooks& hk);
 
 // Cleanup: valid = regular && first of its key run in M; compact into C.
 // tile_counts: cleanup_tiles(n) u32; offsets: cleanup_tiles(n)+1 u64.

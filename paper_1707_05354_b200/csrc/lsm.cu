@@ -515,23 +515,18 @@ lsm_status lsm_range(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2, uint6
   }
   if (!d_k1 || !d_k2) return LSM_ERR_INVALID_ARG;
   LaunchHooks hk = hooks(h);
-  const uint64_t cbytes = align_up(nq * 4, 256);
-  const uint64_t sbytes = scan_scratch_words(nq) * 8;
-  CK(ensure_qbuf(h, cbytes + sbytes, s));
-  uint32_t* counts = static_cast<uint32_t*>(h->qbuf);
-  uint64_t* sums = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(h->qbuf) + cbytes);
+  if (capacity > 0 && (!d_keys_out || !d_vals_out)) return LSM_ERR_INVALID_ARG;
+  CK(ensure_qbuf(h, range_scratch_words(nq) * 8, s));
   CK(ensure_index(h, s, hk));
   LevelTable T = level_table(h);
-  CK(launch_count(T, d_k1, d_k2, nq, counts, s, hk, LSM_K_COUNT));
-  CK(launch_scan(counts, nq, d_offsets_out, sums, s, hk));
+  // one pass: bounds, count, warp scan + look-back offsets, pairs
+  CK(launch_range(T, d_k1, d_k2, nq, d_offsets_out, d_keys_out, d_vals_out, capacity,
+                  static_cast<unsigned long long*>(h->qbuf), s, hk));
   CK(cudaMemcpyAsync(h->h_pinned, d_offsets_out + nq, 8, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   const uint64_t total = h->h_pinned[0];
   *total_out = total;
   if (total > capacity) return LSM_ERR_CAPACITY;
-  if (total > 0 && (!d_keys_out || !d_vals_out)) return LSM_ERR_INVALID_ARG;
-  if (total > 0)
-    CK(launch_range_write(T, d_k1, d_k2, nq, d_offsets_out, d_keys_out, d_vals_out, s, hk));
   return LSM_OK;
 }
 

@@ -338,28 +338,101 @@ __global__ void __launch_bounds__(kQThreads, 1) count_kernel(
   }
 }
 
+// ---- single-pass range ----
+// Warps claim tasks of 32 consecutive queries in order; after counting, a
+// warp publishes its task total and finds the total of all earlier tasks by
+// a warp-wide decoupled look-back (32 predecessors per round trip), so the
+// per-query offsets (the paper's stage-2 scan) come out of
+// the same kernel, and the pairs are emitted by a second walk from the saved
+// bounds -- no second search, no separate scan launch.
+constexpr uint64_t kAgg = 1ull << 62;
+constexpr uint64_t kPre = 2ull << 62;
+constexpr uint64_t kVal62 = kAgg - 1;
+
+__device__ __forceinline__ uint64_t ld_cg64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint64_t warp_sum64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// exclusive prefix of the totals of tasks [0, t)
+__device__ __forceinline__ uint64_t task_lookback(unsigned long long* status, uint64_t t,
+                                                  uint64_t mine) {
+  const uint32_t lane = lane_id();
+  if (lane == 0) atomicExch(status + t, (unsigned long long)((t == 0 ? kPre : kAgg) | mine));
+  uint64_t excl = 0;
+  int64_t j = (int64_t)t - 1;
+  while (j >= 0) {
+    const int64_t idx = j - (int64_t)lane;
+    uint64_t w = idx >= 0 ? ld_cg64(status + idx) : kPre;
+    while (__any_sync(kFull, (w >> 62) == 0)) {  // wait for every predecessor in the window
+      __nanosleep(32);
+      if ((w >> 62) == 0) w = ld_cg64(status + idx);
+    }
+    const uint32_t pre = __ballot_sync(kFull, (w >> 62) == 2);
+    if (pre) {
+      const int k = __ffs(pre) - 1;  // nearest task with an inclusive prefix
+      excl += warp_sum64((int)lane <= k ? (w & kVal62) : 0ull);
+      break;
+    }
+    excl += warp_sum64(w & kVal62);
+    j -= 32;
+  }
+  if (lane == 0 && t > 0) atomicExch(status + t, (unsigned long long)(kPre | (excl + mine)));
+  return excl;
+}
+
 template <int NL>
-__global__ void __launch_bounds__(kQThreads, 1) range_write_kernel(
+__global__ void __launch_bounds__(kQThreads, 1) range_kernel(
     LevelTable T, const uint32_t* __restrict__ k1, const uint32_t* __restrict__ k2, uint64_t nq,
-    const uint64_t* __restrict__ offsets, uint32_t* __restrict__ keys_out,
-    uint32_t* __restrict__ vals_out) {
+    uint64_t* __restrict__ offsets, uint32_t* __restrict__ keys_out,
+    uint32_t* __restrict__ vals_out, uint64_t capacity, unsigned long long* __restrict__ ctr,
+    unsigned long long* __restrict__ status) {
   extern __shared__ uint32_t sF3[];
   stage_f3(T, sF3);
   constexpr int CAP = NL > 0 ? NL : LSM_MAX_LEVELS;
   const int L = NL > 0 ? NL : T.count;
   const uint32_t lane = lane_id();
+  const uint64_t ntasks = (nq + 31) / 32;
+  // static assignment: warp w takes tasks w, w + nw, ... in increasing order.
+  // The grid is fully co-resident (sized from the occupancy), so the
+  // smallest unfinished task never waits on a task that has not started.
+  (void)ctr;
   const uint64_t gw = ((uint64_t)blockIdx.x * kQThreads + threadIdx.x) / 32;
   const uint64_t nw = (uint64_t)gridDim.x * kQThreads / 32;
-  for (uint64_t base = gw * 32; base < nq; base += nw * 32) {
-    const uint64_t i = base + lane;
+  for (uint64_t t = gw; t < ntasks; t += nw) {
+    const uint64_t i = t * 32 + lane;
     const bool act = i < nq;
     const uint32_t a = act ? __ldg(k1 + i) : 1u, z = act ? __ldg(k2 + i) : 0u;
-    uint64_t pos[CAP], end[CAP];
+    uint64_t pos[CAP], end[CAP], pos0[CAP];
     bounds<NL>(T, sF3, a, z, a > z, pos, end, L);
-    const uint64_t o = act ? offsets[i] : 0;
-    walk_slices<NL>(T, pos, end, L, [&](uint32_t c, uint32_t key, uint32_t val) {
-      keys_out[o + c] = key;
-      vals_out[o + c] = val;
+#pragma unroll
+    for (int j = 0; j < CAP; ++j)
+      if (j < L) pos0[j] = pos[j];
+    const uint32_t c = walk_slices<NL>(T, pos, end, L, [](uint32_t, uint32_t, uint32_t) {});
+    // warp exclusive scan of the counts
+    uint64_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(kFull, x, o);
+      if ((int)lane >= o) x += y;
+    }
+    const uint64_t wtot = __shfl_sync(kFull, x, 31);
+    const uint64_t base = task_lookback(status, t, wtot) + x - c;
+    if (act) offsets[i] = base;
+    if (t == ntasks - 1 && lane == 31) offsets[nq] = base + c;
+    walk_slices<NL>(T, pos0, end, L, [&](uint32_t k, uint32_t key, uint32_t val) {
+      const uint64_t o = base + k;
+      if (o < capacity) {
+        keys_out[o] = key;
+        vals_out[o] = val;
+      }
     });
   }
 }
@@ -375,6 +448,17 @@ unsigned query_grid(uint64_t nq) {
   const uint64_t warps = (nq + 31) / 32;
   const uint64_t want = (warps + kQThreads / 32 - 1) / (kQThreads / 32);
   return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)g_sms * kQCtasPerSm));
+}
+
+// CTAs that fit on the whole GPU at once for this kernel and smem size
+template <typename K>
+unsigned occ_grid(K kern, size_t smem) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kQThreads, smem) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  query_grid(1);
+  return (unsigned)(per_sm * g_sms);
 }
 
 template <typename K>
@@ -396,6 +480,7 @@ struct CountLauncher {
         if (e != cudaSuccess) return e;
         attr = true;
       }
+      g = std::min(g, occ_grid(count_kernel<N>, smem));
       count_kernel<N><<<g, kQThreads, smem, s>>>(T, k1, k2, nq, out);
       return cudaGetLastError();
     }
@@ -412,6 +497,7 @@ struct CountLauncher<0> {
       if (e != cudaSuccess) return e;
       attr = true;
     }
+    g = std::min(g, occ_grid(count_kernel<0>, smem));
     count_kernel<0><<<g, kQThreads, smem, s>>>(T, k1, k2, nq, out);
     return cudaGetLastError();
   }
@@ -420,33 +506,35 @@ struct CountLauncher<0> {
 template <int N>
 struct RangeLauncher {
   static cudaError_t go(int nl, unsigned g, cudaStream_t s, size_t smem, const LevelTable& T,
-                        const uint32_t* k1, const uint32_t* k2, uint64_t nq, const uint64_t* off,
-                        uint32_t* ko, uint32_t* vo) {
+                        const uint32_t* k1, const uint32_t* k2, uint64_t nq, uint64_t* off,
+                        uint32_t* ko, uint32_t* vo, uint64_t cap, unsigned long long* scr) {
     if (nl == N) {
       static bool attr = false;
       if (!attr) {
-        cudaError_t e = set_smem(range_write_kernel<N>);
+        cudaError_t e = set_smem(range_kernel<N>);
         if (e != cudaSuccess) return e;
         attr = true;
       }
-      range_write_kernel<N><<<g, kQThreads, smem, s>>>(T, k1, k2, nq, off, ko, vo);
+      g = occ_grid(range_kernel<N>, smem);
+      range_kernel<N><<<g, kQThreads, smem, s>>>(T, k1, k2, nq, off, ko, vo, cap, scr, scr + 1);
       return cudaGetLastError();
     }
-    return RangeLauncher<N - 1>::go(nl, g, s, smem, T, k1, k2, nq, off, ko, vo);
+    return RangeLauncher<N - 1>::go(nl, g, s, smem, T, k1, k2, nq, off, ko, vo, cap, scr);
   }
 };
 template <>
 struct RangeLauncher<0> {
   static cudaError_t go(int, unsigned g, cudaStream_t s, size_t smem, const LevelTable& T,
-                        const uint32_t* k1, const uint32_t* k2, uint64_t nq, const uint64_t* off,
-                        uint32_t* ko, uint32_t* vo) {
+                        const uint32_t* k1, const uint32_t* k2, uint64_t nq, uint64_t* off,
+                        uint32_t* ko, uint32_t* vo, uint64_t cap, unsigned long long* scr) {
     static bool attr = false;
     if (!attr) {
-      cudaError_t e = set_smem(range_write_kernel<0>);
+      cudaError_t e = set_smem(range_kernel<0>);
       if (e != cudaSuccess) return e;
       attr = true;
     }
-    range_write_kernel<0><<<g, kQThreads, smem, s>>>(T, k1, k2, nq, off, ko, vo);
+    g = occ_grid(range_kernel<0>, smem);
+    range_kernel<0><<<g, kQThreads, smem, s>>>(T, k1, k2, nq, off, ko, vo, cap, scr, scr + 1);
     return cudaGetLastError();
   }
 };
@@ -469,8 +557,8 @@ cudaError_t launch_lookup(const LevelTable& T, const uint32_t* q, uint64_t nq,
     attr = true;
   }
   hk.begin(hk.ctx, LSM_K_LOOKUP, s);
-  lookup_kernel<<<query_grid(nq), kQThreads, T.f3_smem_total * 4, s>>>(T, q, nq, vals_out,
-                                                                       found_out);
+  const unsigned g = std::min(query_grid(nq), occ_grid(lookup_kernel, T.f3_smem_total * 4));
+  lookup_kernel<<<g, kQThreads, T.f3_smem_total * 4, s>>>(T, q, nq, vals_out, found_out);
   // algorithmic bytes per query: 4 B in + 5 B out, and per
   // searched level one 32 B sector of keys (the fence lines are L2-resident)
   hk.end(hk.ctx, LSM_K_LOOKUP, (double)nq * (9.0 + 32.0 * T.count), s, 1);
@@ -495,14 +583,26 @@ cudaError_t launch_count(const LevelTable& T, const uint32_t* k1, const uint32_t
   return e;
 }
 
-cudaError_t launch_range_write(const LevelTable& T, const uint32_t* k1, const uint32_t* k2,
-                               uint64_t nq, const uint64_t* offsets, uint32_t* keys_out,
-                               uint32_t* vals_out, cudaStream_t s, const LaunchHooks& hk) {
-  if (nq == 0 || T.count == 0) return cudaSuccess;
+uint64_t range_scratch_words(uint64_t nq) { return 1 + (nq + 31) / 32; }
+
+cudaError_t launch_range(const LevelTable& T, const uint32_t* k1, const uint32_t* k2,
+                         uint64_t nq, uint64_t* offsets, uint32_t* keys_out, uint32_t* vals_out,
+                         uint64_t capacity, unsigned long long* scratch, cudaStream_t s,
+                         const LaunchHooks& hk) {
+  if (nq == 0) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(scratch, 0, range_scratch_words(nq) * 8, s);
+  if (e != cudaSuccess) return e;
   hk.begin(hk.ctx, LSM_K_RANGE, s);
-  const int nl = T.count <= kMaxUnrolled ? T.count : 0;
-  cudaError_t e = RangeLauncher<kMaxUnrolled>::go(nl, query_grid(nq), s, T.f3_smem_total * 4, T,
-                                                  k1, k2, nq, offsets, keys_out, vals_out);
+  if (T.count == 0) {
+    e = cudaMemsetAsync(offsets, 0, (nq + 1) * 8, s);
+  } else {
+    const int nl = T.count <= kMaxUnrolled ? T.count : 0;
+    e = RangeLauncher<kMaxUnrolled>::go(nl, (unsigned)std::max(1, device_sms()), s,
+                                        T.f3_smem_total * 4, T, k1, k2, nq, offsets, keys_out,
+                                        vals_out, capacity, scratch);
+  }
+  // 8 B in, 8 B offset out, two 32 B key sectors per level; pairs are
+  // accounted with their 8 B each by the caller's count
   hk.end(hk.ctx, LSM_K_RANGE, (double)nq * (16.0 + 64.0 * T.count), s, 1);
   return e;
 }
