@@ -177,6 +177,10 @@ struct SortScratch {
   uint64_t tiles_cap;     // status capacity in tiles
   int parity;             // which hist half this sort uses
   uint32_t epoch;         // sort counter -> look-back word epochs
+  uint32_t* bkt;          // [2][256] bucket starts / sizes (MSD + local mode)
+  uint32_t* overflow_dev; // mapped host word: a bucket overflowed shared memory
+  volatile uint32_t* overflow_host;
+  bool lsd_only;          // skewed keys seen: use the 4-pass LSD path
 };
 
 // one fat tile per SM: 1024 threads x 7 records (b = 2^20 -> 147 tiles)

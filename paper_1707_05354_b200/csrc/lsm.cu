@@ -178,8 +178,9 @@ cudaError_t home_idx_ensure(lsm* h, int i, cudaStream_t s) {
 
 cudaError_t ensure_sort_scratch(lsm* h, cudaStream_t s) {
   if (h->sort_meta == nullptr) {
-    // hist[2][4][256] | bases[4][256] | tile_ctr[4] | err | done | pad | status
-    const uint64_t head = 3 * kPasses * kRadix + 16;
+    // hist[2][4][256] | bases[4][256] | tile_ctr[4] | err | done | pad |
+    // bkt[2][256] | status
+    const uint64_t head = 3 * kPasses * kRadix + 16 + 2 * kRadix;
     h->sort_meta_words = head + sort_status_words(h->b);
     cudaError_t e = pool_alloc(h, (void**)&h->sort_meta, h->sort_meta_words * 4, s);
     if (e != cudaSuccess) return e;
@@ -190,7 +191,18 @@ cudaError_t ensure_sort_scratch(lsm* h, cudaStream_t s) {
     h->sort.tile_ctr = h->sort_meta + 3 * kPasses * kRadix;
     h->sort.err = h->sort.tile_ctr + 4;
     h->sort.done_ctr = h->sort.tile_ctr + 5;
+    h->sort.bkt = h->sort_meta + 3 * kPasses * kRadix + 16;
     h->sort.status = h->sort_meta + head;
+    // overflow flag of the MSD + local sort: a mapped host word, so the host
+    // reads it without a copy or a sync
+    uint32_t* hp = nullptr;
+    e = cudaHostAlloc((void**)&hp, 64, cudaHostAllocMapped);
+    if (e != cudaSuccess) return e;
+    *hp = 0;
+    e = cudaHostGetDevicePointer((void**)&h->sort.overflow_dev, hp, 0);
+    if (e != cudaSuccess) return e;
+    h->sort.overflow_host = hp;
+    h->sort.lsd_only = false;
     h->sort.tiles_cap = sort_tiles(h->b);
     for (int k = 0; k < 2; ++k) {
       e = pool_alloc(h, (void**)&h->sort.tmp_keys[k], h->b * 4, s);
@@ -345,6 +357,7 @@ lsm_status lsm_destroy(lsm_t* h) {
   }
   for (auto e : h->ev_free) cudaEventDestroy(e);
   if (h->h_pinned) cudaFreeHost(h->h_pinned);
+  if (h->sort.overflow_host) cudaFreeHost((void*)h->sort.overflow_host);
   cudaMemPoolDestroy(h->pool);
   delete h;
   return LSM_OK;

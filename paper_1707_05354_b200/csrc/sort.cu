@@ -250,7 +250,8 @@ __global__ void __launch_bounds__(kSortThreads, 1) onesweep_pass_kernel(
     uint32_t* __restrict__ out_keys, uint32_t* __restrict__ out_vals, uint64_t b,
     const uint32_t* __restrict__ dbase, uint32_t* __restrict__ tile_st,
     uint32_t* __restrict__ group_st, uint32_t* __restrict__ tile_ctr, int use_ctr, int shift,
-    uint32_t* __restrict__ err, uint32_t epoch, uint32_t* __restrict__ out_f1) {
+    uint32_t* __restrict__ err, uint32_t epoch, uint32_t* __restrict__ out_f1,
+    uint32_t* __restrict__ bkt_out) {
   // use_ctr == 0 <=> all tiles are co-resident (one wave): the digit bases
   // then come from the totals of ALL groups (no histogram kernel)
   extern __shared__ __align__(16) uint8_t pass_smem[];
@@ -422,6 +423,11 @@ __global__ void __launch_bounds__(kSortThreads, 1) onesweep_pass_kernel(
   } else {  // exclusive scan of the global digit totals
     uint32_t t2;
     base = block_exclusive_scan<kSortThreads, uint32_t>(total, S.scan, &t2);
+    // MSD mode: publish the bucket (digit) starts and sizes for pass B
+    if (bkt_out != nullptr && tile == 0 && tid < kRadix) {
+      bkt_out[tid] = base;
+      bkt_out[kRadix + tid] = total;
+    }
   }
   if (tid < kRadix) S.goff[tid] = base + gp + wp - tstart;
   __syncthreads();
@@ -440,6 +446,225 @@ __global__ void __launch_bounds__(kSortThreads, 1) onesweep_pass_kernel(
     }
   }
   PROBE(7);
+}
+
+// ---------------------------------------------------------------------------
+// CTA-local stable LSD (MSD + local mode). One sub-pass moves
+// n <= T*ITEMS records from (sk, sv) to (dk, dv) ordered by the 8-bit digit
+// at `shift`, stably: ballot ranks + per-warp counters, a block scan of the
+// digit counts, a scatter. `gbase` (optional, shared) adds a running offset
+// per digit and `gout` selects global destination pointers (the chunked
+// fallback for oversized buckets). Pointers may be shared or global.
+// ---------------------------------------------------------------------------
+template <int T>
+struct LocalScratch {
+  uint32_t whist[T / 32][kRadix];
+  uint32_t tstart[kRadix];
+  uint32_t cnt[kRadix];
+  uint32_t scan[T / 32 + 1];
+};
+
+template <int T, int ITEMS>
+__device__ __forceinline__ void local_subpass(const uint32_t* sk, const uint32_t* sv, uint32_t n,
+                                              uint32_t* dk, uint32_t* dv, int shift,
+                                              LocalScratch<T>& L, const uint32_t* gbase) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < (T / 32) * kRadix; i += T) (&L.whist[0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t wbase = warp * (32 * ITEMS);
+  uint32_t k[ITEMS], v[ITEMS], rk[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const uint32_t p = wbase + i * 32 + lane;
+    k[i] = p < n ? sk[p] : 0u;
+    v[i] = p < n ? sv[p] : 0u;
+  }
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const bool valid = wbase + i * 32 + lane < n;
+    const uint32_t d = (k[i] >> shift) & (kRadix - 1);
+    const uint32_t peers = digit_peers(d, valid);
+    const int leader = __ffs(peers) - 1;
+    uint32_t old = 0;
+    if (valid && lane == leader) {
+      old = L.whist[warp][d];
+      L.whist[warp][d] = old + __popc(peers);
+    }
+    old = __shfl_sync(kFull, old, leader < 0 ? 0 : leader);
+    rk[i] = old + __popc(peers & lt);
+    __syncwarp();
+  }
+  __syncthreads();
+  uint32_t c = 0;
+  if (tid < kRadix) {
+#pragma unroll 8
+    for (int w = 0; w < T / 32; ++w) {
+      const uint32_t x = L.whist[w][tid];
+      L.whist[w][tid] = c;
+      c += x;
+    }
+    L.cnt[tid] = c;
+  }
+  uint32_t tot;
+  const uint32_t ts = block_exclusive_scan<T, uint32_t>(c, L.scan, &tot);
+  if (tid < kRadix) L.tstart[tid] = gbase ? gbase[tid] : ts;
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    if (wbase + i * 32 + lane < n) {
+      const uint32_t d = (k[i] >> shift) & (kRadix - 1);
+      const uint32_t p = L.tstart[d] + L.whist[warp][d] + rk[i];
+      dk[p] = k[i];
+      dv[p] = v[i];
+    }
+  }
+  __syncthreads();
+}
+
+// single-CTA sort of a whole small batch (b <= kSmallCap), all 4 digits
+constexpr int kSmallThreads = 1024;
+constexpr int kSmallItems = 7;
+constexpr int kSmallCap = kSmallThreads * kSmallItems;  // 7168
+
+struct SmallSmem {
+  uint32_t k[2][kSmallCap];
+  uint32_t v[2][kSmallCap];
+  LocalScratch<kSmallThreads> L;
+};
+
+__global__ void __launch_bounds__(kSmallThreads, 1) small_sort_kernel(
+    RawBatch in, uint32_t b, uint32_t* __restrict__ out_keys, uint32_t* __restrict__ out_vals,
+    uint32_t* __restrict__ out_f1, uint32_t* __restrict__ err) {
+  extern __shared__ __align__(16) uint8_t small_smem[];
+  SmallSmem& S = *reinterpret_cast<SmallSmem*>(small_smem);
+  pdl_wait();
+  pdl_trigger();
+  bool any_bad = false;
+  for (uint32_t p = threadIdx.x; p < b; p += kSmallThreads) {  // encode (A1)
+    uint32_t k = 0, v = 0, op = 0;
+    if (p < in.n) {
+      k = __ldg(in.keys + p);
+      v = in.vals ? __ldg(in.vals + p) : 0u;
+      op = in.mode == kModeMixed ? (uint32_t)__ldg(in.ops + p) : 0u;
+    }
+    bool bad;
+    encode_loaded(in, p, k, v, op, S.k[0][p], S.v[0][p], bad);
+    any_bad |= bad;
+  }
+  if (any_bad) atomicOr(err, 1u);
+  __syncthreads();
+  int cur = 0;
+  for (int pass = 0; pass < kPasses; ++pass) {
+    local_subpass<kSmallThreads, kSmallItems>(S.k[cur], S.v[cur], b, S.k[cur ^ 1], S.v[cur ^ 1],
+                                              pass * kRadixBits, S.L, nullptr);
+    cur ^= 1;
+  }
+  for (uint32_t p = threadIdx.x; p < b; p += kSmallThreads) {
+    const uint32_t key = S.k[cur][p];
+    out_keys[p] = key;
+    out_vals[p] = S.v[cur][p];
+    if (out_f1 != nullptr && (p & (kF1Step - 1)) == 0) out_f1[p / kF1Step] = key;
+  }
+}
+
+// pass B of MSD + local: CTA d sorts bucket d (all records whose top digit
+// is d, in input order after pass A) by the lower three digits
+constexpr int kBktThreads = 512;
+constexpr int kBktItems = 11;
+constexpr int kBktCap = kBktThreads * kBktItems;  // 5632
+
+struct BktSmem {
+  uint32_t k[2][kBktCap];
+  uint32_t v[2][kBktCap];
+  LocalScratch<kBktThreads> L;
+  uint32_t run[kRadix];
+  uint32_t hist[kRadix];
+};
+
+__global__ void __launch_bounds__(kBktThreads, 2) bucket_sort_kernel(
+    const uint32_t* __restrict__ bkt, const uint32_t* __restrict__ ak,
+    const uint32_t* __restrict__ av, uint32_t* __restrict__ tk, uint32_t* __restrict__ tv,
+    uint32_t* __restrict__ out_keys, uint32_t* __restrict__ out_vals,
+    uint32_t* __restrict__ out_f1, uint32_t* __restrict__ overflow) {
+  extern __shared__ __align__(16) uint8_t bkt_smem[];
+  BktSmem& S = *reinterpret_cast<BktSmem*>(bkt_smem);
+  const int tid = threadIdx.x;
+  pdl_wait();
+  pdl_trigger();
+  const uint32_t d = blockIdx.x;
+  const uint32_t start = bkt[d], size = bkt[kRadix + d];
+  if (size == 0) return;
+  if (size <= (uint32_t)kBktCap) {
+    for (uint32_t p = tid; p < size; p += kBktThreads) {
+      S.k[0][p] = __ldg(ak + start + p);
+      S.v[0][p] = __ldg(av + start + p);
+    }
+    __syncthreads();
+    int cur = 0;
+    for (int pass = 0; pass < kPasses - 1; ++pass) {
+      local_subpass<kBktThreads, kBktItems>(S.k[cur], S.v[cur], size, S.k[cur ^ 1],
+                                            S.v[cur ^ 1], pass * kRadixBits, S.L, nullptr);
+      cur ^= 1;
+    }
+    for (uint32_t p = tid; p < size; p += kBktThreads) {
+      const uint32_t key = S.k[cur][p];
+      const uint32_t g = start + p;
+      out_keys[g] = key;
+      out_vals[g] = S.v[cur][p];
+      if (out_f1 != nullptr && (g & (kF1Step - 1)) == 0) out_f1[g / kF1Step] = key;
+    }
+    return;
+  }
+  // Oversized bucket (skewed keys): correct but slow chunked LSD by this one
+  // CTA through global memory; the host switches to the 4-pass path for
+  // later batches when it sees the flag.
+  if (tid == 0) atomicOr(overflow, 1u);
+  const uint32_t* srck = ak + start;
+  const uint32_t* srcv = av + start;
+  for (int pass = 0; pass < kPasses - 1; ++pass) {
+    const int shift = pass * kRadixBits;
+    uint32_t* dk = (pass == kPasses - 2 ? out_keys : (pass & 1 ? (uint32_t*)ak : tk)) + start;
+    uint32_t* dv = (pass == kPasses - 2 ? out_vals : (pass & 1 ? (uint32_t*)av : tv)) + start;
+    for (int i = tid; i < kRadix; i += kBktThreads) S.hist[i] = 0;
+    __syncthreads();
+    for (uint32_t p = tid; p < size; p += kBktThreads)
+      atomicAdd(&S.hist[(srck[p] >> shift) & (kRadix - 1)], 1u);
+    __syncthreads();
+    uint32_t tot;
+    const uint32_t hv = tid < kRadix ? S.hist[tid] : 0u;
+    const uint32_t ex = block_exclusive_scan<kBktThreads, uint32_t>(hv, S.L.scan, &tot);
+    if (tid < kRadix) S.run[tid] = ex;
+    __syncthreads();
+    for (uint32_t c0 = 0; c0 < size; c0 += kBktCap) {
+      const uint32_t nc = min((uint32_t)kBktCap, size - c0);
+      // rank the chunk locally (stable), place it at the running offsets
+      local_subpass<kBktThreads, kBktItems>(srck + c0, srcv + c0, nc, S.k[0], S.v[0], shift, S.L,
+                                            nullptr);
+      // S.k[0] holds the chunk grouped by digit; L.tstart / L.cnt describe it
+      for (uint32_t p = tid; p < nc; p += kBktThreads) {
+        const uint32_t key = S.k[0][p];
+        const uint32_t dg = (key >> shift) & (kRadix - 1);
+        const uint32_t g = S.run[dg] + (p - S.L.tstart[dg]);
+        dk[g] = key;
+        dv[g] = S.v[0][p];
+      }
+      __syncthreads();
+      if (tid < kRadix) S.run[tid] += S.L.cnt[tid];
+      __syncthreads();
+    }
+    __threadfence_block();
+    srck = dk;
+    srcv = dv;
+    __syncthreads();
+  }
+  if (out_f1 != nullptr) {
+    __syncthreads();
+    for (uint32_t p = tid; p < size; p += kBktThreads) {
+      const uint32_t g = start + p;
+      if ((g & (kF1Step - 1)) == 0) out_f1[g / kF1Step] = out_keys[g];
+    }
+  }
 }
 
 int g_sms = 0;
@@ -464,9 +689,26 @@ cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals
     e = cudaFuncSetAttribute(onesweep_pass_kernel<false>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PassSmem));
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(small_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(SmallSmem));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(bucket_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(BktSmem));
+    if (e != cudaSuccess) return e;
     g_attr = true;
   }
   RawBatch in{raw_keys, raw_vals, ops, mode, n};
+  cudaError_t e = cudaSuccess;
+
+  // (1) small batch: one CTA sorts all four digits in shared memory
+  if (b <= (uint64_t)kSmallCap) {
+    hk.begin(hk.ctx, LSM_K_SORT_PASS, s);
+    e = launch_pdl(small_sort_kernel, 1u, kSmallThreads, sizeof(SmallSmem), s, in, (uint32_t)b,
+                   out_keys, out_vals, out_f1, S.err);
+    hk.end(hk.ctx, LSM_K_SORT_PASS, (double)b * 17.0, s, 1);
+    return e;
+  }
+
   const uint32_t epoch = (uint32_t)(S.epoch++ % 127u) + 1u;  // 1..127
   const uint64_t tiles = sort_tiles(b);
   const uint64_t groups = sort_groups(b);
@@ -479,8 +721,29 @@ cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals
   const uint64_t status_words = (uint64_t)kPasses * (tiles + groups) * kRadix;
   // one wave (1 CTA per SM) -> tile = blockIdx, no counter round trip
   const int use_ctr = tiles > (uint64_t)g_sms ? 1 : 0;
+  if (S.overflow_host && *S.overflow_host) S.lsd_only = true;  // skewed keys seen
 
-  cudaError_t e = cudaSuccess;
+  // (2) MSD + local: pass A scatters by the top digit into 256 stable
+  //     buckets, pass B sorts each bucket by the other three digits in
+  //     shared memory (one CTA per bucket)
+  if (!use_ctr && !S.lsd_only) {
+    hk.begin(hk.ctx, LSM_K_SORT_PASS, s);
+    e = launch_pdl(onesweep_pass_kernel<true>, (unsigned)tiles, kSortThreads, sizeof(PassSmem), s,
+                   in, (const uint32_t*)nullptr, (const uint32_t*)nullptr, S.tmp_keys[0],
+                   S.tmp_vals[0], b, (const uint32_t*)S.bases, tile_st, group_st, S.tile_ctr, 0,
+                   (kPasses - 1) * kRadixBits, S.err, epoch, (uint32_t*)nullptr, S.bkt);
+    hk.end(hk.ctx, LSM_K_SORT_PASS, (double)b * 17.0, s, 1);
+    if (e != cudaSuccess) return e;
+    hk.begin(hk.ctx, LSM_K_SORT_PASS, s);
+    e = launch_pdl(bucket_sort_kernel, (unsigned)kRadix, kBktThreads, sizeof(BktSmem), s,
+                   (const uint32_t*)S.bkt, (const uint32_t*)S.tmp_keys[0],
+                   (const uint32_t*)S.tmp_vals[0], S.tmp_keys[1], S.tmp_vals[1], out_keys, out_vals,
+                   out_f1, S.overflow_dev);
+    hk.end(hk.ctx, LSM_K_SORT_PASS, (double)b * 16.0, s, 1);
+    return e;
+  }
+
+  // (3) 4-pass LSD onesweep (multi-wave batches or skewed key sets)
   if (use_ctr) {  // multi-wave: digit bases from an upfront histogram
     uint64_t hgrid = (b + 4 * kHistThreads - 1) / (4 * kHistThreads);
     if (hgrid < 1) hgrid = 1;
@@ -505,12 +768,12 @@ cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals
       e = launch_pdl(onesweep_pass_kernel<true>, (unsigned)tiles, kSortThreads, sizeof(PassSmem), s,
                      in, (const uint32_t*)nullptr, (const uint32_t*)nullptr, ok, ov, b,
                      (const uint32_t*)S.bases, ts, gs, S.tile_ctr + p, use_ctr, 0, S.err, epoch,
-                     (uint32_t*)(p == kPasses - 1 ? out_f1 : nullptr));
+                     (uint32_t*)(p == kPasses - 1 ? out_f1 : nullptr), (uint32_t*)nullptr);
     else
       e = launch_pdl(onesweep_pass_kernel<false>, (unsigned)tiles, kSortThreads, sizeof(PassSmem),
                      s, in, ik, iv, ok, ov, b, (const uint32_t*)(S.bases + p * kRadix), ts, gs,
                      S.tile_ctr + p, use_ctr, p * kRadixBits, S.err, epoch,
-                     (uint32_t*)(p == kPasses - 1 ? out_f1 : nullptr));
+                     (uint32_t*)(p == kPasses - 1 ? out_f1 : nullptr), (uint32_t*)nullptr);
     // bytes: pass 0 reads raw (k,v,op = 9 B) writes 8 B; others 16 B
     hk.end(hk.ctx, LSM_K_SORT_PASS, (double)b * (p == 0 ? 17.0 : 16.0), s, 1);
     if (e != cudaSuccess) return e;

@@ -33,13 +33,17 @@ int main(int argc, char** argv) {
   SortScratch S{};
   S.hist = meta; S.bases = meta + 2 * kPasses * kRadix; S.tile_ctr = meta + 3 * kPasses * kRadix;
   S.err = S.tile_ctr + 4; S.done_ctr = S.tile_ctr + 5; S.status = meta + head;
-  S.tiles_cap = tiles; S.tmp_keys[0] = tk[0]; S.tmp_keys[1] = tk[1]; S.tmp_vals[0] = tv[0]; S.tmp_vals[1] = tv[1];
+  S.tiles_cap = tiles;
+  cudaMalloc(&S.bkt, 512 * 4);
+  uint32_t* hp; cudaHostAlloc((void**)&hp, 64, cudaHostAllocMapped); *hp = 0;
+  cudaHostGetDevicePointer((void**)&S.overflow_dev, hp, 0); S.overflow_host = hp;
+  if (getenv("LSD_ONLY")) S.lsd_only = true; S.tmp_keys[0] = tk[0]; S.tmp_keys[1] = tk[1]; S.tmp_vals[0] = tv[0]; S.tmp_vals[1] = tv[1];
   gen<<<512, 256>>>(k, v, o, b, 12345);
   LaunchHooks hk{hb, he, nullptr};
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  for (int i = 0; i < 20; ++i) launch_sort_batch(k, v, o, kModeMixed, b, b, S, ok, ov, 0, hk);
+  for (int i = 0; i < 20; ++i) launch_sort_batch(k, v, o, kModeMixed, b, b, S, ok, ov, nullptr, 0, hk);
   cudaEventRecord(e0);
-  for (int i = 0; i < 100; ++i) launch_sort_batch(k, v, o, kModeMixed, b, b, S, ok, ov, 0, hk);
+  for (int i = 0; i < 100; ++i) launch_sort_batch(k, v, o, kModeMixed, b, b, S, ok, ov, nullptr, 0, hk);
   cudaEventRecord(e1); cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1);
   printf("b=%llu tiles=%llu sort avg %.2f us (%.2f G pairs/s)\n", (unsigned long long)b, (unsigned long long)tiles, ms * 10, b / (ms * 1e-2) / 1e9 * 1e-3 * 1e3 / 1e3);
@@ -49,7 +53,7 @@ int main(int argc, char** argv) {
   unsigned long long* probe; size_t pn = 4ull * 4096 * 8 + 4096 * 4;
   cudaMalloc(&probe, pn * 8); cudaMemset(probe, 0, pn * 8);
   cudaMemcpyToSymbol(g_probe, &probe, sizeof(probe));
-  launch_sort_batch(k, v, o, kModeMixed, b, b, S, ok, ov, 0, hk);
+  launch_sort_batch(k, v, o, kModeMixed, b, b, S, ok, ov, nullptr, 0, hk);
   cudaDeviceSynchronize();
   std::vector<unsigned long long> P(pn);
   cudaMemcpy(P.data(), probe, pn * 8, cudaMemcpyDeviceToHost);

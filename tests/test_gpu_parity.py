@@ -156,6 +156,13 @@ def test_multi_wave_sort():
     _run_schedule((1 << 21) + 4097, 3, 99, frac4=1, nlook=20_000, nrange=1000)
 
 
+def test_skewed_keys_bucket_overflow():
+    # keys < 3000: every key variable has top digit 0, so the MSD pass puts
+    # the whole batch into one bucket larger than shared memory: the chunked
+    # fallback must still be exact, and later batches switch to 4-pass LSD
+    _run_schedule(50_000, 5, 123, frac4=1, alphabet=3000, nlook=3000, nrange=300)
+
+
 def test_one_wave_boundary_sort():
     # exactly 148 tiles (largest one-wave batch) and one record more
     for b in (148 * 7168, 148 * 7168 + 1):
@@ -284,10 +291,16 @@ def test_launch_counter_counts_kernels():
     k, v, d = synth.updates(1, 0, 4096)
     n0 = g.launch_count
     g.update(to_device(k), to_device(v), to_device(d))
-    # one-wave batch (b <= 148 tiles): 4 onesweep passes, no histogram kernel
-    assert g.launch_count - n0 == 4
+    # small batch (b <= 7168): one CTA sorts it in shared memory
+    assert g.launch_count - n0 == 1
     g.update(to_device(k), to_device(v), to_device(d))
-    assert g.launch_count - n0 == 9  # + 4 + one merge
+    assert g.launch_count - n0 == 3  # + sort + one merge
+    # one-wave batch: MSD pass + per-bucket shared-memory sorts
+    mid = pkg.GpuLSM(1 << 20)
+    km, vm, dm = synth.updates(3, 0, 1 << 20)
+    n2 = mid.launch_count
+    mid.update(to_device(km), to_device(vm), to_device(dm))
+    assert mid.launch_count - n2 == 2
     # multi-wave batch: histogram kernel + 4 passes
     big = pkg.GpuLSM(2_000_000)
     kb, vb, db = synth.updates(2, 0, 2_000_000)
