@@ -467,10 +467,18 @@ struct LocalScratch {
 template <int T, int ITEMS>
 __device__ __forceinline__ void local_subpass(const uint32_t* sk, const uint32_t* sv, uint32_t n,
                                               uint32_t* dk, uint32_t* dv, int shift,
-                                              LocalScratch<T>& L, const uint32_t* gbase) {
+                                              LocalScratch<T>& L, const uint32_t* gbase,
+                                              int probe_slot = -1) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#ifdef GPULSM_PROBE
+#define LPROBE(k) \
+  do { if (probe_slot >= 0 && tid == 0 && g_probe) g_probe[5ull * 4096 * 8 + 4096 + blockIdx.x * 16 + probe_slot * 4 + (k)] = gtimer(); } while (0)
+#else
+#define LPROBE(k) do {} while (0)
+#endif
   for (int i = tid; i < (T / 32) * kRadix; i += T) (&L.whist[0][0])[i] = 0;
   __syncthreads();
+  LPROBE(0);
   const uint32_t wbase = warp * (32 * ITEMS);
   uint32_t k[ITEMS], v[ITEMS], rk[ITEMS];
 #pragma unroll
@@ -496,6 +504,7 @@ __device__ __forceinline__ void local_subpass(const uint32_t* sk, const uint32_t
     __syncwarp();
   }
   __syncthreads();
+  LPROBE(1);
   uint32_t c = 0;
   if (tid < kRadix) {
 #pragma unroll 8
@@ -510,6 +519,7 @@ __device__ __forceinline__ void local_subpass(const uint32_t* sk, const uint32_t
   const uint32_t ts = block_exclusive_scan<T, uint32_t>(c, L.scan, &tot);
   if (tid < kRadix) L.tstart[tid] = gbase ? gbase[tid] : ts;
   __syncthreads();
+  LPROBE(2);
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     if (wbase + i * 32 + lane < n) {
@@ -533,11 +543,21 @@ struct SmallSmem {
   LocalScratch<kSmallThreads> L;
 };
 
+// CTA j sorts batch j = records [j*b, (j+1)*b) of the input (one CTA for a
+// single batch; k CTAs for the multi-batch insertion of N1).
 __global__ void __launch_bounds__(kSmallThreads, 1) small_sort_kernel(
-    RawBatch in, uint32_t b, uint32_t* __restrict__ out_keys, uint32_t* __restrict__ out_vals,
+    RawBatch in_all, uint32_t b, uint32_t* __restrict__ out_keys, uint32_t* __restrict__ out_vals,
     uint32_t* __restrict__ out_f1, uint32_t* __restrict__ err) {
   extern __shared__ __align__(16) uint8_t small_smem[];
   SmallSmem& S = *reinterpret_cast<SmallSmem*>(small_smem);
+  const uint64_t off = (uint64_t)blockIdx.x * b;
+  RawBatch in = in_all;
+  in.keys += off;
+  if (in.vals) in.vals += off;
+  if (in.ops) in.ops += off;
+  in.n = in_all.n > off ? (in_all.n - off < b ? in_all.n - off : b) : 0;
+  out_keys += off;
+  out_vals += off;
   pdl_wait();
   pdl_trigger();
   bool any_bad = false;
@@ -593,6 +613,16 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_sort_kernel(
   pdl_wait();
   pdl_trigger();
   const uint32_t d = blockIdx.x;
+#ifdef GPULSM_PROBE
+#define BPROBE(k) \
+  do { if (tid == 0 && g_probe) g_probe[5ull * 4096 * 8 + d * 8 + (k)] = gtimer(); } while (0)
+#else
+#define BPROBE(k) do {} while (0)
+#endif
+  BPROBE(0);
+#ifdef GPULSM_PROBE
+  if (tid == 0 && g_probe) { uint32_t sm; asm volatile("mov.u32 %0, %%smid;" : "=r"(sm)); g_probe[5ull * 4096 * 8 + d * 8 + 7] = sm + 1; }
+#endif
   const uint32_t start = bkt[d], size = bkt[kRadix + d];
   if (size == 0) return;
   if (size <= (uint32_t)kBktCap) {
@@ -601,11 +631,19 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_sort_kernel(
       S.v[0][p] = __ldg(av + start + p);
     }
     __syncthreads();
+    BPROBE(1);
     int cur = 0;
     for (int pass = 0; pass < kPasses - 1; ++pass) {
+#ifdef GPULSM_PROBE_DUP0
+      if (pass == 0) {
+        local_subpass<kBktThreads, kBktItems>(S.k[cur], S.v[cur], size, S.k[cur ^ 1],
+                                              S.v[cur ^ 1], 0, S.L, nullptr, 3);
+      }
+#endif
       local_subpass<kBktThreads, kBktItems>(S.k[cur], S.v[cur], size, S.k[cur ^ 1],
-                                            S.v[cur ^ 1], pass * kRadixBits, S.L, nullptr);
+                                            S.v[cur ^ 1], pass * kRadixBits, S.L, nullptr, pass);
       cur ^= 1;
+      BPROBE(2 + pass);
     }
     for (uint32_t p = tid; p < size; p += kBktThreads) {
       const uint32_t key = S.k[cur][p];
@@ -614,6 +652,8 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_sort_kernel(
       out_vals[g] = S.v[cur][p];
       if (out_f1 != nullptr && (g & (kF1Step - 1)) == 0) out_f1[g / kF1Step] = key;
     }
+    __syncthreads();
+    BPROBE(5);
     return;
   }
   // Oversized bucket (skewed keys): correct but slow chunked LSD by this one
@@ -672,10 +712,7 @@ bool g_attr = false;
 
 }  // namespace
 
-cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals,
-                              const uint8_t* ops, int mode, uint64_t n, uint64_t b,
-                              SortScratch& S, uint32_t* out_keys, uint32_t* out_vals,
-                              uint32_t* out_f1, cudaStream_t s, const LaunchHooks& hk) {
+static cudaError_t sort_attrs() {
   if (!g_attr) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -696,6 +733,17 @@ cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals
                              (int)sizeof(BktSmem));
     if (e != cudaSuccess) return e;
     g_attr = true;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals,
+                              const uint8_t* ops, int mode, uint64_t n, uint64_t b,
+                              SortScratch& S, uint32_t* out_keys, uint32_t* out_vals,
+                              uint32_t* out_f1, cudaStream_t s, const LaunchHooks& hk) {
+  {
+    cudaError_t e = sort_attrs();
+    if (e != cudaSuccess) return e;
   }
   RawBatch in{raw_keys, raw_vals, ops, mode, n};
   cudaError_t e = cudaSuccess;
@@ -779,6 +827,36 @@ cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals
     if (e != cudaSuccess) return e;
     ik = ok;
     iv = ov;
+  }
+  return cudaSuccess;
+}
+
+// N1 multi-batch insertion: sort k consecutive batches of b records
+// (batch j = raw records [j*b, (j+1)*b), the last one possibly partial, n
+// in total) each on its own, into out[j*b ..). Small batches: one launch,
+// one CTA per batch; larger ones: one sort per batch.
+cudaError_t launch_sort_segments(const uint32_t* raw_keys, const uint32_t* raw_vals,
+                                 const uint8_t* ops, int mode, uint64_t n, uint64_t b,
+                                 uint64_t k, SortScratch& S, uint32_t* out_keys,
+                                 uint32_t* out_vals, cudaStream_t s, const LaunchHooks& hk) {
+  if (k == 0) return cudaSuccess;
+  if (b <= (uint64_t)kSmallCap && k > 1) {
+    cudaError_t e = sort_attrs();
+    if (e != cudaSuccess) return e;
+    RawBatch in{raw_keys, raw_vals, ops, mode, n};
+    hk.begin(hk.ctx, LSM_K_SORT_PASS, s);
+    e = launch_pdl(small_sort_kernel, (unsigned)k, kSmallThreads, sizeof(SmallSmem), s, in,
+                   (uint32_t)b, out_keys, out_vals, (uint32_t*)nullptr, S.err);
+    hk.end(hk.ctx, LSM_K_SORT_PASS, (double)k * b * 17.0, s, 1);
+    return e;
+  }
+  for (uint64_t j = 0; j < k; ++j) {
+    const uint64_t o = j * b;
+    const uint64_t nj = n - o < b ? n - o : b;
+    cudaError_t e = launch_sort_batch(raw_keys + o, raw_vals ? raw_vals + o : nullptr,
+                                      ops ? ops + o : nullptr, mode, nj, b, S, out_keys + o,
+                                      out_vals + o, nullptr, s, hk);
+    if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
 }

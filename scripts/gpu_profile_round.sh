@@ -8,9 +8,13 @@ echo "bench exit $?" >> gpurun_out/bench_full.log
 timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.log 2>&1
 timeout 1500 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_list.log 2>&1
 P="python scripts/prof_step.py"
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:count_kernel -s 0 -c 1 -o gpurun_out/prof_count $P > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:range_write -s 0 -c 1 -o gpurun_out/prof_range $P > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:lookup_kernel -s 0 -c 1 -o gpurun_out/prof_lookup $P > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:merge_kernel -s 62 -c 1 -o gpurun_out/prof_merge $P --no-cleanup --nq 1024 > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:onesweep -s 252 -c 2 -o gpurun_out/prof_sort $P --no-cleanup --nq 1024 > /dev/null 2>&1
+NCU="timeout 600 ncu --set full --clock-control none --import-source on"
+$NCU -k regex:count_kernel -s 0 -c 1 -o gpurun_out/prof_count $P > /dev/null 2>&1
+$NCU -k regex:range_kernel -s 0 -c 1 -o gpurun_out/prof_range $P > /dev/null 2>&1
+$NCU -k regex:lookup_kernel -s 0 -c 1 -o gpurun_out/prof_lookup $P > /dev/null 2>&1
+$NCU -k regex:merge_kernel -s 62 -c 1 -o gpurun_out/prof_merge $P --no-cleanup --nq 1024 > /dev/null 2>&1
+$NCU -k regex:merge_kernel -s 0 -c 1 -o gpurun_out/prof_merge0 $P --batches 4 --no-cleanup --nq 1024 > /dev/null 2>&1
+$NCU -k regex:onesweep -s 60 -c 1 -o gpurun_out/prof_sort $P --no-cleanup --nq 1024 > /dev/null 2>&1
+$NCU -k regex:bucket_sort -s 60 -c 1 -o gpurun_out/prof_bucket $P --no-cleanup --nq 1024 > /dev/null 2>&1
+$NCU -k regex:cleanup_write -s 0 -c 1 -o gpurun_out/prof_cleanup $P --nq 1024 > /dev/null 2>&1
 ls -la gpurun_out

@@ -20,8 +20,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 MUL = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
 TMUL = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "ns": 1e-3, "us": 1.0, "ms": 1e3}
 
-CLASS = [("onesweep", "sort_pass"), ("sort_hist", "sort_hist"), ("merge_kernel", "merge"),
-         ("lookup_kernel", "lookup"), ("count_kernel", "count"), ("range_write", "range"),
+CLASS = [("onesweep", "sort_pass"), ("bucket_sort", "sort_pass"), ("small_sort", "sort_pass"),
+         ("sort_hist", "sort_hist"), ("merge_kernel", "merge"),
+         ("lookup_kernel", "lookup"), ("count_kernel", "count"), ("range_kernel", "range"),
+         ("build_f1", "other"), ("finalize_index", "other"),
          ("scan_", "scan"), ("cleanup_", "cleanup"), ("fill_placebo", "cleanup"),
          ("bucket_", "other"), ("scatter_back", "other"), ("clip_kernel", "other"),
          ("sum_parts", "other")]
@@ -86,6 +88,10 @@ def full(rep):
             "issue_active_pct": g("smsp__issue_active.avg.pct_of_peak_sustained_active"),
             "warps_active_pct": g("sm__warps_active.avg.pct_of_peak_sustained_active"),
             "l2_throughput_pct": g("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+            "smem_wavefronts": g("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"),
+            "smem_bank_conflicts": g("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
+            "l1_hit_pct": g("l1tex__t_sector_hit_rate.pct"),
+            "l2_hit_pct": g("lts__t_sector_hit_rate.pct"),
             "top_stalls": [(n, round(v, 2)) for v, n in sorted(stalls, reverse=True)[:5]],
             "rep": os.path.basename(rep),
         })
@@ -121,7 +127,8 @@ def main():
             lines.append(f"{x['kernel']} [{x['class']}] grid={x['grid']} block={x['block']} regs={x['regs']} "
                          f"t={x['time_us']:.2f}us dram={(x['dram_read_bytes'] + x['dram_write_bytes']) / 1e6:.2f}MB "
                          f"({x['dram_GBps'] or 0:.0f} GB/s) issue={x['issue_active_pct']}% "
-                         f"warps={x['warps_active_pct']}% l2={x['l2_throughput_pct']}% stalls={x['top_stalls']} "
+                         f"warps={x['warps_active_pct']}% l2={x['l2_throughput_pct']}% l2hit={x['l2_hit_pct']}% "
+                         f"smem_wf={x['smem_wavefronts']} smem_conf={x['smem_bank_conflicts']} stalls={x['top_stalls']} "
                          f"[{x['rep']}]")
         open(os.path.join(prof, f"{a.round}_ncu_full_summary.txt"), "w").write("\n".join(lines) + "\n")
         json.dump(allres, open(os.path.join(prof, f"{a.round}_ncu_full.json"), "w"), indent=1)

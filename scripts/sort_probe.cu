@@ -50,7 +50,7 @@ int main(int argc, char** argv) {
 #ifdef GPULSM_PROBE
   unsigned int zero8[8] = {0};
   cudaMemcpyToSymbol(g_repolls, zero8, sizeof(zero8));
-  unsigned long long* probe; size_t pn = 4ull * 4096 * 8 + 4096 * 4;
+  unsigned long long* probe; size_t pn = 6ull * 4096 * 8;
   cudaMalloc(&probe, pn * 8); cudaMemset(probe, 0, pn * 8);
   cudaMemcpyToSymbol(g_probe, &probe, sizeof(probe));
   launch_sort_batch(k, v, o, kModeMixed, b, b, S, ok, ov, nullptr, 0, hk);
@@ -91,6 +91,35 @@ int main(int argc, char** argv) {
     }
     std::sort(a.begin(), a.end()); std::sort(bb.begin(), bb.end()); std::sort(c.begin(), c.end());
     if (!a.empty()) printf("hist ctas=%zu start min %.2f max %.2f | counted min %.2f p50 %.2f max %.2f | end min %.2f max %.2f\n", a.size(), a[0], a.back(), bb[0], bb[bb.size()/2], bb.back(), c[0], c.back());
+  }
+  {
+    const char* bn[6] = {"entry", "loaded", "sub0", "sub1", "sub2", "stored"};
+    for (int ph = 0; ph < 6; ++ph) {
+      std::vector<double> x;
+      for (int c = 0; c < 256; ++c) { unsigned long long t = P[5ull * 4096 * 8 + c * 8 + ph]; if (t) x.push_back(((double)t - (double)t0) / 1e3); }
+      std::sort(x.begin(), x.end());
+      if (!x.empty()) printf("bucket %-7s min %8.2f p50 %8.2f p90 %8.2f max %8.2f us\n", bn[ph], x[0], x[x.size()/2], x[x.size()*9/10], x.back());
+    }
+  }
+  for (int sp = 0; sp < 4; ++sp) {
+    const char* ln[4] = {"zeroed", "ranked", "scanned", "-"};
+    for (int k = 0; k < 3; ++k) {
+      std::vector<double> x;
+      for (int c = 0; c < 256; ++c) { unsigned long long t = P[5ull * 4096 * 8 + 4096 + c * 16 + sp * 4 + k]; if (t) x.push_back(((double)t - (double)t0) / 1e3); }
+      std::sort(x.begin(), x.end());
+      if (!x.empty()) printf("  sub%d %-8s min %8.2f p50 %8.2f p90 %8.2f max %8.2f us\n", sp, ln[k], x[0], x[x.size()/2], x[x.size()*9/10], x.back());
+    }
+  }
+  if (getenv("PROBE_BKT")) {
+    std::vector<int> cnt(256, 0);
+    for (int c = 0; c < 256; ++c) cnt[P[5ull * 4096 * 8 + c * 8 + 7] - 1]++;
+    for (int c = 0; c < 256; ++c) {
+      unsigned long long* q = &P[5ull * 4096 * 8 + c * 8];
+      unsigned long long* l = &P[5ull * 4096 * 8 + 4096 + c * 16];
+      int sm = (int)q[7] - 1;
+      printf("B %3d sm %3d n_on_sm %d size %u loaded %7.2f rank0 %6.2f scan0 %6.2f sub1 %6.2f sub2 %6.2f\n", c, sm, cnt[sm], 0u,
+             (q[1] - t0) / 1e3, (l[1] - l[0]) / 1e3, (l[2] - l[1]) / 1e3, (q[3] - q[2]) / 1e3, (q[4] - q[3]) / 1e3);
+    }
   }
   if (getenv("PROBE_TILES")) {
     int p = 1;
