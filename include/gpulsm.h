@@ -110,6 +110,28 @@ lsm_status lsm_insert(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals,
 /* All-delete batch: Delete(batch) = Insert(tombed(batch)). */
 lsm_status lsm_delete(lsm_t* h, const uint32_t* d_keys, uint64_t n, void* stream);
 
+/* Bulk build ("Bulk build"): build the dictionary from n
+ * elements at once. Only into an EMPTY structure (r == 0, else
+ * LSM_ERR_INVALID_ARG). The n elements form ONE batch (rules 1-6 of
+ * PAPER.md:260-279 apply across all of them; R24); they are
+ * encoded, padded with placebos to k*b (k = ceil(n/b)), radix-sorted once
+ * and segmented into the levels at the set bits of k, ascending key slices
+ * into ascending levels (views of one buffer, no copy). Afterwards r = k.
+ * d_keys[n], d_vals[n] (may be NULL with d_is_delete NULL: values 0),
+ * d_is_delete[n] u8 or NULL (all inserts). n >= 1, k*b <= 2^32.
+ * Errors as lsm_update; out-of-domain keys set the sticky LSM_ERR_KEY_DOMAIN. */
+lsm_status lsm_bulk_build(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals,
+                          const uint8_t* d_is_delete, uint64_t n, void* stream);
+
+/* Multi-batch insertion (footnote of PAPER.md:860): insert k = ceil(n/b)
+ * consecutive batches (batch j = elements [j*b, (j+1)*b), the last one
+ * possibly partial), oldest first. The result is identical, level for level
+ * and bit for bit, to k calls of lsm_update; all k batches are sorted before
+ * the merges (small b: one launch, one CTA per batch).
+ * Arguments as lsm_bulk_build; r grows by k.                               */
+lsm_status lsm_update_batches(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals,
+                              const uint8_t* d_is_delete, uint64_t n, void* stream);
+
 /* lsm_update from HOST buffers: copies the batch (9 B/update) into internal
  * device staging on `stream`, then runs lsm_update. h_* must stay valid until
  * the stream reaches the copy (use pinned memory for async overlap).       */
@@ -128,6 +150,23 @@ lsm_status lsm_update_host(lsm_t* h, const uint32_t* h_keys, const uint32_t* h_v
  * d_found_out[nq] u8 (1 found / 0 ⊥), may be NULL. nq == 0 is a no-op.    */
 lsm_status lsm_lookup(lsm_t* h, const uint32_t* d_q, uint64_t nq,
                       uint32_t* d_vals_out, uint8_t* d_found_out, void* stream);
+
+/* successor(k) / predecessor(k) for nq query keys -- the order-based
+ * queries the paper calls straightforward (footnote), read
+ * inclusively (R23): successor = the live pair with the smallest
+ * key >= k, predecessor = the live pair with the largest key <= k.
+ * Per query: one cursor per occupied level at lower_bound(k) (upper_bound(k)
+ * - 1), then a walk in key order that answers with the first key whose
+ * newest record (run head in the lowest level holding it, PAPER.md:386-387,
+ * 422-425) is regular, skipping deleted keys.
+ * d_q[nq] u32 (any 32-bit value; keys above LSM_MAX_KEY have no successor);
+ * d_keys_out[nq], d_vals_out[nq] u32 (LSM_NOT_FOUND on ⊥);
+ * d_found_out[nq] u8, may be NULL. Stream-ordered, asynchronous.
+ * Cost grows with the number of deleted keys skipped (no cleanup).       */
+lsm_status lsm_successor(lsm_t* h, const uint32_t* d_q, uint64_t nq, uint32_t* d_keys_out,
+                         uint32_t* d_vals_out, uint8_t* d_found_out, void* stream);
+lsm_status lsm_predecessor(lsm_t* h, const uint32_t* d_q, uint64_t nq, uint32_t* d_keys_out,
+                           uint32_t* d_vals_out, uint8_t* d_found_out, void* stream);
 
 /* Host-buffer variant of lsm_lookup (copies in, runs, copies out; h_found_out
  * may be NULL). Synchronises `stream` before returning.                    */

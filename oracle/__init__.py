@@ -48,7 +48,11 @@ def lib():
             "o1_apply_batch": ([vp, u32p, u32p, u8p, u64], None),
             "o1_lookup": ([vp, u32p, u64, u32p, u8p], None),
             "o1_count": ([vp, u32p, u32p, u64, u32p], None),
+            "o1_successor": ([vp, u32p, u64, u32p, u32p, u8p], None),
+            "o1_predecessor": ([vp, u32p, u64, u32p, u32p, u8p], None),
             "o1_range": ([vp, u32p, u32p, u64, u64p, u32p, u32p, u64], u64),
+            "o1_bulk_build": ([vp, u32p, u32p, u8p, u64], None),
+            "s1_bulk_build": ([vp, u32p, u32p, u8p, u64], ctypes.c_int),
             "o1_cleanup": ([vp], None), "o1_size": ([vp], u64),
             "o1_num_batches": ([vp], u64), "o1_dump": ([vp, u32p, u32p], None),
             "s1_create": ([u64], vp), "s1_destroy": ([vp], None),
@@ -132,6 +136,22 @@ class OracleDict:
         lib().o1_lookup(self.h, _p(q, u32p), len(q), _p(v, u32p), _p(f, u8p))
         return v, f
 
+    def _order_query(self, fn, q):
+        q = _u32(q)
+        k = np.empty(len(q), np.uint32)
+        v = np.empty(len(q), np.uint32)
+        f = np.empty(len(q), np.uint8)
+        fn(self.h, _p(q, u32p), len(q), _p(k, u32p), _p(v, u32p), _p(f, u8p))
+        return k, v, f
+
+    def successor(self, q):
+        """Smallest live key >= q (R23): (keys, vals, found)."""
+        return self._order_query(lib().o1_successor, q)
+
+    def predecessor(self, q):
+        """Largest live key <= q (R23): (keys, vals, found)."""
+        return self._order_query(lib().o1_predecessor, q)
+
     def count(self, k1, k2):
         k1, k2 = _u32(k1), _u32(k2)
         out = np.empty(len(k1), np.uint32)
@@ -148,6 +168,13 @@ class OracleDict:
         tot = lib().o1_range(self.h, _p(k1, u32p), _p(k2, u32p), nq, _p(off, u64p),
                              _p(ko, u32p), _p(vo, u32p), cap)
         return off, ko[:tot], vo[:tot]
+
+    def bulk_build(self, keys, vals=None, is_delete=None):
+        """N1 (R24): all elements as one batch; r = ceil(n/b)."""
+        keys = _u32(keys)
+        vals = _u32(vals) if vals is not None else np.zeros_like(keys)
+        d = _u8(is_delete)
+        lib().o1_bulk_build(self.h, _p(keys, u32p), _p(vals, u32p), _p(d, u8p), len(keys))
 
     def cleanup(self):
         lib().o1_cleanup(self.h)
@@ -185,6 +212,15 @@ class ShadowLSM:
         vals = _u32(vals) if vals is not None else np.zeros_like(keys)
         d = _u8(is_delete)
         lib().s1_update(self.h, _p(keys, u32p), _p(vals, u32p), _p(d, u8p), len(keys))
+
+    def bulk_build(self, keys, vals=None, is_delete=None):
+        """N1 bulk build (R24): one sort, sliced into levels."""
+        keys = _u32(keys)
+        vals = _u32(vals) if vals is not None else np.zeros_like(keys)
+        d = _u8(is_delete)
+        rc = lib().s1_bulk_build(self.h, _p(keys, u32p), _p(vals, u32p), _p(d, u8p), len(keys))
+        if rc != 0:
+            raise ValueError("bulk_build needs an empty structure and n >= 1")
 
     def cleanup(self):
         lib().s1_cleanup(self.h)

@@ -67,3 +67,26 @@ class BruteDict:
 
     def count(self, k1, k2):
         return len(self.range(k1, k2))
+
+    def successor(self, k):
+        """Smallest key >= k whose lookup is not ⊥ (R23), by scanning every
+        key that ever occurred; (key, val) or None."""
+        k = int(k)
+        best = None
+        for kk in self._keys_ever():
+            if kk >= k and (best is None or kk < best[0]):
+                v = self.lookup(kk)
+                if v is not None:
+                    best = (kk, v)
+        return best
+
+    def predecessor(self, k):
+        """Largest key <= k whose lookup is not ⊥ (R23); (key, val) or None."""
+        k = int(k)
+        best = None
+        for kk in self._keys_ever():
+            if kk <= k and (best is None or kk > best[0]):
+                v = self.lookup(kk)
+                if v is not None:
+                    best = (kk, v)
+        return best

@@ -131,6 +131,15 @@ void o1_apply_batch(void* h, const uint32_t* keys, const uint32_t* vals,
   o->r += 1;
 }
 
+// bulk build (R24): the n elements are ONE batch (rules 1-6
+// over all of them) applied to the empty dictionary; r = ceil(n/b).
+void o1_bulk_build(void* h, const uint32_t* keys, const uint32_t* vals,
+                   const uint8_t* is_delete, uint64_t n) {
+  O1* o = static_cast<O1*>(h);
+  o1_apply_batch(h, keys, vals, is_delete, n);
+  o->r = (n + o->b - 1) / o->b;
+}
+
 // lookup(k): <k,v> in S or ⊥.
 void o1_lookup(void* h, const uint32_t* q, uint64_t nq, uint32_t* vals_out,
                uint8_t* found_out) {
@@ -181,6 +190,36 @@ uint64_t o1_range(void* h, const uint32_t* k1, const uint32_t* k2, uint64_t nq,
   }
   offsets[nq] = pos;
   return pos;
+}
+
+// successor(k) / predecessor(k): the order-based queries of the footnote at
+// PAPER.md:113 ("finding a successor or a predecessor of a certain key"),
+// read inclusively (R23): succ(k) = the pair of S with the smallest
+// key >= k, pred(k) = the pair with the largest key <= k; ⊥ if none.
+// ⊥ writes key = val = 0xFFFFFFFF and found = 0.
+void o1_successor(void* h, const uint32_t* q, uint64_t nq, uint32_t* keys_out,
+                  uint32_t* vals_out, uint8_t* found_out) {
+  O1* o = static_cast<O1*>(h);
+  for (uint64_t i = 0; i < nq; ++i) {
+    auto it = o->S.lower_bound(q[i]);
+    bool f = it != o->S.end();
+    keys_out[i] = f ? it->first : 0xFFFFFFFFu;
+    vals_out[i] = f ? it->second : 0xFFFFFFFFu;
+    if (found_out) found_out[i] = f ? 1 : 0;
+  }
+}
+
+void o1_predecessor(void* h, const uint32_t* q, uint64_t nq, uint32_t* keys_out,
+                    uint32_t* vals_out, uint8_t* found_out) {
+  O1* o = static_cast<O1*>(h);
+  for (uint64_t i = 0; i < nq; ++i) {
+    auto it = o->S.upper_bound(q[i]);  // first key > q
+    bool f = it != o->S.begin();
+    if (f) --it;
+    keys_out[i] = f ? it->first : 0xFFFFFFFFu;
+    vals_out[i] = f ? it->second : 0xFFFFFFFFu;
+    if (found_out) found_out[i] = f ? 1 : 0;
+  }
 }
 
 // cleanup is transparent to S; r' = ceil(|S|/b) (R10,R11).
@@ -281,6 +320,53 @@ void s1_update(void* h, const uint32_t* keys, const uint32_t* vals,
 // largest, stable, on the original key; 2) mark stale elements; 3) compact;
 // 4) pad with < b placebos; 5) redistribute, smaller keys to smaller levels
 // (R10-R13).
+// bulk build (R24): "a sort" of all k*b elements -- encode as
+// in s1_update, pad with placebos to k*b (k = ceil(n/b)), stable sort on the
+// key variable -- then "segment this array into ... sorted levels
+// corresponding to its GPU LSM levels": ascending key slices into the set
+// bits of k, ascending (as cleanup, R12). Only on an empty structure
+// (returns -1 otherwise).
+int s1_bulk_build(void* h, const uint32_t* keys, const uint32_t* vals, const uint8_t* is_delete,
+                  uint64_t n) {
+  S1* s = static_cast<S1*>(h);
+  if (s->r != 0 || n == 0) return -1;
+  const uint64_t b = s->b;
+  const uint64_t k = (n + b - 1) / b;
+  std::vector<Rec> buf;
+  buf.reserve(k * b);
+  for (uint64_t i = 0; i < n; ++i) {
+    bool del = is_delete ? is_delete[i] != 0 : false;
+    Rec e;
+    if (keys[i] > kMaxKey) {
+      e.key = kPlacebo;
+      e.val = 0;
+      s->domain_error = 1;
+    } else {
+      e.key = (keys[i] << 1) | (del ? 0u : 1u);
+      e.val = del ? 0u : (vals ? vals[i] : 0u);
+    }
+    buf.push_back(e);
+  }
+  while (buf.size() < k * b) buf.push_back(Rec{kPlacebo, 0u});
+  std::stable_sort(buf.begin(), buf.end(),
+                   [](const Rec& a, const Rec& c) { return a.key < c.key; });
+  const uint64_t tag = s->batches_seen++;
+  uint64_t off = 0;
+  for (uint64_t i = 0; (k >> i) != 0; ++i) {
+    if (s->level.size() <= i) {
+      s->level.resize(i + 1);
+      s->tag.resize(i + 1);
+    }
+    if (!((k >> i) & 1ull)) continue;
+    const uint64_t sz = b << i;
+    s->level[i].assign(buf.begin() + off, buf.begin() + off + sz);
+    s->tag[i].assign(sz, tag);
+    off += sz;
+  }
+  s->r = k;
+  return 0;
+}
+
 void s1_cleanup(void* h) {
   S1* s = static_cast<S1*>(h);
   const uint64_t b = s->b;

@@ -44,6 +44,10 @@ SIGNATURES = {
     "lsm_lookup": ([_vp, _vp, _u64, _vp, _vp, _vp], _st),
     "lsm_lookup_host": ([_vp, _vp, _u64, _vp, _vp, _vp], _st),
     "lsm_count": ([_vp, _vp, _vp, _u64, _vp, _vp], _st),
+    "lsm_bulk_build": ([_vp, _vp, _vp, _vp, _u64, _vp], _st),
+    "lsm_update_batches": ([_vp, _vp, _vp, _vp, _u64, _vp], _st),
+    "lsm_successor": ([_vp, _vp, _u64, _vp, _vp, _vp, _vp], _st),
+    "lsm_predecessor": ([_vp, _vp, _u64, _vp, _vp, _vp, _vp], _st),
     "lsm_range": ([_vp, _vp, _vp, _u64, _vp, _vp, _vp, _u64, ctypes.POINTER(_u64), _vp], _st),
     "lsm_cleanup": ([_vp, _vp], _st),
     "lsm_batch_size": ([_vp, ctypes.POINTER(_u64)], _st),
@@ -180,6 +184,20 @@ class GpuLSM:
                                     _dev(is_delete, 1, "is_delete"), n, _stream_ptr(stream)),
                "lsm_update")
 
+    def bulk_build(self, keys, vals=None, is_delete=None, stream=None):
+        """N1 bulk build into an empty structure: all n elements form one batch,
+        one sort, levels at the set bits of ceil(n/b)."""
+        _check(self._lib.lsm_bulk_build(self.h, _dev(keys, 4, "keys"), _dev(vals, 4, "vals"),
+                                        _dev(is_delete, 1, "is_delete"), keys.numel(),
+                                        _stream_ptr(stream)), "lsm_bulk_build")
+
+    def update_batches(self, keys, vals=None, is_delete=None, stream=None):
+        """N1 multi-batch insertion: ceil(n/b) consecutive batches, oldest first,
+        identical to that many update() calls (PAPER.md:860 footnote)."""
+        _check(self._lib.lsm_update_batches(self.h, _dev(keys, 4, "keys"), _dev(vals, 4, "vals"),
+                                            _dev(is_delete, 1, "is_delete"), keys.numel(),
+                                            _stream_ptr(stream)), "lsm_update_batches")
+
     def insert(self, keys, vals, stream=None):
         _check(self._lib.lsm_insert(self.h, _dev(keys, 4, "keys"), _dev(vals, 4, "vals"),
                                     keys.numel(), _stream_ptr(stream)), "lsm_insert")
@@ -222,6 +240,24 @@ class GpuLSM:
                                          ctypes.c_void_p(f.ctypes.data), _stream_ptr(stream)),
                "lsm_lookup_host")
         return v, f
+
+    def _order(self, fn, name, q, stream):
+        torch = _torch()
+        nq = q.numel()
+        keys = torch.empty(nq, dtype=torch.int32, device=q.device)
+        vals = torch.empty(nq, dtype=torch.int32, device=q.device)
+        found = torch.empty(nq, dtype=torch.uint8, device=q.device)
+        _check(fn(self.h, _dev(q, 4, "q"), nq, _dev(keys, 4, "keys"), _dev(vals, 4, "vals"),
+                  _dev(found, 1, "found"), _stream_ptr(stream)), name)
+        return keys, vals, found
+
+    def successor(self, q, stream=None):
+        """Smallest live key >= q per query (reading R23): (keys, vals, found)."""
+        return self._order(self._lib.lsm_successor, "lsm_successor", q, stream)
+
+    def predecessor(self, q, stream=None):
+        """Largest live key <= q per query (reading R23): (keys, vals, found)."""
+        return self._order(self._lib.lsm_predecessor, "lsm_predecessor", q, stream)
 
     def count(self, k1, k2, stream=None):
         torch = _torch()

@@ -44,11 +44,18 @@ struct LevelTable {
   const uint32_t* vals[LSM_MAX_LEVELS];
   const uint32_t* idx[LSM_MAX_LEVELS];   // F1 | F2 | F3 (see idx_f*_off)
   uint64_t n[LSM_MAX_LEVELS];
-  uint32_t f3_smem_off[LSM_MAX_LEVELS];  // offset of the level's F3 in smem
+  uint32_t f3_smem_off[LSM_MAX_LEVELS];  // offset of the level's F3 tree in smem
+  uint32_t f3_h[LSM_MAX_LEVELS];         // its height (2^h words, Eytzinger order)
   uint32_t f3_smem_total;                // words of F3 staged in smem
   int count;
 };
 constexpr uint32_t kF3SmemMax = 24 * 1024;  // words (96 KB); larger indexes use global F3
+// height of the complete search tree over n3 F3 entries: 2^h - 1 >= n3
+inline __host__ __device__ uint32_t f3_tree_h(uint64_t n3) {
+  uint32_t h = 1;
+  while (((1ull << h) - 1) < n3) ++h;
+  return h;
+}
 
 __device__ __forceinline__ uint32_t lane_id() {
   uint32_t r;
@@ -231,6 +238,10 @@ struct LaunchHooks {
 };
 
 // out_f1 (nullable): F1 of the output level (every 8th sorted key).
+cudaError_t launch_sort_segments(const uint32_t* raw_keys, const uint32_t* raw_vals,
+                                 const uint8_t* ops, int mode, uint64_t n, uint64_t b,
+                                 uint64_t k, SortScratch& S, uint32_t* out_keys,
+                                 uint32_t* out_vals, cudaStream_t s, const LaunchHooks& hk);
 cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals,
                               const uint8_t* ops, int mode, uint64_t n, uint64_t b,
                               SortScratch& S, uint32_t* out_keys, uint32_t* out_vals,
@@ -258,6 +269,9 @@ cudaError_t launch_lookup(const LevelTable& T, const uint32_t* q, uint64_t nq,
                           const LaunchHooks& hk);
 int device_sms();
 
+cudaError_t launch_order(const LevelTable& T, const uint32_t* q, uint64_t nq, bool succ,
+                         uint32_t* keys_out, uint32_t* vals_out, uint8_t* found_out,
+                         cudaStream_t s, const LaunchHooks& hk);
 cudaError_t launch_count(const LevelTable& T, const uint32_t* k1, const uint32_t* k2,
                          uint64_t nq, uint32_t* counts_out, cudaStream_t s,
                          const LaunchHooks& hk, int cls);
@@ -275,6 +289,15 @@ cudaError_t launch_range(const LevelTable& T, const uint32_t* k1, const uint32_t
                          uint64_t nq, uint64_t* offsets, uint32_t* keys_out, uint32_t* vals_out,
                          uint64_t capacity, unsigned long long* scratch, cudaStream_t s,
                          const LaunchHooks& hk);
+
+// Three-pass range (count + save positions, scan, write walk) when every
+// level has < 2^32 records and at most 8 levels are occupied.
+bool range3_ok(const LevelTable& T);
+uint64_t range3_scratch_bytes(const LevelTable& T, uint64_t nq);
+cudaError_t launch_range3(const LevelTable& T, const uint32_t* k1, const uint32_t* k2,
+                          uint64_t nq, uint64_t* offsets, uint32_t* keys_out, uint32_t* vals_out,
+                          uint64_t capacity, void* scratch, cudaStream_t s,
+                          const LaunchHooks& hk);
 
 // Cleanup: valid = regular && first of its key run in M; compact into C.
 // tile_counts: cleanup_tiles(n) u32; offsets: cleanup_tiles(n)+1 u64.

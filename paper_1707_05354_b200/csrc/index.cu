@@ -28,13 +28,20 @@ __global__ void finalize_index_kernel(IndexJobs J) {
   const uint32_t* f1 = idx;
   uint32_t* f2 = idx + idx_f2_off(n);
   uint32_t* f3 = idx + idx_f3_off(n);
-  const uint64_t n2 = idx_f2_len(n), n3 = idx_f3_len(n);
+  const uint64_t n1 = idx_f1_len(n), n2 = idx_f2_len(n), n3 = idx_f3_len(n);
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n2 + n3;
        j += (uint64_t)gridDim.x * blockDim.x) {
     if (j < n2)
       f2[j] = __ldg(f1 + j * kFanout);
     else
       f3[j - n2] = __ldg(f1 + (j - n2) * kFanout * kFanout);
+  }
+  // the query kernels read whole 32-entry lines of F1 and F2: the padding up
+  // to the line boundary holds 0xFFFFFFFF, which is never below a query
+  if (blockIdx.x == 0 && threadIdx.x < kFanout) {
+    const uint64_t p1 = n1 + threadIdx.x, p2 = n2 + threadIdx.x;
+    if (p1 < idx_f2_off(n)) idx[p1] = 0xFFFFFFFFu;
+    if (p2 < idx_f3_off(n) - idx_f2_off(n)) f2[p2] = 0xFFFFFFFFu;
   }
 }
 

@@ -62,6 +62,12 @@ struct lsm {
   SortScratch sort{};
   uint32_t* sort_meta = nullptr;
   uint64_t sort_meta_words = 0;
+  // N1: scratch of the bulk-build sort (k*b records), grown on demand; shares
+  // the error word and the overflow flag of `sort`
+  SortScratch bulk{};
+  uint32_t* bulk_meta = nullptr;
+  uint64_t bulk_cap = 0;
+  Buffer stage;  // N1 multi-batch insertion: the k sorted batches
   // host-update staging
   uint32_t* st_keys = nullptr;
   uint32_t* st_vals = nullptr;
@@ -214,6 +220,50 @@ cudaError_t ensure_sort_scratch(lsm* h, cudaStream_t s) {
   return cudaSuccess;
 }
 
+void bulk_free(lsm* h, cudaStream_t s) {
+  if (h->bulk_meta) cudaFreeAsync(h->bulk_meta, s);
+  for (int k = 0; k < 2; ++k) {
+    if (h->bulk.tmp_keys[k]) cudaFreeAsync(h->bulk.tmp_keys[k], s);
+    if (h->bulk.tmp_vals[k]) cudaFreeAsync(h->bulk.tmp_vals[k], s);
+  }
+  h->bulk = SortScratch{};
+  h->bulk_meta = nullptr;
+  h->bulk_cap = 0;
+}
+
+// sort scratch for one sort of up to `cap` records (bulk build)
+cudaError_t ensure_bulk_scratch(lsm* h, uint64_t cap, cudaStream_t s) {
+  cudaError_t e = ensure_sort_scratch(h, s);
+  if (e != cudaSuccess || h->bulk_cap >= cap) return e;
+  bulk_free(h, s);
+  const uint64_t head = 3 * kPasses * kRadix + 16 + 2 * kRadix;
+  const uint64_t words = head + sort_status_words(cap);
+  e = pool_alloc(h, (void**)&h->bulk_meta, words * 4, s);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(h->bulk_meta, 0, words * 4, s);
+  if (e != cudaSuccess) return e;
+  SortScratch& B = h->bulk;
+  B.hist = h->bulk_meta;
+  B.bases = h->bulk_meta + 2 * kPasses * kRadix;
+  B.tile_ctr = h->bulk_meta + 3 * kPasses * kRadix;
+  B.err = h->sort.err;  // one sticky domain-error word per handle
+  B.done_ctr = B.tile_ctr + 5;
+  B.bkt = h->bulk_meta + 3 * kPasses * kRadix + 16;
+  B.status = h->bulk_meta + head;
+  B.overflow_dev = h->sort.overflow_dev;
+  B.overflow_host = h->sort.overflow_host;
+  B.lsd_only = h->sort.lsd_only;
+  B.tiles_cap = sort_tiles(cap);
+  for (int k = 0; k < 2; ++k) {
+    e = pool_alloc(h, (void**)&B.tmp_keys[k], cap * 4, s);
+    if (e != cudaSuccess) return e;
+    e = pool_alloc(h, (void**)&B.tmp_vals[k], cap * 4, s);
+    if (e != cudaSuccess) return e;
+  }
+  h->bulk_cap = cap;
+  return cudaSuccess;
+}
+
 cudaError_t ensure_qbuf(lsm* h, uint64_t bytes, cudaStream_t s) {
   if (h->qbuf_bytes >= bytes) return cudaSuccess;
   if (h->qbuf) cudaFreeAsync(h->qbuf, s);
@@ -239,10 +289,13 @@ LevelTable level_table(const lsm* h) {
       T.vals[c] = h->level[i].vals;
       T.idx[c] = h->level[i].idx;
       T.n[c] = h->b << i;
-      const uint64_t n3 = (idx_f3_len(T.n[c]) + 3) / 4 * 4;
-      if (off + n3 <= kF3SmemMax) {
+      // F3 is staged as a complete search tree in Eytzinger order: 2^h words
+      const uint32_t h3 = f3_tree_h(idx_f3_len(T.n[c]));
+      const uint64_t words = 1ull << h3;
+      T.f3_h[c] = h3;
+      if (off + words <= kF3SmemMax) {
         T.f3_smem_off[c] = off;
-        off += (uint32_t)n3;
+        off += (uint32_t)words;
       } else {
         T.f3_smem_off[c] = 0xFFFFFFFFu;  // searched in global memory
       }
@@ -346,6 +399,8 @@ lsm_status lsm_destroy(lsm_t* h) {
     if (h->sort.tmp_keys[k]) cudaFreeAsync(h->sort.tmp_keys[k], nullptr);
     if (h->sort.tmp_vals[k]) cudaFreeAsync(h->sort.tmp_vals[k], nullptr);
   }
+  bulk_free(h, nullptr);
+  buf_free(h->stage, nullptr);
   if (h->st_keys) cudaFreeAsync(h->st_keys, nullptr);
   if (h->st_vals) cudaFreeAsync(h->st_vals, nullptr);
   if (h->st_ops) cudaFreeAsync(h->st_ops, nullptr);
@@ -390,36 +445,26 @@ lsm_status lsm_clear(lsm_t* h, void* stream) {
 }
 
 // Insert(batch), PAPER.md:462-473 / Fig. 4 PAPER.md:662-677.
-static lsm_status do_update(lsm_t* h, const uint32_t* keys, const uint32_t* vals,
-                            const uint8_t* ops, int mode, uint64_t n, cudaStream_t s) {
-  if (!h || !keys) return LSM_ERR_INVALID_ARG;
-  if (n == 0 || n > h->b) return LSM_ERR_BATCH_SIZE;
-  if (mode == kModeMixed && ops == nullptr) mode = kModeInsert;
+// make room for one insert: level t's home buffer + index, and the cascade
+// scratch (sorted batch and ping-pong buffers) when t >= 1
+static lsm_status prepare_insert(lsm_t* h, int t, cudaStream_t s) {
   const uint64_t b = h->b;
-  const int t = ffz(h->r);  // first empty level (PAPER.md:864)
-  if (t >= LSM_MAX_LEVELS) return LSM_ERR_INVALID_ARG;
-  LaunchHooks hk = hooks(h);
-  CK(ensure_sort_scratch(h, s));
   CK(buf_ensure(h, h->home[t], b << t, s));
   CK(home_idx_ensure(h, t, s));
-  // sort (A1+A2): straight into level 0 when t == 0
-  uint32_t* sk = (t == 0) ? h->home[0].keys : nullptr;
-  uint32_t* sv = (t == 0) ? h->home[0].vals : nullptr;
-  if (t > 0) {
-    CK(buf_ensure(h, h->sortout, b, s));
-    sk = h->sortout.keys;
-    sv = h->sortout.vals;
-    if (t >= 2) {
-      CK(buf_ensure(h, h->ping[0], b << (t - 1), s));
-      CK(buf_ensure(h, h->ping[1], b << (t - 1), s));
-    }
+  if (t > 0) CK(buf_ensure(h, h->sortout, b, s));
+  if (t >= 2) {
+    CK(buf_ensure(h, h->ping[0], b << (t - 1), s));
+    CK(buf_ensure(h, h->ping[1], b << (t - 1), s));
   }
-  // the producer of level t also writes its fence keys F1 (t == 0: the sort)
-  CK(launch_sort_batch(keys, vals, ops, mode, n, b, h->sort, sk, sv,
-                       t == 0 ? h->home_idx[0] : nullptr, s, hk));
-  // cascade (A3): while level i is full, buffer <- merge(buffer, level i)
-  const uint32_t* ck = sk;
-  const uint32_t* cv = sv;
+  return LSM_OK;
+}
+
+// cascade (A3) of the sorted batch (ck, cv) with t = ffz(r) >= 1: while
+// level i is full, buffer <- merge(buffer, level i), newer first on ties
+// (PAPER.md:621-624); the last merge writes level t and its fence keys F1.
+static lsm_status cascade(lsm_t* h, const uint32_t* ck, const uint32_t* cv, int t,
+                          cudaStream_t s, const LaunchHooks& hk) {
+  const uint64_t b = h->b;
   for (int i = 0; i < t; ++i) {
     uint32_t* ok = (i == t - 1) ? h->home[t].keys : h->ping[i & 1].keys;
     uint32_t* ov = (i == t - 1) ? h->home[t].vals : h->ping[i & 1].vals;
@@ -430,13 +475,40 @@ static lsm_status do_update(lsm_t* h, const uint32_t* keys, const uint32_t* vals
     ck = ok;
     cv = ov;
   }
-  h->level[t].keys = h->home[t].keys;  // level t <- buffer
+  return LSM_OK;
+}
+
+// level t <- its home buffer; r += 1
+static void commit_insert(lsm_t* h, int t) {
+  h->level[t].keys = h->home[t].keys;
   h->level[t].vals = h->home[t].vals;
   h->level[t].owner = nullptr;
   h->level[t].idx = h->home_idx[t];
   h->level[t].idx_owned = false;
   h->level[t].idx_ready = false;  // F2/F3 derived before the next query
-  h->r += 1;  // num_batch++ 
+  h->r += 1;
+}
+
+static lsm_status do_update(lsm_t* h, const uint32_t* keys, const uint32_t* vals,
+                            const uint8_t* ops, int mode, uint64_t n, cudaStream_t s) {
+  if (!h || !keys) return LSM_ERR_INVALID_ARG;
+  if (n == 0 || n > h->b) return LSM_ERR_BATCH_SIZE;
+  if (mode == kModeMixed && ops == nullptr) mode = kModeInsert;
+  const uint64_t b = h->b;
+  const int t = ffz(h->r);  // first empty level (PAPER.md:864)
+  if (t >= LSM_MAX_LEVELS) return LSM_ERR_INVALID_ARG;
+  LaunchHooks hk = hooks(h);
+  CK(ensure_sort_scratch(h, s));
+  lsm_status st = prepare_insert(h, t, s);
+  if (st != LSM_OK) return st;
+  // sort (A1+A2): straight into level 0 (with its F1) when t == 0
+  uint32_t* sk = (t == 0) ? h->home[0].keys : h->sortout.keys;
+  uint32_t* sv = (t == 0) ? h->home[0].vals : h->sortout.vals;
+  CK(launch_sort_batch(keys, vals, ops, mode, n, b, h->sort, sk, sv,
+                       t == 0 ? h->home_idx[0] : nullptr, s, hk));
+  st = cascade(h, sk, sv, t, s, hk);
+  if (st != LSM_OK) return st;
+  commit_insert(h, t);
   return LSM_OK;
 }
 
@@ -452,6 +524,92 @@ lsm_status lsm_insert(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals, 
 
 lsm_status lsm_delete(lsm_t* h, const uint32_t* d_keys, uint64_t n, void* stream) {
   return do_update(h, d_keys, nullptr, nullptr, kModeDelete, n, S(stream));
+}
+
+// ---------------- N1: bulk build and multi-batch insertion ----------------
+// Bulk build: the n elements form one batch (rules 1-6 of
+// PAPER.md:260-279 apply across all of them, R24); they are encoded, padded
+// with placebos to k*b (k = ceil(n/b)), sorted once, and the sorted array is
+// segmented into the levels at the set bits of k -- ascending key slices into
+// ascending levels, as views of one buffer (like cleanup, R12). r = k.
+lsm_status lsm_bulk_build(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals,
+                          const uint8_t* d_is_delete, uint64_t n, void* stream) {
+  if (!h || !d_keys) return LSM_ERR_INVALID_ARG;
+  if (h->r != 0) return LSM_ERR_INVALID_ARG;  // only into an empty dictionary
+  if (n == 0) return LSM_ERR_BATCH_SIZE;
+  const uint64_t b = h->b;
+  const uint64_t k = (n + b - 1) / b;
+  if (k >= (1ull << LSM_MAX_LEVELS) || k * b > (1ull << 32)) return LSM_ERR_INVALID_ARG;
+  cudaStream_t s = S(stream);
+  LaunchHooks hk = hooks(h);
+  const int mode = d_is_delete ? kModeMixed : kModeInsert;
+  Buffer* C = new Buffer;
+  cudaError_t e = buf_ensure(h, *C, k * b, s);
+  if (e == cudaSuccess) e = ensure_bulk_scratch(h, k * b, s);
+  if (e == cudaSuccess)
+    e = launch_sort_batch(d_keys, d_vals, d_is_delete, mode, n, k * b, h->bulk, C->keys, C->vals,
+                          nullptr, s, hk);
+  if (e != cudaSuccess) {
+    buf_free(*C, s);
+    delete C;
+    return cuda_err(e);
+  }
+  h->sort.lsd_only = h->sort.lsd_only || h->bulk.lsd_only;
+  uint64_t off = 0;
+  int refs = 0;
+  for (int i = 0; i < LSM_MAX_LEVELS; ++i) {
+    if (!((k >> i) & 1ull)) continue;
+    h->level[i].keys = C->keys + off;
+    h->level[i].vals = C->vals + off;
+    h->level[i].owner = C;
+    ++refs;
+    C->refs = refs;
+    CK(pool_alloc(h, (void**)&h->level[i].idx, idx_words(b << i) * 4, s));
+    h->level[i].idx_owned = true;
+    h->level[i].idx_ready = false;
+    CK(launch_build_f1(h->level[i].keys, b << i, h->level[i].idx, s, hk));
+    off += b << i;
+  }
+  h->r = k;
+  return LSM_OK;
+}
+
+// Multi-batch insertion (footnote of PAPER.md:860): k = ceil(n/b) consecutive
+// batches (batch j = elements [j*b, (j+1)*b), the last possibly partial),
+// oldest first. All batches are sorted first (small b: one launch, one CTA per
+// batch), then each is merged in, oldest to newest, exactly as k calls of
+// lsm_update would (same levels bit for bit).
+lsm_status lsm_update_batches(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals,
+                              const uint8_t* d_is_delete, uint64_t n, void* stream) {
+  if (!h || !d_keys) return LSM_ERR_INVALID_ARG;
+  if (n == 0) return LSM_ERR_BATCH_SIZE;
+  const uint64_t b = h->b;
+  const uint64_t k = (n + b - 1) / b;
+  if (h->r + k >= (1ull << LSM_MAX_LEVELS)) return LSM_ERR_INVALID_ARG;
+  cudaStream_t s = S(stream);
+  LaunchHooks hk = hooks(h);
+  const int mode = d_is_delete ? kModeMixed : kModeInsert;
+  CK(ensure_sort_scratch(h, s));
+  CK(buf_ensure(h, h->stage, k * b, s));
+  CK(launch_sort_segments(d_keys, d_vals, d_is_delete, mode, n, b, k, h->sort, h->stage.keys,
+                          h->stage.vals, s, hk));
+  for (uint64_t j = 0; j < k; ++j) {
+    const int t = ffz(h->r);
+    lsm_status st = prepare_insert(h, t, s);
+    if (st != LSM_OK) return st;
+    const uint32_t* ck = h->stage.keys + j * b;
+    const uint32_t* cv = h->stage.vals + j * b;
+    if (t == 0) {  // level 0 <- the sorted batch, and its fence keys
+      CK(cudaMemcpyAsync(h->home[0].keys, ck, b * 4, cudaMemcpyDeviceToDevice, s));
+      CK(cudaMemcpyAsync(h->home[0].vals, cv, b * 4, cudaMemcpyDeviceToDevice, s));
+      CK(launch_build_f1(h->home[0].keys, b, h->home_idx[0], s, hk));
+    } else {
+      st = cascade(h, ck, cv, t, s, hk);
+      if (st != LSM_OK) return st;
+    }
+    commit_insert(h, t);
+  }
+  return LSM_OK;
 }
 
 lsm_status lsm_update_host(lsm_t* h, const uint32_t* h_keys, const uint32_t* h_vals,
@@ -504,6 +662,28 @@ lsm_status lsm_lookup_host(lsm_t* h, const uint32_t* h_q, uint64_t nq, uint32_t*
   return LSM_OK;
 }
 
+static lsm_status order_query(lsm_t* h, const uint32_t* d_q, uint64_t nq, bool succ,
+                              uint32_t* d_keys_out, uint32_t* d_vals_out, uint8_t* d_found_out,
+                              void* stream) {
+  if (!h) return LSM_ERR_INVALID_ARG;
+  if (nq == 0) return LSM_OK;
+  if (!d_q || !d_keys_out || !d_vals_out) return LSM_ERR_INVALID_ARG;
+  CK(ensure_index(h, S(stream), hooks(h)));
+  LevelTable T = level_table(h);
+  CK(launch_order(T, d_q, nq, succ, d_keys_out, d_vals_out, d_found_out, S(stream), hooks(h)));
+  return LSM_OK;
+}
+
+lsm_status lsm_successor(lsm_t* h, const uint32_t* d_q, uint64_t nq, uint32_t* d_keys_out,
+                         uint32_t* d_vals_out, uint8_t* d_found_out, void* stream) {
+  return order_query(h, d_q, nq, true, d_keys_out, d_vals_out, d_found_out, stream);
+}
+
+lsm_status lsm_predecessor(lsm_t* h, const uint32_t* d_q, uint64_t nq, uint32_t* d_keys_out,
+                           uint32_t* d_vals_out, uint8_t* d_found_out, void* stream) {
+  return order_query(h, d_q, nq, false, d_keys_out, d_vals_out, d_found_out, stream);
+}
+
 lsm_status lsm_count(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2, uint64_t nq,
                      uint32_t* d_counts_out, void* stream) {
   if (!h) return LSM_ERR_INVALID_ARG;
@@ -529,16 +709,31 @@ lsm_status lsm_range(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2, uint6
   if (!d_k1 || !d_k2) return LSM_ERR_INVALID_ARG;
   LaunchHooks hk = hooks(h);
   if (capacity > 0 && (!d_keys_out || !d_vals_out)) return LSM_ERR_INVALID_ARG;
-  CK(ensure_qbuf(h, range_scratch_words(nq) * 8, s));
   CK(ensure_index(h, s, hk));
   LevelTable T = level_table(h);
-  // one pass: bounds, count, warp scan + look-back offsets, pairs
-  CK(launch_range(T, d_k1, d_k2, nq, d_offsets_out, d_keys_out, d_vals_out, capacity,
-                  static_cast<unsigned long long*>(h->qbuf), s, hk));
+  if (range3_ok(T)) {
+    // count + saved start positions, scan of the counts, write walk
+    CK(ensure_qbuf(h, range3_scratch_bytes(T, nq), s));
+    CK(launch_range3(T, d_k1, d_k2, nq, d_offsets_out, d_keys_out, d_vals_out, capacity, h->qbuf,
+                     s, hk));
+  } else {
+    // one pass: bounds, count, warp scan + look-back offsets, pairs
+    CK(ensure_qbuf(h, range_scratch_words(nq) * 8, s));
+    CK(launch_range(T, d_k1, d_k2, nq, d_offsets_out, d_keys_out, d_vals_out, capacity,
+                    static_cast<unsigned long long*>(h->qbuf), s, hk));
+  }
   CK(cudaMemcpyAsync(h->h_pinned, d_offsets_out + nq, 8, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   const uint64_t total = h->h_pinned[0];
   *total_out = total;
+  if (h->prof_on) {  // the pairs written (8 B each) join the range's bytes
+    for (auto it = h->prof.rbegin(); it != h->prof.rend(); ++it) {
+      if (it->cls == LSM_K_RANGE) {
+        it->bytes += 8.0 * (double)std::min(total, capacity);
+        break;
+      }
+    }
+  }
   if (total > capacity) return LSM_ERR_CAPACITY;
   return LSM_OK;
 }

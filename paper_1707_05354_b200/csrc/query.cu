@@ -28,6 +28,8 @@
 // one coalesced load and a ballot counts the fences below the query, so a
 // step issues 32 independent line loads per warp.
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace gpulsm {
@@ -43,9 +45,10 @@ struct LvView {
   const uint32_t* V;
   const uint32_t* f1;
   const uint32_t* f2;
-  const uint32_t* f3;  // shared memory when staged, else global
+  const uint32_t* f3;  // smem: Eytzinger tree E[1..2^h); global: sorted
   uint64_t n;
   uint32_t n1, n2, n3;
+  uint32_t h3;  // > 0: f3 is the staged tree of height h3
 };
 
 __device__ __forceinline__ LvView level_view(const LevelTable& T, int j, const uint32_t* sF3) {
@@ -56,20 +59,34 @@ __device__ __forceinline__ LvView level_view(const LevelTable& T, int j, const u
   const uint32_t* idx = T.idx[j];
   L.f1 = idx;
   L.f2 = idx + idx_f2_off(L.n);
-  L.f3 = T.f3_smem_off[j] != 0xFFFFFFFFu ? sF3 + T.f3_smem_off[j] : idx + idx_f3_off(L.n);
+  const bool staged = T.f3_smem_off[j] != 0xFFFFFFFFu;
+  L.f3 = staged ? sF3 + T.f3_smem_off[j] : idx + idx_f3_off(L.n);
+  L.h3 = staged ? T.f3_h[j] : 0u;
   L.n1 = (uint32_t)idx_f1_len(L.n);
   L.n2 = (uint32_t)idx_f2_len(L.n);
   L.n3 = (uint32_t)idx_f3_len(L.n);
   return L;
 }
 
-// Stage the F3 arrays that fit into shared memory (kF3SmemMax words).
+// Stage F3 of the levels that fit into shared memory (kF3SmemMax words) as a
+// complete binary search tree in Eytzinger (breadth-first) order: node e at
+// depth d = floor(log2 e), position p = e - 2^d holds the entry of inorder
+// rank (2p+1) * 2^(h-1-d) - 1, padding ranks >= n3 with 0xFFFFFFFF (never
+// below a query). The first levels of the tree then sit in the first words,
+// so the warp's early search steps touch distinct banks, and the search path
+// IS the rank (f3_count).
 __device__ __forceinline__ void stage_f3(const LevelTable& T, uint32_t* sF3) {
   for (int j = 0; j < T.count; ++j) {
     if (T.f3_smem_off[j] == 0xFFFFFFFFu) continue;
     const uint32_t* g = T.idx[j] + idx_f3_off(T.n[j]);
     const uint32_t n3 = (uint32_t)idx_f3_len(T.n[j]);
-    for (uint32_t i = threadIdx.x; i < n3; i += blockDim.x) sF3[T.f3_smem_off[j] + i] = __ldg(g + i);
+    const uint32_t h = T.f3_h[j];
+    uint32_t* E = sF3 + T.f3_smem_off[j];
+    for (uint32_t e = threadIdx.x + 1; e < (1u << h); e += blockDim.x) {
+      const uint32_t d = 31 - __clz(e);
+      const uint32_t rank = ((2u * (e - (1u << d)) + 1u) << (h - 1 - d)) - 1u;
+      E[e] = rank < n3 ? __ldg(g + rank) : 0xFFFFFFFFu;
+    }
   }
   __syncthreads();
 }
@@ -89,75 +106,13 @@ __device__ __forceinline__ uint32_t count_below(const uint32_t* a, uint32_t len,
   return lo;
 }
 
-// For every lane: entries of a[32*ln .. 32*ln+32) (within [0, len)) with
-// (entry >> 1) < x, where ln and x are the lane's own. The warp loads each
-// lane's line with one coalesced 128-byte load, then counts with a ballot.
-__device__ __forceinline__ uint32_t coop_line_count(const uint32_t* __restrict__ a, uint32_t len,
-                                                    uint32_t ln, uint32_t x) {
-  const uint32_t lane = lane_id();
-  uint32_t res = 0;
-#pragma unroll
-  for (int h = 0; h < 32; h += 16) {  // two rounds of 16 independent line loads
-    uint32_t v[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const uint32_t lj = __shfl_sync(kFull, ln, h + j);
-      const uint64_t i = (uint64_t)lj * 32 + lane;
-      v[j] = i < len ? __ldg(a + i) : 0u;
-    }
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const uint32_t lj = __shfl_sync(kFull, ln, h + j);
-      const uint32_t xj = __shfl_sync(kFull, x, h + j);
-      const bool below = ((uint64_t)lj * 32 + lane < len) && ((v[j] >> 1) < xj);
-      const uint32_t m = __ballot_sync(kFull, below);
-      if (lane == (uint32_t)(h + j)) res = __popc(m);
-    }
-  }
-  return res;
-}
-
-// Same for 8-record groups of K: four queries per warp load (lanes 8s..8s+7
-// read query 4i+s's group).
-__device__ __forceinline__ uint32_t coop_group_count(const uint32_t* __restrict__ K, uint64_t n,
-                                                     uint32_t g, uint32_t x) {
-  const uint32_t lane = lane_id();
-  const uint32_t sub = lane >> 3, e = lane & 7;
-  uint32_t v[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint32_t gj = __shfl_sync(kFull, g, 4 * i + sub);
-    const uint64_t idx = (uint64_t)gj * kF1Step + e;
-    v[i] = idx < n ? __ldg(K + idx) : 0u;
-  }
-  uint32_t res = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint32_t gj = __shfl_sync(kFull, g, 4 * i + sub);
-    const uint32_t xj = __shfl_sync(kFull, x, 4 * i + sub);
-    const bool below = ((uint64_t)gj * kF1Step + e < n) && ((v[i] >> 1) < xj);
-    const uint32_t m = __ballot_sync(kFull, below);
-    const uint32_t cg = __popc((m >> (8 * sub)) & 0xFFu);
-    const uint32_t t = __shfl_sync(kFull, cg, 8 * (lane & 3));
-    if ((lane >> 2) == (uint32_t)i) res = t;
-  }
-  return res;
-}
-
-// lower_bound on the original key for every lane's x: the first position p
-// with (K[p] >> 1) >= x. Whole warp; each lane may have a different x.
-// F3[c3-1] < x <= F3[c3] brackets 8192 records; the F2 line below it, the F1
-// line below that and the 8-record group below that narrow it to p.
-__device__ __noinline__ uint64_t coop_lower_bound(const LvView L, uint32_t x) {
-  const uint32_t c3 = count_below(L.f3, L.n3, x);
-  const bool zero = c3 == 0;  // K[0] >= x
-  const uint32_t l2 = zero ? 0u : c3 - 1;
-  const uint32_t c2 = l2 * kFanout + coop_line_count(L.f2, L.n2, l2, x);
-  const uint32_t l1 = zero ? 0u : c2 - 1;
-  const uint32_t c1 = l1 * kFanout + coop_line_count(L.f1, L.n1, l1, x);
-  const uint32_t g = zero ? 0u : c1 - 1;
-  const uint64_t p = (uint64_t)g * kF1Step + coop_group_count(L.K, L.n, g, x);
-  return zero ? 0ull : p;
+// F3 entries below x: h steps down the staged tree (the path bits are the
+// rank), or a binary search of the sorted global copy.
+__device__ __forceinline__ uint32_t f3_count(const LvView& L, uint32_t x) {
+  if (L.h3 == 0) return count_below(L.f3, L.n3, x);
+  uint32_t e = 1;
+  for (uint32_t k = 0; k < L.h3; ++k) e = 2 * e + ((L.f3[e] >> 1) < x);
+  return e - (1u << L.h3);
 }
 
 // Entries of a[base .. base+len_run) below x (orig < x), given a[base] < x:
@@ -178,9 +133,8 @@ __device__ __forceinline__ uint32_t run_count(const uint32_t* __restrict__ a, ui
 }
 
 // Entries of the 32-entry line a[32*ln ..) (within len) below x, given that
-// its first entry is below x. One round trip loads the three other sector
-// heads (the whole line lands in L1), then a search inside the chosen
-// 8-entry sector hits L1.
+// its first entry is below x (lane-private): the three other sector heads,
+// then a search inside the chosen 8-entry sector.
 __device__ __forceinline__ uint32_t line_count(const uint32_t* __restrict__ a, uint64_t len,
                                                uint32_t ln, uint32_t x) {
   const uint64_t base = (uint64_t)ln * kFanout;
@@ -195,15 +149,118 @@ __device__ __forceinline__ uint32_t line_count(const uint32_t* __restrict__ a, u
 }
 
 // Lane-private lower_bound on the original key through the fence index:
-// F3 (shared memory) -> F2 line -> F1 line -> 8-record group of K.
+// F3 tree (shared memory) -> F2 line -> F1 line -> 8-record group of K.
+// Used where lanes diverge (the successor/predecessor run skips).
 __device__ __forceinline__ uint64_t idx_lower_bound(const LvView& L, uint32_t x) {
   if (x > 0x7FFFFFFFu) return L.n;  // above every original key (R8)
-  const uint32_t c3 = count_below(L.f3, L.n3, x);
+  const uint32_t c3 = f3_count(L, x);
   if (c3 == 0) return 0;  // K[0] >= x
   const uint32_t c2 = (c3 - 1) * kFanout + line_count(L.f2, L.n2, c3 - 1, x);
   const uint32_t c1 = (c2 - 1) * kFanout + line_count(L.f1, L.n1, c2 - 1, x);
   const uint64_t g = (uint64_t)(c1 - 1) * kF1Step;
   return g + run_count(L.K, g, (uint32_t)(L.n - g < kF1Step ? L.n - g : kF1Step), x);
+}
+
+// ---- warp-cooperative steps (all 32 lanes, each with its own query) ----
+// The per-lane search above issues about six uncoalesced loads per line, and
+// a warp load whose lanes hit 32 different lines costs 32 L1 wavefronts: the
+// query kernels were L1-wavefront bound (profiles/r01_ncu_full_summary.txt).
+// Here 4 lanes read one query's 128-byte line with two 16-byte loads each, so
+// one warp load serves 8 queries for 8 wavefronts. Comparisons use the packed
+// form: (k >> 1) < x  <=>  k < 2x for x <= 2^31 - 1 (x2 below).
+
+__device__ __forceinline__ uint32_t dbl(uint32_t x) { return x > 0x7FFFFFFFu ? 0xFFFFFFFFu : 2 * x; }
+
+// For every lane: entries of the line a[32*ln ..) below x (x2 = dbl(x)).
+// The padding of the last line holds 0xFFFFFFFF (finalize_index_kernel).
+__device__ __forceinline__ uint32_t grp_line_count(const uint32_t* __restrict__ a, uint32_t ln,
+                                                   uint32_t x2) {
+  const uint32_t lane = lane_id(), e = lane & 3;
+  const uint4* A = reinterpret_cast<const uint4*>(a);
+  uint32_t res = 0;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const uint32_t src = (lane & ~3u) | r;  // round r: lanes 4G..4G+3 serve lane 4G+r
+    const uint32_t lj = __shfl_sync(kFull, ln, src);
+    const uint32_t xj = __shfl_sync(kFull, x2, src);
+    const uint4 v0 = __ldg(A + lj * 8 + 2 * e);
+    const uint4 v1 = __ldg(A + lj * 8 + 2 * e + 1);
+    uint32_t c = (v0.x < xj) + (v0.y < xj) + (v0.z < xj) + (v0.w < xj) + (v1.x < xj) +
+                 (v1.y < xj) + (v1.z < xj) + (v1.w < xj);
+    c += __shfl_xor_sync(kFull, c, 1);
+    c += __shfl_xor_sync(kFull, c, 2);
+    if (e == (uint32_t)r) res = c;
+  }
+  return res;
+}
+
+// For every lane: records of the 8-record group K[8*gi ..) (within n) below
+// x. 16-byte aligned K: 2 lanes x 16 B per query, 16 queries per load;
+// otherwise 8 lanes x 4 B, 4 queries per load.
+__device__ __forceinline__ uint32_t grp_group_count(const uint32_t* __restrict__ K, uint64_t n,
+                                                    uint32_t gi, uint32_t x2) {
+  const uint32_t lane = lane_id();
+  uint32_t res = 0;
+  if ((reinterpret_cast<uintptr_t>(K) & 15) == 0) {
+    const uint32_t hf = lane & 1;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const uint32_t src = (lane & ~1u) | r;  // round r: lanes 2P, 2P+1 serve lane 2P+r
+      const uint32_t gj = __shfl_sync(kFull, gi, src);
+      const uint32_t xj = __shfl_sync(kFull, x2, src);
+      const uint64_t base = (uint64_t)gj * kF1Step + 4 * hf;
+      uint4 v = __ldg(reinterpret_cast<const uint4*>(K + base));  // +16 words of slack
+      if (base + 4 > n) {  // the level's last group
+        if (base + 0 >= n) v.x = 0xFFFFFFFFu;
+        if (base + 1 >= n) v.y = 0xFFFFFFFFu;
+        if (base + 2 >= n) v.z = 0xFFFFFFFFu;
+        v.w = 0xFFFFFFFFu;
+      }
+      uint32_t c = (v.x < xj) + (v.y < xj) + (v.z < xj) + (v.w < xj);
+      c += __shfl_xor_sync(kFull, c, 1);
+      if (hf == (uint32_t)r) res = c;
+    }
+  } else {
+    const uint32_t sub = lane >> 3, e = lane & 7;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const uint32_t src = 4 * r + sub;
+      const uint32_t gj = __shfl_sync(kFull, gi, src);
+      const uint32_t xj = __shfl_sync(kFull, x2, src);
+      const uint64_t idx = (uint64_t)gj * kF1Step + e;
+      const bool below = idx < n && __ldg(K + idx) < xj;
+      const uint32_t m = __ballot_sync(kFull, below);
+      const uint32_t t = __popc((m >> (8 * (lane & 3))) & 0xFFu);
+      if ((lane >> 2) == (uint32_t)r) res = t;
+    }
+  }
+  return res;
+}
+
+// F3 entries below x through the staged tree (packed compare, x2 = dbl(x)).
+__device__ __forceinline__ uint32_t f3_count2(const LvView& L, uint32_t x, uint32_t x2) {
+  if (L.h3 == 0) return count_below(L.f3, L.n3, x);
+  uint32_t e = 1;
+  for (uint32_t k = 0; k < L.h3; ++k) e = 2 * e + (L.f3[e] < x2);
+  return e - (1u << L.h3);
+}
+
+// lower_bound on the original key for every lane's x (whole warp): the first
+// position p with (K[p] >> 1) >= x. F3[c3-1] < x <= F3[c3] brackets 8192
+// records; the F2 line below it, the F1 line below that and the 8-record
+// group below that narrow it to p.
+__device__ __noinline__ uint64_t warp_lower_bound(const LvView L, uint32_t x) {
+  const uint32_t x2 = dbl(x);
+  const uint32_t c3 = f3_count2(L, x, x2);
+  const bool zero = c3 == 0;  // K[0] >= x
+  const uint32_t l2 = zero ? 0u : c3 - 1;
+  const uint32_t c2 = l2 * kFanout + grp_line_count(L.f2, l2, x2);
+  const uint32_t l1 = zero ? 0u : c2 - 1;
+  const uint32_t c1 = l1 * kFanout + grp_line_count(L.f1, l1, x2);
+  const uint32_t g = zero ? 0u : c1 - 1;
+  const uint64_t p = (uint64_t)g * kF1Step + grp_group_count(L.K, L.n, g, x2);
+  if (x > 0x7FFFFFFFu) return L.n;  // above every original key (R8)
+  return zero ? 0ull : p;
 }
 
 // x for an upper bound: (K[p] >> 1) <= z  <=>  (K[p] >> 1) < z + 1
@@ -229,7 +286,7 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) lookup_kernel(
     for (int j = 0; j < T.count; ++j) {
       if (__all_sync(kFull, done)) break;
       const LvView L = level_view(T, j, sF3);
-      const uint64_t p = done ? L.n : idx_lower_bound(L, x);
+      const uint64_t p = warp_lower_bound(L, x);  // every lane takes part
       if (!done && p < L.n) {
         const uint32_t kk = __ldg(L.K + p);
         if ((kk >> 1) == x) {
@@ -248,17 +305,27 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) lookup_kernel(
   }
 }
 
-// Per-query walk over the candidate slices [pos_j, end_j) of the occupied
-// levels (state in registers for NL > 0). emit(idx, key, val) is called for
-// each valid key in ascending order; returns the number of valid keys.
+// Per-query walk over the candidate slices of the occupied levels: level j's
+// slice starts at pos_j = lower_bound(k1) and ends at the first key above z
+// = k2 (found by the walk itself, so the paper's upper_bound search of stage
+// 1 is not needed; state in registers for NL > 0). emit(idx, key, val) is
+// called for each valid key in ascending order; returns the number of valid
+// keys.
 template <int NL, typename Emit>
-__device__ __forceinline__ uint32_t walk_slices(const LevelTable& T, uint64_t* pos, uint64_t* end,
+__device__ __forceinline__ uint32_t walk_slices(const LevelTable& T, uint64_t* pos, uint32_t z,
                                                 int L, Emit emit) {
   constexpr int CAP = NL > 0 ? NL : LSM_MAX_LEVELS;
   uint32_t head[CAP];
 #pragma unroll
-  for (int j = 0; j < CAP; ++j)
-    if (j < L) head[j] = pos[j] < end[j] ? (__ldg(T.keys[j] + pos[j]) >> 1) : kSent;
+  for (int j = 0; j < CAP; ++j) {
+    if (j < L) {
+      head[j] = kSent;
+      if (pos[j] < T.n[j]) {
+        const uint32_t k = __ldg(T.keys[j] + pos[j]) >> 1;
+        if (k <= z) head[j] = k;
+      }
+    }
+  }
   uint32_t cnt = 0;
   while (true) {
     uint32_t m = kSent;
@@ -272,6 +339,7 @@ __device__ __forceinline__ uint32_t walk_slices(const LevelTable& T, uint64_t* p
     for (int j = 0; j < CAP; ++j) {
       if (j < L && head[j] == m) {
         const uint32_t* K = T.keys[j];
+        const uint64_t n = T.n[j];
         uint64_t p = pos[j];
         if (first) {  // newest record of key m: run head in the lowest level
           first = false;
@@ -280,13 +348,13 @@ __device__ __forceinline__ uint32_t walk_slices(const LevelTable& T, uint64_t* p
         }
         // skip the rest of this level's run of key m (stale copies)
         uint32_t nk = kSent;
-        while (++p < end[j]) {
+        while (++p < n) {
           nk = __ldg(K + p) >> 1;
           if (nk != m) break;
           nk = kSent;
         }
         pos[j] = p;
-        head[j] = p < end[j] ? nk : kSent;
+        head[j] = nk <= z ? nk : kSent;
       }
     }
     if (valid) {
@@ -297,29 +365,28 @@ __device__ __forceinline__ uint32_t walk_slices(const LevelTable& T, uint64_t* p
   return cnt;
 }
 
-// Stage 1 for all occupied levels: [l_j, u_j) = [lower_bound(k1),
-// upper_bound(k2)) per level, cooperative across the warp; empty when k1 > k2
-// (R9).
+// Stage 1 for all occupied levels: pos_j = lower_bound(k1) per level,
+// cooperative across the warp; empty (pos_j = n_j) when k1 > k2 (R9).
 template <int NL>
 __device__ __forceinline__ void bounds(const LevelTable& T, const uint32_t* sF3, uint32_t a,
-                                       uint32_t z, bool empty, uint64_t* pos, uint64_t* end,
-                                       int L) {
+                                       bool empty, uint64_t* pos, int L) {
   constexpr int CAP = NL > 0 ? NL : LSM_MAX_LEVELS;
-  const uint32_t xz = ub_arg(z);
 #pragma unroll
   for (int j = 0; j < CAP; ++j) {
     if (j < L) {
       const LvView V = level_view(T, j, sF3);
-      pos[j] = empty ? 0 : idx_lower_bound(V, a);
-      end[j] = empty ? 0 : idx_lower_bound(V, xz);
+      const uint64_t lo = warp_lower_bound(V, a);  // whole warp
+      pos[j] = empty ? V.n : lo;
     }
   }
 }
 
-template <int NL>
-__global__ void __launch_bounds__(kQThreads, 1) count_kernel(
+// Count (A5). SAVE (range's first pass): also store every level's start
+// position pos_out[j * nq + i] (u32) for the write pass.
+template <int NL, bool SAVE>
+__global__ void __launch_bounds__(kQThreads, kQCtasPerSm) count_kernel(
     LevelTable T, const uint32_t* __restrict__ k1, const uint32_t* __restrict__ k2, uint64_t nq,
-    uint32_t* __restrict__ counts) {
+    uint32_t* __restrict__ counts, uint32_t* __restrict__ pos_out) {
   extern __shared__ uint32_t sF3[];
   stage_f3(T, sF3);
   constexpr int CAP = NL > 0 ? NL : LSM_MAX_LEVELS;
@@ -331,10 +398,43 @@ __global__ void __launch_bounds__(kQThreads, 1) count_kernel(
     const uint64_t i = base + lane;
     const bool act = i < nq;
     const uint32_t a = act ? __ldg(k1 + i) : 1u, z = act ? __ldg(k2 + i) : 0u;
-    uint64_t pos[CAP], end[CAP];
-    bounds<NL>(T, sF3, a, z, a > z, pos, end, L);
-    const uint32_t c = walk_slices<NL>(T, pos, end, L, [](uint32_t, uint32_t, uint32_t) {});
+    uint64_t pos[CAP];
+    bounds<NL>(T, sF3, a, a > z, pos, L);
+    if (SAVE && act) {
+#pragma unroll
+      for (int j = 0; j < CAP; ++j)
+        if (j < L) pos_out[(uint64_t)j * nq + i] = (uint32_t)pos[j];
+    }
+    const uint32_t c = walk_slices<NL>(T, pos, z, L, [](uint32_t, uint32_t, uint32_t) {});
     if (act) counts[i] = c;
+  }
+}
+
+// Range (A6) write pass: from the saved start positions and the scanned
+// offsets, walk again and emit the valid pairs in key order.
+template <int NL>
+__global__ void __launch_bounds__(kQThreads, kQCtasPerSm) range_write_kernel(
+    LevelTable T, const uint32_t* __restrict__ k2, uint64_t nq,
+    const uint32_t* __restrict__ pos_in, const uint64_t* __restrict__ offsets,
+    uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint64_t capacity) {
+  constexpr int CAP = NL > 0 ? NL : LSM_MAX_LEVELS;
+  const int L = NL > 0 ? NL : T.count;
+  const uint64_t stride = (uint64_t)gridDim.x * kQThreads;
+  for (uint64_t i = (uint64_t)blockIdx.x * kQThreads + threadIdx.x; i < nq; i += stride) {
+    const uint32_t z = __ldg(k2 + i);
+    const uint64_t base = __ldg(offsets + i);
+    if (__ldg(offsets + i + 1) == base) continue;  // nothing valid
+    uint64_t pos[CAP];
+#pragma unroll
+    for (int j = 0; j < CAP; ++j)
+      if (j < L) pos[j] = __ldg(pos_in + (uint64_t)j * nq + i);
+    walk_slices<NL>(T, pos, z, L, [&](uint32_t k, uint32_t key, uint32_t val) {
+      const uint64_t o = base + k;
+      if (o < capacity) {
+        keys_out[o] = key;
+        vals_out[o] = val;
+      }
+    });
   }
 }
 
@@ -389,7 +489,7 @@ __device__ __forceinline__ uint64_t task_lookback(unsigned long long* status, ui
 }
 
 template <int NL>
-__global__ void __launch_bounds__(kQThreads, 1) range_kernel(
+__global__ void __launch_bounds__(kQThreads, kQCtasPerSm) range_kernel(
     LevelTable T, const uint32_t* __restrict__ k1, const uint32_t* __restrict__ k2, uint64_t nq,
     uint64_t* __restrict__ offsets, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out, uint64_t capacity, unsigned long long* __restrict__ ctr,
@@ -410,12 +510,12 @@ __global__ void __launch_bounds__(kQThreads, 1) range_kernel(
     const uint64_t i = t * 32 + lane;
     const bool act = i < nq;
     const uint32_t a = act ? __ldg(k1 + i) : 1u, z = act ? __ldg(k2 + i) : 0u;
-    uint64_t pos[CAP], end[CAP], pos0[CAP];
-    bounds<NL>(T, sF3, a, z, a > z, pos, end, L);
+    uint64_t pos[CAP], pos0[CAP];
+    bounds<NL>(T, sF3, a, a > z, pos, L);
 #pragma unroll
     for (int j = 0; j < CAP; ++j)
       if (j < L) pos0[j] = pos[j];
-    const uint32_t c = walk_slices<NL>(T, pos, end, L, [](uint32_t, uint32_t, uint32_t) {});
+    const uint32_t c = walk_slices<NL>(T, pos, z, L, [](uint32_t, uint32_t, uint32_t) {});
     // warp exclusive scan of the counts
     uint64_t x = c;
 #pragma unroll
@@ -427,13 +527,127 @@ __global__ void __launch_bounds__(kQThreads, 1) range_kernel(
     const uint64_t base = task_lookback(status, t, wtot) + x - c;
     if (act) offsets[i] = base;
     if (t == ntasks - 1 && lane == 31) offsets[nq] = base + c;
-    walk_slices<NL>(T, pos0, end, L, [&](uint32_t k, uint32_t key, uint32_t val) {
+    walk_slices<NL>(T, pos0, z, L, [&](uint32_t k, uint32_t key, uint32_t val) {
       const uint64_t o = base + k;
       if (o < capacity) {
         keys_out[o] = key;
         vals_out[o] = val;
       }
     });
+  }
+}
+
+// ---- N3: successor / predecessor (PAPER.md:113 footnote; reading R23) ----
+// One cursor per occupied level: at lower_bound(x) (successor) or at
+// upper_bound(x) - 1 (predecessor). The candidate key m is the minimum
+// (maximum) of the cursor heads; its newest record is the run head in the
+// lowest level that holds m. A regular head is
+// the answer; a tombstone head means m is deleted, every level holding m
+// moves its cursor past m's run, and the walk goes on.
+
+// First index after the run of m that contains p. Runs are short unless a
+// key repeats a lot (placebo padding, hot keys), so look at the next few
+// records first and fall back to an index search.
+__device__ __forceinline__ uint64_t run_end(const LvView& V, uint64_t p, uint32_t m) {
+#pragma unroll 1
+  for (int s = 0; s < 4; ++s) {
+    if (++p >= V.n) return V.n;
+    if ((__ldg(V.K + p) >> 1) != m) return p;
+  }
+  return idx_lower_bound(V, ub_arg(m));
+}
+
+// First index of the run of m that contains p.
+__device__ __forceinline__ uint64_t run_start(const LvView& V, uint64_t p, uint32_t m) {
+#pragma unroll 1
+  for (int s = 0; s < 4; ++s) {
+    if (p == 0 || (__ldg(V.K + p - 1) >> 1) != m) return p;
+    --p;
+  }
+  return idx_lower_bound(V, m);
+}
+
+template <int NL, bool SUCC>
+__global__ void __launch_bounds__(kQThreads, kQCtasPerSm) order_kernel(
+    LevelTable T, const uint32_t* __restrict__ q, uint64_t nq, uint32_t* __restrict__ keys_out,
+    uint32_t* __restrict__ vals_out, uint8_t* __restrict__ found_out) {
+  extern __shared__ uint32_t sF3[];
+  stage_f3(T, sF3);
+  constexpr int CAP = NL > 0 ? NL : LSM_MAX_LEVELS;
+  const int L = NL > 0 ? NL : T.count;
+  const uint32_t lane = lane_id();
+  const uint64_t gw = ((uint64_t)blockIdx.x * kQThreads + threadIdx.x) / 32;
+  const uint64_t nw = (uint64_t)gridDim.x * kQThreads / 32;
+  for (uint64_t wb = gw * 32; wb < nq; wb += nw * 32) {  // warp-uniform loop
+    const uint64_t i = wb + lane;
+    const bool act = i < nq;
+    const uint32_t x = act ? __ldg(q + i) : 0u;
+    uint64_t pos[CAP];
+    uint32_t head[CAP];  // successor: key (kSent = none); predecessor: key + 1 (0 = none)
+#pragma unroll
+    for (int j = 0; j < CAP; ++j) {
+      if (j < L) {
+        const LvView V = level_view(T, j, sF3);
+        const uint64_t u0 = warp_lower_bound(V, SUCC ? x : ub_arg(x));  // whole warp
+        if (SUCC) {
+          pos[j] = act ? u0 : V.n;
+          head[j] = pos[j] < V.n ? (__ldg(V.K + pos[j]) >> 1) : kSent;
+        } else {
+          const uint64_t u = act ? u0 : 0;
+          pos[j] = u - 1;
+          head[j] = u > 0 ? (__ldg(V.K + u - 1) >> 1) + 1 : 0u;
+        }
+      }
+    }
+    uint32_t rk = LSM_NOT_FOUND, rv = LSM_NOT_FOUND;
+    uint8_t f = 0;
+    while (true) {
+      uint32_t m = SUCC ? kSent : 0u;
+#pragma unroll
+      for (int j = 0; j < CAP; ++j)
+        if (j < L) m = SUCC ? min(m, head[j]) : max(m, head[j]);
+      if (SUCC ? m == kSent : m == 0u) break;
+      const uint32_t key = SUCC ? m : m - 1;
+      bool first = true, valid = false;
+      uint32_t val = 0;
+#pragma unroll
+      for (int j = 0; j < CAP; ++j) {
+        if (j < L && head[j] == m) {
+          const LvView V = level_view(T, j, sF3);
+          if (SUCC) {  // the cursor sits on the run head
+            const uint64_t p = pos[j];
+            if (first) {
+              first = false;
+              valid = (__ldg(V.K + p) & 1u) != 0;
+              if (valid) val = __ldg(V.V + p);
+            }
+            const uint64_t e = run_end(V, p, key);
+            pos[j] = e;
+            head[j] = e < V.n ? (__ldg(V.K + e) >> 1) : kSent;
+          } else {  // the cursor sits on the run's last record
+            const uint64_t st = run_start(V, pos[j], key);
+            if (first) {
+              first = false;
+              valid = (__ldg(V.K + st) & 1u) != 0;
+              if (valid) val = __ldg(V.V + st);
+            }
+            pos[j] = st - 1;
+            head[j] = st > 0 ? (__ldg(V.K + st - 1) >> 1) + 1 : 0u;
+          }
+        }
+      }
+      if (valid) {
+        rk = key;
+        rv = val;
+        f = 1;
+        break;
+      }
+    }
+    if (act) {
+      keys_out[i] = rk;
+      vals_out[i] = rv;
+      if (found_out) found_out[i] = f;
+    }
   }
 }
 
@@ -469,75 +683,17 @@ cudaError_t set_smem(K kern) {
 
 constexpr int kMaxUnrolled = 8;
 
-template <int N>
-struct CountLauncher {
-  static cudaError_t go(int nl, unsigned g, cudaStream_t s, size_t smem, const LevelTable& T,
-                        const uint32_t* k1, const uint32_t* k2, uint64_t nq, uint32_t* out) {
-    if (nl == N) {
-      static bool attr = false;
-      if (!attr) {
-        cudaError_t e = set_smem(count_kernel<N>);
-        if (e != cudaSuccess) return e;
-        attr = true;
-      }
-      g = std::min(g, occ_grid(count_kernel<N>, smem));
-      count_kernel<N><<<g, kQThreads, smem, s>>>(T, k1, k2, nq, out);
-      return cudaGetLastError();
-    }
-    return CountLauncher<N - 1>::go(nl, g, s, smem, T, k1, k2, nq, out);
+// NL dispatch: f(std::integral_constant<int, N>) for N = nl in [1, kMaxUnrolled],
+// N = 0 (generic, level state in local memory) above that.
+template <int N, typename F>
+cudaError_t dispatch_nl(int nl, F&& f) {
+  if constexpr (N == 0) {
+    return f(std::integral_constant<int, 0>{});
+  } else {
+    if (nl == N) return f(std::integral_constant<int, N>{});
+    return dispatch_nl<N - 1>(nl, f);
   }
-};
-template <>
-struct CountLauncher<0> {
-  static cudaError_t go(int, unsigned g, cudaStream_t s, size_t smem, const LevelTable& T,
-                        const uint32_t* k1, const uint32_t* k2, uint64_t nq, uint32_t* out) {
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = set_smem(count_kernel<0>);
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
-    g = std::min(g, occ_grid(count_kernel<0>, smem));
-    count_kernel<0><<<g, kQThreads, smem, s>>>(T, k1, k2, nq, out);
-    return cudaGetLastError();
-  }
-};
-
-template <int N>
-struct RangeLauncher {
-  static cudaError_t go(int nl, unsigned g, cudaStream_t s, size_t smem, const LevelTable& T,
-                        const uint32_t* k1, const uint32_t* k2, uint64_t nq, uint64_t* off,
-                        uint32_t* ko, uint32_t* vo, uint64_t cap, unsigned long long* scr) {
-    if (nl == N) {
-      static bool attr = false;
-      if (!attr) {
-        cudaError_t e = set_smem(range_kernel<N>);
-        if (e != cudaSuccess) return e;
-        attr = true;
-      }
-      g = occ_grid(range_kernel<N>, smem);
-      range_kernel<N><<<g, kQThreads, smem, s>>>(T, k1, k2, nq, off, ko, vo, cap, scr, scr + 1);
-      return cudaGetLastError();
-    }
-    return RangeLauncher<N - 1>::go(nl, g, s, smem, T, k1, k2, nq, off, ko, vo, cap, scr);
-  }
-};
-template <>
-struct RangeLauncher<0> {
-  static cudaError_t go(int, unsigned g, cudaStream_t s, size_t smem, const LevelTable& T,
-                        const uint32_t* k1, const uint32_t* k2, uint64_t nq, uint64_t* off,
-                        uint32_t* ko, uint32_t* vo, uint64_t cap, unsigned long long* scr) {
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = set_smem(range_kernel<0>);
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
-    g = occ_grid(range_kernel<0>, smem);
-    range_kernel<0><<<g, kQThreads, smem, s>>>(T, k1, k2, nq, off, ko, vo, cap, scr, scr + 1);
-    return cudaGetLastError();
-  }
-};
+}
 
 }  // namespace
 
@@ -565,6 +721,23 @@ cudaError_t launch_lookup(const LevelTable& T, const uint32_t* q, uint64_t nq,
   return cudaGetLastError();
 }
 
+template <bool SAVE>
+cudaError_t count_dispatch(const LevelTable& T, const uint32_t* k1, const uint32_t* k2,
+                           uint64_t nq, uint32_t* counts_out, uint32_t* pos_out,
+                           cudaStream_t s) {
+  const size_t smem = T.f3_smem_total * 4;
+  const int nl = T.count <= kMaxUnrolled ? T.count : 0;
+  return dispatch_nl<kMaxUnrolled>(nl, [&](auto c) -> cudaError_t {
+    constexpr int N = decltype(c)::value;
+    auto kern = count_kernel<N, SAVE>;
+    cudaError_t err = set_smem(kern);
+    if (err != cudaSuccess) return err;
+    const unsigned g = std::min(query_grid(nq), occ_grid(kern, smem));
+    kern<<<g, kQThreads, smem, s>>>(T, k1, k2, nq, counts_out, pos_out);
+    return cudaGetLastError();
+  });
+}
+
 cudaError_t launch_count(const LevelTable& T, const uint32_t* k1, const uint32_t* k2,
                          uint64_t nq, uint32_t* counts_out, cudaStream_t s,
                          const LaunchHooks& hk, int cls) {
@@ -574,12 +747,40 @@ cudaError_t launch_count(const LevelTable& T, const uint32_t* k1, const uint32_t
   if (T.count == 0) {
     e = cudaMemsetAsync(counts_out, 0, nq * 4, s);
   } else {
-    const int nl = T.count <= kMaxUnrolled ? T.count : 0;
-    e = CountLauncher<kMaxUnrolled>::go(nl, query_grid(nq), s, T.f3_smem_total * 4, T, k1, k2, nq,
-                                        counts_out);
+    e = count_dispatch<false>(T, k1, k2, nq, counts_out, nullptr, s);
   }
-  // 8 B in, 4 B out, two 32 B key sectors per level
-  hk.end(hk.ctx, cls, (double)nq * (12.0 + 64.0 * T.count), s, 1);
+  // 8 B in, 4 B out, one 32 B key sector per level (the search's last step;
+  // the L = 8 candidates share it)
+  hk.end(hk.ctx, cls, (double)nq * (12.0 + 32.0 * T.count), s, 1);
+  return e;
+}
+
+cudaError_t launch_order(const LevelTable& T, const uint32_t* q, uint64_t nq, bool succ,
+                         uint32_t* keys_out, uint32_t* vals_out, uint8_t* found_out,
+                         cudaStream_t s, const LaunchHooks& hk) {
+  if (nq == 0) return cudaSuccess;
+  hk.begin(hk.ctx, LSM_K_LOOKUP, s);
+  cudaError_t e = cudaSuccess;
+  const size_t smem = T.f3_smem_total * 4;
+  const int nl = T.count <= kMaxUnrolled ? T.count : 0;
+  auto go = [&](auto c) -> cudaError_t {
+    constexpr int N = decltype(c)::value;
+    auto kern = succ ? order_kernel<N, true> : order_kernel<N, false>;
+    cudaError_t err = set_smem(kern);
+    if (err != cudaSuccess) return err;
+    const unsigned g = std::min(query_grid(nq), occ_grid(kern, smem));
+    kern<<<g, kQThreads, smem, s>>>(T, q, nq, keys_out, vals_out, found_out);
+    return cudaGetLastError();
+  };
+  if (T.count == 0) {  // empty dictionary: every answer is ⊥
+    e = cudaMemsetAsync(keys_out, 0xFF, nq * 4, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(vals_out, 0xFF, nq * 4, s);
+    if (e == cudaSuccess && found_out) e = cudaMemsetAsync(found_out, 0, nq, s);
+  } else {
+    e = dispatch_nl<kMaxUnrolled>(nl, go);
+  }
+  // 4 B in, 9 B out, one 32 B key sector per level (+ the value sector)
+  hk.end(hk.ctx, LSM_K_LOOKUP, (double)nq * (13.0 + 32.0 * T.count + 32.0), s, 1);
   return e;
 }
 
@@ -596,14 +797,67 @@ cudaError_t launch_range(const LevelTable& T, const uint32_t* k1, const uint32_t
   if (T.count == 0) {
     e = cudaMemsetAsync(offsets, 0, (nq + 1) * 8, s);
   } else {
+    const size_t smem = T.f3_smem_total * 4;
     const int nl = T.count <= kMaxUnrolled ? T.count : 0;
-    e = RangeLauncher<kMaxUnrolled>::go(nl, (unsigned)std::max(1, device_sms()), s,
-                                        T.f3_smem_total * 4, T, k1, k2, nq, offsets, keys_out,
-                                        vals_out, capacity, scratch);
+    e = dispatch_nl<kMaxUnrolled>(nl, [&](auto c) -> cudaError_t {
+      constexpr int N = decltype(c)::value;
+      auto kern = range_kernel<N>;
+      cudaError_t err = set_smem(kern);
+      if (err != cudaSuccess) return err;
+      kern<<<occ_grid(kern, smem), kQThreads, smem, s>>>(T, k1, k2, nq, offsets, keys_out,
+                                                          vals_out, capacity, scratch, scratch + 1);
+      return cudaGetLastError();
+    });
   }
-  // 8 B in, 8 B offset out, two 32 B key sectors per level; pairs are
-  // accounted with their 8 B each by the caller's count
+  // 8 B in, 8 B offset out, per level one 32 B key sector, one 32 B value
+  // sector; the pairs' 8 B each are added once the total is known
   hk.end(hk.ctx, LSM_K_RANGE, (double)nq * (16.0 + 64.0 * T.count), s, 1);
+  return e;
+}
+
+bool range3_ok(const LevelTable& T) {
+  if (T.count == 0 || T.count > kMaxUnrolled) return false;
+  for (int j = 0; j < T.count; ++j)
+    if (T.n[j] > 0xFFFFFFFFull) return false;
+  return true;
+}
+
+uint64_t range3_scratch_bytes(const LevelTable& T, uint64_t nq) {
+  auto al = [](uint64_t x) { return (x + 255) / 256 * 256; };
+  return al((uint64_t)T.count * nq * 4) + al(nq * 4) + al(scan_scratch_words(nq) * 8);
+}
+
+cudaError_t launch_range3(const LevelTable& T, const uint32_t* k1, const uint32_t* k2,
+                          uint64_t nq, uint64_t* offsets, uint32_t* keys_out, uint32_t* vals_out,
+                          uint64_t capacity, void* scratch, cudaStream_t s,
+                          const LaunchHooks& hk) {
+  if (nq == 0) return cudaSuccess;
+  auto al = [](uint64_t x) { return (x + 255) / 256 * 256; };
+  uint8_t* b = static_cast<uint8_t*>(scratch);
+  uint32_t* pos = reinterpret_cast<uint32_t*>(b);
+  uint32_t* counts = reinterpret_cast<uint32_t*>(b + al((uint64_t)T.count * nq * 4));
+  uint64_t* sums = reinterpret_cast<uint64_t*>(b + al((uint64_t)T.count * nq * 4) + al(nq * 4));
+  // pass 1: bounds + counting walk, saving the start positions
+  hk.begin(hk.ctx, LSM_K_RANGE, s);
+  cudaError_t e = count_dispatch<true>(T, k1, k2, nq, counts, pos, s);
+  hk.end(hk.ctx, LSM_K_RANGE, (double)nq * (8.0 + 32.0 * T.count + 8.0 * T.count), s, 1);
+  if (e != cudaSuccess) return e;
+  // pass 2: offsets = exclusive scan of the counts (the paper's stage 2)
+  e = launch_scan(counts, nq, offsets, sums, s, hk);
+  if (e != cudaSuccess) return e;
+  // pass 3: write walk from the saved positions
+  hk.begin(hk.ctx, LSM_K_RANGE, s);
+  const int nl = T.count;
+  e = dispatch_nl<kMaxUnrolled>(nl, [&](auto c) -> cudaError_t {
+    constexpr int N = decltype(c)::value;
+    auto kern = range_write_kernel<N>;
+    const unsigned g = std::min(query_grid(nq), occ_grid(kern, 0));
+    kern<<<g, kQThreads, 0, s>>>(T, k2, nq, pos, offsets, keys_out, vals_out, capacity);
+    return cudaGetLastError();
+  });
+  // 4 B in + offsets 16 B + positions 4 B per level + one 32 B value sector
+  // per level; the pairs' 8 B each are added once the total is known
+  hk.end(hk.ctx, LSM_K_RANGE, (double)nq * (20.0 + 36.0 * T.count), s, 1);
   return e;
 }
 

@@ -34,6 +34,14 @@ class GpuAdapter:
     def count(self, k1, k2):
         return to_numpy_u32(self.lsm.count(to_device(k1), to_device(k2)))
 
+    def successor(self, q):
+        k, v, f = self.lsm.successor(to_device(q))
+        return to_numpy_u32(k), to_numpy_u32(v), f.cpu().numpy()
+
+    def predecessor(self, q):
+        k, v, f = self.lsm.predecessor(to_device(q))
+        return to_numpy_u32(k), to_numpy_u32(v), f.cpu().numpy()
+
     def range(self, k1, k2):
         off, ks, vs = self.lsm.range(to_device(k1), to_device(k2))
         return off.cpu().numpy().astype(np.uint64), to_numpy_u32(ks), to_numpy_u32(vs)
@@ -79,6 +87,17 @@ def assert_queries_equal(gpu, o1, lookups, k1, k2, where=""):
     assert np.array_equal(goff, ooff), f"{where} range offsets mismatch"
     assert np.array_equal(gk, ok) and np.array_equal(gvv, ovv), f"{where} range pairs mismatch"
     assert np.array_equal(np.diff(goff).astype(np.uint32), gc)  # count == len(range)
+    assert_order_equal(gpu, o1, lookups, where)
+
+
+def assert_order_equal(gpu, o1, q, where=""):
+    """N3 successor / predecessor (R23), exact vs O1."""
+    for name in ("successor", "predecessor"):
+        gk, gv, gf = getattr(gpu, name)(q)
+        ok, ov, of = getattr(o1, name)(q)
+        bad = np.nonzero((gk != ok) | (gv != ov) | (gf != of))[0]
+        assert len(bad) == 0, (f"{where} {name} mismatch at {bad[:8]}: q={q[bad[:8]]} "
+                               f"gpu={gk[bad[:8]]},{gf[bad[:8]]} o1={ok[bad[:8]]},{of[bad[:8]]}")
 
 
 @pytest.mark.parametrize("path", lsm_script.golden_files(), ids=lambda p: p.split("/")[-1])
@@ -374,3 +393,109 @@ def len_live(g):
         kk = to_numpy_u32(k)
         tot += int(np.count_nonzero(kk & 1))
     return tot
+
+
+def test_successor_predecessor_tombstone_runs_and_many_levels():
+    # Long runs of deleted keys (the walk must skip them), placebo tails from
+    # partial batches, queries beyond every key, and r = 511 (9 levels: the
+    # generic, non-unrolled kernel).
+    b = 64
+    gpu, o1 = GpuAdapter(b), oracle.OracleDict(b)
+    rng = np.random.default_rng(77)
+    q = np.concatenate([np.arange(0, 4200, 7, dtype=np.uint32),
+                        np.array([0, 1, 4095, 4096, 0x7FFFFFFE, 0x7FFFFFFF, 0x80000000,
+                                  0xFFFFFFFF], np.uint32)])
+    for j in range(511):
+        if j < 40:  # dense inserts of keys 0..2559
+            k = np.arange(j * b, (j + 1) * b, dtype=np.uint32)
+            d = np.zeros(b, np.uint8)
+        elif j < 60:  # delete a contiguous block -> long tombstone stretch
+            k = np.arange(1000 + (j - 40) * b, 1000 + (j - 39) * b, dtype=np.uint32)
+            d = np.ones(b, np.uint8)
+        else:
+            n = int(rng.integers(1, b + 1))  # partial batches: placebo padding
+            k = rng.integers(0, 4096, n).astype(np.uint32)
+            d = (rng.integers(0, 4, n) == 0).astype(np.uint8)
+        v = np.arange(j * b, j * b + len(k), dtype=np.uint32)
+        gpu.update(k, v, d)
+        o1.apply_batch(k, v, d)
+        if j in (0, 39, 59, 60, 127, 255, 300, 510):
+            assert_order_equal(gpu, o1, q, f"batch {j}")
+    assert gpu.r == 511
+    gpu.cleanup()
+    o1.cleanup()
+    assert_order_equal(gpu, o1, q, "after cleanup")
+    # everything deleted -> no successor / predecessor anywhere
+    gpu2, o2 = GpuAdapter(8), oracle.OracleDict(8)
+    k = np.arange(8, dtype=np.uint32)
+    for d in (np.zeros(8, np.uint8), np.ones(8, np.uint8)):
+        gpu2.update(k, k, d)
+        o2.apply_batch(k, k, d)
+    assert_order_equal(gpu2, o2, np.arange(12, dtype=np.uint32), "all deleted")
+    gk, _, gf = gpu2.successor(np.arange(12, dtype=np.uint32))
+    assert not gf.any() and np.all(gk == 0xFFFFFFFF)
+
+
+@pytest.mark.parametrize("b,n", [(64, 1), (64, 64), (64, 1000), (4096, 4096 * 5 + 17),
+                                 (1 << 16, (1 << 16) * 3), (1 << 20, (1 << 20) * 3 + 5)])
+def test_bulk_build(b, n):
+    # N1: one sort + level views; bit-exact vs S1, queries vs O1,
+    # then ordinary batches on top (newer than the bulk epoch) and a cleanup.
+    seed = synth.SEED_BASE + 50 + n % 97
+    k, v, d = synth.updates(seed, 0, n, delete_frac4=1, alphabet=max(8, n // 2))
+    gpu, s1, o1 = GpuAdapter(b), oracle.ShadowLSM(b), oracle.OracleDict(b)
+    gpu.lsm.bulk_build(to_device(k), to_device(v), to_device(d))
+    s1.bulk_build(k, v, d)
+    o1.bulk_build(k, v, d)
+    assert gpu.r == s1.r == o1.r == -(-n // b)
+    assert_levels_equal(gpu, s1, "bulk")
+    q = synth.lookup_queries(seed, 3000, n, alphabet=max(8, n // 2))
+    k1, k2 = synth.range_queries(seed, 500, max(n, 1), 8, domain=max(8, n // 2))
+    assert_queries_equal(gpu, o1, q, k1, k2, "bulk")
+    for j in range(3):
+        kk, vv, dd = synth.updates(seed, n + j * b, b, delete_frac4=1, alphabet=max(8, n // 2))
+        gpu.update(kk, vv, dd)
+        s1.update(kk, vv, dd)
+        o1.apply_batch(kk, vv, dd)
+        assert_levels_equal(gpu, s1, f"bulk+{j}")
+    assert_queries_equal(gpu, o1, q, k1, k2, "bulk+3")
+    gpu.cleanup()
+    s1.cleanup()
+    o1.cleanup()
+    assert_levels_equal(gpu, s1, "bulk cleanup")
+
+
+def test_bulk_build_errors():
+    g = pkg.GpuLSM(64)
+    k = to_device(np.arange(10, dtype=np.uint32))
+    with pytest.raises(pkg.LsmError):
+        g.bulk_build(k[:0])
+    g.bulk_build(k, k)
+    with pytest.raises(pkg.LsmError):  # only into an empty structure
+        g.bulk_build(k, k)
+
+
+@pytest.mark.parametrize("b,nb,r0", [(64, 13, 0), (64, 9, 5), (1000, 7, 3), (4096, 6, 1),
+                                     (10_000, 5, 2), (1 << 17, 3, 1)])
+def test_update_batches_equals_sequential(b, nb, r0):
+    # N1 multi-batch insertion (PAPER.md:860 footnote): bit-exact equal to nb
+    # sequential lsm_update calls (S1), the last batch partial.
+    seed = synth.SEED_BASE + 60 + b % 89
+    gpu, s1, o1 = GpuAdapter(b), oracle.ShadowLSM(b), oracle.OracleDict(b)
+    for j in range(r0):
+        kk, vv, dd = synth.updates(seed, j * b, b, delete_frac4=1, alphabet=3 * b)
+        gpu.update(kk, vv, dd)
+        s1.update(kk, vv, dd)
+        o1.apply_batch(kk, vv, dd)
+    n = nb * b - b // 3
+    k, v, d = synth.updates(seed, r0 * b, n, delete_frac4=1, alphabet=3 * b)
+    gpu.lsm.update_batches(to_device(k), to_device(v), to_device(d))
+    for j in range(nb):
+        sl = slice(j * b, min(n, (j + 1) * b))
+        s1.update(k[sl], v[sl], d[sl])
+        o1.apply_batch(k[sl], v[sl], d[sl])
+    assert gpu.r == s1.r == r0 + nb
+    assert_levels_equal(gpu, s1, "multi")
+    q = synth.lookup_queries(seed, 2000, (r0 + nb) * b, alphabet=3 * b)
+    k1, k2 = synth.range_queries(seed, 300, (r0 + nb) * b, 8, domain=3 * b)
+    assert_queries_equal(gpu, o1, q, k1, k2, "multi")

@@ -346,3 +346,174 @@ def test_out_of_domain_key_dropped_with_flag():
     assert len(o) == 2
     kk, vv = s.level(0)
     assert kk.tolist() == [11, 13, 0xFFFFFFFE, 0xFFFFFFFE]
+
+
+def _succ_pred_brute_check(o, o0, qs):
+    ks, vs, fs = o.successor(qs)
+    kp, vp, fp = o.predecessor(qs)
+    for i, qq in enumerate(qs.tolist()):
+        bs, bp = o0.successor(qq), o0.predecessor(qq)
+        assert (bs is None) == (fs[i] == 0), (qq, bs)
+        assert (bp is None) == (fp[i] == 0), (qq, bp)
+        if bs is None:
+            assert ks[i] == vs[i] == 0xFFFFFFFF
+        else:
+            assert (int(ks[i]), int(vs[i])) == bs
+        if bp is None:
+            assert kp[i] == vp[i] == 0xFFFFFFFF
+        else:
+            assert (int(kp[i]), int(vp[i])) == bp
+
+
+def test_successor_predecessor_vs_brute_exhaustive_tiny():
+    # N3 (PAPER.md:113 footnote, reading R23) against O0's history scan:
+    # b = 2, 3-key alphabet, all 2-batch schedules, every query key 0..3 plus
+    # the domain edges.
+    ops = [(k, d) for k in range(3) for d in (0, 1)]
+    b = 2
+    qs = np.array([0, 1, 2, 3, 0x7FFFFFFE, 0x7FFFFFFF, 0xFFFFFFFF], np.uint32)
+    for combo in itertools.product(ops, repeat=2 * b):
+        o = oracle.OracleDict(b)
+        o0 = oracle.BruteDict()
+        for j in range(2):
+            part = combo[j * b:(j + 1) * b]
+            keys = np.array([k for k, _ in part], np.uint32)
+            dels = np.array([d for _, d in part], np.uint8)
+            vals = np.arange(j * b + 1, (j + 1) * b + 1, dtype=np.uint32)
+            o.apply_batch(keys, vals, dels)
+            o0.apply_batch(keys, vals, dels)
+            _succ_pred_brute_check(o, o0, qs)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_successor_predecessor_vs_brute_random(seed):
+    rng = np.random.default_rng(900 + seed)
+    o = oracle.OracleDict(4)
+    o0 = oracle.BruteDict()
+    for j in range(10):
+        keys = rng.integers(0, 12, 4).astype(np.uint32)
+        dels = (rng.integers(0, 3, 4) == 0).astype(np.uint8)
+        vals = np.arange(j * 4, j * 4 + 4, dtype=np.uint32)
+        o.apply_batch(keys, vals, dels)
+        o0.apply_batch(keys, vals, dels)
+        _succ_pred_brute_check(o, o0, np.arange(14, dtype=np.uint32))
+
+
+def test_successor_predecessor_count_invariants():
+    # Properties fixed by the definitions, checked through count (itself
+    # pinned to O0): succ(q) = s  =>  count(q, s-1) == 0 and count(s, s) == 1;
+    # no successor  =>  count(q, MAX) == 0; mirror for pred. lookup(q) found
+    # <=> succ(q) == q == pred(q).
+    b = 256
+    seed = synth.SEED_BASE + 41
+    o = oracle.OracleDict(b)
+    for j in range(9):
+        k, v, d = synth.updates(seed, j * b, b, delete_frac4=2, alphabet=2000)
+        o.apply_batch(k, v, d)
+    qs = np.concatenate([np.arange(0, 2100, dtype=np.uint32),
+                         np.array([0x7FFFFFFE, 0x7FFFFFFF, 0xFFFFFFFF], np.uint32)])
+    ks, vs, fs = o.successor(qs)
+    kp, vp, fp = o.predecessor(qs)
+    lv, lf = o.lookup(qs)
+    mx = np.full(len(qs), 0x7FFFFFFE, np.uint32)
+    zero = np.zeros(len(qs), np.uint32)
+    for i, qq in enumerate(qs.tolist()):
+        if fs[i]:
+            assert ks[i] >= qq
+            if ks[i] > qq:
+                assert o.count([qq], [ks[i] - 1])[0] == 0
+            assert o.count([ks[i]], [ks[i]])[0] == 1
+            assert vs[i] == o.lookup([ks[i]])[0][0]
+        else:
+            assert o.count([min(qq, 0x7FFFFFFF)], [mx[i]])[0] == 0
+        if fp[i]:
+            assert kp[i] <= qq
+            if kp[i] < qq:
+                assert o.count([kp[i] + 1], [min(qq, 0xFFFFFFFE)])[0] == 0
+            assert o.count([kp[i]], [kp[i]])[0] == 1
+        else:
+            assert o.count([zero[i]], [qq])[0] == 0
+        assert bool(lf[i]) == (bool(fs[i]) and ks[i] == qq) == (bool(fp[i]) and kp[i] == qq)
+
+
+def test_bulk_build_single_batch_equals_update():
+    # k = 1: a bulk build of n <= b elements is one batch inserted into the
+    # empty structure, i.e. exactly s1_update's level 0 (pinned by the paper's
+    # worked examples above).
+    rng = np.random.default_rng(5)
+    for n in (1, 7, 64):
+        keys = rng.integers(0, 40, n).astype(np.uint32)
+        vals = np.arange(n, dtype=np.uint32) + 1
+        dels = (rng.integers(0, 4, n) == 0).astype(np.uint8)
+        a, c = oracle.ShadowLSM(64), oracle.ShadowLSM(64)
+        a.bulk_build(keys, vals, dels)
+        c.update(keys, vals, dels)
+        assert a.r == c.r == 1
+        assert all(np.array_equal(x, y) for x, y in zip(a.level(0), c.level(0)))
+
+
+def test_bulk_build_image_from_sorted_unique_keys():
+    # Unique keys, inserts only: the structure is the sorted pairs encoded
+    # (k << 1) | 1, then placebos up to k*b, cut into the set bits of k in
+    # ascending order ("segment this array"). Built here with
+    # numpy alone.
+    b = 16
+    rng = np.random.default_rng(11)
+    for n in (16, 17, 100, 16 * 7, 16 * 13 - 3):
+        keys = rng.choice(1 << 20, n, replace=False).astype(np.uint32)
+        vals = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+        s = oracle.ShadowLSM(b)
+        s.bulk_build(keys, vals)
+        k = -(-n // b)
+        order = np.argsort(keys, kind="stable")
+        img_k = np.concatenate([(keys[order] << 1) | 1, np.full(k * b - n, 0xFFFFFFFE, np.uint32)])
+        img_v = np.concatenate([vals[order], np.zeros(k * b - n, np.uint32)])
+        assert s.r == k
+        off = 0
+        for i in range(k.bit_length()):
+            lk, lv = s.level(i)
+            if not (k >> i) & 1:
+                assert len(lk) == 0
+                continue
+            assert np.array_equal(lk, img_k[off:off + (b << i)])
+            assert np.array_equal(lv, img_v[off:off + (b << i)])
+            off += b << i
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_bulk_build_queries_vs_brute(seed):
+    # Duplicates and deletes inside the bulk input: it is ONE batch (R24), so
+    # O0 applies it as one batch; S1 queries and O1 must agree with O0.
+    rng = np.random.default_rng(300 + seed)
+    b, n = 8, 45
+    keys = rng.integers(0, 20, n).astype(np.uint32)
+    vals = np.arange(n, dtype=np.uint32) + 100
+    dels = (rng.integers(0, 4, n) == 0).astype(np.uint8)
+    s, o, o0 = oracle.ShadowLSM(b), oracle.OracleDict(b), oracle.BruteDict()
+    s.bulk_build(keys, vals, dels)
+    o.bulk_build(keys, vals, dels)
+    o0.apply_batch(keys, vals, dels)
+    assert s.r == o.r == 6
+    q = np.arange(22, dtype=np.uint32)
+    sv, sf = s.lookup(q)
+    ov, of = o.lookup(q)
+    for i in range(22):
+        bv = o0.lookup(i)
+        assert (bv is None) == (sf[i] == 0) == (of[i] == 0)
+        if bv is not None:
+            assert bv == sv[i] == ov[i]
+    for a1, a2 in ((0, 21), (3, 9), (10, 10), (15, 2)):
+        assert o0.count(a1, a2) == int(s.count([a1], [a2])[0]) == int(o.count([a1], [a2])[0])
+    # later batches are newer than the whole bulk epoch
+    k2 = np.array([1, 2, 3], np.uint32)
+    v2 = np.array([7, 8, 9], np.uint32)
+    d2 = np.array([0, 1, 0], np.uint8)
+    s.update(k2, v2, d2)
+    o.apply_batch(k2, v2, d2)
+    o0.apply_batch(k2, v2, d2)
+    sv, sf = s.lookup(q)
+    for i in range(22):
+        bv = o0.lookup(i)
+        assert (bv is None) == (sf[i] == 0)
+        if bv is not None:
+            assert bv == sv[i]
