@@ -70,6 +70,18 @@ typedef enum {
  * handle. Errors: LSM_ERR_INVALID_ARG (b == 0, out NULL), LSM_ERR_NO_DEVICE. */
 lsm_status lsm_create(uint64_t b, lsm_t** out);
 
+/* N2 -- the paper's GPU SA comparison structure ("a
+ * GPU-maintained sorted array"): same handle, same calls, but ONE sorted
+ * array of r*b records. An update sorts the batch (A1+A2) and merges it,
+ * newer first on ties (R1), with the whole array ("merging an
+ * already-sorted set of elements into an existing GPU SA"); queries search
+ * that single level; cleanup compacts it; lsm_level_view(0) returns
+ * the whole array. Merge work after r batches: b(r-1)(r+2)/2 records
+ * (SPEC.md:350). Errors as lsm_create.                                     */
+lsm_status lsm_create_sa(uint64_t b, lsm_t** out);
+/* *sa_out = 1 for a GPU SA handle, 0 for a GPU LSM. */
+lsm_status lsm_is_sa(const lsm_t* h, int* sa_out);
+
 /* Free all device memory owned by h (synchronises the device first). */
 lsm_status lsm_destroy(lsm_t* h);
 

@@ -53,6 +53,12 @@ def lib():
             "o1_range": ([vp, u32p, u32p, u64, u64p, u32p, u32p, u64], u64),
             "o1_bulk_build": ([vp, u32p, u32p, u8p, u64], None),
             "s1_bulk_build": ([vp, u32p, u32p, u8p, u64], ctypes.c_int),
+            "sa_create": ([u64], vp), "sa_destroy": ([vp], None),
+            "sa_update": ([vp, u32p, u32p, u8p, u64], None),
+            "sa_bulk_build": ([vp, u32p, u32p, u8p, u64], ctypes.c_int),
+            "sa_cleanup": ([vp], None), "sa_size": ([vp], u64),
+            "sa_num_batches": ([vp], u64), "sa_merged_records": ([vp], u64),
+            "sa_array": ([vp, u32p, u32p], None),
             "o1_cleanup": ([vp], None), "o1_size": ([vp], u64),
             "o1_num_batches": ([vp], u64), "o1_dump": ([vp, u32p, u32p], None),
             "s1_create": ([u64], vp), "s1_destroy": ([vp], None),
@@ -273,3 +279,48 @@ class ShadowLSM:
         tot = lib().s1_range(self.h, _p(k1, u32p), _p(k2, u32p), nq, _p(off, u64p),
                              _p(ko, u32p), _p(vo, u32p), cap)
         return off, ko[:tot], vo[:tot]
+
+
+class ShadowSA:
+    """N2: the paper's GPU SA (one sorted array)."""
+
+    def __init__(self, b: int):
+        self.b = b
+        self.h = lib().sa_create(b)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().sa_destroy(self.h)
+            self.h = None
+
+    def update(self, keys, vals=None, is_delete=None):
+        keys = _u32(keys)
+        vals = _u32(vals) if vals is not None else np.zeros_like(keys)
+        d = _u8(is_delete)
+        lib().sa_update(self.h, _p(keys, u32p), _p(vals, u32p), _p(d, u8p), len(keys))
+
+    def bulk_build(self, keys, vals=None, is_delete=None):
+        keys = _u32(keys)
+        vals = _u32(vals) if vals is not None else np.zeros_like(keys)
+        d = _u8(is_delete)
+        if lib().sa_bulk_build(self.h, _p(keys, u32p), _p(vals, u32p), _p(d, u8p), len(keys)):
+            raise ValueError("bulk_build needs an empty structure and n >= 1")
+
+    def cleanup(self):
+        lib().sa_cleanup(self.h)
+
+    @property
+    def r(self):
+        return int(lib().sa_num_batches(self.h))
+
+    @property
+    def merged_records(self):
+        return int(lib().sa_merged_records(self.h))
+
+    def array(self):
+        n = int(lib().sa_size(self.h))
+        k = np.empty(n, np.uint32)
+        v = np.empty(n, np.uint32)
+        if n:
+            lib().sa_array(self.h, _p(k, u32p), _p(v, u32p))
+        return k, v

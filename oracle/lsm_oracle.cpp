@@ -411,6 +411,100 @@ void s1_cleanup(void* h) {
   s->r = r2;
 }
 
+// ============================== SA (N2) =====================================
+// The paper's GPU SA: ONE sorted array. An update encodes
+// and sorts the batch exactly as S1 does, then std::merge(batch, array) with
+// the batch (newer) first on ties (R1) replaces the array ("merging an
+// already-sorted set of elements into an existing GPU SA"). Merge work: the
+// old length + b records per merge into a non-empty array, b(r-1)(r+2)/2 in
+// total.
+struct SA {
+  uint64_t b = 0;
+  uint64_t r = 0;
+  std::vector<Rec> arr;
+  uint64_t merged = 0;
+  int domain_error = 0;
+};
+
+static std::vector<Rec> sa_encode(SA* s, const uint32_t* keys, const uint32_t* vals,
+                                  const uint8_t* is_delete, uint64_t n, uint64_t size) {
+  std::vector<Rec> buf;
+  buf.reserve(size);
+  for (uint64_t i = 0; i < n; ++i) {
+    bool del = is_delete ? is_delete[i] != 0 : false;
+    Rec e;
+    if (keys[i] > kMaxKey) {  // R5
+      e.key = kPlacebo;
+      e.val = 0;
+      s->domain_error = 1;
+    } else {  // PAPER.md:605-610; R6
+      e.key = (keys[i] << 1) | (del ? 0u : 1u);
+      e.val = del ? 0u : (vals ? vals[i] : 0u);
+    }
+    buf.push_back(e);
+  }
+  while (buf.size() < size) buf.push_back(Rec{kPlacebo, 0u});  // R7
+  std::stable_sort(buf.begin(), buf.end(),
+                   [](const Rec& a, const Rec& c) { return a.key < c.key; });
+  return buf;
+}
+
+void* sa_create(uint64_t b) {
+  SA* s = new SA;
+  s->b = b;
+  return s;
+}
+void sa_destroy(void* h) { delete static_cast<SA*>(h); }
+
+void sa_update(void* h, const uint32_t* keys, const uint32_t* vals, const uint8_t* is_delete,
+               uint64_t n) {
+  SA* s = static_cast<SA*>(h);
+  std::vector<Rec> batch = sa_encode(s, keys, vals, is_delete, n, s->b);
+  if (!s->arr.empty()) s->merged += s->arr.size() + batch.size();
+  std::vector<Rec> out(batch.size() + s->arr.size());
+  std::merge(batch.begin(), batch.end(), s->arr.begin(), s->arr.end(), out.begin(),
+             [](const Rec& x, const Rec& y) { return orig(x.key) < orig(y.key); });
+  s->arr.swap(out);
+  s->r += 1;
+}
+
+// bulk build (R24) of the SA: one sort of the k*b padded records
+int sa_bulk_build(void* h, const uint32_t* keys, const uint32_t* vals, const uint8_t* is_delete,
+                  uint64_t n) {
+  SA* s = static_cast<SA*>(h);
+  if (s->r != 0 || n == 0) return -1;
+  const uint64_t k = (n + s->b - 1) / s->b;
+  s->arr = sa_encode(s, keys, vals, is_delete, n, k * s->b);
+  s->r = k;
+  return 0;
+}
+
+// cleanup (PAPER.md:737-755 on the single array): keep regular run heads,
+// pad to r'b with placebos (R10, R11)
+void sa_cleanup(void* h) {
+  SA* s = static_cast<SA*>(h);
+  std::vector<Rec> C;
+  for (size_t p = 0; p < s->arr.size(); ++p) {
+    bool run_start = (p == 0) || orig(s->arr[p - 1].key) != orig(s->arr[p].key);
+    if (run_start && (s->arr[p].key & 1u)) C.push_back(s->arr[p]);
+  }
+  const uint64_t r2 = (C.size() + s->b - 1) / s->b;
+  while (C.size() < r2 * s->b) C.push_back(Rec{kPlacebo, 0u});
+  s->arr.swap(C);
+  s->r = r2;
+}
+
+uint64_t sa_size(void* h) { return static_cast<SA*>(h)->arr.size(); }
+uint64_t sa_num_batches(void* h) { return static_cast<SA*>(h)->r; }
+uint64_t sa_merged_records(void* h) { return static_cast<SA*>(h)->merged; }
+void sa_array(void* h, uint32_t* keys, uint32_t* vals) {
+  SA* s = static_cast<SA*>(h);
+  for (size_t i = 0; i < s->arr.size(); ++i) {
+    keys[i] = s->arr[i].key;
+    vals[i] = s->arr[i].val;
+  }
+}
+
 // The two search primitives of S1, exposed for their pins.
 uint64_t s1_lower_bound(const uint32_t* packed, uint64_t n, uint32_t q) {
   std::vector<Rec> L(n);

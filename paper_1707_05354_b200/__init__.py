@@ -34,6 +34,8 @@ _st = ctypes.c_int
 # name -> (argtypes, restype); the exact entry points of include/gpulsm.h
 SIGNATURES = {
     "lsm_create": ([_u64, ctypes.POINTER(_vp)], _st),
+    "lsm_create_sa": ([_u64, ctypes.POINTER(_vp)], _st),
+    "lsm_is_sa": ([_vp, ctypes.POINTER(ctypes.c_int)], _st),
     "lsm_destroy": ([_vp], _st),
     "lsm_reserve": ([_vp, _u64, _vp], _st),
     "lsm_clear": ([_vp, _vp], _st),
@@ -151,17 +153,22 @@ def to_numpy_u32(t):
 
 
 class GpuLSM:
-    """A GPU LSM dictionary with batch size b on the current CUDA device."""
+    """A GPU LSM dictionary with batch size b on the current CUDA device.
 
-    def __init__(self, b: int, reserve_batches: int = 0):
+    sa=True builds the paper's GPU SA comparison structure instead (N2: one
+    sorted array, each batch merged into all of it; same calls)."""
+
+    def __init__(self, b: int, reserve_batches: int = 0, sa: bool = False):
         self._lib = load_library()
         torch = _torch()
         if not torch.cuda.is_available():
             raise RuntimeError("GpuLSM needs a CUDA device (no CPU fallback)")
         h = ctypes.c_void_p()
-        _check(self._lib.lsm_create(int(b), ctypes.byref(h)), "lsm_create")
+        create = self._lib.lsm_create_sa if sa else self._lib.lsm_create
+        _check(create(int(b), ctypes.byref(h)), "lsm_create_sa" if sa else "lsm_create")
         self.h = h
         self.b = int(b)
+        self.sa = bool(sa)
         if reserve_batches:
             _check(self._lib.lsm_reserve(self.h, int(reserve_batches), _stream_ptr()),
                    "lsm_reserve")

@@ -68,6 +68,13 @@ struct lsm {
   uint32_t* bulk_meta = nullptr;
   uint64_t bulk_cap = 0;
   Buffer stage;  // N1 multi-batch insertion: the k sorted batches
+  // N2 GPU SA mode: one sorted array of r*b records
+  bool sa = false;
+  Buffer sa_buf[2];
+  int sa_cur = 0;
+  uint32_t* sa_idx = nullptr;
+  uint64_t sa_idx_words = 0;
+  bool sa_idx_ready = false;
   // host-update staging
   uint32_t* st_keys = nullptr;
   uint32_t* st_vals = nullptr;
@@ -284,11 +291,11 @@ LevelTable level_table(const lsm* h) {
   int c = 0;
   uint32_t off = 0;
   for (int i = 0; i < LSM_MAX_LEVELS; ++i) {
-    if ((h->r >> i) & 1ull) {
-      T.keys[c] = h->level[i].keys;
-      T.vals[c] = h->level[i].vals;
-      T.idx[c] = h->level[i].idx;
-      T.n[c] = h->b << i;
+    if (h->sa ? (i == 0 && h->r > 0) : ((h->r >> i) & 1ull)) {
+      T.keys[c] = h->sa ? h->sa_buf[h->sa_cur].keys : h->level[i].keys;
+      T.vals[c] = h->sa ? h->sa_buf[h->sa_cur].vals : h->level[i].vals;
+      T.idx[c] = h->sa ? h->sa_idx : h->level[i].idx;
+      T.n[c] = h->sa ? h->r * h->b : h->b << i;
       // F3 is staged as a complete search tree in Eytzinger order: 2^h words
       const uint32_t h3 = f3_tree_h(idx_f3_len(T.n[c]));
       const uint64_t words = 1ull << h3;
@@ -311,6 +318,15 @@ LevelTable level_table(const lsm* h) {
 cudaError_t ensure_index(lsm* h, cudaStream_t s, const LaunchHooks& hk) {
   IndexJobs J;
   std::memset(&J, 0, sizeof(J));
+  if (h->sa) {
+    if (h->r > 0 && !h->sa_idx_ready) {
+      J.idx[0] = h->sa_idx;
+      J.n[0] = h->r * h->b;
+      J.count = 1;
+      h->sa_idx_ready = true;
+    }
+    return launch_finalize_index(J, s, hk);
+  }
   for (int i = 0; i < LSM_MAX_LEVELS; ++i) {
     if (((h->r >> i) & 1ull) && !h->level[i].idx_ready) {
       J.idx[J.count] = h->level[i].idx;
@@ -401,6 +417,9 @@ lsm_status lsm_destroy(lsm_t* h) {
   }
   bulk_free(h, nullptr);
   buf_free(h->stage, nullptr);
+  buf_free(h->sa_buf[0], nullptr);
+  buf_free(h->sa_buf[1], nullptr);
+  if (h->sa_idx) cudaFreeAsync(h->sa_idx, nullptr);
   if (h->st_keys) cudaFreeAsync(h->st_keys, nullptr);
   if (h->st_vals) cudaFreeAsync(h->st_vals, nullptr);
   if (h->st_ops) cudaFreeAsync(h->st_ops, nullptr);
@@ -418,10 +437,19 @@ lsm_status lsm_destroy(lsm_t* h) {
   return LSM_OK;
 }
 
+static cudaError_t sa_buf_ensure(lsm* h, Buffer& B, uint64_t n, cudaStream_t s);
+static cudaError_t sa_idx_ensure(lsm* h, uint64_t n, cudaStream_t s);
+
 lsm_status lsm_reserve(lsm_t* h, uint64_t max_batches, void* stream) {
   if (!h) return LSM_ERR_INVALID_ARG;
   cudaStream_t s = S(stream);
   CK(ensure_sort_scratch(h, s));
+  if (h->sa) {
+    CK(sa_buf_ensure(h, h->sa_buf[0], max_batches * h->b, s));
+    CK(sa_buf_ensure(h, h->sa_buf[1], max_batches * h->b, s));
+    CK(sa_idx_ensure(h, max_batches * h->b, s));
+    return LSM_OK;
+  }
   int top = 0;
   while (top + 1 < LSM_MAX_LEVELS && (1ull << (top + 1)) <= max_batches) ++top;
   for (int i = 0; i <= top; ++i) {
@@ -438,6 +466,10 @@ lsm_status lsm_reserve(lsm_t* h, uint64_t max_batches, void* stream) {
 
 lsm_status lsm_clear(lsm_t* h, void* stream) {
   if (!h) return LSM_ERR_INVALID_ARG;
+  if (h->sa) {
+    h->r = 0;
+    return LSM_OK;
+  }
   for (int i = 0; i < LSM_MAX_LEVELS; ++i)
     if ((h->r >> i) & 1ull) level_release(h, i, S(stream));
   h->r = 0;
@@ -489,11 +521,79 @@ static void commit_insert(lsm_t* h, int t) {
   h->r += 1;
 }
 
+// ---------------- N2: GPU SA mode ----------------
+// "Merging an already-sorted set of elements into an existing GPU SA"
+// (P:767): sort the batch (A1+A2), then ONE merge of the sorted batch (newer,
+// first on ties, R1) with the whole array (older) into the other buffer; the
+// merge writes the array's F1. Queries see one level of r*b records.
+
+// grow-only buffer (1.5x) so the array does not reallocate every batch
+static cudaError_t sa_buf_ensure(lsm* h, Buffer& B, uint64_t n, cudaStream_t s) {
+  if (B.cap >= n) return cudaSuccess;
+  return buf_ensure(h, B, std::max<uint64_t>(n, B.cap + B.cap / 2), s);
+}
+
+static cudaError_t sa_idx_ensure(lsm* h, uint64_t n, cudaStream_t s) {
+  const uint64_t w = idx_words(n);
+  if (h->sa_idx_words >= w) return cudaSuccess;
+  if (h->sa_idx) cudaFreeAsync(h->sa_idx, s);
+  h->sa_idx = nullptr;
+  h->sa_idx_words = 0;
+  const uint64_t want = std::max<uint64_t>(w, h->sa_idx_words + h->sa_idx_words / 2);
+  cudaError_t e = pool_alloc(h, (void**)&h->sa_idx, want * 4, s);
+  if (e == cudaSuccess) h->sa_idx_words = want;
+  return e;
+}
+
+// merge the sorted batch (ck, cv) of b records into the array
+static lsm_status sa_merge_in(lsm_t* h, const uint32_t* ck, const uint32_t* cv, cudaStream_t s,
+                              const LaunchHooks& hk) {
+  const uint64_t b = h->b, n_old = h->r * b, n_new = n_old + b;
+  CK(sa_idx_ensure(h, n_new, s));
+  Buffer& dst = h->sa_buf[h->sa_cur ^ 1];
+  CK(sa_buf_ensure(h, dst, n_new, s));
+  if (n_old == 0) {
+    CK(cudaMemcpyAsync(dst.keys, ck, b * 4, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(dst.vals, cv, b * 4, cudaMemcpyDeviceToDevice, s));
+    CK(launch_build_f1(dst.keys, b, h->sa_idx, s, hk));
+  } else {
+    const Buffer& src = h->sa_buf[h->sa_cur];
+    CK(launch_merge(ck, cv, b, src.keys, src.vals, n_old, dst.keys, dst.vals, h->sa_idx, s, hk));
+  }
+  h->sa_cur ^= 1;
+  h->r += 1;
+  h->sa_idx_ready = false;
+  return LSM_OK;
+}
+
+static lsm_status sa_update(lsm_t* h, const uint32_t* keys, const uint32_t* vals,
+                            const uint8_t* ops, int mode, uint64_t n, cudaStream_t s) {
+  LaunchHooks hk = hooks(h);
+  CK(ensure_sort_scratch(h, s));
+  CK(buf_ensure(h, h->sortout, h->b, s));
+  CK(launch_sort_batch(keys, vals, ops, mode, n, h->b, h->sort, h->sortout.keys,
+                       h->sortout.vals, nullptr, s, hk));
+  return sa_merge_in(h, h->sortout.keys, h->sortout.vals, s, hk);
+}
+
+lsm_status lsm_create_sa(uint64_t b, lsm_t** out) {
+  lsm_status st = lsm_create(b, out);
+  if (st == LSM_OK) (*out)->sa = true;
+  return st;
+}
+
+lsm_status lsm_is_sa(const lsm_t* h, int* sa_out) {
+  if (!h || !sa_out) return LSM_ERR_INVALID_ARG;
+  *sa_out = h->sa ? 1 : 0;
+  return LSM_OK;
+}
+
 static lsm_status do_update(lsm_t* h, const uint32_t* keys, const uint32_t* vals,
                             const uint8_t* ops, int mode, uint64_t n, cudaStream_t s) {
   if (!h || !keys) return LSM_ERR_INVALID_ARG;
   if (n == 0 || n > h->b) return LSM_ERR_BATCH_SIZE;
   if (mode == kModeMixed && ops == nullptr) mode = kModeInsert;
+  if (h->sa) return sa_update(h, keys, vals, ops, mode, n, s);
   const uint64_t b = h->b;
   const int t = ffz(h->r);  // first empty level
   if (t >= LSM_MAX_LEVELS) return LSM_ERR_INVALID_ARG;
@@ -543,6 +643,18 @@ lsm_status lsm_bulk_build(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_va
   cudaStream_t s = S(stream);
   LaunchHooks hk = hooks(h);
   const int mode = d_is_delete ? kModeMixed : kModeInsert;
+  if (h->sa) {  // one sort straight into the array (with its F1)
+    Buffer& A = h->sa_buf[h->sa_cur];
+    CK(sa_buf_ensure(h, A, k * b, s));
+    CK(sa_idx_ensure(h, k * b, s));
+    CK(ensure_bulk_scratch(h, k * b, s));
+    CK(launch_sort_batch(d_keys, d_vals, d_is_delete, mode, n, k * b, h->bulk, A.keys, A.vals,
+                         h->sa_idx, s, hk));
+    h->sort.lsd_only = h->sort.lsd_only || h->bulk.lsd_only;
+    h->r = k;
+    h->sa_idx_ready = false;
+    return LSM_OK;
+  }
   Buffer* C = new Buffer;
   cudaError_t e = buf_ensure(h, *C, k * b, s);
   if (e == cudaSuccess) e = ensure_bulk_scratch(h, k * b, s);
@@ -594,6 +706,11 @@ lsm_status lsm_update_batches(lsm_t* h, const uint32_t* d_keys, const uint32_t* 
   CK(launch_sort_segments(d_keys, d_vals, d_is_delete, mode, n, b, k, h->sort, h->stage.keys,
                           h->stage.vals, s, hk));
   for (uint64_t j = 0; j < k; ++j) {
+    if (h->sa) {
+      lsm_status st = sa_merge_in(h, h->stage.keys + j * b, h->stage.vals + j * b, s, hk);
+      if (st != LSM_OK) return st;
+      continue;
+    }
     const int t = ffz(h->r);
     lsm_status st = prepare_insert(h, t, s);
     if (st != LSM_OK) return st;
@@ -749,11 +866,12 @@ lsm_status lsm_cleanup(lsm_t* h, void* stream) {
   for (int i = 0; i < LSM_MAX_LEVELS; ++i)
     if ((h->r >> i) & 1ull) occ.push_back(i);
   if (occ.empty()) return LSM_OK;
+  if (h->sa) occ.assign(1, 0);  // GPU SA: the one array, no merge
   const uint64_t n = h->r * b;
   // 1) iterative merges, newer (lower index) first on ties
-  const uint32_t* mk = h->level[occ[0]].keys;
-  const uint32_t* mv = h->level[occ[0]].vals;
-  uint64_t mn = b << occ[0];
+  const uint32_t* mk = h->sa ? h->sa_buf[h->sa_cur].keys : h->level[occ[0]].keys;
+  const uint32_t* mv = h->sa ? h->sa_buf[h->sa_cur].vals : h->level[occ[0]].vals;
+  uint64_t mn = h->sa ? n : b << occ[0];
   int pp = 0;
   if (occ.size() > 1) {
     CK(buf_ensure(h, h->ping[0], n, s));
@@ -794,6 +912,15 @@ lsm_status lsm_cleanup(lsm_t* h, void* stream) {
   const uint64_t r2 = (V + b - 1) / b;  // R10
   // 4) placebos fill [V, r'b) (R11)
   CK(launch_fill_placebo(C->keys, C->vals, V, r2 * b, s, hk));
+  if (h->sa) {  // the compacted buffer becomes the array; its F1 is rebuilt
+    buf_free(h->sa_buf[h->sa_cur], s);
+    h->sa_buf[h->sa_cur] = *C;
+    delete C;
+    if (r2 > 0) CK(launch_build_f1(h->sa_buf[h->sa_cur].keys, r2 * b, h->sa_idx, s, hk));
+    h->sa_idx_ready = false;
+    h->r = r2;
+    return LSM_OK;
+  }
   // 5) new levels are views of C: ascending keys into ascending set bits of
   //    r' (R12), no copy
   for (int i : occ) level_release(h, i, s);
@@ -885,6 +1012,13 @@ lsm_status lsm_num_batches(const lsm_t* h, uint64_t* r_out) {
 lsm_status lsm_level_view(const lsm_t* h, uint32_t i, const uint32_t** d_keys,
                           const uint32_t** d_vals, uint64_t* n) {
   if (!h || !d_keys || !d_vals || !n || i >= LSM_MAX_LEVELS) return LSM_ERR_INVALID_ARG;
+  if (h->sa) {  // the whole sorted array is "level 0"
+    const bool occ = i == 0 && h->r > 0;
+    *d_keys = occ ? h->sa_buf[h->sa_cur].keys : nullptr;
+    *d_vals = occ ? h->sa_buf[h->sa_cur].vals : nullptr;
+    *n = occ ? h->r * h->b : 0;
+    return LSM_OK;
+  }
   if ((h->r >> i) & 1ull) {
     *d_keys = h->level[i].keys;
     *d_vals = h->level[i].vals;

@@ -499,3 +499,70 @@ def test_update_batches_equals_sequential(b, nb, r0):
     q = synth.lookup_queries(seed, 2000, (r0 + nb) * b, alphabet=3 * b)
     k1, k2 = synth.range_queries(seed, 300, (r0 + nb) * b, 8, domain=3 * b)
     assert_queries_equal(gpu, o1, q, k1, k2, "multi")
+
+
+class GpuSAAdapter(GpuAdapter):
+    def __init__(self, b):
+        self.lsm = pkg.GpuLSM(b, sa=True)
+
+
+def assert_sa_equal(gpu, sa, where=""):
+    gk, gv = gpu.level(0)
+    ak, av = sa.array()
+    assert gpu.r == sa.r, where
+    assert np.array_equal(gk, ak), f"{where} SA keys differ at {np.nonzero(gk != ak)[0][:8]}"
+    assert np.array_equal(gv, av), f"{where} SA vals differ"
+    for i in range(1, 6):
+        assert len(gpu.level(i)[0]) == 0
+
+
+@pytest.mark.parametrize("b", [4, 100, 4096, 1 << 16])
+def test_gpu_sa(b):
+    # N2: the one-array structure, bit-exact vs the oracle's
+    # SA after every batch; queries (one level) vs O1; cleanup; more batches.
+    seed = synth.SEED_BASE + 80 + b % 13
+    gpu, sa, o1 = GpuSAAdapter(b), oracle.ShadowSA(b), oracle.OracleDict(b)
+    nb = 12 if b <= 4096 else 5
+    alpha = 3 * b
+    for j in range(nb):
+        n = b if j % 4 else max(1, b - b // 3)
+        k, v, d = synth.updates(seed, j * b, n, delete_frac4=1, alphabet=alpha)
+        gpu.update(k, v, d)
+        sa.update(k, v, d)
+        o1.apply_batch(k, v, d)
+        assert_sa_equal(gpu, sa, f"batch {j}")
+    q = synth.lookup_queries(seed, 3000, nb * b, alphabet=alpha)
+    k1, k2 = synth.range_queries(seed, 500, nb * b, 8, domain=alpha)
+    assert_queries_equal(gpu, o1, q, k1, k2, "sa")
+    gpu.cleanup()
+    sa.cleanup()
+    o1.cleanup()
+    assert_sa_equal(gpu, sa, "sa cleanup")
+    assert_queries_equal(gpu, o1, q, k1, k2, "sa cleanup")
+    k, v, d = synth.updates(seed, nb * b, b, delete_frac4=1, alphabet=alpha)
+    gpu.update(k, v, d)
+    sa.update(k, v, d)
+    o1.apply_batch(k, v, d)
+    assert_sa_equal(gpu, sa, "sa after cleanup")
+    assert_queries_equal(gpu, o1, q, k1, k2, "sa after cleanup")
+
+
+def test_gpu_sa_bulk_and_multi_batch():
+    b = 64
+    seed = synth.SEED_BASE + 81
+    k, v, d = synth.updates(seed, 0, 1000, delete_frac4=1, alphabet=300)
+    gpu, sa, o1 = GpuSAAdapter(b), oracle.ShadowSA(b), oracle.OracleDict(b)
+    gpu.lsm.bulk_build(to_device(k), to_device(v), to_device(d))
+    sa.bulk_build(k, v, d)
+    o1.bulk_build(k, v, d)
+    assert_sa_equal(gpu, sa, "sa bulk")
+    k2_, v2_, d2_ = synth.updates(seed, 1000, 5 * b - 7, delete_frac4=1, alphabet=300)
+    gpu.lsm.update_batches(to_device(k2_), to_device(v2_), to_device(d2_))
+    for j in range(5):
+        sl = slice(j * b, min(len(k2_), (j + 1) * b))
+        sa.update(k2_[sl], v2_[sl], d2_[sl])
+        o1.apply_batch(k2_[sl], v2_[sl], d2_[sl])
+    assert_sa_equal(gpu, sa, "sa multi")
+    q = synth.lookup_queries(seed, 2000, 1400, alphabet=300)
+    k1, kk2 = synth.range_queries(seed, 300, 1400, 8, domain=300)
+    assert_queries_equal(gpu, o1, q, k1, kk2, "sa multi")

@@ -517,3 +517,67 @@ def test_bulk_build_queries_vs_brute(seed):
         assert (bv is None) == (sf[i] == 0)
         if bv is not None:
             assert bv == sv[i]
+
+
+def _s1_merged_image(s):
+    """All S1 levels concatenated newest (lowest index) first, stable-sorted on
+    the original key with numpy: the record order both structures must share."""
+    ks, vs = [], []
+    for i in range(s.num_levels()):
+        k, v = s.level(i)
+        ks.append(k)
+        vs.append(v)
+    k = np.concatenate(ks) if ks else np.zeros(0, np.uint32)
+    v = np.concatenate(vs) if vs else np.zeros(0, np.uint32)
+    o = np.argsort(k >> 1, kind="stable")
+    return k[o], v[o]
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_sa_array_equals_merged_lsm_levels(seed):
+    # N2 (PAPER.md:759-770): the SA keeps every record in one array, newest
+    # first within a key; the LSM's levels hold the same records split by
+    # recency, so their newest-first stable merge (done here by numpy) must be
+    # the SA array, bit for bit, after every batch and after cleanup.
+    b = 16
+    seed = synth.SEED_BASE + 70 + seed
+    sa, s1 = oracle.ShadowSA(b), oracle.ShadowLSM(b)
+    for j in range(23):
+        n = b if j % 5 else b - 5  # partial batches too
+        k, v, d = synth.updates(seed, j * b, n, delete_frac4=1, alphabet=60)
+        sa.update(k, v, d)
+        s1.update(k, v, d)
+        ak, av = sa.array()
+        mk, mv = _s1_merged_image(s1)
+        assert sa.r == s1.r == j + 1 and len(ak) == (j + 1) * b
+        assert np.array_equal(ak, mk) and np.array_equal(av, mv)
+    sa.cleanup()
+    s1.cleanup()
+    ak, av = sa.array()
+    ck = np.concatenate([s1.level(i)[0] for i in range(s1.num_levels())])
+    cv = np.concatenate([s1.level(i)[1] for i in range(s1.num_levels())])
+    assert sa.r == s1.r and np.array_equal(ak, ck) and np.array_equal(av, cv)
+
+
+def test_sa_merge_work_closed_form():
+    # SPEC.md:350: SA merge work after r batches = b(r-1)(r+2)/2 records.
+    for b in (4, 16):
+        sa = oracle.ShadowSA(b)
+        for r in range(1, 25):
+            k, v, d = synth.updates(synth.SEED_BASE + 71, r * b, b, delete_frac4=0)
+            sa.update(k, v, d)
+            assert sa.merged_records == b * (r - 1) * (r + 2) // 2
+
+
+def test_sa_bulk_build_equals_lsm_bulk_image():
+    # bulk build of the SA = the LSM bulk image read level by level in
+    # ascending order (both are one sort of the padded k*b records, R24)
+    b = 8
+    k, v, d = synth.updates(synth.SEED_BASE + 72, 0, 45, delete_frac4=1, alphabet=30)
+    sa, s1 = oracle.ShadowSA(b), oracle.ShadowLSM(b)
+    sa.bulk_build(k, v, d)
+    s1.bulk_build(k, v, d)
+    ck = np.concatenate([s1.level(i)[0] for i in range(s1.num_levels())])
+    cv = np.concatenate([s1.level(i)[1] for i in range(s1.num_levels())])
+    ak, av = sa.array()
+    assert sa.r == s1.r == 6 and np.array_equal(ak, ck) and np.array_equal(av, cv)
