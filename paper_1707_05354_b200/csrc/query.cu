@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) lookup_kernel(
 // 1 is not needed; state in registers for NL > 0). emit(idx, key, val) is
 // called for each valid key in ascending order; returns the number of valid
 // keys.
-template <int NL, typename Emit>
+template <int NL, bool NEED_VAL, typename Emit>
 __device__ __forceinline__ uint32_t walk_slices(const LevelTable& T, uint64_t* pos, uint32_t z,
                                                 int L, Emit emit) {
   constexpr int CAP = NL > 0 ? NL : LSM_MAX_LEVELS;
@@ -344,7 +344,7 @@ __device__ __forceinline__ uint32_t walk_slices(const LevelTable& T, uint64_t* p
         if (first) {  // newest record of key m: run head in the lowest level
           first = false;
           valid = (__ldg(K + p) & 1u) != 0;
-          if (valid) val = __ldg(T.vals[j] + p);
+          if (NEED_VAL && valid) val = __ldg(T.vals[j] + p);
         }
         // skip the rest of this level's run of key m (stale copies)
         uint32_t nk = kSent;
@@ -361,6 +361,46 @@ __device__ __forceinline__ uint32_t walk_slices(const LevelTable& T, uint64_t* p
       emit(cnt, m, val);
       ++cnt;
     }
+  }
+  return cnt;
+}
+
+// One occupied level: a record is valid iff it is a regular run head (the
+// "no lower level" condition is vacuous), so the slice [pos, first key > z)
+// is evaluated 8 records at a time from two independent 16-byte loads of the
+// aligned group, instead of one dependent load per record. K must be 16-byte
+// aligned (the caller falls back to walk_slices otherwise).
+template <bool NEED_VAL, typename Emit>
+__device__ __forceinline__ uint32_t walk_one(const uint32_t* __restrict__ K,
+                                             const uint32_t* __restrict__ V, uint64_t n,
+                                             uint64_t pos, uint32_t z, Emit emit) {
+  uint32_t cnt = 0;
+  if (pos >= n) return 0;
+  uint32_t prev = 0xFFFFFFFFu;  // K[pos] starts a run: pos = lower_bound(k1)
+  uint64_t g = pos & ~7ull;
+  while (true) {
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(K + g));  // +16 words of slack
+    const uint4 b = __ldg(reinterpret_cast<const uint4*>(K + g + 4));
+    const uint32_t kk[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    bool stop = false;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint64_t p = g + i;
+      if (!stop && p >= pos) {
+        const uint32_t k = kk[i] >> 1;
+        if (p >= n || k > z) {
+          stop = true;
+        } else {
+          if (k != prev && (kk[i] & 1u)) {
+            emit(cnt, k, NEED_VAL ? __ldg(V + p) : 0u);
+            ++cnt;
+          }
+          prev = k;
+        }
+      }
+    }
+    if (stop) break;
+    g += 8;
   }
   return cnt;
 }
@@ -405,7 +445,12 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) count_kernel(
       for (int j = 0; j < CAP; ++j)
         if (j < L) pos_out[(uint64_t)j * nq + i] = (uint32_t)pos[j];
     }
-    const uint32_t c = walk_slices<NL>(T, pos, z, L, [](uint32_t, uint32_t, uint32_t) {});
+    uint32_t c;
+    if (NL == 1 && (reinterpret_cast<uintptr_t>(T.keys[0]) & 15) == 0)
+      c = walk_one<false>(T.keys[0], T.vals[0], T.n[0], pos[0], z,
+                          [](uint32_t, uint32_t, uint32_t) {});
+    else
+      c = walk_slices<NL, false>(T, pos, z, L, [](uint32_t, uint32_t, uint32_t) {});
     if (act) counts[i] = c;
   }
 }
@@ -428,13 +473,17 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) range_write_kernel(
 #pragma unroll
     for (int j = 0; j < CAP; ++j)
       if (j < L) pos[j] = __ldg(pos_in + (uint64_t)j * nq + i);
-    walk_slices<NL>(T, pos, z, L, [&](uint32_t k, uint32_t key, uint32_t val) {
+    auto put = [&](uint32_t k, uint32_t key, uint32_t val) {
       const uint64_t o = base + k;
       if (o < capacity) {
         keys_out[o] = key;
         vals_out[o] = val;
       }
-    });
+    };
+    if (NL == 1 && (reinterpret_cast<uintptr_t>(T.keys[0]) & 15) == 0)
+      walk_one<true>(T.keys[0], T.vals[0], T.n[0], pos[0], z, put);
+    else
+      walk_slices<NL, true>(T, pos, z, L, put);
   }
 }
 
@@ -515,7 +564,7 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) range_kernel(
 #pragma unroll
     for (int j = 0; j < CAP; ++j)
       if (j < L) pos0[j] = pos[j];
-    const uint32_t c = walk_slices<NL>(T, pos, z, L, [](uint32_t, uint32_t, uint32_t) {});
+    const uint32_t c = walk_slices<NL, false>(T, pos, z, L, [](uint32_t, uint32_t, uint32_t) {});
     // warp exclusive scan of the counts
     uint64_t x = c;
 #pragma unroll
@@ -527,7 +576,7 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) range_kernel(
     const uint64_t base = task_lookback(status, t, wtot) + x - c;
     if (act) offsets[i] = base;
     if (t == ntasks - 1 && lane == 31) offsets[nq] = base + c;
-    walk_slices<NL>(T, pos0, z, L, [&](uint32_t k, uint32_t key, uint32_t val) {
+    walk_slices<NL, true>(T, pos0, z, L, [&](uint32_t k, uint32_t key, uint32_t val) {
       const uint64_t o = base + k;
       if (o < capacity) {
         keys_out[o] = key;
