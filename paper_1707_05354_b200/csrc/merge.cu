@@ -37,9 +37,19 @@ constexpr int kMergeThreads = kConsumers + 32;
 // 15 (odd) records per thread: neighbouring lanes then read the staged
 // windows ~7.5 words apart, spread over all 32 banks (16 gave 8-way
 // conflicts, measured: the merge was shared-memory bound)
-constexpr int kMergeItems = 15;
+#ifndef MERGE_ITEMS
+#define MERGE_ITEMS 15
+#endif
+constexpr int kMergeItems = MERGE_ITEMS;
 constexpr int kMergeTile = kConsumers * kMergeItems;  // 3840
-constexpr int kStages = 3;
+#ifndef MERGE_STAGES
+#define MERGE_STAGES 2
+#endif
+#ifndef MERGE_CTAS
+#define MERGE_CTAS 3
+#endif
+constexpr int kStages = MERGE_STAGES;
+constexpr int kMergeCtasPerSm = MERGE_CTAS;
 constexpr int kBufElems = kMergeTile + 16;  // A + B windows incl. alignment slack
 
 struct StageInfo {
@@ -278,10 +288,12 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(
 #pragma unroll
       for (int q = 0; q < kMergeItems; ++q) rv[q] = V[min(src[q], (uint32_t)kBufElems - 1)];
       if (out_f1 != nullptr) {  // fence keys of the new level: every 8th output
+        const uint64_t g0 = info.d0 + dt;
+        const uint32_t q0 = (uint32_t)((kF1Step - (g0 & (kF1Step - 1))) & (kF1Step - 1));
 #pragma unroll
         for (int q = 0; q < kMergeItems; ++q) {
-          const uint64_t g = info.d0 + dt + q;
-          if (dt + q < tile_n && (g & (kF1Step - 1)) == 0) out_f1[g / kF1Step] = rk[q];
+          if ((uint32_t)q >= q0 && ((q - q0) & (kF1Step - 1)) == 0 && dt + q < tile_n)
+            out_f1[(g0 + q) / kF1Step] = rk[q];
         }
       }
       consumers_sync();  // every consumer is done reading this stage
@@ -340,7 +352,7 @@ cudaError_t launch_merge(const uint32_t* ak, const uint32_t* av, uint64_t na,
   if ((reinterpret_cast<uintptr_t>(ok) | reinterpret_cast<uintptr_t>(ov)) & 15)
     return cudaErrorMisalignedAddress;
   const uint64_t ntiles = (total + kMergeTile - 1) / kMergeTile;
-  const uint64_t grid = std::min<uint64_t>(ntiles, (uint64_t)g_num_sms * 2);
+  const uint64_t grid = std::min<uint64_t>(ntiles, (uint64_t)g_num_sms * kMergeCtasPerSm);
   hk.begin(hk.ctx, LSM_K_MERGE, s);
   cudaError_t e = launch_pdl(merge_kernel, (unsigned)grid, kMergeThreads, sizeof(MergeSmem), s, ak,
                              av, na, bk, bv, nb, ok, ov, ntiles, out_f1);

@@ -21,16 +21,16 @@ int main(int argc, char** argv) {
   gen_sorted<<<512, 256>>>(ak, av, n, 1); gen_sorted<<<512, 256>>>(bk, bv, n, 2);
   LaunchHooks hk{hb, he, nullptr};
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  for (int i = 0; i < 10; ++i) launch_merge(ak, av, n, bk, bv, n, ok, ov, 0, hk);
+  for (int i = 0; i < 10; ++i) launch_merge(ak, av, n, bk, bv, n, ok, ov, nullptr, 0, hk);
   cudaEventRecord(e0);
-  for (int i = 0; i < 50; ++i) launch_merge(ak, av, n, bk, bv, n, ok, ov, 0, hk);
+  for (int i = 0; i < 50; ++i) launch_merge(ak, av, n, bk, bv, n, ok, ov, nullptr, 0, hk);
   cudaEventRecord(e1); cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1);
   printf("n=%llu+%llu merge avg %.2f us  %.1f GB/s\n", (unsigned long long)n, (unsigned long long)n, ms * 20, 2 * n * 16 / (ms / 50 * 1e-3) / 1e9);
   unsigned long long* probe; size_t pn = 4096 * 8;
   cudaMalloc(&probe, pn * 8); cudaMemset(probe, 0, pn * 8);
   cudaMemcpyToSymbol(g_mprobe, &probe, sizeof(probe));
-  launch_merge(ak, av, n, bk, bv, n, ok, ov, 0, hk);
+  launch_merge(ak, av, n, bk, bv, n, ok, ov, nullptr, 0, hk);
   cudaDeviceSynchronize();
   std::vector<unsigned long long> P(pn);
   cudaMemcpy(P.data(), probe, pn * 8, cudaMemcpyDeviceToHost);
