@@ -254,6 +254,21 @@ lsm_status lsm_shard_clip(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2, 
 lsm_status lsm_shard_sum(lsm_t* h, const uint32_t* d_in, uint32_t parts, uint64_t n,
                          uint32_t* d_out, void* stream);
 
+/* Range assembly at a query's origin rank (the concatenation
+ * in shard order of SURVEY §8(e)): shard s returned, for this rank's nq
+ * queries, its offsets slice d_offs[s*nq + q] (u64, in the sender's own
+ * numbering, i.e. not rebased) and a block of d_block_len[s] (key, value)
+ * pairs; the P blocks are concatenated in shard order in d_keys_in /
+ * d_vals_in. Writes d_offsets_out[nq+1] and each query's pairs, shard 0's
+ * first (shards own ascending key intervals, so the result is sorted by key,
+ * PAPER.md:736); pairs are written while < capacity. Syncs the stream;
+ * *total_out = number of pairs; LSM_ERR_CAPACITY if it exceeds capacity.   */
+lsm_status lsm_shard_range_assemble(lsm_t* h, const uint64_t* d_offs, const uint64_t* d_block_len,
+                                   uint32_t parts, uint64_t nq, const uint32_t* d_keys_in,
+                                   const uint32_t* d_vals_in, uint64_t* d_offsets_out,
+                                   uint32_t* d_keys_out, uint32_t* d_vals_out, uint64_t capacity,
+                                   uint64_t* total_out, void* stream);
+
 /* ------------------------------------------------------------------------ */
 /* Introspection                                                             */
 /* ------------------------------------------------------------------------ */

@@ -66,6 +66,8 @@ SIGNATURES = {
     "lsm_shard_scatter": ([_vp, _vp, _vp, _vp, _u64, _vp, _vp, _vp], _st),
     "lsm_shard_clip": ([_vp, _vp, _vp, _u64, ctypes.c_uint32, ctypes.c_uint32, _vp, _vp, _vp], _st),
     "lsm_shard_sum": ([_vp, _vp, ctypes.c_uint32, _u64, _vp, _vp], _st),
+    "lsm_shard_range_assemble": ([_vp, _vp, _vp, ctypes.c_uint32, _u64, _vp, _vp, _vp, _vp, _vp,
+                                  _u64, ctypes.POINTER(_u64), _vp], _st),
 }
 
 
@@ -360,6 +362,26 @@ class GpuLSM:
                                           _dev(oo, 1), _dev(po), _dev(cnt), _stream_ptr(stream)),
                "lsm_shard_bucket")
         return ko, vo, oo, po, cnt
+
+    def shard_range_assemble(self, offs, block_len, parts, nq, keys_in, vals_in, stream=None):
+        """Assemble this rank's range results from the shards' parts:
+        offs int64 [parts*nq] (each shard's offsets slice), block_len int64
+        [parts], the pair blocks concatenated in shard order. Returns
+        (offsets[nq+1] int64, keys, vals)."""
+        torch = _torch()
+        dev = offs.device
+        cap = int(keys_in.numel())
+        offsets = torch.empty(nq + 1, dtype=torch.int64, device=dev)
+        keys = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+        vals = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+        total = _u64(0)
+        _check(self._lib.lsm_shard_range_assemble(
+            self.h, _dev(offs, 8, "offs"), _dev(block_len, 8, "block_len"), int(parts), int(nq),
+            _dev(keys_in, 4, "keys_in"), _dev(vals_in, 4, "vals_in"), _dev(offsets, 8, "offsets"),
+            _dev(keys, 4, "keys"), _dev(vals, 4, "vals"), cap, ctypes.byref(total),
+            _stream_ptr(stream)), "lsm_shard_range_assemble")
+        t = int(total.value)
+        return offsets, keys[:t], vals[:t]
 
     def shard_scatter(self, perm, vals_in, found_in, vals_out, found_out, stream=None):
         _check(self._lib.lsm_shard_scatter(self.h, _dev(perm), _dev(vals_in), _dev(found_in, 1),

@@ -320,6 +320,11 @@ cudaError_t launch_scatter_back(const uint32_t* perm, const uint32_t* vin, const
 cudaError_t launch_clip(const uint32_t* k1, const uint32_t* k2, uint64_t n, uint32_t lo,
                         uint32_t hi, uint32_t* o1, uint32_t* o2, cudaStream_t s,
                         const LaunchHooks& hk);
+cudaError_t launch_range_assemble(const uint64_t* offs, const uint64_t* blen, uint32_t P,
+                                  uint64_t nq, const uint32_t* kin, const uint32_t* vin,
+                                  uint64_t* offsets, uint32_t* kout, uint32_t* vout,
+                                  uint64_t capacity, uint32_t* totals, uint64_t* sums,
+                                  cudaStream_t s, const LaunchHooks& hk);
 cudaError_t launch_sum_parts(const uint32_t* in, uint32_t parts, uint64_t n, uint32_t* out,
                              cudaStream_t s, const LaunchHooks& hk);
 

@@ -997,6 +997,33 @@ lsm_status lsm_shard_sum(lsm_t* h, const uint32_t* d_in, uint32_t parts, uint64_
   return LSM_OK;
 }
 
+lsm_status lsm_shard_range_assemble(lsm_t* h, const uint64_t* d_offs, const uint64_t* d_block_len,
+                                   uint32_t parts, uint64_t nq, const uint32_t* d_keys_in,
+                                   const uint32_t* d_vals_in, uint64_t* d_offsets_out,
+                                   uint32_t* d_keys_out, uint32_t* d_vals_out, uint64_t capacity,
+                                   uint64_t* total_out, void* stream) {
+  if (!h || parts == 0 || !total_out || !d_offsets_out) return LSM_ERR_INVALID_ARG;
+  cudaStream_t s = S(stream);
+  if (nq == 0) {
+    CK(cudaMemsetAsync(d_offsets_out, 0, 8, s));
+    *total_out = 0;
+    return LSM_OK;
+  }
+  if (!d_offs || !d_block_len) return LSM_ERR_INVALID_ARG;
+  if (capacity > 0 && (!d_keys_out || !d_vals_out || !d_keys_in || !d_vals_in))
+    return LSM_ERR_INVALID_ARG;
+  const uint64_t tb = align_up(nq * 4, 256);
+  CK(ensure_qbuf(h, tb + scan_scratch_words(nq) * 8, s));
+  uint8_t* qb = static_cast<uint8_t*>(h->qbuf);
+  CK(launch_range_assemble(d_offs, d_block_len, parts, nq, d_keys_in, d_vals_in, d_offsets_out,
+                           d_keys_out, d_vals_out, capacity, reinterpret_cast<uint32_t*>(qb),
+                           reinterpret_cast<uint64_t*>(qb + tb), s, hooks(h)));
+  CK(cudaMemcpyAsync(h->h_pinned, d_offsets_out + nq, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  *total_out = h->h_pinned[0];
+  return *total_out > capacity ? LSM_ERR_CAPACITY : LSM_OK;
+}
+
 lsm_status lsm_batch_size(const lsm_t* h, uint64_t* b_out) {
   if (!h || !b_out) return LSM_ERR_INVALID_ARG;
   *b_out = h->b;

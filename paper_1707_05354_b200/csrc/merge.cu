@@ -147,14 +147,14 @@ __device__ __forceinline__ uint64_t warp_merge_path(const uint32_t* __restrict__
 }
 
 #ifdef GPULSM_PROBE
-__device__ unsigned long long* g_mprobe = nullptr;  // [cta][8] globaltimer stamps
+__device__ unsigned long long* g_mprobe = nullptr;  // [cta][16] globaltimer stamps
 __device__ __forceinline__ unsigned long long mtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
 #define MPROBE(k) \
-  do { if (g_mprobe) g_mprobe[blockIdx.x * 8 + (k)] = mtimer(); } while (0)
+  do { if (g_mprobe) g_mprobe[blockIdx.x * 16 + (k)] = mtimer(); } while (0)
 #else
 #define MPROBE(k) \
   do {            \
@@ -265,6 +265,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(
         else
           hi = mid;
       }
+      if (tid == 32 && k == 0) MPROBE(7);
       uint32_t ai = lo, bi = dt - lo;
       uint32_t ka = ai < na_t ? K[info.ka + ai] : 0u;
       uint32_t kb = bi < nb_t ? K[info.kb + bi] : 0u;
@@ -284,6 +285,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(
           kb = bi < nb_t ? K[info.kb + bi] : 0u;
         }
       }
+      if (tid == 32 && k == 0) MPROBE(8);
       uint32_t rv[kMergeItems];
 #pragma unroll
       for (int q = 0; q < kMergeItems; ++q) rv[q] = V[min(src[q], (uint32_t)kBufElems - 1)];
@@ -296,7 +298,9 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(
             out_f1[(g0 + q) / kF1Step] = rk[q];
         }
       }
+      if (tid == 32 && k == 0) MPROBE(9);
       consumers_sync();  // every consumer is done reading this stage
+      if (tid == 32 && k == 0) MPROBE(10);
       // stage the merged tile in place (lane stride 15 words: conflict-free)
 #pragma unroll
       for (int q = 0; q < kMergeItems; ++q) {
@@ -307,6 +311,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(
       }
       fence_proxy_async_smem();  // generic smem writes -> visible to the bulk copy
       consumers_sync();
+      if (tid == 32 && k == 0) MPROBE(11);
       if (ct == 0) {
         // one TMA bulk store per array, then free the stage once read
         const uint32_t n16 = tile_n & ~3u;

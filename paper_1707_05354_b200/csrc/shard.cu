@@ -12,6 +12,8 @@
 //  * scatter_back: out[perm[i]] = in[i] for lookup results.
 //  * clip: intersect [k1, k2] with a shard's key range (empty stays empty).
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace gpulsm {
@@ -158,6 +160,57 @@ __global__ void clip_kernel(const uint32_t* __restrict__ k1, const uint32_t* __r
   }
 }
 
+// Range assembly at the query's origin: shard s sent, for
+// each of this rank's nq queries, its offsets slice offs[s][q] (u64, the
+// sender's numbering) and one block of pairs (block_len[s] of them, blocks
+// concatenated in shard order). count[s][q] = offs[s][q+1] - offs[s][q]
+// (the block end for the last query).
+__device__ __forceinline__ uint64_t part_count(const uint64_t* offs, const uint64_t* blen,
+                                               uint32_t s, uint64_t q, uint64_t nq) {
+  const uint64_t* o = offs + (uint64_t)s * nq;
+  const uint64_t end = q + 1 < nq ? o[q + 1] : o[0] + blen[s];
+  return end - o[q];
+}
+
+__global__ void range_totals_kernel(const uint64_t* __restrict__ offs,
+                                    const uint64_t* __restrict__ blen, uint32_t P, uint64_t nq,
+                                    uint32_t* __restrict__ totals) {
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t t = 0;
+    for (uint32_t s = 0; s < P; ++s) t += part_count(offs, blen, s, q, nq);
+    totals[q] = (uint32_t)t;
+  }
+}
+
+// pairs of (shard s, query q) -> out[offsets[q] + (pairs of shards < s)],
+// shard order = key order, so each query's pairs stay sorted
+__global__ void range_scatter_kernel(const uint64_t* __restrict__ offs,
+                                     const uint64_t* __restrict__ blen, uint32_t P, uint64_t nq,
+                                     const uint32_t* __restrict__ kin,
+                                     const uint32_t* __restrict__ vin,
+                                     const uint64_t* __restrict__ offsets,
+                                     uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
+                                     uint64_t capacity) {
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t dst = offsets[q], base = 0;
+    for (uint32_t s = 0; s < P; ++s) {
+      const uint64_t* o = offs + (uint64_t)s * nq;
+      const uint64_t c = part_count(offs, blen, s, q, nq);
+      const uint64_t src = base + (o[q] - o[0]);
+      for (uint64_t i = 0; i < c; ++i) {
+        if (dst + i < capacity) {
+          kout[dst + i] = kin[src + i];
+          vout[dst + i] = vin[src + i];
+        }
+      }
+      dst += c;
+      base += blen[s];
+    }
+  }
+}
+
 __global__ void sum_parts_kernel(const uint32_t* __restrict__ in, uint32_t parts, uint64_t n,
                                  uint32_t* __restrict__ out) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -220,6 +273,24 @@ cudaError_t launch_clip(const uint32_t* k1, const uint32_t* k2, uint64_t n, uint
   hk.begin(hk.ctx, LSM_K_OTHER, s);
   clip_kernel<<<grid, 256, 0, s>>>(k1, k2, n, lo, hi, o1, o2);
   hk.end(hk.ctx, LSM_K_OTHER, (double)n * 16.0, s, 1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_range_assemble(const uint64_t* offs, const uint64_t* blen, uint32_t P,
+                                  uint64_t nq, const uint32_t* kin, const uint32_t* vin,
+                                  uint64_t* offsets, uint32_t* kout, uint32_t* vout,
+                                  uint64_t capacity, uint32_t* totals, uint64_t* sums,
+                                  cudaStream_t s, const LaunchHooks& hk) {
+  const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nq + 255) / 256, 148 * 8));
+  hk.begin(hk.ctx, LSM_K_OTHER, s);
+  range_totals_kernel<<<g, 256, 0, s>>>(offs, blen, P, nq, totals);
+  hk.end(hk.ctx, LSM_K_OTHER, (double)nq * (8.0 * P + 4.0), s, 1);
+  cudaError_t e = launch_scan(totals, nq, offsets, sums, s, hk);
+  if (e != cudaSuccess) return e;
+  hk.begin(hk.ctx, LSM_K_OTHER, s);
+  range_scatter_kernel<<<g, 256, 0, s>>>(offs, blen, P, nq, kin, vin, offsets, kout, vout,
+                                         capacity);
+  hk.end(hk.ctx, LSM_K_OTHER, (double)nq * (8.0 * P + 8.0), s, 1);
   return cudaGetLastError();
 }
 

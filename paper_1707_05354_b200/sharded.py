@@ -27,6 +27,12 @@ interval (lsm_shard_clip), counts locally, and the per-shard partial counts
 go back to each query's origin with an all-to-all and are summed there
 (lsm_shard_sum): a range that spans shards is the sum of its pieces.
 
+Ranges: the same gather + clip, one local range over all ranks' queries, then
+each origin receives from every shard its offsets slice and its block of
+pairs (an all-to-all-v after an exchange of the block lengths) and
+lsm_shard_range_assemble concatenates each query's pieces in shard order --
+key order, since shards own ascending key intervals.
+
 All data-path arithmetic runs in libgpulsm kernels; torch.distributed only
 moves bytes. The backend is pluggable so the routing logic can be tested on
 CPU with gloo (tests/test_sharded_gloo.py); the GPU backend is the product.
@@ -96,6 +102,12 @@ class GpuShardBackend:
 
     def count(self, k1, k2):
         return self.lsm.count(k1, k2)
+
+    def range(self, k1, k2):
+        return self.lsm.range(k1, k2)
+
+    def range_assemble(self, offs, block_len, P, nq, keys, vals):
+        return self.lsm.shard_range_assemble(offs, block_len, P, nq, keys, vals)
 
 
 class ShardedLSM:
@@ -191,6 +203,30 @@ class ShardedLSM:
         partial = self.backend.count(c1, c2)
         recv = self._a2a(partial, [nq] * self.P, [nq] * self.P, torch.int32)
         return self.backend.sum_parts(recv, self.P, nq)
+
+    def range(self, k1, k2):
+        """Ranges for this rank's (k1, k2) queries: (offsets[nq+1], keys, vals)
+        with each query's pairs in key order; every rank passes the same number
+        of queries."""
+        nq = k1.numel()
+        P = self.P
+        all1 = self.backend.empty(nq * P, torch.int32)
+        all2 = self.backend.empty(nq * P, torch.int32)
+        dist.all_gather_into_tensor(all1, k1, group=self.group)
+        dist.all_gather_into_tensor(all2, k2, group=self.group)
+        c1, c2 = self.backend.clip(all1, all2, self.lo, self.hi)
+        off, rk, rv = self.backend.range(c1, c2)  # queries of origin o at [o*nq, (o+1)*nq)
+        bnd = self.backend.host_list(off[0:P * nq + 1:nq])
+        send = [bnd[o + 1] - bnd[o] for o in range(P)]
+        sl = self.backend.empty(P, torch.int64)
+        sl.copy_(torch.tensor(send, dtype=torch.int64))
+        rl = self.backend.empty(P, torch.int64)
+        dist.all_to_all_single(rl, sl, group=self.group)
+        recv = self.backend.host_list(rl)
+        roffs = self._a2a(off[:P * nq].contiguous(), [nq] * P, [nq] * P, torch.int64)
+        rkk = self._a2a(rk[bnd[0]:bnd[P]].contiguous(), send, recv, torch.int32)
+        rvv = self._a2a(rv[bnd[0]:bnd[P]].contiguous(), send, recv, torch.int32)
+        return self.backend.range_assemble(roffs, rl, P, nq, rkk, rvv)
 
 
 def run_sharded_bench(args, dist_mod, rank, world, local_rank):

@@ -71,6 +71,39 @@ def test_scatter_clip_sum_kernels():
     assert np.array_equal(to_numpy_u32(s), parts.reshape(3, n).sum(axis=0).astype(np.uint32))
 
 
+def test_range_assemble_kernel():
+    # lsm_shard_range_assemble vs a numpy definition: P = 3 shards' parts for
+    # nq queries, offsets slices in the senders' numbering, blocks in shard
+    # order; each query's pieces concatenated shard 0 first.
+    g = pkg.GpuLSM(16)
+    rng = np.random.default_rng(4)
+    P, nq = 3, 5000
+    cnt = rng.integers(0, 6, (P, nq))
+    cnt[:, 7] = 0  # a query with nothing anywhere
+    offs = np.zeros((P, nq), np.int64)
+    blen = cnt.sum(axis=1)
+    for s_ in range(P):
+        start = int(rng.integers(0, 1000))  # sender numbering need not start at 0
+        offs[s_] = start + np.concatenate([[0], np.cumsum(cnt[s_])[:-1]])
+    tot = int(blen.sum())
+    keys = rng.integers(0, 1 << 31, tot).astype(np.uint32)
+    vals = np.arange(tot, dtype=np.uint32)
+    o, k, v = g.shard_range_assemble(torch.from_numpy(offs.reshape(-1)).cuda(),
+                                     torch.from_numpy(blen.astype(np.int64)).cuda(), P, nq,
+                                     to_device(keys), to_device(vals))
+    eoff = np.concatenate([[0], np.cumsum(cnt.sum(axis=0))])
+    base = np.concatenate([[0], np.cumsum(blen)])
+    ek, ev = [], []
+    for q in range(nq):
+        for s_ in range(P):
+            src = base[s_] + offs[s_, q] - offs[s_, 0]
+            ek.append(keys[src:src + cnt[s_, q]])
+            ev.append(vals[src:src + cnt[s_, q]])
+    assert np.array_equal(o.cpu().numpy(), eoff)
+    assert np.array_equal(to_numpy_u32(k), np.concatenate(ek))
+    assert np.array_equal(to_numpy_u32(v), np.concatenate(ev))
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -101,5 +134,9 @@ def test_sharded_router_single_gpu_nccl():
         k1, k2 = synth.range_queries(7, 3000, 9 * b, 12, domain=50_002)
         c = sh.count(to_device(k1), to_device(k2))
         assert np.array_equal(to_numpy_u32(c), o.count(k1, k2))
+        ro, rk, rv = sh.range(to_device(k1), to_device(k2))
+        ooff, ok, ov2 = o.range(k1, k2)
+        assert np.array_equal(ro.cpu().numpy().astype(np.uint64), ooff)
+        assert np.array_equal(to_numpy_u32(rk), ok) and np.array_equal(to_numpy_u32(rv), ov2)
     finally:
         dist.destroy_process_group()

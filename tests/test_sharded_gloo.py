@@ -88,6 +88,35 @@ class CpuTestBackend:
         c = self.store.count(k1.numpy().view(np.uint32), k2.numpy().view(np.uint32))
         return torch.from_numpy(c.view(np.int32).copy())
 
+    def range(self, k1, k2):
+        off, k, v = self.store.range(k1.numpy().view(np.uint32), k2.numpy().view(np.uint32))
+        return (torch.from_numpy(off.astype(np.int64)), torch.from_numpy(k.view(np.int32).copy()),
+                torch.from_numpy(v.view(np.int32).copy()))
+
+    def range_assemble(self, offs, block_len, P, nq, keys, vals):
+        # numpy stand-in of lsm_shard_range_assemble
+        o = offs.numpy().reshape(P, nq)
+        bl = block_len.numpy()
+        base = np.concatenate([[0], np.cumsum(bl)])
+        cnt = np.zeros((P, nq), np.int64)
+        for s_ in range(P):
+            ends = np.append(o[s_, 1:], o[s_, 0] + bl[s_])
+            cnt[s_] = ends - o[s_]
+        tot = cnt.sum(axis=0)
+        offsets = np.concatenate([[0], np.cumsum(tot)]).astype(np.int64)
+        ko = np.empty(int(offsets[-1]), np.int32)
+        vo = np.empty(int(offsets[-1]), np.int32)
+        kn, vn = keys.numpy(), vals.numpy()
+        for q in range(nq):
+            d = offsets[q]
+            for s_ in range(P):
+                src = base[s_] + o[s_, q] - o[s_, 0]
+                c = cnt[s_, q]
+                ko[d:d + c] = kn[src:src + c]
+                vo[d:d + c] = vn[src:src + c]
+                d += c
+        return torch.from_numpy(offsets), torch.from_numpy(ko), torch.from_numpy(vo)
+
 
 def _free_port():
     s = socket.socket()
@@ -126,8 +155,11 @@ def _worker(rank, world, port, scenario, out_q):
         k1 = np.concatenate([k1, np.array([0, (1 << 30) - 5, 0], np.uint32)])
         k2 = np.concatenate([k2, np.array([0xFFFFFFFF, (1 << 30) + 5, 3], np.uint32)])
         c = sh.count(torch.from_numpy(k1.view(np.int32).copy()), torch.from_numpy(k2.view(np.int32).copy()))
+        ro, rk, rv = sh.range(torch.from_numpy(k1.view(np.int32).copy()),
+                              torch.from_numpy(k2.view(np.int32).copy()))
         out_q.put((rank, q, qv.numpy().view(np.uint32), qf.numpy(), k1, k2,
-                   c.numpy().view(np.uint32), sh.overflow_splits, sh.backend.batch_sizes))
+                   c.numpy().view(np.uint32), sh.overflow_splits, sh.backend.batch_sizes,
+                   (ro.numpy(), rk.numpy().view(np.uint32), rv.numpy().view(np.uint32))))
     finally:
         dist.destroy_process_group()
 
@@ -165,11 +197,14 @@ def _global_oracle(scenario):
 def test_sharded_router_matches_global_oracle(scenario):
     res = _run(scenario)
     o = _global_oracle(scenario)
-    for (rank, q, qv, qf, k1, k2, c, splits, sizes) in res:
+    for (rank, q, qv, qf, k1, k2, c, splits, sizes, rng) in res:
         ov, of = o.lookup(q)
         assert np.array_equal(qf, of), rank
         assert np.array_equal(qv[qf == 1], ov[of == 1]), rank
         assert np.array_equal(c, o.count(k1, k2)), rank
+        ooff, ok, ovv = o.range(k1, k2)
+        assert np.array_equal(rng[0].astype(np.uint64), ooff), rank
+        assert np.array_equal(rng[1], ok) and np.array_equal(rng[2], ovv), rank
 
 
 def test_sharded_router_oversize_split():
@@ -181,10 +216,13 @@ def test_sharded_router_oversize_split():
     r0 = res[0]
     assert r0[7] == 4  # one split per batch on shard 0
     assert max(r0[8]) <= 128
-    for (rank, q, qv, qf, k1, k2, c, splits, sizes) in res:
+    for (rank, q, qv, qf, k1, k2, c, splits, sizes, rng) in res:
         ov, of = o.lookup(q)
         assert np.array_equal(qf, of) and np.array_equal(qv[qf == 1], ov[of == 1])
         assert np.array_equal(c, o.count(k1, k2))
+        ooff, ok, ovv = o.range(k1, k2)
+        assert np.array_equal(rng[0].astype(np.uint64), ooff)
+        assert np.array_equal(rng[1], ok) and np.array_equal(rng[2], ovv)
 
 
 def test_shard_bounds_partition_the_domain():
