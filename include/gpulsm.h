@@ -269,6 +269,16 @@ lsm_status lsm_shard_range_assemble(lsm_t* h, const uint64_t* d_offs, const uint
                                    uint32_t* d_keys_out, uint32_t* d_vals_out, uint64_t capacity,
                                    uint64_t* total_out, void* stream);
 
+/* Successor / predecessor across shards (R23): d_keys,
+ * d_vals, d_found hold `parts` shards' local answers for the same n queries
+ * ([part][n], shard order = ascending key intervals). Per query: the first
+ * shard with an answer (last = 0: successor) or the last one (last = 1:
+ * predecessor); ⊥ (LSM_NOT_FOUND, found 0) if none. d_found_out may be NULL. */
+lsm_status lsm_shard_pick(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals,
+                          const uint8_t* d_found, uint32_t parts, uint64_t n, int last,
+                          uint32_t* d_keys_out, uint32_t* d_vals_out, uint8_t* d_found_out,
+                          void* stream);
+
 /* ------------------------------------------------------------------------ */
 /* Introspection                                                             */
 /* ------------------------------------------------------------------------ */

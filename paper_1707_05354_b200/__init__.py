@@ -66,6 +66,8 @@ SIGNATURES = {
     "lsm_shard_scatter": ([_vp, _vp, _vp, _vp, _u64, _vp, _vp, _vp], _st),
     "lsm_shard_clip": ([_vp, _vp, _vp, _u64, ctypes.c_uint32, ctypes.c_uint32, _vp, _vp, _vp], _st),
     "lsm_shard_sum": ([_vp, _vp, ctypes.c_uint32, _u64, _vp, _vp], _st),
+    "lsm_shard_pick": ([_vp, _vp, _vp, _vp, ctypes.c_uint32, _u64, ctypes.c_int, _vp, _vp, _vp,
+                        _vp], _st),
     "lsm_shard_range_assemble": ([_vp, _vp, _vp, ctypes.c_uint32, _u64, _vp, _vp, _vp, _vp, _vp,
                                   _u64, ctypes.POINTER(_u64), _vp], _st),
 }
@@ -362,6 +364,19 @@ class GpuLSM:
                                           _dev(oo, 1), _dev(po), _dev(cnt), _stream_ptr(stream)),
                "lsm_shard_bucket")
         return ko, vo, oo, po, cnt
+
+    def shard_pick(self, keys, vals, found, parts, n, last, stream=None):
+        """First (last=False) / last (last=True) shard answer per query."""
+        torch = _torch()
+        ko = torch.empty(n, dtype=torch.int32, device=keys.device)
+        vo = torch.empty(n, dtype=torch.int32, device=keys.device)
+        fo = torch.empty(n, dtype=torch.uint8, device=keys.device)
+        _check(self._lib.lsm_shard_pick(self.h, _dev(keys, 4, "keys"), _dev(vals, 4, "vals"),
+                                        _dev(found, 1, "found"), int(parts), int(n), int(bool(last)),
+                                        _dev(ko, 4, "keys_out"), _dev(vo, 4, "vals_out"),
+                                        _dev(fo, 1, "found_out"), _stream_ptr(stream)),
+               "lsm_shard_pick")
+        return ko, vo, fo
 
     def shard_range_assemble(self, offs, block_len, parts, nq, keys_in, vals_in, stream=None):
         """Assemble this rank's range results from the shards' parts:

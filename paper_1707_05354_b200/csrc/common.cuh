@@ -325,6 +325,9 @@ cudaError_t launch_range_assemble(const uint64_t* offs, const uint64_t* blen, ui
                                   uint64_t* offsets, uint32_t* kout, uint32_t* vout,
                                   uint64_t capacity, uint32_t* totals, uint64_t* sums,
                                   cudaStream_t s, const LaunchHooks& hk);
+cudaError_t launch_pick(const uint32_t* kin, const uint32_t* vin, const uint8_t* fin,
+                        uint32_t parts, uint64_t n, int last, uint32_t* kout, uint32_t* vout,
+                        uint8_t* fout, cudaStream_t s, const LaunchHooks& hk);
 cudaError_t launch_sum_parts(const uint32_t* in, uint32_t parts, uint64_t n, uint32_t* out,
                              cudaStream_t s, const LaunchHooks& hk);
 

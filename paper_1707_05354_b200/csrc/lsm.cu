@@ -1024,6 +1024,18 @@ lsm_status lsm_shard_range_assemble(lsm_t* h, const uint64_t* d_offs, const uint
   return *total_out > capacity ? LSM_ERR_CAPACITY : LSM_OK;
 }
 
+lsm_status lsm_shard_pick(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals,
+                          const uint8_t* d_found, uint32_t parts, uint64_t n, int last,
+                          uint32_t* d_keys_out, uint32_t* d_vals_out, uint8_t* d_found_out,
+                          void* stream) {
+  if (!h || parts == 0) return LSM_ERR_INVALID_ARG;
+  if (n == 0) return LSM_OK;
+  if (!d_keys || !d_vals || !d_found || !d_keys_out || !d_vals_out) return LSM_ERR_INVALID_ARG;
+  CK(launch_pick(d_keys, d_vals, d_found, parts, n, last, d_keys_out, d_vals_out, d_found_out,
+                 S(stream), hooks(h)));
+  return LSM_OK;
+}
+
 lsm_status lsm_batch_size(const lsm_t* h, uint64_t* b_out) {
   if (!h || !b_out) return LSM_ERR_INVALID_ARG;
   *b_out = h->b;

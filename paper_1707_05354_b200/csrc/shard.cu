@@ -211,6 +211,32 @@ __global__ void range_scatter_kernel(const uint64_t* __restrict__ offs,
   }
 }
 
+// successor / predecessor across shards: the answer is the first shard (in
+// shard = key order) with an answer for a successor, the last one for a
+// predecessor (shards own ascending key intervals)
+__global__ void pick_kernel(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+                            const uint8_t* __restrict__ fin, uint32_t parts, uint64_t n, int last,
+                            uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
+                            uint8_t* __restrict__ fout) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t k = 0xFFFFFFFFu, v = 0xFFFFFFFFu;
+    uint8_t f = 0;
+    for (uint32_t p = 0; p < parts; ++p) {
+      const uint32_t s = last ? parts - 1 - p : p;
+      if (fin[(uint64_t)s * n + i]) {
+        k = kin[(uint64_t)s * n + i];
+        v = vin[(uint64_t)s * n + i];
+        f = 1;
+        break;
+      }
+    }
+    kout[i] = k;
+    vout[i] = v;
+    if (fout) fout[i] = f;
+  }
+}
+
 __global__ void sum_parts_kernel(const uint32_t* __restrict__ in, uint32_t parts, uint64_t n,
                                  uint32_t* __restrict__ out) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -291,6 +317,16 @@ cudaError_t launch_range_assemble(const uint64_t* offs, const uint64_t* blen, ui
   range_scatter_kernel<<<g, 256, 0, s>>>(offs, blen, P, nq, kin, vin, offsets, kout, vout,
                                          capacity);
   hk.end(hk.ctx, LSM_K_OTHER, (double)nq * (8.0 * P + 8.0), s, 1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pick(const uint32_t* kin, const uint32_t* vin, const uint8_t* fin,
+                        uint32_t parts, uint64_t n, int last, uint32_t* kout, uint32_t* vout,
+                        uint8_t* fout, cudaStream_t s, const LaunchHooks& hk) {
+  const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, 148 * 8));
+  hk.begin(hk.ctx, LSM_K_OTHER, s);
+  pick_kernel<<<g, 256, 0, s>>>(kin, vin, fin, parts, n, last, kout, vout, fout);
+  hk.end(hk.ctx, LSM_K_OTHER, (double)n * (9.0 * parts + 9.0), s, 1);
   return cudaGetLastError();
 }
 

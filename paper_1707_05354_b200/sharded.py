@@ -33,6 +33,11 @@ pairs (an all-to-all-v after an exchange of the block lengths) and
 lsm_shard_range_assemble concatenates each query's pieces in shard order --
 key order, since shards own ascending key intervals.
 
+Successor / predecessor: all-gather the queries, every shard answers all of
+them locally (its keys lie in its own interval, so no clipping), the answers
+go back to the origins and lsm_shard_pick keeps the first shard's answer
+(successor) or the last one's (predecessor).
+
 All data-path arithmetic runs in libgpulsm kernels; torch.distributed only
 moves bytes. The backend is pluggable so the routing logic can be tested on
 CPU with gloo (tests/test_sharded_gloo.py); the GPU backend is the product.
@@ -108,6 +113,12 @@ class GpuShardBackend:
 
     def range_assemble(self, offs, block_len, P, nq, keys, vals):
         return self.lsm.shard_range_assemble(offs, block_len, P, nq, keys, vals)
+
+    def order(self, q, succ):
+        return self.lsm.successor(q) if succ else self.lsm.predecessor(q)
+
+    def pick(self, k, v, f, P, n, last):
+        return self.lsm.shard_pick(k, v, f, P, n, last)
 
 
 class ShardedLSM:
@@ -203,6 +214,25 @@ class ShardedLSM:
         partial = self.backend.count(c1, c2)
         recv = self._a2a(partial, [nq] * self.P, [nq] * self.P, torch.int32)
         return self.backend.sum_parts(recv, self.P, nq)
+
+    def _order(self, q, succ):
+        nq = q.numel()
+        P = self.P
+        allq = self.backend.empty(nq * P, torch.int32)
+        dist.all_gather_into_tensor(allq, q, group=self.group)
+        k, v, f = self.backend.order(allq, succ)  # local answers: keys of this shard only
+        rk = self._a2a(k, [nq] * P, [nq] * P, torch.int32)
+        rv = self._a2a(v, [nq] * P, [nq] * P, torch.int32)
+        rf = self._a2a(f, [nq] * P, [nq] * P, torch.uint8)
+        return self.backend.pick(rk, rv, rf, P, nq, not succ)
+
+    def successor(self, q):
+        """Smallest live key >= q per query (R23): (keys, vals, found)."""
+        return self._order(q, True)
+
+    def predecessor(self, q):
+        """Largest live key <= q per query (R23): (keys, vals, found)."""
+        return self._order(q, False)
 
     def range(self, k1, k2):
         """Ranges for this rank's (k1, k2) queries: (offsets[nq+1], keys, vals)

@@ -134,6 +134,11 @@ def test_sharded_router_single_gpu_nccl():
         k1, k2 = synth.range_queries(7, 3000, 9 * b, 12, domain=50_002)
         c = sh.count(to_device(k1), to_device(k2))
         assert np.array_equal(to_numpy_u32(c), o.count(k1, k2))
+        for fn, ofn in ((sh.successor, o.successor), (sh.predecessor, o.predecessor)):
+            gk, gv, gf = fn(to_device(q))
+            ek, ev, ef = ofn(q)
+            assert np.array_equal(gf.cpu().numpy(), ef)
+            assert np.array_equal(to_numpy_u32(gk), ek) and np.array_equal(to_numpy_u32(gv), ev)
         ro, rk, rv = sh.range(to_device(k1), to_device(k2))
         ooff, ok, ov2 = o.range(k1, k2)
         assert np.array_equal(ro.cpu().numpy().astype(np.uint64), ooff)

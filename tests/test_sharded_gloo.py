@@ -93,6 +93,26 @@ class CpuTestBackend:
         return (torch.from_numpy(off.astype(np.int64)), torch.from_numpy(k.view(np.int32).copy()),
                 torch.from_numpy(v.view(np.int32).copy()))
 
+    def order(self, q, succ):
+        fn = self.store.successor if succ else self.store.predecessor
+        k, v, f = fn(q.numpy().view(np.uint32))
+        return (torch.from_numpy(k.view(np.int32).copy()), torch.from_numpy(v.view(np.int32).copy()),
+                torch.from_numpy(f.copy()))
+
+    def pick(self, k, v, f, P, n, last):
+        kk = k.numpy().reshape(P, n)
+        vv = v.numpy().reshape(P, n)
+        ff = f.numpy().reshape(P, n)
+        ko = np.full(n, -1, np.int32)
+        vo = np.full(n, -1, np.int32)
+        fo = np.zeros(n, np.uint8)
+        for s_ in (range(P - 1, -1, -1) if last else range(P)):
+            take = (ff[s_] == 1) & (fo == 0)
+            ko[take] = kk[s_][take]
+            vo[take] = vv[s_][take]
+            fo[take] = 1
+        return torch.from_numpy(ko), torch.from_numpy(vo), torch.from_numpy(fo)
+
     def range_assemble(self, offs, block_len, P, nq, keys, vals):
         # numpy stand-in of lsm_shard_range_assemble
         o = offs.numpy().reshape(P, nq)
@@ -157,9 +177,11 @@ def _worker(rank, world, port, scenario, out_q):
         c = sh.count(torch.from_numpy(k1.view(np.int32).copy()), torch.from_numpy(k2.view(np.int32).copy()))
         ro, rk, rv = sh.range(torch.from_numpy(k1.view(np.int32).copy()),
                               torch.from_numpy(k2.view(np.int32).copy()))
+        qt = torch.from_numpy(q.view(np.int32).copy())
+        order = [tuple(x.numpy() for x in fn(qt)) for fn in (sh.successor, sh.predecessor)]
         out_q.put((rank, q, qv.numpy().view(np.uint32), qf.numpy(), k1, k2,
                    c.numpy().view(np.uint32), sh.overflow_splits, sh.backend.batch_sizes,
-                   (ro.numpy(), rk.numpy().view(np.uint32), rv.numpy().view(np.uint32))))
+                   (ro.numpy(), rk.numpy().view(np.uint32), rv.numpy().view(np.uint32)), order))
     finally:
         dist.destroy_process_group()
 
@@ -197,7 +219,11 @@ def _global_oracle(scenario):
 def test_sharded_router_matches_global_oracle(scenario):
     res = _run(scenario)
     o = _global_oracle(scenario)
-    for (rank, q, qv, qf, k1, k2, c, splits, sizes, rng) in res:
+    for (rank, q, qv, qf, k1, k2, c, splits, sizes, rng, order) in res:
+        for (gk, gv, gf), fn in zip(order, (o.successor, o.predecessor)):
+            ok_, ov_, of_ = fn(q)
+            assert np.array_equal(gf, of_), rank
+            assert np.array_equal(gk.view(np.uint32), ok_) and np.array_equal(gv.view(np.uint32), ov_)
         ov, of = o.lookup(q)
         assert np.array_equal(qf, of), rank
         assert np.array_equal(qv[qf == 1], ov[of == 1]), rank
@@ -216,7 +242,7 @@ def test_sharded_router_oversize_split():
     r0 = res[0]
     assert r0[7] == 4  # one split per batch on shard 0
     assert max(r0[8]) <= 128
-    for (rank, q, qv, qf, k1, k2, c, splits, sizes, rng) in res:
+    for (rank, q, qv, qf, k1, k2, c, splits, sizes, rng, order) in res:
         ov, of = o.lookup(q)
         assert np.array_equal(qf, of) and np.array_equal(qv[qf == 1], ov[of == 1])
         assert np.array_equal(c, o.count(k1, k2))
