@@ -327,6 +327,10 @@ __device__ __forceinline__ uint32_t walk_slices(const LevelTable& T, uint64_t* p
     }
   }
   uint32_t cnt = 0;
+  // NEED_VAL: a found pair is emitted one step later, so its value load
+  // overlaps the next step of the walk instead of stalling the store
+  bool pend = false;
+  uint32_t pk = 0, pv = 0;
   while (true) {
     uint32_t m = kSent;
 #pragma unroll
@@ -358,10 +362,18 @@ __device__ __forceinline__ uint32_t walk_slices(const LevelTable& T, uint64_t* p
       }
     }
     if (valid) {
-      emit(cnt, m, val);
+      if (NEED_VAL) {
+        if (pend) emit(cnt - 1, pk, pv);
+        pend = true;
+        pk = m;
+        pv = val;
+      } else {
+        emit(cnt, m, val);
+      }
       ++cnt;
     }
   }
+  if (NEED_VAL && pend) emit(cnt - 1, pk, pv);
   return cnt;
 }
 
@@ -382,7 +394,9 @@ __device__ __forceinline__ uint32_t walk_one(const uint32_t* __restrict__ K,
     const uint4 a = __ldg(reinterpret_cast<const uint4*>(K + g));  // +16 words of slack
     const uint4 b = __ldg(reinterpret_cast<const uint4*>(K + g + 4));
     const uint32_t kk[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    // validity of the 8 records first, then all value loads at once
     bool stop = false;
+    uint32_t valid = 0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const uint64_t p = g + i;
@@ -391,13 +405,24 @@ __device__ __forceinline__ uint32_t walk_one(const uint32_t* __restrict__ K,
         if (p >= n || k > z) {
           stop = true;
         } else {
-          if (k != prev && (kk[i] & 1u)) {
-            emit(cnt, k, NEED_VAL ? __ldg(V + p) : 0u);
-            ++cnt;
-          }
+          if (k != prev && (kk[i] & 1u)) valid |= 1u << i;
           prev = k;
         }
       }
+    }
+    if (NEED_VAL) {
+      uint32_t vv[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) vv[i] = (valid >> i) & 1u ? __ldg(V + g + i) : 0u;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if ((valid >> i) & 1u) {
+          emit(cnt, kk[i] >> 1, vv[i]);
+          ++cnt;
+        }
+      }
+    } else {
+      cnt += __popc(valid);
     }
     if (stop) break;
     g += 8;
