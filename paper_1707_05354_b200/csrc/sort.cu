@@ -532,14 +532,76 @@ __device__ __forceinline__ void local_subpass(const uint32_t* sk, const uint32_t
   __syncthreads();
 }
 
+// Shared-memory-to-shared-memory digit pass on interleaved (key, value)
+// records: one 8-byte load and one 8-byte store per record, and the digit
+// bases are folded into the per-warp counters during the digit scan, so the
+// scatter reads one counter per record (about a quarter fewer shared-memory
+// wavefronts than local_subpass on split arrays).
+template <int T, int ITEMS>
+__device__ __forceinline__ void local_subpass_kv(const uint2* src, uint32_t n, uint2* dst,
+                                                 int shift, LocalScratch<T>& L) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < (T / 32) * kRadix; i += T) (&L.whist[0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t wbase = warp * (32 * ITEMS);
+  uint2 kv[ITEMS];
+  uint32_t rk[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const uint32_t p = wbase + i * 32 + lane;
+    kv[i] = p < n ? src[p] : make_uint2(0u, 0u);
+  }
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const bool valid = wbase + i * 32 + lane < n;
+    const uint32_t d = (kv[i].x >> shift) & (kRadix - 1);
+    const uint32_t peers = digit_peers(d, valid);
+    const int leader = __ffs(peers) - 1;
+    uint32_t old = 0;
+    if (valid && lane == leader) {
+      old = L.whist[warp][d];
+      L.whist[warp][d] = old + __popc(peers);
+    }
+    old = __shfl_sync(kFull, old, leader < 0 ? 0 : leader);
+    rk[i] = old + __popc(peers & lt);
+    __syncwarp();
+  }
+  __syncthreads();
+  uint32_t c = 0;
+  if (tid < kRadix) {
+#pragma unroll 8
+    for (int w = 0; w < T / 32; ++w) c += L.whist[w][tid];
+  }
+  uint32_t tot;
+  const uint32_t base = block_exclusive_scan<T, uint32_t>(c, L.scan, &tot);
+  if (tid < kRadix) {
+    uint32_t run = base;
+#pragma unroll 8
+    for (int w = 0; w < T / 32; ++w) {
+      const uint32_t x = L.whist[w][tid];
+      L.whist[w][tid] = run;
+      run += x;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    if (wbase + i * 32 + lane < n) {
+      const uint32_t d = (kv[i].x >> shift) & (kRadix - 1);
+      dst[L.whist[warp][d] + rk[i]] = kv[i];
+    }
+  }
+  __syncthreads();
+}
+
 // single-CTA sort of a whole small batch (b <= kSmallCap), all 4 digits
 constexpr int kSmallThreads = 1024;
 constexpr int kSmallItems = 7;
 constexpr int kSmallCap = kSmallThreads * kSmallItems;  // 7168
 
 struct SmallSmem {
-  uint32_t k[2][kSmallCap];
-  uint32_t v[2][kSmallCap];
+  uint2 kv[2][kSmallCap];  // interleaved (key, value)
   LocalScratch<kSmallThreads> L;
 };
 
@@ -569,22 +631,24 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_sort_kernel(
       op = in.mode == kModeMixed ? (uint32_t)__ldg(in.ops + p) : 0u;
     }
     bool bad;
-    encode_loaded(in, p, k, v, op, S.k[0][p], S.v[0][p], bad);
+    uint32_t ek, evv;
+    encode_loaded(in, p, k, v, op, ek, evv, bad);
+    S.kv[0][p] = make_uint2(ek, evv);
     any_bad |= bad;
   }
   if (any_bad) atomicOr(err, 1u);
   __syncthreads();
   int cur = 0;
   for (int pass = 0; pass < kPasses; ++pass) {
-    local_subpass<kSmallThreads, kSmallItems>(S.k[cur], S.v[cur], b, S.k[cur ^ 1], S.v[cur ^ 1],
-                                              pass * kRadixBits, S.L, nullptr);
+    local_subpass_kv<kSmallThreads, kSmallItems>(S.kv[cur], b, S.kv[cur ^ 1], pass * kRadixBits,
+                                                 S.L);
     cur ^= 1;
   }
   for (uint32_t p = threadIdx.x; p < b; p += kSmallThreads) {
-    const uint32_t key = S.k[cur][p];
-    out_keys[p] = key;
-    out_vals[p] = S.v[cur][p];
-    if (out_f1 != nullptr && (p & (kF1Step - 1)) == 0) out_f1[p / kF1Step] = key;
+    const uint2 r = S.kv[cur][p];
+    out_keys[p] = r.x;
+    out_vals[p] = r.y;
+    if (out_f1 != nullptr && (p & (kF1Step - 1)) == 0) out_f1[p / kF1Step] = r.x;
   }
 }
 
@@ -595,8 +659,7 @@ constexpr int kBktItems = 11;
 constexpr int kBktCap = kBktThreads * kBktItems;  // 5632
 
 struct BktSmem {
-  uint32_t k[2][kBktCap];
-  uint32_t v[2][kBktCap];
+  uint2 kv[2][kBktCap];  // interleaved (key, value)
   LocalScratch<kBktThreads> L;
   uint32_t run[kRadix];
   uint32_t hist[kRadix];
@@ -626,31 +689,23 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_sort_kernel(
   const uint32_t start = bkt[d], size = bkt[kRadix + d];
   if (size == 0) return;
   if (size <= (uint32_t)kBktCap) {
-    for (uint32_t p = tid; p < size; p += kBktThreads) {
-      S.k[0][p] = __ldg(ak + start + p);
-      S.v[0][p] = __ldg(av + start + p);
-    }
+    for (uint32_t p = tid; p < size; p += kBktThreads)
+      S.kv[0][p] = make_uint2(__ldg(ak + start + p), __ldg(av + start + p));
     __syncthreads();
     BPROBE(1);
     int cur = 0;
     for (int pass = 0; pass < kPasses - 1; ++pass) {
-#ifdef GPULSM_PROBE_DUP0
-      if (pass == 0) {
-        local_subpass<kBktThreads, kBktItems>(S.k[cur], S.v[cur], size, S.k[cur ^ 1],
-                                              S.v[cur ^ 1], 0, S.L, nullptr, 3);
-      }
-#endif
-      local_subpass<kBktThreads, kBktItems>(S.k[cur], S.v[cur], size, S.k[cur ^ 1],
-                                            S.v[cur ^ 1], pass * kRadixBits, S.L, nullptr, pass);
+      local_subpass_kv<kBktThreads, kBktItems>(S.kv[cur], size, S.kv[cur ^ 1], pass * kRadixBits,
+                                               S.L);
       cur ^= 1;
       BPROBE(2 + pass);
     }
     for (uint32_t p = tid; p < size; p += kBktThreads) {
-      const uint32_t key = S.k[cur][p];
+      const uint2 r = S.kv[cur][p];
       const uint32_t g = start + p;
-      out_keys[g] = key;
-      out_vals[g] = S.v[cur][p];
-      if (out_f1 != nullptr && (g & (kF1Step - 1)) == 0) out_f1[g / kF1Step] = key;
+      out_keys[g] = r.x;
+      out_vals[g] = r.y;
+      if (out_f1 != nullptr && (g & (kF1Step - 1)) == 0) out_f1[g / kF1Step] = r.x;
     }
     __syncthreads();
     BPROBE(5);
@@ -660,6 +715,8 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_sort_kernel(
   // CTA through global memory; the host switches to the 4-pass path for
   // later batches when it sees the flag.
   if (tid == 0) atomicOr(overflow, 1u);
+  uint32_t* fk = reinterpret_cast<uint32_t*>(S.kv[0]);  // 2 * kBktCap words
+  uint32_t* fv = fk + kBktCap;
   const uint32_t* srck = ak + start;
   const uint32_t* srcv = av + start;
   for (int pass = 0; pass < kPasses - 1; ++pass) {
@@ -679,15 +736,15 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_sort_kernel(
     for (uint32_t c0 = 0; c0 < size; c0 += kBktCap) {
       const uint32_t nc = min((uint32_t)kBktCap, size - c0);
       // rank the chunk locally (stable), place it at the running offsets
-      local_subpass<kBktThreads, kBktItems>(srck + c0, srcv + c0, nc, S.k[0], S.v[0], shift, S.L,
+      local_subpass<kBktThreads, kBktItems>(srck + c0, srcv + c0, nc, fk, fv, shift, S.L,
                                             nullptr);
-      // S.k[0] holds the chunk grouped by digit; L.tstart / L.cnt describe it
+      // fk holds the chunk grouped by digit; L.tstart / L.cnt describe it
       for (uint32_t p = tid; p < nc; p += kBktThreads) {
-        const uint32_t key = S.k[0][p];
+        const uint32_t key = fk[p];
         const uint32_t dg = (key >> shift) & (kRadix - 1);
         const uint32_t g = S.run[dg] + (p - S.L.tstart[dg]);
         dk[g] = key;
-        dv[g] = S.v[0][p];
+        dv[g] = fv[p];
       }
       __syncthreads();
       if (tid < kRadix) S.run[tid] += S.L.cnt[tid];

@@ -9,12 +9,19 @@ timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/b
 timeout 1500 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_list.log 2>&1
 P="python scripts/prof_step.py"
 NCU="timeout 600 ncu --set full --clock-control none --import-source on"
-$NCU -k regex:count_kernel -s 0 -c 1 -o gpurun_out/prof_count $P > /dev/null 2>&1
-$NCU -k regex:range_kernel -s 0 -c 1 -o gpurun_out/prof_range $P > /dev/null 2>&1
+$NCU -k regex:^count_kernel -s 0 -c 1 -o gpurun_out/prof_count $P > /dev/null 2>&1
+$NCU -k regex:"^count_kernel|^range_write" -s 1 -c 2 -o gpurun_out/prof_range $P > /dev/null 2>&1
 $NCU -k regex:lookup_kernel -s 0 -c 1 -o gpurun_out/prof_lookup $P > /dev/null 2>&1
 $NCU -k regex:merge_kernel -s 62 -c 1 -o gpurun_out/prof_merge $P --no-cleanup --nq 1024 > /dev/null 2>&1
 $NCU -k regex:merge_kernel -s 0 -c 1 -o gpurun_out/prof_merge0 $P --batches 4 --no-cleanup --nq 1024 > /dev/null 2>&1
-$NCU -k regex:onesweep -s 60 -c 1 -o gpurun_out/prof_sort $P --no-cleanup --nq 1024 > /dev/null 2>&1
+$NCU --replay-mode application -k regex:onesweep -s 60 -c 1 -o gpurun_out/prof_sort $P --no-cleanup --nq 1024 > /dev/null 2>&1
 $NCU -k regex:bucket_sort -s 60 -c 1 -o gpurun_out/prof_bucket $P --no-cleanup --nq 1024 > /dev/null 2>&1
 $NCU -k regex:cleanup_write -s 0 -c 1 -o gpurun_out/prof_cleanup $P --nq 1024 > /dev/null 2>&1
-ls -la gpurun_out
+# summarise on the box (the reports are too big to bring back): profiles
+# summaries under gpurun_out/prof_summary, reports deleted except small ones
+python scripts/ncu_summary.py --launches gpurun_out/launches.csv --reps 'gpurun_out/prof_*.ncu-rep' \
+    --round r01 --outdir gpurun_out/prof_summary > gpurun_out/ncu_summary.log 2>&1
+mkdir -p gpurun_out/keep
+for f in prof_range prof_bucket prof_merge; do mv gpurun_out/$f.ncu-rep gpurun_out/keep/ 2>/dev/null; done
+rm -f gpurun_out/*.ncu-rep
+du -sh gpurun_out/* | sort -h | tail -20

@@ -22,7 +22,8 @@ TMUL = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "ns": 1e-3, "us": 1.0, 
 
 CLASS = [("onesweep", "sort_pass"), ("bucket_sort", "sort_pass"), ("small_sort", "sort_pass"),
          ("sort_hist", "sort_hist"), ("merge_kernel", "merge"),
-         ("lookup_kernel", "lookup"), ("count_kernel", "count"), ("range_kernel", "range"),
+         ("lookup_kernel", "lookup"), ("count_kernel<1, 1>", "range"), ("count_kernel<3, 1>", "range"),
+         ("count_kernel", "count"), ("range_write", "range"), ("range_kernel", "range"),
          ("build_f1", "other"), ("finalize_index", "other"),
          ("scan_", "scan"), ("cleanup_", "cleanup"), ("fill_placebo", "cleanup"),
          ("bucket_", "other"), ("scatter_back", "other"), ("clip_kernel", "other"),
@@ -104,8 +105,9 @@ def main():
     ap.add_argument("--reps", nargs="*", default=[])
     ap.add_argument("--round", default="r01")
     ap.add_argument("--units", default="{}", help="json: class -> units per captured launch")
+    ap.add_argument("--outdir", default=os.path.join(ROOT, "profiles"))
     a = ap.parse_args()
-    prof = os.path.join(ROOT, "profiles")
+    prof = a.outdir
     os.makedirs(prof, exist_ok=True)
     if a.launches:
         agg = launches(a.launches)
@@ -133,15 +135,21 @@ def main():
         open(os.path.join(prof, f"{a.round}_ncu_full_summary.txt"), "w").write("\n".join(lines) + "\n")
         json.dump(allres, open(os.path.join(prof, f"{a.round}_ncu_full.json"), "w"), indent=1)
         print("\n".join(lines))
-        # traffic per class: bytes per launch of the LARGEST captured launch
+        # traffic per class: DRAM bytes per launch averaged over the captured
+        # launches of the class's largest-traffic report (range = count pass +
+        # write pass, both captured from one range call)
         units = json.loads(a.units)
-        traffic = {}
+        by = collections.defaultdict(list)
         for x in allres:
-            c = x["class"]
-            b = x["dram_read_bytes"] + x["dram_write_bytes"]
+            by[(x["class"], x["rep"])].append(x)
+        traffic = {}
+        for (c, rep), xs in by.items():
+            b = sum(x["dram_read_bytes"] + x["dram_write_bytes"] for x in xs) / len(xs)
             if c not in traffic or b > traffic[c]["dram_bytes_per_launch"]:
-                traffic[c] = {"dram_bytes_per_launch": b, "time_us": x["time_us"], "kernel": x["kernel"],
-                              "rep": x["rep"], "units_per_launch": units.get(c)}
+                traffic[c] = {"dram_bytes_per_launch": b, "launches_captured": len(xs),
+                              "time_us": sum(x["time_us"] for x in xs) / len(xs),
+                              "kernel": "+".join(sorted({x["kernel"] for x in xs})),
+                              "rep": rep, "units_per_launch": units.get(c)}
         json.dump(traffic, open(os.path.join(prof, "ncu_traffic.json"), "w"), indent=1)
 
 
