@@ -566,3 +566,72 @@ def test_gpu_sa_bulk_and_multi_batch():
     q = synth.lookup_queries(seed, 2000, 1400, alphabet=300)
     k1, kk2 = synth.range_queries(seed, 300, 1400, 8, domain=300)
     assert_queries_equal(gpu, o1, q, k1, kk2, "sa multi")
+
+
+@pytest.mark.slow
+def test_config_c2_full():
+    # BASELINE configs[1] (C2): b = 2^16, insert-only, R = 64 batches from
+    # empty; lookups, counts and ranges at L = 8 at r in {1, 3, 7, 15, 31, 63,
+    # 64} (the occupancy patterns of Table II-IV), exact vs O1 on samples of
+    # the paper's nq = n protocol.
+    b = 1 << 16
+    seed = synth.SEED_BASE + 1
+    g = GpuAdapter(b)
+    o1 = oracle.OracleDict(b)
+    check_at = {1, 3, 7, 15, 31, 63, 64}
+    for j in range(64):
+        k, v, d = synth.updates(seed, j * b, b, delete_frac4=0)
+        g.update(k, v, d)
+        o1.apply_batch(k, v, d)
+        r = j + 1
+        if r in check_at:
+            n = r * b
+            q = synth.lookup_queries(seed, 50_000, n)
+            k1, k2 = synth.range_queries(seed, 20_000, n, 8)
+            assert_queries_equal(g, o1, q, k1, k2, f"C2 r={r}")
+
+
+@pytest.mark.slow
+def test_config_c4_shape_sampled():
+    # BASELINE configs[3] (C4) shape: b = 2^20, insert-only, r = 127 (seven
+    # occupied levels, n = 127 * 2^20), queries at L in {8, 64, 1024}. O1 is
+    # fed the updates of one key sub-range (exact: keys never interact); the
+    # answers it can vouch for are compared.
+    b = 1 << 20
+    R = 127
+    seed = synth.SEED_BASE + 3
+    lo_key, hi_key = 3 << 25, (3 << 25) + (1 << 25)  # 1/64 of the domain
+    g = pkg.GpuLSM(b, reserve_batches=R)
+    o1 = oracle.OracleDict(b)
+    for j in range(R):
+        k, v, d = synth.updates(seed, j * b, b, delete_frac4=0)
+        g.update(to_device(k), to_device(v), to_device(d))
+        sel = (k >= lo_key) & (k < hi_key)
+        o1.apply_batch(k[sel], v[sel], d[sel])
+    g.sync()
+    assert g.r == R
+    n = R * b
+    rng = np.random.default_rng(11)
+    for L in (8, 64, 1024):
+        w = max(1, round(L * synth.D / n))
+        k1 = rng.integers(lo_key, hi_key - w, 4000).astype(np.uint32)
+        k2 = (k1 + w - 1).astype(np.uint32)
+        gc = to_numpy_u32(g.count(to_device(k1), to_device(k2)))
+        assert np.array_equal(gc, o1.count(k1, k2)), L
+        assert abs(gc.mean() - L) < 0.2 * L + 2, (L, gc.mean())  # R15: E[count] = L
+        off, ks, vs = g.range(to_device(k1), to_device(k2))
+        ooff, oks, ovs = o1.range(k1, k2)
+        assert np.array_equal(off.cpu().numpy().astype(np.uint64), ooff), L
+        assert np.array_equal(to_numpy_u32(ks), oks) and np.array_equal(to_numpy_u32(vs), ovs), L
+    q = np.concatenate([o1.items()[0][::7][:20000],
+                        rng.integers(lo_key, hi_key, 20000).astype(np.uint32)])
+    gv, gf = g.lookup(to_device(q))
+    ov, of = o1.lookup(q)
+    assert np.array_equal(gf.cpu().numpy(), of) and np.array_equal(to_numpy_u32(gv), ov)
+    for name in ("successor", "predecessor"):
+        gk, gvv, gff = getattr(g, name)(to_device(q))
+        ok, ovv, off_ = getattr(o1, name)(q)
+        sure = off_ == 1  # an answer inside the sub-range is the global answer
+        assert np.array_equal(to_numpy_u32(gk)[sure], ok[sure]), name
+        assert np.array_equal(to_numpy_u32(gvv)[sure], ovv[sure]), name
+        assert np.all(gff.cpu().numpy()[sure] == 1), name
