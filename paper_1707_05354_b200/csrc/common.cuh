@@ -290,14 +290,16 @@ cudaError_t launch_range(const LevelTable& T, const uint32_t* k1, const uint32_t
                          uint64_t capacity, unsigned long long* scratch, cudaStream_t s,
                          const LaunchHooks& hk);
 
-// Three-pass range (count + save positions, scan, write walk) when every
-// level has < 2^32 records and at most 8 levels are occupied.
-bool range3_ok(const LevelTable& T);
-uint64_t range3_scratch_bytes(const LevelTable& T, uint64_t nq);
-cudaError_t launch_range3(const LevelTable& T, const uint32_t* k1, const uint32_t* k2,
-                          uint64_t nq, uint64_t* offsets, uint32_t* keys_out, uint32_t* vals_out,
-                          uint64_t capacity, void* scratch, cudaStream_t s,
-                          const LaunchHooks& hk);
+// Single-pass range over CTA blocks of 1024 queries (<= 8 levels, levels
+// < 2^32 records): scratch range_block_scratch_words(nq) u64 (zeroed here).
+uint64_t range_block_scratch_words(uint64_t nq);
+cudaError_t launch_range_block(const LevelTable& T, const uint32_t* k1, const uint32_t* k2,
+                               uint64_t nq, uint64_t* offsets, uint32_t* keys_out,
+                               uint32_t* vals_out, uint64_t capacity,
+                               unsigned long long* scratch, cudaStream_t s,
+                               const LaunchHooks& hk);
+// whether the block range kernel applies (<= 8 levels, each < 2^32 records)
+bool range_block_ok(const LevelTable& T);
 
 // Cleanup: valid = regular && first of its key run in M; compact into C.
 // tile_counts: cleanup_tiles(n) u32; offsets: cleanup_tiles(n)+1 u64.

@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -828,13 +829,13 @@ lsm_status lsm_range(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2, uint6
   if (capacity > 0 && (!d_keys_out || !d_vals_out)) return LSM_ERR_INVALID_ARG;
   CK(ensure_index(h, s, hk));
   LevelTable T = level_table(h);
-  if (range3_ok(T)) {
-    // count + saved start positions, scan of the counts, write walk
-    CK(ensure_qbuf(h, range3_scratch_bytes(T, nq), s));
-    CK(launch_range3(T, d_k1, d_k2, nq, d_offsets_out, d_keys_out, d_vals_out, capacity, h->qbuf,
-                     s, hk));
+  if (range_block_ok(T)) {
+    // one pass over CTA blocks: count, look-back per block, write
+    CK(ensure_qbuf(h, range_block_scratch_words(nq) * 8, s));
+    CK(launch_range_block(T, d_k1, d_k2, nq, d_offsets_out, d_keys_out, d_vals_out, capacity,
+                          static_cast<unsigned long long*>(h->qbuf), s, hk));
   } else {
-    // one pass: bounds, count, warp scan + look-back offsets, pairs
+    // > 8 levels: one pass with a per-warp look-back
     CK(ensure_qbuf(h, range_scratch_words(nq) * 8, s));
     CK(launch_range(T, d_k1, d_k2, nq, d_offsets_out, d_keys_out, d_vals_out, capacity,
                     static_cast<unsigned long long*>(h->qbuf), s, hk));

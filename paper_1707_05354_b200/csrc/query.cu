@@ -446,12 +446,11 @@ __device__ __forceinline__ void bounds(const LevelTable& T, const uint32_t* sF3,
   }
 }
 
-// Count (A5). SAVE (range's first pass): also store every level's start
-// position pos_out[j * nq + i] (u32) for the write pass.
-template <int NL, bool SAVE>
+// Count (A5).
+template <int NL>
 __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) count_kernel(
     LevelTable T, const uint32_t* __restrict__ k1, const uint32_t* __restrict__ k2, uint64_t nq,
-    uint32_t* __restrict__ counts, uint32_t* __restrict__ pos_out) {
+    uint32_t* __restrict__ counts) {
   extern __shared__ uint32_t sF3[];
   stage_f3(T, sF3);
   constexpr int CAP = NL > 0 ? NL : LSM_MAX_LEVELS;
@@ -465,11 +464,6 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) count_kernel(
     const uint32_t a = act ? __ldg(k1 + i) : 1u, z = act ? __ldg(k2 + i) : 0u;
     uint64_t pos[CAP];
     bounds<NL>(T, sF3, a, a > z, pos, L);
-    if (SAVE && act) {
-#pragma unroll
-      for (int j = 0; j < CAP; ++j)
-        if (j < L) pos_out[(uint64_t)j * nq + i] = (uint32_t)pos[j];
-    }
     uint32_t c;
     if (NL == 1 && (reinterpret_cast<uintptr_t>(T.keys[0]) & 15) == 0)
       c = walk_one<false>(T.keys[0], T.vals[0], T.n[0], pos[0], z,
@@ -477,38 +471,6 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) count_kernel(
     else
       c = walk_slices<NL, false>(T, pos, z, L, [](uint32_t, uint32_t, uint32_t) {});
     if (act) counts[i] = c;
-  }
-}
-
-// Range (A6) write pass: from the saved start positions and the scanned
-// offsets, walk again and emit the valid pairs in key order.
-template <int NL>
-__global__ void __launch_bounds__(kQThreads, kQCtasPerSm) range_write_kernel(
-    LevelTable T, const uint32_t* __restrict__ k2, uint64_t nq,
-    const uint32_t* __restrict__ pos_in, const uint64_t* __restrict__ offsets,
-    uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint64_t capacity) {
-  constexpr int CAP = NL > 0 ? NL : LSM_MAX_LEVELS;
-  const int L = NL > 0 ? NL : T.count;
-  const uint64_t stride = (uint64_t)gridDim.x * kQThreads;
-  for (uint64_t i = (uint64_t)blockIdx.x * kQThreads + threadIdx.x; i < nq; i += stride) {
-    const uint32_t z = __ldg(k2 + i);
-    const uint64_t base = __ldg(offsets + i);
-    if (__ldg(offsets + i + 1) == base) continue;  // nothing valid
-    uint64_t pos[CAP];
-#pragma unroll
-    for (int j = 0; j < CAP; ++j)
-      if (j < L) pos[j] = __ldg(pos_in + (uint64_t)j * nq + i);
-    auto put = [&](uint32_t k, uint32_t key, uint32_t val) {
-      const uint64_t o = base + k;
-      if (o < capacity) {
-        keys_out[o] = key;
-        vals_out[o] = val;
-      }
-    };
-    if (NL == 1 && (reinterpret_cast<uintptr_t>(T.keys[0]) & 15) == 0)
-      walk_one<true>(T.keys[0], T.vals[0], T.n[0], pos[0], z, put);
-    else
-      walk_slices<NL, true>(T, pos, z, L, put);
   }
 }
 
@@ -725,6 +687,115 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) order_kernel(
   }
 }
 
+// ---- single-pass range over CTA blocks ----
+// A persistent CTA takes blocks of kRBQueries consecutive queries in
+// increasing order (atomic counter). Phase 1 counts every query of the block
+// (warp-cooperative bounds + counting walk) and keeps the start positions
+// and counts in shared memory; one warp then finds the block's global base by
+// a decoupled look-back over earlier blocks (every earlier block is held by a
+// running CTA, so the wait is short and cannot deadlock); phase 2 walks again
+// from the saved positions while the key sectors are still L2-resident and
+// writes the pairs. One look-back per 1024 queries, no position array in
+// global memory, keys read from DRAM once.
+constexpr int kRBTasks = 2;                       // 32-query tasks per warp per block
+constexpr int kRBQueries = kQThreads * kRBTasks;  // 1024
+
+template <int NL>
+__global__ void __launch_bounds__(kQThreads, kQCtasPerSm) range_block_kernel(
+    LevelTable T, const uint32_t* __restrict__ k1, const uint32_t* __restrict__ k2, uint64_t nq,
+    uint64_t* __restrict__ offsets, uint32_t* __restrict__ keys_out,
+    uint32_t* __restrict__ vals_out, uint64_t capacity, unsigned long long* __restrict__ ctr,
+    unsigned long long* __restrict__ status) {
+  extern __shared__ uint32_t smem_q[];
+  static_assert(NL > 0, "range_block_kernel needs a fixed level count");
+  uint32_t* sF3 = smem_q;
+  uint32_t* sPos = smem_q + ((T.f3_smem_total + 3) & ~3u);  // [NL][kRBQueries]
+  uint32_t* sOff = sPos + NL * kRBQueries;                   // counts, then exclusive offsets
+  __shared__ uint32_t sScan[kQThreads / 32 + 1];
+  __shared__ unsigned long long sBlk, sBase;
+  stage_f3(T, sF3);
+  const uint32_t tid = threadIdx.x, lane = lane_id();
+  const uint64_t nblocks = (nq + kRBQueries - 1) / kRBQueries;
+  while (true) {
+    if (tid == 0) sBlk = atomicAdd(ctr, 1ull);
+    __syncthreads();
+    const uint64_t blk = sBlk;
+    if (blk >= nblocks) break;
+    const uint64_t q0 = blk * kRBQueries;
+    // ---- phase 1: bounds and counting walk, state kept in shared memory ----
+#pragma unroll 1
+    for (int u = 0; u < kRBTasks; ++u) {
+      const uint32_t li = u * kQThreads + tid;
+      const uint64_t i = q0 + li;
+      const bool act = i < nq;
+      const uint32_t a = act ? __ldg(k1 + i) : 1u, z = act ? __ldg(k2 + i) : 0u;
+      uint64_t pos[NL];
+      bounds<NL>(T, sF3, a, a > z, pos, NL);
+#pragma unroll
+      for (int j = 0; j < NL; ++j) sPos[j * kRBQueries + li] = (uint32_t)pos[j];
+      uint32_t c;
+      if (NL == 1 && (reinterpret_cast<uintptr_t>(T.keys[0]) & 15) == 0)
+        c = walk_one<false>(T.keys[0], T.vals[0], T.n[0], pos[0], z,
+                            [](uint32_t, uint32_t, uint32_t) {});
+      else
+        c = walk_slices<NL, false>(T, pos, z, NL, [](uint32_t, uint32_t, uint32_t) {});
+      sOff[li] = act ? c : 0u;
+    }
+    __syncthreads();
+    // ---- block-exclusive offsets (query order li = u * kQThreads + tid) ----
+    uint32_t run = 0;
+#pragma unroll 1
+    for (int u = 0; u < kRBTasks; ++u) {
+      const uint32_t li = u * kQThreads + tid;
+      const uint32_t c = sOff[li];
+      uint32_t tot;
+      const uint32_t ex = block_exclusive_scan<kQThreads, uint32_t>(c, sScan, &tot);
+      sOff[li] = run + ex;
+      run += tot;
+    }
+    // ---- global base of the block: decoupled look-back (warp 0) ----
+    if (tid < 32) {
+      const uint64_t excl = task_lookback(status, blk, run);
+      if (lane == 0) sBase = excl;
+    }
+    __syncthreads();
+    const uint64_t base = sBase;
+#pragma unroll 1
+    for (int u = 0; u < kRBTasks; ++u) {
+      const uint32_t li = u * kQThreads + tid;
+      const uint64_t i = q0 + li;
+      if (i < nq) offsets[i] = base + sOff[li];
+    }
+    if (blk == nblocks - 1 && tid == 0) offsets[nq] = base + run;
+    // ---- phase 2: walk again from the saved positions and write ----
+#pragma unroll 1
+    for (int u = 0; u < kRBTasks; ++u) {
+      const uint32_t li = u * kQThreads + tid;
+      const uint64_t i = q0 + li;
+      if (i >= nq) continue;
+      const uint32_t z = __ldg(k2 + i);
+      const uint32_t nxt = (li + 1 < kRBQueries) ? sOff[li + 1] : run;
+      const uint64_t ob = base + sOff[li];
+      if (nxt == sOff[li] && li + 1 < kRBQueries) continue;  // nothing valid
+      uint64_t pos[NL];
+#pragma unroll
+      for (int j = 0; j < NL; ++j) pos[j] = sPos[j * kRBQueries + li];
+      auto put = [&](uint32_t k, uint32_t key, uint32_t val) {
+        const uint64_t o = ob + k;
+        if (o < capacity) {
+          keys_out[o] = key;
+          vals_out[o] = val;
+        }
+      };
+      if (NL == 1 && (reinterpret_cast<uintptr_t>(T.keys[0]) & 15) == 0)
+        walk_one<true>(T.keys[0], T.vals[0], T.n[0], pos[0], z, put);
+      else
+        walk_slices<NL, true>(T, pos, z, NL, put);
+    }
+    __syncthreads();  // shared state is reused by the next block
+  }
+}
+
 int g_sms = 0;
 
 unsigned query_grid(uint64_t nq) {
@@ -795,19 +866,17 @@ cudaError_t launch_lookup(const LevelTable& T, const uint32_t* q, uint64_t nq,
   return cudaGetLastError();
 }
 
-template <bool SAVE>
 cudaError_t count_dispatch(const LevelTable& T, const uint32_t* k1, const uint32_t* k2,
-                           uint64_t nq, uint32_t* counts_out, uint32_t* pos_out,
-                           cudaStream_t s) {
+                           uint64_t nq, uint32_t* counts_out, cudaStream_t s) {
   const size_t smem = T.f3_smem_total * 4;
   const int nl = T.count <= kMaxUnrolled ? T.count : 0;
   return dispatch_nl<kMaxUnrolled>(nl, [&](auto c) -> cudaError_t {
     constexpr int N = decltype(c)::value;
-    auto kern = count_kernel<N, SAVE>;
+    auto kern = count_kernel<N>;
     cudaError_t err = set_smem(kern);
     if (err != cudaSuccess) return err;
     const unsigned g = std::min(query_grid(nq), occ_grid(kern, smem));
-    kern<<<g, kQThreads, smem, s>>>(T, k1, k2, nq, counts_out, pos_out);
+    kern<<<g, kQThreads, smem, s>>>(T, k1, k2, nq, counts_out);
     return cudaGetLastError();
   });
 }
@@ -821,7 +890,7 @@ cudaError_t launch_count(const LevelTable& T, const uint32_t* k1, const uint32_t
   if (T.count == 0) {
     e = cudaMemsetAsync(counts_out, 0, nq * 4, s);
   } else {
-    e = count_dispatch<false>(T, k1, k2, nq, counts_out, nullptr, s);
+    e = count_dispatch(T, k1, k2, nq, counts_out, s);
   }
   // 8 B in, 4 B out, one 32 B key sector per level (the search's last step;
   // the L = 8 candidates share it)
@@ -889,50 +958,51 @@ cudaError_t launch_range(const LevelTable& T, const uint32_t* k1, const uint32_t
   return e;
 }
 
-bool range3_ok(const LevelTable& T) {
+size_t rb_smem(const LevelTable& T) {
+  return (((size_t)T.f3_smem_total + 3) & ~(size_t)3) * 4 + (size_t)T.count * kRBQueries * 4 +
+         (size_t)kRBQueries * 4;
+}
+
+uint64_t range_block_scratch_words(uint64_t nq) { return 1 + (nq + kRBQueries - 1) / kRBQueries; }
+
+cudaError_t launch_range_block(const LevelTable& T, const uint32_t* k1, const uint32_t* k2,
+                               uint64_t nq, uint64_t* offsets, uint32_t* keys_out,
+                               uint32_t* vals_out, uint64_t capacity,
+                               unsigned long long* scratch, cudaStream_t s,
+                               const LaunchHooks& hk) {
+  if (nq == 0) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(scratch, 0, range_block_scratch_words(nq) * 8, s);
+  if (e != cudaSuccess) return e;
+  hk.begin(hk.ctx, LSM_K_RANGE, s);
+  const size_t smem = rb_smem(T);
+  e = dispatch_nl<kMaxUnrolled>(T.count, [&](auto c) -> cudaError_t {
+    constexpr int N = decltype(c)::value;
+    if constexpr (N == 0) {
+      return cudaErrorInvalidValue;  // callers check range3_ok (<= 8 levels)
+    } else {
+      auto kern = range_block_kernel<N>;
+      cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)(kF3SmemMax * 4 + 8 * kRBQueries * 4 +
+                                                   kRBQueries * 4 + 64));
+      if (err != cudaSuccess) return err;
+      const unsigned g = std::min<unsigned>(
+          occ_grid(kern, smem), (unsigned)((nq + kRBQueries - 1) / kRBQueries));
+      kern<<<g, kQThreads, smem, s>>>(T, k1, k2, nq, offsets, keys_out, vals_out, capacity,
+                                      scratch, scratch + 1);
+      return cudaGetLastError();
+    }
+  });
+  // 8 B in, 8 B offset out, per level one 32 B key sector and one 32 B value
+  // sector; the pairs' 8 B each are added once the total is known
+  hk.end(hk.ctx, LSM_K_RANGE, (double)nq * (16.0 + 64.0 * T.count), s, 1);
+  return e;
+}
+
+bool range_block_ok(const LevelTable& T) {
   if (T.count == 0 || T.count > kMaxUnrolled) return false;
   for (int j = 0; j < T.count; ++j)
     if (T.n[j] > 0xFFFFFFFFull) return false;
   return true;
-}
-
-uint64_t range3_scratch_bytes(const LevelTable& T, uint64_t nq) {
-  auto al = [](uint64_t x) { return (x + 255) / 256 * 256; };
-  return al((uint64_t)T.count * nq * 4) + al(nq * 4) + al(scan_scratch_words(nq) * 8);
-}
-
-cudaError_t launch_range3(const LevelTable& T, const uint32_t* k1, const uint32_t* k2,
-                          uint64_t nq, uint64_t* offsets, uint32_t* keys_out, uint32_t* vals_out,
-                          uint64_t capacity, void* scratch, cudaStream_t s,
-                          const LaunchHooks& hk) {
-  if (nq == 0) return cudaSuccess;
-  auto al = [](uint64_t x) { return (x + 255) / 256 * 256; };
-  uint8_t* b = static_cast<uint8_t*>(scratch);
-  uint32_t* pos = reinterpret_cast<uint32_t*>(b);
-  uint32_t* counts = reinterpret_cast<uint32_t*>(b + al((uint64_t)T.count * nq * 4));
-  uint64_t* sums = reinterpret_cast<uint64_t*>(b + al((uint64_t)T.count * nq * 4) + al(nq * 4));
-  // pass 1: bounds + counting walk, saving the start positions
-  hk.begin(hk.ctx, LSM_K_RANGE, s);
-  cudaError_t e = count_dispatch<true>(T, k1, k2, nq, counts, pos, s);
-  hk.end(hk.ctx, LSM_K_RANGE, (double)nq * (8.0 + 32.0 * T.count + 8.0 * T.count), s, 1);
-  if (e != cudaSuccess) return e;
-  // pass 2: offsets = exclusive scan of the counts (the paper's stage 2)
-  e = launch_scan(counts, nq, offsets, sums, s, hk);
-  if (e != cudaSuccess) return e;
-  // pass 3: write walk from the saved positions
-  hk.begin(hk.ctx, LSM_K_RANGE, s);
-  const int nl = T.count;
-  e = dispatch_nl<kMaxUnrolled>(nl, [&](auto c) -> cudaError_t {
-    constexpr int N = decltype(c)::value;
-    auto kern = range_write_kernel<N>;
-    const unsigned g = std::min(query_grid(nq), occ_grid(kern, 0));
-    kern<<<g, kQThreads, 0, s>>>(T, k2, nq, pos, offsets, keys_out, vals_out, capacity);
-    return cudaGetLastError();
-  });
-  // 4 B in + offsets 16 B + positions 4 B per level + one 32 B value sector
-  // per level; the pairs' 8 B each are added once the total is known
-  hk.end(hk.ctx, LSM_K_RANGE, (double)nq * (20.0 + 36.0 * T.count), s, 1);
-  return e;
 }
 
 }  // namespace gpulsm

@@ -10,7 +10,7 @@ timeout 1500 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byt
 P="python scripts/prof_step.py"
 NCU="timeout 600 ncu --set full --clock-control none --import-source on"
 $NCU -k regex:^count_kernel -s 0 -c 1 -o gpurun_out/prof_count $P > /dev/null 2>&1
-$NCU -k regex:"^count_kernel|^range_write" -s 1 -c 2 -o gpurun_out/prof_range $P > /dev/null 2>&1
+$NCU -k regex:range_block -s 0 -c 1 -o gpurun_out/prof_range $P > /dev/null 2>&1
 $NCU -k regex:lookup_kernel -s 0 -c 1 -o gpurun_out/prof_lookup $P > /dev/null 2>&1
 $NCU -k regex:merge_kernel -s 62 -c 1 -o gpurun_out/prof_merge $P --no-cleanup --nq 1024 > /dev/null 2>&1
 $NCU -k regex:merge_kernel -s 0 -c 1 -o gpurun_out/prof_merge0 $P --batches 4 --no-cleanup --nq 1024 > /dev/null 2>&1

@@ -27,7 +27,7 @@ int main(int argc, char** argv) {
   cudaEventRecord(e1); cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1);
   printf("n=%llu+%llu merge avg %.2f us  %.1f GB/s\n", (unsigned long long)n, (unsigned long long)n, ms * 20, 2 * n * 16 / (ms / 50 * 1e-3) / 1e9);
-  unsigned long long* probe; size_t pn = 4096 * 8;
+  unsigned long long* probe; size_t pn = 4096 * 16;
   cudaMalloc(&probe, pn * 8); cudaMemset(probe, 0, pn * 8);
   cudaMemcpyToSymbol(g_mprobe, &probe, sizeof(probe));
   launch_merge(ak, av, n, bk, bv, n, ok, ov, nullptr, 0, hk);
@@ -35,12 +35,12 @@ int main(int argc, char** argv) {
   std::vector<unsigned long long> P(pn);
   cudaMemcpy(P.data(), probe, pn * 8, cudaMemcpyDeviceToHost);
   unsigned long long t0 = ~0ull; int nc = 0;
-  for (int c = 0; c < 4096; ++c) if (P[c * 8]) { t0 = std::min(t0, P[c * 8]); nc++; }
-  const char* names[7] = {"entry", "waited", "search0", "search1", "data0", "merged0", "done"};
+  for (int c = 0; c < 4096; ++c) if (P[c * 16]) { t0 = std::min(t0, P[c * 16]); nc++; }
+  const char* names[12] = {"entry", "waited", "search0", "search1", "data0", "merged0", "done", "c_search", "c_merge", "c_gather", "c_sync1", "c_staged"};
   printf("ctas %d\n", nc);
-  for (int ph = 0; ph < 7; ++ph) {
+  for (int ph = 0; ph < 12; ++ph) {
     std::vector<double> x;
-    for (int c = 0; c < 4096; ++c) if (P[c * 8] && P[c * 8 + ph]) x.push_back((P[c * 8 + ph] - t0) / 1000.0);
+    for (int c = 0; c < 4096; ++c) if (P[c * 16] && P[c * 16 + ph]) x.push_back((P[c * 16 + ph] - t0) / 1000.0);
     std::sort(x.begin(), x.end());
     if (x.empty()) continue;
     printf("  %-8s min %8.2f p50 %8.2f p90 %8.2f max %8.2f us\n", names[ph], x[0], x[x.size() / 2], x[x.size() * 9 / 10], x.back());

@@ -22,8 +22,8 @@ TMUL = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "ns": 1e-3, "us": 1.0, 
 
 CLASS = [("onesweep", "sort_pass"), ("bucket_sort", "sort_pass"), ("small_sort", "sort_pass"),
          ("sort_hist", "sort_hist"), ("merge_kernel", "merge"),
-         ("lookup_kernel", "lookup"), ("count_kernel<1, 1>", "range"), ("count_kernel<3, 1>", "range"),
-         ("count_kernel", "count"), ("range_write", "range"), ("range_kernel", "range"),
+         ("lookup_kernel", "lookup"), ("range_block", "range"),
+         ("count_kernel", "count"), ("range_kernel", "range"),
          ("build_f1", "other"), ("finalize_index", "other"),
          ("scan_", "scan"), ("cleanup_", "cleanup"), ("fill_placebo", "cleanup"),
          ("bucket_", "other"), ("scatter_back", "other"), ("clip_kernel", "other"),
