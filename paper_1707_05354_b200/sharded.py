@@ -102,6 +102,9 @@ class GpuShardBackend:
     def update(self, k, v, o):
         self.lsm.update(k, v, o)
 
+    def clear(self):
+        self.lsm.clear()
+
     def lookup(self, q):
         return self.lsm.lookup(q)
 
@@ -139,6 +142,16 @@ class ShardedLSM:
             self.b_local, reserve_batches=reserve_batches)
         self.batches = 0
         self.overflow_splits = 0
+        # GPU: the per-batch count exchange runs on a side stream over its own
+        # communicator, so the host waits only for the bucket kernel and that
+        # exchange -- never for the previous batch's local insert, which keeps
+        # the device busy while the next batch is routed
+        self._pipelined = isinstance(self.backend, GpuShardBackend)
+        self._pending = None
+        self._routed = 0
+        if self._pipelined:
+            self._meta = dist.new_group(list(range(self.P)))
+            self._h_cnt = torch.empty((2, 2 * self.P), dtype=torch.int32, pin_memory=True)
 
     # ---- collectives (bytes only) ----
     def _a2a(self, send, send_counts, recv_counts, dtype):
@@ -154,13 +167,51 @@ class ShardedLSM:
     # ---- updates ----
     def update(self, keys, vals=None, is_delete=None):
         """This rank's slice of one global batch (global positions
-        [rank*b_in, (rank+1)*b_in)); all ranks call it together."""
+        [rank*b_in, (rank+1)*b_in)); all ranks call it together.
+
+        On GPUs the batch is inserted one call later (the next update, or
+        flush(), which every query and cleanup calls first): its bucket kernel
+        and count exchange are enqueued now, the exchange of the records and
+        the local insert of the PREVIOUS batch -- whose counts are already on
+        the host -- follow, so the host never waits for device work in flight."""
         if vals is None:
             vals = self.backend.empty(keys.numel(), torch.int32).zero_()
         if is_delete is None:
             is_delete = self.backend.empty(keys.numel(), torch.uint8).zero_()
+        if not self._pipelined:
+            k, v, o, _, cnt = self.backend.bucket(keys, vals, is_delete, self.P, 0, False)
+            send, recv = self._exchange_counts(cnt)
+            self._deliver(k, v, o, send, recv)
+            return
         k, v, o, _, cnt = self.backend.bucket(keys, vals, is_delete, self.P, 0, False)
-        send, recv = self._exchange_counts(cnt)
+        rcnt = self.backend.empty(self.P, torch.int32)
+        dist.all_to_all_single(rcnt, cnt, group=self._meta)
+        self._routed += 1
+        slot = self._routed & 1
+        self._h_cnt[slot, :self.P].copy_(cnt, non_blocking=True)
+        self._h_cnt[slot, self.P:].copy_(rcnt, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self.flush()
+        self._pending = (k, v, o, ev, slot)
+
+    def clear(self):
+        """Drop every resident record on this rank (pending batch included)."""
+        self.flush()
+        self.backend.clear()
+        self.batches = 0
+
+    def flush(self):
+        """Insert the batch routed by the last update() (no-op otherwise)."""
+        if not self._pipelined or self._pending is None:
+            return
+        k, v, o, ev, slot = self._pending
+        self._pending = None
+        ev.synchronize()  # its bucket kernel and count exchange only
+        h = self._h_cnt[slot].tolist()
+        self._deliver(k, v, o, h[:self.P], h[self.P:])
+
+    def _deliver(self, k, v, o, send, recv):
         rk = self._a2a(k, send, recv, torch.int32)
         rv = self._a2a(v, send, recv, torch.int32)
         ro = self._a2a(o, send, recv, torch.uint8)
@@ -194,6 +245,7 @@ class ShardedLSM:
     # ---- queries ----
     def lookup(self, q):
         """Lookup this rank's queries; returns (vals, found) in query order."""
+        self.flush()
         k, _, _, perm, cnt = self.backend.bucket(q, None, None, self.P, 0, True)
         send, recv = self._exchange_counts(cnt)
         rq = self._a2a(k, send, recv, torch.int32)
@@ -205,6 +257,7 @@ class ShardedLSM:
     def count(self, k1, k2):
         """Counts for this rank's (k1, k2) queries; every rank passes the same
         number of queries."""
+        self.flush()
         nq = k1.numel()
         all1 = self.backend.empty(nq * self.P, torch.int32)
         all2 = self.backend.empty(nq * self.P, torch.int32)
@@ -216,6 +269,7 @@ class ShardedLSM:
         return self.backend.sum_parts(recv, self.P, nq)
 
     def _order(self, q, succ):
+        self.flush()
         nq = q.numel()
         P = self.P
         allq = self.backend.empty(nq * P, torch.int32)
@@ -238,6 +292,7 @@ class ShardedLSM:
         """Ranges for this rank's (k1, k2) queries: (offsets[nq+1], keys, vals)
         with each query's pairs in key order; every rank passes the same number
         of queries."""
+        self.flush()
         nq = k1.numel()
         P = self.P
         all1 = self.backend.empty(nq * P, torch.int32)
@@ -293,7 +348,7 @@ def run_sharded_bench(args, dist_mod, rank, world, local_rank):
     sh = ShardedLSM(b_global, reserve_batches=R + 2)
 
     def step():
-        sh.backend.lsm.clear()
+        sh.clear()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e2 = torch.cuda.Event(enable_timing=True)

@@ -75,6 +75,10 @@ class CpuTestBackend:
     def sum_parts(self, t, P, n):
         return torch.from_numpy(t.numpy().reshape(P, n).sum(axis=0).astype(np.int32))
 
+    def clear(self):
+        import oracle
+        self.store = oracle.OracleDict(self.b_local)
+
     def update(self, k, v, o):
         assert k.numel() <= self.b_local
         self.batch_sizes.append(k.numel())
