@@ -185,7 +185,8 @@ def run_native(args):
         dist.init_process_group("nccl", rank=rank, world_size=world,
                                 device_id=torch.device("cuda", local_rank))
         from paper_1707_05354_b200.sharded import run_sharded_bench
-        return run_sharded_bench(args, dist, rank, world, local_rank)
+        return run_sharded_bench(args, dist, rank, world, local_rank, clock_cls=ClockSampler,
+                                 peaks_fn=measured_peaks)
 
     seed = synth.SEED_BASE + 2
     dev = torch.device("cuda", local_rank)

@@ -314,13 +314,15 @@ class ShardedLSM:
         return self.backend.range_assemble(roffs, rl, P, nq, rkk, rvv)
 
 
-def run_sharded_bench(args, dist_mod, rank, world, local_rank):
+def run_sharded_bench(args, dist_mod, rank, world, local_rank, clock_cls=None, peaks_fn=None):
     """bench.py --gpus N (N > 1): weak scaling of the sharded LSM.
 
     Global batch b_global = N * 2^20 (each rank contributes 2^20 positions of
     the global order), R = 64 global batches from empty (2^26 resident per
-    GPU), then 2^24 lookups per rank routed to their owners. Times are CUDA
-    events on each rank, max over ranks."""
+    GPU), then 2^24 lookups per rank routed to their owners. Device times are
+    CUDA events on each rank, max over ranks; e2e adds the pinned host->device
+    copy of every batch and a device->host read of the result."""
+    import contextlib
     import json
     import os
     import sys
@@ -338,14 +340,19 @@ def run_sharded_bench(args, dist_mod, rank, world, local_rank):
     b_global = B_IN * world
     seed = synth.SEED_BASE + 4
     dev = torch.device("cuda", local_rank)
-    keys, vals, ops = [], [], []
+    keys, vals, ops, host = [], [], [], []
     for j in range(R):
         k, v, d = synth.updates(seed, j * b_global + rank * B_IN, B_IN, delete_frac4=0)
         keys.append(to_device(k, dev))
         vals.append(to_device(v, dev))
         ops.append(to_device(d, dev))
+        if args.e2e:
+            host.append((torch.from_numpy(k.view(np.int32)).pin_memory(),
+                         torch.from_numpy(v.view(np.int32)).pin_memory(),
+                         torch.from_numpy(d).pin_memory()))
     q = to_device(synth.lookup_queries(seed + rank, NQ, R * b_global), dev)
     sh = ShardedLSM(b_global, reserve_batches=R + 2)
+    lsm = sh.backend.lsm
 
     def step():
         sh.clear()
@@ -355,6 +362,7 @@ def run_sharded_bench(args, dist_mod, rank, world, local_rank):
         e0.record()
         for j in range(R):
             sh.update(keys[j], vals[j], ops[j])
+        sh.flush()
         e1.record()
         sh.lookup(q)
         e2.record()
@@ -365,30 +373,83 @@ def run_sharded_bench(args, dist_mod, rank, world, local_rank):
     torch.cuda.synchronize()
     dist_mod.barrier()
     recs = []
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        recs.append(step())
-    torch.cuda.synchronize()
-    dist_mod.barrier()
-    wall = time.perf_counter() - t0
+    l0 = lsm.launch_count
+    clk_ctx = clock_cls(local_rank) if clock_cls is not None else contextlib.nullcontext()
+    with clk_ctx as clk:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            recs.append(step())
+        torch.cuda.synchronize()
+        dist_mod.barrier()
+        wall = time.perf_counter() - t0
+    launches = lsm.launch_count - l0
     upd = sum(a.elapsed_time(b) for a, b, _ in recs) / args.steps
     look = sum(b.elapsed_time(c) for _, b, c in recs) / args.steps
-    t = torch.tensor([upd, look, wall], device=dev, dtype=torch.float64)
+    # per-class breakdown of this rank's kernels (K more identical steps)
+    lsm.profile_enable(True)
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
+    prof = lsm.profile_read()
+    lsm.profile_enable(False)
+    e2e_s = 0.0
+    if args.e2e:
+        dk = [torch.empty(B_IN, dtype=torch.int32, device=dev) for _ in range(3)]
+        dvv = [torch.empty(B_IN, dtype=torch.int32, device=dev) for _ in range(3)]
+        do = [torch.empty(B_IN, dtype=torch.uint8, device=dev) for _ in range(3)]
+
+        def e2e_step():
+            sh.clear()
+            for j in range(R):
+                s3 = j % 3
+                dk[s3].copy_(host[j][0], non_blocking=True)
+                dvv[s3].copy_(host[j][1], non_blocking=True)
+                do[s3].copy_(host[j][2], non_blocking=True)
+                sh.update(dk[s3], dvv[s3], do[s3])
+            sh.flush()
+            return lsm.r  # device->host read of the result (r after the batches)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        dist_mod.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / args.steps
+    t = torch.tensor([upd, look, wall, e2e_s], device=dev, dtype=torch.float64)
     dist_mod.all_reduce(t, op=dist_mod.ReduceOp.MAX)
-    upd, look, wall = [float(x) for x in t.tolist()]
+    upd, look, wall, e2e_s = [float(x) for x in t.tolist()]
+    lt = torch.tensor([launches], device=dev, dtype=torch.int64)
+    dist_mod.all_reduce(lt, op=dist_mod.ReduceOp.SUM)
     if rank == 0:
+        peak, peak_src = peaks_fn() if peaks_fn is not None else (6551.0, "fallback")
+        dom = max(prof, key=lambda c: prof[c]["ms"])
+        ach = prof[dom]["alg_bytes"] / (prof[dom]["ms"] * 1e-3) / 1e9 if prof[dom]["ms"] else 0.0
         line = {
             "metric": "M updates/s at batch b; M lookup/count/range queries/s; HBM GB/s vs peak",
             "value": R * b_global / (upd * 1e-3) / 1e6, "unit": "M updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": (upd + look), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u32", "data": "synthetic (splitmix64 uniform keys)",
+            "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (splitmix64 uniform keys, insert-only)",
             "config": {"workload": "C5: key-range sharded LSM, global batch b = N x 2^20 routed by "
                                    "bucket kernel + NCCL all-to-all, 64 global batches "
                                    f"(2^26 resident per GPU), 2^24 lookups per rank",
                        "b_global": b_global, "b_local": sh.b_local, "batches": R,
-                       "parallelism": f"key-range shards x{world}"},
+                       "parallelism": f"key-range shards x{world}",
+                       "l2": "inputs larger than L2 -- no flush"},
             "lookup_mqps": world * NQ / (look * 1e-3) / 1e6,
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak,
+                         "peak_source": peak_src, "unit": "GB/s", "frac": ach / peak,
+                         "traffic": None, "scope": "rank 0's local kernels",
+                         "timing": "per-launch CUDA events over K more identical steps"},
+            "gpu_launches": int(lt.item()),
+            "clocks": clk.summary() if clk is not None else None,
+            "e2e": ({"value": R * b_global / e2e_s / 1e6, "unit": "M updates/s",
+                     "h2d_bytes_per_step": R * b_global * 9, "d2h_bytes_per_step": 8 * world,
+                     "note": "pinned H2D of each rank's batch slice + sharded update, wall clock, "
+                             "max over ranks"} if args.e2e else None),
             "overflow_splits": sh.overflow_splits,
             "wall_s": wall,
         }
