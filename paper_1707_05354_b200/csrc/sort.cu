@@ -263,10 +263,10 @@ __global__ void __launch_bounds__(kSortThreads, 1) onesweep_pass_kernel(
   for (int i = tid; i < kWarps * kRadix; i += kSortThreads) (&S.whist[0][0])[i] = 0;
   pdl_wait();
   pdl_trigger();
-  if (use_ctr) {
-    if (tid == 0) S.tile = atomicAdd(tile_ctr, 1u);
-    __syncthreads();
-  }
+  if (use_ctr && tid == 0) S.tile = atomicAdd(tile_ctr, 1u);
+  // every warp's counter row is zeroed by other warps' threads: all zeroing
+  // must be visible before any ranking (racecheck)
+  __syncthreads();
   const uint32_t tile = use_ctr ? S.tile : blockIdx.x;
 #ifdef GPULSM_PROBE
   if (threadIdx.x == 0 && g_probe) g_probe[((uint64_t)(shift / 8) * 4096 + tile) * 8 + 0] = t_entry;
