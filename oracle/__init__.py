@@ -32,7 +32,7 @@ u8p = ctypes.POINTER(ctypes.c_uint8)
 
 def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC",
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-pthread",
                                "-o", _LIB, _SRC])
     return _LIB
 
@@ -59,6 +59,9 @@ def lib():
             "sa_cleanup": ([vp], None), "sa_size": ([vp], u64),
             "sa_num_batches": ([vp], u64), "sa_merged_records": ([vp], u64),
             "sa_array": ([vp, u32p, u32p], None),
+            "o1mt_create": ([u64, ctypes.c_uint32], vp), "o1mt_destroy": ([vp], None),
+            "o1mt_apply_batch": ([vp, u32p, u32p, u8p, u64], None),
+            "o1mt_lookup": ([vp, u32p, u64, u32p, u8p], None), "o1mt_size": ([vp], u64),
             "o1_cleanup": ([vp], None), "o1_size": ([vp], u64),
             "o1_num_batches": ([vp], u64), "o1_dump": ([vp, u32p, u32p], None),
             "s1_create": ([u64], vp), "s1_destroy": ([vp], None),
@@ -324,3 +327,32 @@ class ShadowSA:
         if n:
             lib().sa_array(self.h, _p(k, u32p), _p(v, u32p))
         return k, v
+
+
+class ShardedOracleDict:
+    """O1 over T key-range shards, one thread each (CPU-baseline timing only)."""
+
+    def __init__(self, b: int, threads: int):
+        self.threads = int(threads)
+        self.h = lib().o1mt_create(b, self.threads)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().o1mt_destroy(self.h)
+            self.h = None
+
+    def apply_batch(self, keys, vals=None, is_delete=None):
+        keys = _u32(keys)
+        vals = _u32(vals) if vals is not None else np.zeros_like(keys)
+        d = _u8(is_delete)
+        lib().o1mt_apply_batch(self.h, _p(keys, u32p), _p(vals, u32p), _p(d, u8p), len(keys))
+
+    def lookup(self, q):
+        q = _u32(q)
+        v = np.empty(len(q), np.uint32)
+        f = np.empty(len(q), np.uint8)
+        lib().o1mt_lookup(self.h, _p(q, u32p), len(q), _p(v, u32p), _p(f, u8p))
+        return v, f
+
+    def __len__(self):
+        return int(lib().o1mt_size(self.h))

@@ -38,6 +38,7 @@
 #include <cstdint>
 #include <cstring>
 #include <map>
+#include <thread>
 #include <vector>
 
 namespace {
@@ -409,6 +410,86 @@ void s1_cleanup(void* h) {
     off += sz;
   }
   s->r = r2;
+}
+
+// ============================ O1 sharded (timing) ============================
+// O1 split into T std::maps by key range (shard s owns [s*D/T, (s+1)*D/T)),
+// for the T-thread CPU baseline of SURVEY §8(d). Exact: keys never interact,
+// so every shard applies its part of each batch in order with O1's rules
+// (R4). One thread per shard; lookups split by position.
+struct O1MT {
+  uint64_t b = 0;
+  uint32_t T = 1;
+  std::vector<O1> shard;
+};
+
+static uint32_t o1mt_owner(const O1MT* o, uint32_t k) {
+  const uint64_t s = (uint64_t)k * o->T / 0x7FFFFFFFull;
+  return s >= o->T ? o->T - 1 : (uint32_t)s;
+}
+
+void* o1mt_create(uint64_t b, uint32_t threads) {
+  O1MT* o = new O1MT;
+  o->b = b;
+  o->T = threads ? threads : 1;
+  o->shard.resize(o->T);
+  for (auto& x : o->shard) x.b = b;
+  return o;
+}
+void o1mt_destroy(void* h) { delete static_cast<O1MT*>(h); }
+
+void o1mt_apply_batch(void* h, const uint32_t* keys, const uint32_t* vals,
+                      const uint8_t* is_delete, uint64_t n) {
+  O1MT* o = static_cast<O1MT*>(h);
+  std::vector<std::thread> th;
+  for (uint32_t t = 0; t < o->T; ++t) {
+    th.emplace_back([o, t, keys, vals, is_delete, n] {
+      struct St { bool del = false; bool ins = false; uint32_t v = 0; };
+      std::map<uint32_t, St> B;
+      for (uint64_t i = 0; i < n; ++i) {
+        const uint32_t k = keys[i];
+        if (k > kMaxKey || o1mt_owner(o, k) != t) continue;
+        St& st = B[k];
+        if (is_delete && is_delete[i]) {
+          st.del = true;
+        } else if (!st.ins) {
+          st.ins = true;
+          st.v = vals ? vals[i] : 0u;
+        }
+      }
+      auto& S = o->shard[t].S;
+      for (auto& kv : B) {
+        if (kv.second.del) S.erase(kv.first);
+        else S[kv.first] = kv.second.v;
+      }
+    });
+  }
+  for (auto& x : th) x.join();
+}
+
+void o1mt_lookup(void* h, const uint32_t* q, uint64_t nq, uint32_t* vals_out,
+                 uint8_t* found_out) {
+  O1MT* o = static_cast<O1MT*>(h);
+  std::vector<std::thread> th;
+  for (uint32_t t = 0; t < o->T; ++t) {
+    th.emplace_back([o, t, q, nq, vals_out, found_out] {
+      const uint64_t lo = nq * t / o->T, hi = nq * (t + 1) / o->T;
+      for (uint64_t i = lo; i < hi; ++i) {
+        const auto& S = o->shard[o1mt_owner(o, q[i] > kMaxKey ? kMaxKey : q[i])].S;
+        auto it = S.find(q[i]);
+        const bool f = it != S.end();
+        vals_out[i] = f ? it->second : 0xFFFFFFFFu;
+        if (found_out) found_out[i] = f ? 1 : 0;
+      }
+    });
+  }
+  for (auto& x : th) x.join();
+}
+
+uint64_t o1mt_size(void* h) {
+  uint64_t n = 0;
+  for (auto& x : static_cast<O1MT*>(h)->shard) n += x.S.size();
+  return n;
 }
 
 // ============================== SA (N2) =====================================

@@ -581,3 +581,18 @@ def test_sa_bulk_build_equals_lsm_bulk_image():
     cv = np.concatenate([s1.level(i)[1] for i in range(s1.num_levels())])
     ak, av = sa.array()
     assert sa.r == s1.r == 6 and np.array_equal(ak, ck) and np.array_equal(av, cv)
+
+
+def test_sharded_oracle_equals_o1():
+    # the T-thread timing oracle must be O1 exactly
+    b = 512
+    seed = synth.SEED_BASE + 90
+    o, m = oracle.OracleDict(b), oracle.ShardedOracleDict(b, 4)
+    for j in range(12):
+        k, v, d = synth.updates(seed, j * b, b, delete_frac4=1, alphabet=3000)
+        o.apply_batch(k, v, d)
+        m.apply_batch(k, v, d)
+    q = np.concatenate([np.arange(3100, dtype=np.uint32), np.array([0x7FFFFFFF, 0xFFFFFFFF], np.uint32)])
+    assert len(o) == len(m)
+    a, b_ = o.lookup(q), m.lookup(q)
+    assert np.array_equal(a[0], b_[0]) and np.array_equal(a[1], b_[1])
