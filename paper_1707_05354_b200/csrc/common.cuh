@@ -249,6 +249,20 @@ cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals
 
 // Stable merge on key>>1, A (newer) first on ties, into out[na+nb];
 // out_f1 (nullable) receives F1 of the output.
+// k-way cascade (kway.cu): runs 0..runs-1 newest first, run runs-1 the
+// oldest and largest; f1 = each run's fence keys (every 8th key).
+struct KwayRuns {
+  const uint32_t* k[LSM_MAX_LEVELS + 1];
+  const uint32_t* v[LSM_MAX_LEVELS + 1];
+  const uint32_t* f1[LSM_MAX_LEVELS + 1];
+  uint64_t n[LSM_MAX_LEVELS + 1];
+  int runs;
+};
+uint64_t kway_cut_words(const KwayRuns& R);
+cudaError_t launch_kway_merge(const KwayRuns& R, uint64_t* cuts, uint32_t* ok, uint32_t* ov,
+                              uint32_t* out_f1, uint32_t* gk, uint32_t* gv, cudaStream_t s,
+                              const LaunchHooks& hk);
+
 cudaError_t launch_merge(const uint32_t* ak, const uint32_t* av, uint64_t na,
                          const uint32_t* bk, const uint32_t* bv, uint64_t nb, uint32_t* ok,
                          uint32_t* ov, uint32_t* out_f1, cudaStream_t s, const LaunchHooks& hk);

@@ -60,6 +60,8 @@ struct lsm {
   uint32_t* home_idx[LSM_MAX_LEVELS] = {};  // index storage of each home level
   Buffer ping[2];         // merge ping-pong scratch
   Buffer sortout;         // sorted batch when t >= 1
+  uint32_t* sortout_f1 = nullptr;  // its fence keys (k-way cascade, t >= 2)
+  Buffer kscratch;        // k-way cascade: scratch for oversized chunks
   SortScratch sort{};
   uint32_t* sort_meta = nullptr;
   uint64_t sort_meta_words = 0;
@@ -411,6 +413,8 @@ lsm_status lsm_destroy(lsm_t* h) {
   buf_free(h->ping[0], nullptr);
   buf_free(h->ping[1], nullptr);
   buf_free(h->sortout, nullptr);
+  buf_free(h->kscratch, nullptr);
+  if (h->sortout_f1) cudaFreeAsync(h->sortout_f1, nullptr);
   if (h->sort_meta) cudaFreeAsync(h->sort_meta, nullptr);
   for (int k = 0; k < 2; ++k) {
     if (h->sort.tmp_keys[k]) cudaFreeAsync(h->sort.tmp_keys[k], nullptr);
@@ -605,6 +609,38 @@ static lsm_status do_update(lsm_t* h, const uint32_t* keys, const uint32_t* vals
   // sort (A1+A2): straight into level 0 (with its F1) when t == 0
   uint32_t* sk = (t == 0) ? h->home[0].keys : h->sortout.keys;
   uint32_t* sv = (t == 0) ? h->home[0].vals : h->sortout.vals;
+  // the one-pass cascade (kway.cu) is exact but not yet faster than the
+  // iterated merges: opt-in with GPULSM_KWAY=1
+  static const bool kway = [] {
+    const char* e = std::getenv("GPULSM_KWAY");
+    return e && e[0] == '1';
+  }();
+  if (t >= 2 && kway) {
+    // one pass: the sorted batch (with fence keys) and levels 0..t-1 into
+    // level t (kway.cu; same bytes as the iterated merges)
+    if (!h->sortout_f1) CK(pool_alloc(h, (void**)&h->sortout_f1, idx_f1_len(b) * 4 + 64, s));
+    CK(launch_sort_batch(keys, vals, ops, mode, n, b, h->sort, sk, sv, h->sortout_f1, s, hk));
+    KwayRuns R;
+    std::memset(&R, 0, sizeof(R));
+    R.runs = t + 1;
+    R.k[0] = sk;
+    R.v[0] = sv;
+    R.f1[0] = h->sortout_f1;
+    R.n[0] = b;
+    for (int i = 0; i < t; ++i) {
+      R.k[i + 1] = h->level[i].keys;
+      R.v[i + 1] = h->level[i].vals;
+      R.f1[i + 1] = h->level[i].idx;
+      R.n[i + 1] = b << i;
+    }
+    CK(buf_ensure(h, h->kscratch, b << t, s));
+    CK(ensure_qbuf(h, kway_cut_words(R) * 8, s));
+    CK(launch_kway_merge(R, static_cast<uint64_t*>(h->qbuf), h->home[t].keys, h->home[t].vals,
+                         h->home_idx[t], h->kscratch.keys, h->kscratch.vals, s, hk));
+    for (int i = 0; i < t; ++i) level_release(h, i, s);  // levels 0..t-1 <- empty
+    commit_insert(h, t);
+    return LSM_OK;
+  }
   CK(launch_sort_batch(keys, vals, ops, mode, n, b, h->sort, sk, sv,
                        t == 0 ? h->home_idx[0] : nullptr, s, hk));
   st = cascade(h, sk, sv, t, s, hk);

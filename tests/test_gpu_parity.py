@@ -635,3 +635,30 @@ def test_config_c4_shape_sampled():
         assert np.array_equal(to_numpy_u32(gk)[sure], ok[sure]), name
         assert np.array_equal(to_numpy_u32(gvv)[sure], ovv[sure]), name
         assert np.all(gff.cpu().numpy()[sure] == 1), name
+
+
+def test_kway_cascade_skewed_chunk():
+    # The one-pass cascade (kway.cu) cuts the merge at every 1024th record of
+    # the oldest level; a batch whose keys all fall into one narrow key range
+    # puts the whole batch into one chunk (over the shared-memory capacity),
+    # which must take the global-memory path -- bit-exact vs S1 regardless.
+    b = 8192
+    gpu, s1, o1 = GpuAdapter(b), oracle.ShadowLSM(b), oracle.OracleDict(b)
+    seed = synth.SEED_BASE + 95
+    for j in range(15):
+        if j in (7, 14):  # t = 3 cascades with a concentrated batch
+            rng = np.random.default_rng(j)
+            k = rng.integers(1_000_000, 1_000_400, b).astype(np.uint32)
+            v = np.arange(j * b, (j + 1) * b, dtype=np.uint32)
+            d = (rng.integers(0, 4, b) == 0).astype(np.uint8)
+        else:
+            k, v, d = synth.updates(seed, j * b, b, delete_frac4=1, alphabet=4_000_000)
+        gpu.update(k, v, d)
+        s1.update(k, v, d)
+        o1.apply_batch(k, v, d)
+        assert_levels_equal(gpu, s1, f"batch {j}")
+    q = np.concatenate([np.arange(999_990, 1_000_410, dtype=np.uint32),
+                        synth.lookup_queries(seed, 2000, 15 * b, alphabet=4_000_000)])
+    k1 = np.array([999_000, 1_000_100, 0], np.uint32)
+    k2 = np.array([1_000_500, 1_000_200, 4_000_000], np.uint32)
+    assert_queries_equal(gpu, o1, q, k1, k2, "skewed")
