@@ -351,18 +351,7 @@ __global__ void __launch_bounds__(kSortThreads, 1) onesweep_pass_kernel(
   const uint32_t tstart = block_exclusive_scan<kSortThreads, uint32_t>(tile_cnt, S.scan, &tot);
   if (tid < kRadix) S.tstart[tid] = tstart;
   __syncthreads();
-
-  // ---- stage in smem in digit order (needs only tile-local offsets) ----
-#pragma unroll
-  for (int i = 0; i < kSortItems; ++i) {
-    const uint32_t off = wbase + i * 32 + lane;
-    if (off < tile_n) {
-      const uint32_t d = (k[i] >> shift) & (kRadix - 1);
-      const uint32_t p = S.tstart[d] + S.whist[warp][d] + rk[i];
-      S.keys[p] = k[i];
-      S.vals[p] = v[i];
-    }
-  }
+  PROBE(4);
 
   // ---- two-level decoupled look-back (threads 0..255 = digits) ----
   uint32_t gp = 0, wp = 0, total = 0;
@@ -394,6 +383,25 @@ __global__ void __launch_bounds__(kSortThreads, 1) onesweep_pass_kernel(
     // the group total
     if (tile == g0 + kGroup - 1 || tile == ntiles - 1)
       atomicExch(group_st + (uint64_t)g * kRadix + dgt, st_word(epoch, wp + tile_cnt));
+  }
+
+  // ---- stage in smem in digit order (needs only tile-local offsets); the
+  //      group totals above are already on their way ----
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const uint32_t off = wbase + i * 32 + lane;
+    if (off < tile_n) {
+      const uint32_t d = (k[i] >> shift) & (kRadix - 1);
+      const uint32_t p = S.tstart[d] + S.whist[warp][d] + rk[i];
+      S.keys[p] = k[i];
+      S.vals[p] = v[i];
+    }
+  }
+  PROBE(6);
+
+  if (tid < kRadix) {
+    const uint32_t dgt = tid;
+    const uint32_t g = tile / kGroup;
     // earlier groups (multi-wave) or all groups (one wave: also the totals)
     const uint32_t ng = use_ctr ? g : (ntiles + kGroup - 1) / kGroup;
     for (uint32_t G0 = 0; G0 < ng; G0 += kGroup) {
