@@ -15,7 +15,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgpulsm.so")
+# GPULSM_LIB selects another in-tree build of the same sources (A/B variants
+# built by build.build_variant); default: libgpulsm.so
+LIB_PATH = os.path.join(_HERE, os.environ.get("GPULSM_LIB", "libgpulsm.so"))
 
 LSM_OK = 0
 LSM_ERR_CAPACITY = 4
