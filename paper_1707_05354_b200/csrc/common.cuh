@@ -93,6 +93,58 @@ __device__ __forceinline__ uint4 ldg_nc_v4(const void* p) {
                : "l"(p));
   return r;
 }
+// L2 eviction-priority policies (createpolicy + ld ... .L2::cache_hint). The
+// query kernels read the fence-key index (F1/F2 lines, reused by every query
+// that lands in the same key interval) and random 32-byte sectors of the
+// levels (touched once). Without hints the sector stream evicts the index
+// from L2; with evict_last on the index and evict_first on the sectors the
+// index stays resident. GPULSM_L2HINT=0 disables them (A/B).
+#ifndef GPULSM_L2HINT
+#define GPULSM_L2HINT 1
+#endif
+__device__ __forceinline__ uint64_t l2_policy_keep() {
+  uint64_t p = 0;
+#if GPULSM_L2HINT
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+#endif
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_stream() {
+  uint64_t p = 0;
+#if GPULSM_L2HINT
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+#endif
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_normal() {
+  uint64_t p = 0;
+#if GPULSM_L2HINT
+  asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+#endif
+  return p;
+}
+__device__ __forceinline__ uint4 ldg_v4_pol(const void* ptr, uint64_t pol) {
+  uint4 r;
+#if GPULSM_L2HINT
+  asm("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(ptr), "l"(pol));
+#else
+  (void)pol;
+  r = __ldg(reinterpret_cast<const uint4*>(ptr));
+#endif
+  return r;
+}
+__device__ __forceinline__ uint32_t ldg_pol(const uint32_t* ptr, uint64_t pol) {
+  uint32_t r;
+#if GPULSM_L2HINT
+  asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(ptr), "l"(pol));
+#else
+  (void)pol;
+  r = __ldg(ptr);
+#endif
+  return r;
+}
 __device__ __forceinline__ void stg_v4(void* p, uint4 v) {
   asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
                "r"(v.w)
@@ -188,7 +240,12 @@ struct SortScratch {
   uint32_t* overflow_dev; // mapped host word: a bucket overflowed shared memory
   volatile uint32_t* overflow_host;
   bool lsd_only;          // skewed keys seen: use the 4-pass LSD path
+  uint32_t* msd_cnt;      // [2][256] bucket counts of the MSD + rank mode (double-buffered)
+  uint32_t* msd_bar;      // [2] its grid-barrier words
+  int msd_parity;
 };
+// words of the sort metadata head (before the look-back status words)
+constexpr uint64_t kSortMetaHead = 3 * 4 * 256 + 16 + 2 * 256 + 2 * 256 + 16;
 
 // one fat tile per SM: 1024 threads x 7 records (b = 2^20 -> 147 tiles)
 constexpr int kSortThreads = 1024;
@@ -197,6 +254,7 @@ constexpr int kSortTile = kSortThreads * kSortItems;
 constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;
 constexpr int kPasses = 4;
+static_assert(kSortMetaHead == 3 * kPasses * kRadix + 16 + 4 * kRadix + 16, "sort meta layout");
 
 inline uint64_t sort_tiles(uint64_t b) { return (b + kSortTile - 1) / kSortTile; }
 inline uint64_t sort_groups(uint64_t b) { return (sort_tiles(b) + 31) / 32; }
@@ -242,10 +300,24 @@ cudaError_t launch_sort_segments(const uint32_t* raw_keys, const uint32_t* raw_v
                                  const uint8_t* ops, int mode, uint64_t n, uint64_t b,
                                  uint64_t k, SortScratch& S, uint32_t* out_keys,
                                  uint32_t* out_vals, cudaStream_t s, const LaunchHooks& hk);
+// Optional first cascade step fused into the sort (MSD + rank mode only):
+// the sorted batch (newer, first on ties) is merged with the sorted run
+// (keys, vals, n) -- level 0 -- straight into (out_keys, out_vals) of
+// n + b records, with F1 into out_f1 when not null. *fused reports whether
+// the sort took this path (otherwise the plain sorted batch was written).
+struct SortMerge {
+  const uint32_t* keys;
+  const uint32_t* vals;
+  uint64_t n;
+  uint32_t* out_keys;
+  uint32_t* out_vals;
+  uint32_t* out_f1;
+};
 cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals,
                               const uint8_t* ops, int mode, uint64_t n, uint64_t b,
                               SortScratch& S, uint32_t* out_keys, uint32_t* out_vals,
-                              uint32_t* out_f1, cudaStream_t s, const LaunchHooks& hk);
+                              uint32_t* out_f1, cudaStream_t s, const LaunchHooks& hk,
+                              const SortMerge* merge = nullptr, bool* fused = nullptr);
 
 // Stable merge on key>>1, A (newer) first on ties, into out[na+nb];
 // out_f1 (nullable) receives F1 of the output.

@@ -196,7 +196,7 @@ cudaError_t ensure_sort_scratch(lsm* h, cudaStream_t s) {
   if (h->sort_meta == nullptr) {
     // hist[2][4][256] | bases[4][256] | tile_ctr[4] | err | done | pad |
     // bkt[2][256] | status
-    const uint64_t head = 3 * kPasses * kRadix + 16 + 2 * kRadix;
+    const uint64_t head = kSortMetaHead;
     h->sort_meta_words = head + sort_status_words(h->b);
     cudaError_t e = pool_alloc(h, (void**)&h->sort_meta, h->sort_meta_words * 4, s);
     if (e != cudaSuccess) return e;
@@ -208,6 +208,9 @@ cudaError_t ensure_sort_scratch(lsm* h, cudaStream_t s) {
     h->sort.err = h->sort.tile_ctr + 4;
     h->sort.done_ctr = h->sort.tile_ctr + 5;
     h->sort.bkt = h->sort_meta + 3 * kPasses * kRadix + 16;
+    h->sort.msd_cnt = h->sort.bkt + 2 * kRadix;
+    h->sort.msd_bar = h->sort.msd_cnt + 2 * kRadix;
+    h->sort.msd_parity = 0;
     h->sort.status = h->sort_meta + head;
     // overflow flag of the MSD + local sort: a mapped host word, so the host
     // reads it without a copy or a sync
@@ -246,7 +249,7 @@ cudaError_t ensure_bulk_scratch(lsm* h, uint64_t cap, cudaStream_t s) {
   cudaError_t e = ensure_sort_scratch(h, s);
   if (e != cudaSuccess || h->bulk_cap >= cap) return e;
   bulk_free(h, s);
-  const uint64_t head = 3 * kPasses * kRadix + 16 + 2 * kRadix;
+  const uint64_t head = kSortMetaHead;
   const uint64_t words = head + sort_status_words(cap);
   e = pool_alloc(h, (void**)&h->bulk_meta, words * 4, s);
   if (e != cudaSuccess) return e;
@@ -259,6 +262,9 @@ cudaError_t ensure_bulk_scratch(lsm* h, uint64_t cap, cudaStream_t s) {
   B.err = h->sort.err;  // one sticky domain-error word per handle
   B.done_ctr = B.tile_ctr + 5;
   B.bkt = h->bulk_meta + 3 * kPasses * kRadix + 16;
+  B.msd_cnt = B.bkt + 2 * kRadix;
+  B.msd_bar = B.msd_cnt + 2 * kRadix;
+  B.msd_parity = 0;
   B.status = h->bulk_meta + head;
   B.overflow_dev = h->sort.overflow_dev;
   B.overflow_host = h->sort.overflow_host;
@@ -391,6 +397,12 @@ lsm_status lsm_create(uint64_t b, lsm_t** out) {
   }
   uint64_t thr = ~0ull;
   cudaMemPoolSetAttribute(h->pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  {
+    // L2 fetch granularity (A/B knob): the query kernels'
+    // level accesses are random 32-byte sectors
+    const char* g = std::getenv("GPULSM_L2FETCH");
+    if (g != nullptr) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)std::atoi(g));
+  }
   e = cudaMallocHost((void**)&h->h_pinned, 64);
   if (e != cudaSuccess) {
     cudaMemPoolDestroy(h->pool);
@@ -500,9 +512,9 @@ static lsm_status prepare_insert(lsm_t* h, int t, cudaStream_t s) {
 // level i is full, buffer <- merge(buffer, level i), newer first on ties
 // (PAPER.md:621-624); the last merge writes level t and its fence keys F1.
 static lsm_status cascade(lsm_t* h, const uint32_t* ck, const uint32_t* cv, int t,
-                          cudaStream_t s, const LaunchHooks& hk) {
+                          cudaStream_t s, const LaunchHooks& hk, int i0 = 0) {
   const uint64_t b = h->b;
-  for (int i = 0; i < t; ++i) {
+  for (int i = i0; i < t; ++i) {
     uint32_t* ok = (i == t - 1) ? h->home[t].keys : h->ping[i & 1].keys;
     uint32_t* ov = (i == t - 1) ? h->home[t].vals : h->ping[i & 1].vals;
     const uint64_t ni = b << i;
@@ -641,9 +653,30 @@ static lsm_status do_update(lsm_t* h, const uint32_t* keys, const uint32_t* vals
     commit_insert(h, t);
     return LSM_OK;
   }
+  // t >= 1: the sort may also do the cascade's first merge (batch with
+  // level 0, sort.cu fused_merge) and write the 2b-record buffer directly
+  static const bool fuse_ok = [] {
+    const char* e = std::getenv("GPULSM_FUSE");
+    return !(e && e[0] == '0');
+  }();
+  SortMerge M{};
+  if (t >= 1 && fuse_ok) {
+    M.keys = h->level[0].keys;
+    M.vals = h->level[0].vals;
+    M.n = b;
+    M.out_keys = (t == 1) ? h->home[1].keys : h->ping[0].keys;
+    M.out_vals = (t == 1) ? h->home[1].vals : h->ping[0].vals;
+    M.out_f1 = (t == 1) ? h->home_idx[1] : nullptr;
+  }
+  bool fused = false;
   CK(launch_sort_batch(keys, vals, ops, mode, n, b, h->sort, sk, sv,
-                       t == 0 ? h->home_idx[0] : nullptr, s, hk));
-  st = cascade(h, sk, sv, t, s, hk);
+                       t == 0 ? h->home_idx[0] : nullptr, s, hk, M.keys ? &M : nullptr, &fused));
+  if (fused) {
+    level_release(h, 0, s);  // level 0 <- empty
+    st = cascade(h, M.out_keys, M.out_vals, t, s, hk, 1);
+  } else {
+    st = cascade(h, sk, sv, t, s, hk);
+  }
   if (st != LSM_OK) return st;
   commit_insert(h, t);
   return LSM_OK;

@@ -177,14 +177,15 @@ __device__ __forceinline__ uint32_t grp_line_count(const uint32_t* __restrict__ 
                                                    uint32_t x2) {
   const uint32_t lane = lane_id(), e = lane & 3;
   const uint4* A = reinterpret_cast<const uint4*>(a);
+  const uint64_t keep = l2_policy_keep();  // index lines: keep in L2
   uint32_t res = 0;
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     const uint32_t src = (lane & ~3u) | r;  // round r: lanes 4G..4G+3 serve lane 4G+r
     const uint32_t lj = __shfl_sync(kFull, ln, src);
     const uint32_t xj = __shfl_sync(kFull, x2, src);
-    const uint4 v0 = __ldg(A + lj * 8 + 2 * e);
-    const uint4 v1 = __ldg(A + lj * 8 + 2 * e + 1);
+    const uint4 v0 = ldg_v4_pol(A + lj * 8 + 2 * e, keep);
+    const uint4 v1 = ldg_v4_pol(A + lj * 8 + 2 * e + 1, keep);
     uint32_t c = (v0.x < xj) + (v0.y < xj) + (v0.z < xj) + (v0.w < xj) + (v1.x < xj) +
                  (v1.y < xj) + (v1.z < xj) + (v1.w < xj);
     c += __shfl_xor_sync(kFull, c, 1);
@@ -198,7 +199,7 @@ __device__ __forceinline__ uint32_t grp_line_count(const uint32_t* __restrict__ 
 // x. 16-byte aligned K: 2 lanes x 16 B per query, 16 queries per load;
 // otherwise 8 lanes x 4 B, 4 queries per load.
 __device__ __forceinline__ uint32_t grp_group_count(const uint32_t* __restrict__ K, uint64_t n,
-                                                    uint32_t gi, uint32_t x2) {
+                                                    uint32_t gi, uint32_t x2, uint64_t strm) {
   const uint32_t lane = lane_id();
   uint32_t res = 0;
   if ((reinterpret_cast<uintptr_t>(K) & 15) == 0) {
@@ -209,7 +210,7 @@ __device__ __forceinline__ uint32_t grp_group_count(const uint32_t* __restrict__
       const uint32_t gj = __shfl_sync(kFull, gi, src);
       const uint32_t xj = __shfl_sync(kFull, x2, src);
       const uint64_t base = (uint64_t)gj * kF1Step + 4 * hf;
-      uint4 v = __ldg(reinterpret_cast<const uint4*>(K + base));  // +16 words of slack
+      uint4 v = ldg_v4_pol(K + base, strm);  // +16 words of slack
       if (base + 4 > n) {  // the level's last group
         if (base + 0 >= n) v.x = 0xFFFFFFFFu;
         if (base + 1 >= n) v.y = 0xFFFFFFFFu;
@@ -249,7 +250,9 @@ __device__ __forceinline__ uint32_t f3_count2(const LvView& L, uint32_t x, uint3
 // position p with (K[p] >> 1) >= x. F3[c3-1] < x <= F3[c3] brackets 8192
 // records; the F2 line below it, the F1 line below that and the 8-record
 // group below that narrow it to p.
-__device__ __noinline__ uint64_t warp_lower_bound(const LvView L, uint32_t x) {
+// kpol: L2 policy of the level-sector load (evict_first where the sector is
+// not read again, evict_normal where a later walk re-reads it).
+__device__ __noinline__ uint64_t warp_lower_bound(const LvView L, uint32_t x, uint64_t kpol) {
   const uint32_t x2 = dbl(x);
   const uint32_t c3 = f3_count2(L, x, x2);
   const bool zero = c3 == 0;  // K[0] >= x
@@ -258,7 +261,7 @@ __device__ __noinline__ uint64_t warp_lower_bound(const LvView L, uint32_t x) {
   const uint32_t l1 = zero ? 0u : c2 - 1;
   const uint32_t c1 = l1 * kFanout + grp_line_count(L.f1, l1, x2);
   const uint32_t g = zero ? 0u : c1 - 1;
-  const uint64_t p = (uint64_t)g * kF1Step + grp_group_count(L.K, L.n, g, x2);
+  const uint64_t p = (uint64_t)g * kF1Step + grp_group_count(L.K, L.n, g, x2, kpol);
   if (x > 0x7FFFFFFFu) return L.n;  // above every original key (R8)
   return zero ? 0ull : p;
 }
@@ -286,21 +289,21 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) lookup_kernel(
     for (int j = 0; j < T.count; ++j) {
       if (__all_sync(kFull, done)) break;
       const LvView L = level_view(T, j, sF3);
-      const uint64_t p = warp_lower_bound(L, x);  // every lane takes part
+      const uint64_t p = warp_lower_bound(L, x, l2_policy_stream());  // every lane takes part
       if (!done && p < L.n) {
-        const uint32_t kk = __ldg(L.K + p);
+        const uint32_t kk = ldg_pol(L.K + p, l2_policy_stream());
         if ((kk >> 1) == x) {
           done = true;
           if (kk & 1u) {  // regular: its value; a tombstone: ⊥
-            v = __ldg(L.V + p);
+            v = ldg_pol(L.V + p, l2_policy_stream());
             f = 1;
           }
         }
       }
     }
-    if (act) {
-      vals_out[i] = v;
-      if (found_out) found_out[i] = f;
+    if (act) {  // outputs are not re-read: streaming stores
+      __stcs(vals_out + i, v);
+      if (found_out) __stcs(reinterpret_cast<char*>(found_out) + i, (char)f);
     }
   }
 }
@@ -348,7 +351,7 @@ __device__ __forceinline__ uint32_t walk_slices(const LevelTable& T, uint64_t* p
         if (first) {  // newest record of key m: run head in the lowest level
           first = false;
           valid = (__ldg(K + p) & 1u) != 0;
-          if (NEED_VAL && valid) val = __ldg(T.vals[j] + p);
+          if (NEED_VAL && valid) val = ldg_pol(T.vals[j] + p, l2_policy_stream());
         }
         // skip the rest of this level's run of key m (stale copies)
         uint32_t nk = kSent;
@@ -411,9 +414,10 @@ __device__ __forceinline__ uint32_t walk_one(const uint32_t* __restrict__ K,
       }
     }
     if (NEED_VAL) {
+      const uint64_t vpol = l2_policy_stream();  // values are read once
       uint32_t vv[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) vv[i] = (valid >> i) & 1u ? __ldg(V + g + i) : 0u;
+      for (int i = 0; i < 8; ++i) vv[i] = (valid >> i) & 1u ? ldg_pol(V + g + i, vpol) : 0u;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         if ((valid >> i) & 1u) {
@@ -434,13 +438,13 @@ __device__ __forceinline__ uint32_t walk_one(const uint32_t* __restrict__ K,
 // cooperative across the warp; empty (pos_j = n_j) when k1 > k2 (R9).
 template <int NL>
 __device__ __forceinline__ void bounds(const LevelTable& T, const uint32_t* sF3, uint32_t a,
-                                       bool empty, uint64_t* pos, int L) {
+                                       bool empty, uint64_t* pos, int L, uint64_t kpol) {
   constexpr int CAP = NL > 0 ? NL : LSM_MAX_LEVELS;
 #pragma unroll
   for (int j = 0; j < CAP; ++j) {
     if (j < L) {
       const LvView V = level_view(T, j, sF3);
-      const uint64_t lo = warp_lower_bound(V, a);  // whole warp
+      const uint64_t lo = warp_lower_bound(V, a, kpol);  // whole warp
       pos[j] = empty ? V.n : lo;
     }
   }
@@ -463,14 +467,14 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) count_kernel(
     const bool act = i < nq;
     const uint32_t a = act ? __ldg(k1 + i) : 1u, z = act ? __ldg(k2 + i) : 0u;
     uint64_t pos[CAP];
-    bounds<NL>(T, sF3, a, a > z, pos, L);
+    bounds<NL>(T, sF3, a, a > z, pos, L, l2_policy_stream());
     uint32_t c;
     if (NL == 1 && (reinterpret_cast<uintptr_t>(T.keys[0]) & 15) == 0)
       c = walk_one<false>(T.keys[0], T.vals[0], T.n[0], pos[0], z,
                           [](uint32_t, uint32_t, uint32_t) {});
     else
       c = walk_slices<NL, false>(T, pos, z, L, [](uint32_t, uint32_t, uint32_t) {});
-    if (act) counts[i] = c;
+    if (act) __stcs(counts + i, c);
   }
 }
 
@@ -547,7 +551,7 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) range_kernel(
     const bool act = i < nq;
     const uint32_t a = act ? __ldg(k1 + i) : 1u, z = act ? __ldg(k2 + i) : 0u;
     uint64_t pos[CAP], pos0[CAP];
-    bounds<NL>(T, sF3, a, a > z, pos, L);
+    bounds<NL>(T, sF3, a, a > z, pos, L, l2_policy_normal());
 #pragma unroll
     for (int j = 0; j < CAP; ++j)
       if (j < L) pos0[j] = pos[j];
@@ -624,7 +628,7 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) order_kernel(
     for (int j = 0; j < CAP; ++j) {
       if (j < L) {
         const LvView V = level_view(T, j, sF3);
-        const uint64_t u0 = warp_lower_bound(V, SUCC ? x : ub_arg(x));  // whole warp
+        const uint64_t u0 = warp_lower_bound(V, SUCC ? x : ub_arg(x), l2_policy_normal());  // whole warp
         if (SUCC) {
           pos[j] = act ? u0 : V.n;
           head[j] = pos[j] < V.n ? (__ldg(V.K + pos[j]) >> 1) : kSent;
@@ -730,7 +734,7 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) range_block_kernel(
       const bool act = i < nq;
       const uint32_t a = act ? __ldg(k1 + i) : 1u, z = act ? __ldg(k2 + i) : 0u;
       uint64_t pos[NL];
-      bounds<NL>(T, sF3, a, a > z, pos, NL);
+      bounds<NL>(T, sF3, a, a > z, pos, NL, l2_policy_normal());
 #pragma unroll
       for (int j = 0; j < NL; ++j) sPos[j * kRBQueries + li] = (uint32_t)pos[j];
       uint32_t c;
@@ -764,7 +768,7 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) range_block_kernel(
     for (int u = 0; u < kRBTasks; ++u) {
       const uint32_t li = u * kQThreads + tid;
       const uint64_t i = q0 + li;
-      if (i < nq) offsets[i] = base + sOff[li];
+      if (i < nq) __stcs(reinterpret_cast<unsigned long long*>(offsets) + i, (unsigned long long)(base + sOff[li]));
     }
     if (blk == nblocks - 1 && tid == 0) offsets[nq] = base + run;
     // ---- phase 2: walk again from the saved positions and write ----
@@ -783,8 +787,8 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) range_block_kernel(
       auto put = [&](uint32_t k, uint32_t key, uint32_t val) {
         const uint64_t o = ob + k;
         if (o < capacity) {
-          keys_out[o] = key;
-          vals_out[o] = val;
+          __stcs(keys_out + o, key);
+          __stcs(vals_out + o, val);
         }
       };
       if (NL == 1 && (reinterpret_cast<uintptr_t>(T.keys[0]) & 15) == 0)

@@ -37,6 +37,8 @@
 //    status bit, tombstone value 0 (R6), placebo padding of a partial batch
 //    (R7), domain check -> placebo + sticky error (R5).
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace gpulsm {
@@ -772,8 +774,466 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_sort_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// MSD + rank mode (default for one-wave batches). The batch
+// is sorted by the total order on (key variable, input position): that order
+// is unique, so no pass has to be stable -- stability (reading R4: the first
+// of equal key variables wins) comes from the explicit position instead.
+//  * msd_scatter_kernel: one fat tile per SM encodes its records (A1), ranks
+//    them by the top digit with shared-memory atomics, takes its slot in each
+//    global bucket with one L2 atomic per digit, waits at a grid barrier for
+//    all counts (every tile is resident: one wave) and writes (key, position)
+//    bucket by bucket from a digit-ordered shared-memory stage.
+//  * bucket_rank_kernel: CTA d loads bucket d, groups it by the next 11 bits
+//    (2048 bins, about two records each at b = 2^20) with shared-memory
+//    atomics, ranks every record inside its bin by counting the bin's records
+//    below it in (key, position) order, and writes the sorted bucket with the
+//    value gathered from the user's array by position (tombstones and
+//    placebos carry 0, R5-R7) and the level's F1.
+// Skew fallbacks: a bin above kBinMax records is sorted by a stable
+// shared-memory LSD on the position then the key; a bucket above kBktCap is
+// regathered in input order from the raw batch and sorted by the chunked LSD
+// of bucket_sort_kernel. Both set the overflow flag, which moves the handle to
+// the 4-pass LSD for later batches.
+// ---------------------------------------------------------------------------
+struct MsdSmem {
+  uint32_t keys[kSortTile];
+  uint32_t pos[kSortTile];
+  uint32_t hist[kRadix];    // tile digit counts (atomic ranks)
+  uint32_t tstart[kRadix];  // tile-local digit starts
+  uint32_t toff[kRadix];    // the tile's slot inside each global bucket
+  uint32_t gdst[kRadix];    // global destination - tile-local start
+  uint32_t scan[kWarps + 1];
+};
+
+__global__ void __launch_bounds__(kSortThreads, 1) msd_scatter_kernel(
+    RawBatch in, uint64_t b, uint32_t* __restrict__ out_keys, uint32_t* __restrict__ out_pos,
+    uint32_t* __restrict__ cnt, uint32_t* __restrict__ cnt_next, uint32_t* __restrict__ bar,
+    uint32_t* __restrict__ bar_next, uint32_t* __restrict__ err, uint32_t* __restrict__ bkt_out) {
+  extern __shared__ __align__(16) uint8_t msd_smem[];
+  MsdSmem& S = *reinterpret_cast<MsdSmem*>(msd_smem);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < kRadix) S.hist[tid] = 0;
+  pdl_wait();
+  pdl_trigger();
+  // the next sort's counters (the previous sort finished: pdl_wait)
+  if (blockIdx.x == 0) {
+    if (tid < kRadix) cnt_next[tid] = 0;
+    if (tid == 0) *bar_next = 0;
+  }
+  __syncthreads();
+  const uint32_t tile = blockIdx.x;
+  const uint64_t tile_base = (uint64_t)tile * kSortTile;
+  const uint32_t tile_n =
+      (uint32_t)((b - tile_base) < (uint64_t)kSortTile ? (b - tile_base) : (uint64_t)kSortTile);
+  const uint32_t wbase = warp * (32 * kSortItems);
+  uint32_t k[kSortItems], rk[kSortItems];
+  {
+    uint32_t op[kSortItems];
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {  // independent loads first
+      const uint64_t p = tile_base + wbase + i * 32 + lane;
+      const bool in_batch = p < in.n;
+      k[i] = in_batch ? __ldg(in.keys + p) : 0u;
+      op[i] = (in_batch && in.mode == kModeMixed) ? (uint32_t)__ldg(in.ops + p) : 0u;
+    }
+    bool any_bad = false;
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+      const uint64_t p = tile_base + wbase + i * 32 + lane;
+      uint32_t key, val;
+      bool bad;
+      encode_loaded(in, p, k[i], 0u, op[i], key, val, bad);
+      k[i] = key;
+      any_bad |= bad;
+    }
+    if (any_bad) atomicOr(err, 1u);
+  }
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i)
+    if (wbase + i * 32 + lane < tile_n) rk[i] = atomicAdd(&S.hist[k[i] >> 24], 1u);
+  __syncthreads();
+  const uint32_t c = tid < kRadix ? S.hist[tid] : 0u;
+  if (tid < kRadix) S.toff[tid] = c ? atomicAdd(cnt + tid, c) : 0u;
+  uint32_t tot;
+  const uint32_t ts = block_exclusive_scan<kSortThreads, uint32_t>(c, S.scan, &tot);
+  if (tid < kRadix) S.tstart[tid] = ts;
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const uint32_t off = wbase + i * 32 + lane;
+    if (off < tile_n) {
+      const uint32_t p = S.tstart[k[i] >> 24] + rk[i];
+      S.keys[p] = k[i];
+      S.pos[p] = (uint32_t)(tile_base + off);
+    }
+  }
+  // grid barrier: every tile has added its counts (all tiles are resident)
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    while (ld_cg(bar) < gridDim.x) __nanosleep(LB_SLEEP);
+    __threadfence();
+  }
+  __syncthreads();
+  const uint32_t total = tid < kRadix ? ld_cg(cnt + tid) : 0u;
+  const uint32_t bstart = block_exclusive_scan<kSortThreads, uint32_t>(total, S.scan, &tot);
+  if (tid < kRadix) {
+    S.gdst[tid] = bstart + S.toff[tid] - S.tstart[tid];
+    if (tile == 0) {
+      bkt_out[tid] = bstart;
+      bkt_out[kRadix + tid] = total;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const uint32_t idx = i * kSortThreads + tid;
+    if (idx < tile_n) {
+      const uint32_t key = S.keys[idx];
+      const uint32_t g = S.gdst[key >> 24] + idx;
+      out_keys[g] = key;
+      out_pos[g] = S.pos[idx];
+    }
+  }
+}
+
+constexpr int kBinBits = 11;
+constexpr int kBins = 1 << kBinBits;
+constexpr int kBinShift = 24 - kBinBits;  // bins = key bits [13, 24)
+constexpr uint32_t kBinMax = 64;           // larger bins: stable LSD fallback
+
+struct RankSmem {
+  uint2 kv[2][kBktCap];  // (key, position)
+  union {
+    struct {
+      uint32_t cnt[kBins];
+      uint32_t start[kBins];
+    } b;
+    LocalScratch<kBktThreads> L;
+  } u;
+  uint32_t scan[kBktThreads / 32 + 1];
+  uint32_t run[kRadix];
+  uint32_t hist[kRadix];
+  uint64_t mb[2];  // fused merge: the run's records with this top digit
+};
+
+// first position p of the sorted run K[0, n) with K[p] >= x (key variables),
+// whole warp: 32-ary search, each round one probe per lane (4 rounds at 2^20)
+__device__ __forceinline__ uint64_t warp_lower_bound_kv(const uint32_t* __restrict__ K, uint64_t n,
+                                                        uint32_t x) {
+  const uint32_t lane = lane_id();
+  uint64_t lo = 0, hi = n;  // answer in [lo, hi]; hi == n or K[hi] >= x
+  while (hi > lo) {
+    const uint64_t len = hi - lo, sz = (len + 31) / 32;
+    const uint64_t q = lo + (uint64_t)lane * sz;
+    const bool below = q < hi && __ldg(K + q) < x;
+    const uint32_t c = __popc(__ballot_sync(kFull, below));  // chunks starting below x
+    if (c == 0) break;                                        // K[lo] >= x
+    const uint64_t nlo = lo + (uint64_t)(c - 1) * sz + 1;
+    hi = min(hi, lo + (uint64_t)c * sz);
+    lo = nlo;
+  }
+  return lo;
+}
+
+// value of the record at input position p with key variable `key` (A1:
+// tombstones, placebos and out-of-domain keys carry 0)
+__device__ __forceinline__ uint32_t enc_val(const RawBatch& in, uint32_t key, uint32_t p) {
+  return ((key & 1u) && in.vals != nullptr) ? __ldg(in.vals + p) : 0u;
+}
+
+// Fused first cascade step (A3): merge the sorted bucket d
+// (size records, newer, first on equal original keys, R1) with the run's
+// records of top digit d; the merged records land at start + a0, where a0 =
+// the run's records below digit d. A is the bucket as (key, position) pairs
+// in shared memory (A_SMEM) or as (key, value) arrays in global memory.
+template <bool A_SMEM>
+__device__ __forceinline__ void fused_merge(const uint2* As, const uint32_t* Ak,
+                                            const uint32_t* Av, uint32_t size, const RawBatch& in,
+                                            const SortMerge& M, uint32_t start, RankSmem& S,
+                                            uint2* stage, uint32_t d) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (warp < 2) {
+    const uint64_t r = (warp == 1 && d == kRadix - 1)
+                           ? M.n
+                           : warp_lower_bound_kv(M.keys, M.n, (d + warp) << 24);
+    if (lane == 0) S.mb[warp] = r;
+  }
+  __syncthreads();
+  const uint64_t a0 = S.mb[0];
+  const uint32_t m0 = (uint32_t)(S.mb[1] - a0);
+  const uint32_t* bk;
+  const uint32_t* bv;
+  if (m0 <= (uint32_t)kBktCap) {  // stage the run's slice in shared memory
+    uint32_t* sk = reinterpret_cast<uint32_t*>(stage);
+    uint32_t* sv = sk + kBktCap;
+    for (uint32_t p = tid; p < m0; p += kBktThreads) {
+      sk[p] = __ldg(M.keys + a0 + p);
+      sv[p] = __ldg(M.vals + a0 + p);
+    }
+    bk = sk;
+    bv = sv;
+    __syncthreads();
+  } else {  // skewed run: merge from global memory
+    bk = M.keys + a0;
+    bv = M.vals + a0;
+  }
+  auto akey = [&](uint32_t i) { return A_SMEM ? As[i].x : Ak[i]; };
+  const uint32_t tot = size + m0;
+  const uint32_t per = (tot + kBktThreads - 1) / kBktThreads;
+  const uint32_t k0 = min(tid * per, tot), k1 = min(k0 + per, tot);
+  // merge path: i = records of A among the first k0 outputs
+  uint32_t lo = k0 > m0 ? k0 - m0 : 0u, hi = min(k0, size);
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if ((akey(mid) >> 1) <= (bk[k0 - mid - 1] >> 1)) lo = mid + 1;
+    else hi = mid;
+  }
+  uint32_t i = lo, j = k0 - lo;
+  const uint64_t gb = start + a0;
+  for (uint32_t k = k0; k < k1; ++k) {
+    const bool takeA = j >= m0 || (i < size && (akey(i) >> 1) <= (bk[j] >> 1));
+    uint32_t key, val;
+    if (takeA) {
+      if (A_SMEM) {
+        const uint2 kv = As[i];
+        key = kv.x;
+        val = enc_val(in, kv.x, kv.y);
+      } else {
+        key = Ak[i];
+        val = Av[i];
+      }
+      ++i;
+    } else {
+      key = bk[j];
+      val = bv[j];
+      ++j;
+    }
+    const uint64_t g = gb + k;
+    M.out_keys[g] = key;
+    M.out_vals[g] = val;
+    if (M.out_f1 != nullptr && (g & (kF1Step - 1)) == 0) M.out_f1[g / kF1Step] = key;
+  }
+}
+
+__global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
+    const uint32_t* __restrict__ bkt, uint32_t* __restrict__ ak, uint32_t* __restrict__ ap,
+    RawBatch in, uint64_t b, uint32_t* __restrict__ tk, uint32_t* __restrict__ tv,
+    uint32_t* __restrict__ out_keys, uint32_t* __restrict__ out_vals, uint32_t* __restrict__ out_f1,
+    uint32_t* __restrict__ overflow, SortMerge M) {
+  extern __shared__ __align__(16) uint8_t rank_smem[];
+  RankSmem& S = *reinterpret_cast<RankSmem*>(rank_smem);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  pdl_wait();
+  pdl_trigger();
+  const uint32_t d = blockIdx.x;
+  const uint32_t start = bkt[d], size = bkt[kRadix + d];
+  if (size == 0 && M.keys == nullptr) return;
+  if (size > (uint32_t)kBktCap) {
+    // oversized bucket (skewed keys): regather it in input order from the raw
+    // batch (stable compaction), then the chunked LSD of the lower 3 digits
+    if (tid == 0) atomicOr(overflow, 1u);
+    uint32_t cursor = 0;
+    for (uint64_t c0 = 0; c0 < b; c0 += kBktThreads * 8) {
+      uint32_t key[8], val[8];
+      bool sel[8];
+      uint32_t mine = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint64_t p = c0 + (uint64_t)(warp * 8 + i) * 32 + lane;  // warp-contiguous
+        sel[i] = false;
+        key[i] = 0;
+        val[i] = 0;
+        if (p < b) {
+          const bool inb = p < in.n;
+          const uint32_t rk = inb ? __ldg(in.keys + p) : 0u;
+          const uint32_t rv = (inb && in.vals) ? __ldg(in.vals + p) : 0u;
+          const uint32_t op = (inb && in.mode == kModeMixed) ? (uint32_t)__ldg(in.ops + p) : 0u;
+          bool bad;
+          encode_loaded(in, p, rk, rv, op, key[i], val[i], bad);
+          sel[i] = (key[i] >> 24) == d;
+        }
+        mine += __popc(__ballot_sync(kFull, sel[i]));
+      }
+      if (lane == 0) S.scan[warp] = mine;
+      __syncthreads();
+      uint32_t before = cursor;
+      for (int w = 0; w < warp; ++w) before += S.scan[w];
+      uint32_t all = 0;
+      for (int w = 0; w < kBktThreads / 32; ++w) all += S.scan[w];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t m = __ballot_sync(kFull, sel[i]);
+        if (sel[i]) {
+          const uint32_t g = start + before + __popc(m & lanemask_lt());
+          ak[g] = key[i];
+          ap[g] = val[i];
+        }
+        before += __popc(m);
+      }
+      cursor += all;
+      __syncthreads();
+    }
+    __threadfence_block();
+    __syncthreads();
+    uint32_t* fk = reinterpret_cast<uint32_t*>(S.kv[0]);  // 2 * kBktCap words
+    uint32_t* fv = fk + kBktCap;
+    const uint32_t* srck = ak + start;
+    const uint32_t* srcv = ap + start;
+    for (int pass = 0; pass < kPasses - 1; ++pass) {
+      const int shift = pass * kRadixBits;
+      uint32_t* dk = (pass == kPasses - 2 ? out_keys : (pass & 1 ? ak : tk)) + start;
+      uint32_t* dv = (pass == kPasses - 2 ? out_vals : (pass & 1 ? ap : tv)) + start;
+      for (int i = tid; i < kRadix; i += kBktThreads) S.hist[i] = 0;
+      __syncthreads();
+      for (uint32_t p = tid; p < size; p += kBktThreads)
+        atomicAdd(&S.hist[(srck[p] >> shift) & (kRadix - 1)], 1u);
+      __syncthreads();
+      uint32_t tot;
+      const uint32_t hv = tid < kRadix ? S.hist[tid] : 0u;
+      const uint32_t ex = block_exclusive_scan<kBktThreads, uint32_t>(hv, S.scan, &tot);
+      if (tid < kRadix) S.run[tid] = ex;
+      __syncthreads();
+      for (uint32_t c0 = 0; c0 < size; c0 += kBktCap) {
+        const uint32_t nc = min((uint32_t)kBktCap, size - c0);
+        local_subpass<kBktThreads, kBktItems>(srck + c0, srcv + c0, nc, fk, fv, shift, S.u.L,
+                                              nullptr);
+        for (uint32_t p = tid; p < nc; p += kBktThreads) {
+          const uint32_t key = fk[p];
+          const uint32_t dg = (key >> shift) & (kRadix - 1);
+          const uint32_t g = S.run[dg] + (p - S.u.L.tstart[dg]);
+          dk[g] = key;
+          dv[g] = fv[p];
+        }
+        __syncthreads();
+        if (tid < kRadix) S.run[tid] += S.u.L.cnt[tid];
+        __syncthreads();
+      }
+      __threadfence_block();
+      srck = dk;
+      srcv = dv;
+      __syncthreads();
+    }
+    if (out_f1 != nullptr && M.keys == nullptr) {
+      __syncthreads();
+      for (uint32_t p = tid; p < size; p += kBktThreads) {
+        const uint32_t g = start + p;
+        if ((g & (kF1Step - 1)) == 0) out_f1[g / kF1Step] = out_keys[g];
+      }
+    }
+    if (M.keys != nullptr) {
+      __threadfence_block();
+      __syncthreads();
+      fused_merge<false>(nullptr, out_keys + start, out_vals + start, size, in, M, start, S,
+                         S.kv[0], d);
+    }
+    return;
+  }
+
+  // ---- load (key, position); bin counts with shared-memory atomics ----
+  for (int i = tid; i < kBins; i += kBktThreads) S.u.b.cnt[i] = 0;
+  __syncthreads();
+  uint32_t rk[kBktItems];
+#pragma unroll
+  for (int i = 0; i < kBktItems; ++i) {
+    const uint32_t p = i * kBktThreads + tid;
+    if (p < size) {
+      const uint2 kv = make_uint2(__ldg(ak + start + p), __ldg(ap + start + p));
+      S.kv[0][p] = kv;
+      rk[i] = atomicAdd(&S.u.b.cnt[(kv.x >> kBinShift) & (kBins - 1)], 1u);
+    }
+  }
+  __syncthreads();
+  // ---- bin starts: each thread scans kBins / kBktThreads consecutive bins ----
+  constexpr int kPer = kBins / kBktThreads;
+  uint32_t c[kPer], sum = 0, mx = 0;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    c[j] = S.u.b.cnt[tid * kPer + j];
+    sum += c[j];
+    mx = max(mx, c[j]);
+  }
+  uint32_t tot;
+  uint32_t run = block_exclusive_scan<kBktThreads, uint32_t>(sum, S.scan, &tot);
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    S.u.b.start[tid * kPer + j] = run;
+    run += c[j];
+  }
+  const bool skew = __syncthreads_or(mx > kBinMax);
+  int res = 0;
+  if (!skew) {
+    // group by bin (any order inside a bin) ...
+#pragma unroll
+    for (int i = 0; i < kBktItems; ++i) {
+      const uint32_t p = i * kBktThreads + tid;
+      if (p < size) {
+        const uint2 kv = S.kv[0][p];
+        S.kv[1][S.u.b.start[(kv.x >> kBinShift) & (kBins - 1)] + rk[i]] = kv;
+      }
+    }
+    __syncthreads();
+    // ... then rank inside the bin by counting in (key, position) order
+#pragma unroll
+    for (int i = 0; i < kBktItems; ++i) {
+      const uint32_t p = i * kBktThreads + tid;
+      if (p < size) {
+        const uint2 kv = S.kv[1][p];
+        const uint32_t bin = (kv.x >> kBinShift) & (kBins - 1);
+        const uint32_t lo = S.u.b.start[bin], hi = lo + S.u.b.cnt[bin];
+        uint32_t r = 0;
+        for (uint32_t j = lo; j < hi; ++j) {
+          const uint2 o = S.kv[1][j];
+          r += (o.x < kv.x) || (o.x == kv.x && o.y < kv.y);
+        }
+        S.kv[0][lo + r] = kv;
+      }
+    }
+    __syncthreads();
+  } else {
+    // skewed bin: stable LSD on the position, then on the key (3 digits each;
+    // one-wave batches have positions < 2^24)
+    if (tid == 0) atomicOr(overflow, 1u);
+    for (uint32_t p = tid; p < size; p += kBktThreads) {
+      const uint2 kv = S.kv[0][p];
+      S.kv[0][p] = make_uint2(kv.y, kv.x);
+    }
+    __syncthreads();
+    for (int pass = 0; pass < 3; ++pass) {
+      local_subpass_kv<kBktThreads, kBktItems>(S.kv[res], size, S.kv[res ^ 1], pass * kRadixBits,
+                                               S.u.L);
+      res ^= 1;
+    }
+    for (uint32_t p = tid; p < size; p += kBktThreads) {
+      const uint2 kv = S.kv[res][p];
+      S.kv[res][p] = make_uint2(kv.y, kv.x);
+    }
+    __syncthreads();
+    for (int pass = 0; pass < 3; ++pass) {
+      local_subpass_kv<kBktThreads, kBktItems>(S.kv[res], size, S.kv[res ^ 1], pass * kRadixBits,
+                                               S.u.L);
+      res ^= 1;
+    }
+  }
+  if (M.keys == nullptr) {
+    // ---- write the sorted bucket: key, gathered value, F1 ----
+    for (uint32_t p = tid; p < size; p += kBktThreads) {
+      const uint2 kv = S.kv[res][p];
+      const uint32_t g = start + p;
+      out_keys[g] = kv.x;
+      out_vals[g] = enc_val(in, kv.x, kv.y);
+      if (out_f1 != nullptr && (g & (kF1Step - 1)) == 0) out_f1[g / kF1Step] = kv.x;
+    }
+    return;
+  }
+  fused_merge<true>(S.kv[res], nullptr, nullptr, size, in, M, start, S, S.kv[res ^ 1], d);
+}
+
 int g_sms = 0;
 bool g_attr = false;
+int g_sort_mode = -1;  // GPULSM_SORT: 0 = MSD + stable local LSD (previous), 1 = MSD + rank
 
 }  // namespace
 
@@ -797,6 +1257,14 @@ static cudaError_t sort_attrs() {
     e = cudaFuncSetAttribute(bucket_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(BktSmem));
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(msd_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(MsdSmem));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(bucket_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(RankSmem));
+    if (e != cudaSuccess) return e;
+    const char* m = getenv("GPULSM_SORT");
+    g_sort_mode = (m != nullptr && m[0] == '0') ? 0 : 1;
     g_attr = true;
   }
   return cudaSuccess;
@@ -805,7 +1273,9 @@ static cudaError_t sort_attrs() {
 cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals,
                               const uint8_t* ops, int mode, uint64_t n, uint64_t b,
                               SortScratch& S, uint32_t* out_keys, uint32_t* out_vals,
-                              uint32_t* out_f1, cudaStream_t s, const LaunchHooks& hk) {
+                              uint32_t* out_f1, cudaStream_t s, const LaunchHooks& hk,
+                              const SortMerge* merge, bool* fused) {
+  if (fused) *fused = false;
   {
     cudaError_t e = sort_attrs();
     if (e != cudaSuccess) return e;
@@ -839,6 +1309,30 @@ cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals
   // (2) MSD + local: pass A scatters by the top digit into 256 stable
   //     buckets, pass B sorts each bucket by the other three digits in
   //     shared memory (one CTA per bucket)
+  if (!use_ctr && !S.lsd_only && g_sort_mode == 1) {
+    uint32_t* cnt = S.msd_cnt + (S.msd_parity ? kRadix : 0);
+    uint32_t* cnt_next = S.msd_cnt + (S.msd_parity ? 0 : kRadix);
+    uint32_t* bar = S.msd_bar + S.msd_parity;
+    uint32_t* bar_next = S.msd_bar + (S.msd_parity ^ 1);
+    S.msd_parity ^= 1;
+    hk.begin(hk.ctx, LSM_K_SORT_PASS, s);
+    e = launch_pdl(msd_scatter_kernel, (unsigned)tiles, kSortThreads, sizeof(MsdSmem), s, in, b,
+                   S.tmp_keys[0], S.tmp_vals[0], cnt, cnt_next, bar, bar_next, S.err, S.bkt);
+    // bytes: keys + ops read (5 B), (key, position) written (8 B)
+    hk.end(hk.ctx, LSM_K_SORT_PASS, (double)b * 13.0, s, 1);
+    if (e != cudaSuccess) return e;
+    SortMerge M{};
+    if (merge != nullptr && merge->n + b <= 0xFFFFFFFFull) M = *merge;
+    hk.begin(hk.ctx, LSM_K_SORT_PASS, s);
+    e = launch_pdl(bucket_rank_kernel, (unsigned)kRadix, kBktThreads, sizeof(RankSmem), s,
+                   (const uint32_t*)S.bkt, S.tmp_keys[0], S.tmp_vals[0], in, b, S.tmp_keys[1],
+                   S.tmp_vals[1], out_keys, out_vals, out_f1, S.overflow_dev, M);
+    // bytes: (key, position) read (8 B), value gathered (4 B), (key, value)
+    // written (8 B); fused: + the run read (8 B each) and written again
+    hk.end(hk.ctx, LSM_K_SORT_PASS, (double)b * 20.0 + (double)M.n * 16.0, s, 1);
+    if (fused) *fused = M.keys != nullptr;
+    return e;
+  }
   if (!use_ctr && !S.lsd_only) {
     hk.begin(hk.ctx, LSM_K_SORT_PASS, s);
     e = launch_pdl(onesweep_pass_kernel<true>, (unsigned)tiles, kSortThreads, sizeof(PassSmem), s,

@@ -182,6 +182,41 @@ def test_skewed_keys_bucket_overflow():
     _run_schedule(50_000, 5, 123, frac4=1, alphabet=3000, nlook=3000, nrange=300)
 
 
+def _run_custom_keys(b, nbatch, seed, keyfn):
+    """Mixed batches whose keys are keyfn(h) of the seeded hash stream (75%
+    insert / 25% delete); levels vs S1 and queries vs O1 after every batch."""
+    g = GpuAdapter(b)
+    s1 = oracle.ShadowLSM(b)
+    o1 = oracle.OracleDict(b)
+    for j in range(nbatch):
+        idx = np.arange(j * b, (j + 1) * b, dtype=np.uint64)
+        k = keyfn(synth.h(seed, 0, idx), synth.h(seed, 5, idx)).astype(np.uint32)
+        v = idx.astype(np.uint32)
+        d = ((synth.h(seed, 1, idx) % np.uint64(4)) == 0).astype(np.uint8)
+        g.update(k, v, d)
+        s1.update(k, v, d)
+        o1.apply_batch(k, v, d)
+        assert_levels_equal(g, s1, f"custom b={b} batch {j}")
+    q = k[: min(b, 5000)].copy()
+    k1 = np.sort(k[:1000])
+    k2 = k1 + np.uint32(1 << 20)
+    assert_queries_equal(g, o1, q, k1, k2, "custom keys")
+
+
+def test_sort_duplicate_keys_position_tiebreak():
+    # 5000 distinct keys spread over the domain, b = 50,000: every key occurs
+    # about ten times per batch (inserts and deletes), so the MSD + rank sort
+    # must order equal key variables by input position (R4: first wins)
+    _run_custom_keys(50_000, 3, 31, lambda h, h2: (h % np.uint64(5000)) * np.uint64(429_000))
+
+
+def test_sort_skewed_bin_fallback():
+    # every key of a top-digit bucket falls into one 11-bit bin (low key bits
+    # < 200): bins far above kBinMax take the stable shared-memory fallback
+    _run_custom_keys(30_000, 3, 32,
+                     lambda h, h2: ((h % np.uint64(256)) << np.uint64(23)) | (h2 % np.uint64(200)))
+
+
 def test_one_wave_boundary_sort():
     # exactly 148 tiles (largest one-wave batch) and one record more
     for b in (148 * 7168, 148 * 7168 + 1):
