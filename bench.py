@@ -301,10 +301,26 @@ def run_native(args):
             traffic = tr[dom].get("dram_bytes_per_launch")
             traffic_src = f"profiles/ncu_traffic.json ({tr[dom].get('kernel')}, {tr[dom].get('rep')})"
     alg_per_launch = prof[dom]["alg_bytes"] / max(prof[dom]["launches"], 1)
+    # what the kernel's DRAM actually moved per launch (ncu) over its live
+    # event time, and -- for the random-access classes -- the rate of random
+    # 128-byte line fills against the ceiling measured by scripts/rand_probe.cu
+    dram_live = None
+    if traffic:
+        t_live = prof[dom]["ms"] / max(prof[dom]["launches"], 1) * 1e-3
+        dram_live = {"GBps": traffic / t_live / 1e9, "frac": traffic / t_live / 1e9 / peak}
+        rp = os.path.join(ROOT, "profiles", "rand_probe.json")
+        if dom in ("lookup", "count", "range") and os.path.exists(rp):
+            with open(rp) as f:
+                ceil = json.load(f)
+            lines = traffic / ceil["bytes_per_random_read"] / t_live
+            dram_live["random_lines_per_s"] = lines
+            dram_live["random_line_ceiling_per_s"] = ceil["random_reads_per_s"]
+            dram_live["frac_of_random_ceiling"] = lines / ceil["random_reads_per_s"]
     roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak,
                 "peak_source": peak_src, "unit": "GB/s", "frac": ach / peak,
                 "traffic": traffic, "traffic_source": traffic_src,
                 "alg_bytes_per_launch": alg_per_launch,
+                "dram_live": dram_live,
                 "timing": "per-launch CUDA events on the launching stream over K more identical "
                           "steps right after the timed ones (the timed steps run without them: "
                           "per-launch events split programmatic dependent launch)",

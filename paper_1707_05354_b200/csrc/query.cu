@@ -701,7 +701,10 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) order_kernel(
 // from the saved positions while the key sectors are still L2-resident and
 // writes the pairs. One look-back per 1024 queries, no position array in
 // global memory, keys read from DRAM once.
-constexpr int kRBTasks = 2;                       // 32-query tasks per warp per block
+#ifndef RB_TASKS
+#define RB_TASKS 2
+#endif
+constexpr int kRBTasks = RB_TASKS;                // 32-query tasks per warp per block
 constexpr int kRBQueries = kQThreads * kRBTasks;  // 1024
 
 template <int NL>

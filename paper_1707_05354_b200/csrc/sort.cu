@@ -947,11 +947,15 @@ __device__ __forceinline__ uint32_t enc_val(const RawBatch& in, uint32_t key, ui
 // Fused first cascade step (A3): merge the sorted bucket d
 // (size records, newer, first on equal original keys, R1) with the run's
 // records of top digit d; the merged records land at start + a0, where a0 =
-// the run's records below digit d. A is the bucket as (key, position) pairs
-// in shared memory (A_SMEM) or as (key, value) arrays in global memory.
+// the run's records below digit d. Merge by ranks: an A record's output
+// position is its index plus the B records with a smaller original key, a B
+// record's is its index plus the A records with an original key <= its own
+// (binary searches in shared memory; a warp's stores stay nearly contiguous).
+// A is the bucket as (key, value) pairs in shared memory (A_SMEM) or as
+// (key, value) arrays in global memory (oversized bucket).
 template <bool A_SMEM>
 __device__ __forceinline__ void fused_merge(const uint2* As, const uint32_t* Ak,
-                                            const uint32_t* Av, uint32_t size, const RawBatch& in,
+                                            const uint32_t* Av, uint32_t size,
                                             const SortMerge& M, uint32_t start, RankSmem& S,
                                             uint2* stage, uint32_t d) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -975,46 +979,45 @@ __device__ __forceinline__ void fused_merge(const uint2* As, const uint32_t* Ak,
     }
     bk = sk;
     bv = sv;
-    __syncthreads();
   } else {  // skewed run: merge from global memory
     bk = M.keys + a0;
     bv = M.vals + a0;
   }
+  __syncthreads();
   auto akey = [&](uint32_t i) { return A_SMEM ? As[i].x : Ak[i]; };
-  const uint32_t tot = size + m0;
-  const uint32_t per = (tot + kBktThreads - 1) / kBktThreads;
-  const uint32_t k0 = min(tid * per, tot), k1 = min(k0 + per, tot);
-  // merge path: i = records of A among the first k0 outputs
-  uint32_t lo = k0 > m0 ? k0 - m0 : 0u, hi = min(k0, size);
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if ((akey(mid) >> 1) <= (bk[k0 - mid - 1] >> 1)) lo = mid + 1;
-    else hi = mid;
-  }
-  uint32_t i = lo, j = k0 - lo;
   const uint64_t gb = start + a0;
-  for (uint32_t k = k0; k < k1; ++k) {
-    const bool takeA = j >= m0 || (i < size && (akey(i) >> 1) <= (bk[j] >> 1));
-    uint32_t key, val;
-    if (takeA) {
-      if (A_SMEM) {
-        const uint2 kv = As[i];
-        key = kv.x;
-        val = enc_val(in, kv.x, kv.y);
-      } else {
-        key = Ak[i];
-        val = Av[i];
-      }
-      ++i;
-    } else {
-      key = bk[j];
-      val = bv[j];
-      ++j;
-    }
-    const uint64_t g = gb + k;
+  auto put = [&](uint64_t g, uint32_t key, uint32_t val) {
     M.out_keys[g] = key;
     M.out_vals[g] = val;
     if (M.out_f1 != nullptr && (g & (kF1Step - 1)) == 0) M.out_f1[g / kF1Step] = key;
+  };
+  for (uint32_t i = tid; i < size; i += kBktThreads) {  // A: + #B with orig < x
+    const uint32_t key = akey(i), x = key >> 1;
+    uint32_t lo = 0, n = m0;
+    while (n > 0) {
+      const uint32_t h = n >> 1;
+      if ((bk[lo + h] >> 1) < x) {
+        lo += h + 1;
+        n -= h + 1;
+      } else {
+        n = h;
+      }
+    }
+    put(gb + i + lo, key, A_SMEM ? As[i].y : Av[i]);
+  }
+  for (uint32_t j = tid; j < m0; j += kBktThreads) {  // B: + #A with orig <= y
+    const uint32_t key = bk[j], y = key >> 1;
+    uint32_t lo = 0, n = size;
+    while (n > 0) {
+      const uint32_t h = n >> 1;
+      if ((akey(lo + h) >> 1) <= y) {
+        lo += h + 1;
+        n -= h + 1;
+      } else {
+        n = h;
+      }
+    }
+    put(gb + j + lo, key, bv[j]);
   }
 }
 
@@ -1126,7 +1129,7 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
     if (M.keys != nullptr) {
       __threadfence_block();
       __syncthreads();
-      fused_merge<false>(nullptr, out_keys + start, out_vals + start, size, in, M, start, S,
+      fused_merge<false>(nullptr, out_keys + start, out_vals + start, size, M, start, S,
                          S.kv[0], d);
     }
     return;
@@ -1217,18 +1220,39 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
       res ^= 1;
     }
   }
+  // ---- values: gather by position, all loads of a thread in flight at once
+  //      (a dependent gather per store serialised the write loop) ----
+  {
+    uint32_t v[kBktItems];
+#pragma unroll
+    for (int i = 0; i < kBktItems; ++i) {
+      const uint32_t p = i * kBktThreads + tid;
+      v[i] = 0;
+      if (p < size) {
+        const uint2 kv = S.kv[res][p];
+        v[i] = enc_val(in, kv.x, kv.y);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kBktItems; ++i) {
+      const uint32_t p = i * kBktThreads + tid;
+      if (p < size) S.kv[res][p].y = v[i];
+    }
+  }
   if (M.keys == nullptr) {
-    // ---- write the sorted bucket: key, gathered value, F1 ----
+    __syncthreads();
+    // ---- write the sorted bucket (key, value) and its F1 ----
+#pragma unroll 4
     for (uint32_t p = tid; p < size; p += kBktThreads) {
       const uint2 kv = S.kv[res][p];
       const uint32_t g = start + p;
       out_keys[g] = kv.x;
-      out_vals[g] = enc_val(in, kv.x, kv.y);
+      out_vals[g] = kv.y;
       if (out_f1 != nullptr && (g & (kF1Step - 1)) == 0) out_f1[g / kF1Step] = kv.x;
     }
     return;
   }
-  fused_merge<true>(S.kv[res], nullptr, nullptr, size, in, M, start, S, S.kv[res ^ 1], d);
+  fused_merge<true>(S.kv[res], nullptr, nullptr, size, M, start, S, S.kv[res ^ 1], d);
 }
 
 int g_sms = 0;
