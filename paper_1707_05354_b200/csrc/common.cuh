@@ -305,6 +305,7 @@ cudaError_t launch_sort_segments(const uint32_t* raw_keys, const uint32_t* raw_v
 // (keys, vals, n) -- level 0 -- straight into (out_keys, out_vals) of
 // n + b records, with F1 into out_f1 when not null. *fused reports whether
 // the sort took this path (otherwise the plain sorted batch was written).
+uint64_t sort_tmp_words(uint64_t b);  // words of each sort ping-pong buffer
 struct SortMerge {
   const uint32_t* keys;
   const uint32_t* vals;

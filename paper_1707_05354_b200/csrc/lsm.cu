@@ -224,9 +224,9 @@ cudaError_t ensure_sort_scratch(lsm* h, cudaStream_t s) {
     h->sort.lsd_only = false;
     h->sort.tiles_cap = sort_tiles(h->b);
     for (int k = 0; k < 2; ++k) {
-      e = pool_alloc(h, (void**)&h->sort.tmp_keys[k], h->b * 4, s);
+      e = pool_alloc(h, (void**)&h->sort.tmp_keys[k], sort_tmp_words(h->b) * 4, s);
       if (e != cudaSuccess) return e;
-      e = pool_alloc(h, (void**)&h->sort.tmp_vals[k], h->b * 4, s);
+      e = pool_alloc(h, (void**)&h->sort.tmp_vals[k], sort_tmp_words(h->b) * 4, s);
       if (e != cudaSuccess) return e;
     }
   }
@@ -271,9 +271,9 @@ cudaError_t ensure_bulk_scratch(lsm* h, uint64_t cap, cudaStream_t s) {
   B.lsd_only = h->sort.lsd_only;
   B.tiles_cap = sort_tiles(cap);
   for (int k = 0; k < 2; ++k) {
-    e = pool_alloc(h, (void**)&B.tmp_keys[k], cap * 4, s);
+    e = pool_alloc(h, (void**)&B.tmp_keys[k], sort_tmp_words(cap) * 4, s);
     if (e != cudaSuccess) return e;
-    e = pool_alloc(h, (void**)&B.tmp_vals[k], cap * 4, s);
+    e = pool_alloc(h, (void**)&B.tmp_vals[k], sort_tmp_words(cap) * 4, s);
     if (e != cudaSuccess) return e;
   }
   h->bulk_cap = cap;

@@ -781,10 +781,11 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_sort_kernel(
 // of equal key variables wins) comes from the explicit position instead.
 //  * msd_scatter_kernel: one fat tile per SM encodes its records (A1), ranks
 //    them by the top digit with shared-memory atomics, takes its slot in each
-//    global bucket with one L2 atomic per digit, waits at a grid barrier for
-//    all counts (every tile is resident: one wave) and writes (key, position)
-//    bucket by bucket from a digit-ordered shared-memory stage.
-//  * bucket_rank_kernel: CTA d loads bucket d, groups it by the next 11 bits
+//    bucket with one L2 atomic per digit and writes (key, position) from a
+//    digit-ordered shared-memory stage into the bucket's fixed-capacity
+//    region (kBktCap records per digit). No tile waits for another.
+//  * bucket_rank_kernel: CTA d finds its output start (the counts of the
+//    buckets below d), loads bucket d, groups it by the next 11 bits
 //    (2048 bins, about two records each at b = 2^20) with shared-memory
 //    atomics, ranks every record inside its bin by counting the bin's records
 //    below it in (key, position) order, and writes the sorted bucket with the
@@ -808,8 +809,7 @@ struct MsdSmem {
 
 __global__ void __launch_bounds__(kSortThreads, 1) msd_scatter_kernel(
     RawBatch in, uint64_t b, uint32_t* __restrict__ out_keys, uint32_t* __restrict__ out_pos,
-    uint32_t* __restrict__ cnt, uint32_t* __restrict__ cnt_next, uint32_t* __restrict__ bar,
-    uint32_t* __restrict__ bar_next, uint32_t* __restrict__ err, uint32_t* __restrict__ bkt_out) {
+    uint32_t* __restrict__ cnt, uint32_t* __restrict__ cnt_next, uint32_t* __restrict__ err) {
   extern __shared__ __align__(16) uint8_t msd_smem[];
   MsdSmem& S = *reinterpret_cast<MsdSmem*>(msd_smem);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -817,16 +817,23 @@ __global__ void __launch_bounds__(kSortThreads, 1) msd_scatter_kernel(
   pdl_wait();
   pdl_trigger();
   // the next sort's counters (the previous sort finished: pdl_wait)
-  if (blockIdx.x == 0) {
-    if (tid < kRadix) cnt_next[tid] = 0;
-    if (tid == 0) *bar_next = 0;
-  }
+  if (blockIdx.x == 0 && tid < kRadix) cnt_next[tid] = 0;
   __syncthreads();
   const uint32_t tile = blockIdx.x;
   const uint64_t tile_base = (uint64_t)tile * kSortTile;
   const uint32_t tile_n =
       (uint32_t)((b - tile_base) < (uint64_t)kSortTile ? (b - tile_base) : (uint64_t)kSortTile);
   const uint32_t wbase = warp * (32 * kSortItems);
+  // the values are gathered by position in the bucket pass: pull this tile's
+  // range into L2 now (one bulk prefetch; random 4-byte gathers from DRAM
+  // would each cost a 128-byte line fill and a full miss latency)
+  if (tid == 0 && in.vals != nullptr && tile_base < in.n) {
+    const uint64_t e = min(in.n, tile_base + kSortTile);
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(in.vals + tile_base) & ~(uintptr_t)15;
+    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(in.vals + e) + 15) & ~(uintptr_t)15;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0))
+                 : "memory");
+  }
   uint32_t k[kSortItems], rk[kSortItems];
   {
     uint32_t op[kSortItems];
@@ -868,33 +875,23 @@ __global__ void __launch_bounds__(kSortThreads, 1) msd_scatter_kernel(
       S.pos[p] = (uint32_t)(tile_base + off);
     }
   }
-  // grid barrier: every tile has added its counts (all tiles are resident)
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    atomicAdd(bar, 1u);
-    while (ld_cg(bar) < gridDim.x) __nanosleep(LB_SLEEP);
-    __threadfence();
-  }
-  __syncthreads();
-  const uint32_t total = tid < kRadix ? ld_cg(cnt + tid) : 0u;
-  const uint32_t bstart = block_exclusive_scan<kSortThreads, uint32_t>(total, S.scan, &tot);
-  if (tid < kRadix) {
-    S.gdst[tid] = bstart + S.toff[tid] - S.tstart[tid];
-    if (tile == 0) {
-      bkt_out[tid] = bstart;
-      bkt_out[kRadix + tid] = total;
-    }
-  }
+  // bucket d owns the fixed region [d * kBktCap, (d + 1) * kBktCap) of the
+  // output: the tile's records of digit d go to its slot there. No tile waits
+  // for another. Records past the region's end are dropped: that bucket is
+  // oversized, and the bucket pass regathers it from the raw batch.
+  if (tid < kRadix) S.gdst[tid] = tid * (uint32_t)kBktCap + S.toff[tid] - S.tstart[tid];
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const uint32_t idx = i * kSortThreads + tid;
     if (idx < tile_n) {
       const uint32_t key = S.keys[idx];
-      const uint32_t g = S.gdst[key >> 24] + idx;
-      out_keys[g] = key;
-      out_pos[g] = S.pos[idx];
+      const uint32_t d = key >> 24;
+      const uint32_t g = S.gdst[d] + idx;
+      if (g < (d + 1) * (uint32_t)kBktCap) {
+        out_keys[g] = key;
+        out_pos[g] = S.pos[idx];
+      }
     }
   }
 }
@@ -917,6 +914,7 @@ struct RankSmem {
   uint32_t run[kRadix];
   uint32_t hist[kRadix];
   uint64_t mb[2];  // fused merge: the run's records with this top digit
+  uint32_t start_d, size_d;
 };
 
 // first position p of the sorted run K[0, n) with K[p] >= x (key variables),
@@ -1022,7 +1020,7 @@ __device__ __forceinline__ void fused_merge(const uint2* As, const uint32_t* Ak,
 }
 
 __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
-    const uint32_t* __restrict__ bkt, uint32_t* __restrict__ ak, uint32_t* __restrict__ ap,
+    const uint32_t* __restrict__ cnt, uint32_t* __restrict__ ak, uint32_t* __restrict__ ap,
     RawBatch in, uint64_t b, uint32_t* __restrict__ tk, uint32_t* __restrict__ tv,
     uint32_t* __restrict__ out_keys, uint32_t* __restrict__ out_vals, uint32_t* __restrict__ out_f1,
     uint32_t* __restrict__ overflow, SortMerge M) {
@@ -1032,11 +1030,25 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
   pdl_wait();
   pdl_trigger();
   const uint32_t d = blockIdx.x;
-  const uint32_t start = bkt[d], size = bkt[kRadix + d];
+  {  // output start = records in the buckets below d
+    const uint32_t c = tid < kRadix ? __ldg(cnt + tid) : 0u;
+    uint32_t tot;
+    const uint32_t ex = block_exclusive_scan<kBktThreads, uint32_t>(c, S.scan, &tot);
+    if (tid == (int)d) {
+      S.start_d = ex;
+      S.size_d = c;
+    }
+    __syncthreads();
+  }
+  const uint32_t start = S.start_d, size = S.size_d;
+  ak += (uint64_t)d * kBktCap;  // the bucket's region (msd_scatter_kernel)
+  ap += (uint64_t)d * kBktCap;
   if (size == 0 && M.keys == nullptr) return;
   if (size > (uint32_t)kBktCap) {
-    // oversized bucket (skewed keys): regather it in input order from the raw
-    // batch (stable compaction), then the chunked LSD of the lower 3 digits
+    // oversized bucket (skewed keys): its region holds only the first
+    // kBktCap records, so regather it in input order from the raw batch
+    // (stable compaction) into tk/tv[start ..), then the chunked LSD of the
+    // lower 3 digits (tk -> out -> tk -> out; both ranges are this bucket's)
     if (tid == 0) atomicOr(overflow, 1u);
     uint32_t cursor = 0;
     for (uint64_t c0 = 0; c0 < b; c0 += kBktThreads * 8) {
@@ -1071,8 +1083,8 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
         const uint32_t m = __ballot_sync(kFull, sel[i]);
         if (sel[i]) {
           const uint32_t g = start + before + __popc(m & lanemask_lt());
-          ak[g] = key[i];
-          ap[g] = val[i];
+          tk[g] = key[i];
+          tv[g] = val[i];
         }
         before += __popc(m);
       }
@@ -1083,12 +1095,12 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
     __syncthreads();
     uint32_t* fk = reinterpret_cast<uint32_t*>(S.kv[0]);  // 2 * kBktCap words
     uint32_t* fv = fk + kBktCap;
-    const uint32_t* srck = ak + start;
-    const uint32_t* srcv = ap + start;
+    const uint32_t* srck = tk + start;
+    const uint32_t* srcv = tv + start;
     for (int pass = 0; pass < kPasses - 1; ++pass) {
       const int shift = pass * kRadixBits;
-      uint32_t* dk = (pass == kPasses - 2 ? out_keys : (pass & 1 ? ak : tk)) + start;
-      uint32_t* dv = (pass == kPasses - 2 ? out_vals : (pass & 1 ? ap : tv)) + start;
+      uint32_t* dk = (pass == 1 ? tk : out_keys) + start;
+      uint32_t* dv = (pass == 1 ? tv : out_vals) + start;
       for (int i = tid; i < kRadix; i += kBktThreads) S.hist[i] = 0;
       __syncthreads();
       for (uint32_t p = tid; p < size; p += kBktThreads)
@@ -1143,7 +1155,7 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
   for (int i = 0; i < kBktItems; ++i) {
     const uint32_t p = i * kBktThreads + tid;
     if (p < size) {
-      const uint2 kv = make_uint2(__ldg(ak + start + p), __ldg(ap + start + p));
+      const uint2 kv = make_uint2(__ldg(ak + p), __ldg(ap + p));
       S.kv[0][p] = kv;
       rk[i] = atomicAdd(&S.u.b.cnt[(kv.x >> kBinShift) & (kBins - 1)], 1u);
     }
@@ -1294,6 +1306,12 @@ static cudaError_t sort_attrs() {
   return cudaSuccess;
 }
 
+// words of each sort ping-pong buffer for batches of b records: the MSD +
+// rank mode scatters into 256 fixed regions of kBktCap records
+uint64_t sort_tmp_words(uint64_t b) {
+  return b > (uint64_t)kSmallCap ? std::max<uint64_t>(b, (uint64_t)kRadix * kBktCap) : b;
+}
+
 cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals,
                               const uint8_t* ops, int mode, uint64_t n, uint64_t b,
                               SortScratch& S, uint32_t* out_keys, uint32_t* out_vals,
@@ -1336,12 +1354,10 @@ cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals
   if (!use_ctr && !S.lsd_only && g_sort_mode == 1) {
     uint32_t* cnt = S.msd_cnt + (S.msd_parity ? kRadix : 0);
     uint32_t* cnt_next = S.msd_cnt + (S.msd_parity ? 0 : kRadix);
-    uint32_t* bar = S.msd_bar + S.msd_parity;
-    uint32_t* bar_next = S.msd_bar + (S.msd_parity ^ 1);
     S.msd_parity ^= 1;
     hk.begin(hk.ctx, LSM_K_SORT_PASS, s);
     e = launch_pdl(msd_scatter_kernel, (unsigned)tiles, kSortThreads, sizeof(MsdSmem), s, in, b,
-                   S.tmp_keys[0], S.tmp_vals[0], cnt, cnt_next, bar, bar_next, S.err, S.bkt);
+                   S.tmp_keys[0], S.tmp_vals[0], cnt, cnt_next, S.err);
     // bytes: keys + ops read (5 B), (key, position) written (8 B)
     hk.end(hk.ctx, LSM_K_SORT_PASS, (double)b * 13.0, s, 1);
     if (e != cudaSuccess) return e;
@@ -1349,7 +1365,7 @@ cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals
     if (merge != nullptr && merge->n + b <= 0xFFFFFFFFull) M = *merge;
     hk.begin(hk.ctx, LSM_K_SORT_PASS, s);
     e = launch_pdl(bucket_rank_kernel, (unsigned)kRadix, kBktThreads, sizeof(RankSmem), s,
-                   (const uint32_t*)S.bkt, S.tmp_keys[0], S.tmp_vals[0], in, b, S.tmp_keys[1],
+                   (const uint32_t*)cnt, S.tmp_keys[0], S.tmp_vals[0], in, b, S.tmp_keys[1],
                    S.tmp_vals[1], out_keys, out_vals, out_f1, S.overflow_dev, M);
     // bytes: (key, position) read (8 B), value gathered (4 B), (key, value)
     // written (8 B); fused: + the run read (8 B each) and written again
