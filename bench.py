@@ -363,7 +363,9 @@ def run_native(args):
         dt = (time.perf_counter() - t0) / args.steps
         e2e = {"value": R * B / dt / 1e6, "unit": UNIT,
                "h2d_bytes_per_step": R * B * 9, "d2h_bytes_per_step": 4,
-               "note": "lsm_update_host x64 (pinned H2D inside) + lsm_sync, wall clock"}
+               "note": "lsm_update_host x64 (pinned H2D on the library's copy stream, double-"
+                       "buffered so batch j+1's copy overlaps batch j's update) + lsm_sync, "
+                       "wall clock"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1,

@@ -144,9 +144,13 @@ lsm_status lsm_bulk_build(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_va
 lsm_status lsm_update_batches(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals,
                               const uint8_t* d_is_delete, uint64_t n, void* stream);
 
-/* lsm_update from HOST buffers: copies the batch (9 B/update) into internal
- * device staging on `stream`, then runs lsm_update. h_* must stay valid until
- * the stream reaches the copy (use pinned memory for async overlap).       */
+/* lsm_update from HOST buffers: copies the batch (9 B/update) into one of two
+ * internal device staging buffers on an internal copy stream, then runs
+ * lsm_update on `stream` after the copy (stream-ordered: later work on
+ * `stream` sees the update). Consecutive calls alternate buffers, so batch
+ * j+1's copy overlaps batch j's update. h_* must stay valid and unmodified
+ * until the copy has run (lsm_sync or a synchronize of `stream` guarantees
+ * it); use pinned memory for asynchronous copies.                          */
 lsm_status lsm_update_host(lsm_t* h, const uint32_t* h_keys, const uint32_t* h_vals,
                            const uint8_t* h_is_delete, uint64_t n, void* stream);
 

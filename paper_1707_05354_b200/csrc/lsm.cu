@@ -79,9 +79,15 @@ struct lsm {
   uint64_t sa_idx_words = 0;
   bool sa_idx_ready = false;
   // host-update staging
-  uint32_t* st_keys = nullptr;
-  uint32_t* st_vals = nullptr;
-  uint8_t* st_ops = nullptr;
+  // lsm_update_host: double-buffered device staging filled on a copy stream,
+  // so batch j+1's H2D copy overlaps batch j's update
+  uint32_t* st_keys[2] = {nullptr, nullptr};
+  uint32_t* st_vals[2] = {nullptr, nullptr};
+  uint8_t* st_ops[2] = {nullptr, nullptr};
+  cudaStream_t st_stream = nullptr;
+  cudaEvent_t st_copied[2] = {nullptr, nullptr};
+  cudaEvent_t st_free[2] = {nullptr, nullptr};
+  int st_cur = 0;
   // query scratch
   void* qbuf = nullptr;
   uint64_t qbuf_bytes = 0;
@@ -437,9 +443,11 @@ lsm_status lsm_destroy(lsm_t* h) {
   buf_free(h->sa_buf[0], nullptr);
   buf_free(h->sa_buf[1], nullptr);
   if (h->sa_idx) cudaFreeAsync(h->sa_idx, nullptr);
-  if (h->st_keys) cudaFreeAsync(h->st_keys, nullptr);
-  if (h->st_vals) cudaFreeAsync(h->st_vals, nullptr);
-  if (h->st_ops) cudaFreeAsync(h->st_ops, nullptr);
+  for (int k = 0; k < 2; ++k) {
+    if (h->st_keys[k]) cudaFreeAsync(h->st_keys[k], nullptr);
+    if (h->st_vals[k]) cudaFreeAsync(h->st_vals[k], nullptr);
+    if (h->st_ops[k]) cudaFreeAsync(h->st_ops[k], nullptr);
+  }
   if (h->qbuf) cudaFreeAsync(h->qbuf, nullptr);
   cudaDeviceSynchronize();
   for (auto& p : h->prof) {
@@ -447,6 +455,11 @@ lsm_status lsm_destroy(lsm_t* h) {
     cudaEventDestroy(p.e1);
   }
   for (auto e : h->ev_free) cudaEventDestroy(e);
+  for (int k = 0; k < 2; ++k) {
+    if (h->st_copied[k]) cudaEventDestroy(h->st_copied[k]);
+    if (h->st_free[k]) cudaEventDestroy(h->st_free[k]);
+  }
+  if (h->st_stream) cudaStreamDestroy(h->st_stream);
   if (h->h_pinned) cudaFreeHost(h->h_pinned);
   if (h->sort.overflow_host) cudaFreeHost((void*)h->sort.overflow_host);
   cudaMemPoolDestroy(h->pool);
@@ -806,16 +819,31 @@ lsm_status lsm_update_host(lsm_t* h, const uint32_t* h_keys, const uint32_t* h_v
   if (!h || !h_keys) return LSM_ERR_INVALID_ARG;
   if (n == 0 || n > h->b) return LSM_ERR_BATCH_SIZE;
   cudaStream_t s = S(stream);
-  if (!h->st_keys) {
-    CK(pool_alloc(h, (void**)&h->st_keys, h->b * 4, s));
-    CK(pool_alloc(h, (void**)&h->st_vals, h->b * 4, s));
-    CK(pool_alloc(h, (void**)&h->st_ops, h->b, s));
+  if (!h->st_stream) {
+    CK(cudaStreamCreateWithFlags(&h->st_stream, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+      CK(cudaEventCreateWithFlags(&h->st_copied[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&h->st_free[k], cudaEventDisableTiming));
+      CK(pool_alloc(h, (void**)&h->st_keys[k], h->b * 4, s));
+      CK(pool_alloc(h, (void**)&h->st_vals[k], h->b * 4, s));
+      CK(pool_alloc(h, (void**)&h->st_ops[k], h->b, s));
+      CK(cudaEventRecord(h->st_free[k], s));  // allocations ordered on s
+    }
   }
-  CK(cudaMemcpyAsync(h->st_keys, h_keys, n * 4, cudaMemcpyHostToDevice, s));
-  if (h_vals) CK(cudaMemcpyAsync(h->st_vals, h_vals, n * 4, cudaMemcpyHostToDevice, s));
-  if (h_is_delete) CK(cudaMemcpyAsync(h->st_ops, h_is_delete, n, cudaMemcpyHostToDevice, s));
-  return do_update(h, h->st_keys, h_vals ? h->st_vals : nullptr,
-                   h_is_delete ? h->st_ops : nullptr, kModeMixed, n, s);
+  const int k = h->st_cur;
+  h->st_cur ^= 1;
+  cudaStream_t cs = h->st_stream;
+  // staging k is free once the update that last read it has finished on s
+  CK(cudaStreamWaitEvent(cs, h->st_free[k], 0));
+  CK(cudaMemcpyAsync(h->st_keys[k], h_keys, n * 4, cudaMemcpyHostToDevice, cs));
+  if (h_vals) CK(cudaMemcpyAsync(h->st_vals[k], h_vals, n * 4, cudaMemcpyHostToDevice, cs));
+  if (h_is_delete) CK(cudaMemcpyAsync(h->st_ops[k], h_is_delete, n, cudaMemcpyHostToDevice, cs));
+  CK(cudaEventRecord(h->st_copied[k], cs));
+  CK(cudaStreamWaitEvent(s, h->st_copied[k], 0));
+  const lsm_status st = do_update(h, h->st_keys[k], h_vals ? h->st_vals[k] : nullptr,
+                                  h_is_delete ? h->st_ops[k] : nullptr, kModeMixed, n, s);
+  CK(cudaEventRecord(h->st_free[k], s));
+  return st;
 }
 
 lsm_status lsm_lookup(lsm_t* h, const uint32_t* d_q, uint64_t nq, uint32_t* d_vals_out,

@@ -896,17 +896,26 @@ __global__ void __launch_bounds__(kSortThreads, 1) msd_scatter_kernel(
   }
 }
 
-constexpr int kBinBits = 11;
+#ifndef SORT_BIN_BITS
+#define SORT_BIN_BITS 11
+#endif
+constexpr int kBinBits = SORT_BIN_BITS;
 constexpr int kBins = 1 << kBinBits;
-constexpr int kBinShift = 24 - kBinBits;  // bins = key bits [13, 24)
+constexpr int kBinShift = 24 - kBinBits;  // bins = key bits [24 - kBinBits, 24)
+// bin counts and starts are 16-bit halves of 32-bit words (a bucket holds at
+// most kBktCap < 2^16 records), so 4096 bins fit where 2048 words would
+static_assert(kBktCap < 65536 && (kBins / kBktThreads) % 2 == 0, "16-bit bin halves");
+__device__ __forceinline__ uint32_t half16(const uint32_t* w, uint32_t bin) {
+  return (w[bin >> 1] >> ((bin & 1u) * 16u)) & 0xFFFFu;
+}
 constexpr uint32_t kBinMax = 64;           // larger bins: stable LSD fallback
 
 struct RankSmem {
   uint2 kv[2][kBktCap];  // (key, position)
   union {
     struct {
-      uint32_t cnt[kBins];
-      uint32_t start[kBins];
+      uint32_t cnt[kBins / 2];    // 16-bit halves
+      uint32_t start[kBins / 2];
     } b;
     LocalScratch<kBktThreads> L;
   } u;
@@ -1148,16 +1157,28 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
   }
 
   // ---- load (key, position); bin counts with shared-memory atomics ----
-  for (int i = tid; i < kBins; i += kBktThreads) S.u.b.cnt[i] = 0;
+  for (int i = tid; i < kBins / 2; i += kBktThreads) S.u.b.cnt[i] = 0;
   __syncthreads();
   uint32_t rk[kBktItems];
+  {
+    // all loads first (the region holds kBktCap words, so every load is in
+    // bounds): a load guarded together with its atomic was issued one item
+    // at a time, a full memory latency each
+    uint32_t kx[kBktItems], ky[kBktItems];
 #pragma unroll
-  for (int i = 0; i < kBktItems; ++i) {
-    const uint32_t p = i * kBktThreads + tid;
-    if (p < size) {
-      const uint2 kv = make_uint2(__ldg(ak + p), __ldg(ap + p));
-      S.kv[0][p] = kv;
-      rk[i] = atomicAdd(&S.u.b.cnt[(kv.x >> kBinShift) & (kBins - 1)], 1u);
+    for (int i = 0; i < kBktItems; ++i) {
+      kx[i] = __ldg(ak + i * kBktThreads + tid);
+      ky[i] = __ldg(ap + i * kBktThreads + tid);
+    }
+#pragma unroll
+    for (int i = 0; i < kBktItems; ++i) {
+      const uint32_t p = i * kBktThreads + tid;
+      if (p < size) {
+        S.kv[0][p] = make_uint2(kx[i], ky[i]);
+        const uint32_t bin = (kx[i] >> kBinShift) & (kBins - 1);
+        const uint32_t sh = (bin & 1u) * 16u;
+        rk[i] = (atomicAdd(&S.u.b.cnt[bin >> 1], 1u << sh) >> sh) & 0xFFFFu;
+      }
     }
   }
   __syncthreads();
@@ -1166,16 +1187,16 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
   uint32_t c[kPer], sum = 0, mx = 0;
 #pragma unroll
   for (int j = 0; j < kPer; ++j) {
-    c[j] = S.u.b.cnt[tid * kPer + j];
+    c[j] = half16(S.u.b.cnt, tid * kPer + j);
     sum += c[j];
     mx = max(mx, c[j]);
   }
   uint32_t tot;
   uint32_t run = block_exclusive_scan<kBktThreads, uint32_t>(sum, S.scan, &tot);
 #pragma unroll
-  for (int j = 0; j < kPer; ++j) {
-    S.u.b.start[tid * kPer + j] = run;
-    run += c[j];
+  for (int j = 0; j < kPer; j += 2) {
+    S.u.b.start[(tid * kPer + j) >> 1] = run | ((run + c[j]) << 16);
+    run += c[j] + c[j + 1];
   }
   const bool skew = __syncthreads_or(mx > kBinMax);
   int res = 0;
@@ -1186,7 +1207,7 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
       const uint32_t p = i * kBktThreads + tid;
       if (p < size) {
         const uint2 kv = S.kv[0][p];
-        S.kv[1][S.u.b.start[(kv.x >> kBinShift) & (kBins - 1)] + rk[i]] = kv;
+        S.kv[1][half16(S.u.b.start, (kv.x >> kBinShift) & (kBins - 1)) + rk[i]] = kv;
       }
     }
     __syncthreads();
@@ -1197,7 +1218,7 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
       if (p < size) {
         const uint2 kv = S.kv[1][p];
         const uint32_t bin = (kv.x >> kBinShift) & (kBins - 1);
-        const uint32_t lo = S.u.b.start[bin], hi = lo + S.u.b.cnt[bin];
+        const uint32_t lo = half16(S.u.b.start, bin), hi = lo + half16(S.u.b.cnt, bin);
         uint32_t r = 0;
         for (uint32_t j = lo; j < hi; ++j) {
           const uint2 o = S.kv[1][j];
@@ -1234,22 +1255,25 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
   }
   // ---- values: gather by position, all loads of a thread in flight at once
   //      (a dependent gather per store serialised the write loop) ----
-  {
+  if (in.vals != nullptr) {
+    // unguarded loads (positions clamped to 0 where unused) so that all of a
+    // thread's gathers are in flight at once
     uint32_t v[kBktItems];
 #pragma unroll
     for (int i = 0; i < kBktItems; ++i) {
       const uint32_t p = i * kBktThreads + tid;
-      v[i] = 0;
-      if (p < size) {
-        const uint2 kv = S.kv[res][p];
-        v[i] = enc_val(in, kv.x, kv.y);
-      }
+      const uint2 kv = S.kv[res][p];  // p < kBktCap: in bounds
+      const bool use = p < size && (kv.x & 1u);
+      v[i] = __ldg(in.vals + (use ? kv.y : 0u));
+      v[i] = use ? v[i] : 0u;
     }
 #pragma unroll
     for (int i = 0; i < kBktItems; ++i) {
       const uint32_t p = i * kBktThreads + tid;
       if (p < size) S.kv[res][p].y = v[i];
     }
+  } else {
+    for (uint32_t p = tid; p < size; p += kBktThreads) S.kv[res][p].y = 0u;
   }
   if (M.keys == nullptr) {
     __syncthreads();

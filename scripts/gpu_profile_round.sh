@@ -14,13 +14,13 @@ $NCU -k regex:range_block -s 0 -c 1 -o gpurun_out/prof_range $P > /dev/null 2>&1
 $NCU -k regex:lookup_kernel -s 0 -c 1 -o gpurun_out/prof_lookup $P > /dev/null 2>&1
 $NCU -k regex:merge_kernel -s 62 -c 1 -o gpurun_out/prof_merge $P --no-cleanup --nq 1024 > /dev/null 2>&1
 $NCU -k regex:merge_kernel -s 0 -c 1 -o gpurun_out/prof_merge0 $P --batches 4 --no-cleanup --nq 1024 > /dev/null 2>&1
-$NCU --replay-mode application -k regex:onesweep -s 60 -c 1 -o gpurun_out/prof_sort $P --no-cleanup --nq 1024 > /dev/null 2>&1
-$NCU -k regex:bucket_sort -s 60 -c 1 -o gpurun_out/prof_bucket $P --no-cleanup --nq 1024 > /dev/null 2>&1
+$NCU -k regex:msd_scatter -s 60 -c 1 -o gpurun_out/prof_sort $P --no-cleanup --nq 1024 > /dev/null 2>&1
+$NCU -k regex:bucket_rank -s 60 -c 1 -o gpurun_out/prof_bucket $P --no-cleanup --nq 1024 > /dev/null 2>&1
 $NCU -k regex:cleanup_write -s 0 -c 1 -o gpurun_out/prof_cleanup $P --nq 1024 > /dev/null 2>&1
 # summarise on the box (the reports are too big to bring back): profiles
 # summaries under gpurun_out/prof_summary, reports deleted except small ones
 python scripts/ncu_summary.py --launches gpurun_out/launches.csv --reps 'gpurun_out/prof_*.ncu-rep' \
-    --round r01 --outdir gpurun_out/prof_summary > gpurun_out/ncu_summary.log 2>&1
+    --round ${ROUND:-r01} --outdir gpurun_out/prof_summary > gpurun_out/ncu_summary.log 2>&1
 mkdir -p gpurun_out/keep
 for f in prof_range prof_bucket prof_merge; do mv gpurun_out/$f.ncu-rep gpurun_out/keep/ 2>/dev/null; done
 rm -f gpurun_out/*.ncu-rep

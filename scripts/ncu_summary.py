@@ -21,6 +21,7 @@ MUL = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6
 TMUL = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "ns": 1e-3, "us": 1.0, "ms": 1e3}
 
 CLASS = [("onesweep", "sort_pass"), ("bucket_sort", "sort_pass"), ("small_sort", "sort_pass"),
+         ("msd_scatter", "sort_pass"), ("bucket_rank", "sort_pass"),
          ("sort_hist", "sort_hist"), ("merge_kernel", "merge"),
          ("lookup_kernel", "lookup"), ("range_block", "range"),
          ("count_kernel", "count"), ("range_kernel", "range"),
