@@ -56,6 +56,12 @@ inline __host__ __device__ uint32_t f3_tree_h(uint64_t n3) {
   while (((1ull << h) - 1) < n3) ++h;
   return h;
 }
+// height of the staged F3 tree: the tree holds ranks [0, 2^h - 1) and the
+// unused word E[0] holds rank 2^h - 1, so 2^h words cover n3 <= 2^h entries
+// (n3 = 2^k, e.g. 8192 for a 2^26-record level, takes 2^k words, not 2^(k+1))
+inline __host__ __device__ uint32_t f3_stage_h(uint64_t n3) {
+  return n3 >= 2 ? f3_tree_h(n3 - 1) : 1u;
+}
 
 __device__ __forceinline__ uint32_t lane_id() {
   uint32_t r;

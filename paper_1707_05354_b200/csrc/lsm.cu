@@ -312,7 +312,7 @@ LevelTable level_table(const lsm* h) {
       T.idx[c] = h->sa ? h->sa_idx : h->level[i].idx;
       T.n[c] = h->sa ? h->r * h->b : h->b << i;
       // F3 is staged as a complete search tree in Eytzinger order: 2^h words
-      const uint32_t h3 = f3_tree_h(idx_f3_len(T.n[c]));
+      const uint32_t h3 = f3_stage_h(idx_f3_len(T.n[c]));
       const uint64_t words = 1ull << h3;
       T.f3_h[c] = h3;
       if (off + words <= kF3SmemMax) {

@@ -327,6 +327,26 @@ def test_host_buffer_entry_points():
     assert np.array_equal(hf, of) and np.array_equal(hv, ov)
 
 
+def test_host_updates_double_buffered_pinned():
+    # lsm_update_host from pinned host tensors: batch j+1's copy runs on the
+    # library's copy stream while batch j updates; the levels must equal those
+    # of the device-buffer path (and S1) after every batch
+    b = (1 << 16) + 77
+    gh = pkg.GpuLSM(b)
+    s1 = oracle.ShadowLSM(b)
+    host = []
+    for j in range(7):
+        k, v, d = synth.updates(23, j * b, b, delete_frac4=1)
+        host.append(tuple(torch.from_numpy(x).pin_memory() for x in (k, v, d)))
+        s1.update(k, v, d)
+    for j, (k, v, d) in enumerate(host):
+        gh.update_host(k, v, d)
+    gh.sync()
+    ga = GpuAdapter(b)
+    ga.lsm = gh
+    assert_levels_equal(ga, s1, "pinned host updates")
+
+
 def test_determinism():
     b = 3000
     imgs = []
