@@ -549,6 +549,12 @@ __device__ __forceinline__ uint32_t walk_window(const LevelTable& T, uint64_t* p
     w1[j] = ld(j, p + 1);
     w2[j] = ld(j, p + 2);
     w3[j] = ld(j, p + 3);
+#if !defined(GPULSM_NO_WALK_PREFETCH)
+    // the refills past the first 8-record sector come from L2; pull the next
+    // sector into L1 now so a refill issued 3 records ahead finds it there
+    if (p + 8 < T.n[j])
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(T.keys[j] + ((p + 8) & ~7ull)));
+#endif
   }
   // head of level j: its original key, or kSent past the slice (> z or >= n)
   auto head = [&](int j) -> uint32_t {

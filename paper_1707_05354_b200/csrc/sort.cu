@@ -797,17 +797,27 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_sort_kernel(
 // of bucket_sort_kernel. Both set the overflow flag, which moves the handle to
 // the 4-pass LSD for later batches.
 // ---------------------------------------------------------------------------
+// tiles of the scatter: MSD_THREADS threads x kSortItems records, and as many
+// CTAs per SM as fit (two 512-thread tiles per SM overlap each other's load
+// and barrier latency; one 1024-thread tile per SM was the first design)
+#ifndef MSD_THREADS
+#define MSD_THREADS 512
+#endif
+constexpr int kMsdThreads = MSD_THREADS;
+constexpr int kMsdCtas = 1024 / kMsdThreads;
+constexpr int kMsdTile = kMsdThreads * kSortItems;
+
 struct MsdSmem {
-  uint32_t keys[kSortTile];
-  uint32_t pos[kSortTile];
+  uint32_t keys[kMsdTile];
+  uint32_t pos[kMsdTile];
   uint32_t hist[kRadix];    // tile digit counts (atomic ranks)
   uint32_t tstart[kRadix];  // tile-local digit starts
   uint32_t toff[kRadix];    // the tile's slot inside each global bucket
   uint32_t gdst[kRadix];    // global destination - tile-local start
-  uint32_t scan[kWarps + 1];
+  uint32_t scan[kMsdThreads / 32 + 1];
 };
 
-__global__ void __launch_bounds__(kSortThreads, 1) msd_scatter_kernel(
+__global__ void __launch_bounds__(kMsdThreads, kMsdCtas) msd_scatter_kernel(
     RawBatch in, uint64_t b, uint32_t* __restrict__ out_keys, uint32_t* __restrict__ out_pos,
     uint32_t* __restrict__ cnt, uint32_t* __restrict__ cnt_next, uint32_t* __restrict__ err) {
   extern __shared__ __align__(16) uint8_t msd_smem[];
@@ -820,15 +830,15 @@ __global__ void __launch_bounds__(kSortThreads, 1) msd_scatter_kernel(
   if (blockIdx.x == 0 && tid < kRadix) cnt_next[tid] = 0;
   __syncthreads();
   const uint32_t tile = blockIdx.x;
-  const uint64_t tile_base = (uint64_t)tile * kSortTile;
+  const uint64_t tile_base = (uint64_t)tile * kMsdTile;
   const uint32_t tile_n =
-      (uint32_t)((b - tile_base) < (uint64_t)kSortTile ? (b - tile_base) : (uint64_t)kSortTile);
+      (uint32_t)((b - tile_base) < (uint64_t)kMsdTile ? (b - tile_base) : (uint64_t)kMsdTile);
   const uint32_t wbase = warp * (32 * kSortItems);
   // the values are gathered by position in the bucket pass: pull this tile's
   // range into L2 now (one bulk prefetch; random 4-byte gathers from DRAM
   // would each cost a 128-byte line fill and a full miss latency)
   if (tid == 0 && in.vals != nullptr && tile_base < in.n) {
-    const uint64_t e = min(in.n, tile_base + kSortTile);
+    const uint64_t e = min(in.n, tile_base + kMsdTile);
     const uintptr_t a0 = reinterpret_cast<uintptr_t>(in.vals + tile_base) & ~(uintptr_t)15;
     const uintptr_t a1 = (reinterpret_cast<uintptr_t>(in.vals + e) + 15) & ~(uintptr_t)15;
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0))
@@ -863,7 +873,7 @@ __global__ void __launch_bounds__(kSortThreads, 1) msd_scatter_kernel(
   const uint32_t c = tid < kRadix ? S.hist[tid] : 0u;
   if (tid < kRadix) S.toff[tid] = c ? atomicAdd(cnt + tid, c) : 0u;
   uint32_t tot;
-  const uint32_t ts = block_exclusive_scan<kSortThreads, uint32_t>(c, S.scan, &tot);
+  const uint32_t ts = block_exclusive_scan<kMsdThreads, uint32_t>(c, S.scan, &tot);
   if (tid < kRadix) S.tstart[tid] = ts;
   __syncthreads();
 #pragma unroll
@@ -883,7 +893,7 @@ __global__ void __launch_bounds__(kSortThreads, 1) msd_scatter_kernel(
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
-    const uint32_t idx = i * kSortThreads + tid;
+    const uint32_t idx = i * kMsdThreads + tid;
     if (idx < tile_n) {
       const uint32_t key = S.keys[idx];
       const uint32_t d = key >> 24;
@@ -943,12 +953,6 @@ __device__ __forceinline__ uint64_t warp_lower_bound_kv(const uint32_t* __restri
     lo = nlo;
   }
   return lo;
-}
-
-// value of the record at input position p with key variable `key` (A1:
-// tombstones, placebos and out-of-domain keys carry 0)
-__device__ __forceinline__ uint32_t enc_val(const RawBatch& in, uint32_t key, uint32_t p) {
-  return ((key & 1u) && in.vals != nullptr) ? __ldg(in.vals + p) : 0u;
 }
 
 // Fused first cascade step (A3): merge the sorted bucket d
@@ -1380,7 +1384,8 @@ cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals
     uint32_t* cnt_next = S.msd_cnt + (S.msd_parity ? 0 : kRadix);
     S.msd_parity ^= 1;
     hk.begin(hk.ctx, LSM_K_SORT_PASS, s);
-    e = launch_pdl(msd_scatter_kernel, (unsigned)tiles, kSortThreads, sizeof(MsdSmem), s, in, b,
+    e = launch_pdl(msd_scatter_kernel, (unsigned)((b + kMsdTile - 1) / kMsdTile), kMsdThreads,
+                   sizeof(MsdSmem), s, in, b,
                    S.tmp_keys[0], S.tmp_vals[0], cnt, cnt_next, S.err);
     // bytes: keys + ops read (5 B), (key, position) written (8 B)
     hk.end(hk.ctx, LSM_K_SORT_PASS, (double)b * 13.0, s, 1);
