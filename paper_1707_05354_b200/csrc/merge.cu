@@ -24,6 +24,7 @@
 // tile k; there is no partition launch and no block-wide barrier in the loop.
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -58,13 +59,15 @@ struct StageInfo {
   uint32_t ka, kb, va, vb;  // element offsets of A/B data in the key/val buffers
 };
 
-struct MergeSmem {
-  uint32_t keys[kStages][kBufElems];
-  uint32_t vals[kStages][kBufElems];
-  StageInfo info[kStages];
-  unsigned long long full[kStages];
-  unsigned long long empty[kStages];
+template <int STAGES>
+struct MergeSmemT {
+  uint32_t keys[STAGES][kBufElems];
+  uint32_t vals[STAGES][kBufElems];
+  StageInfo info[STAGES];
+  unsigned long long full[STAGES];
+  unsigned long long empty[STAGES];
 };
+using MergeSmem = MergeSmemT<kStages>;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -161,13 +164,17 @@ __device__ __forceinline__ unsigned long long mtimer() {
   } while (0)
 #endif
 
-__global__ void __launch_bounds__(kMergeThreads) merge_kernel(
+// STAGES = 1: the one-tile-per-CTA variant for small merges (one wave of up to
+// 4 CTAs per SM, no ring to fill); STAGES = kStages: the persistent pipeline.
+template <int STAGES>
+__global__ void __launch_bounds__(kMergeThreads) merge_kernel_t(
     const uint32_t* __restrict__ ak, const uint32_t* __restrict__ av, uint64_t na,
     const uint32_t* __restrict__ bk, const uint32_t* __restrict__ bv, uint64_t nb,
     uint32_t* __restrict__ ok, uint32_t* __restrict__ ov, uint64_t ntiles,
     uint32_t* __restrict__ out_f1) {
+  constexpr int kStages = STAGES;
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  MergeSmem& S = *reinterpret_cast<MergeSmem*>(smem_raw);
+  MergeSmemT<STAGES>& S = *reinterpret_cast<MergeSmemT<STAGES>*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint64_t total = na + nb;
   const uint64_t t_begin = (uint64_t)blockIdx.x * ntiles / gridDim.x;
@@ -335,6 +342,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(
 }
 
 int g_num_sms = 0;
+uint64_t g_single_cap = 0;  // tiles the one-tile-per-CTA variant runs in one wave
 
 }  // namespace
 
@@ -345,22 +353,40 @@ cudaError_t launch_merge(const uint32_t* ak, const uint32_t* av, uint64_t na,
   if (total == 0) return cudaSuccess;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sizeof(MergeSmem));
+    cudaError_t e = cudaFuncSetAttribute(merge_kernel_t<kStages>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(MergeSmemT<kStages>));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(merge_kernel_t<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(MergeSmemT<1>));
     if (e != cudaSuccess) return e;
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, merge_kernel_t<1>, kMergeThreads,
+                                                      sizeof(MergeSmemT<1>)) != cudaSuccess)
+      per_sm = 0;
+    g_single_cap = (uint64_t)per_sm * g_num_sms;
+    const char* env = std::getenv("GPULSM_MERGE_SINGLE");
+    if (env && env[0] == '0') g_single_cap = 0;
     attr_set = true;
   }
   // outputs must be 16-byte aligned for the vector stores
   if ((reinterpret_cast<uintptr_t>(ok) | reinterpret_cast<uintptr_t>(ov)) & 15)
     return cudaErrorMisalignedAddress;
   const uint64_t ntiles = (total + kMergeTile - 1) / kMergeTile;
-  const uint64_t grid = std::min<uint64_t>(ntiles, (uint64_t)g_num_sms * kMergeCtasPerSm);
   hk.begin(hk.ctx, LSM_K_MERGE, s);
-  cudaError_t e = launch_pdl(merge_kernel, (unsigned)grid, kMergeThreads, sizeof(MergeSmem), s, ak,
-                             av, na, bk, bv, nb, ok, ov, ntiles, out_f1);
+  cudaError_t e;
+  if (ntiles <= g_single_cap) {
+    // small merge: one tile per CTA, all resident at once
+    e = launch_pdl(merge_kernel_t<1>, (unsigned)ntiles, kMergeThreads, sizeof(MergeSmemT<1>), s,
+                   ak, av, na, bk, bv, nb, ok, ov, ntiles, out_f1);
+  } else {
+    const uint64_t grid = std::min<uint64_t>(ntiles, (uint64_t)g_num_sms * kMergeCtasPerSm);
+    e = launch_pdl(merge_kernel_t<kStages>, (unsigned)grid, kMergeThreads,
+                   sizeof(MergeSmemT<kStages>), s, ak, av, na, bk, bv, nb, ok, ov, ntiles, out_f1);
+  }
   // algorithmic bytes: each output record is read once (8 B) and written once
   hk.end(hk.ctx, LSM_K_MERGE, (double)total * 16.0, s, 1);
   return e;
