@@ -620,15 +620,32 @@ __device__ __forceinline__ uint32_t walk_levels(const LevelTable& T, uint64_t* p
 // is evaluated 8 records at a time from two independent 16-byte loads of the
 // aligned group, instead of one dependent load per record. K must be 16-byte
 // aligned (the caller falls back to walk_slices otherwise).
+// With `resume` != nullptr the walk stops after kWalkCapGroups groups: a
+// longer slice leaves *resume = the next group and *resume_prev = the last key
+// seen, for the warp-cooperative continuation (warp_walk_long); *resume =
+// kNoResume when the slice ended.
+constexpr uint64_t kNoResume = ~0ull;
+#ifndef WALK_CAP_GROUPS
+#define WALK_CAP_GROUPS 8
+#endif
+constexpr int kWalkCapGroups = WALK_CAP_GROUPS;
 template <bool NEED_VAL, typename Emit>
 __device__ __forceinline__ uint32_t walk_one(const uint32_t* __restrict__ K,
                                              const uint32_t* __restrict__ V, uint64_t n,
-                                             uint64_t pos, uint32_t z, Emit emit) {
+                                             uint64_t pos, uint32_t z, Emit emit,
+                                             uint64_t* resume = nullptr,
+                                             uint32_t* resume_prev = nullptr) {
   uint32_t cnt = 0;
+  if (resume) *resume = kNoResume;
   if (pos >= n) return 0;
   uint32_t prev = 0xFFFFFFFFu;  // K[pos] starts a run: pos = lower_bound(k1)
   uint64_t g = pos & ~7ull;
-  while (true) {
+  for (int grp = 0;; ++grp) {
+    if (resume && grp == kWalkCapGroups) {
+      *resume = g;
+      *resume_prev = prev;
+      break;
+    }
     const uint4 a = __ldg(reinterpret_cast<const uint4*>(K + g));  // +16 words of slack
     const uint4 b = __ldg(reinterpret_cast<const uint4*>(K + g + 4));
     const uint32_t kk[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
@@ -667,6 +684,94 @@ __device__ __forceinline__ uint32_t walk_one(const uint32_t* __restrict__ K,
     g += 8;
   }
   return cnt;
+}
+
+// Continuation of a long single-level slice by the whole warp (the lane's
+// query broadcast by the caller): each step covers 128 records, 4 per lane
+// from one 16-byte load of keys (and of values when writing), the run-head
+// test takes the previous key across lanes with a shuffle, the slice ends at
+// the first record past z or n (ballot), and valid records get their output
+// slot from a warp exclusive scan -- coalesced, streaming at HBM rates instead
+// of one thread walking the slice. g is 8-aligned (walk_one's next group);
+// prev = the original key before K[g]. Returns the valid records found; put(k,
+// key, val) receives the k-th of them (k from 0).
+template <bool NEED_VAL, typename Put>
+__device__ __forceinline__ uint32_t warp_walk_long(const uint32_t* __restrict__ K,
+                                                   const uint32_t* __restrict__ V, uint64_t n,
+                                                   uint64_t g, uint32_t prev, uint32_t z, Put put) {
+  const uint32_t lane = lane_id();
+  uint32_t added = 0;
+  const uint64_t vpol = l2_policy_stream();
+  while (true) {
+    const uint64_t p0 = g + 4ull * lane;
+    uint4 k4 = p0 < n ? __ldg(reinterpret_cast<const uint4*>(K + p0))  // +16 words of slack
+                      : make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+    const uint32_t kk[4] = {k4.x, k4.y, k4.z, k4.w};
+    // in-slice flags, then the first out-of-slice record of the warp
+    uint32_t in = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (p0 + i < n && (kk[i] >> 1) <= z) in |= 1u << i;
+    const bool lane_stops = in != 0xFu;
+    const uint32_t stop_mask = __ballot_sync(kFull, lane_stops);
+    const uint32_t first_stop = stop_mask ? (uint32_t)(__ffs(stop_mask) - 1) : 32u;
+    // records before the first out-of-slice record are in the slice
+    uint32_t live = 0;
+    if (lane < first_stop) live = 0xFu;
+    else if (lane == first_stop) live = (in + 1u) ^ in;  // bits below the first zero ...
+    if (lane == first_stop) live = (live >> 1);           // ... exclusive of it
+    const uint32_t pk = __shfl_up_sync(kFull, kk[3] >> 1, 1);
+    uint32_t before = lane == 0 ? prev : pk;
+    uint32_t valid = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t k = kk[i] >> 1;
+      if (((live >> i) & 1u) && k != before && (kk[i] & 1u)) valid |= 1u << i;
+      before = k;
+    }
+    const uint32_t c = __popc(valid);
+    uint32_t x = c;  // warp inclusive scan of the counts
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= (uint32_t)o) x += y;
+    }
+    if (NEED_VAL && valid) {
+      uint32_t vv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) vv[i] = (valid >> i) & 1u ? ldg_pol(V + p0 + i, vpol) : 0u;
+      uint32_t k = added + x - c;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if ((valid >> i) & 1u) put(k++, kk[i] >> 1, vv[i]);
+    }
+    added += __shfl_sync(kFull, x, 31);
+    if (stop_mask) break;
+    prev = __shfl_sync(kFull, kk[3] >> 1, 31);
+    g += 128;
+  }
+  return added;
+}
+
+// Count on one aligned level with the warp-cooperative continuation of long
+// slices (whole warp; every lane passes its own query).
+__device__ __forceinline__ uint32_t count_one_level(const LevelTable& T, uint64_t pos, uint32_t z) {
+  const uint32_t lane = lane_id();
+  uint64_t res;
+  uint32_t rprev;
+  uint32_t c = walk_one<false>(T.keys[0], T.vals[0], T.n[0], pos, z,
+                               [](uint32_t, uint32_t, uint32_t) {}, &res, &rprev);
+  uint32_t longm = __ballot_sync(kFull, res != kNoResume);
+  while (longm) {
+    const int l = __ffs(longm) - 1;
+    longm &= longm - 1;
+    const uint64_t gl = __shfl_sync(kFull, res, l);
+    const uint32_t pl = __shfl_sync(kFull, rprev, l), zl = __shfl_sync(kFull, z, l);
+    const uint32_t add = warp_walk_long<false>(T.keys[0], T.vals[0], T.n[0], gl, pl, zl,
+                                               [](uint32_t, uint32_t, uint32_t) {});
+    if (lane == (uint32_t)l) c += add;
+  }
+  return c;
 }
 
 // Stage 1 for all occupied levels: pos_j = lower_bound(k1) per level,
@@ -714,8 +819,7 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) count_kernel(
     bounds<NL>(T, sF3, a, a > z, pos, L, l2_policy_stream());
     uint32_t c;
     if (NL == 1 && (reinterpret_cast<uintptr_t>(T.keys[0]) & 15) == 0)
-      c = walk_one<false>(T.keys[0], T.vals[0], T.n[0], pos[0], z,
-                          [](uint32_t, uint32_t, uint32_t) {});
+      c = count_one_level(T, pos[0], z);
     else
       c = walk_levels<NL, false>(T, pos, z, L, [](uint32_t, uint32_t, uint32_t) {});
     if (act) __stcs(counts + i, c);
@@ -986,8 +1090,7 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) range_block_kernel(
       for (int j = 0; j < NL; ++j) sPos[j * kRBQueries + li] = (uint32_t)pos[j];
       uint32_t c;
       if (NL == 1 && (reinterpret_cast<uintptr_t>(T.keys[0]) & 15) == 0)
-        c = walk_one<false>(T.keys[0], T.vals[0], T.n[0], pos[0], z,
-                            [](uint32_t, uint32_t, uint32_t) {});
+        c = count_one_level(T, pos[0], z);
       else
         c = walk_levels<NL, false>(T, pos, z, NL, [](uint32_t, uint32_t, uint32_t) {});
       sOff[li] = act ? c : 0u;
@@ -1023,11 +1126,12 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) range_block_kernel(
     for (int u = 0; u < kRBTasks; ++u) {
       const uint32_t li = u * kQThreads + tid;
       const uint64_t i = q0 + li;
-      if (i >= nq) continue;
-      const uint32_t z = __ldg(k2 + i);
+      const bool act = i < nq;
+      const uint32_t z = act ? __ldg(k2 + i) : 0u;
       const uint32_t nxt = (li + 1 < kRBQueries) ? sOff[li + 1] : run;
       const uint64_t ob = base + sOff[li];
-      if (nxt == sOff[li] && li + 1 < kRBQueries) continue;  // nothing valid
+      // nothing valid (the block's last query always walks)
+      const bool has = act && !(nxt == sOff[li] && li + 1 < kRBQueries);
       uint64_t pos[NL];
 #pragma unroll
       for (int j = 0; j < NL; ++j) pos[j] = sPos[j * kRBQueries + li];
@@ -1038,10 +1142,30 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) range_block_kernel(
           __stcs(vals_out + o, val);
         }
       };
-      if (NL == 1 && (reinterpret_cast<uintptr_t>(T.keys[0]) & 15) == 0)
-        walk_one<true>(T.keys[0], T.vals[0], T.n[0], pos[0], z, put);
-      else
+      if (NL == 1 && (reinterpret_cast<uintptr_t>(T.keys[0]) & 15) == 0) {
+        // whole warp: serial walk per lane, long slices continued together
+        uint64_t res = kNoResume;
+        uint32_t rprev = 0, c0 = 0;
+        if (has) c0 = walk_one<true>(T.keys[0], T.vals[0], T.n[0], pos[0], z, put, &res, &rprev);
+        uint32_t longm = __ballot_sync(kFull, res != kNoResume);
+        while (longm) {
+          const int l = __ffs(longm) - 1;
+          longm &= longm - 1;
+          const uint64_t gl = __shfl_sync(kFull, res, l);
+          const uint32_t pl = __shfl_sync(kFull, rprev, l), zl = __shfl_sync(kFull, z, l);
+          const uint64_t obl = __shfl_sync(kFull, ob, l) + __shfl_sync(kFull, c0, l);
+          warp_walk_long<true>(T.keys[0], T.vals[0], T.n[0], gl, pl, zl,
+                               [&](uint32_t k, uint32_t key, uint32_t val) {
+                                 const uint64_t o = obl + k;
+                                 if (o < capacity) {
+                                   __stcs(keys_out + o, key);
+                                   __stcs(vals_out + o, val);
+                                 }
+                               });
+        }
+      } else if (has) {
         walk_levels<NL, true>(T, pos, z, NL, put);
+      }
     }
     __syncthreads();  // shared state is reused by the next block
   }

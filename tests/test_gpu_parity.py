@@ -217,6 +217,27 @@ def test_sort_skewed_bin_fallback():
                      lambda h, h2: ((h % np.uint64(256)) << np.uint64(23)) | (h2 % np.uint64(200)))
 
 
+@pytest.mark.parametrize("alphabet", [None, 30_000])
+def test_long_ranges_single_level(alphabet):
+    # one occupied level (r = 4) and ranges of ~100..10^4 resident records:
+    # slices longer than the per-lane cap continue warp-cooperatively (run
+    # heads across lane boundaries, the slice end inside a lane); the
+    # duplicate-heavy alphabet puts long stale runs and tombstones in them
+    b = 8192
+    g = GpuAdapter(b)
+    o1 = oracle.OracleDict(b)
+    for j in range(4):
+        k, v, d = synth.updates(41, j * b, b, delete_frac4=1, alphabet=alphabet)
+        g.update(k, v, d)
+        o1.apply_batch(k, v, d)
+    assert g.r == 4
+    dom = synth.D if alphabet is None else alphabet + 2
+    for L in (100, 1000, 10_000):
+        k1, k2 = synth.range_queries(42 + L, 300, 4 * b, L, domain=dom)
+        q = synth.lookup_queries(43, 1000, 4 * b, alphabet)
+        assert_queries_equal(g, o1, q, k1, k2, f"long ranges L={L}")
+
+
 def test_one_wave_boundary_sort():
     # exactly 148 tiles (largest one-wave batch) and one record more
     for b in (148 * 7168, 148 * 7168 + 1):
