@@ -626,7 +626,7 @@ __device__ __forceinline__ uint32_t walk_levels(const LevelTable& T, uint64_t* p
 // kNoResume when the slice ended.
 constexpr uint64_t kNoResume = ~0ull;
 #ifndef WALK_CAP_GROUPS
-#define WALK_CAP_GROUPS 8
+#define WALK_CAP_GROUPS 16
 #endif
 constexpr int kWalkCapGroups = WALK_CAP_GROUPS;
 template <bool NEED_VAL, typename Emit>
@@ -702,53 +702,65 @@ __device__ __forceinline__ uint32_t warp_walk_long(const uint32_t* __restrict__ 
   const uint32_t lane = lane_id();
   uint32_t added = 0;
   const uint64_t vpol = l2_policy_stream();
+  constexpr int kUnr = 4;  // 512 records per round: four loads in flight per lane
   while (true) {
-    const uint64_t p0 = g + 4ull * lane;
-    uint4 k4 = p0 < n ? __ldg(reinterpret_cast<const uint4*>(K + p0))  // +16 words of slack
+    uint4 k4s[kUnr];
+#pragma unroll
+    for (int s = 0; s < kUnr; ++s) {
+      const uint64_t p0 = g + 128ull * s + 4ull * lane;
+      k4s[s] = p0 < n ? __ldg(reinterpret_cast<const uint4*>(K + p0))  // +16 words of slack
                       : make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-    const uint32_t kk[4] = {k4.x, k4.y, k4.z, k4.w};
-    // in-slice flags, then the first out-of-slice record of the warp
-    uint32_t in = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (p0 + i < n && (kk[i] >> 1) <= z) in |= 1u << i;
-    const bool lane_stops = in != 0xFu;
-    const uint32_t stop_mask = __ballot_sync(kFull, lane_stops);
-    const uint32_t first_stop = stop_mask ? (uint32_t)(__ffs(stop_mask) - 1) : 32u;
-    // records before the first out-of-slice record are in the slice
-    uint32_t live = 0;
-    if (lane < first_stop) live = 0xFu;
-    else if (lane == first_stop) live = (in + 1u) ^ in;  // bits below the first zero ...
-    if (lane == first_stop) live = (live >> 1);           // ... exclusive of it
-    const uint32_t pk = __shfl_up_sync(kFull, kk[3] >> 1, 1);
-    uint32_t before = lane == 0 ? prev : pk;
-    uint32_t valid = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t k = kk[i] >> 1;
-      if (((live >> i) & 1u) && k != before && (kk[i] & 1u)) valid |= 1u << i;
-      before = k;
     }
-    const uint32_t c = __popc(valid);
-    uint32_t x = c;  // warp inclusive scan of the counts
+    bool done = false;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFull, x, o);
-      if (lane >= (uint32_t)o) x += y;
-    }
-    if (NEED_VAL && valid) {
-      uint32_t vv[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) vv[i] = (valid >> i) & 1u ? ldg_pol(V + p0 + i, vpol) : 0u;
-      uint32_t k = added + x - c;
+    for (int s = 0; s < kUnr; ++s) {
+      const uint64_t p0 = g + 128ull * s + 4ull * lane;
+      const uint32_t kk[4] = {k4s[s].x, k4s[s].y, k4s[s].z, k4s[s].w};
+      // in-slice flags, then the first out-of-slice record of the warp
+      uint32_t in = 0;
 #pragma unroll
       for (int i = 0; i < 4; ++i)
-        if ((valid >> i) & 1u) put(k++, kk[i] >> 1, vv[i]);
+        if (p0 + i < n && (kk[i] >> 1) <= z) in |= 1u << i;
+      const uint32_t stop_mask = __ballot_sync(kFull, in != 0xFu);
+      const uint32_t first_stop = stop_mask ? (uint32_t)(__ffs(stop_mask) - 1) : 32u;
+      // records before the first out-of-slice record are in the slice
+      uint32_t live = 0;
+      if (lane < first_stop) live = 0xFu;
+      else if (lane == first_stop) live = ((in + 1u) ^ in) >> 1;  // bits below the first zero
+      const uint32_t pk = __shfl_up_sync(kFull, kk[3] >> 1, 1);
+      uint32_t before = lane == 0 ? prev : pk;
+      uint32_t valid = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t k = kk[i] >> 1;
+        if (((live >> i) & 1u) && k != before && (kk[i] & 1u)) valid |= 1u << i;
+        before = k;
+      }
+      const uint32_t c = __popc(valid);
+      uint32_t x = c;  // warp inclusive scan of the counts
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, o);
+        if (lane >= (uint32_t)o) x += y;
+      }
+      if (NEED_VAL && valid) {
+        uint32_t vv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) vv[i] = (valid >> i) & 1u ? ldg_pol(V + p0 + i, vpol) : 0u;
+        uint32_t k = added + x - c;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if ((valid >> i) & 1u) put(k++, kk[i] >> 1, vv[i]);
+      }
+      added += __shfl_sync(kFull, x, 31);
+      if (stop_mask) {
+        done = true;
+        break;
+      }
+      prev = __shfl_sync(kFull, kk[3] >> 1, 31);
     }
-    added += __shfl_sync(kFull, x, 31);
-    if (stop_mask) break;
-    prev = __shfl_sync(kFull, kk[3] >> 1, 31);
-    g += 128;
+    if (done) break;
+    g += 128ull * kUnr;
   }
   return added;
 }
