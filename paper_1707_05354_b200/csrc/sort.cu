@@ -830,6 +830,12 @@ __global__ void __launch_bounds__(kMsdThreads, kMsdCtas) msd_scatter_kernel(
   if (blockIdx.x == 0 && tid < kRadix) cnt_next[tid] = 0;
   __syncthreads();
   const uint32_t tile = blockIdx.x;
+#ifdef GPULSM_PROBE
+#define MSDP(k) do { __syncthreads(); if (tid == 0 && g_probe) g_probe[(3ull * 4096 + tile) * 8 + (k)] = gtimer(); } while (0)
+#else
+#define MSDP(k) do {} while (0)
+#endif
+  MSDP(0);
   const uint64_t tile_base = (uint64_t)tile * kMsdTile;
   const uint32_t tile_n =
       (uint32_t)((b - tile_base) < (uint64_t)kMsdTile ? (b - tile_base) : (uint64_t)kMsdTile);
@@ -866,10 +872,12 @@ __global__ void __launch_bounds__(kMsdThreads, kMsdCtas) msd_scatter_kernel(
     }
     if (any_bad) atomicOr(err, 1u);
   }
+  MSDP(1);
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i)
     if (wbase + i * 32 + lane < tile_n) rk[i] = atomicAdd(&S.hist[k[i] >> 24], 1u);
   __syncthreads();
+  MSDP(2);
   const uint32_t c = tid < kRadix ? S.hist[tid] : 0u;
   if (tid < kRadix) S.toff[tid] = c ? atomicAdd(cnt + tid, c) : 0u;
   uint32_t tot;
@@ -889,6 +897,7 @@ __global__ void __launch_bounds__(kMsdThreads, kMsdCtas) msd_scatter_kernel(
   // output: the tile's records of digit d go to its slot there. No tile waits
   // for another. Records past the region's end are dropped: that bucket is
   // oversized, and the bucket pass regathers it from the raw batch.
+  MSDP(3);
   if (tid < kRadix) S.gdst[tid] = tid * (uint32_t)kBktCap + S.toff[tid] - S.tstart[tid];
   __syncthreads();
 #pragma unroll
@@ -904,6 +913,7 @@ __global__ void __launch_bounds__(kMsdThreads, kMsdCtas) msd_scatter_kernel(
       }
     }
   }
+  MSDP(4);
 }
 
 #ifndef SORT_BIN_BITS
@@ -1043,6 +1053,13 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
   pdl_wait();
   pdl_trigger();
   const uint32_t d = blockIdx.x;
+#ifdef GPULSM_PROBE
+#define RPB(k) do { __syncthreads(); if (tid == 0 && g_probe) g_probe[5ull * 4096 * 8 + d * 8 + (k)] = gtimer(); } while (0)
+  if (tid == 0 && g_probe) { uint32_t sm; asm volatile("mov.u32 %0, %%smid;" : "=r"(sm)); g_probe[5ull * 4096 * 8 + d * 8 + 7] = sm + 1; }
+#else
+#define RPB(k) do {} while (0)
+#endif
+  RPB(0);
   {  // output start = records in the buckets below d
     const uint32_t c = tid < kRadix ? __ldg(cnt + tid) : 0u;
     uint32_t tot;
@@ -1186,6 +1203,7 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
     }
   }
   __syncthreads();
+  RPB(1);
   // ---- bin starts: each thread scans kBins / kBktThreads consecutive bins ----
   constexpr int kPer = kBins / kBktThreads;
   uint32_t c[kPer], sum = 0, mx = 0;
@@ -1203,6 +1221,7 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
     run += c[j] + c[j + 1];
   }
   const bool skew = __syncthreads_or(mx > kBinMax);
+  RPB(2);
   int res = 0;
   if (!skew) {
     // group by bin (any order inside a bin) ...
@@ -1215,6 +1234,7 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
       }
     }
     __syncthreads();
+    RPB(3);
     // ... then rank inside the bin by counting in (key, position) order
 #pragma unroll
     for (int i = 0; i < kBktItems; ++i) {
@@ -1257,6 +1277,7 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
       res ^= 1;
     }
   }
+  RPB(4);
   // ---- values: gather by position, all loads of a thread in flight at once
   //      (a dependent gather per store serialised the write loop) ----
   if (in.vals != nullptr) {
@@ -1279,6 +1300,7 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
   } else {
     for (uint32_t p = tid; p < size; p += kBktThreads) S.kv[res][p].y = 0u;
   }
+  RPB(5);
   if (M.keys == nullptr) {
     __syncthreads();
     // ---- write the sorted bucket (key, value) and its F1 ----
@@ -1290,6 +1312,7 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
       out_vals[g] = kv.y;
       if (out_f1 != nullptr && (g & (kF1Step - 1)) == 0) out_f1[g / kF1Step] = kv.x;
     }
+    RPB(6);
     return;
   }
   fused_merge<true>(S.kv[res], nullptr, nullptr, size, M, start, S, S.kv[res ^ 1], d);
