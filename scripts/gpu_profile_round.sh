@@ -25,3 +25,9 @@ mkdir -p gpurun_out/keep
 for f in prof_range prof_bucket prof_merge; do mv gpurun_out/$f.ncu-rep gpurun_out/keep/ 2>/dev/null; done
 rm -f gpurun_out/*.ncu-rep
 du -sh gpurun_out/* | sort -h | tail -20
+# sort timeline probe and the C4 query sweep
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -DGPULSM_PROBE -I include -I paper_1707_05354_b200/csrc scripts/msd_probe.cu -o scripts/msd_probe > /dev/null 2>&1
+timeout 120 ./scripts/msd_probe > gpurun_out/msd_probe.txt 2>&1
+timeout 900 python scripts/sweep_c4.py --out gpurun_out/r01_sweep_c4.json > gpurun_out/sweep.log 2>&1
+timeout 120 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,lts__t_sectors_op_read.sum,lts__t_sector_hit_rate.pct --csv --log-file gpurun_out/rand.csv scripts/rand_probe > /dev/null 2>&1
+python scripts/rand_probe_summary.py gpurun_out/rand.csv gpurun_out/rand_probe.json > /dev/null 2>&1
