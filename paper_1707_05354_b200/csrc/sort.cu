@@ -1235,7 +1235,20 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
     }
     __syncthreads();
     RPB(3);
-    // ... then rank inside the bin by counting in (key, position) order
+    // ... gather every record's value by its position now (the loads are in
+    // flight during the ranking below instead of forming a phase of their
+    // own) ...
+    uint32_t gv[kBktItems];
+#pragma unroll
+    for (int i = 0; i < kBktItems; ++i) {
+      const uint32_t p = i * kBktThreads + tid;
+      const uint2 kv = S.kv[1][p];  // p < kBktCap: in bounds
+      const bool use = p < size && (kv.x & 1u) && in.vals != nullptr;
+      gv[i] = __ldg((use ? in.vals : in.keys) + (use ? kv.y : 0u));
+      gv[i] = use ? gv[i] : 0u;  // tombstones, placebos: 0 (R5-R7)
+    }
+    // ... then rank inside the bin by counting in (key, position) order and
+    // place (key, value)
 #pragma unroll
     for (int i = 0; i < kBktItems; ++i) {
       const uint32_t p = i * kBktThreads + tid;
@@ -1248,7 +1261,7 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
           const uint2 o = S.kv[1][j];
           r += (o.x < kv.x) || (o.x == kv.x && o.y < kv.y);
         }
-        S.kv[0][lo + r] = kv;
+        S.kv[0][lo + r] = make_uint2(kv.x, gv[i]);
       }
     }
     __syncthreads();
@@ -1278,9 +1291,10 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
     }
   }
   RPB(4);
-  // ---- values: gather by position, all loads of a thread in flight at once
-  //      (a dependent gather per store serialised the write loop) ----
-  if (in.vals != nullptr) {
+  // ---- skew path: values gathered by position, all loads of a thread in
+  //      flight at once (the main path gathered them before its ranking) ----
+  if (!skew) {
+  } else if (in.vals != nullptr) {
     // unguarded loads (positions clamped to 0 where unused) so that all of a
     // thread's gathers are in flight at once
     uint32_t v[kBktItems];
