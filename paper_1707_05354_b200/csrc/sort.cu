@@ -1060,6 +1060,17 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
 #define RPB(k) do {} while (0)
 #endif
   RPB(0);
+  // the bucket's region (msd_scatter_kernel): all loads issued before the
+  // start scan so the two latencies overlap (the region holds kBktCap words:
+  // every load is in bounds)
+  ak += (uint64_t)d * kBktCap;
+  ap += (uint64_t)d * kBktCap;
+  uint32_t kx[kBktItems], ky[kBktItems];
+#pragma unroll
+  for (int i = 0; i < kBktItems; ++i) {
+    kx[i] = __ldg(ak + i * kBktThreads + tid);
+    ky[i] = __ldg(ap + i * kBktThreads + tid);
+  }
   {  // output start = records in the buckets below d
     const uint32_t c = tid < kRadix ? __ldg(cnt + tid) : 0u;
     uint32_t tot;
@@ -1071,8 +1082,6 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
     __syncthreads();
   }
   const uint32_t start = S.start_d, size = S.size_d;
-  ak += (uint64_t)d * kBktCap;  // the bucket's region (msd_scatter_kernel)
-  ap += (uint64_t)d * kBktCap;
   if (size == 0 && M.keys == nullptr) return;
   if (size > (uint32_t)kBktCap) {
     // oversized bucket (skewed keys): its region holds only the first
@@ -1182,15 +1191,6 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
   __syncthreads();
   uint32_t rk[kBktItems];
   {
-    // all loads first (the region holds kBktCap words, so every load is in
-    // bounds): a load guarded together with its atomic was issued one item
-    // at a time, a full memory latency each
-    uint32_t kx[kBktItems], ky[kBktItems];
-#pragma unroll
-    for (int i = 0; i < kBktItems; ++i) {
-      kx[i] = __ldg(ak + i * kBktThreads + tid);
-      ky[i] = __ldg(ap + i * kBktThreads + tid);
-    }
 #pragma unroll
     for (int i = 0; i < kBktItems; ++i) {
       const uint32_t p = i * kBktThreads + tid;
