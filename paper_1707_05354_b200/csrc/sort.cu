@@ -1248,20 +1248,25 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
       gv[i] = use ? gv[i] : 0u;  // tombstones, placebos: 0 (R5-R7)
     }
     // ... then rank inside the bin by counting in (key, position) order and
-    // place (key, value)
+    // place (key, value). Source and destination are distinct buffers
+    // (__restrict__): the next item's loads need not wait for this store.
+    const uint2* __restrict__ src = S.kv[1];
+    uint2* __restrict__ dst = S.kv[0];
+    const uint32_t* __restrict__ bstart = S.u.b.start;
+    const uint32_t* __restrict__ bcnt = S.u.b.cnt;
 #pragma unroll
     for (int i = 0; i < kBktItems; ++i) {
       const uint32_t p = i * kBktThreads + tid;
       if (p < size) {
-        const uint2 kv = S.kv[1][p];
+        const uint2 kv = src[p];
         const uint32_t bin = (kv.x >> kBinShift) & (kBins - 1);
-        const uint32_t lo = half16(S.u.b.start, bin), hi = lo + half16(S.u.b.cnt, bin);
+        const uint32_t lo = half16(bstart, bin), hi = lo + half16(bcnt, bin);
         uint32_t r = 0;
         for (uint32_t j = lo; j < hi; ++j) {
-          const uint2 o = S.kv[1][j];
+          const uint2 o = src[j];
           r += (o.x < kv.x) || (o.x == kv.x && o.y < kv.y);
         }
-        S.kv[0][lo + r] = make_uint2(kv.x, gv[i]);
+        dst[lo + r] = make_uint2(kv.x, gv[i]);
       }
     }
     __syncthreads();
