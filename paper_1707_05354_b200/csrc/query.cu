@@ -798,15 +798,16 @@ __device__ __forceinline__ void bounds(const LevelTable& T, const uint32_t* sF3,
 #pragma unroll
     for (int j = 0; j < NL; ++j)
       if (empty) pos[j] = T.n[j];
-    return;
-  }
+  } else
 #endif
+  {
 #pragma unroll
-  for (int j = 0; j < CAP; ++j) {
-    if (j < L) {
-      const LvView V = level_view(T, j, sF3);
-      const uint64_t lo = warp_lower_bound(V, a, kpol);  // whole warp
-      pos[j] = empty ? V.n : lo;
+    for (int j = 0; j < CAP; ++j) {
+      if (j < L) {
+        const LvView V = level_view(T, j, sF3);
+        const uint64_t lo = warp_lower_bound(V, a, kpol);  // whole warp
+        pos[j] = empty ? V.n : lo;
+      }
     }
   }
 }

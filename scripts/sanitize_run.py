@@ -10,7 +10,7 @@ import synth
 import paper_1707_05354_b200 as pkg
 from paper_1707_05354_b200 import to_device, to_numpy_u32
 
-def run(b, nb, sa=False, alphabet=None, frac4=1, multi=False):
+def run(b, nb, sa=False, alphabet=None, frac4=1, multi=False, L=8):
     g = pkg.GpuLSM(b, sa=sa)
     o = oracle.OracleDict(b)
     seed = synth.SEED_BASE + b % 97
@@ -25,7 +25,7 @@ def run(b, nb, sa=False, alphabet=None, frac4=1, multi=False):
             g.update(to_device(k), to_device(v), to_device(d)); o.apply_batch(k, v, d)
     n = nb * b
     q = synth.lookup_queries(seed, 3000, n, alphabet)
-    k1, k2 = synth.range_queries(seed, 500, n, 8, domain=alphabet or synth.D)
+    k1, k2 = synth.range_queries(seed, 500, n, L, domain=alphabet or synth.D)
     for phase in range(2):
         gv, gf = g.lookup(to_device(q)); ov, of = o.lookup(q)
         assert np.array_equal(gf.cpu().numpy(), of) and np.array_equal(to_numpy_u32(gv), ov)
@@ -43,6 +43,8 @@ run(4096, 9, alphabet=5000)       # small-sort path, duplicates
 run(40_000, 5)                    # MSD + bucket path, multi-level
 run(64, 9, sa=True)               # GPU SA
 run(1000, 7, multi=True)          # multi-batch insertion
+run(8192, 4, L=2000)              # one level, long slices: warp-cooperative walk
+run(20_000, 3, alphabet=3000)     # oversized bucket: regather + chunked LSD
 if os.environ.get("SAN_BIG"):
     run(1 << 21, 2)                   # multi-wave 4-pass LSD sort
 g = pkg.GpuLSM(256)
