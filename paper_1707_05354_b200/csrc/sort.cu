@@ -806,6 +806,13 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_sort_kernel(
 constexpr int kMsdThreads = MSD_THREADS;
 constexpr int kMsdCtas = 1024 / kMsdThreads;
 constexpr int kMsdTile = kMsdThreads * kSortItems;
+// minimum resident CTAs per SM requested from ptxas. MSD_MINB=2 caps the
+// scatter at 32 registers so a bucket-pass CTA fits beside it and waits
+// resident at griddepcontrol.wait: measured slower (31.7 vs 28.2 us per
+// sort, C3 update 3.58 vs 3.42 ms), so 1 (a 1024-thread tile per SM)
+#ifndef MSD_MINB
+#define MSD_MINB 1
+#endif
 
 struct MsdSmem {
   uint32_t keys[kMsdTile];
@@ -817,7 +824,7 @@ struct MsdSmem {
   uint32_t scan[kMsdThreads / 32 + 1];
 };
 
-__global__ void __launch_bounds__(kMsdThreads, kMsdCtas) msd_scatter_kernel(
+__global__ void __launch_bounds__(kMsdThreads, MSD_MINB) msd_scatter_kernel(
     RawBatch in, uint64_t b, uint32_t* __restrict__ out_keys, uint32_t* __restrict__ out_pos,
     uint32_t* __restrict__ cnt, uint32_t* __restrict__ cnt_next, uint32_t* __restrict__ err) {
   extern __shared__ __align__(16) uint8_t msd_smem[];
