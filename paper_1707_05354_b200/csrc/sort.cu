@@ -1268,10 +1268,13 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
         const uint2 kv = src[p];
         const uint32_t bin = (kv.x >> kBinShift) & (kBins - 1);
         const uint32_t lo = half16(bstart, bin), hi = lo + half16(bcnt, bin);
+        // (key, position) as one 64-bit word: one wide compare per bin mate
+        const uint64_t me = ((uint64_t)kv.x << 32) | kv.y;
+        const unsigned long long* src64 = reinterpret_cast<const unsigned long long*>(src);
         uint32_t r = 0;
         for (uint32_t j = lo; j < hi; ++j) {
-          const uint2 o = src[j];
-          r += (o.x < kv.x) || (o.x == kv.x && o.y < kv.y);
+          const uint64_t o = src64[j];
+          r += ((o << 32) | (o >> 32)) < me;  // uint2 {x, y} in memory: y is the high word
         }
         dst[lo + r] = make_uint2(kv.x, gv[i]);
       }
