@@ -6,8 +6,17 @@
 // same key), reading R4 (stability: equal key variables keep input order, so
 // the first of duplicate inserts wins).
 //
-// Design: onesweep-style LSD radix sort, 4 passes of 8 bits
-// over the 32-bit key variable. Every kernel is launched with programmatic
+// Design, by batch size:
+//  * b <= 7168: small_sort_kernel, one CTA, four shared-memory digit passes;
+//  * one-wave b (the paper's b = 2^20 among them): the MSD + rank mode
+//    (msd_scatter_kernel + bucket_rank_kernel, described where they are
+//    defined): the batch is sorted by (key variable, input position), which
+//    is unique, so ranks come from shared-memory atomics and no pass needs
+//    to be stable;
+//  * larger b, skewed key sets, or GPULSM_SORT=0 (the previous one-wave
+//    design: onesweep top-digit pass + bucket_sort_kernel): the onesweep-style
+//    LSD radix sort below, 4 passes of 8 bits over the 32-bit key variable.
+// Notes on the LSD kernels follow. Every kernel is launched with programmatic
 // dependent launch (griddepcontrol) so its prologue overlaps the tail of its
 // predecessor. Measured on B200 with a %globaltimer probe
 // (scripts/sort_probe.cu), the batch sizes of the paper (2^15..2^27) are far
