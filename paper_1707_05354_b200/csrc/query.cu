@@ -15,9 +15,13 @@
 // and within a level a key run is newest-first (invariant
 // 2), so the newest record of a key is the run head in the
 // lowest level holding the key; the walk visits the paper's segments in key
-// order and keeps a key iff that head is regular. For range, a count pass, an
-// exclusive scan of the valid counts (scan.cu) and a write pass give
-// per-query offsets and pairs sorted by key.
+// order and keeps a key iff that head is regular. For range, one persistent
+// kernel per 1024-query block counts (bounds + walk), scans the counts in the
+// block, takes the block's global base by a decoupled look-back (the paper's
+// stage-2 scan) and walks again to write pairs sorted by key.
+// Walk variants: walk_one (one level, 8 records per step; slices past 128
+// records continued by the whole warp, warp_walk_long), walk_window (2-4
+// levels, 4-record look-ahead), walk_slices (general).
 //
 // Searches: the paper's bottleneck is "the random memory
 // accesses required in all binary searches". Every lower_bound
