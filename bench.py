@@ -140,6 +140,75 @@ def cpu_baseline_oracle(seconds_budget=15.0):
             "single_thread": {"value": upd_1, "cores": 1, "batches": nb_1, "lookup_mqps": lk_1}}
 
 
+PARITY_LO, PARITY_HI = 5 << 25, 6 << 25  # 1/64 of the key domain
+
+
+def parity_gate(lsm, sub, q, k1, k2, lv, lf, cnt, roff, rk, rv, tot_pre, tot_post):
+    """Check the timed step's outputs against the oracle before any number is
+    printed. O1 is fed only the updates whose key lies in [LO, HI) (keys never
+    interact, so it answers every query inside that interval
+    exactly); every lookup / count / range of the step inside the interval is
+    compared, the offsets of all NQ ranges must be the exclusive scan of the
+    counts, count == len(range), and the post-cleanup level image restricted
+    to the interval must equal O1's live pairs (R12). Exits non-zero on a
+    mismatch: no timing line is emitted."""
+    import oracle
+    from paper_1707_05354_b200 import to_numpy_u32
+    lo, hi = PARITY_LO, PARITY_HI
+    o1 = oracle.OracleDict(B)
+    for k, v, d in sub:
+        o1.apply_batch(k, v, d)
+    o1.cleanup()
+    fails = []
+    gv, gf = to_numpy_u32(lv), lf.cpu().numpy()
+    sel = (q >= lo) & (q < hi)
+    ov, of = o1.lookup(q[sel])
+    if not (np.array_equal(gf[sel], of) and np.array_equal(gv[sel], ov)):
+        fails.append("lookup")
+    gc = to_numpy_u32(cnt)
+    ins = (k1 >= lo) & (k2 < hi) & (k1 <= k2)
+    if not np.array_equal(gc[ins], o1.count(k1[ins], k2[ins])):
+        fails.append("count")
+    off = roff.cpu().numpy().astype(np.uint64)
+    if off[0] != 0 or not np.array_equal(np.diff(off), gc.astype(np.uint64)):
+        fails.append("range offsets != exclusive scan of counts")
+    if not (tot_pre == tot_post == int(off[-1])):
+        fails.append("range totals before/after cleanup")
+    idx = np.nonzero(ins)[0]
+    ooff, oks, ovs = o1.range(k1[idx], k2[idx])
+    lens = np.diff(ooff).astype(np.int64)
+    pos = np.repeat(off[idx].astype(np.int64), lens) + (
+        np.arange(int(lens.sum())) - np.repeat(ooff[:-1].astype(np.int64), lens))
+    pos_t = torch_index(pos, rk.device)
+    if not (np.array_equal(to_numpy_u32(rk[pos_t]), oks) and
+            np.array_equal(to_numpy_u32(rv[pos_t]), ovs)):
+        fails.append("range pairs")
+    # post-cleanup image inside [lo, hi): the encoded live pairs of O1
+    ik, iv = [], []
+    for i in range(lsm.r.bit_length()):
+        kk, vv = lsm.level(i)
+        kk, vv = to_numpy_u32(kk), to_numpy_u32(vv)
+        m = ((kk >> 1) >= lo) & ((kk >> 1) < hi)
+        ik.append(kk[m])
+        iv.append(vv[m])
+    ok_, ov_ = o1.items()
+    if not (np.array_equal(np.concatenate(ik), (ok_ << 1) | 1) and
+            np.array_equal(np.concatenate(iv), ov_)):
+        fails.append("post-cleanup level image")
+    if fails:
+        sys.stderr.write(f"PARITY FAILED: {fails}\n")
+        sys.exit(3)
+    return {"ok": True, "oracle": "O1 (std::map) on the key sub-range [5*2^25, 6*2^25)",
+            "lookups": int(sel.sum()), "counts": int(ins.sum()), "ranges": int(ins.sum()),
+            "pairs": int(lens.sum()), "live_pairs_in_image": int(len(ok_)),
+            "all_offsets_checked": NQ + 1}
+
+
+def torch_index(pos, device):
+    import torch
+    return torch.from_numpy(pos).to(device)
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle on this arm's config (bounded samples)."""
     rank = int(os.environ.get("RANK", "0"))
@@ -201,8 +270,11 @@ def run_native(args):
     t0 = time.time()
     keys_d, vals_d, ops_d = [], [], []
     host_batches = []
+    sub = []  # the updates inside the parity sub-range (oracle input)
     for j in range(R):
         k, v, d = synth.updates(seed, j * B, B, delete_frac4=1)
+        m = (k >= PARITY_LO) & (k < PARITY_HI)
+        sub.append((k[m], v[m], d[m]))
         keys_d.append(to_device(k, dev))
         vals_d.append(to_device(v, dev))
         ops_d.append(to_device(d, dev))
@@ -211,7 +283,8 @@ def run_native(args):
                                  torch.from_numpy(v.view(np.int32)).pin_memory(),
                                  torch.from_numpy(d).pin_memory()))
     n_res = R * B
-    q_look = to_device(synth.lookup_queries(seed, NQ, n_res), dev)
+    q_host = synth.lookup_queries(seed, NQ, n_res)
+    q_look = to_device(q_host, dev)
     k1, k2 = synth.range_queries(seed, NQ, n_res, L_RANGE)
     k1_d, k2_d = to_device(k1, dev), to_device(k2, dev)
     gen_s = time.time() - t0
@@ -278,6 +351,9 @@ def run_native(args):
     prof = lsm.profile_read()
     lsm.profile_enable(False)
     total_ms = start.elapsed_time(stop)
+    # ---- parity gate: the last step's outputs vs O1 ----
+    parity = parity_gate(lsm, sub, q_host, k1, k2, lv, lf, cnt, roff, rk, rv, recs[-1][1],
+                         recs[-1][2])
     ph = np.zeros(8)
     for e, _, _ in recs:
         for i in range(8):
@@ -379,6 +455,7 @@ def run_native(args):
         "phase_ms": {"update": ph[0], "lookup": ph[1], "count": ph[2], "range": ph[3],
                      "cleanup": ph[4], "lookup_post": ph[5], "count_post": ph[6],
                      "range_post": ph[7]},
+        "parity": parity,
         "queries": queries, "cleanup": cleanup,
         "roofline": roofline, "kernels": per_class,
         "gpu_launches": launches,

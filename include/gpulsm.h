@@ -14,12 +14,24 @@
  *    passed as void*, NULL = legacy default stream). Inputs must stay live
  *    until the stream reaches the operation. h_* pointers are HOST pointers.
  *  - The handle owns the level storage and all scratch. It is bound to the
- *    device current at lsm_create. Mutations (insert/delete/update/cleanup)
+ *    device current at lsm_create; every call switches to that device and
+ *    restores the caller's current device before returning.
+ *  - Mutations (insert/delete/update/bulk_build/update_batches/cleanup/clear)
  *    need exclusive access ("updates and queries are performed in separate
- *    phases"); queries may run concurrently with each other.
+ *    phases"): the caller orders them against every query
+ *    (same stream, or events). Queries (lookup/count/range/successor/
+ *    predecessor and the *_host variants) may be issued concurrently from
+ *    several host threads on several streams: host bookkeeping is guarded by
+ *    a per-handle lock, each query's device scratch is its own (allocated
+ *    stream-ordered from the handle's pool), and a query on another stream
+ *    waits on an event for the fence-key index the first query derived.
+ *    Per-kernel profiling (lsm_profile_*) assumes one issuing thread.
  *  - Host-detectable errors (NULL pointers, n == 0 or n > b, ...) return
- *    immediately and enqueue nothing. Device-detected errors are STICKY and
- *    reported by lsm_sync / lsm_range / lsm_cleanup. Nothing is thrown.
+ *    immediately and enqueue nothing. Device-detected errors are STICKY:
+ *    lsm_sync, lsm_range and lsm_cleanup synchronise their stream, then
+ *    report (and clear) LSM_ERR_KEY_DOMAIN if an earlier update saw an
+ *    out-of-domain key; the range / cleanup itself has completed in that
+ *    case. Nothing is thrown.
  *  - Keys: user ("original") keys lie in [0, LSM_MAX_KEY] (31-bit domain of
  *    PAPER.md:609 minus the reserved placebo key 2^31-1).
  *    Query keys may be any 32-bit word; keys outside the domain are absent.
@@ -106,10 +118,14 @@ lsm_status lsm_clear(lsm_t* h, void* stream);
  * is newer than every resident batch; within the batch a delete of k wins
  * over inserts of k, and among inserts of k the first one (lowest index)
  * wins. n < b is padded with invisible placebos (R7). Increments r.
- * Device work: encode + 4-pass onesweep LSD radix sort on the 32-bit key
- * variable (status bit included), then for i = 0..ffz(r)-1 a
- * merge-path merge on key>>1, batch first on ties (R1),
- * the last merge writing straight into level ffz(r).
+ * Device work: encode + stable radix sort on the 32-bit key variable
+ * (status bit included) -- one CTA for b <= 7168; for a batch
+ * of up to one wave of 7168-record tiles (b = 2^20 among them) an MSD
+ * scatter by the top 8 bits plus a shared-memory rank of each bucket by
+ * (key variable, input position); above that (or after a skewed key set)
+ * a 4-pass onesweep LSD -- then the binary-counter cascade of stable merges
+ * on key>>1, batch first on ties (R1), writing level
+ * ffz(r).
  * Errors: LSM_ERR_BATCH_SIZE, LSM_ERR_INVALID_ARG, LSM_ERR_OOM,
  * LSM_ERR_CUDA; out-of-domain keys set the sticky LSM_ERR_KEY_DOMAIN.      */
 lsm_status lsm_update(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals,
@@ -206,7 +222,8 @@ lsm_status lsm_count(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2, uint6
  * the offsets are written, only pairs at positions < capacity are, and
  * LSM_ERR_CAPACITY is returned (retry with a larger buffer). One kernel:
  * per-level bounds, a counting walk, offsets by a warp scan + decoupled
- * look-back, a writing walk. Synchronises `stream`.                         */
+ * look-back, a writing walk. Synchronises `stream`; reports a sticky
+ * LSM_ERR_KEY_DOMAIN of an earlier update after the range completed.       */
 lsm_status lsm_range(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2, uint64_t nq,
                      uint64_t* d_offsets_out, uint32_t* d_keys_out, uint32_t* d_vals_out,
                      uint64_t capacity, uint64_t* total_out, void* stream);
@@ -294,7 +311,8 @@ lsm_status lsm_num_batches(const lsm_t* h, uint64_t* r_out);
  * b*2^i if full else 0 (pointers NULL). Valid until the next mutation.     */
 lsm_status lsm_level_view(const lsm_t* h, uint32_t i, const uint32_t** d_keys,
                           const uint32_t** d_vals, uint64_t* n);
-/* Synchronise `stream` and return (then clear) any sticky device error.    */
+/* Synchronise `stream` and return (then clear) the sticky device error
+ * (LSM_ERR_KEY_DOMAIN) of earlier updates, if any.                          */
 lsm_status lsm_sync(lsm_t* h, void* stream);
 /* Number of kernels this handle has launched so far (monotone).            */
 uint64_t lsm_launch_count(const lsm_t* h);

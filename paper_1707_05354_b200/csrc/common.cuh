@@ -224,6 +224,15 @@ __device__ __forceinline__ T block_exclusive_scan(T v, T* tmp, T* total) {
   return excl;
 }
 
+// Host-side caches (kernel attributes, SM counts) are kept per device: a
+// process may drive handles on several GPUs.
+constexpr int kMaxDevices = 64;
+inline int dev_slot() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) d = 0;
+  return d;
+}
+
 // ---------------------------------------------------------------------------
 // Launchers (host side). Each returns cudaGetLastError() after the launch.
 // ---------------------------------------------------------------------------
@@ -306,42 +315,14 @@ cudaError_t launch_sort_segments(const uint32_t* raw_keys, const uint32_t* raw_v
                                  const uint8_t* ops, int mode, uint64_t n, uint64_t b,
                                  uint64_t k, SortScratch& S, uint32_t* out_keys,
                                  uint32_t* out_vals, cudaStream_t s, const LaunchHooks& hk);
-// Optional first cascade step fused into the sort (MSD + rank mode only):
-// the sorted batch (newer, first on ties) is merged with the sorted run
-// (keys, vals, n) -- level 0 -- straight into (out_keys, out_vals) of
-// n + b records, with F1 into out_f1 when not null. *fused reports whether
-// the sort took this path (otherwise the plain sorted batch was written).
 uint64_t sort_tmp_words(uint64_t b);  // words of each sort ping-pong buffer
-struct SortMerge {
-  const uint32_t* keys;
-  const uint32_t* vals;
-  uint64_t n;
-  uint32_t* out_keys;
-  uint32_t* out_vals;
-  uint32_t* out_f1;
-};
 cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals,
                               const uint8_t* ops, int mode, uint64_t n, uint64_t b,
                               SortScratch& S, uint32_t* out_keys, uint32_t* out_vals,
-                              uint32_t* out_f1, cudaStream_t s, const LaunchHooks& hk,
-                              const SortMerge* merge = nullptr, bool* fused = nullptr);
+                              uint32_t* out_f1, cudaStream_t s, const LaunchHooks& hk);
 
 // Stable merge on key>>1, A (newer) first on ties, into out[na+nb];
 // out_f1 (nullable) receives F1 of the output.
-// k-way cascade (kway.cu): runs 0..runs-1 newest first, run runs-1 the
-// oldest and largest; f1 = each run's fence keys (every 8th key).
-struct KwayRuns {
-  const uint32_t* k[LSM_MAX_LEVELS + 1];
-  const uint32_t* v[LSM_MAX_LEVELS + 1];
-  const uint32_t* f1[LSM_MAX_LEVELS + 1];
-  uint64_t n[LSM_MAX_LEVELS + 1];
-  int runs;
-};
-uint64_t kway_cut_words(const KwayRuns& R);
-cudaError_t launch_kway_merge(const KwayRuns& R, uint64_t* cuts, uint32_t* ok, uint32_t* ov,
-                              uint32_t* out_f1, uint32_t* gk, uint32_t* gv, cudaStream_t s,
-                              const LaunchHooks& hk);
-
 cudaError_t launch_merge(const uint32_t* ak, const uint32_t* av, uint64_t na,
                          const uint32_t* bk, const uint32_t* bv, uint64_t nb, uint32_t* ok,
                          uint32_t* ov, uint32_t* out_f1, cudaStream_t s, const LaunchHooks& hk);

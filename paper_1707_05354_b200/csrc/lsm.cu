@@ -15,6 +15,8 @@
 // compacted buffer (no redistribution copy).
 
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -60,8 +62,6 @@ struct lsm {
   uint32_t* home_idx[LSM_MAX_LEVELS] = {};  // index storage of each home level
   Buffer ping[2];         // merge ping-pong scratch
   Buffer sortout;         // sorted batch when t >= 1
-  uint32_t* sortout_f1 = nullptr;  // its fence keys (k-way cascade, t >= 2)
-  Buffer kscratch;        // k-way cascade: scratch for oversized chunks
   SortScratch sort{};
   uint32_t* sort_meta = nullptr;
   uint64_t sort_meta_words = 0;
@@ -93,8 +93,12 @@ struct lsm {
   uint64_t qbuf_bytes = 0;
   uint64_t* h_pinned = nullptr;  // host readback words
   cudaMemPool_t pool = nullptr;
-  uint64_t launches = 0;
-  lsm_status sticky = LSM_OK;
+  std::atomic<uint64_t> launches{0};
+  // host bookkeeping (level table, index flags, scratch, profiling) is
+  // guarded by one lock per handle; device scratch of queries is per call
+  std::recursive_mutex mu;
+  cudaEvent_t idx_ev = nullptr;  // recorded after the last F2/F3 finalize
+  bool idx_ev_set = false;
   // profiling
   bool prof_on = false;
   std::vector<ProfRec> prof;
@@ -106,6 +110,23 @@ struct lsm {
 namespace {
 
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Every entry point runs on the handle's device and restores the caller's
+// current device on return.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+#define ENTER(h)                  \
+  DeviceGuard _dg((h)->device);   \
+  std::lock_guard<std::recursive_mutex> _lk((h)->mu)
 
 cudaEvent_t ev_get(lsm* h) {
   if (!h->ev_free.empty()) {
@@ -340,17 +361,31 @@ cudaError_t ensure_index(lsm* h, cudaStream_t s, const LaunchHooks& hk) {
       J.count = 1;
       h->sa_idx_ready = true;
     }
-    return launch_finalize_index(J, s, hk);
-  }
-  for (int i = 0; i < LSM_MAX_LEVELS; ++i) {
-    if (((h->r >> i) & 1ull) && !h->level[i].idx_ready) {
-      J.idx[J.count] = h->level[i].idx;
-      J.n[J.count] = h->b << i;
-      ++J.count;
-      h->level[i].idx_ready = true;
+  } else {
+    for (int i = 0; i < LSM_MAX_LEVELS; ++i) {
+      if (((h->r >> i) & 1ull) && !h->level[i].idx_ready) {
+        J.idx[J.count] = h->level[i].idx;
+        J.n[J.count] = h->b << i;
+        ++J.count;
+        h->level[i].idx_ready = true;
+      }
     }
   }
-  return launch_finalize_index(J, s, hk);
+  if (J.count > 0) {
+    // the finalize runs on this query's stream; queries on other streams
+    // wait for it through idx_ev (they see idx_ready already set)
+    cudaError_t e = launch_finalize_index(J, s, hk);
+    if (e != cudaSuccess) return e;
+    if (!h->idx_ev) {
+      e = cudaEventCreateWithFlags(&h->idx_ev, cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+    }
+    e = cudaEventRecord(h->idx_ev, s);
+    if (e != cudaSuccess) return e;
+    h->idx_ev_set = true;
+    return cudaSuccess;
+  }
+  return h->idx_ev_set ? cudaStreamWaitEvent(s, h->idx_ev, 0) : cudaSuccess;
 }
 
 int ffz(uint64_t r) {
@@ -360,6 +395,33 @@ int ffz(uint64_t r) {
 }
 
 uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+// Device scratch owned by one call: taken from the handle's stream-ordered
+// pool on the call's stream and released on it when the call returns (the
+// kernels that use it are ordered before the release).
+struct CallScratch {
+  lsm* h;
+  cudaStream_t s;
+  void* p = nullptr;
+  CallScratch(lsm* h_, cudaStream_t s_) : h(h_), s(s_) {}
+  cudaError_t get(uint64_t bytes) { return pool_alloc(h, &p, bytes, s); }
+  ~CallScratch() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+
+// The sticky device-detected error (an out-of-domain update key, R5): read
+// after the stream has been synchronised, cleared once reported.
+lsm_status take_sticky(lsm* h, cudaStream_t s) {
+  if (!h->sort.err) return LSM_OK;
+  uint32_t v = 0;
+  if (cudaMemcpyAsync(&v, h->sort.err, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return LSM_ERR_CUDA;
+  if (v == 0) return LSM_OK;
+  if (cudaMemsetAsync(h->sort.err, 0, 4, s) != cudaSuccess) return LSM_ERR_CUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return LSM_ERR_CUDA;
+  return LSM_ERR_KEY_DOMAIN;
+}
 
 }  // namespace
 
@@ -403,12 +465,6 @@ lsm_status lsm_create(uint64_t b, lsm_t** out) {
   }
   uint64_t thr = ~0ull;
   cudaMemPoolSetAttribute(h->pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  {
-    // L2 fetch granularity (A/B knob): the query kernels'
-    // level accesses are random 32-byte sectors
-    const char* g = std::getenv("GPULSM_L2FETCH");
-    if (g != nullptr) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)std::atoi(g));
-  }
   e = cudaMallocHost((void**)&h->h_pinned, 64);
   if (e != cudaSuccess) {
     cudaMemPoolDestroy(h->pool);
@@ -421,7 +477,8 @@ lsm_status lsm_create(uint64_t b, lsm_t** out) {
 
 lsm_status lsm_destroy(lsm_t* h) {
   if (!h) return LSM_ERR_INVALID_ARG;
-  cudaSetDevice(h->device);
+  {
+  ENTER(h);
   cudaDeviceSynchronize();
   for (int i = 0; i < LSM_MAX_LEVELS; ++i) {
     level_release(h, i, nullptr);
@@ -431,8 +488,6 @@ lsm_status lsm_destroy(lsm_t* h) {
   buf_free(h->ping[0], nullptr);
   buf_free(h->ping[1], nullptr);
   buf_free(h->sortout, nullptr);
-  buf_free(h->kscratch, nullptr);
-  if (h->sortout_f1) cudaFreeAsync(h->sortout_f1, nullptr);
   if (h->sort_meta) cudaFreeAsync(h->sort_meta, nullptr);
   for (int k = 0; k < 2; ++k) {
     if (h->sort.tmp_keys[k]) cudaFreeAsync(h->sort.tmp_keys[k], nullptr);
@@ -462,7 +517,9 @@ lsm_status lsm_destroy(lsm_t* h) {
   if (h->st_stream) cudaStreamDestroy(h->st_stream);
   if (h->h_pinned) cudaFreeHost(h->h_pinned);
   if (h->sort.overflow_host) cudaFreeHost((void*)h->sort.overflow_host);
+  if (h->idx_ev) cudaEventDestroy(h->idx_ev);
   cudaMemPoolDestroy(h->pool);
+  }
   delete h;
   return LSM_OK;
 }
@@ -472,6 +529,7 @@ static cudaError_t sa_idx_ensure(lsm* h, uint64_t n, cudaStream_t s);
 
 lsm_status lsm_reserve(lsm_t* h, uint64_t max_batches, void* stream) {
   if (!h) return LSM_ERR_INVALID_ARG;
+  ENTER(h);
   cudaStream_t s = S(stream);
   CK(ensure_sort_scratch(h, s));
   if (h->sa) {
@@ -496,6 +554,7 @@ lsm_status lsm_reserve(lsm_t* h, uint64_t max_batches, void* stream) {
 
 lsm_status lsm_clear(lsm_t* h, void* stream) {
   if (!h) return LSM_ERR_INVALID_ARG;
+  ENTER(h);
   if (h->sa) {
     h->r = 0;
     return LSM_OK;
@@ -525,9 +584,9 @@ static lsm_status prepare_insert(lsm_t* h, int t, cudaStream_t s) {
 // level i is full, buffer <- merge(buffer, level i), newer first on ties
 // (PAPER.md:621-624); the last merge writes level t and its fence keys F1.
 static lsm_status cascade(lsm_t* h, const uint32_t* ck, const uint32_t* cv, int t,
-                          cudaStream_t s, const LaunchHooks& hk, int i0 = 0) {
+                          cudaStream_t s, const LaunchHooks& hk) {
   const uint64_t b = h->b;
-  for (int i = i0; i < t; ++i) {
+  for (int i = 0; i < t; ++i) {
     uint32_t* ok = (i == t - 1) ? h->home[t].keys : h->ping[i & 1].keys;
     uint32_t* ov = (i == t - 1) ? h->home[t].vals : h->ping[i & 1].vals;
     const uint64_t ni = b << i;
@@ -621,6 +680,7 @@ lsm_status lsm_is_sa(const lsm_t* h, int* sa_out) {
 static lsm_status do_update(lsm_t* h, const uint32_t* keys, const uint32_t* vals,
                             const uint8_t* ops, int mode, uint64_t n, cudaStream_t s) {
   if (!h || !keys) return LSM_ERR_INVALID_ARG;
+  ENTER(h);
   if (n == 0 || n > h->b) return LSM_ERR_BATCH_SIZE;
   if (mode == kModeMixed && ops == nullptr) mode = kModeInsert;
   if (h->sa) return sa_update(h, keys, vals, ops, mode, n, s);
@@ -634,64 +694,9 @@ static lsm_status do_update(lsm_t* h, const uint32_t* keys, const uint32_t* vals
   // sort (A1+A2): straight into level 0 (with its F1) when t == 0
   uint32_t* sk = (t == 0) ? h->home[0].keys : h->sortout.keys;
   uint32_t* sv = (t == 0) ? h->home[0].vals : h->sortout.vals;
-  // the one-pass cascade (kway.cu) is exact but not yet faster than the
-  // iterated merges: opt-in with GPULSM_KWAY=1
-  static const bool kway = [] {
-    const char* e = std::getenv("GPULSM_KWAY");
-    return e && e[0] == '1';
-  }();
-  if (t >= 2 && kway) {
-    // one pass: the sorted batch (with fence keys) and levels 0..t-1 into
-    // level t (kway.cu; same bytes as the iterated merges)
-    if (!h->sortout_f1) CK(pool_alloc(h, (void**)&h->sortout_f1, idx_f1_len(b) * 4 + 64, s));
-    CK(launch_sort_batch(keys, vals, ops, mode, n, b, h->sort, sk, sv, h->sortout_f1, s, hk));
-    KwayRuns R;
-    std::memset(&R, 0, sizeof(R));
-    R.runs = t + 1;
-    R.k[0] = sk;
-    R.v[0] = sv;
-    R.f1[0] = h->sortout_f1;
-    R.n[0] = b;
-    for (int i = 0; i < t; ++i) {
-      R.k[i + 1] = h->level[i].keys;
-      R.v[i + 1] = h->level[i].vals;
-      R.f1[i + 1] = h->level[i].idx;
-      R.n[i + 1] = b << i;
-    }
-    CK(buf_ensure(h, h->kscratch, b << t, s));
-    CK(ensure_qbuf(h, kway_cut_words(R) * 8, s));
-    CK(launch_kway_merge(R, static_cast<uint64_t*>(h->qbuf), h->home[t].keys, h->home[t].vals,
-                         h->home_idx[t], h->kscratch.keys, h->kscratch.vals, s, hk));
-    for (int i = 0; i < t; ++i) level_release(h, i, s);  // levels 0..t-1 <- empty
-    commit_insert(h, t);
-    return LSM_OK;
-  }
-  // t >= 1: the sort may also do the cascade's first merge (batch with
-  // level 0, sort.cu fused_merge) and write the 2b-record buffer directly
-  // opt-in (GPULSM_FUSE=1): exact, but measured slower than the separate
-  // merge launch on C3 (update phase 3.96 vs 3.74 ms)
-  static const bool fuse_ok = [] {
-    const char* e = std::getenv("GPULSM_FUSE");
-    return e && e[0] == '1';
-  }();
-  SortMerge M{};
-  if (t >= 1 && fuse_ok) {
-    M.keys = h->level[0].keys;
-    M.vals = h->level[0].vals;
-    M.n = b;
-    M.out_keys = (t == 1) ? h->home[1].keys : h->ping[0].keys;
-    M.out_vals = (t == 1) ? h->home[1].vals : h->ping[0].vals;
-    M.out_f1 = (t == 1) ? h->home_idx[1] : nullptr;
-  }
-  bool fused = false;
   CK(launch_sort_batch(keys, vals, ops, mode, n, b, h->sort, sk, sv,
-                       t == 0 ? h->home_idx[0] : nullptr, s, hk, M.keys ? &M : nullptr, &fused));
-  if (fused) {
-    level_release(h, 0, s);  // level 0 <- empty
-    st = cascade(h, M.out_keys, M.out_vals, t, s, hk, 1);
-  } else {
-    st = cascade(h, sk, sv, t, s, hk);
-  }
+                       t == 0 ? h->home_idx[0] : nullptr, s, hk));
+  st = cascade(h, sk, sv, t, s, hk);
   if (st != LSM_OK) return st;
   commit_insert(h, t);
   return LSM_OK;
@@ -720,6 +725,7 @@ lsm_status lsm_delete(lsm_t* h, const uint32_t* d_keys, uint64_t n, void* stream
 lsm_status lsm_bulk_build(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals,
                           const uint8_t* d_is_delete, uint64_t n, void* stream) {
   if (!h || !d_keys) return LSM_ERR_INVALID_ARG;
+  ENTER(h);
   if (h->r != 0) return LSM_ERR_INVALID_ARG;  // only into an empty dictionary
   if (n == 0) return LSM_ERR_BATCH_SIZE;
   const uint64_t b = h->b;
@@ -779,6 +785,7 @@ lsm_status lsm_bulk_build(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_va
 lsm_status lsm_update_batches(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals,
                               const uint8_t* d_is_delete, uint64_t n, void* stream) {
   if (!h || !d_keys) return LSM_ERR_INVALID_ARG;
+  ENTER(h);
   if (n == 0) return LSM_ERR_BATCH_SIZE;
   const uint64_t b = h->b;
   const uint64_t k = (n + b - 1) / b;
@@ -817,6 +824,7 @@ lsm_status lsm_update_batches(lsm_t* h, const uint32_t* d_keys, const uint32_t* 
 lsm_status lsm_update_host(lsm_t* h, const uint32_t* h_keys, const uint32_t* h_vals,
                            const uint8_t* h_is_delete, uint64_t n, void* stream) {
   if (!h || !h_keys) return LSM_ERR_INVALID_ARG;
+  ENTER(h);
   if (n == 0 || n > h->b) return LSM_ERR_BATCH_SIZE;
   cudaStream_t s = S(stream);
   if (!h->st_stream) {
@@ -849,6 +857,7 @@ lsm_status lsm_update_host(lsm_t* h, const uint32_t* h_keys, const uint32_t* h_v
 lsm_status lsm_lookup(lsm_t* h, const uint32_t* d_q, uint64_t nq, uint32_t* d_vals_out,
                       uint8_t* d_found_out, void* stream) {
   if (!h) return LSM_ERR_INVALID_ARG;
+  ENTER(h);
   if (nq == 0) return LSM_OK;
   if (!d_q || !d_vals_out) return LSM_ERR_INVALID_ARG;
   CK(ensure_index(h, S(stream), hooks(h)));
@@ -863,18 +872,25 @@ lsm_status lsm_lookup_host(lsm_t* h, const uint32_t* h_q, uint64_t nq, uint32_t*
   if (nq == 0) return LSM_OK;
   if (!h_q || !h_vals_out) return LSM_ERR_INVALID_ARG;
   cudaStream_t s = S(stream);
-  const uint64_t need = align_up(nq * 4, 256) * 2 + align_up(nq, 256);
-  CK(ensure_qbuf(h, need, s));
-  uint8_t* base = static_cast<uint8_t*>(h->qbuf);
-  uint32_t* dq = reinterpret_cast<uint32_t*>(base);
-  uint32_t* dv = reinterpret_cast<uint32_t*>(base + align_up(nq * 4, 256));
-  uint8_t* df = base + 2 * align_up(nq * 4, 256);
-  CK(cudaMemcpyAsync(dq, h_q, nq * 4, cudaMemcpyHostToDevice, s));
-  CK(ensure_index(h, s, hooks(h)));
-  LevelTable T = level_table(h);
-  CK(launch_lookup(T, dq, nq, dv, df, s, hooks(h)));
-  CK(cudaMemcpyAsync(h_vals_out, dv, nq * 4, cudaMemcpyDeviceToHost, s));
-  if (h_found_out) CK(cudaMemcpyAsync(h_found_out, df, nq, cudaMemcpyDeviceToHost, s));
+  {
+    ENTER(h);
+    // per-call device buffers (stream-ordered pool): concurrent calls on
+    // other streams never share them
+    CallScratch sc(h, s);
+    const uint64_t need = align_up(nq * 4, 256) * 2 + align_up(nq, 256);
+    CK(sc.get(need));
+    uint8_t* base = static_cast<uint8_t*>(sc.p);
+    uint32_t* dq = reinterpret_cast<uint32_t*>(base);
+    uint32_t* dv = reinterpret_cast<uint32_t*>(base + align_up(nq * 4, 256));
+    uint8_t* df = base + 2 * align_up(nq * 4, 256);
+    CK(cudaMemcpyAsync(dq, h_q, nq * 4, cudaMemcpyHostToDevice, s));
+    CK(ensure_index(h, s, hooks(h)));
+    LevelTable T = level_table(h);
+    CK(launch_lookup(T, dq, nq, dv, df, s, hooks(h)));
+    CK(cudaMemcpyAsync(h_vals_out, dv, nq * 4, cudaMemcpyDeviceToHost, s));
+    if (h_found_out) CK(cudaMemcpyAsync(h_found_out, df, nq, cudaMemcpyDeviceToHost, s));
+  }
+  DeviceGuard dg(h->device);
   CK(cudaStreamSynchronize(s));
   return LSM_OK;
 }
@@ -883,6 +899,7 @@ static lsm_status order_query(lsm_t* h, const uint32_t* d_q, uint64_t nq, bool s
                               uint32_t* d_keys_out, uint32_t* d_vals_out, uint8_t* d_found_out,
                               void* stream) {
   if (!h) return LSM_ERR_INVALID_ARG;
+  ENTER(h);
   if (nq == 0) return LSM_OK;
   if (!d_q || !d_keys_out || !d_vals_out) return LSM_ERR_INVALID_ARG;
   CK(ensure_index(h, S(stream), hooks(h)));
@@ -904,6 +921,7 @@ lsm_status lsm_predecessor(lsm_t* h, const uint32_t* d_q, uint64_t nq, uint32_t*
 lsm_status lsm_count(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2, uint64_t nq,
                      uint32_t* d_counts_out, void* stream) {
   if (!h) return LSM_ERR_INVALID_ARG;
+  ENTER(h);
   if (nq == 0) return LSM_OK;
   if (!d_k1 || !d_k2 || !d_counts_out) return LSM_ERR_INVALID_ARG;
   CK(ensure_index(h, S(stream), hooks(h)));
@@ -915,42 +933,49 @@ lsm_status lsm_count(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2, uint6
 lsm_status lsm_range(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2, uint64_t nq,
                      uint64_t* d_offsets_out, uint32_t* d_keys_out, uint32_t* d_vals_out,
                      uint64_t capacity, uint64_t* total_out, void* stream) {
-  if (!h || !total_out) return LSM_ERR_INVALID_ARG;
+  if (!h || !total_out || !d_offsets_out) return LSM_ERR_INVALID_ARG;
   cudaStream_t s = S(stream);
-  if (!d_offsets_out) return LSM_ERR_INVALID_ARG;
-  if (nq == 0) {
-    CK(cudaMemsetAsync(d_offsets_out, 0, 8, s));
-    *total_out = 0;
-    return LSM_OK;
-  }
-  if (!d_k1 || !d_k2) return LSM_ERR_INVALID_ARG;
-  LaunchHooks hk = hooks(h);
-  if (capacity > 0 && (!d_keys_out || !d_vals_out)) return LSM_ERR_INVALID_ARG;
-  CK(ensure_index(h, s, hk));
-  LevelTable T = level_table(h);
-  if (range_block_ok(T)) {
-    // one pass over CTA blocks: count, look-back per block, write
-    CK(ensure_qbuf(h, range_block_scratch_words(nq) * 8, s));
-    CK(launch_range_block(T, d_k1, d_k2, nq, d_offsets_out, d_keys_out, d_vals_out, capacity,
-                          static_cast<unsigned long long*>(h->qbuf), s, hk));
-  } else {
-    // > 8 levels: one pass with a per-warp look-back
-    CK(ensure_qbuf(h, range_scratch_words(nq) * 8, s));
-    CK(launch_range(T, d_k1, d_k2, nq, d_offsets_out, d_keys_out, d_vals_out, capacity,
-                    static_cast<unsigned long long*>(h->qbuf), s, hk));
-  }
-  CK(cudaMemcpyAsync(h->h_pinned, d_offsets_out + nq, 8, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  const uint64_t total = h->h_pinned[0];
-  *total_out = total;
-  if (h->prof_on) {  // the pairs written (8 B each) join the range's bytes
-    for (auto it = h->prof.rbegin(); it != h->prof.rend(); ++it) {
-      if (it->cls == LSM_K_RANGE) {
-        it->bytes += 8.0 * (double)std::min(total, capacity);
-        break;
+  if (nq > 0 && (!d_k1 || !d_k2)) return LSM_ERR_INVALID_ARG;
+  if (nq > 0 && capacity > 0 && (!d_keys_out || !d_vals_out)) return LSM_ERR_INVALID_ARG;
+  size_t prof_slot = SIZE_MAX;
+  {
+    ENTER(h);
+    if (nq == 0) {
+      CK(cudaMemsetAsync(d_offsets_out, 0, 8, s));
+    } else {
+      LaunchHooks hk = hooks(h);
+      CK(ensure_index(h, s, hk));
+      LevelTable T = level_table(h);
+      // per-call look-back scratch (stream-ordered pool), so concurrent
+      // ranges on other streams never share status words
+      CallScratch sc(h, s);
+      if (range_block_ok(T)) {
+        // one pass over CTA blocks: count, look-back per block, write
+        CK(sc.get(range_block_scratch_words(nq) * 8));
+        CK(launch_range_block(T, d_k1, d_k2, nq, d_offsets_out, d_keys_out, d_vals_out, capacity,
+                              static_cast<unsigned long long*>(sc.p), s, hk));
+      } else {
+        // > 8 levels: one pass with a per-warp look-back
+        CK(sc.get(range_scratch_words(nq) * 8));
+        CK(launch_range(T, d_k1, d_k2, nq, d_offsets_out, d_keys_out, d_vals_out, capacity,
+                        static_cast<unsigned long long*>(sc.p), s, hk));
       }
+      if (h->prof_on && !h->prof.empty()) prof_slot = h->prof.size() - 1;
     }
   }
+  // the total needs the result on the host: wait without holding the lock
+  DeviceGuard dg(h->device);
+  uint64_t total = 0;
+  if (nq > 0) CK(cudaMemcpyAsync(&total, d_offsets_out + nq, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  *total_out = total;
+  if (prof_slot != SIZE_MAX) {  // the pairs written (8 B each) join the range's bytes
+    std::lock_guard<std::recursive_mutex> lk(h->mu);
+    if (prof_slot < h->prof.size() && h->prof[prof_slot].cls == LSM_K_RANGE)
+      h->prof[prof_slot].bytes += 8.0 * (double)std::min(total, capacity);
+  }
+  const lsm_status st = take_sticky(h, s);
+  if (st != LSM_OK) return st;
   if (total > capacity) return LSM_ERR_CAPACITY;
   return LSM_OK;
 }
@@ -959,6 +984,7 @@ lsm_status lsm_range(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2, uint6
 // 2) mark stale; 3) compact; 4) pad with placebos; 5) redistribute.
 lsm_status lsm_cleanup(lsm_t* h, void* stream) {
   if (!h) return LSM_ERR_INVALID_ARG;
+  ENTER(h);
   cudaStream_t s = S(stream);
   LaunchHooks hk = hooks(h);
   const uint64_t b = h->b;
@@ -1019,7 +1045,7 @@ lsm_status lsm_cleanup(lsm_t* h, void* stream) {
     if (r2 > 0) CK(launch_build_f1(h->sa_buf[h->sa_cur].keys, r2 * b, h->sa_idx, s, hk));
     h->sa_idx_ready = false;
     h->r = r2;
-    return LSM_OK;
+    return take_sticky(h, s);
   }
   // 5) new levels are views of C: ascending keys into ascending set bits of
   //    r' (R12), no copy
@@ -1045,7 +1071,7 @@ lsm_status lsm_cleanup(lsm_t* h, void* stream) {
     delete C;
   }
   h->r = r2;
-  return LSM_OK;
+  return take_sticky(h, s);  // the cleanup itself is complete either way
 }
 
 // ---------------- key-range sharding support ----------------
@@ -1054,15 +1080,17 @@ lsm_status lsm_shard_bucket(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_
                             uint32_t* d_keys_out, uint32_t* d_vals_out, uint8_t* d_ops_out,
                             uint32_t* d_perm_out, uint32_t* d_counts_out, void* stream) {
   if (!h || nshards == 0 || nshards > 64 || !d_counts_out) return LSM_ERR_INVALID_ARG;
+  ENTER(h);
   if (mode == 1 && (nshards & (nshards - 1))) return LSM_ERR_INVALID_ARG;
   if (n > 0 && (!d_keys || !d_keys_out)) return LSM_ERR_INVALID_ARG;
   if ((d_vals == nullptr) != (d_vals_out == nullptr) || (d_ops == nullptr) != (d_ops_out == nullptr))
     return LSM_ERR_INVALID_ARG;
   if (n > 0xFFFFFFFFull) return LSM_ERR_INVALID_ARG;
   cudaStream_t s = S(stream);
-  CK(ensure_qbuf(h, bucket_scratch_words(n, nshards) * 4, s));
+  CallScratch sc(h, s);
+  CK(sc.get(bucket_scratch_words(n, nshards) * 4));
   CK(launch_bucket(d_keys, d_vals, d_ops, n, nshards, mode, d_keys_out, d_vals_out, d_ops_out,
-                   d_perm_out, d_counts_out, static_cast<uint32_t*>(h->qbuf), s, hooks(h)));
+                   d_perm_out, d_counts_out, static_cast<uint32_t*>(sc.p), s, hooks(h)));
   return LSM_OK;
 }
 
@@ -1070,6 +1098,7 @@ lsm_status lsm_shard_scatter(lsm_t* h, const uint32_t* d_perm, const uint32_t* d
                              const uint8_t* d_found_in, uint64_t n, uint32_t* d_vals_out,
                              uint8_t* d_found_out, void* stream) {
   if (!h) return LSM_ERR_INVALID_ARG;
+  ENTER(h);
   if (n == 0) return LSM_OK;
   if (!d_perm || !d_vals_in || !d_vals_out || (d_found_in == nullptr) != (d_found_out == nullptr))
     return LSM_ERR_INVALID_ARG;
@@ -1082,6 +1111,7 @@ lsm_status lsm_shard_clip(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2, 
                           uint32_t lo, uint32_t hi, uint32_t* d_k1_out, uint32_t* d_k2_out,
                           void* stream) {
   if (!h) return LSM_ERR_INVALID_ARG;
+  ENTER(h);
   if (n == 0) return LSM_OK;
   if (!d_k1 || !d_k2 || !d_k1_out || !d_k2_out) return LSM_ERR_INVALID_ARG;
   CK(launch_clip(d_k1, d_k2, n, lo, hi, d_k1_out, d_k2_out, S(stream), hooks(h)));
@@ -1091,6 +1121,7 @@ lsm_status lsm_shard_clip(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2, 
 lsm_status lsm_shard_sum(lsm_t* h, const uint32_t* d_in, uint32_t parts, uint64_t n,
                          uint32_t* d_out, void* stream) {
   if (!h || parts == 0) return LSM_ERR_INVALID_ARG;
+  ENTER(h);
   if (n == 0) return LSM_OK;
   if (!d_in || !d_out) return LSM_ERR_INVALID_ARG;
   CK(launch_sum_parts(d_in, parts, n, d_out, S(stream), hooks(h)));
@@ -1103,6 +1134,7 @@ lsm_status lsm_shard_range_assemble(lsm_t* h, const uint64_t* d_offs, const uint
                                    uint32_t* d_keys_out, uint32_t* d_vals_out, uint64_t capacity,
                                    uint64_t* total_out, void* stream) {
   if (!h || parts == 0 || !total_out || !d_offsets_out) return LSM_ERR_INVALID_ARG;
+  ENTER(h);
   cudaStream_t s = S(stream);
   if (nq == 0) {
     CK(cudaMemsetAsync(d_offsets_out, 0, 8, s));
@@ -1113,14 +1145,18 @@ lsm_status lsm_shard_range_assemble(lsm_t* h, const uint64_t* d_offs, const uint
   if (capacity > 0 && (!d_keys_out || !d_vals_out || !d_keys_in || !d_vals_in))
     return LSM_ERR_INVALID_ARG;
   const uint64_t tb = align_up(nq * 4, 256);
-  CK(ensure_qbuf(h, tb + scan_scratch_words(nq) * 8, s));
-  uint8_t* qb = static_cast<uint8_t*>(h->qbuf);
-  CK(launch_range_assemble(d_offs, d_block_len, parts, nq, d_keys_in, d_vals_in, d_offsets_out,
-                           d_keys_out, d_vals_out, capacity, reinterpret_cast<uint32_t*>(qb),
-                           reinterpret_cast<uint64_t*>(qb + tb), s, hooks(h)));
-  CK(cudaMemcpyAsync(h->h_pinned, d_offsets_out + nq, 8, cudaMemcpyDeviceToHost, s));
+  {
+    CallScratch sc(h, s);
+    CK(sc.get(tb + scan_scratch_words(nq) * 8));
+    uint8_t* qb = static_cast<uint8_t*>(sc.p);
+    CK(launch_range_assemble(d_offs, d_block_len, parts, nq, d_keys_in, d_vals_in, d_offsets_out,
+                             d_keys_out, d_vals_out, capacity, reinterpret_cast<uint32_t*>(qb),
+                             reinterpret_cast<uint64_t*>(qb + tb), s, hooks(h)));
+  }
+  uint64_t total = 0;
+  CK(cudaMemcpyAsync(&total, d_offsets_out + nq, 8, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  *total_out = h->h_pinned[0];
+  *total_out = total;
   return *total_out > capacity ? LSM_ERR_CAPACITY : LSM_OK;
 }
 
@@ -1129,6 +1165,7 @@ lsm_status lsm_shard_pick(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_va
                           uint32_t* d_keys_out, uint32_t* d_vals_out, uint8_t* d_found_out,
                           void* stream) {
   if (!h || parts == 0) return LSM_ERR_INVALID_ARG;
+  ENTER(h);
   if (n == 0) return LSM_OK;
   if (!d_keys || !d_vals || !d_found || !d_keys_out || !d_vals_out) return LSM_ERR_INVALID_ARG;
   CK(launch_pick(d_keys, d_vals, d_found, parts, n, last, d_keys_out, d_vals_out, d_found_out,
@@ -1172,27 +1209,20 @@ lsm_status lsm_level_view(const lsm_t* h, uint32_t i, const uint32_t** d_keys,
 
 lsm_status lsm_sync(lsm_t* h, void* stream) {
   if (!h) return LSM_ERR_INVALID_ARG;
+  ENTER(h);
   cudaStream_t s = S(stream);
-  if (h->sort.err) {
-    CK(cudaMemcpyAsync(h->h_pinned + 1, h->sort.err, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    uint32_t v = (uint32_t)(h->h_pinned[1] & 0xFFFFFFFFu);
-    if (v) {
-      CK(cudaMemsetAsync(h->sort.err, 0, 4, s));
-      CK(cudaStreamSynchronize(s));
-      return LSM_ERR_KEY_DOMAIN;
-    }
-  } else {
-    CK(cudaStreamSynchronize(s));
-  }
+  CK(cudaStreamSynchronize(s));
+  const lsm_status st = take_sticky(h, s);
+  if (st != LSM_OK) return st;
   CK(cudaGetLastError());
   return LSM_OK;
 }
 
-uint64_t lsm_launch_count(const lsm_t* h) { return h ? h->launches : 0; }
+uint64_t lsm_launch_count(const lsm_t* h) { return h ? h->launches.load() : 0ull; }
 
 lsm_status lsm_profile_enable(lsm_t* h, int on) {
   if (!h) return LSM_ERR_INVALID_ARG;
+  ENTER(h);
   cudaDeviceSynchronize();
   for (auto& p : h->prof) {
     h->ev_free.push_back(p.e0);
@@ -1206,6 +1236,7 @@ lsm_status lsm_profile_enable(lsm_t* h, int on) {
 
 lsm_status lsm_profile_read(lsm_t* h, lsm_profile* out) {
   if (!h || !out) return LSM_ERR_INVALID_ARG;
+  ENTER(h);
   for (auto& p : h->prof) {
     CK(cudaEventSynchronize(p.e1));
     float ms = 0.f;

@@ -341,8 +341,9 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel_t(
   }
 }
 
-int g_num_sms = 0;
-uint64_t g_single_cap = 0;  // tiles the one-tile-per-CTA variant runs in one wave
+int g_num_sms_dev[kMaxDevices];
+uint64_t g_single_cap_dev[kMaxDevices];  // tiles the one-tile-per-CTA variant runs in one wave
+bool g_merge_attr_dev[kMaxDevices];
 
 }  // namespace
 
@@ -351,8 +352,8 @@ cudaError_t launch_merge(const uint32_t* ak, const uint32_t* av, uint64_t na,
                          uint32_t* ov, uint32_t* out_f1, cudaStream_t s, const LaunchHooks& hk) {
   const uint64_t total = na + nb;
   if (total == 0) return cudaSuccess;
-  static bool attr_set = false;
-  if (!attr_set) {
+  const int dv = dev_slot();
+  if (!g_merge_attr_dev[dv]) {
     cudaError_t e = cudaFuncSetAttribute(merge_kernel_t<kStages>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)sizeof(MergeSmemT<kStages>));
@@ -360,18 +361,16 @@ cudaError_t launch_merge(const uint32_t* ak, const uint32_t* av, uint64_t na,
     e = cudaFuncSetAttribute(merge_kernel_t<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(MergeSmemT<1>));
     if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&g_num_sms_dev[dv], cudaDevAttrMultiProcessorCount, dv);
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, merge_kernel_t<1>, kMergeThreads,
                                                       sizeof(MergeSmemT<1>)) != cudaSuccess)
       per_sm = 0;
-    g_single_cap = (uint64_t)per_sm * g_num_sms;
-    const char* env = std::getenv("GPULSM_MERGE_SINGLE");
-    if (env && env[0] == '0') g_single_cap = 0;
-    attr_set = true;
+    g_single_cap_dev[dv] = (uint64_t)per_sm * g_num_sms_dev[dv];
+    g_merge_attr_dev[dv] = true;
   }
+  const int g_num_sms = g_num_sms_dev[dv];
+  const uint64_t g_single_cap = g_single_cap_dev[dv];
   // outputs must be 16-byte aligned for the vector stores
   if ((reinterpret_cast<uintptr_t>(ok) | reinterpret_cast<uintptr_t>(ov)) & 15)
     return cudaErrorMisalignedAddress;

@@ -905,13 +905,14 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) range_kernel(
   const int L = NL > 0 ? NL : T.count;
   const uint32_t lane = lane_id();
   const uint64_t ntasks = (nq + 31) / 32;
-  // static assignment: warp w takes tasks w, w + nw, ... in increasing order.
-  // The grid is fully co-resident (sized from the occupancy), so the
-  // smallest unfinished task never waits on a task that has not started.
-  (void)ctr;
-  const uint64_t gw = ((uint64_t)blockIdx.x * kQThreads + threadIdx.x) / 32;
-  const uint64_t nw = (uint64_t)gridDim.x * kQThreads / 32;
-  for (uint64_t t = gw; t < ntasks; t += nw) {
+  // tasks are claimed in increasing order from an atomic counter: every task
+  // a look-back waits on was claimed earlier by a running warp, so the wait
+  // ends whatever else shares the GPU (no co-residency assumption)
+  while (true) {
+    unsigned long long tc = 0;
+    if (lane == 0) tc = atomicAdd(ctr, 1ull);
+    const uint64_t t = __shfl_sync(kFull, tc, 0);
+    if (t >= ntasks) break;
     const uint64_t i = t * 32 + lane;
     const bool act = i < nq;
     const uint32_t a = act ? __ldg(k1 + i) : 1u, z = act ? __ldg(k2 + i) : 0u;
@@ -1188,14 +1189,16 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) range_block_kernel(
   }
 }
 
-int g_sms = 0;
+int g_sms_dev[kMaxDevices];
+
+int sm_count() {
+  const int dv = dev_slot();
+  if (g_sms_dev[dv] == 0) cudaDeviceGetAttribute(&g_sms_dev[dv], cudaDevAttrMultiProcessorCount, dv);
+  return g_sms_dev[dv];
+}
 
 unsigned query_grid(uint64_t nq) {
-  if (g_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int g_sms = sm_count();
   const uint64_t warps = (nq + 31) / 32;
   const uint64_t want = (warps + kQThreads / 32 - 1) / (kQThreads / 32);
   return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)g_sms * kQCtasPerSm));
@@ -1208,8 +1211,7 @@ unsigned occ_grid(K kern, size_t smem) {
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kQThreads, smem) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
-  query_grid(1);
-  return (unsigned)(per_sm * g_sms);
+  return (unsigned)(per_sm * sm_count());
 }
 
 template <typename K>
@@ -1234,16 +1236,14 @@ cudaError_t dispatch_nl(int nl, F&& f) {
 
 }  // namespace
 
-int device_sms() {
-  query_grid(1);
-  return g_sms;
-}
+int device_sms() { return sm_count(); }
 
 cudaError_t launch_lookup(const LevelTable& T, const uint32_t* q, uint64_t nq,
                           uint32_t* vals_out, uint8_t* found_out, cudaStream_t s,
                           const LaunchHooks& hk) {
   if (nq == 0) return cudaSuccess;
-  static bool attr = false;
+  static bool attr_dev[kMaxDevices];
+  bool& attr = attr_dev[dev_slot()];
   if (!attr) {
     cudaError_t e = set_smem(lookup_kernel);
     if (e != cudaSuccess) return e;
@@ -1252,7 +1252,8 @@ cudaError_t launch_lookup(const LevelTable& T, const uint32_t* q, uint64_t nq,
   hk.begin(hk.ctx, LSM_K_LOOKUP, s);
 #if !defined(GPULSM_NO_MULTISEARCH)
   if (T.count >= 2 && T.count <= 4) {  // interleaved searches of all levels
-    static bool attr_n = false;
+    static bool attr_n_dev[kMaxDevices];
+    bool& attr_n = attr_n_dev[dev_slot()];
     if (!attr_n) {
       cudaError_t e = set_smem(lookup_n_kernel<2>);
       if (e == cudaSuccess) e = set_smem(lookup_n_kernel<3>);

@@ -13,9 +13,9 @@
 //    defined): the batch is sorted by (key variable, input position), which
 //    is unique, so ranks come from shared-memory atomics and no pass needs
 //    to be stable;
-//  * larger b, skewed key sets, or GPULSM_SORT=0 (the previous one-wave
-//    design: onesweep top-digit pass + bucket_sort_kernel): the onesweep-style
-//    LSD radix sort below, 4 passes of 8 bits over the 32-bit key variable.
+//  * larger b (more than one wave of tiles), or a handle that has seen a
+//    skewed key set: the onesweep-style LSD radix sort below, 4 passes of
+//    8 bits over the 32-bit key variable.
 // Notes on the LSD kernels follow. Every kernel is launched with programmatic
 // dependent launch (griddepcontrol) so its prologue overlaps the tail of its
 // predecessor. Measured on B200 with a %globaltimer probe
@@ -261,8 +261,7 @@ __global__ void __launch_bounds__(kSortThreads, 1) onesweep_pass_kernel(
     uint32_t* __restrict__ out_keys, uint32_t* __restrict__ out_vals, uint64_t b,
     const uint32_t* __restrict__ dbase, uint32_t* __restrict__ tile_st,
     uint32_t* __restrict__ group_st, uint32_t* __restrict__ tile_ctr, int use_ctr, int shift,
-    uint32_t* __restrict__ err, uint32_t epoch, uint32_t* __restrict__ out_f1,
-    uint32_t* __restrict__ bkt_out) {
+    uint32_t* __restrict__ err, uint32_t epoch, uint32_t* __restrict__ out_f1) {
   // use_ctr == 0 <=> all tiles are co-resident (one wave): the digit bases
   // then come from the totals of ALL groups (no histogram kernel)
   extern __shared__ __align__(16) uint8_t pass_smem[];
@@ -442,11 +441,6 @@ __global__ void __launch_bounds__(kSortThreads, 1) onesweep_pass_kernel(
   } else {  // exclusive scan of the global digit totals
     uint32_t t2;
     base = block_exclusive_scan<kSortThreads, uint32_t>(total, S.scan, &t2);
-    // MSD mode: publish the bucket (digit) starts and sizes for pass B
-    if (bkt_out != nullptr && tile == 0 && tid < kRadix) {
-      bkt_out[tid] = base;
-      bkt_out[kRadix + tid] = total;
-    }
   }
   if (tid < kRadix) S.goff[tid] = base + gp + wp - tstart;
   __syncthreads();
@@ -671,117 +665,11 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_sort_kernel(
   }
 }
 
-// pass B of MSD + local: CTA d sorts bucket d (all records whose top digit
-// is d, in input order after pass A) by the lower three digits
+// bucket pass of the MSD + rank mode: CTA d sorts bucket d (all records whose
+// top digit is d)
 constexpr int kBktThreads = 512;
 constexpr int kBktItems = 11;
 constexpr int kBktCap = kBktThreads * kBktItems;  // 5632
-
-struct BktSmem {
-  uint2 kv[2][kBktCap];  // interleaved (key, value)
-  LocalScratch<kBktThreads> L;
-  uint32_t run[kRadix];
-  uint32_t hist[kRadix];
-};
-
-__global__ void __launch_bounds__(kBktThreads, 2) bucket_sort_kernel(
-    const uint32_t* __restrict__ bkt, const uint32_t* __restrict__ ak,
-    const uint32_t* __restrict__ av, uint32_t* __restrict__ tk, uint32_t* __restrict__ tv,
-    uint32_t* __restrict__ out_keys, uint32_t* __restrict__ out_vals,
-    uint32_t* __restrict__ out_f1, uint32_t* __restrict__ overflow) {
-  extern __shared__ __align__(16) uint8_t bkt_smem[];
-  BktSmem& S = *reinterpret_cast<BktSmem*>(bkt_smem);
-  const int tid = threadIdx.x;
-  pdl_wait();
-  pdl_trigger();
-  const uint32_t d = blockIdx.x;
-#ifdef GPULSM_PROBE
-#define BPROBE(k) \
-  do { if (tid == 0 && g_probe) g_probe[5ull * 4096 * 8 + d * 8 + (k)] = gtimer(); } while (0)
-#else
-#define BPROBE(k) do {} while (0)
-#endif
-  BPROBE(0);
-#ifdef GPULSM_PROBE
-  if (tid == 0 && g_probe) { uint32_t sm; asm volatile("mov.u32 %0, %%smid;" : "=r"(sm)); g_probe[5ull * 4096 * 8 + d * 8 + 7] = sm + 1; }
-#endif
-  const uint32_t start = bkt[d], size = bkt[kRadix + d];
-  if (size == 0) return;
-  if (size <= (uint32_t)kBktCap) {
-    for (uint32_t p = tid; p < size; p += kBktThreads)
-      S.kv[0][p] = make_uint2(__ldg(ak + start + p), __ldg(av + start + p));
-    __syncthreads();
-    BPROBE(1);
-    int cur = 0;
-    for (int pass = 0; pass < kPasses - 1; ++pass) {
-      local_subpass_kv<kBktThreads, kBktItems>(S.kv[cur], size, S.kv[cur ^ 1], pass * kRadixBits,
-                                               S.L);
-      cur ^= 1;
-      BPROBE(2 + pass);
-    }
-    for (uint32_t p = tid; p < size; p += kBktThreads) {
-      const uint2 r = S.kv[cur][p];
-      const uint32_t g = start + p;
-      out_keys[g] = r.x;
-      out_vals[g] = r.y;
-      if (out_f1 != nullptr && (g & (kF1Step - 1)) == 0) out_f1[g / kF1Step] = r.x;
-    }
-    __syncthreads();
-    BPROBE(5);
-    return;
-  }
-  // Oversized bucket (skewed keys): correct but slow chunked LSD by this one
-  // CTA through global memory; the host switches to the 4-pass path for
-  // later batches when it sees the flag.
-  if (tid == 0) atomicOr(overflow, 1u);
-  uint32_t* fk = reinterpret_cast<uint32_t*>(S.kv[0]);  // 2 * kBktCap words
-  uint32_t* fv = fk + kBktCap;
-  const uint32_t* srck = ak + start;
-  const uint32_t* srcv = av + start;
-  for (int pass = 0; pass < kPasses - 1; ++pass) {
-    const int shift = pass * kRadixBits;
-    uint32_t* dk = (pass == kPasses - 2 ? out_keys : (pass & 1 ? (uint32_t*)ak : tk)) + start;
-    uint32_t* dv = (pass == kPasses - 2 ? out_vals : (pass & 1 ? (uint32_t*)av : tv)) + start;
-    for (int i = tid; i < kRadix; i += kBktThreads) S.hist[i] = 0;
-    __syncthreads();
-    for (uint32_t p = tid; p < size; p += kBktThreads)
-      atomicAdd(&S.hist[(srck[p] >> shift) & (kRadix - 1)], 1u);
-    __syncthreads();
-    uint32_t tot;
-    const uint32_t hv = tid < kRadix ? S.hist[tid] : 0u;
-    const uint32_t ex = block_exclusive_scan<kBktThreads, uint32_t>(hv, S.L.scan, &tot);
-    if (tid < kRadix) S.run[tid] = ex;
-    __syncthreads();
-    for (uint32_t c0 = 0; c0 < size; c0 += kBktCap) {
-      const uint32_t nc = min((uint32_t)kBktCap, size - c0);
-      // rank the chunk locally (stable), place it at the running offsets
-      local_subpass<kBktThreads, kBktItems>(srck + c0, srcv + c0, nc, fk, fv, shift, S.L,
-                                            nullptr);
-      // fk holds the chunk grouped by digit; L.tstart / L.cnt describe it
-      for (uint32_t p = tid; p < nc; p += kBktThreads) {
-        const uint32_t key = fk[p];
-        const uint32_t dg = (key >> shift) & (kRadix - 1);
-        const uint32_t g = S.run[dg] + (p - S.L.tstart[dg]);
-        dk[g] = key;
-        dv[g] = fv[p];
-      }
-      __syncthreads();
-      if (tid < kRadix) S.run[tid] += S.L.cnt[tid];
-      __syncthreads();
-    }
-    __threadfence_block();
-    srck = dk;
-    srcv = dv;
-    __syncthreads();
-  }
-  if (out_f1 != nullptr) {
-    __syncthreads();
-    for (uint32_t p = tid; p < size; p += kBktThreads) {
-      const uint32_t g = start + p;
-      if ((g & (kF1Step - 1)) == 0) out_f1[g / kF1Step] = out_keys[g];
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------
 // MSD + rank mode (default for one-wave batches). The batch
@@ -802,8 +690,8 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_sort_kernel(
 //    placebos carry 0, R5-R7) and the level's F1.
 // Skew fallbacks: a bin above kBinMax records is sorted by a stable
 // shared-memory LSD on the position then the key; a bucket above kBktCap is
-// regathered in input order from the raw batch and sorted by the chunked LSD
-// of bucket_sort_kernel. Both set the overflow flag, which moves the handle to
+// regathered in input order from the raw batch and sorted by a chunked
+// stable LSD through global memory. Both set the overflow flag, which moves the handle to
 // the 4-pass LSD for later batches.
 // ---------------------------------------------------------------------------
 // tiles of the scatter: MSD_THREADS threads x kSortItems records, 1024 / MSD_THREADS
@@ -958,111 +846,14 @@ struct RankSmem {
   uint32_t scan[kBktThreads / 32 + 1];
   uint32_t run[kRadix];
   uint32_t hist[kRadix];
-  uint64_t mb[2];  // fused merge: the run's records with this top digit
   uint32_t start_d, size_d;
 };
-
-// first position p of the sorted run K[0, n) with K[p] >= x (key variables),
-// whole warp: 32-ary search, each round one probe per lane (4 rounds at 2^20)
-__device__ __forceinline__ uint64_t warp_lower_bound_kv(const uint32_t* __restrict__ K, uint64_t n,
-                                                        uint32_t x) {
-  const uint32_t lane = lane_id();
-  uint64_t lo = 0, hi = n;  // answer in [lo, hi]; hi == n or K[hi] >= x
-  while (hi > lo) {
-    const uint64_t len = hi - lo, sz = (len + 31) / 32;
-    const uint64_t q = lo + (uint64_t)lane * sz;
-    const bool below = q < hi && __ldg(K + q) < x;
-    const uint32_t c = __popc(__ballot_sync(kFull, below));  // chunks starting below x
-    if (c == 0) break;                                        // K[lo] >= x
-    const uint64_t nlo = lo + (uint64_t)(c - 1) * sz + 1;
-    hi = min(hi, lo + (uint64_t)c * sz);
-    lo = nlo;
-  }
-  return lo;
-}
-
-// Fused first cascade step (A3): merge the sorted bucket d
-// (size records, newer, first on equal original keys, R1) with the run's
-// records of top digit d; the merged records land at start + a0, where a0 =
-// the run's records below digit d. Merge by ranks: an A record's output
-// position is its index plus the B records with a smaller original key, a B
-// record's is its index plus the A records with an original key <= its own
-// (binary searches in shared memory; a warp's stores stay nearly contiguous).
-// A is the bucket as (key, value) pairs in shared memory (A_SMEM) or as
-// (key, value) arrays in global memory (oversized bucket).
-template <bool A_SMEM>
-__device__ __forceinline__ void fused_merge(const uint2* As, const uint32_t* Ak,
-                                            const uint32_t* Av, uint32_t size,
-                                            const SortMerge& M, uint32_t start, RankSmem& S,
-                                            uint2* stage, uint32_t d) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (warp < 2) {
-    const uint64_t r = (warp == 1 && d == kRadix - 1)
-                           ? M.n
-                           : warp_lower_bound_kv(M.keys, M.n, (d + warp) << 24);
-    if (lane == 0) S.mb[warp] = r;
-  }
-  __syncthreads();
-  const uint64_t a0 = S.mb[0];
-  const uint32_t m0 = (uint32_t)(S.mb[1] - a0);
-  const uint32_t* bk;
-  const uint32_t* bv;
-  if (m0 <= (uint32_t)kBktCap) {  // stage the run's slice in shared memory
-    uint32_t* sk = reinterpret_cast<uint32_t*>(stage);
-    uint32_t* sv = sk + kBktCap;
-    for (uint32_t p = tid; p < m0; p += kBktThreads) {
-      sk[p] = __ldg(M.keys + a0 + p);
-      sv[p] = __ldg(M.vals + a0 + p);
-    }
-    bk = sk;
-    bv = sv;
-  } else {  // skewed run: merge from global memory
-    bk = M.keys + a0;
-    bv = M.vals + a0;
-  }
-  __syncthreads();
-  auto akey = [&](uint32_t i) { return A_SMEM ? As[i].x : Ak[i]; };
-  const uint64_t gb = start + a0;
-  auto put = [&](uint64_t g, uint32_t key, uint32_t val) {
-    M.out_keys[g] = key;
-    M.out_vals[g] = val;
-    if (M.out_f1 != nullptr && (g & (kF1Step - 1)) == 0) M.out_f1[g / kF1Step] = key;
-  };
-  for (uint32_t i = tid; i < size; i += kBktThreads) {  // A: + #B with orig < x
-    const uint32_t key = akey(i), x = key >> 1;
-    uint32_t lo = 0, n = m0;
-    while (n > 0) {
-      const uint32_t h = n >> 1;
-      if ((bk[lo + h] >> 1) < x) {
-        lo += h + 1;
-        n -= h + 1;
-      } else {
-        n = h;
-      }
-    }
-    put(gb + i + lo, key, A_SMEM ? As[i].y : Av[i]);
-  }
-  for (uint32_t j = tid; j < m0; j += kBktThreads) {  // B: + #A with orig <= y
-    const uint32_t key = bk[j], y = key >> 1;
-    uint32_t lo = 0, n = size;
-    while (n > 0) {
-      const uint32_t h = n >> 1;
-      if ((akey(lo + h) >> 1) <= y) {
-        lo += h + 1;
-        n -= h + 1;
-      } else {
-        n = h;
-      }
-    }
-    put(gb + j + lo, key, bv[j]);
-  }
-}
 
 __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
     const uint32_t* __restrict__ cnt, uint32_t* __restrict__ ak, uint32_t* __restrict__ ap,
     RawBatch in, uint64_t b, uint32_t* __restrict__ tk, uint32_t* __restrict__ tv,
     uint32_t* __restrict__ out_keys, uint32_t* __restrict__ out_vals, uint32_t* __restrict__ out_f1,
-    uint32_t* __restrict__ overflow, SortMerge M) {
+    uint32_t* __restrict__ overflow) {
   extern __shared__ __align__(16) uint8_t rank_smem[];
   RankSmem& S = *reinterpret_cast<RankSmem*>(rank_smem);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1098,7 +889,7 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
     __syncthreads();
   }
   const uint32_t start = S.start_d, size = S.size_d;
-  if (size == 0 && M.keys == nullptr) return;
+  if (size == 0) return;
   if (size > (uint32_t)kBktCap) {
     // oversized bucket (skewed keys): its region holds only the first
     // kBktCap records, so regather it in input order from the raw batch
@@ -1186,18 +977,12 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
       srcv = dv;
       __syncthreads();
     }
-    if (out_f1 != nullptr && M.keys == nullptr) {
+    if (out_f1 != nullptr) {
       __syncthreads();
       for (uint32_t p = tid; p < size; p += kBktThreads) {
         const uint32_t g = start + p;
         if ((g & (kF1Step - 1)) == 0) out_f1[g / kF1Step] = out_keys[g];
       }
-    }
-    if (M.keys != nullptr) {
-      __threadfence_block();
-      __syncthreads();
-      fused_merge<false>(nullptr, out_keys + start, out_vals + start, size, M, start, S,
-                         S.kv[0], d);
     }
     return;
   }
@@ -1339,34 +1124,28 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
     for (uint32_t p = tid; p < size; p += kBktThreads) S.kv[res][p].y = 0u;
   }
   RPB(5);
-  if (M.keys == nullptr) {
-    __syncthreads();
-    // ---- write the sorted bucket (key, value) and its F1 ----
+  __syncthreads();
+  // ---- write the sorted bucket (key, value) and its F1 ----
 #pragma unroll 4
-    for (uint32_t p = tid; p < size; p += kBktThreads) {
-      const uint2 kv = S.kv[res][p];
-      const uint32_t g = start + p;
-      out_keys[g] = kv.x;
-      out_vals[g] = kv.y;
-      if (out_f1 != nullptr && (g & (kF1Step - 1)) == 0) out_f1[g / kF1Step] = kv.x;
-    }
-    RPB(6);
-    return;
+  for (uint32_t p = tid; p < size; p += kBktThreads) {
+    const uint2 kv = S.kv[res][p];
+    const uint32_t g = start + p;
+    out_keys[g] = kv.x;
+    out_vals[g] = kv.y;
+    if (out_f1 != nullptr && (g & (kF1Step - 1)) == 0) out_f1[g / kF1Step] = kv.x;
   }
-  fused_merge<true>(S.kv[res], nullptr, nullptr, size, M, start, S, S.kv[res ^ 1], d);
+  RPB(6);
 }
 
-int g_sms = 0;
-bool g_attr = false;
-int g_sort_mode = -1;  // GPULSM_SORT: 0 = MSD + stable local LSD (previous), 1 = MSD + rank
+int g_sms_dev[kMaxDevices];
+bool g_attr_dev[kMaxDevices];
 
 }  // namespace
 
 static cudaError_t sort_attrs() {
-  if (!g_attr) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+  const int dv = dev_slot();
+  if (!g_attr_dev[dv]) {
+    cudaDeviceGetAttribute(&g_sms_dev[dv], cudaDevAttrMultiProcessorCount, dv);
     cudaError_t e = cudaFuncSetAttribute(sort_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)sizeof(HistSmem));
     if (e != cudaSuccess) return e;
@@ -1379,18 +1158,13 @@ static cudaError_t sort_attrs() {
     e = cudaFuncSetAttribute(small_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(SmallSmem));
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(bucket_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(BktSmem));
-    if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(msd_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(MsdSmem));
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(bucket_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(RankSmem));
     if (e != cudaSuccess) return e;
-    const char* m = getenv("GPULSM_SORT");
-    g_sort_mode = (m != nullptr && m[0] == '0') ? 0 : 1;
-    g_attr = true;
+    g_attr_dev[dv] = true;
   }
   return cudaSuccess;
 }
@@ -1404,9 +1178,7 @@ uint64_t sort_tmp_words(uint64_t b) {
 cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals,
                               const uint8_t* ops, int mode, uint64_t n, uint64_t b,
                               SortScratch& S, uint32_t* out_keys, uint32_t* out_vals,
-                              uint32_t* out_f1, cudaStream_t s, const LaunchHooks& hk,
-                              const SortMerge* merge, bool* fused) {
-  if (fused) *fused = false;
+                              uint32_t* out_f1, cudaStream_t s, const LaunchHooks& hk) {
   {
     cudaError_t e = sort_attrs();
     if (e != cudaSuccess) return e;
@@ -1434,13 +1206,13 @@ cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals
   uint32_t* group_st = S.status + (uint64_t)kPasses * tiles * kRadix;
   const uint64_t status_words = (uint64_t)kPasses * (tiles + groups) * kRadix;
   // one wave (1 CTA per SM) -> tile = blockIdx, no counter round trip
+  const int g_sms = g_sms_dev[dev_slot()];
   const int use_ctr = tiles > (uint64_t)g_sms ? 1 : 0;
   if (S.overflow_host && *S.overflow_host) S.lsd_only = true;  // skewed keys seen
 
-  // (2) MSD + local: pass A scatters by the top digit into 256 stable
-  //     buckets, pass B sorts each bucket by the other three digits in
-  //     shared memory (one CTA per bucket)
-  if (!use_ctr && !S.lsd_only && g_sort_mode == 1) {
+  // (2) MSD + rank: the scatter puts every record into its top-digit bucket,
+  //     the bucket pass sorts each bucket in shared memory (one CTA each)
+  if (!use_ctr && !S.lsd_only) {
     uint32_t* cnt = S.msd_cnt + (S.msd_parity ? kRadix : 0);
     uint32_t* cnt_next = S.msd_cnt + (S.msd_parity ? 0 : kRadix);
     S.msd_parity ^= 1;
@@ -1451,32 +1223,13 @@ cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals
     // bytes: keys + ops read (5 B), (key, position) written (8 B)
     hk.end(hk.ctx, LSM_K_SORT_PASS, (double)b * 13.0, s, 1);
     if (e != cudaSuccess) return e;
-    SortMerge M{};
-    if (merge != nullptr && merge->n + b <= 0xFFFFFFFFull) M = *merge;
     hk.begin(hk.ctx, LSM_K_SORT_PASS, s);
     e = launch_pdl(bucket_rank_kernel, (unsigned)kRadix, kBktThreads, sizeof(RankSmem), s,
                    (const uint32_t*)cnt, S.tmp_keys[0], S.tmp_vals[0], in, b, S.tmp_keys[1],
-                   S.tmp_vals[1], out_keys, out_vals, out_f1, S.overflow_dev, M);
+                   S.tmp_vals[1], out_keys, out_vals, out_f1, S.overflow_dev);
     // bytes: (key, position) read (8 B), value gathered (4 B), (key, value)
-    // written (8 B); fused: + the run read (8 B each) and written again
-    hk.end(hk.ctx, LSM_K_SORT_PASS, (double)b * 20.0 + (double)M.n * 16.0, s, 1);
-    if (fused) *fused = M.keys != nullptr;
-    return e;
-  }
-  if (!use_ctr && !S.lsd_only) {
-    hk.begin(hk.ctx, LSM_K_SORT_PASS, s);
-    e = launch_pdl(onesweep_pass_kernel<true>, (unsigned)tiles, kSortThreads, sizeof(PassSmem), s,
-                   in, (const uint32_t*)nullptr, (const uint32_t*)nullptr, S.tmp_keys[0],
-                   S.tmp_vals[0], b, (const uint32_t*)S.bases, tile_st, group_st, S.tile_ctr, 0,
-                   (kPasses - 1) * kRadixBits, S.err, epoch, (uint32_t*)nullptr, S.bkt);
-    hk.end(hk.ctx, LSM_K_SORT_PASS, (double)b * 17.0, s, 1);
-    if (e != cudaSuccess) return e;
-    hk.begin(hk.ctx, LSM_K_SORT_PASS, s);
-    e = launch_pdl(bucket_sort_kernel, (unsigned)kRadix, kBktThreads, sizeof(BktSmem), s,
-                   (const uint32_t*)S.bkt, (const uint32_t*)S.tmp_keys[0],
-                   (const uint32_t*)S.tmp_vals[0], S.tmp_keys[1], S.tmp_vals[1], out_keys, out_vals,
-                   out_f1, S.overflow_dev);
-    hk.end(hk.ctx, LSM_K_SORT_PASS, (double)b * 16.0, s, 1);
+    // written (8 B)
+    hk.end(hk.ctx, LSM_K_SORT_PASS, (double)b * 20.0, s, 1);
     return e;
   }
 
@@ -1505,12 +1258,12 @@ cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals
       e = launch_pdl(onesweep_pass_kernel<true>, (unsigned)tiles, kSortThreads, sizeof(PassSmem), s,
                      in, (const uint32_t*)nullptr, (const uint32_t*)nullptr, ok, ov, b,
                      (const uint32_t*)S.bases, ts, gs, S.tile_ctr + p, use_ctr, 0, S.err, epoch,
-                     (uint32_t*)(p == kPasses - 1 ? out_f1 : nullptr), (uint32_t*)nullptr);
+                     (uint32_t*)(p == kPasses - 1 ? out_f1 : nullptr));
     else
       e = launch_pdl(onesweep_pass_kernel<false>, (unsigned)tiles, kSortThreads, sizeof(PassSmem),
                      s, in, ik, iv, ok, ov, b, (const uint32_t*)(S.bases + p * kRadix), ts, gs,
                      S.tile_ctr + p, use_ctr, p * kRadixBits, S.err, epoch,
-                     (uint32_t*)(p == kPasses - 1 ? out_f1 : nullptr), (uint32_t*)nullptr);
+                     (uint32_t*)(p == kPasses - 1 ? out_f1 : nullptr));
     // bytes: pass 0 reads raw (k,v,op = 9 B) writes 8 B; others 16 B
     hk.end(hk.ctx, LSM_K_SORT_PASS, (double)b * (p == 0 ? 17.0 : 16.0), s, 1);
     if (e != cudaSuccess) return e;

@@ -713,11 +713,11 @@ def test_config_c4_shape_sampled():
         assert np.all(gff.cpu().numpy()[sure] == 1), name
 
 
-def test_kway_cascade_skewed_chunk():
-    # The one-pass cascade (kway.cu) cuts the merge at every 1024th record of
-    # the oldest level; a batch whose keys all fall into one narrow key range
-    # puts the whole batch into one chunk (over the shared-memory capacity),
-    # which must take the global-memory path -- bit-exact vs S1 regardless.
+def test_cascade_concentrated_batch():
+    # batches whose keys all fall into one narrow key range (400 keys) merged
+    # into uniform levels by t = 3 cascades: every merge tile (and every
+    # prefix chunk of a partitioned merge) straddling that range is dominated
+    # by one run -- bit-exact vs S1 regardless.
     b = 8192
     gpu, s1, o1 = GpuAdapter(b), oracle.ShadowLSM(b), oracle.OracleDict(b)
     seed = synth.SEED_BASE + 95
