@@ -738,3 +738,78 @@ def test_cascade_concentrated_batch():
     k1 = np.array([999_000, 1_000_100, 0], np.uint32)
     k2 = np.array([1_000_500, 1_000_200, 4_000_000], np.uint32)
     assert_queries_equal(gpu, o1, q, k1, k2, "skewed")
+
+
+def test_kmerge_concentrated_batch_over_capacity():
+    # b >= 32768: the cascade is one kmerge launch split by key-prefix tables.
+    # Batches whose 32768 keys all lie in 400 consecutive keys put one prefix
+    # chunk far over the shared-memory capacity: that chunk is merged by ranks
+    # from global memory -- bit-exact vs S1 regardless.
+    b = 32768
+    gpu, s1, o1 = GpuAdapter(b), oracle.ShadowLSM(b), oracle.OracleDict(b)
+    seed = synth.SEED_BASE + 96
+    for j in range(15):
+        if j in (3, 7, 14):
+            rng = np.random.default_rng(j)
+            k = rng.integers(1_000_000, 1_000_400, b).astype(np.uint32)
+            v = np.arange(j * b, (j + 1) * b, dtype=np.uint32)
+            d = (rng.integers(0, 4, b) == 0).astype(np.uint8)
+        else:
+            k, v, d = synth.updates(seed, j * b, b, delete_frac4=1, alphabet=4_000_000)
+        gpu.update(k, v, d)
+        s1.update(k, v, d)
+        o1.apply_batch(k, v, d)
+        assert_levels_equal(gpu, s1, f"batch {j}")
+    q = np.concatenate([np.arange(999_990, 1_000_410, dtype=np.uint32),
+                        synth.lookup_queries(seed, 2000, 15 * b, alphabet=4_000_000)])
+    k1 = np.array([999_000, 1_000_100, 0], np.uint32)
+    k2 = np.array([1_000_500, 1_000_200, 4_000_000], np.uint32)
+    assert_queries_equal(gpu, o1, q, k1, k2, "concentrated")
+    gpu.cleanup()
+    s1.cleanup()
+    o1.cleanup()
+    assert_levels_equal(gpu, s1, "concentrated cleanup")
+    assert_queries_equal(gpu, o1, q, k1, k2, "concentrated cleanup")
+
+
+def test_kmerge_more_runs_than_one_pass():
+    # r up to 257 with b = 32768: at r = 255 the cascade has t = 8 (9 runs,
+    # above kmerge's 8) and takes the iterated merges, whose output then gets
+    # its prefix table for later one-pass cascades
+    b = 32768
+    gpu, s1, o1 = GpuAdapter(b), oracle.ShadowLSM(b), oracle.OracleDict(b)
+    seed = synth.SEED_BASE + 97
+    for j in range(257):
+        k, v, d = synth.updates(seed, j * b, b, delete_frac4=1)
+        gpu.update(k, v, d)
+        s1.update(k, v, d)
+        o1.apply_batch(k, v, d)
+        if j + 1 in (3, 8, 127, 255, 256, 257):
+            assert_levels_equal(gpu, s1, f"r={j + 1}")
+    q = synth.lookup_queries(seed, 20_000, 257 * b)
+    k1, k2 = synth.range_queries(seed, 5000, 257 * b, 8)
+    assert_queries_equal(gpu, o1, q, k1, k2, "r=257")
+
+
+def test_kmerge_unaligned_views():
+    # b = 40003 (odd): staged batches, cleanup views and bulk-build views start
+    # at element offsets that are not 16-byte aligned; the kmerge staging
+    # copies read aligned supersets around them
+    b = 40003
+    _run_schedule(b, 11, synth.SEED_BASE + 98, frac4=1, alphabet=200_000, nlook=3000,
+                  nrange=500, cleanup_every=5)
+    gpu, s1 = GpuAdapter(b), oracle.ShadowLSM(b)
+    k, v, d = synth.updates(synth.SEED_BASE + 99, 0, 5 * b + 7, delete_frac4=1)
+    gpu.lsm.bulk_build(to_device(k), to_device(v), to_device(d))
+    s1.bulk_build(k, v, d)
+    for j in range(3):
+        kk, vv, dd = synth.updates(synth.SEED_BASE + 99, 6 * b + j * b, b, delete_frac4=1)
+        gpu.update(kk, vv, dd)
+        s1.update(kk, vv, dd)
+        assert_levels_equal(gpu, s1, f"bulk+{j}")
+    k2_, v2_, d2_ = synth.updates(synth.SEED_BASE + 99, 20 * b, 3 * b - 11, delete_frac4=1)
+    gpu.lsm.update_batches(to_device(k2_), to_device(v2_), to_device(d2_))
+    for j in range(3):
+        sl = slice(j * b, min(len(k2_), (j + 1) * b))
+        s1.update(k2_[sl], v2_[sl], d2_[sl])
+    assert_levels_equal(gpu, s1, "multi on views")
