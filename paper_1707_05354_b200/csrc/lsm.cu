@@ -123,9 +123,16 @@ inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 // tables; below it the 1 MB per-level tables are not worth
 // it and the iterated merge-path merges run (A/B: -DGPULSM_KWAY_MIN_B=...)
 #ifndef GPULSM_KWAY_MIN_B
-#define GPULSM_KWAY_MIN_B 32768
+#define GPULSM_KWAY_MIN_B 0xFFFFFFFFFFFFull
 #endif
-constexpr uint64_t kKwayMinB = GPULSM_KWAY_MIN_B;
+// A/B without a rebuild: GPULSM_KWAY_MIN_B=<b> in the environment (read once)
+uint64_t kway_min_b() {
+  static const uint64_t v = [] {
+    const char* e = std::getenv("GPULSM_KWAY_MIN_B");
+    return e ? (uint64_t)std::strtoull(e, nullptr, 0) : (uint64_t)GPULSM_KWAY_MIN_B;
+  }();
+  return v;
+}
 
 // Every entry point runs on the handle's device and restores the caller's
 // current device on return.
@@ -175,17 +182,17 @@ void hook_end(void* ctx, int cls, double bytes, cudaStream_t s, int nk) {
 
 LaunchHooks hooks(lsm* h) { return LaunchHooks{hook_begin, hook_end, h}; }
 
-lsm_status cuda_err(cudaError_t e) {
+lsm_status cuda_err(cudaError_t e, int line = 0) {
   if (e == cudaSuccess) return LSM_OK;
   if (e == cudaErrorMemoryAllocation) return LSM_ERR_OOM;
-  std::fprintf(stderr, "gpulsm: CUDA error %s\n", cudaGetErrorString(e));
+  std::fprintf(stderr, "gpulsm: CUDA error %s (lsm.cu:%d)\n", cudaGetErrorString(e), line);
   return LSM_ERR_CUDA;
 }
 
 #define CK(expr)                                  \
   do {                                            \
     cudaError_t _e = (expr);                      \
-    if (_e != cudaSuccess) return cuda_err(_e);   \
+    if (_e != cudaSuccess) return cuda_err(_e, __LINE__); \
   } while (0)
 
 cudaError_t pool_alloc(lsm* h, void** p, uint64_t bytes, cudaStream_t s) {
@@ -477,7 +484,7 @@ lsm_status lsm_create(uint64_t b, lsm_t** out) {
   if (!h) return LSM_ERR_OOM;
   h->device = dev;
   h->b = b;
-  h->kway = b >= kKwayMinB;
+  h->kway = b >= kway_min_b();
   cudaMemPoolProps props{};
   props.allocType = cudaMemAllocationTypePinned;
   props.location.type = cudaMemLocationTypeDevice;
@@ -619,6 +626,7 @@ static lsm_status prepare_insert(lsm_t* h, int t, cudaStream_t s) {
 static lsm_status cascade(lsm_t* h, const uint32_t* ck, const uint32_t* cv, const uint32_t* cp,
                           int t, cudaStream_t s, const LaunchHooks& hk) {
   const uint64_t b = h->b;
+  if (t == 0) return LSM_OK;  // the sort wrote level 0 (and do_update its prefix table)
   if (h->kway && t + 1 <= kKmMaxRuns && (b << t) < (1ull << 32)) {
     // one pass (kmerge.cu): [batch, level 0, ..., level t-1] -> level t,
     // with level t's F1 and prefix table

@@ -396,6 +396,8 @@ def test_launch_counter_counts_kernels():
     n2 = mid.launch_count
     mid.update(to_device(km), to_device(vm), to_device(dm))
     assert mid.launch_count - n2 == 2
+    mid.update(to_device(km), to_device(vm), to_device(dm))
+    assert mid.launch_count - n2 == 2 + 3  # sort (2) + one merge
     # multi-wave batch: histogram kernel + 4 passes
     big = pkg.GpuLSM(2_000_000)
     kb, vb, db = synth.updates(2, 0, 2_000_000)
