@@ -15,7 +15,7 @@ INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libgpulsm.so")
 BUILD = os.path.join(HERE, "_build")
 
-SOURCES = ["sort.cu", "merge.cu", "kmerge.cu", "query.cu", "scan.cu", "index.cu", "cleanup.cu", "shard.cu", "lsm.cu"]
+SOURCES = ["sort.cu", "merge.cu", "query.cu", "scan.cu", "index.cu", "cleanup.cu", "shard.cu", "lsm.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

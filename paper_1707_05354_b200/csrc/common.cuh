@@ -323,31 +323,6 @@ cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals
 
 // Stable merge on key>>1, A (newer) first on ties, into out[na+nb];
 // out_f1 (nullable) receives F1 of the output.
-// Key-prefix tables (kmerge.cu): P[x] = number of records of
-// a sorted run whose key variable has top kPrefixBits bits < x, for x in
-// [0, kPrefixes]; kPrefixes + 1 words.
-constexpr int kPrefixBits = 18;
-constexpr uint32_t kPrefixes = 1u << kPrefixBits;
-constexpr int kPrefixShift = 32 - kPrefixBits;
-inline uint64_t prefix_words() { return (uint64_t)kPrefixes + 1; }
-cudaError_t launch_build_prefix(const uint32_t* keys, uint64_t n, uint32_t* P, cudaStream_t s,
-                                const LaunchHooks& hk);
-// One-pass merge of up to kKmMaxRuns sorted runs (run 0 the newest: first on
-// equal original keys) into (ok, ov) of `total` records, with the output's
-// F1 and prefix table (both nullable). Every run needs its prefix table and
-// fewer than 2^32 records; keys / values 16-byte aligned with 16 elements of
-// readable slack past the end (the staging copies read aligned supersets).
-constexpr int kKmMaxRuns = 8;
-struct KmRuns {
-  const uint32_t* k[kKmMaxRuns];
-  const uint32_t* v[kKmMaxRuns];
-  const uint32_t* p[kKmMaxRuns];
-  int runs;
-};
-cudaError_t launch_kmerge(const KmRuns& R, uint64_t total, uint32_t* ok, uint32_t* ov,
-                          uint32_t* out_f1, uint32_t* out_p, cudaStream_t s,
-                          const LaunchHooks& hk);
-
 cudaError_t launch_merge(const uint32_t* ak, const uint32_t* av, uint64_t na,
                          const uint32_t* bk, const uint32_t* bv, uint64_t nb, uint32_t* ok,
                          uint32_t* ov, uint32_t* out_f1, cudaStream_t s, const LaunchHooks& hk);

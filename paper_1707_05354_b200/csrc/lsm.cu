@@ -43,8 +43,6 @@ struct Level {
   uint32_t* idx = nullptr;  // fence-key index F1 | F2 | F3
   bool idx_owned = false;   // allocated for a view (freed with the level)
   bool idx_ready = false;   // F2/F3 derived from F1
-  uint32_t* P = nullptr;    // key-prefix table (one-pass cascade, kmerge.cu)
-  bool P_owned = false;     // allocated for a view (freed with the level)
 };
 
 struct ProfRec {
@@ -62,12 +60,6 @@ struct lsm {
   Level level[LSM_MAX_LEVELS];
   Buffer home[LSM_MAX_LEVELS];
   uint32_t* home_idx[LSM_MAX_LEVELS] = {};  // index storage of each home level
-  // one-pass cascade (kmerge.cu): on when b >= kKwayMinB; every level and the
-  // sorted batch then carry a key-prefix table
-  bool kway = false;
-  uint32_t* home_P[LSM_MAX_LEVELS] = {};
-  uint32_t* sortout_P = nullptr;
-  uint32_t* sa_P[2] = {nullptr, nullptr};
   Buffer ping[2];         // merge ping-pong scratch
   Buffer sortout;         // sorted batch when t >= 1
   SortScratch sort{};
@@ -118,21 +110,6 @@ struct lsm {
 namespace {
 
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
-
-// Batch sizes from which the cascade runs as one kmerge launch over prefix
-// tables; below it the 1 MB per-level tables are not worth
-// it and the iterated merge-path merges run (A/B: -DGPULSM_KWAY_MIN_B=...)
-#ifndef GPULSM_KWAY_MIN_B
-#define GPULSM_KWAY_MIN_B 0xFFFFFFFFFFFFull
-#endif
-// A/B without a rebuild: GPULSM_KWAY_MIN_B=<b> in the environment (read once)
-uint64_t kway_min_b() {
-  static const uint64_t v = [] {
-    const char* e = std::getenv("GPULSM_KWAY_MIN_B");
-    return e ? (uint64_t)std::strtoull(e, nullptr, 0) : (uint64_t)GPULSM_KWAY_MIN_B;
-  }();
-  return v;
-}
 
 // Every entry point runs on the handle's device and restores the caller's
 // current device on return.
@@ -233,7 +210,6 @@ void level_release(lsm* h, int i, cudaStream_t s) {
     }
   }
   if (L.idx_owned && L.idx) cudaFreeAsync(L.idx, s);
-  if (L.P_owned && L.P) cudaFreeAsync(L.P, s);
   L = Level{};
 }
 
@@ -241,12 +217,6 @@ void level_release(lsm* h, int i, cudaStream_t s) {
 cudaError_t home_idx_ensure(lsm* h, int i, cudaStream_t s) {
   if (h->home_idx[i]) return cudaSuccess;
   return pool_alloc(h, (void**)&h->home_idx[i], idx_words(h->b << i) * 4, s);
-}
-
-// key-prefix table storage (prefix_words() words) allocated on first use
-cudaError_t ptab_ensure(lsm* h, uint32_t** P, cudaStream_t s) {
-  if (*P) return cudaSuccess;
-  return pool_alloc(h, (void**)P, prefix_words() * 4, s);
 }
 
 cudaError_t ensure_sort_scratch(lsm* h, cudaStream_t s) {
@@ -484,7 +454,6 @@ lsm_status lsm_create(uint64_t b, lsm_t** out) {
   if (!h) return LSM_ERR_OOM;
   h->device = dev;
   h->b = b;
-  h->kway = b >= kway_min_b();
   cudaMemPoolProps props{};
   props.allocType = cudaMemAllocationTypePinned;
   props.location.type = cudaMemLocationTypeDevice;
@@ -515,11 +484,7 @@ lsm_status lsm_destroy(lsm_t* h) {
     level_release(h, i, nullptr);
     buf_free(h->home[i], nullptr);
     if (h->home_idx[i]) cudaFreeAsync(h->home_idx[i], nullptr);
-    if (h->home_P[i]) cudaFreeAsync(h->home_P[i], nullptr);
   }
-  if (h->sortout_P) cudaFreeAsync(h->sortout_P, nullptr);
-  for (int k = 0; k < 2; ++k)
-    if (h->sa_P[k]) cudaFreeAsync(h->sa_P[k], nullptr);
   buf_free(h->ping[0], nullptr);
   buf_free(h->ping[1], nullptr);
   buf_free(h->sortout, nullptr);
@@ -608,11 +573,6 @@ static lsm_status prepare_insert(lsm_t* h, int t, cudaStream_t s) {
   CK(buf_ensure(h, h->home[t], b << t, s));
   CK(home_idx_ensure(h, t, s));
   if (t > 0) CK(buf_ensure(h, h->sortout, b, s));
-  if (h->kway) {
-    CK(ptab_ensure(h, &h->home_P[t], s));
-    if (t > 0) CK(ptab_ensure(h, &h->sortout_P, s));
-    if (t + 1 <= kKmMaxRuns) return LSM_OK;  // one kmerge: no ping-pong buffers
-  }
   if (t >= 2) {
     CK(buf_ensure(h, h->ping[0], b << (t - 1), s));
     CK(buf_ensure(h, h->ping[1], b << (t - 1), s));
@@ -623,29 +583,9 @@ static lsm_status prepare_insert(lsm_t* h, int t, cudaStream_t s) {
 // cascade (A3) of the sorted batch (ck, cv) with t = ffz(r) >= 1: while
 // level i is full, buffer <- merge(buffer, level i), newer first on ties
 // (PAPER.md:621-624); the last merge writes level t and its fence keys F1.
-static lsm_status cascade(lsm_t* h, const uint32_t* ck, const uint32_t* cv, const uint32_t* cp,
-                          int t, cudaStream_t s, const LaunchHooks& hk) {
+static lsm_status cascade(lsm_t* h, const uint32_t* ck, const uint32_t* cv, int t,
+                          cudaStream_t s, const LaunchHooks& hk) {
   const uint64_t b = h->b;
-  if (t == 0) return LSM_OK;  // the sort wrote level 0 (and do_update its prefix table)
-  if (h->kway && t + 1 <= kKmMaxRuns && (b << t) < (1ull << 32)) {
-    // one pass (kmerge.cu): [batch, level 0, ..., level t-1] -> level t,
-    // with level t's F1 and prefix table
-    KmRuns R;
-    std::memset(&R, 0, sizeof(R));
-    R.runs = t + 1;
-    R.k[0] = ck;
-    R.v[0] = cv;
-    R.p[0] = cp;
-    for (int i = 0; i < t; ++i) {
-      R.k[i + 1] = h->level[i].keys;
-      R.v[i + 1] = h->level[i].vals;
-      R.p[i + 1] = h->level[i].P;
-    }
-    CK(launch_kmerge(R, b << t, h->home[t].keys, h->home[t].vals, h->home_idx[t], h->home_P[t],
-                     s, hk));
-    for (int i = 0; i < t; ++i) level_release(h, i, s);  // levels 0..t-1 <- empty
-    return LSM_OK;
-  }
   for (int i = 0; i < t; ++i) {
     uint32_t* ok = (i == t - 1) ? h->home[t].keys : h->ping[i & 1].keys;
     uint32_t* ov = (i == t - 1) ? h->home[t].vals : h->ping[i & 1].vals;
@@ -656,7 +596,6 @@ static lsm_status cascade(lsm_t* h, const uint32_t* ck, const uint32_t* cv, cons
     ck = ok;
     cv = ov;
   }
-  if (h->kway) CK(launch_build_prefix(h->home[t].keys, b << t, h->home_P[t], s, hk));
   return LSM_OK;
 }
 
@@ -668,19 +607,7 @@ static void commit_insert(lsm_t* h, int t) {
   h->level[t].idx = h->home_idx[t];
   h->level[t].idx_owned = false;
   h->level[t].idx_ready = false;  // F2/F3 derived before the next query
-  h->level[t].P = h->kway ? h->home_P[t] : nullptr;
-  h->level[t].P_owned = false;
   h->r += 1;
-}
-
-// prefix table of a level view (cleanup / bulk build), one-pass cascade only
-static cudaError_t view_prefix(lsm_t* h, int i, cudaStream_t s, const LaunchHooks& hk) {
-  if (!h->kway) return cudaSuccess;
-  Level& L = h->level[i];
-  cudaError_t e = pool_alloc(h, (void**)&L.P, prefix_words() * 4, s);
-  if (e != cudaSuccess) return e;
-  L.P_owned = true;
-  return launch_build_prefix(L.keys, h->b << i, L.P, s, hk);
 }
 
 // ---------------- N2: GPU SA mode ----------------
@@ -708,40 +635,19 @@ static cudaError_t sa_idx_ensure(lsm* h, uint64_t n, cudaStream_t s) {
 }
 
 // merge the sorted batch (ck, cv) of b records into the array
-static lsm_status sa_merge_in(lsm_t* h, const uint32_t* ck, const uint32_t* cv,
-                              const uint32_t* cp, cudaStream_t s, const LaunchHooks& hk) {
+static lsm_status sa_merge_in(lsm_t* h, const uint32_t* ck, const uint32_t* cv, cudaStream_t s,
+                              const LaunchHooks& hk) {
   const uint64_t b = h->b, n_old = h->r * b, n_new = n_old + b;
   CK(sa_idx_ensure(h, n_new, s));
   Buffer& dst = h->sa_buf[h->sa_cur ^ 1];
   CK(sa_buf_ensure(h, dst, n_new, s));
-  uint32_t* dp = nullptr;
-  if (h->kway) {
-    CK(ptab_ensure(h, &h->sa_P[0], s));
-    CK(ptab_ensure(h, &h->sa_P[1], s));
-    dp = h->sa_P[h->sa_cur ^ 1];
-  }
   if (n_old == 0) {
     CK(cudaMemcpyAsync(dst.keys, ck, b * 4, cudaMemcpyDeviceToDevice, s));
     CK(cudaMemcpyAsync(dst.vals, cv, b * 4, cudaMemcpyDeviceToDevice, s));
     CK(launch_build_f1(dst.keys, b, h->sa_idx, s, hk));
-    if (dp) CK(launch_build_prefix(dst.keys, b, dp, s, hk));
-  } else if (dp && cp && n_new < (1ull << 32)) {
-    // one kmerge of the batch (newer) with the array, split by prefix tables
-    const Buffer& src = h->sa_buf[h->sa_cur];
-    KmRuns R;
-    std::memset(&R, 0, sizeof(R));
-    R.runs = 2;
-    R.k[0] = ck;
-    R.v[0] = cv;
-    R.p[0] = cp;
-    R.k[1] = src.keys;
-    R.v[1] = src.vals;
-    R.p[1] = h->sa_P[h->sa_cur];
-    CK(launch_kmerge(R, n_new, dst.keys, dst.vals, h->sa_idx, dp, s, hk));
   } else {
     const Buffer& src = h->sa_buf[h->sa_cur];
     CK(launch_merge(ck, cv, b, src.keys, src.vals, n_old, dst.keys, dst.vals, h->sa_idx, s, hk));
-    if (dp) CK(launch_build_prefix(dst.keys, n_new, dp, s, hk));
   }
   h->sa_cur ^= 1;
   h->r += 1;
@@ -756,11 +662,7 @@ static lsm_status sa_update(lsm_t* h, const uint32_t* keys, const uint32_t* vals
   CK(buf_ensure(h, h->sortout, h->b, s));
   CK(launch_sort_batch(keys, vals, ops, mode, n, h->b, h->sort, h->sortout.keys,
                        h->sortout.vals, nullptr, s, hk));
-  if (h->kway) {
-    CK(ptab_ensure(h, &h->sortout_P, s));
-    CK(launch_build_prefix(h->sortout.keys, h->b, h->sortout_P, s, hk));
-  }
-  return sa_merge_in(h, h->sortout.keys, h->sortout.vals, h->kway ? h->sortout_P : nullptr, s, hk);
+  return sa_merge_in(h, h->sortout.keys, h->sortout.vals, s, hk);
 }
 
 lsm_status lsm_create_sa(uint64_t b, lsm_t** out) {
@@ -794,12 +696,7 @@ static lsm_status do_update(lsm_t* h, const uint32_t* keys, const uint32_t* vals
   uint32_t* sv = (t == 0) ? h->home[0].vals : h->sortout.vals;
   CK(launch_sort_batch(keys, vals, ops, mode, n, b, h->sort, sk, sv,
                        t == 0 ? h->home_idx[0] : nullptr, s, hk));
-  uint32_t* sp = nullptr;
-  if (h->kway) {  // the sorted batch's prefix table (level 0's when t == 0)
-    sp = (t == 0) ? h->home_P[0] : h->sortout_P;
-    CK(launch_build_prefix(sk, b, sp, s, hk));
-  }
-  st = cascade(h, sk, sv, sp, t, s, hk);
+  st = cascade(h, sk, sv, t, s, hk);
   if (st != LSM_OK) return st;
   commit_insert(h, t);
   return LSM_OK;
@@ -845,10 +742,6 @@ lsm_status lsm_bulk_build(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_va
     CK(launch_sort_batch(d_keys, d_vals, d_is_delete, mode, n, k * b, h->bulk, A.keys, A.vals,
                          h->sa_idx, s, hk));
     h->sort.lsd_only = h->sort.lsd_only || h->bulk.lsd_only;
-    if (h->kway && k * b < (1ull << 32)) {
-      CK(ptab_ensure(h, &h->sa_P[h->sa_cur], s));
-      CK(launch_build_prefix(A.keys, k * b, h->sa_P[h->sa_cur], s, hk));
-    }
     h->r = k;
     h->sa_idx_ready = false;
     return LSM_OK;
@@ -878,7 +771,6 @@ lsm_status lsm_bulk_build(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_va
     h->level[i].idx_owned = true;
     h->level[i].idx_ready = false;
     CK(launch_build_f1(h->level[i].keys, b << i, h->level[i].idx, s, hk));
-    CK(view_prefix(h, i, s, hk));
     off += b << i;
   }
   h->r = k;
@@ -907,12 +799,7 @@ lsm_status lsm_update_batches(lsm_t* h, const uint32_t* d_keys, const uint32_t* 
                           h->stage.vals, s, hk));
   for (uint64_t j = 0; j < k; ++j) {
     if (h->sa) {
-      if (h->kway) {
-        CK(ptab_ensure(h, &h->sortout_P, s));
-        CK(launch_build_prefix(h->stage.keys + j * b, b, h->sortout_P, s, hk));
-      }
-      lsm_status st = sa_merge_in(h, h->stage.keys + j * b, h->stage.vals + j * b,
-                                  h->kway ? h->sortout_P : nullptr, s, hk);
+      lsm_status st = sa_merge_in(h, h->stage.keys + j * b, h->stage.vals + j * b, s, hk);
       if (st != LSM_OK) return st;
       continue;
     }
@@ -925,10 +812,8 @@ lsm_status lsm_update_batches(lsm_t* h, const uint32_t* d_keys, const uint32_t* 
       CK(cudaMemcpyAsync(h->home[0].keys, ck, b * 4, cudaMemcpyDeviceToDevice, s));
       CK(cudaMemcpyAsync(h->home[0].vals, cv, b * 4, cudaMemcpyDeviceToDevice, s));
       CK(launch_build_f1(h->home[0].keys, b, h->home_idx[0], s, hk));
-      if (h->kway) CK(launch_build_prefix(h->home[0].keys, b, h->home_P[0], s, hk));
     } else {
-      if (h->kway) CK(launch_build_prefix(ck, b, h->sortout_P, s, hk));
-      st = cascade(h, ck, cv, h->kway ? h->sortout_P : nullptr, t, s, hk);
+      st = cascade(h, ck, cv, t, s, hk);
       if (st != LSM_OK) return st;
     }
     commit_insert(h, t);
@@ -1108,7 +993,6 @@ lsm_status lsm_cleanup(lsm_t* h, void* stream) {
     if ((h->r >> i) & 1ull) occ.push_back(i);
   if (occ.empty()) return LSM_OK;
   if (h->sa) occ.assign(1, 0);  // GPU SA: the one array, no merge
-  const std::vector<int> occ0 = occ;  // the occupied levels (released below)
   const uint64_t n = h->r * b;
   // 1) iterative merges, newer (lower index) first on ties
   const uint32_t* mk = h->sa ? h->sa_buf[h->sa_cur].keys : h->level[occ[0]].keys;
@@ -1118,23 +1002,6 @@ lsm_status lsm_cleanup(lsm_t* h, void* stream) {
   if (occ.size() > 1) {
     CK(buf_ensure(h, h->ping[0], n, s));
     CK(buf_ensure(h, h->ping[1], n, s));
-  }
-  if (!h->sa && h->kway && occ.size() > 1 && occ.size() <= (size_t)kKmMaxRuns &&
-      n < (1ull << 32)) {
-    // 1') one pass over all occupied levels (kmerge.cu), newest first
-    KmRuns R;
-    std::memset(&R, 0, sizeof(R));
-    R.runs = (int)occ.size();
-    for (size_t j = 0; j < occ.size(); ++j) {
-      R.k[j] = h->level[occ[j]].keys;
-      R.v[j] = h->level[occ[j]].vals;
-      R.p[j] = h->level[occ[j]].P;
-    }
-    CK(launch_kmerge(R, n, h->ping[0].keys, h->ping[0].vals, nullptr, nullptr, s, hk));
-    mk = h->ping[0].keys;
-    mv = h->ping[0].vals;
-    mn = n;
-    occ.resize(1);  // no pairwise merges left (the loop below is skipped)
   }
   for (size_t j = 1; j < occ.size(); ++j) {
     const int i = occ[j];
@@ -1176,17 +1043,13 @@ lsm_status lsm_cleanup(lsm_t* h, void* stream) {
     h->sa_buf[h->sa_cur] = *C;
     delete C;
     if (r2 > 0) CK(launch_build_f1(h->sa_buf[h->sa_cur].keys, r2 * b, h->sa_idx, s, hk));
-    if (r2 > 0 && h->kway) {
-      CK(ptab_ensure(h, &h->sa_P[h->sa_cur], s));
-      CK(launch_build_prefix(h->sa_buf[h->sa_cur].keys, r2 * b, h->sa_P[h->sa_cur], s, hk));
-    }
     h->sa_idx_ready = false;
     h->r = r2;
     return take_sticky(h, s);
   }
   // 5) new levels are views of C: ascending keys into ascending set bits of
   //    r' (R12), no copy
-  for (int i : occ0) level_release(h, i, s);
+  for (int i : occ) level_release(h, i, s);
   uint64_t off = 0;
   int refs = 0;
   for (int i = 0; i < LSM_MAX_LEVELS; ++i) {
@@ -1199,7 +1062,6 @@ lsm_status lsm_cleanup(lsm_t* h, void* stream) {
     h->level[i].idx_owned = true;
     h->level[i].idx_ready = false;
     CK(launch_build_f1(h->level[i].keys, b << i, h->level[i].idx, s, hk));
-    CK(view_prefix(h, i, s, hk));
     off += b << i;
     ++refs;
   }

@@ -7,21 +7,25 @@
 // (comparator (x >> 1) < (y >> 1)); reading R1 (the text, not Fig. 4's
 // argument order, fixes the tie rule).
 //
-// Design: a persistent, warp-specialised merge-path kernel.
-//  * grid = 2 CTAs per SM; CTA c owns a contiguous run of 4096-output tiles.
+// Design: a warp-specialised merge-path kernel.
+//  * persistent for large merges: 3 CTAs per SM (MERGE_CTAS), CTA c owns a
+//    contiguous run of 3840-output tiles; small merges (at most one wave of
+//    tiles) run a single-stage variant, one tile per CTA;
 //  * warp 0 (producer) finds the merge-path split of every tile boundary:
 //    a full 32-ary cooperative search (one ballot per round) for the CTA's
 //    first diagonal, then a search HINTED by the previous split (the next
-//    split lies within 4096 of it: 3 rounds). It then moves the tile's A and
-//    B windows (keys and values) into a 3-stage shared-memory ring with
-//    cp.async.bulk (TMA bulk copies, 16-byte aligned supersets of the
-//    windows) completing on an mbarrier (expect_tx).
+//    split lies within one tile of it). It then moves the tile's A and B
+//    windows (keys and values) into a 2-stage shared-memory ring
+//    (MERGE_STAGES) with cp.async.bulk (TMA bulk copies, 16-byte aligned
+//    supersets of the windows) completing on an mbarrier (expect_tx);
 //  * warps 1..8 (consumers) wait on the stage's mbarrier, each thread finds
-//    its own 16-output split inside the stage by binary search, merges 16
-//    records into registers and stores them with 128-bit writes, then
+//    its own 15-output split inside the stage by binary search (15 is odd:
+//    neighbouring lanes read ~7.5 words apart, no bank conflicts), merges 15
+//    keys into registers, gathers their values, stages the merged tile in
+//    place and one thread writes it with one TMA bulk store per array, then
 //    releases the stage.
-// The search latency and the loads of tiles k+1, k+2 overlap the merge of
-// tile k; there is no partition launch and no block-wide barrier in the loop.
+// The search latency and the loads of the next tile overlap the merge of
+// the current one; there is no partition launch.
 
 #include <algorithm>
 #include <cstdlib>

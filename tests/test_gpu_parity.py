@@ -742,11 +742,10 @@ def test_cascade_concentrated_batch():
     assert_queries_equal(gpu, o1, q, k1, k2, "skewed")
 
 
-def test_kmerge_concentrated_batch_over_capacity():
-    # b >= 32768: the cascade is one kmerge launch split by key-prefix tables.
-    # Batches whose 32768 keys all lie in 400 consecutive keys put one prefix
-    # chunk far over the shared-memory capacity: that chunk is merged by ranks
-    # from global memory -- bit-exact vs S1 regardless.
+def test_concentrated_batches_and_cleanup():
+    # one-wave batches (b = 32768) whose keys all lie in 400 consecutive keys:
+    # oversized sort buckets and merge tiles dominated by one run, then a
+    # cleanup merging several such levels -- bit-exact vs S1 regardless.
     b = 32768
     gpu, s1, o1 = GpuAdapter(b), oracle.ShadowLSM(b), oracle.OracleDict(b)
     seed = synth.SEED_BASE + 96
@@ -774,10 +773,9 @@ def test_kmerge_concentrated_batch_over_capacity():
     assert_queries_equal(gpu, o1, q, k1, k2, "concentrated cleanup")
 
 
-def test_kmerge_more_runs_than_one_pass():
-    # r up to 257 with b = 32768: at r = 255 the cascade has t = 8 (9 runs,
-    # above kmerge's 8) and takes the iterated merges, whose output then gets
-    # its prefix table for later one-pass cascades
+def test_nine_levels_r257():
+    # r up to 257 with b = 32768: cascades up to t = 8 (nine levels merged at
+    # r = 255) and the >8-level query kernels at r = 255
     b = 32768
     gpu, s1, o1 = GpuAdapter(b), oracle.ShadowLSM(b), oracle.OracleDict(b)
     seed = synth.SEED_BASE + 97
@@ -793,9 +791,9 @@ def test_kmerge_more_runs_than_one_pass():
     assert_queries_equal(gpu, o1, q, k1, k2, "r=257")
 
 
-def test_kmerge_unaligned_views():
+def test_unaligned_views():
     # b = 40003 (odd): staged batches, cleanup views and bulk-build views start
-    # at element offsets that are not 16-byte aligned; the kmerge staging
+    # at element offsets that are not 16-byte aligned; the merges' staging
     # copies read aligned supersets around them
     b = 40003
     _run_schedule(b, 11, synth.SEED_BASE + 98, frac4=1, alphabet=200_000, nlook=3000,
