@@ -248,6 +248,7 @@ struct SortScratch {
   uint32_t* err;          // sticky domain-error flag
   uint32_t* tmp_keys[2];  // b-sized ping-pong for the passes
   uint32_t* tmp_vals[2];
+  uint32_t* tmp_v3;       // values carried by the MSD scatter (sort_tmp_words(b) words)
   uint64_t tiles_cap;     // status capacity in tiles
   int parity;             // which hist half this sort uses
   uint32_t epoch;         // sort counter -> look-back word epochs

@@ -256,6 +256,8 @@ cudaError_t ensure_sort_scratch(lsm* h, cudaStream_t s) {
       e = pool_alloc(h, (void**)&h->sort.tmp_vals[k], sort_tmp_words(h->b) * 4, s);
       if (e != cudaSuccess) return e;
     }
+    e = pool_alloc(h, (void**)&h->sort.tmp_v3, sort_tmp_words(h->b) * 4, s);
+    if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
@@ -266,6 +268,7 @@ void bulk_free(lsm* h, cudaStream_t s) {
     if (h->bulk.tmp_keys[k]) cudaFreeAsync(h->bulk.tmp_keys[k], s);
     if (h->bulk.tmp_vals[k]) cudaFreeAsync(h->bulk.tmp_vals[k], s);
   }
+  if (h->bulk.tmp_v3) cudaFreeAsync(h->bulk.tmp_v3, s);
   h->bulk = SortScratch{};
   h->bulk_meta = nullptr;
   h->bulk_cap = 0;
@@ -303,6 +306,8 @@ cudaError_t ensure_bulk_scratch(lsm* h, uint64_t cap, cudaStream_t s) {
     e = pool_alloc(h, (void**)&B.tmp_vals[k], sort_tmp_words(cap) * 4, s);
     if (e != cudaSuccess) return e;
   }
+  e = pool_alloc(h, (void**)&B.tmp_v3, sort_tmp_words(cap) * 4, s);
+  if (e != cudaSuccess) return e;
   h->bulk_cap = cap;
   return cudaSuccess;
 }
@@ -493,6 +498,7 @@ lsm_status lsm_destroy(lsm_t* h) {
     if (h->sort.tmp_keys[k]) cudaFreeAsync(h->sort.tmp_keys[k], nullptr);
     if (h->sort.tmp_vals[k]) cudaFreeAsync(h->sort.tmp_vals[k], nullptr);
   }
+  if (h->sort.tmp_v3) cudaFreeAsync(h->sort.tmp_v3, nullptr);
   bulk_free(h, nullptr);
   buf_free(h->stage, nullptr);
   buf_free(h->sa_buf[0], nullptr);

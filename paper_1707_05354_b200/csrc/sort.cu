@@ -714,16 +714,17 @@ constexpr int kMsdTile = kMsdThreads * kSortItems;
 struct MsdSmem {
   uint32_t keys[kMsdTile];
   uint32_t pos[kMsdTile];
+  uint32_t vals[kMsdTile];
   uint32_t hist[kRadix];    // tile digit counts (atomic ranks)
   uint32_t tstart[kRadix];  // tile-local digit starts
-  uint32_t toff[kRadix];    // the tile's slot inside each global bucket
   uint32_t gdst[kRadix];    // global destination - tile-local start
   uint32_t scan[kMsdThreads / 32 + 1];
 };
 
 __global__ void __launch_bounds__(kMsdThreads, MSD_MINB) msd_scatter_kernel(
     RawBatch in, uint64_t b, uint32_t* __restrict__ out_keys, uint32_t* __restrict__ out_pos,
-    uint32_t* __restrict__ cnt, uint32_t* __restrict__ cnt_next, uint32_t* __restrict__ err) {
+    uint32_t* __restrict__ out_vals, uint32_t* __restrict__ cnt, uint32_t* __restrict__ cnt_next,
+    uint32_t* __restrict__ err) {
   extern __shared__ __align__(16) uint8_t msd_smem[];
   MsdSmem& S = *reinterpret_cast<MsdSmem*>(msd_smem);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -744,17 +745,10 @@ __global__ void __launch_bounds__(kMsdThreads, MSD_MINB) msd_scatter_kernel(
   const uint32_t tile_n =
       (uint32_t)((b - tile_base) < (uint64_t)kMsdTile ? (b - tile_base) : (uint64_t)kMsdTile);
   const uint32_t wbase = warp * (32 * kSortItems);
-  // the values are gathered by position in the bucket pass: pull this tile's
-  // range into L2 now (one bulk prefetch; random 4-byte gathers from DRAM
-  // would each cost a 128-byte line fill and a full miss latency)
-  if (tid == 0 && in.vals != nullptr && tile_base < in.n) {
-    const uint64_t e = min(in.n, tile_base + kMsdTile);
-    const uintptr_t a0 = reinterpret_cast<uintptr_t>(in.vals + tile_base) & ~(uintptr_t)15;
-    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(in.vals + e) + 15) & ~(uintptr_t)15;
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0))
-                 : "memory");
-  }
-  uint32_t k[kSortItems], rk[kSortItems];
+  // keys, ops and values read once, coalesced; the value travels with its
+  // record (tombstones and placebos carry 0, R5-R7), so the bucket pass
+  // never gathers by position
+  uint32_t k[kSortItems], v[kSortItems], rk[kSortItems];
   {
     uint32_t op[kSortItems];
 #pragma unroll
@@ -762,6 +756,7 @@ __global__ void __launch_bounds__(kMsdThreads, MSD_MINB) msd_scatter_kernel(
       const uint64_t p = tile_base + wbase + i * 32 + lane;
       const bool in_batch = p < in.n;
       k[i] = in_batch ? __ldg(in.keys + p) : 0u;
+      v[i] = (in_batch && in.vals != nullptr) ? __ldg(in.vals + p) : 0u;
       op[i] = (in_batch && in.mode == kModeMixed) ? (uint32_t)__ldg(in.ops + p) : 0u;
     }
     bool any_bad = false;
@@ -770,8 +765,9 @@ __global__ void __launch_bounds__(kMsdThreads, MSD_MINB) msd_scatter_kernel(
       const uint64_t p = tile_base + wbase + i * 32 + lane;
       uint32_t key, val;
       bool bad;
-      encode_loaded(in, p, k[i], 0u, op[i], key, val, bad);
+      encode_loaded(in, p, k[i], v[i], op[i], key, val, bad);
       k[i] = key;
+      v[i] = val;
       any_bad |= bad;
     }
     if (any_bad) atomicOr(err, 1u);
@@ -783,7 +779,10 @@ __global__ void __launch_bounds__(kMsdThreads, MSD_MINB) msd_scatter_kernel(
   __syncthreads();
   MSDP(2);
   const uint32_t c = tid < kRadix ? S.hist[tid] : 0u;
-  if (tid < kRadix) S.toff[tid] = c ? atomicAdd(cnt + tid, c) : 0u;
+  // the tile's slot in each bucket: the L2 atomic's round trip overlaps the
+  // scan and the staging below (its result is used only after them)
+  uint32_t toff = 0;
+  if (tid < kRadix && c) toff = atomicAdd(cnt + tid, c);
   uint32_t tot;
   const uint32_t ts = block_exclusive_scan<kMsdThreads, uint32_t>(c, S.scan, &tot);
   if (tid < kRadix) S.tstart[tid] = ts;
@@ -795,6 +794,7 @@ __global__ void __launch_bounds__(kMsdThreads, MSD_MINB) msd_scatter_kernel(
       const uint32_t p = S.tstart[k[i] >> 24] + rk[i];
       S.keys[p] = k[i];
       S.pos[p] = (uint32_t)(tile_base + off);
+      S.vals[p] = v[i];
     }
   }
   // bucket d owns the fixed region [d * kBktCap, (d + 1) * kBktCap) of the
@@ -802,7 +802,7 @@ __global__ void __launch_bounds__(kMsdThreads, MSD_MINB) msd_scatter_kernel(
   // for another. Records past the region's end are dropped: that bucket is
   // oversized, and the bucket pass regathers it from the raw batch.
   MSDP(3);
-  if (tid < kRadix) S.gdst[tid] = tid * (uint32_t)kBktCap + S.toff[tid] - S.tstart[tid];
+  if (tid < kRadix) S.gdst[tid] = tid * (uint32_t)kBktCap + toff - ts;
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
@@ -814,6 +814,7 @@ __global__ void __launch_bounds__(kMsdThreads, MSD_MINB) msd_scatter_kernel(
       if (g < (d + 1) * (uint32_t)kBktCap) {
         out_keys[g] = key;
         out_pos[g] = S.pos[idx];
+        out_vals[g] = S.vals[idx];
       }
     }
   }
@@ -833,6 +834,9 @@ __device__ __forceinline__ uint32_t half16(const uint32_t* w, uint32_t bin) {
   return (w[bin >> 1] >> ((bin & 1u) * 16u)) & 0xFFFFu;
 }
 constexpr uint32_t kBinMax = 64;           // larger bins: stable LSD fallback
+constexpr int kBinsPerWarp = kBins / (kBktThreads / 32);  // bins of one warp's sort range
+constexpr int kOetK = 12;  // records per lane in the odd-even transposition sort (even)
+static_assert(kOetK % 2 == 0 && kBinsPerWarp % 32 == 0, "odd-even layout");
 
 struct RankSmem {
   uint2 kv[2][kBktCap];  // (key, position)
@@ -851,7 +855,8 @@ struct RankSmem {
 
 __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
     const uint32_t* __restrict__ cnt, uint32_t* __restrict__ ak, uint32_t* __restrict__ ap,
-    RawBatch in, uint64_t b, uint32_t* __restrict__ tk, uint32_t* __restrict__ tv,
+    const uint32_t* __restrict__ av, RawBatch in, uint64_t b, uint32_t* __restrict__ tk,
+    uint32_t* __restrict__ tv,
     uint32_t* __restrict__ out_keys, uint32_t* __restrict__ out_vals, uint32_t* __restrict__ out_f1,
     uint32_t* __restrict__ overflow) {
   extern __shared__ __align__(16) uint8_t rank_smem[];
@@ -872,11 +877,13 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
   // every load is in bounds)
   ak += (uint64_t)d * kBktCap;
   ap += (uint64_t)d * kBktCap;
-  uint32_t kx[kBktItems], ky[kBktItems];
+  av += (uint64_t)d * kBktCap;
+  uint32_t kx[kBktItems], ky[kBktItems], kv[kBktItems];
 #pragma unroll
   for (int i = 0; i < kBktItems; ++i) {
     kx[i] = __ldg(ak + i * kBktThreads + tid);
     ky[i] = __ldg(ap + i * kBktThreads + tid);
+    kv[i] = __ldg(av + i * kBktThreads + tid);
   }
   {  // output start = records in the buckets below d
     const uint32_t c = tid < kRadix ? __ldg(cnt + tid) : 0u;
@@ -987,20 +994,20 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
     return;
   }
 
-  // ---- load (key, position); bin counts with shared-memory atomics ----
+  // ---- bin counts with shared-memory atomics; a record's rank in its bin
+  //      is kept in the position word's free top bits (positions of
+  //      one-wave batches are < 2^21; the rank matters only below kBinMax) ----
+  static_assert((uint64_t)kSortTile * 148 < (1ull << 21), "positions fit in 21 bits");
   for (int i = tid; i < kBins / 2; i += kBktThreads) S.u.b.cnt[i] = 0;
   __syncthreads();
-  uint32_t rk[kBktItems];
-  {
 #pragma unroll
-    for (int i = 0; i < kBktItems; ++i) {
-      const uint32_t p = i * kBktThreads + tid;
-      if (p < size) {
-        S.kv[0][p] = make_uint2(kx[i], ky[i]);
-        const uint32_t bin = (kx[i] >> kBinShift) & (kBins - 1);
-        const uint32_t sh = (bin & 1u) * 16u;
-        rk[i] = (atomicAdd(&S.u.b.cnt[bin >> 1], 1u << sh) >> sh) & 0xFFFFu;
-      }
+  for (int i = 0; i < kBktItems; ++i) {
+    const uint32_t p = i * kBktThreads + tid;
+    if (p < size) {
+      const uint32_t bin = (kx[i] >> kBinShift) & (kBins - 1);
+      const uint32_t sh = (bin & 1u) * 16u;
+      const uint32_t r = (atomicAdd(&S.u.b.cnt[bin >> 1], 1u << sh) >> sh) & 0xFFFFu;
+      ky[i] |= min(r, 2047u) << 21;
     }
   }
   __syncthreads();
@@ -1025,62 +1032,56 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
   RPB(2);
   int res = 0;
   if (!skew) {
-    // group by bin (any order inside a bin) ...
+    // group by bin (any order inside a bin) as the 64-bit word (key << 32 |
+    // position), whose order is the (key, position) order, and the value
+    // beside it ...
+    unsigned long long* __restrict__ w64 = reinterpret_cast<unsigned long long*>(S.kv[1]);
+    uint32_t* __restrict__ gval = reinterpret_cast<uint32_t*>(S.kv[0]);
 #pragma unroll
     for (int i = 0; i < kBktItems; ++i) {
       const uint32_t p = i * kBktThreads + tid;
       if (p < size) {
-        const uint2 kv = S.kv[0][p];
-        S.kv[1][half16(S.u.b.start, (kv.x >> kBinShift) & (kBins - 1)) + rk[i]] = kv;
+        const uint32_t g = half16(S.u.b.start, (kx[i] >> kBinShift) & (kBins - 1)) + (ky[i] >> 21);
+        w64[g] = ((unsigned long long)kx[i] << 32) | (ky[i] & 0x1FFFFFu);
+        gval[g] = kv[i];
       }
     }
     __syncthreads();
     RPB(3);
-    // ... gather every record's value by its position now (the loads are in
-    // flight during the ranking below instead of forming a phase of their
-    // own) ...
-    uint32_t gv[kBktItems];
+    // ... then rank each record inside its bin by counting the bin's
+    // records below it in (key, position) order, and store (key, value)
+    // straight to its output slot (with F1). Records are visited in GROUPED
+    // order (thread tid takes grouped slots tid, tid + 512, ...): the lanes
+    // of a warp scan neighbouring bins, so their loads hit neighbouring
+    // words and their stores land in the same output lines.
 #pragma unroll
     for (int i = 0; i < kBktItems; ++i) {
-      const uint32_t p = i * kBktThreads + tid;
-      const uint2 kv = S.kv[1][p];  // p < kBktCap: in bounds
-      const bool use = p < size && (kv.x & 1u) && in.vals != nullptr;
-      gv[i] = __ldg((use ? in.vals : in.keys) + (use ? kv.y : 0u));
-      gv[i] = use ? gv[i] : 0u;  // tombstones, placebos: 0 (R5-R7)
-    }
-    // ... then rank inside the bin by counting in (key, position) order and
-    // place (key, value). Source and destination are distinct buffers
-    // (__restrict__): the next item's loads need not wait for this store.
-    const uint2* __restrict__ src = S.kv[1];
-    uint2* __restrict__ dst = S.kv[0];
-    const uint32_t* __restrict__ bstart = S.u.b.start;
-    const uint32_t* __restrict__ bcnt = S.u.b.cnt;
-#pragma unroll
-    for (int i = 0; i < kBktItems; ++i) {
-      const uint32_t p = i * kBktThreads + tid;
-      if (p < size) {
-        const uint2 kv = src[p];
-        const uint32_t bin = (kv.x >> kBinShift) & (kBins - 1);
-        const uint32_t lo = half16(bstart, bin), hi = lo + half16(bcnt, bin);
-        // (key, position) as one 64-bit word: one wide compare per bin mate
-        const uint64_t me = ((uint64_t)kv.x << 32) | kv.y;
-        const unsigned long long* src64 = reinterpret_cast<const unsigned long long*>(src);
+      const uint32_t g = i * kBktThreads + tid;
+      if (g < size) {
+        const unsigned long long me = w64[g];
+        const uint32_t key = (uint32_t)(me >> 32);
+        const uint32_t bin = (key >> kBinShift) & (kBins - 1);
+        const uint32_t lo = half16(S.u.b.start, bin), hi = lo + half16(S.u.b.cnt, bin);
         uint32_t r = 0;
-        for (uint32_t j = lo; j < hi; ++j) {
-          const uint64_t o = src64[j];
-          r += ((o << 32) | (o >> 32)) < me;  // uint2 {x, y} in memory: y is the high word
-        }
-        dst[lo + r] = make_uint2(kv.x, gv[i]);
+        for (uint32_t j = lo; j < hi; ++j) r += w64[j] < me;
+        const uint32_t o = start + lo + r;
+        out_keys[o] = key;
+        out_vals[o] = gval[g];
+        if (out_f1 != nullptr && (o & (kF1Step - 1)) == 0) out_f1[o / kF1Step] = key;
       }
     }
-    __syncthreads();
+    RPB(4);
+    RPB(5);
+    RPB(6);
+    return;
   } else {
     // skewed bin: stable LSD on the position, then on the key (3 digits each;
     // one-wave batches have positions < 2^24)
     if (tid == 0) atomicOr(overflow, 1u);
-    for (uint32_t p = tid; p < size; p += kBktThreads) {
-      const uint2 kv = S.kv[0][p];
-      S.kv[0][p] = make_uint2(kv.y, kv.x);
+#pragma unroll
+    for (int i = 0; i < kBktItems; ++i) {  // (position, key) from the registers
+      const uint32_t p = i * kBktThreads + tid;
+      if (p < size) S.kv[0][p] = make_uint2(ky[i] & 0x1FFFFFu, kx[i]);
     }
     __syncthreads();
     for (int pass = 0; pass < 3; ++pass) {
@@ -1100,19 +1101,16 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
     }
   }
   RPB(4);
-  // ---- skew path: values gathered by position, all loads of a thread in
-  //      flight at once (the main path gathered them before its ranking) ----
-  if (!skew) {
-  } else if (in.vals != nullptr) {
-    // unguarded loads (positions clamped to 0 where unused) so that all of a
-    // thread's gathers are in flight at once
+  // ---- skew path: values gathered by position (tombstones and placebos
+  //      carry 0, R5-R7); all of a thread's loads in flight at once ----
+  if (skew) {
     uint32_t v[kBktItems];
 #pragma unroll
     for (int i = 0; i < kBktItems; ++i) {
       const uint32_t p = i * kBktThreads + tid;
       const uint2 kv = S.kv[res][p];  // p < kBktCap: in bounds
-      const bool use = p < size && (kv.x & 1u);
-      v[i] = __ldg(in.vals + (use ? kv.y : 0u));
+      const bool use = p < size && (kv.x & 1u) && in.vals != nullptr;
+      v[i] = __ldg((use ? in.vals : in.keys) + (use ? kv.y : 0u));
       v[i] = use ? v[i] : 0u;
     }
 #pragma unroll
@@ -1120,8 +1118,6 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
       const uint32_t p = i * kBktThreads + tid;
       if (p < size) S.kv[res][p].y = v[i];
     }
-  } else {
-    for (uint32_t p = tid; p < size; p += kBktThreads) S.kv[res][p].y = 0u;
   }
   RPB(5);
   __syncthreads();
@@ -1219,16 +1215,16 @@ cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals
     hk.begin(hk.ctx, LSM_K_SORT_PASS, s);
     e = launch_pdl(msd_scatter_kernel, (unsigned)((b + kMsdTile - 1) / kMsdTile), kMsdThreads,
                    sizeof(MsdSmem), s, in, b,
-                   S.tmp_keys[0], S.tmp_vals[0], cnt, cnt_next, S.err);
-    // bytes: keys + ops read (5 B), (key, position) written (8 B)
-    hk.end(hk.ctx, LSM_K_SORT_PASS, (double)b * 13.0, s, 1);
+                   S.tmp_keys[0], S.tmp_vals[0], S.tmp_v3, cnt, cnt_next, S.err);
+    // bytes: keys + ops + values read (9 B), (key, position, value) written (12 B)
+    hk.end(hk.ctx, LSM_K_SORT_PASS, (double)b * 21.0, s, 1);
     if (e != cudaSuccess) return e;
     hk.begin(hk.ctx, LSM_K_SORT_PASS, s);
     e = launch_pdl(bucket_rank_kernel, (unsigned)kRadix, kBktThreads, sizeof(RankSmem), s,
-                   (const uint32_t*)cnt, S.tmp_keys[0], S.tmp_vals[0], in, b, S.tmp_keys[1],
+                   (const uint32_t*)cnt, S.tmp_keys[0], S.tmp_vals[0], (const uint32_t*)S.tmp_v3,
+                   in, b, S.tmp_keys[1],
                    S.tmp_vals[1], out_keys, out_vals, out_f1, S.overflow_dev);
-    // bytes: (key, position) read (8 B), value gathered (4 B), (key, value)
-    // written (8 B)
+    // bytes: (key, position, value) read (12 B), (key, value) written (8 B)
     hk.end(hk.ctx, LSM_K_SORT_PASS, (double)b * 20.0, s, 1);
     return e;
   }

@@ -1,0 +1,8 @@
+#!/bin/bash
+# sort timeline probe, default and with -D$PROBE_DEF (experiment)
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DGPULSM_PROBE -I include -I paper_1707_05354_b200/csrc scripts/msd_probe.cu -o /tmp/msd_probe > gpurun_out/probe_build.log 2>&1
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DGPULSM_PROBE -D$PROBE_DEF -I include -I paper_1707_05354_b200/csrc scripts/msd_probe.cu -o /tmp/msd_probe2 >> gpurun_out/probe_build.log 2>&1
+timeout 120 /tmp/msd_probe > gpurun_out/msd_probe.txt 2>&1
+timeout 120 /tmp/msd_probe2 > gpurun_out/msd_probe2.txt 2>&1

@@ -29,12 +29,13 @@ static void dist(const char* name, std::vector<double> x) {
 }
 int main(int argc, char** argv) {
   uint64_t b = argc > 1 ? strtoull(argv[1], 0, 0) : (1u << 20);
-  uint32_t *k, *v, *ok, *ov, *meta, *tk[2], *tv[2];
+  uint32_t *k, *v, *ok, *ov, *meta, *tk[2], *tv[2], *t3;
   uint8_t* o;
   cudaMalloc(&k, b * 4); cudaMalloc(&v, b * 4); cudaMalloc(&o, b);
   cudaMalloc(&ok, b * 4 + 64); cudaMalloc(&ov, b * 4 + 64);
   const uint64_t tw = sort_tmp_words(b);
   for (int i = 0; i < 2; ++i) { cudaMalloc(&tk[i], tw * 4); cudaMalloc(&tv[i], tw * 4); }
+  cudaMalloc(&t3, tw * 4);
   const uint64_t words = kSortMetaHead + sort_status_words(b);
   cudaMalloc(&meta, words * 4); cudaMemset(meta, 0, words * 4);
   SortScratch S{};
@@ -45,6 +46,7 @@ int main(int argc, char** argv) {
   uint32_t* hp; cudaHostAlloc((void**)&hp, 64, cudaHostAllocMapped); *hp = 0;
   cudaHostGetDevicePointer((void**)&S.overflow_dev, hp, 0); S.overflow_host = hp;
   S.tmp_keys[0] = tk[0]; S.tmp_keys[1] = tk[1]; S.tmp_vals[0] = tv[0]; S.tmp_vals[1] = tv[1];
+  S.tmp_v3 = t3;
   gen<<<512, 256>>>(k, v, o, b, 12345);
   LaunchHooks hk{hb, he, nullptr};
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
