@@ -109,49 +109,99 @@ class ClockSampler:
 
 
 def cpu_baseline_oracle(seconds_budget=15.0):
-    """The oracle O1 on a bounded sample of C3: key-range sharded over all host
-    cores (SURVEY §8(d), the reported value) and the plain 1-thread std::map."""
+    """The oracle O1 on a bounded sample of C3: key-range sharded
+    over all host cores (the reported value) -- the first 56 batches are applied
+    untimed so the timed last 8 batches go into a map of ~2^25.6 live keys, as
+    on the GPU -- and the plain 1-thread std::map on the first batches (a
+    near-empty map: an upper bound for its rate), under single_thread."""
     import oracle
     seed = synth.SEED_BASE + 2
     threads = os.cpu_count() or 1
-    batches = [synth.updates(seed, j * B, B, delete_frac4=1) for j in range(8)]
-
-    def timed(make):
-        o = make()
-        nb = 0
-        t0 = time.perf_counter()
-        for k, v, d in batches:
-            o.apply_batch(k, v, d)
-            nb += 1
-            if time.perf_counter() - t0 > seconds_budget * 0.4:
-                break
-        t_upd = time.perf_counter() - t0
-        q = synth.lookup_queries(seed, 1 << 20, nb * B)
-        t1 = time.perf_counter()
-        o.lookup(q)
-        return nb, nb * B / t_upd / 1e6, (1 << 20) / (time.perf_counter() - t1) / 1e6
-
-    nb_t, upd_t, lk_t = timed(lambda: oracle.ShardedOracleDict(B, threads))
-    nb_1, upd_1, lk_1 = timed(lambda: oracle.OracleDict(B))
-    return {"value": upd_t, "unit": UNIT, "cores": threads, "kind": "oracle",
-            "sample": f"first {nb_t} of 64 C3 batches ({nb_t}x2^20 mixed updates) into {threads} "
-                      f"key-range std::map shards, one thread each; then 2^20 lookups",
-            "lookup_mqps": lk_t,
-            "single_thread": {"value": upd_1, "cores": 1, "batches": nb_1, "lookup_mqps": lk_1}}
+    o = oracle.ShardedOracleDict(B, threads)
+    t0 = time.perf_counter()
+    for j in range(R - 8):
+        o.apply_batch(*synth.updates(seed, j * B, B, delete_frac4=1))
+    prefill_s = time.perf_counter() - t0
+    tail = [synth.updates(seed, j * B, B, delete_frac4=1) for j in range(R - 8, R)]
+    t0 = time.perf_counter()
+    for k, v, d in tail:
+        o.apply_batch(k, v, d)
+    t_upd = time.perf_counter() - t0
+    q = synth.lookup_queries(seed, 1 << 20, R * B)
+    t1 = time.perf_counter()
+    o.lookup(q)
+    lk = (1 << 20) / (time.perf_counter() - t1) / 1e6
+    resident = len(o)
+    del o
+    one = oracle.OracleDict(B)
+    nb1 = 0
+    t0 = time.perf_counter()
+    for j in range(8):
+        one.apply_batch(*synth.updates(seed, j * B, B, delete_frac4=1))
+        nb1 += 1
+        if time.perf_counter() - t0 > seconds_budget * 0.3:
+            break
+    upd_1 = nb1 * B / (time.perf_counter() - t0) / 1e6
+    return {"value": 8 * B / t_upd / 1e6, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"C3 batches 57..64 (8x2^20 mixed updates) into {threads} key-range std::map "
+                      f"shards (one thread each) already holding batches 1..56 (untimed, "
+                      f"{prefill_s:.1f} s); then 2^20 lookups on the {resident} live keys",
+            "lookup_mqps": lk, "resident_after": resident,
+            "single_thread": {"value": upd_1, "cores": 1, "batches": nb1,
+                              "sample": "first C3 batches into one empty std::map"}}
 
 
 PARITY_LO, PARITY_HI = 5 << 25, 6 << 25  # 1/64 of the key domain
 
 
+def check_queries(o1, lo, hi, q=None, lv=None, lf=None, k1=None, k2=None, cnt=None,
+                  roff=None, rk=None, rv=None):
+    """Compare one structure's query outputs with O1 on the key sub-range [lo, hi):
+    O1 was fed only the updates whose key lies in [lo, hi) -- keys never interact
+    (PAPER.md:94-110), so it answers every query inside the interval exactly. For
+    range, the offsets of ALL queries must be the exclusive scan of the counts
+    (count == len(range)). Returns (failures, numbers checked)."""
+    from paper_1707_05354_b200 import to_numpy_u32
+    fails, n = [], {}
+    if q is not None:
+        gv, gf = to_numpy_u32(lv), lf.cpu().numpy()
+        sel = (q >= lo) & (q < hi)
+        ov, of = o1.lookup(q[sel])
+        if not (np.array_equal(gf[sel], of) and np.array_equal(gv[sel], ov)):
+            fails.append("lookup")
+        n["lookups"] = int(sel.sum())
+    if k1 is not None and cnt is not None:
+        gc = to_numpy_u32(cnt)
+        ins = (k1 >= lo) & (k2 < hi) & (k1 <= k2)
+        if not np.array_equal(gc[ins], o1.count(k1[ins], k2[ins])):
+            fails.append("count")
+        n["counts"] = int(ins.sum())
+        if roff is not None:
+            off = roff.cpu().numpy().astype(np.uint64)
+            if off[0] != 0 or not np.array_equal(np.diff(off), gc.astype(np.uint64)):
+                fails.append("range offsets != exclusive scan of counts")
+            idx = np.nonzero(ins)[0]
+            ooff, oks, ovs = o1.range(k1[idx], k2[idx])
+            lens = np.diff(ooff).astype(np.int64)
+            pos = np.repeat(off[idx].astype(np.int64), lens) + (
+                np.arange(int(lens.sum())) - np.repeat(ooff[:-1].astype(np.int64), lens))
+            pos_t = torch_index(pos, rk.device)
+            if not (np.array_equal(to_numpy_u32(rk[pos_t]), oks) and
+                    np.array_equal(to_numpy_u32(rv[pos_t]), ovs)):
+                fails.append("range pairs")
+            n["ranges"] = int(ins.sum())
+            n["pairs"] = int(lens.sum())
+            n["all_offsets_checked"] = len(off)
+    return fails, n
+
+
 def parity_gate(lsm, sub, q, k1, k2, lv, lf, cnt, roff, rk, rv, tot_pre, tot_post):
     """Check the timed step's outputs against the oracle before any number is
-    printed. O1 is fed only the updates whose key lies in [LO, HI) (keys never
-    interact, so it answers every query inside that interval
-    exactly); every lookup / count / range of the step inside the interval is
-    compared, the offsets of all NQ ranges must be the exclusive scan of the
-    counts, count == len(range), and the post-cleanup level image restricted
-    to the interval must equal O1's live pairs (R12). Exits non-zero on a
-    mismatch: no timing line is emitted."""
+    printed: every lookup / count / range of the step inside the key sub-range
+    (check_queries), the range totals before and after cleanup, and the
+    post-cleanup level image restricted to the interval against O1's live
+    pairs (R12). Exits non-zero on a mismatch: no timing line is emitted
+    (S:477)."""
     import oracle
     from paper_1707_05354_b200 import to_numpy_u32
     lo, hi = PARITY_LO, PARITY_HI
@@ -159,30 +209,10 @@ def parity_gate(lsm, sub, q, k1, k2, lv, lf, cnt, roff, rk, rv, tot_pre, tot_pos
     for k, v, d in sub:
         o1.apply_batch(k, v, d)
     o1.cleanup()
-    fails = []
-    gv, gf = to_numpy_u32(lv), lf.cpu().numpy()
-    sel = (q >= lo) & (q < hi)
-    ov, of = o1.lookup(q[sel])
-    if not (np.array_equal(gf[sel], of) and np.array_equal(gv[sel], ov)):
-        fails.append("lookup")
-    gc = to_numpy_u32(cnt)
-    ins = (k1 >= lo) & (k2 < hi) & (k1 <= k2)
-    if not np.array_equal(gc[ins], o1.count(k1[ins], k2[ins])):
-        fails.append("count")
-    off = roff.cpu().numpy().astype(np.uint64)
-    if off[0] != 0 or not np.array_equal(np.diff(off), gc.astype(np.uint64)):
-        fails.append("range offsets != exclusive scan of counts")
-    if not (tot_pre == tot_post == int(off[-1])):
+    fails, n = check_queries(o1, lo, hi, q, lv, lf, k1, k2, cnt, roff, rk, rv)
+    off_last = int(roff[-1].item())
+    if not (tot_pre == tot_post == off_last):
         fails.append("range totals before/after cleanup")
-    idx = np.nonzero(ins)[0]
-    ooff, oks, ovs = o1.range(k1[idx], k2[idx])
-    lens = np.diff(ooff).astype(np.int64)
-    pos = np.repeat(off[idx].astype(np.int64), lens) + (
-        np.arange(int(lens.sum())) - np.repeat(ooff[:-1].astype(np.int64), lens))
-    pos_t = torch_index(pos, rk.device)
-    if not (np.array_equal(to_numpy_u32(rk[pos_t]), oks) and
-            np.array_equal(to_numpy_u32(rv[pos_t]), ovs)):
-        fails.append("range pairs")
     # post-cleanup image inside [lo, hi): the encoded live pairs of O1
     ik, iv = [], []
     for i in range(lsm.r.bit_length()):
@@ -198,15 +228,278 @@ def parity_gate(lsm, sub, q, k1, k2, lv, lf, cnt, roff, rk, rv, tot_pre, tot_pos
     if fails:
         sys.stderr.write(f"PARITY FAILED: {fails}\n")
         sys.exit(3)
-    return {"ok": True, "oracle": "O1 (std::map) on the key sub-range [5*2^25, 6*2^25)",
-            "lookups": int(sel.sum()), "counts": int(ins.sum()), "ranges": int(ins.sum()),
-            "pairs": int(lens.sum()), "live_pairs_in_image": int(len(ok_)),
-            "all_offsets_checked": NQ + 1}
+    n.update({"ok": True, "oracle": "O1 (std::map) on the key sub-range [5*2^25, 6*2^25)",
+              "live_pairs_in_image": int(len(ok_))})
+    return n
+
+
+def gate(name, fails):
+    """Secondary configurations are parity-gated too: a mismatch ends the run."""
+    if fails:
+        sys.stderr.write(f"PARITY FAILED ({name}): {fails}\n")
+        sys.exit(3)
 
 
 def torch_index(pos, device):
     import torch
     return torch.from_numpy(pos).to(device)
+
+
+# ---------------------------------------------------------------------------
+# Secondary configurations (SURVEY.md §8(d), §8(f)); each parity-gated against
+# O1 on the key sub-range [PARITY_LO, PARITY_HI). Reported under "secondary".
+# ---------------------------------------------------------------------------
+
+def _ev_timer(stream):
+    import torch
+
+    def timed(fn, reps=3):
+        fn()
+        ts = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return float(np.median(ts))
+    return timed
+
+
+def _queries(lsm, dev, q, k1, k2, timed, cap_factor=1.3):
+    """lookup / count / range of the given queries (device tensors), timed;
+    returns (rates, output tensors)."""
+    import torch
+    nq = q.numel()
+    lv = torch.empty(nq, dtype=torch.int32, device=dev)
+    lf = torch.empty(nq, dtype=torch.uint8, device=dev)
+    nr = k1.numel()
+    cnt = torch.empty(nr, dtype=torch.int32, device=dev)
+    t_l = timed(lambda: lsm.lookup_into(q, lv, lf))
+    t_c = timed(lambda: lsm.count_into(k1, k2, cnt))
+    total = int(cnt.to(torch.int64).sum().item())
+    roff = torch.empty(nr + 1, dtype=torch.int64, device=dev)
+    rk = torch.empty(max(16, total + 16), dtype=torch.int32, device=dev)
+    rv = torch.empty(max(16, total + 16), dtype=torch.int32, device=dev)
+    got = []
+    t_r = timed(lambda: got.append(lsm.range_into(k1, k2, roff, rk, rv)))
+    rates = {"lookup_mqps": nq / (t_l * 1e-3) / 1e6, "count_mqps": nr / (t_c * 1e-3) / 1e6,
+             "range_mqps": nr / (t_r * 1e-3) / 1e6, "pairs_per_range": total / max(nr, 1),
+             "count_eq_len_range": got[-1] == total}
+    return rates, (lv, lf, cnt, roff, rk, rv)
+
+
+def _sub_oracle(b):
+    import oracle
+    return oracle.OracleDict(b)
+
+
+def extra_c2(pkg, dev, stream):
+    """C2 (BASELINE configs[1]; Table II protocol):
+    b = 2^16 insert-only, 64 batches from empty; every batch's insert time
+    (CUDA events around each lsm_update) -> min / max / harmonic mean rate
+    over r (R17); at r in {1, 3, 7, 15, 31, 63, 64}: nq = n lookups (50 %
+    hit), counts and ranges at L = 8."""
+    import torch
+    from paper_1707_05354_b200 import to_device
+    b, R2 = 1 << 16, 64
+    seed = synth.SEED_BASE + 1
+    timed = _ev_timer(stream)
+    data = [synth.updates(seed, j * b, b, delete_frac4=0) for j in range(R2)]
+    dd = [(to_device(k, dev), to_device(v, dev), to_device(d, dev)) for k, v, d in data]
+    lsm = pkg.GpuLSM(b, reserve_batches=R2)
+    o1 = _sub_oracle(b)
+    # (1) timing pass: the 64 inserts back to back, an event pair around each
+    for _ in range(2):  # warm-up cycles (pool allocations, index storage)
+        lsm.clear()
+        for j in range(R2):
+            lsm.update(*dd[j])
+    lsm.clear()
+    torch.cuda.synchronize()
+    per = []
+    for j in range(R2):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        lsm.update(*dd[j])
+        e1.record(stream)
+        per.append((e0, e1))
+    torch.cuda.synchronize()
+    # (2) query pass: the same inserts again, queries at the Table II-IV
+    #     occupancies, O1 fed alongside
+    lsm.clear()
+    rows = []
+    for j in range(R2):
+        lsm.update(*dd[j])
+        k, v, d = data[j]
+        m = (k >= PARITY_LO) & (k < PARITY_HI)
+        o1.apply_batch(k[m], v[m], d[m])
+        r = j + 1
+        if r in (1, 3, 7, 15, 31, 63, 64):
+            n = r * b
+            q = synth.lookup_queries(seed, n, n)
+            k1, k2 = synth.range_queries(seed, n, n, 8)
+            rates, outs = _queries(lsm, dev, to_device(q, dev), to_device(k1, dev),
+                                   to_device(k2, dev), timed)
+            fails, _ = check_queries(o1, PARITY_LO, PARITY_HI, q, outs[0], outs[1], k1, k2,
+                                     outs[2], outs[3], outs[4], outs[5])
+            gate(f"C2 r={r}", fails + ([] if rates["count_eq_len_range"] else ["count != len(range)"]))
+            rows.append({"r": r, "levels": bin(r).count("1"), "nq": n, **rates})
+    torch.cuda.synchronize()
+    ms = np.array([a.elapsed_time(e) for a, e in per])
+    rate = b / (ms * 1e-3) / 1e6
+    lsm.close()
+    return {"workload": "C2: b=2^16 insert-only, 64 batches from empty; queries nq=n at L=8",
+            "insert_mups": {"min": float(rate.min()), "max": float(rate.max()),
+                            "harmonic_mean": float(R2 * b / (ms.sum() * 1e-3) / 1e6),
+                            "min_at_r": int(np.argmin(rate)), "max_at_r": int(np.argmax(rate))},
+            "timing": "CUDA events around each lsm_update (per-batch, Table II protocol)",
+            "queries": rows, "parity": "O1 on the key sub-range, every checked r"}
+
+
+def extra_c3p_sa_bulk(pkg, dev, stream, keys_d, vals_d, ops_d, sub, q, k1, k2):
+    """C3' (§5.4 shape): 63 mixed batches of 2^20 (six
+    occupied levels), queries, a multi-level cleanup (elem/s, GB/s), queries;
+    N2: the GPU SA fed the same 63 batches, LSM-vs-SA
+    ratios; N1: bulk build of all 64 C3 batches (2^26
+    elements) into an empty LSM."""
+    import torch
+    from paper_1707_05354_b200 import to_device
+    timed = _ev_timer(stream)
+    R3 = 63
+    dq, dk1, dk2 = to_device(q, dev), to_device(k1, dev), to_device(k2, dev)
+    o1 = _sub_oracle(B)
+    for k, v, d in sub[:R3]:
+        o1.apply_batch(k, v, d)
+    out = {}
+    for name, sa in (("lsm", False), ("sa", True)):
+        st = pkg.GpuLSM(B, reserve_batches=R, sa=sa)
+        for _ in range(1):  # warm-up
+            st.clear()
+            for j in range(8):
+                st.update(keys_d[j], vals_d[j], ops_d[j])
+        st.clear()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for j in range(R3):
+            st.update(keys_d[j], vals_d[j], ops_d[j])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        upd_ms = e0.elapsed_time(e1)
+        rates, outs = _queries(st, dev, dq, dk1, dk2, timed)
+        fails, _ = check_queries(o1, PARITY_LO, PARITY_HI, q, outs[0], outs[1], k1, k2, *outs[2:])
+        gate(f"C3' {name} r=63", fails)
+        res = {"update_mups": R3 * B / (upd_ms * 1e-3) / 1e6, "update_ms": upd_ms,
+               "levels": bin(R3).count("1") if not sa else 1, **rates}
+        if not sa:
+            n = R3 * B
+            # the first cleanup of a handle allocates its merge and compaction
+            # buffers: run one untimed, then rebuild r = 63 and time the next
+            st.cleanup()
+            st.clear()
+            for j in range(R3):
+                st.update(keys_d[j], vals_d[j], ops_d[j])
+            torch.cuda.synchronize()
+            e0.record(stream)
+            st.cleanup()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            c_ms = e0.elapsed_time(e1)
+            r2 = st.r
+            rates2, outs2 = _queries(st, dev, dq, dk1, dk2, timed)
+            o1.cleanup()
+            fails, _ = check_queries(o1, PARITY_LO, PARITY_HI, q, outs2[0], outs2[1], k1, k2,
+                                     *outs2[2:])
+            gate("C3' after cleanup", fails)
+            res["cleanup"] = {"ms": c_ms, "melem_per_s": n / (c_ms * 1e-3) / 1e6,
+                              "alg_GBps": (8.0 * n + 8.0 * r2 * B) / (c_ms * 1e-3) / 1e9,
+                              "levels_merged": bin(R3).count("1"), "r_after": r2,
+                              "stale_fraction": 1.0 - (len(o1) * 64.0) / n if len(o1) else None,
+                              "note": "stale_fraction estimated from the 1/64 key sub-range"}
+            res["after_cleanup"] = {**rates2, "levels": bin(r2).count("1")}
+        st.close()
+        out[name] = res
+    L, S = out["lsm"], out["sa"]
+    out["lsm_over_sa"] = {"updates": L["update_mups"] / S["update_mups"],
+                          "lookup": L["lookup_mqps"] / S["lookup_mqps"],
+                          "count": L["count_mqps"] / S["count_mqps"],
+                          "range": L["range_mqps"] / S["range_mqps"],
+                          "paper_K40c": "updates 13.5x; lookups 1/1.75; count/range 1/1.36-1/1.84 "
+                                        "(PAPER.md:846, 946, 979-980; other b and n)"}
+    # N1 bulk build: the 64 C3 batches as one input of 2^26 elements
+    allk = torch.cat(keys_d)
+    allv = torch.cat(vals_d)
+    allo = torch.cat(ops_d)
+    bl = pkg.GpuLSM(B)
+    def build():
+        bl.clear()
+        bl.bulk_build(allk, allv, allo)
+    t_b = timed(build)
+    ob = _sub_oracle(B)
+    ob.bulk_build(np.concatenate([x[0] for x in sub]), np.concatenate([x[1] for x in sub]),
+                  np.concatenate([x[2] for x in sub]))
+    rates, outs = _queries(bl, dev, dq, dk1, dk2, timed)
+    fails, _ = check_queries(ob, PARITY_LO, PARITY_HI, q, outs[0], outs[1], k1, k2, *outs[2:])
+    gate("N1 bulk build", fails)
+    out["bulk_build"] = {"n": int(allk.numel()), "ms": t_b,
+                         "melem_per_s": allk.numel() / (t_b * 1e-3) / 1e6, "r": bl.r,
+                         "paper_K40c_melem_per_s": "770 (KV sort) / 728 (bulk build), PAPER.md:860"}
+    bl.close()
+    del allk, allv, allo
+    out["workload"] = ("C3 batches: LSM and GPU SA at r=63 (2^24 queries, L=8), cleanup of the "
+                       "6-level LSM; bulk build of all 64 batches")
+    out["parity"] = "O1 on the key sub-range at r=63, after cleanup, and for the bulk build"
+    return out
+
+
+def extra_c4(pkg, dev, stream):
+    """C4 (BASELINE configs[3]): b = 2^20 insert-only, r =
+    127 (seven levels, n = 127*2^20) and r = 128 (one level, 2^27): count and
+    range at L in {8, 128, 1024}, nq = min(2^24, 2^27 / L) (R16)."""
+    import torch
+    from paper_1707_05354_b200 import to_device
+    timed = _ev_timer(stream)
+    seed = synth.SEED_BASE + 3
+    lsm = pkg.GpuLSM(B, reserve_batches=128)
+    o1 = _sub_oracle(B)
+    rows = []
+    r = 0
+    for target in (127, 128):
+        while r < target:
+            k, v, d = synth.updates(seed, r * B, B, delete_frac4=0)
+            lsm.update(to_device(k, dev), to_device(v, dev), to_device(d, dev))
+            m = (k >= PARITY_LO) & (k < PARITY_HI)
+            o1.apply_batch(k[m], v[m], d[m])
+            r += 1
+        torch.cuda.synchronize()
+        n = r * B
+        for L in (8, 128, 1024):
+            nq = min(1 << 24, (1 << 27) // L)
+            k1, k2 = synth.range_queries(seed + L, nq, n, L)
+            dk1, dk2 = to_device(k1, dev), to_device(k2, dev)
+            cnt = torch.empty(nq, dtype=torch.int32, device=dev)
+            t_c = timed(lambda: lsm.count_into(dk1, dk2, cnt))
+            total = int(cnt.to(torch.int64).sum().item())
+            roff = torch.empty(nq + 1, dtype=torch.int64, device=dev)
+            rk = torch.empty(total + 16, dtype=torch.int32, device=dev)
+            rv = torch.empty(total + 16, dtype=torch.int32, device=dev)
+            got = []
+            t_r = timed(lambda: got.append(lsm.range_into(dk1, dk2, roff, rk, rv)))
+            fails, nchk = check_queries(o1, PARITY_LO, PARITY_HI, None, None, None, k1, k2, cnt,
+                                        roff, rk, rv)
+            gate(f"C4 r={r} L={L}", fails + ([] if got[-1] == total else ["count != len(range)"]))
+            rows.append({"r": r, "levels": bin(r).count("1"), "L": L, "nq": nq,
+                         "count_mqps": nq / (t_c * 1e-3) / 1e6, "range_mqps": nq / (t_r * 1e-3) / 1e6,
+                         "pairs_per_query": total / nq,
+                         "range_out_GBps": total * 8 / (t_r * 1e-3) / 1e9,
+                         "checked_ranges": nchk.get("ranges")})
+            del rk, rv, roff, cnt
+    lsm.close()
+    return {"workload": "C4: b=2^20 insert-only, r in {127 (7 levels), 128 (1 level)}, "
+                        "L in {8, 128, 1024}, nq = min(2^24, 2^27/L)",
+            "rows": rows, "parity": "O1 on the key sub-range; count == len(range) on every row",
+            "full_sweep": "scripts/sweep_c4.py (r in 96..128, L in 8..1024)"}
 
 
 def run_reference(args):
@@ -463,6 +756,15 @@ def run_native(args):
         "e2e": e2e,
         "input_gen_s": gen_s,
     }
+    if args.extra:
+        t_x = time.time()
+        sec = {}
+        sec["c2"] = extra_c2(pkg, dev, stream)
+        sec["c3_r63_sa_bulk"] = extra_c3p_sa_bulk(pkg, dev, stream, keys_d, vals_d, ops_d, sub,
+                                                  q_host, k1, k2)
+        sec["c4"] = extra_c4(pkg, dev, stream)
+        sec["seconds"] = time.time() - t_x
+        line["secondary"] = sec
     if args.cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_oracle()
     print(json.dumps(line), flush=True)
@@ -477,6 +779,8 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    ap.add_argument("--no-extra", dest="extra", action="store_false",
+                    help="skip the secondary configurations (C2, C3' + SA + bulk build, C4)")
     ap.add_argument("--sharded", action="store_true",
                     help="use the key-range sharded router even at N=1")
     args = ap.parse_args()
