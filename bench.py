@@ -538,6 +538,99 @@ def run_reference(args):
     return 0
 
 
+C5_B = 1 << 24
+C5_NQ = 1 << 26
+C5_LO, C5_HI = 5 << 22, 6 << 22  # parity sub-range: 1/512 of the key domain
+
+
+def run_c5_single(args):
+    """--config c5 at N = 1 (BASELINE configs[4] on one GPU): global batch
+    b = 2^24 mixed 75/25, 64 batches from empty -> 2^30 resident records,
+    then 2^26 lookups (50 % hit). A batch of 2^24 takes the multi-wave
+    onesweep LSD sort. Inputs are generated in device memory
+    (synth's torch copy of the generator); lookups inside the key sub-range
+    [5*2^22, 6*2^22) are checked against O1 fed the updates in that range."""
+    import torch
+    import oracle
+    import paper_1707_05354_b200 as pkg
+    from paper_1707_05354_b200 import to_numpy_u32
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    seed = synth.SEED_BASE + 4
+    t0 = time.time()
+    batches = [synth.updates_t(seed, j * C5_B, C5_B, delete_frac4=1, device=dev) for j in range(R)]
+    q = synth.lookup_queries_t(seed, C5_NQ, R * C5_B, device=dev)
+    gen_s = time.time() - t0
+    lsm = pkg.GpuLSM(C5_B, reserve_batches=R)
+    stream = torch.cuda.current_stream()
+    lv = torch.empty(C5_NQ, dtype=torch.int32, device=dev)
+    lf = torch.empty(C5_NQ, dtype=torch.uint8, device=dev)
+
+    def step(rec):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        lsm.clear()
+        e[0].record(stream)
+        for k, v, d in batches:
+            lsm.update(k, v, d)
+        e[1].record(stream)
+        lsm.lookup_into(q, lv, lf)
+        e[2].record(stream)
+        if rec is not None:
+            rec.append(e)
+
+    for _ in range(args.warmup):
+        step(None)
+    torch.cuda.synchronize()
+    recs = []
+    l0 = lsm.launch_count
+    with ClockSampler(0) as clk:
+        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        for _ in range(args.steps):
+            step(recs)
+        stop.record(stream)
+        torch.cuda.synchronize()
+    launches = lsm.launch_count - l0
+    upd = float(np.mean([e[0].elapsed_time(e[1]) for e in recs]))
+    look = float(np.mean([e[1].elapsed_time(e[2]) for e in recs]))
+    lsm.profile_enable(True)
+    step(None)
+    torch.cuda.synchronize()
+    prof = lsm.profile_read()
+    lsm.profile_enable(False)
+    # parity: lookups inside the sub-range vs O1 fed the sub-range updates
+    o1 = oracle.OracleDict(C5_B)
+    for k, v, d in batches:
+        m = (k >= C5_LO) & (k < C5_HI)  # keys < 2^31: int32 compares are exact
+        o1.apply_batch(to_numpy_u32(k[m]), to_numpy_u32(v[m]), d[m].cpu().numpy())
+    qh = to_numpy_u32(q)
+    fails, nchk = check_queries(o1, C5_LO, C5_HI, qh, lv, lf)
+    gate("C5 (N=1)", fails)
+    peak, peak_src = measured_peaks()
+    per_class = {c: {"ms_per_step": p["ms"], "launches_per_step": p["launches"],
+                     "alg_GBps": (p["alg_bytes"] / (p["ms"] * 1e-3) / 1e9) if p["ms"] else None}
+                 for c, p in prof.items() if p["launches"]}
+    dom = max(prof, key=lambda c: prof[c]["ms"])
+    ach = prof[dom]["alg_bytes"] / (prof[dom]["ms"] * 1e-3) / 1e9
+    line = {"metric": METRIC, "value": R * C5_B / (upd * 1e-3) / 1e6, "unit": UNIT, "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": start.elapsed_time(stop) / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (splitmix64 uniform 31-bit keys, generated on the device)",
+            "config": {"workload": "C5 on one GPU: b=2^24 mixed 75/25, 64 batches -> 2^30 resident; "
+                                   "2^26 lookups (50% hit)", "b": C5_B, "batches": R,
+                       "resident": R * C5_B, "nq": C5_NQ, "parallelism": "1 GPU"},
+            "update_ms_per_step": upd, "lookup_mqps": C5_NQ / (look * 1e-3) / 1e6,
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak,
+                         "peak_source": peak_src, "unit": "GB/s", "frac": ach / peak,
+                         "traffic": None},
+            "kernels": per_class, "gpu_launches": launches, "clocks": clk.summary(),
+            "parity": {"ok": True, **nchk, "oracle": "O1 on the key sub-range [5*2^22, 6*2^22)"},
+            "input_gen_s": gen_s}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def run_native(args):
     import torch
     import paper_1707_05354_b200 as pkg
@@ -781,6 +874,9 @@ def main():
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-extra", dest="extra", action="store_false",
                     help="skip the secondary configurations (C2, C3' + SA + bulk build, C4)")
+    ap.add_argument("--config", default="c3", choices=["c3", "c5"],
+                    help="c3 (default): BASELINE configs[2]; c5: configs[4] (global b = 2^24, "
+                         "2^30 resident; strong scaling under torchrun)")
     ap.add_argument("--sharded", action="store_true",
                     help="use the key-range sharded router even at N=1")
     args = ap.parse_args()
@@ -788,6 +884,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == "c5" and int(os.environ.get("WORLD_SIZE", "1")) == 1 and not args.sharded:
+        return run_c5_single(args)
     return run_native(args)
 
 

@@ -121,8 +121,9 @@ lsm_status lsm_clear(lsm_t* h, void* stream);
  * Device work: encode + stable radix sort on the 32-bit key variable
  * (status bit included) -- one CTA for b <= 7168; for a batch
  * of up to one wave of 7168-record tiles (b = 2^20 among them) an MSD
- * scatter by the top 8 bits plus a shared-memory rank of each bucket by
- * (key variable, input position); above that (or after a skewed key set)
+ * scatter by the top 8 bits (key, input position and value carried) plus
+ * a shared-memory rank of each bucket by (key variable, input position);
+ * above that (or after a skewed key set)
  * a 4-pass onesweep LSD -- then the binary-counter cascade of stable merges
  * on key>>1, batch first on ties (R1), writing level
  * ffz(r).
@@ -130,6 +131,14 @@ lsm_status lsm_clear(lsm_t* h, void* stream);
  * LSM_ERR_CUDA; out-of-domain keys set the sticky LSM_ERR_KEY_DOMAIN.      */
 lsm_status lsm_update(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals,
                       const uint8_t* d_is_delete, uint64_t n, void* stream);
+
+/* A batch of n already-encoded records, 1 <= n <= b: d_records[2*i] is the
+ * key variable (original key << 1 | 1 for an insert, | 0 for a tombstone,
+ * PAPER.md:605-610; 0xFFFFFFFE = placebo) and d_records[2*i+1] its value
+ * (0 for a tombstone, R6). The records of the multi-GPU router: produced by
+ * lsm_shard_bucket_records on the source rank and exchanged with one
+ * all-to-all. Same semantics and errors as lsm_update. */
+lsm_status lsm_update_records(lsm_t* h, const uint32_t* d_records, uint64_t n, void* stream);
 
 /* All-insert batch (lsm_update with d_is_delete = NULL). */
 lsm_status lsm_insert(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals,
@@ -249,7 +258,8 @@ lsm_status lsm_cleanup(lsm_t* h, void* stream);
 /* Stable partition of n records by destination shard. mode 0: owner(k) as
  * above (range partition); mode 1: the top log2(P) bits of k*0x9E3779B1
  * (P a power of two; used to split an oversized local batch without
- * separating equal keys). Outputs are grouped by destination, input order
+ * separating equal keys); mode 2: as mode 1 on k >> 1 (k a key variable,
+ * for encoded records). Outputs are grouped by destination, input order
  * kept inside each group. d_vals / d_ops / their outputs and d_perm_out
  * (source index of each output slot, u32) may be NULL. d_counts_out[P] (u32,
  * device) receives the group sizes. 1 <= P <= 64. Uses h for scratch.       */
@@ -257,6 +267,16 @@ lsm_status lsm_shard_bucket(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_
                             const uint8_t* d_ops, uint64_t n, uint32_t nshards, int mode,
                             uint32_t* d_keys_out, uint32_t* d_vals_out, uint8_t* d_ops_out,
                             uint32_t* d_perm_out, uint32_t* d_counts_out, void* stream);
+
+/* Range partition (mode 0 of lsm_shard_bucket) of n raw updates into
+ * ENCODED records for lsm_update_records: d_records_out[2*j], [2*j+1] =
+ * (key variable, value) of the j-th record in destination order (input order
+ * kept inside each destination group), d_counts_out[P] the group sizes.
+ * d_vals / d_ops may be NULL (values 0 / all inserts). An out-of-domain key
+ * becomes a placebo and sets h's sticky LSM_ERR_KEY_DOMAIN (R5).           */
+lsm_status lsm_shard_bucket_records(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals,
+                                    const uint8_t* d_ops, uint64_t n, uint32_t nshards,
+                                    uint32_t* d_records_out, uint32_t* d_counts_out, void* stream);
 
 /* out[perm[i]] = in[i] for i < n: routes lookup results back to the query
  * order a lsm_shard_bucket permutation came from. d_found_* may be NULL.   */

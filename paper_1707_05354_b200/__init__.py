@@ -42,6 +42,7 @@ SIGNATURES = {
     "lsm_reserve": ([_vp, _u64, _vp], _st),
     "lsm_clear": ([_vp, _vp], _st),
     "lsm_update": ([_vp, _vp, _vp, _vp, _u64, _vp], _st),
+    "lsm_update_records": ([_vp, _vp, _u64, _vp], _st),
     "lsm_insert": ([_vp, _vp, _vp, _u64, _vp], _st),
     "lsm_delete": ([_vp, _vp, _u64, _vp], _st),
     "lsm_update_host": ([_vp, _vp, _vp, _vp, _u64, _vp], _st),
@@ -65,6 +66,7 @@ SIGNATURES = {
     "lsm_profile_read": ([_vp, _vp], _st),
     "lsm_shard_bucket": ([_vp, _vp, _vp, _vp, _u64, ctypes.c_uint32, ctypes.c_int, _vp, _vp, _vp,
                           _vp, _vp, _vp], _st),
+    "lsm_shard_bucket_records": ([_vp, _vp, _vp, _vp, _u64, ctypes.c_uint32, _vp, _vp, _vp], _st),
     "lsm_shard_scatter": ([_vp, _vp, _vp, _vp, _u64, _vp, _vp, _vp], _st),
     "lsm_shard_clip": ([_vp, _vp, _vp, _u64, ctypes.c_uint32, ctypes.c_uint32, _vp, _vp, _vp], _st),
     "lsm_shard_sum": ([_vp, _vp, ctypes.c_uint32, _u64, _vp, _vp], _st),
@@ -196,6 +198,12 @@ class GpuLSM:
         _check(self._lib.lsm_update(self.h, _dev(keys, 4, "keys"), _dev(vals, 4, "vals"),
                                     _dev(is_delete, 1, "is_delete"), n, _stream_ptr(stream)),
                "lsm_update")
+
+    def update_records(self, records, stream=None):
+        """A batch of encoded (key variable, value) records: int32 [n, 2]."""
+        n = records.shape[0]
+        _check(self._lib.lsm_update_records(self.h, _dev(records, 4, "records"), n,
+                                            _stream_ptr(stream)), "lsm_update_records")
 
     def bulk_build(self, keys, vals=None, is_delete=None, stream=None):
         """N1 bulk build into an empty structure: all n elements form one batch,
@@ -366,6 +374,20 @@ class GpuLSM:
                                           _dev(oo, 1), _dev(po), _dev(cnt), _stream_ptr(stream)),
                "lsm_shard_bucket")
         return ko, vo, oo, po, cnt
+
+    def shard_bucket_records(self, keys, nshards, vals=None, ops=None, out=None, counts=None,
+                             stream=None):
+        """Range partition into encoded records -> (records int32 [n, 2], counts[P])."""
+        torch = _torch()
+        n = keys.numel()
+        dev = keys.device
+        rec = out if out is not None else torch.empty((n, 2), dtype=torch.int32, device=dev)
+        cnt = counts if counts is not None else torch.empty(nshards, dtype=torch.int32, device=dev)
+        _check(self._lib.lsm_shard_bucket_records(self.h, _dev(keys, 4, "keys"),
+                                                  _dev(vals, 4, "vals"), _dev(ops, 1, "ops"), n,
+                                                  nshards, _dev(rec), _dev(cnt),
+                                                  _stream_ptr(stream)), "lsm_shard_bucket_records")
+        return rec, cnt
 
     def shard_pick(self, keys, vals, found, parts, n, last, stream=None):
         """First (last=False) / last (last=True) shard answer per query."""

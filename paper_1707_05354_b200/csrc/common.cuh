@@ -237,7 +237,10 @@ inline int dev_slot() {
 // Launchers (host side). Each returns cudaGetLastError() after the launch.
 // ---------------------------------------------------------------------------
 
-enum UpdateMode { kModeInsert = 0, kModeDelete = 1, kModeMixed = 2 };
+// kModeEncoded: the records are already (key variable, value) pairs, stored
+// interleaved (the router's exchanged records); keys = base,
+// vals = base + 1, stride 2
+enum UpdateMode { kModeInsert = 0, kModeDelete = 1, kModeMixed = 2, kModeEncoded = 3 };
 
 struct SortScratch {
   uint32_t* hist;         // [2][4][256] double-buffered digit histograms
@@ -390,7 +393,8 @@ cudaError_t launch_bucket(const uint32_t* keys, const uint32_t* vals, const uint
                           uint64_t n, uint32_t P, int mode, uint32_t* keys_out,
                           uint32_t* vals_out, uint8_t* ops_out, uint32_t* perm_out,
                           uint32_t* counts_out, uint32_t* scratch, cudaStream_t s,
-                          const LaunchHooks& hk);
+                          const LaunchHooks& hk, uint32_t* rec_out = nullptr,
+                          uint32_t* err = nullptr);
 cudaError_t launch_scatter_back(const uint32_t* perm, const uint32_t* vin, const uint8_t* fin,
                                 uint64_t n, uint32_t* vout, uint8_t* fout, cudaStream_t s,
                                 const LaunchHooks& hk);

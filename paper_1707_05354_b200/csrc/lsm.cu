@@ -713,6 +713,11 @@ lsm_status lsm_update(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals,
   return do_update(h, d_keys, d_vals, d_is_delete, kModeMixed, n, S(stream));
 }
 
+lsm_status lsm_update_records(lsm_t* h, const uint32_t* d_records, uint64_t n, void* stream) {
+  if (!d_records) return LSM_ERR_INVALID_ARG;
+  return do_update(h, d_records, d_records + 1, nullptr, kModeEncoded, n, S(stream));
+}
+
 lsm_status lsm_insert(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals, uint64_t n,
                       void* stream) {
   return do_update(h, d_keys, d_vals, nullptr, kModeInsert, n, S(stream));
@@ -1087,7 +1092,8 @@ lsm_status lsm_shard_bucket(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_
                             uint32_t* d_perm_out, uint32_t* d_counts_out, void* stream) {
   if (!h || nshards == 0 || nshards > 64 || !d_counts_out) return LSM_ERR_INVALID_ARG;
   ENTER(h);
-  if (mode == 1 && (nshards & (nshards - 1))) return LSM_ERR_INVALID_ARG;
+  if (mode < 0 || mode > 2) return LSM_ERR_INVALID_ARG;
+  if (mode >= 1 && (nshards & (nshards - 1))) return LSM_ERR_INVALID_ARG;
   if (n > 0 && (!d_keys || !d_keys_out)) return LSM_ERR_INVALID_ARG;
   if ((d_vals == nullptr) != (d_vals_out == nullptr) || (d_ops == nullptr) != (d_ops_out == nullptr))
     return LSM_ERR_INVALID_ARG;
@@ -1097,6 +1103,24 @@ lsm_status lsm_shard_bucket(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_
   CK(sc.get(bucket_scratch_words(n, nshards) * 4));
   CK(launch_bucket(d_keys, d_vals, d_ops, n, nshards, mode, d_keys_out, d_vals_out, d_ops_out,
                    d_perm_out, d_counts_out, static_cast<uint32_t*>(sc.p), s, hooks(h)));
+  return LSM_OK;
+}
+
+lsm_status lsm_shard_bucket_records(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals,
+                                    const uint8_t* d_ops, uint64_t n, uint32_t nshards,
+                                    uint32_t* d_records_out, uint32_t* d_counts_out,
+                                    void* stream) {
+  if (!h || nshards == 0 || nshards > 64 || !d_counts_out) return LSM_ERR_INVALID_ARG;
+  ENTER(h);
+  if (n > 0 && (!d_keys || !d_records_out)) return LSM_ERR_INVALID_ARG;
+  if (n > 0xFFFFFFFFull) return LSM_ERR_INVALID_ARG;
+  cudaStream_t s = S(stream);
+  CK(ensure_sort_scratch(h, s));  // the sticky error word
+  CallScratch sc(h, s);
+  CK(sc.get(bucket_scratch_words(n, nshards) * 4));
+  CK(launch_bucket(d_keys, d_vals, d_ops, n, nshards, 0, nullptr, nullptr, nullptr, nullptr,
+                   d_counts_out, static_cast<uint32_t*>(sc.p), s, hooks(h), d_records_out,
+                   h->sort.err));
   return LSM_OK;
 }
 

@@ -30,8 +30,9 @@ __device__ __forceinline__ uint32_t owner_of(uint32_t k, uint32_t P, int mode) {
     if (k > kMaxKey) return P - 1;
     return (uint32_t)(((uint64_t)k * P) >> 31);
   }
-  // hash mode: P is a power of two
-  const uint32_t h = k * 0x9E3779B1u;
+  // hash modes (P a power of two): 1 hashes the original key, 2 a key
+  // VARIABLE's original key (k >> 1: a key's tombstones and inserts together)
+  const uint32_t h = (mode == 2 ? k >> 1 : k) * 0x9E3779B1u;
   return P == 1 ? 0u : (h >> (32 - (31 - __clz(P))));
 }
 
@@ -81,7 +82,7 @@ __global__ void __launch_bounds__(kBThreads) bucket_scatter_kernel(
     const uint8_t* __restrict__ ops, uint64_t n, uint32_t P, int mode,
     const uint32_t* __restrict__ toffs, uint64_t ntiles, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out, uint8_t* __restrict__ ops_out,
-    uint32_t* __restrict__ perm_out) {
+    uint32_t* __restrict__ perm_out, uint2* __restrict__ rec_out, uint32_t* __restrict__ err) {
   __shared__ uint32_t wcnt[kBThreads / 32][kMaxShards];
   __shared__ uint32_t wbase[kBThreads / 32][kMaxShards];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -122,9 +123,25 @@ __global__ void __launch_bounds__(kBThreads) bucket_scatter_kernel(
     const uint64_t p = base + warp * (32 * kBItems) + i * 32 + lane;
     if (p < n) {
       const uint32_t dst = wbase[warp][own[i]] + rk[i];
-      keys_out[dst] = __ldg(keys + p);
-      if (vals) vals_out[dst] = __ldg(vals + p);
-      if (ops) ops_out[dst] = __ldg(ops + p);
+      if (rec_out != nullptr) {
+        // encoded record for the owner's local insert (A1):
+        // key variable (k << 1 | regular), value 0 for a tombstone (R6), an
+        // out-of-domain key as a placebo + the sticky error (R5)
+        const uint32_t k = __ldg(keys + p);
+        const bool del = ops != nullptr && __ldg(ops + p) != 0;
+        uint2 r;
+        if (k > kMaxKey) {
+          r = make_uint2(kPlacebo, 0u);
+          atomicOr(err, 1u);
+        } else {
+          r = make_uint2((k << 1) | (del ? 0u : 1u), (del || vals == nullptr) ? 0u : __ldg(vals + p));
+        }
+        rec_out[dst] = r;
+      } else {
+        keys_out[dst] = __ldg(keys + p);
+        if (vals) vals_out[dst] = __ldg(vals + p);
+        if (ops) ops_out[dst] = __ldg(ops + p);
+      }
       if (perm_out) perm_out[dst] = (uint32_t)p;
     }
   }
@@ -267,7 +284,7 @@ cudaError_t launch_bucket(const uint32_t* keys, const uint32_t* vals, const uint
                           uint64_t n, uint32_t P, int mode, uint32_t* keys_out,
                           uint32_t* vals_out, uint8_t* ops_out, uint32_t* perm_out,
                           uint32_t* counts_out, uint32_t* scratch, cudaStream_t s,
-                          const LaunchHooks& hk) {
+                          const LaunchHooks& hk, uint32_t* rec_out, uint32_t* err) {
   const uint64_t ntiles = (n + kBTile - 1) / kBTile;
   hk.begin(hk.ctx, LSM_K_OTHER, s);
   if (ntiles > 0)
@@ -275,7 +292,8 @@ cudaError_t launch_bucket(const uint32_t* keys, const uint32_t* vals, const uint
   bucket_scan_kernel<<<1, 1024, 0, s>>>(scratch, (uint64_t)P * ntiles, P, ntiles, counts_out);
   if (ntiles > 0)
     bucket_scatter_kernel<<<(unsigned)ntiles, kBThreads, 0, s>>>(
-        keys, vals, ops, n, P, mode, scratch, ntiles, keys_out, vals_out, ops_out, perm_out);
+        keys, vals, ops, n, P, mode, scratch, ntiles, keys_out, vals_out, ops_out, perm_out,
+        reinterpret_cast<uint2*>(rec_out), err);
   hk.end(hk.ctx, LSM_K_OTHER, (double)n * 18.0, s, 3);
   return cudaGetLastError();
 }

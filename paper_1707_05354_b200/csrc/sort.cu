@@ -79,6 +79,7 @@ struct RawBatch {
   const uint8_t* ops;
   int mode;
   uint64_t n;  // real updates; [n, b) are placebo padding
+  uint32_t stride;  // elements between consecutive keys (values): 1, or 2 for kModeEncoded
 };
 
 #ifdef GPULSM_PROBE
@@ -106,6 +107,11 @@ __device__ __forceinline__ void encode_loaded(const RawBatch& in, uint64_t pos, 
                                               uint32_t v, uint32_t op, uint32_t& key,
                                               uint32_t& val, bool& bad) {
   bad = false;
+  if (in.mode == kModeEncoded) {  // already a key variable (the router's records)
+    key = pos < in.n ? k : kPlacebo;
+    val = (pos < in.n && (k & 1u)) ? v : 0u;
+    return;
+  }
   const bool del = in.mode == kModeDelete || (in.mode == kModeMixed && op != 0);
   if (pos >= in.n || k > kMaxKey) {  // R7 padding / R5 out of domain
     bad = pos < in.n;
@@ -185,7 +191,7 @@ __global__ void __launch_bounds__(kHistThreads, 1) sort_hist_kernel(
     for (int j = 0; j < kHistBatch; ++j) {
       const uint64_t pos = base + j * 32 + lane;
       const bool ld = pos < w1 && pos < in.n;
-      k[j] = ld ? __ldg(in.keys + pos) : 0u;
+      k[j] = ld ? __ldg(in.keys + (pos) * in.stride) : 0u;
       op[j] = (ld && in.mode == kModeMixed) ? (uint32_t)__ldg(in.ops + pos) : 0u;
     }
 #pragma unroll
@@ -295,8 +301,8 @@ __global__ void __launch_bounds__(kSortThreads, 1) onesweep_pass_kernel(
     for (int i = 0; i < kSortItems; ++i) {  // independent loads first
       const uint64_t pos = tile_base + wbase + i * 32 + lane;
       const bool in_batch = pos < in.n;
-      k[i] = in_batch ? __ldg(in.keys + pos) : 0u;
-      v[i] = (in_batch && in.vals) ? __ldg(in.vals + pos) : 0u;
+      k[i] = in_batch ? __ldg(in.keys + (pos) * in.stride) : 0u;
+      v[i] = (in_batch && in.vals) ? __ldg(in.vals + (pos) * in.stride) : 0u;
       op[i] = (in_batch && in.mode == kModeMixed) ? (uint32_t)__ldg(in.ops + pos) : 0u;
     }
     bool any_bad = false;
@@ -627,8 +633,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_sort_kernel(
   SmallSmem& S = *reinterpret_cast<SmallSmem*>(small_smem);
   const uint64_t off = (uint64_t)blockIdx.x * b;
   RawBatch in = in_all;
-  in.keys += off;
-  if (in.vals) in.vals += off;
+  in.keys += off * in.stride;
+  if (in.vals) in.vals += off * in.stride;
   if (in.ops) in.ops += off;
   in.n = in_all.n > off ? (in_all.n - off < b ? in_all.n - off : b) : 0;
   out_keys += off;
@@ -639,8 +645,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_sort_kernel(
   for (uint32_t p = threadIdx.x; p < b; p += kSmallThreads) {  // encode (A1)
     uint32_t k = 0, v = 0, op = 0;
     if (p < in.n) {
-      k = __ldg(in.keys + p);
-      v = in.vals ? __ldg(in.vals + p) : 0u;
+      k = __ldg(in.keys + (p) * in.stride);
+      v = in.vals ? __ldg(in.vals + (p) * in.stride) : 0u;
       op = in.mode == kModeMixed ? (uint32_t)__ldg(in.ops + p) : 0u;
     }
     bool bad;
@@ -755,8 +761,8 @@ __global__ void __launch_bounds__(kMsdThreads, MSD_MINB) msd_scatter_kernel(
     for (int i = 0; i < kSortItems; ++i) {  // independent loads first
       const uint64_t p = tile_base + wbase + i * 32 + lane;
       const bool in_batch = p < in.n;
-      k[i] = in_batch ? __ldg(in.keys + p) : 0u;
-      v[i] = (in_batch && in.vals != nullptr) ? __ldg(in.vals + p) : 0u;
+      k[i] = in_batch ? __ldg(in.keys + (p) * in.stride) : 0u;
+      v[i] = (in_batch && in.vals != nullptr) ? __ldg(in.vals + (p) * in.stride) : 0u;
       op[i] = (in_batch && in.mode == kModeMixed) ? (uint32_t)__ldg(in.ops + p) : 0u;
     }
     bool any_bad = false;
@@ -916,8 +922,8 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
         val[i] = 0;
         if (p < b) {
           const bool inb = p < in.n;
-          const uint32_t rk = inb ? __ldg(in.keys + p) : 0u;
-          const uint32_t rv = (inb && in.vals) ? __ldg(in.vals + p) : 0u;
+          const uint32_t rk = inb ? __ldg(in.keys + (p) * in.stride) : 0u;
+          const uint32_t rv = (inb && in.vals) ? __ldg(in.vals + (p) * in.stride) : 0u;
           const uint32_t op = (inb && in.mode == kModeMixed) ? (uint32_t)__ldg(in.ops + p) : 0u;
           bool bad;
           encode_loaded(in, p, rk, rv, op, key[i], val[i], bad);
@@ -1110,7 +1116,7 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
       const uint32_t p = i * kBktThreads + tid;
       const uint2 kv = S.kv[res][p];  // p < kBktCap: in bounds
       const bool use = p < size && (kv.x & 1u) && in.vals != nullptr;
-      v[i] = __ldg((use ? in.vals : in.keys) + (use ? kv.y : 0u));
+      v[i] = __ldg((use ? in.vals : in.keys) + (use ? (uint64_t)kv.y * in.stride : 0u));
       v[i] = use ? v[i] : 0u;
     }
 #pragma unroll
@@ -1179,7 +1185,7 @@ cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals
     cudaError_t e = sort_attrs();
     if (e != cudaSuccess) return e;
   }
-  RawBatch in{raw_keys, raw_vals, ops, mode, n};
+  RawBatch in{raw_keys, raw_vals, ops, mode, n, mode == kModeEncoded ? 2u : 1u};
   cudaError_t e = cudaSuccess;
 
   // (1) small batch: one CTA sorts all four digits in shared memory
@@ -1281,7 +1287,7 @@ cudaError_t launch_sort_segments(const uint32_t* raw_keys, const uint32_t* raw_v
   if (b <= (uint64_t)kSmallCap && k > 1) {
     cudaError_t e = sort_attrs();
     if (e != cudaSuccess) return e;
-    RawBatch in{raw_keys, raw_vals, ops, mode, n};
+    RawBatch in{raw_keys, raw_vals, ops, mode, n, mode == kModeEncoded ? 2u : 1u};
     hk.begin(hk.ctx, LSM_K_SORT_PASS, s);
     e = launch_pdl(small_sort_kernel, (unsigned)k, kSmallThreads, sizeof(SmallSmem), s, in,
                    (uint32_t)b, out_keys, out_vals, (uint32_t*)nullptr, S.err);

@@ -102,6 +102,20 @@ class GpuShardBackend:
     def update(self, k, v, o):
         self.lsm.update(k, v, o)
 
+    def bucket_records(self, keys, vals, ops, P, out=None, counts=None):
+        return self.lsm.shard_bucket_records(keys, P, vals=vals, ops=ops, out=out, counts=counts)
+
+    def update_records(self, rec):
+        self.lsm.update_records(rec)
+
+    def split_records(self, rec, nparts):
+        """Oversized local batch: group the records by a hash of their original
+        key (equal keys together) -> (records, counts[nparts])."""
+        kv = rec[:, 0].contiguous()
+        vv = rec[:, 1].contiguous()
+        k2, v2, _, _, c2 = self.lsm.shard_bucket(kv, nparts, vals=vv, mode=2)
+        return torch.stack([k2, v2], dim=1), c2
+
     def clear(self):
         self.lsm.clear()
 
@@ -124,11 +138,21 @@ class GpuShardBackend:
         return self.lsm.shard_pick(k, v, f, P, n, last)
 
 
+class _DoneEvent:
+    """CPU stand-in for a CUDA event (CPU collectives complete synchronously)."""
+
+    def record(self):
+        pass
+
+    def synchronize(self):
+        pass
+
+
 class ShardedLSM:
     """One LSM per rank, keys partitioned by range, routed by all-to-all."""
 
     def __init__(self, b_global: int, group=None, backend=None, slack_sigma: float = 8.0,
-                 reserve_batches: int = 0):
+                 reserve_batches: int = 0, pipelined=None):
         self.group = group
         self.P = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -146,12 +170,16 @@ class ShardedLSM:
         # communicator, so the host waits only for the bucket kernel and that
         # exchange -- never for the previous batch's local insert, which keeps
         # the device busy while the next batch is routed
-        self._pipelined = isinstance(self.backend, GpuShardBackend)
+        gpu = isinstance(self.backend, GpuShardBackend)
+        self._pipelined = gpu if pipelined is None else bool(pipelined)
         self._pending = None
         self._routed = 0
         if self._pipelined:
             self._meta = dist.new_group(list(range(self.P)))
-            self._h_cnt = torch.empty((2, 2 * self.P), dtype=torch.int32, pin_memory=True)
+            self._h_cnt = torch.empty((2, 2 * self.P), dtype=torch.int32, pin_memory=gpu)
+            # host-side completion of the bucket kernel + count exchange: a CUDA
+            # event on GPUs; CPU backends (the gloo tests) complete synchronously
+            self._event = torch.cuda.Event if gpu else _DoneEvent
 
     # ---- collectives (bytes only) ----
     def _a2a(self, send, send_counts, recv_counts, dtype):
@@ -169,31 +197,30 @@ class ShardedLSM:
         """This rank's slice of one global batch (global positions
         [rank*b_in, (rank+1)*b_in)); all ranks call it together.
 
-        On GPUs the batch is inserted one call later (the next update, or
-        flush(), which every query and cleanup calls first): its bucket kernel
-        and count exchange are enqueued now, the exchange of the records and
-        the local insert of the PREVIOUS batch -- whose counts are already on
-        the host -- follow, so the host never waits for device work in flight."""
-        if vals is None:
-            vals = self.backend.empty(keys.numel(), torch.int32).zero_()
-        if is_delete is None:
-            is_delete = self.backend.empty(keys.numel(), torch.uint8).zero_()
+        The bucket kernel encodes the slice (A1: key variable, tombstone value
+        0) and groups it by owner as (key variable, value) records, which go
+        to their owners in ONE all-to-all; the owner inserts them with
+        lsm_update_records. On GPUs the batch is inserted one call later (the
+        next update, or flush(), which every query and cleanup calls first):
+        its bucket kernel and the count exchange are enqueued now, the record
+        exchange and the local insert of the PREVIOUS batch -- whose counts
+        are already on the host -- follow, so the host never waits for device
+        work in flight."""
+        rec, cnt = self.backend.bucket_records(keys, vals, is_delete, self.P)
         if not self._pipelined:
-            k, v, o, _, cnt = self.backend.bucket(keys, vals, is_delete, self.P, 0, False)
             send, recv = self._exchange_counts(cnt)
-            self._deliver(k, v, o, send, recv)
+            self._deliver(rec, send, recv)
             return
-        k, v, o, _, cnt = self.backend.bucket(keys, vals, is_delete, self.P, 0, False)
         rcnt = self.backend.empty(self.P, torch.int32)
         dist.all_to_all_single(rcnt, cnt, group=self._meta)
         self._routed += 1
         slot = self._routed & 1
         self._h_cnt[slot, :self.P].copy_(cnt, non_blocking=True)
         self._h_cnt[slot, self.P:].copy_(rcnt, non_blocking=True)
-        ev = torch.cuda.Event()
+        ev = self._event()
         ev.record()
         self.flush()
-        self._pending = (k, v, o, ev, slot)
+        self._pending = (rec, ev, slot)
 
     def clear(self):
         """Drop every resident record on this rank (pending batch included)."""
@@ -205,29 +232,37 @@ class ShardedLSM:
         """Insert the batch routed by the last update() (no-op otherwise)."""
         if not self._pipelined or self._pending is None:
             return
-        k, v, o, ev, slot = self._pending
+        rec, ev, slot = self._pending
         self._pending = None
         ev.synchronize()  # its bucket kernel and count exchange only
         h = self._h_cnt[slot].tolist()
-        self._deliver(k, v, o, h[:self.P], h[self.P:])
+        self._deliver(rec, h[:self.P], h[self.P:])
 
-    def _deliver(self, k, v, o, send, recv):
-        rk = self._a2a(k, send, recv, torch.int32)
-        rv = self._a2a(v, send, recv, torch.int32)
-        ro = self._a2a(o, send, recv, torch.uint8)
-        self._local_insert(rk, rv, ro, sum(recv))
+    def _recv_buffer(self, n):
+        """Receive buffer for n records, reused across batches (grow-only)."""
+        buf = getattr(self, "_rbuf", None)
+        if buf is None or buf.shape[0] < n:
+            buf = self.backend.empty(2 * max(n, self.b_local), torch.int32).view(-1, 2)
+            self._rbuf = buf
+        return buf[:n]
+
+    def _deliver(self, rec, send, recv):
+        n = sum(recv)
+        rr = self._recv_buffer(n)
+        dist.all_to_all_single(rr, rec, recv, send, group=self.group)
+        self._local_insert(rr, n)
         self.batches += 1
 
-    def _local_insert(self, rk, rv, ro, n):
+    def _local_insert(self, rr, n):
         if n == 0:
             return
         if n <= self.b_local:
-            self.backend.update(rk[:n], rv[:n], ro[:n])
+            self.backend.update_records(rr)
             return
-        # oversized local batch: 64 hash buckets (equal keys stay together),
-        # packed in order into sub-batches of at most b_local
+        # oversized local batch: 64 hash buckets of the original key (equal
+        # keys stay together), packed in order into sub-batches <= b_local
         self.overflow_splits += 1
-        k2, v2, o2, _, c2 = self.backend.bucket(rk[:n], rv[:n], ro[:n], 64, 1, False)
+        r2, c2 = self.backend.split_records(rr, 64)
         counts = self.backend.host_list(c2)
         if max(counts) > self.b_local:
             raise RuntimeError("shard overflow: one key-hash bucket exceeds b_local; "
@@ -236,8 +271,7 @@ class ShardedLSM:
         for c in counts + [self.b_local + 1]:
             if cur + c > self.b_local:
                 if cur:
-                    self.backend.update(k2[start:start + cur], v2[start:start + cur],
-                                        o2[start:start + cur])
+                    self.backend.update_records(r2[start:start + cur])
                 start += cur
                 cur = 0
             cur += c
@@ -334,23 +368,29 @@ def run_sharded_bench(args, dist_mod, rank, world, local_rank, clock_cls=None, p
     import synth
     from . import to_device
 
-    B_IN = 1 << 20
+    c5 = getattr(args, "config", "c3") == "c5"
     R = 64
-    NQ = 1 << 24
-    b_global = B_IN * world
-    seed = synth.SEED_BASE + 4
+    if c5:   # BASELINE configs[4]: global b = 2^24 split over the ranks (strong scaling)
+        b_global = 1 << 24
+        B_IN = b_global // world
+        NQ = (1 << 26) // world
+        seed = synth.SEED_BASE + 4
+    else:    # C3 per GPU (weak scaling): each rank contributes 2^20 of the global batch
+        B_IN = 1 << 20
+        b_global = B_IN * world
+        NQ = 1 << 24
+        seed = synth.SEED_BASE + 2
     dev = torch.device("cuda", local_rank)
     keys, vals, ops, host = [], [], [], []
     for j in range(R):
-        k, v, d = synth.updates(seed, j * b_global + rank * B_IN, B_IN, delete_frac4=0)
-        keys.append(to_device(k, dev))
-        vals.append(to_device(v, dev))
-        ops.append(to_device(d, dev))
+        k, v, d = synth.updates_t(seed, j * b_global + rank * B_IN, B_IN, delete_frac4=1,
+                                  device=dev)
+        keys.append(k)
+        vals.append(v)
+        ops.append(d)
         if args.e2e:
-            host.append((torch.from_numpy(k.view(np.int32)).pin_memory(),
-                         torch.from_numpy(v.view(np.int32)).pin_memory(),
-                         torch.from_numpy(d).pin_memory()))
-    q = to_device(synth.lookup_queries(seed + rank, NQ, R * b_global), dev)
+            host.append((k.cpu().pin_memory(), v.cpu().pin_memory(), d.cpu().pin_memory()))
+    q = synth.lookup_queries_t(seed + rank, NQ, R * b_global, device=dev)
     sh = ShardedLSM(b_global, reserve_batches=R + 2)
     lsm = sh.backend.lsm
 
@@ -430,12 +470,18 @@ def run_sharded_bench(args, dist_mod, rank, world, local_rank, clock_cls=None, p
             "metric": "M updates/s at batch b; M lookup/count/range queries/s; HBM GB/s vs peak",
             "value": R * b_global / (upd * 1e-3) / 1e6, "unit": "M updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": (upd + look), "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": (upd + look), "higher_is_better": True,
+            "scaling": "strong" if c5 else "weak",
             "vs_baseline": None, "dtype": "u32",
-            "data": "synthetic (splitmix64 uniform keys, insert-only)",
-            "config": {"workload": "C5: key-range sharded LSM, global batch b = N x 2^20 routed by "
-                                   "bucket kernel + NCCL all-to-all, 64 global batches "
-                                   f"(2^26 resident per GPU), 2^24 lookups per rank",
+            "data": "synthetic (splitmix64 uniform keys, 75% insert / 25% delete)",
+            "config": {"workload": ("C5: key-range sharded LSM, global batch b = 2^24 split over "
+                                    "the ranks, routed by the bucket kernel + one NCCL all-to-all "
+                                    "of encoded records, 64 global batches (2^30 resident over "
+                                    "the box), 2^26 lookups over the box") if c5 else
+                                   ("C3 per GPU, key-range sharded: global batch b = N x 2^20 "
+                                    "routed by the bucket kernel + one NCCL all-to-all of encoded "
+                                    "records, 64 global batches (2^26 resident per GPU), 2^24 "
+                                    "lookups per rank"),
                        "b_global": b_global, "b_local": sh.b_local, "batches": R,
                        "parallelism": f"key-range shards x{world}",
                        "l2": "inputs larger than L2 -- no flush"},

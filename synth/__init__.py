@@ -119,3 +119,96 @@ def range_queries(seed: int, nq: int, n_resident: int, L: float,
 def uniform_u32(seed: int, stream: int, count: int) -> np.ndarray:
     """Arbitrary 32-bit words (edge-case query keys incl. >= 2^31-1)."""
     return (h(seed, stream, np.arange(count, dtype=np.uint64)) >> np.uint64(32)).astype(np.uint32)
+
+
+# ---------------------------------------------------------------------------
+# The same generator on a torch device (bit-identical to the numpy one above;
+# pinned by tests/test_synth_torch.py): int64 arithmetic wraps like uint64,
+# and right shifts are made logical with a mask. Used to create bench inputs
+# directly in device memory.
+# ---------------------------------------------------------------------------
+
+def _t():
+    import torch
+    return torch
+
+
+def _i64(x):
+    """A uint64 constant as the int64 with the same bits."""
+    x &= 0xFFFFFFFFFFFFFFFF
+    return x - (1 << 64) if x >= (1 << 63) else x
+
+
+def _lsr(x, k):
+    return (x >> k) & ((1 << (64 - k)) - 1)
+
+
+def splitmix64_t(x):
+    z = x + _i64(0x9E3779B97F4A7C15)
+    z = (z ^ _lsr(z, 30)) * _i64(0xBF58476D1CE4E5B9)
+    z = (z ^ _lsr(z, 27)) * _i64(0x94D049BB133111EB)
+    return z ^ _lsr(z, 31)
+
+
+def h_t(seed: int, stream: int, idx):
+    return splitmix64_t(idx ^ _i64(seed ^ (stream << 56)))
+
+
+def mulhi_t(hv, m):
+    """floor(hv * m / 2^64) for 0 <= m < 2^32 (m a Python int or an int64 tensor)."""
+    lo = hv & 0xFFFFFFFF
+    hi = _lsr(hv, 32)
+    x = lo * m
+    return _lsr(hi * m + _lsr(x, 32), 32)
+
+
+def _u32_t(x):
+    """int64 values in [0, 2^32) -> int32 tensor with the same 32 bits."""
+    torch = _t()
+    return (x - ((x >> 31) & 1) * (1 << 32)).to(torch.int32)
+
+
+def raw_keys_t(seed: int, idx, alphabet: int | None = None):
+    k = mulhi_t(h_t(seed, 0, idx), D)
+    if alphabet is not None:
+        k = k % alphabet
+    return k
+
+
+def updates_t(seed: int, start: int, count: int, delete_frac4: int = 1, device="cuda"):
+    """updates() on a torch device: (keys int32, vals int32, is_delete uint8), the
+    same bits as the numpy arrays."""
+    torch = _t()
+    idx = torch.arange(start, start + count, dtype=torch.int64, device=device)
+    keys = raw_keys_t(seed, idx)
+    vals = idx
+    if delete_frac4 <= 0:
+        return _u32_t(keys), _u32_t(vals & 0xFFFFFFFF), torch.zeros(count, dtype=torch.uint8,
+                                                                   device=device)
+    is_del = (h_t(seed, 1, idx) & 3) < delete_frac4  # % 4 of a uint64 = its low 2 bits
+    safe = torch.clamp(idx, min=1)
+    u = mulhi_t(h_t(seed, 2, idx), safe)
+    tgt = raw_keys_t(seed, u)
+    tgt = torch.where(idx == 0, keys, tgt)
+    keys = torch.where(is_del, tgt, keys)
+    vals = torch.where(is_del, torch.zeros_like(vals), vals & 0xFFFFFFFF)
+    return _u32_t(keys), _u32_t(vals), is_del.to(torch.uint8)
+
+
+def lookup_queries_t(seed: int, nq: int, n_updates: int, device="cuda"):
+    torch = _t()
+    j = torch.arange(nq, dtype=torch.int64, device=device)
+    u = mulhi_t(h_t(seed, 4, j), max(n_updates, 1))
+    hit = raw_keys_t(seed, u)
+    fresh = mulhi_t(h_t(seed, 3, j), D)
+    return _u32_t(torch.where((j & 1) == 0, hit, fresh))
+
+
+def range_queries_t(seed: int, nq: int, n_resident: int, L: float, device="cuda"):
+    torch = _t()
+    w = max(1, int(round(L * D / max(n_resident, 1))))
+    w = min(w, D)
+    j = torch.arange(nq, dtype=torch.int64, device=device)
+    k1 = mulhi_t(h_t(seed, 5, j), D - w + 1)
+    k2 = k1 + (w - 1)
+    return _u32_t(k1), _u32_t(k2)

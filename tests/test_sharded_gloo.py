@@ -84,6 +84,34 @@ class CpuTestBackend:
         self.batch_sizes.append(k.numel())
         self.store.apply_batch(k.numpy().view(np.uint32), v.numpy().view(np.uint32), o.numpy())
 
+    # encoded records (key variable << 1 | regular, value): the GPU router's format
+    def bucket_records(self, keys, vals, ops, P, out=None, counts=None):
+        n = keys.numel()
+        v = vals if vals is not None else torch.zeros(n, dtype=torch.int32)
+        o = ops if ops is not None else torch.zeros(n, dtype=torch.uint8)
+        kb, vb, ob, _, cnt = self.bucket(keys, v, o, P, 0, False)
+        k = kb.numpy().view(np.uint32).astype(np.uint64)
+        dele = ob.numpy() != 0
+        bad = k > 0x7FFFFFFE
+        kv = np.where(bad, 0xFFFFFFFE, (k << np.uint64(1)) | np.where(dele, 0, 1).astype(np.uint64))
+        vv = np.where(dele | bad, 0, vb.numpy().view(np.uint32))
+        rec = np.stack([kv.astype(np.uint32), vv.astype(np.uint32)], axis=1).view(np.int32)
+        return torch.from_numpy(np.ascontiguousarray(rec)), cnt
+
+    def update_records(self, rec):
+        r = rec.numpy().view(np.uint32)
+        kv, vv = r[:, 0], r[:, 1]
+        self.update(torch.from_numpy((kv >> 1).view(np.int32).copy()),
+                    torch.from_numpy(vv.view(np.int32).copy()),
+                    torch.from_numpy(((kv & 1) == 0).astype(np.uint8)))
+
+    def split_records(self, rec, nparts):
+        r = rec.numpy().view(np.uint32)
+        o = self.owner(r[:, 0] >> 1, nparts, 1)
+        perm = np.argsort(o, kind="stable")
+        counts = np.bincount(o, minlength=nparts).astype(np.int32)
+        return torch.from_numpy(np.ascontiguousarray(r[perm]).view(np.int32)), torch.from_numpy(counts)
+
     def lookup(self, q):
         v, f = self.store.lookup(q.numpy().view(np.uint32))
         return torch.from_numpy(v.view(np.int32).copy()), torch.from_numpy(f.copy())
@@ -159,9 +187,10 @@ def _worker(rank, world, port, scenario, out_q):
     try:
         import synth
         from paper_1707_05354_b200.sharded import ShardedLSM, local_batch_size
-        b_global, nbatch, alphabet, slack = scenario
+        b_global, nbatch, alphabet, slack = scenario[:4]
+        pipelined = scenario[4] if len(scenario) > 4 else False
         sh = ShardedLSM(b_global, backend=CpuTestBackend(local_batch_size(b_global, world, slack)),
-                        slack_sigma=slack)
+                        slack_sigma=slack, pipelined=pipelined)
         b_in = b_global // world
         for j in range(nbatch):
             k, v, d = synth.updates(77, j * b_global + rank * b_in, b_in, delete_frac4=1,
@@ -208,7 +237,7 @@ def _run(scenario):
 def _global_oracle(scenario):
     import oracle
     import synth
-    b_global, nbatch, alphabet, _ = scenario
+    b_global, nbatch, alphabet = scenario[:3]
     o = oracle.OracleDict(b_global)
     for j in range(nbatch):
         k, v, d = synth.updates(77, j * b_global, b_global, delete_frac4=1, alphabet=alphabet)
@@ -219,6 +248,8 @@ def _global_oracle(scenario):
 @pytest.mark.parametrize("scenario", [
     (512, 6, None, 8.0),       # uniform keys, normal slack
     (256, 5, 300, 8.0),        # duplicate-heavy: in-batch ties cross ranks
+    (512, 6, None, 8.0, True),  # the GPU path's one-batch-lag pipeline (flush before queries)
+    (256, 5, 300, 8.0, True),
 ])
 def test_sharded_router_matches_global_oracle(scenario):
     res = _run(scenario)
