@@ -99,6 +99,16 @@ struct lsm {
   std::recursive_mutex mu;
   cudaEvent_t idx_ev = nullptr;  // recorded after the last F2/F3 finalize
   bool idx_ev_set = false;
+  // The output of a cleanup (or a bulk build) is ONE sorted array sliced into
+  // views at the set bits of r' (R12): while all of its views are still
+  // occupied, the queries see them as a single level of cv_n records with
+  // its own fence-key index -- same results (one epoch,
+  // unique keys, disjoint key ranges), single-level query kernels.
+  Buffer* cv_owner = nullptr;
+  uint64_t cv_mask = 0;       // the view levels
+  uint64_t cv_n = 0;
+  uint32_t* cv_idx = nullptr;  // F1 | F2 | F3 over cv_n records
+  bool cv_idx_ready = false;
   // profiling
   bool prof_on = false;
   std::vector<ProfRec> prof;
@@ -213,6 +223,36 @@ void level_release(lsm* h, int i, cudaStream_t s) {
   L = Level{};
 }
 
+bool cv_valid(const lsm* h);
+
+// forget the coalesced cleanup/bulk-build level
+void cv_drop(lsm* h, cudaStream_t s) {
+  if (h->cv_idx) cudaFreeAsync(h->cv_idx, s);
+  h->cv_idx = nullptr;
+  h->cv_owner = nullptr;
+  h->cv_mask = 0;
+  h->cv_n = 0;
+  h->cv_idx_ready = false;
+}
+
+// views of one sorted buffer C at the set bits of `mask` (ascending keys into
+// ascending levels): queried as one level with an index over all of them
+cudaError_t cv_set(lsm* h, Buffer* C, uint64_t mask, cudaStream_t s, const LaunchHooks& hk) {
+  cv_drop(h, s);
+  if (mask == 0 || (mask & (mask - 1)) == 0) return cudaSuccess;  // 0 or 1 level: nothing to merge
+  const uint64_t n = mask * h->b;
+  cudaError_t e = pool_alloc(h, (void**)&h->cv_idx, idx_words(n) * 4, s);
+  if (e != cudaSuccess) {
+    h->cv_idx = nullptr;
+    return e;
+  }
+  h->cv_owner = C;
+  h->cv_mask = mask;
+  h->cv_n = n;
+  h->cv_idx_ready = false;
+  return launch_build_f1(C->keys, n, h->cv_idx, s, hk);
+}
+
 // index storage of home level i (F1 | F2 | F3 for b*2^i records)
 cudaError_t home_idx_ensure(lsm* h, int i, cudaStream_t s) {
   if (h->home_idx[i]) return cudaSuccess;
@@ -324,19 +364,35 @@ cudaError_t ensure_qbuf(lsm* h, uint64_t bytes, cudaStream_t s) {
   return cudaSuccess;
 }
 
+// The cleanup / bulk-build views still form one sorted array: all of them
+// occupied and still owned by that buffer. (A cascade that merges a view away
+// releases it; every non-view level is then newer and of lower index.)
+bool cv_valid(const lsm* h) {
+  if (h->sa || h->cv_owner == nullptr || h->cv_mask == 0) return false;
+  if ((h->r & h->cv_mask) != h->cv_mask) return false;
+  for (int i = 0; i < LSM_MAX_LEVELS; ++i)
+    if (((h->cv_mask >> i) & 1ull) && h->level[i].owner != h->cv_owner) return false;
+  return true;
+}
+
 // Level table of the occupied levels, newest first; F3 of as many levels as
 // fit in kF3SmemMax words is staged in shared memory by the query kernels.
+// The cleanup views, while intact, are one entry (the oldest).
 LevelTable level_table(const lsm* h) {
   LevelTable T;
   std::memset(&T, 0, sizeof(T));
   int c = 0;
   uint32_t off = 0;
+  const bool cv = cv_valid(h);
+  const int cv_first = cv ? __builtin_ctzll(h->cv_mask) : -1;
   for (int i = 0; i < LSM_MAX_LEVELS; ++i) {
+    if (cv && ((h->cv_mask >> i) & 1ull) && i != cv_first) continue;
     if (h->sa ? (i == 0 && h->r > 0) : ((h->r >> i) & 1ull)) {
+      const bool v = cv && i == cv_first;
       T.keys[c] = h->sa ? h->sa_buf[h->sa_cur].keys : h->level[i].keys;
       T.vals[c] = h->sa ? h->sa_buf[h->sa_cur].vals : h->level[i].vals;
-      T.idx[c] = h->sa ? h->sa_idx : h->level[i].idx;
-      T.n[c] = h->sa ? h->r * h->b : h->b << i;
+      T.idx[c] = h->sa ? h->sa_idx : (v ? h->cv_idx : h->level[i].idx);
+      T.n[c] = h->sa ? h->r * h->b : (v ? h->cv_n : h->b << i);
       // F3 is staged as a complete search tree in Eytzinger order: 2^h words
       const uint32_t h3 = f3_stage_h(idx_f3_len(T.n[c]));
       const uint64_t words = 1ull << h3;
@@ -367,13 +423,21 @@ cudaError_t ensure_index(lsm* h, cudaStream_t s, const LaunchHooks& hk) {
       h->sa_idx_ready = true;
     }
   } else {
+    const bool cv = cv_valid(h);
     for (int i = 0; i < LSM_MAX_LEVELS; ++i) {
+      if (cv && ((h->cv_mask >> i) & 1ull)) continue;  // queried through cv_idx
       if (((h->r >> i) & 1ull) && !h->level[i].idx_ready) {
         J.idx[J.count] = h->level[i].idx;
         J.n[J.count] = h->b << i;
         ++J.count;
         h->level[i].idx_ready = true;
       }
+    }
+    if (cv && !h->cv_idx_ready) {
+      J.idx[J.count] = h->cv_idx;
+      J.n[J.count] = h->cv_n;
+      ++J.count;
+      h->cv_idx_ready = true;
     }
   }
   if (J.count > 0) {
@@ -485,6 +549,7 @@ lsm_status lsm_destroy(lsm_t* h) {
   {
   ENTER(h);
   cudaDeviceSynchronize();
+  cv_drop(h, nullptr);
   for (int i = 0; i < LSM_MAX_LEVELS; ++i) {
     level_release(h, i, nullptr);
     buf_free(h->home[i], nullptr);
@@ -565,6 +630,7 @@ lsm_status lsm_clear(lsm_t* h, void* stream) {
     h->r = 0;
     return LSM_OK;
   }
+  cv_drop(h, S(stream));
   for (int i = 0; i < LSM_MAX_LEVELS; ++i)
     if ((h->r >> i) & 1ull) level_release(h, i, S(stream));
   h->r = 0;
@@ -705,6 +771,7 @@ static lsm_status do_update(lsm_t* h, const uint32_t* keys, const uint32_t* vals
   st = cascade(h, sk, sv, t, s, hk);
   if (st != LSM_OK) return st;
   commit_insert(h, t);
+  if (h->cv_owner && !cv_valid(h)) cv_drop(h, s);  // a view was merged away
   return LSM_OK;
 }
 
@@ -785,6 +852,7 @@ lsm_status lsm_bulk_build(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_va
     off += b << i;
   }
   h->r = k;
+  CK(cv_set(h, C, k, s, hk));
   return LSM_OK;
 }
 
@@ -828,6 +896,7 @@ lsm_status lsm_update_batches(lsm_t* h, const uint32_t* d_keys, const uint32_t* 
       if (st != LSM_OK) return st;
     }
     commit_insert(h, t);
+    if (h->cv_owner && !cv_valid(h)) cv_drop(h, s);  // a view was merged away
   }
   return LSM_OK;
 }
@@ -1060,6 +1129,7 @@ lsm_status lsm_cleanup(lsm_t* h, void* stream) {
   }
   // 5) new levels are views of C: ascending keys into ascending set bits of
   //    r' (R12), no copy
+  cv_drop(h, s);
   for (int i : occ) level_release(h, i, s);
   uint64_t off = 0;
   int refs = 0;
@@ -1080,8 +1150,10 @@ lsm_status lsm_cleanup(lsm_t* h, void* stream) {
   if (refs == 0) {
     buf_free(*C, s);
     delete C;
+    C = nullptr;
   }
   h->r = r2;
+  if (C) CK(cv_set(h, C, r2, s, hk));
   return take_sticky(h, s);  // the cleanup itself is complete either way
 }
 
