@@ -686,6 +686,8 @@ def run_native(args):
     stream = torch.cuda.current_stream()
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
+    levels_searched = [1, 1]
+
     def step(record):
         e = [ev() for _ in range(10)]
         lsm.clear()
@@ -699,8 +701,10 @@ def run_native(args):
         e[3].record(stream)
         tot_pre = lsm.range_into(k1_d, k2_d, roff, rk, rv)
         e[4].record(stream)
+        levels_searched[0] = lsm.query_levels
         lsm.cleanup()
         e[5].record(stream)
+        levels_searched[1] = lsm.query_levels
         lsm.lookup_into(q_look, lv, lf)
         e[6].record(stream)
         lsm.count_into(k1_d, k2_d, cnt)
@@ -736,6 +740,21 @@ def run_native(args):
     torch.cuda.synchronize()
     prof = lsm.profile_read()
     lsm.profile_enable(False)
+    # SURVEY §8(d) byte model for the query classes (per query; levels = the
+    # sorted runs searched, E[candidates] = L by the generator, R15):
+    #   lookup 9 + 32*levels + 32*hit, count 12 + 64*levels + 4*L,
+    #   range 20 + 64*levels + 12*L + 8*valid
+    hit = float(lf.to(torch.float32).mean().item())
+    lv_pre, lv_post = levels_searched
+    pairs = recs[-1][1] + recs[-1][2]
+    model = {
+        "lookup": NQ * (2 * 9 + 32 * (lv_pre + lv_post) + 2 * 32 * hit),
+        "count": NQ * (2 * 12 + 64 * (lv_pre + lv_post) + 2 * 4 * L_RANGE),
+        "range": NQ * (2 * 20 + 64 * (lv_pre + lv_post) + 2 * 12 * L_RANGE) + 8 * pairs,
+    }
+    for c, bytes_per_step in model.items():
+        if c in prof:
+            prof[c]["alg_bytes"] = bytes_per_step * args.steps
     total_ms = start.elapsed_time(stop)
     # ---- parity gate: the last step's outputs vs O1 ----
     parity = parity_gate(lsm, sub, q_host, k1, k2, lv, lf, cnt, roff, rk, rv, recs[-1][1],
@@ -786,7 +805,12 @@ def run_native(args):
                 "timing": "per-launch CUDA events on the launching stream over K more identical "
                           "steps right after the timed ones (the timed steps run without them: "
                           "per-launch events split programmatic dependent launch)",
-                "share_of_step_kernel_time": prof[dom]["ms"] / step_kernel_ms if step_kernel_ms else None}
+                "share_of_step_kernel_time": prof[dom]["ms"] / step_kernel_ms if step_kernel_ms else None,
+                "byte_model": ("SURVEY §8(d): lookup 9+32*levels+32*hit, count 12+64*levels+4*L, "
+                               "range 20+64*levels+12*L+8*valid B/query (E[candidates]=L, R15); "
+                               "sort/merge/cleanup: the implemented bytes (DESIGN.md §4)"),
+                "levels_searched": {"before_cleanup": levels_searched[0],
+                                    "after_cleanup": levels_searched[1]}}
     per_class = {c: {"ms_per_step": p["ms"] / args.steps,
                      "launches_per_step": p["launches"] / args.steps,
                      "alg_GBps": (p["alg_bytes"] / (p["ms"] * 1e-3) / 1e9) if p["ms"] else None,

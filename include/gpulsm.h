@@ -327,6 +327,11 @@ lsm_status lsm_shard_pick(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_va
 lsm_status lsm_batch_size(const lsm_t* h, uint64_t* b_out);
 /* r: the number of resident batches; level i is full iff bit i of r is set. */
 lsm_status lsm_num_batches(const lsm_t* h, uint64_t* r_out);
+
+/* Number of sorted runs a query searches now: the occupied levels, with the
+ * views of a cleanup or bulk build counted as ONE run while all of them are
+ * still occupied (they form one sorted array). */
+lsm_status lsm_query_levels(lsm_t* h, uint32_t* n_out);
 /* Device view of level i: key variables ((k<<1)|status) and values, n =
  * b*2^i if full else 0 (pointers NULL). Valid until the next mutation.     */
 lsm_status lsm_level_view(const lsm_t* h, uint32_t i, const uint32_t** d_keys,

@@ -57,6 +57,7 @@ SIGNATURES = {
     "lsm_cleanup": ([_vp, _vp], _st),
     "lsm_batch_size": ([_vp, ctypes.POINTER(_u64)], _st),
     "lsm_num_batches": ([_vp, ctypes.POINTER(_u64)], _st),
+    "lsm_query_levels": ([_vp, ctypes.POINTER(ctypes.c_uint32)], _st),
     "lsm_level_view": ([_vp, ctypes.c_uint32, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
                         ctypes.POINTER(_u64)], _st),
     "lsm_sync": ([_vp, _vp], _st),
@@ -331,6 +332,13 @@ class GpuLSM:
     def r(self) -> int:
         v = _u64(0)
         _check(self._lib.lsm_num_batches(self.h, ctypes.byref(v)), "lsm_num_batches")
+        return int(v.value)
+
+    @property
+    def query_levels(self) -> int:
+        """Sorted runs a query searches now (cleanup views count as one)."""
+        v = ctypes.c_uint32()
+        _check(self._lib.lsm_query_levels(self.h, ctypes.byref(v)), "lsm_query_levels")
         return int(v.value)
 
     def level(self, i: int):

@@ -1287,6 +1287,13 @@ lsm_status lsm_num_batches(const lsm_t* h, uint64_t* r_out) {
   return LSM_OK;
 }
 
+lsm_status lsm_query_levels(lsm_t* h, uint32_t* n_out) {
+  if (!h || !n_out) return LSM_ERR_INVALID_ARG;
+  ENTER(h);
+  *n_out = (uint32_t)level_table(h).count;
+  return LSM_OK;
+}
+
 lsm_status lsm_level_view(const lsm_t* h, uint32_t i, const uint32_t** d_keys,
                           const uint32_t** d_vals, uint64_t* n) {
   if (!h || !d_keys || !d_vals || !n || i >= LSM_MAX_LEVELS) return LSM_ERR_INVALID_ARG;
