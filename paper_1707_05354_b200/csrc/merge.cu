@@ -153,6 +153,53 @@ __device__ __forceinline__ uint64_t warp_merge_path(const uint32_t* __restrict__
   return lo + __popc(__ballot_sync(kFull, t));
 }
 
+// Two merge-path searches (diagonals d0 and d1) in the same rounds: every lane
+// probes both per round, so the pair costs the dependent-load rounds of one
+// search (the single-tile merge needs its start and its end split).
+__device__ __forceinline__ void warp_merge_path2(const uint32_t* __restrict__ ak,
+                                                 const uint32_t* __restrict__ bk, uint64_t d0,
+                                                 uint64_t lo0, uint64_t hi0, uint64_t d1,
+                                                 uint64_t lo1, uint64_t hi1, uint64_t& a0,
+                                                 uint64_t& a1) {
+  const uint32_t lane = lane_id();
+  while (hi0 - lo0 > 32 || hi1 - lo1 > 32) {
+    const uint64_t s0 = hi0 - lo0, s1 = hi1 - lo1;
+    const uint64_t p0 = lo0 + ((uint64_t)(lane + 1) * s0) / 33;
+    const uint64_t p1 = lo1 + ((uint64_t)(lane + 1) * s1) / 33;
+    const bool w0 = s0 > 32, w1 = s1 > 32;
+    uint32_t x0 = 0, y0 = 0, x1 = 0, y1 = 0;
+    if (w0) {
+      x0 = __ldg(ak + p0);
+      y0 = __ldg(bk + (d0 - 1 - p0));
+    }
+    if (w1) {
+      x1 = __ldg(ak + p1);
+      y1 = __ldg(bk + (d1 - 1 - p1));
+    }
+    if (w0) {
+      const uint32_t m = __ballot_sync(kFull, (x0 >> 1) <= (y0 >> 1));
+      const int c = __popc(m);
+      const uint64_t plo = __shfl_sync(kFull, p0, c > 0 ? c - 1 : 0);
+      const uint64_t phi = __shfl_sync(kFull, p0, c < 32 ? c : 31);
+      if (c > 0) lo0 = plo + 1;
+      if (c < 32) hi0 = phi;
+    }
+    if (w1) {
+      const uint32_t m = __ballot_sync(kFull, (x1 >> 1) <= (y1 >> 1));
+      const int c = __popc(m);
+      const uint64_t plo = __shfl_sync(kFull, p1, c > 0 ? c - 1 : 0);
+      const uint64_t phi = __shfl_sync(kFull, p1, c < 32 ? c : 31);
+      if (c > 0) lo1 = plo + 1;
+      if (c < 32) hi1 = phi;
+    }
+  }
+  bool t0 = false, t1 = false;
+  if (lane < hi0 - lo0) t0 = (__ldg(ak + lo0 + lane) >> 1) <= (__ldg(bk + (d0 - 1 - lo0 - lane)) >> 1);
+  if (lane < hi1 - lo1) t1 = (__ldg(ak + lo1 + lane) >> 1) <= (__ldg(bk + (d1 - 1 - lo1 - lane)) >> 1);
+  a0 = lo0 + __popc(__ballot_sync(kFull, t0));
+  a1 = lo1 + __popc(__ballot_sync(kFull, t1));
+}
+
 #ifdef GPULSM_PROBE
 __device__ unsigned long long* g_mprobe = nullptr;  // [cta][16] globaltimer stamps
 __device__ __forceinline__ unsigned long long mtimer() {
@@ -200,14 +247,22 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel_t(
   if (warp == 0) {
     // ---------------- producer ----------------
     uint64_t d = t_begin * kMergeTile;
-    uint64_t a = warp_merge_path(ak, bk, d, d > nb ? d - nb : 0, d < na ? d : na);
+    uint64_t a = 0, a_first_end = 0;
+    const uint64_t d_first_end = min(d + (uint64_t)kMergeTile, total);
+    if (STAGES == 1) {  // one tile: its start and end splits searched together
+      warp_merge_path2(ak, bk, d, d > nb ? d - nb : 0, d < na ? d : na, d_first_end,
+                       d_first_end > nb ? d_first_end - nb : 0, d_first_end < na ? d_first_end : na,
+                       a, a_first_end);
+    } else {
+      a = warp_merge_path(ak, bk, d, d > nb ? d - nb : 0, d < na ? d : na);
+    }
     if (lane == 0) MPROBE(2);
     for (uint64_t t = t_begin, k = 0; t < t_end; ++t, ++k) {
       const uint64_t d_end = min(d + (uint64_t)kMergeTile, total);
       uint64_t lo = d_end > nb ? d_end - nb : 0;
       lo = max(lo, a);
       uint64_t hi = min(a + (d_end - d), na);
-      const uint64_t a_end = warp_merge_path(ak, bk, d_end, lo, hi);
+      const uint64_t a_end = (STAGES == 1 && k == 0) ? a_first_end : warp_merge_path(ak, bk, d_end, lo, hi);
       if (lane == 0 && k == 0) MPROBE(3);
       const int s = (int)(k % kStages);
       const uint32_t ph = (uint32_t)((k / kStages) & 1);
