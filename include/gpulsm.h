@@ -82,6 +82,22 @@ typedef enum {
  * handle. Errors: LSM_ERR_INVALID_ARG (b == 0, out NULL), LSM_ERR_NO_DEVICE. */
 lsm_status lsm_create(uint64_t b, lsm_t** out);
 
+/* Stream-ordered device allocator: alloc(bytes, stream, ctx)
+ * returns device memory usable in stream order on `stream` (NULL = out of
+ * memory); free(p, stream, ctx) releases it in stream order, like
+ * cudaFreeAsync. The handle allocates its levels and scratch through it
+ * (the Python binding passes torch's caching allocator). */
+typedef struct {
+  void* (*alloc)(size_t bytes, void* stream, void* ctx);
+  void (*free)(void* p, void* stream, void* ctx);
+  void* ctx;
+} lsm_allocator;
+
+/* lsm_create with the caller's allocator (a == NULL: the handle's own
+ * cudaMemPool, as lsm_create). Errors as lsm_create; LSM_ERR_INVALID_ARG if
+ * a->alloc or a->free is NULL. */
+lsm_status lsm_create_with_allocator(uint64_t b, const lsm_allocator* a, lsm_t** out);
+
 /* N2 -- the paper's GPU SA comparison structure ("a
  * GPU-maintained sorted array"): same handle, same calls, but ONE sorted
  * array of r*b records. An update sorts the batch (A1+A2) and merges it,

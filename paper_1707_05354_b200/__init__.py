@@ -37,6 +37,7 @@ _st = ctypes.c_int
 SIGNATURES = {
     "lsm_create": ([_u64, ctypes.POINTER(_vp)], _st),
     "lsm_create_sa": ([_u64, ctypes.POINTER(_vp)], _st),
+    "lsm_create_with_allocator": ([_u64, _vp, ctypes.POINTER(_vp)], _st),
     "lsm_is_sa": ([_vp, ctypes.POINTER(ctypes.c_int)], _st),
     "lsm_destroy": ([_vp], _st),
     "lsm_reserve": ([_vp, _u64, _vp], _st),
@@ -161,20 +162,60 @@ def to_numpy_u32(t):
     return t.cpu().numpy().view(np.uint32)
 
 
+# lsm_allocator (include/gpulsm.h): a stream-ordered allocator the library
+# calls for its levels and scratch; GpuLSM(..., allocator="torch") passes
+# torch's caching allocator.
+_ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+_FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
+
+
+class LsmAllocator(ctypes.Structure):
+    _fields_ = [("alloc", _ALLOC_FN), ("free", _FREE_FN), ("ctx", ctypes.c_void_p)]
+
+
+def _torch_allocator(device_index):
+    torch = _torch()
+
+    def alloc(nbytes, stream, ctx):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), device_index, int(stream or 0))
+        except Exception:
+            return None  # NULL: out of memory
+
+    def free(p, stream, ctx):
+        try:
+            torch.cuda.caching_allocator_delete(int(p))
+        except Exception:
+            pass
+
+    fa, ff = _ALLOC_FN(alloc), _FREE_FN(free)
+    return LsmAllocator(fa, ff, None), (fa, ff)
+
+
 class GpuLSM:
     """A GPU LSM dictionary with batch size b on the current CUDA device.
 
     sa=True builds the paper's GPU SA comparison structure instead (N2: one
     sorted array, each batch merged into all of it; same calls)."""
 
-    def __init__(self, b: int, reserve_batches: int = 0, sa: bool = False):
+    def __init__(self, b: int, reserve_batches: int = 0, sa: bool = False,
+                 allocator: str | None = None):
         self._lib = load_library()
         torch = _torch()
         if not torch.cuda.is_available():
             raise RuntimeError("GpuLSM needs a CUDA device (no CPU fallback)")
         h = ctypes.c_void_p()
-        create = self._lib.lsm_create_sa if sa else self._lib.lsm_create
-        _check(create(int(b), ctypes.byref(h)), "lsm_create_sa" if sa else "lsm_create")
+        if allocator == "torch":
+            if sa:
+                raise ValueError("allocator='torch' is for the LSM (not the SA) structure")
+            self._alloc, self._alloc_keep = _torch_allocator(torch.cuda.current_device())
+            _check(self._lib.lsm_create_with_allocator(int(b), ctypes.byref(self._alloc),
+                                                       ctypes.byref(h)), "lsm_create_with_allocator")
+        elif allocator is not None:
+            raise ValueError("allocator must be None (the library's pool) or 'torch'")
+        else:
+            create = self._lib.lsm_create_sa if sa else self._lib.lsm_create
+            _check(create(int(b), ctypes.byref(h)), "lsm_create_sa" if sa else "lsm_create")
         self.h = h
         self.b = int(b)
         self.sa = bool(sa)

@@ -93,6 +93,7 @@ struct lsm {
   uint64_t qbuf_bytes = 0;
   uint64_t* h_pinned = nullptr;  // host readback words
   cudaMemPool_t pool = nullptr;
+  lsm_allocator alloc{};  // caller's stream-ordered allocator; alloc == NULL: pool
   std::atomic<uint64_t> launches{0};
   // host bookkeeping (level table, index flags, scratch, profiling) is
   // guarded by one lock per handle; device scratch of queries is per call
@@ -184,13 +185,26 @@ lsm_status cuda_err(cudaError_t e, int line = 0) {
 
 cudaError_t pool_alloc(lsm* h, void** p, uint64_t bytes, cudaStream_t s) {
   if (bytes == 0) bytes = 16;
+  if (h->alloc.alloc != nullptr) {
+    *p = h->alloc.alloc((size_t)bytes, s, h->alloc.ctx);
+    return *p ? cudaSuccess : cudaErrorMemoryAllocation;
+  }
   return cudaMallocFromPoolAsync(p, bytes, h->pool, s);
+}
+
+void pool_free(lsm* h, void* p, cudaStream_t s) {
+  if (p == nullptr) return;
+  if (h->alloc.alloc != nullptr) {
+    h->alloc.free(p, s, h->alloc.ctx);
+    return;
+  }
+  cudaFreeAsync(p, s);
 }
 
 cudaError_t buf_ensure(lsm* h, Buffer& B, uint64_t n, cudaStream_t s) {
   if (B.cap >= n) return cudaSuccess;
-  if (B.keys) cudaFreeAsync(B.keys, s);
-  if (B.vals) cudaFreeAsync(B.vals, s);
+  pool_free(h, B.keys, s);
+  pool_free(h, B.vals, s);
   B.keys = B.vals = nullptr;
   B.cap = 0;
   // +16 elements: the merge's bulk copies read 16-byte-aligned supersets
@@ -202,9 +216,9 @@ cudaError_t buf_ensure(lsm* h, Buffer& B, uint64_t n, cudaStream_t s) {
   return cudaSuccess;
 }
 
-void buf_free(Buffer& B, cudaStream_t s) {
-  if (B.keys) cudaFreeAsync(B.keys, s);
-  if (B.vals) cudaFreeAsync(B.vals, s);
+void buf_free(lsm* h, Buffer& B, cudaStream_t s) {
+  pool_free(h, B.keys, s);
+  pool_free(h, B.vals, s);
   B.keys = B.vals = nullptr;
   B.cap = 0;
 }
@@ -215,11 +229,11 @@ void level_release(lsm* h, int i, cudaStream_t s) {
   Level& L = h->level[i];
   if (L.owner) {
     if (--L.owner->refs == 0) {
-      buf_free(*L.owner, s);
+      buf_free(h, *L.owner, s);
       delete L.owner;
     }
   }
-  if (L.idx_owned && L.idx) cudaFreeAsync(L.idx, s);
+  if (L.idx_owned && L.idx) pool_free(h, L.idx, s);
   L = Level{};
 }
 
@@ -227,7 +241,7 @@ bool cv_valid(const lsm* h);
 
 // forget the coalesced cleanup/bulk-build level
 void cv_drop(lsm* h, cudaStream_t s) {
-  if (h->cv_idx) cudaFreeAsync(h->cv_idx, s);
+  if (h->cv_idx) pool_free(h, h->cv_idx, s);
   h->cv_idx = nullptr;
   h->cv_owner = nullptr;
   h->cv_mask = 0;
@@ -303,12 +317,12 @@ cudaError_t ensure_sort_scratch(lsm* h, cudaStream_t s) {
 }
 
 void bulk_free(lsm* h, cudaStream_t s) {
-  if (h->bulk_meta) cudaFreeAsync(h->bulk_meta, s);
+  if (h->bulk_meta) pool_free(h, h->bulk_meta, s);
   for (int k = 0; k < 2; ++k) {
-    if (h->bulk.tmp_keys[k]) cudaFreeAsync(h->bulk.tmp_keys[k], s);
-    if (h->bulk.tmp_vals[k]) cudaFreeAsync(h->bulk.tmp_vals[k], s);
+    if (h->bulk.tmp_keys[k]) pool_free(h, h->bulk.tmp_keys[k], s);
+    if (h->bulk.tmp_vals[k]) pool_free(h, h->bulk.tmp_vals[k], s);
   }
-  if (h->bulk.tmp_v3) cudaFreeAsync(h->bulk.tmp_v3, s);
+  if (h->bulk.tmp_v3) pool_free(h, h->bulk.tmp_v3, s);
   h->bulk = SortScratch{};
   h->bulk_meta = nullptr;
   h->bulk_cap = 0;
@@ -354,7 +368,7 @@ cudaError_t ensure_bulk_scratch(lsm* h, uint64_t cap, cudaStream_t s) {
 
 cudaError_t ensure_qbuf(lsm* h, uint64_t bytes, cudaStream_t s) {
   if (h->qbuf_bytes >= bytes) return cudaSuccess;
-  if (h->qbuf) cudaFreeAsync(h->qbuf, s);
+  if (h->qbuf) pool_free(h, h->qbuf, s);
   h->qbuf = nullptr;
   h->qbuf_bytes = 0;
   uint64_t nb = std::max<uint64_t>(bytes, 1 << 20);
@@ -475,7 +489,7 @@ struct CallScratch {
   CallScratch(lsm* h_, cudaStream_t s_) : h(h_), s(s_) {}
   cudaError_t get(uint64_t bytes) { return pool_alloc(h, &p, bytes, s); }
   ~CallScratch() {
-    if (p) cudaFreeAsync(p, s);
+    if (p) pool_free(h, p, s);
   }
 };
 
@@ -510,8 +524,11 @@ const char* lsm_status_string(lsm_status s) {
   return "unknown";
 }
 
-lsm_status lsm_create(uint64_t b, lsm_t** out) {
+lsm_status lsm_create(uint64_t b, lsm_t** out) { return lsm_create_with_allocator(b, nullptr, out); }
+
+lsm_status lsm_create_with_allocator(uint64_t b, const lsm_allocator* a, lsm_t** out) {
   if (!out || b == 0 || b > (1ull << 30)) return LSM_ERR_INVALID_ARG;
+  if (a != nullptr && (a->alloc == nullptr || a->free == nullptr)) return LSM_ERR_INVALID_ARG;
   *out = nullptr;
   int dev = 0, ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -523,6 +540,7 @@ lsm_status lsm_create(uint64_t b, lsm_t** out) {
   if (!h) return LSM_ERR_OOM;
   h->device = dev;
   h->b = b;
+  if (a != nullptr) h->alloc = *a;
   cudaMemPoolProps props{};
   props.allocType = cudaMemAllocationTypePinned;
   props.location.type = cudaMemLocationTypeDevice;
@@ -552,29 +570,29 @@ lsm_status lsm_destroy(lsm_t* h) {
   cv_drop(h, nullptr);
   for (int i = 0; i < LSM_MAX_LEVELS; ++i) {
     level_release(h, i, nullptr);
-    buf_free(h->home[i], nullptr);
-    if (h->home_idx[i]) cudaFreeAsync(h->home_idx[i], nullptr);
+    buf_free(h, h->home[i], nullptr);
+    if (h->home_idx[i]) pool_free(h, h->home_idx[i], nullptr);
   }
-  buf_free(h->ping[0], nullptr);
-  buf_free(h->ping[1], nullptr);
-  buf_free(h->sortout, nullptr);
-  if (h->sort_meta) cudaFreeAsync(h->sort_meta, nullptr);
+  buf_free(h, h->ping[0], nullptr);
+  buf_free(h, h->ping[1], nullptr);
+  buf_free(h, h->sortout, nullptr);
+  if (h->sort_meta) pool_free(h, h->sort_meta, nullptr);
   for (int k = 0; k < 2; ++k) {
-    if (h->sort.tmp_keys[k]) cudaFreeAsync(h->sort.tmp_keys[k], nullptr);
-    if (h->sort.tmp_vals[k]) cudaFreeAsync(h->sort.tmp_vals[k], nullptr);
+    if (h->sort.tmp_keys[k]) pool_free(h, h->sort.tmp_keys[k], nullptr);
+    if (h->sort.tmp_vals[k]) pool_free(h, h->sort.tmp_vals[k], nullptr);
   }
-  if (h->sort.tmp_v3) cudaFreeAsync(h->sort.tmp_v3, nullptr);
+  if (h->sort.tmp_v3) pool_free(h, h->sort.tmp_v3, nullptr);
   bulk_free(h, nullptr);
-  buf_free(h->stage, nullptr);
-  buf_free(h->sa_buf[0], nullptr);
-  buf_free(h->sa_buf[1], nullptr);
-  if (h->sa_idx) cudaFreeAsync(h->sa_idx, nullptr);
+  buf_free(h, h->stage, nullptr);
+  buf_free(h, h->sa_buf[0], nullptr);
+  buf_free(h, h->sa_buf[1], nullptr);
+  if (h->sa_idx) pool_free(h, h->sa_idx, nullptr);
   for (int k = 0; k < 2; ++k) {
-    if (h->st_keys[k]) cudaFreeAsync(h->st_keys[k], nullptr);
-    if (h->st_vals[k]) cudaFreeAsync(h->st_vals[k], nullptr);
-    if (h->st_ops[k]) cudaFreeAsync(h->st_ops[k], nullptr);
+    if (h->st_keys[k]) pool_free(h, h->st_keys[k], nullptr);
+    if (h->st_vals[k]) pool_free(h, h->st_vals[k], nullptr);
+    if (h->st_ops[k]) pool_free(h, h->st_ops[k], nullptr);
   }
-  if (h->qbuf) cudaFreeAsync(h->qbuf, nullptr);
+  if (h->qbuf) pool_free(h, h->qbuf, nullptr);
   cudaDeviceSynchronize();
   for (auto& p : h->prof) {
     cudaEventDestroy(p.e0);
@@ -697,7 +715,7 @@ static cudaError_t sa_buf_ensure(lsm* h, Buffer& B, uint64_t n, cudaStream_t s) 
 static cudaError_t sa_idx_ensure(lsm* h, uint64_t n, cudaStream_t s) {
   const uint64_t w = idx_words(n);
   if (h->sa_idx_words >= w) return cudaSuccess;
-  if (h->sa_idx) cudaFreeAsync(h->sa_idx, s);
+  if (h->sa_idx) pool_free(h, h->sa_idx, s);
   h->sa_idx = nullptr;
   h->sa_idx_words = 0;
   const uint64_t want = std::max<uint64_t>(w, h->sa_idx_words + h->sa_idx_words / 2);
@@ -831,7 +849,7 @@ lsm_status lsm_bulk_build(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_va
     e = launch_sort_batch(d_keys, d_vals, d_is_delete, mode, n, k * b, h->bulk, C->keys, C->vals,
                           nullptr, s, hk);
   if (e != cudaSuccess) {
-    buf_free(*C, s);
+    buf_free(h, *C, s);
     delete C;
     return cuda_err(e);
   }
@@ -1119,7 +1137,7 @@ lsm_status lsm_cleanup(lsm_t* h, void* stream) {
   // 4) placebos fill [V, r'b) (R11)
   CK(launch_fill_placebo(C->keys, C->vals, V, r2 * b, s, hk));
   if (h->sa) {  // the compacted buffer becomes the array; its F1 is rebuilt
-    buf_free(h->sa_buf[h->sa_cur], s);
+    buf_free(h, h->sa_buf[h->sa_cur], s);
     h->sa_buf[h->sa_cur] = *C;
     delete C;
     if (r2 > 0) CK(launch_build_f1(h->sa_buf[h->sa_cur].keys, r2 * b, h->sa_idx, s, hk));
@@ -1148,7 +1166,7 @@ lsm_status lsm_cleanup(lsm_t* h, void* stream) {
   }
   C->refs = refs;
   if (refs == 0) {
-    buf_free(*C, s);
+    buf_free(h, *C, s);
     delete C;
     C = nullptr;
   }

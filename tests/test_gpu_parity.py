@@ -813,3 +813,32 @@ def test_unaligned_views():
         sl = slice(j * b, min(len(k2_), (j + 1) * b))
         s1.update(k2_[sl], v2_[sl], d2_[sl])
     assert_levels_equal(gpu, s1, "multi on views")
+
+
+def test_torch_caching_allocator_hook():
+    # lsm_create_with_allocator: levels and scratch come from
+    # torch's caching allocator; results bit-exact as with the library's pool
+    b = 4096
+    before = torch.cuda.memory_allocated()
+    g = pkg.GpuLSM(b, allocator="torch")
+    s1, o1 = oracle.ShadowLSM(b), oracle.OracleDict(b)
+    seed = synth.SEED_BASE + 55
+    for j in range(11):
+        k, v, d = synth.updates(seed, j * b, b, delete_frac4=1, alphabet=30_000)
+        g.update(to_device(k), to_device(v), to_device(d))
+        s1.update(k, v, d)
+        o1.apply_batch(k, v, d)
+    assert torch.cuda.memory_allocated() > before  # the handle's memory is torch's
+    for i in range(s1.num_levels()):
+        gk, gv = g.level(i)
+        sk, sv = s1.level(i)
+        assert np.array_equal(to_numpy_u32(gk), sk) and np.array_equal(to_numpy_u32(gv), sv)
+    q = synth.lookup_queries(seed, 5000, 11 * b, alphabet=30_000)
+    gv_, gf_ = g.lookup(to_device(q))
+    ov, of = o1.lookup(q)
+    assert np.array_equal(gf_.cpu().numpy(), of) and np.array_equal(to_numpy_u32(gv_), ov)
+    g.cleanup()
+    o1.cleanup()
+    gv_, gf_ = g.lookup(to_device(q))
+    assert np.array_equal(gf_.cpu().numpy(), of) and np.array_equal(to_numpy_u32(gv_), ov)
+    g.close()
