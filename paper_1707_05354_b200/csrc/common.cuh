@@ -252,6 +252,8 @@ struct SortScratch {
   uint32_t* tmp_keys[2];  // b-sized ping-pong for the passes
   uint32_t* tmp_vals[2];
   uint32_t* tmp_v3;       // values carried by the MSD scatter (sort_tmp_words(b) words)
+  uint32_t* tmp_v4;       // values of the second MSD level (sort_tmp_words(b) words)
+  uint32_t* msd_cntB;     // [256 << 8] sub-bucket counts of the two-level MSD sort
   uint64_t tiles_cap;     // status capacity in tiles
   int parity;             // which hist half this sort uses
   uint32_t epoch;         // sort counter -> look-back word epochs
@@ -290,10 +292,10 @@ __device__ __forceinline__ void pdl_trigger() {
 }
 
 template <typename... KArgs, typename... Args>
-inline cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, unsigned block, size_t smem,
                               cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
+  cfg.gridDim = grid;
   cfg.blockDim = dim3(block);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;

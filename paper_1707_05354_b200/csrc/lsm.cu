@@ -312,6 +312,10 @@ cudaError_t ensure_sort_scratch(lsm* h, cudaStream_t s) {
     }
     e = pool_alloc(h, (void**)&h->sort.tmp_v3, sort_tmp_words(h->b) * 4, s);
     if (e != cudaSuccess) return e;
+    e = pool_alloc(h, (void**)&h->sort.tmp_v4, sort_tmp_words(h->b) * 4, s);
+    if (e != cudaSuccess) return e;
+    e = pool_alloc(h, (void**)&h->sort.msd_cntB, (256u << 8) * 4, s);
+    if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
@@ -323,6 +327,8 @@ void bulk_free(lsm* h, cudaStream_t s) {
     if (h->bulk.tmp_vals[k]) pool_free(h, h->bulk.tmp_vals[k], s);
   }
   if (h->bulk.tmp_v3) pool_free(h, h->bulk.tmp_v3, s);
+  if (h->bulk.tmp_v4) pool_free(h, h->bulk.tmp_v4, s);
+  if (h->bulk.msd_cntB) pool_free(h, h->bulk.msd_cntB, s);
   h->bulk = SortScratch{};
   h->bulk_meta = nullptr;
   h->bulk_cap = 0;
@@ -361,6 +367,10 @@ cudaError_t ensure_bulk_scratch(lsm* h, uint64_t cap, cudaStream_t s) {
     if (e != cudaSuccess) return e;
   }
   e = pool_alloc(h, (void**)&B.tmp_v3, sort_tmp_words(cap) * 4, s);
+  if (e != cudaSuccess) return e;
+  e = pool_alloc(h, (void**)&B.tmp_v4, sort_tmp_words(cap) * 4, s);
+  if (e != cudaSuccess) return e;
+  e = pool_alloc(h, (void**)&B.msd_cntB, (256u << 8) * 4, s);
   if (e != cudaSuccess) return e;
   h->bulk_cap = cap;
   return cudaSuccess;
@@ -582,6 +592,8 @@ lsm_status lsm_destroy(lsm_t* h) {
     if (h->sort.tmp_vals[k]) pool_free(h, h->sort.tmp_vals[k], nullptr);
   }
   if (h->sort.tmp_v3) pool_free(h, h->sort.tmp_v3, nullptr);
+  if (h->sort.tmp_v4) pool_free(h, h->sort.tmp_v4, nullptr);
+  if (h->sort.msd_cntB) pool_free(h, h->sort.msd_cntB, nullptr);
   bulk_free(h, nullptr);
   buf_free(h, h->stage, nullptr);
   buf_free(h, h->sa_buf[0], nullptr);

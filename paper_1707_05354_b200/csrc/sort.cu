@@ -48,6 +48,8 @@
 
 #include <cstdlib>
 
+#include <cmath>
+
 #include "common.cuh"
 
 namespace gpulsm {
@@ -730,15 +732,19 @@ struct MsdSmem {
 __global__ void __launch_bounds__(kMsdThreads, MSD_MINB) msd_scatter_kernel(
     RawBatch in, uint64_t b, uint32_t* __restrict__ out_keys, uint32_t* __restrict__ out_pos,
     uint32_t* __restrict__ out_vals, uint32_t* __restrict__ cnt, uint32_t* __restrict__ cnt_next,
-    uint32_t* __restrict__ err) {
+    uint32_t* __restrict__ err, uint32_t region_cap, uint32_t* __restrict__ zero_words,
+    uint32_t nzero) {
   extern __shared__ __align__(16) uint8_t msd_smem[];
   MsdSmem& S = *reinterpret_cast<MsdSmem*>(msd_smem);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid < kRadix) S.hist[tid] = 0;
   pdl_wait();
   pdl_trigger();
-  // the next sort's counters (the previous sort finished: pdl_wait)
+  // the next sort's counters (the previous sort finished: pdl_wait), and the
+  // sub-bucket counters of a two-level sort (used only after this kernel)
   if (blockIdx.x == 0 && tid < kRadix) cnt_next[tid] = 0;
+  for (uint32_t i = blockIdx.x * kMsdThreads + tid; i < nzero; i += gridDim.x * kMsdThreads)
+    zero_words[i] = 0;
   __syncthreads();
   const uint32_t tile = blockIdx.x;
 #ifdef GPULSM_PROBE
@@ -808,7 +814,7 @@ __global__ void __launch_bounds__(kMsdThreads, MSD_MINB) msd_scatter_kernel(
   // for another. Records past the region's end are dropped: that bucket is
   // oversized, and the bucket pass regathers it from the raw batch.
   MSDP(3);
-  if (tid < kRadix) S.gdst[tid] = tid * (uint32_t)kBktCap + toff - ts;
+  if (tid < kRadix) S.gdst[tid] = tid * region_cap + toff - ts;
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
@@ -817,7 +823,7 @@ __global__ void __launch_bounds__(kMsdThreads, MSD_MINB) msd_scatter_kernel(
       const uint32_t key = S.keys[idx];
       const uint32_t d = key >> 24;
       const uint32_t g = S.gdst[d] + idx;
-      if (g < (d + 1) * (uint32_t)kBktCap) {
+      if (g < (d + 1) * region_cap) {
         out_keys[g] = key;
         out_pos[g] = S.pos[idx];
         out_vals[g] = S.vals[idx];
@@ -825,6 +831,83 @@ __global__ void __launch_bounds__(kMsdThreads, MSD_MINB) msd_scatter_kernel(
     }
   }
   MSDP(4);
+}
+
+// Second MSD level (two-level sort): CTA (t, d1) takes tile t
+// of top-digit region d1 (written by msd_scatter_kernel) and scatters it by
+// the next w bits into the sub-bucket regions of capB records, exactly like
+// the first level (shared-atomic ranks, one L2 atomic per sub-digit for the
+// tile's slot, digit-ordered staging). A region over capacity is skipped:
+// the rank pass regathers that top digit from the raw batch.
+__global__ void __launch_bounds__(kMsdThreads, 1) msd2_scatter_kernel(
+    const uint32_t* __restrict__ ak, const uint32_t* __restrict__ ap,
+    const uint32_t* __restrict__ av, const uint32_t* __restrict__ cntA, uint32_t capA, uint32_t w,
+    uint32_t* __restrict__ bk, uint32_t* __restrict__ bp, uint32_t* __restrict__ bv,
+    uint32_t* __restrict__ cntB, uint32_t capB) {
+  extern __shared__ __align__(16) uint8_t msd2_smem[];
+  MsdSmem& S = *reinterpret_cast<MsdSmem*>(msd2_smem);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t nd = 1u << w;
+  if (tid < (int)nd) S.hist[tid] = 0;
+  pdl_wait();
+  pdl_trigger();
+  __syncthreads();
+  const uint32_t d1 = blockIdx.y;
+  const uint32_t nA = __ldg(cntA + d1);
+  if (nA > capA) return;  // regathered by the rank pass
+  const uint32_t tile_base = blockIdx.x * (uint32_t)kMsdTile;
+  if (tile_base >= nA) return;
+  const uint32_t tile_n = min((uint32_t)kMsdTile, nA - tile_base);
+  const uint64_t rbase = (uint64_t)d1 * capA + tile_base;
+  const uint32_t wbase = warp * (32 * kSortItems);
+  const uint32_t shift = 24 - w;
+  uint32_t k[kSortItems], pz[kSortItems], v[kSortItems], rk[kSortItems];
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const uint32_t off = wbase + i * 32 + lane;
+    const bool ok = off < tile_n;
+    k[i] = ok ? __ldg(ak + rbase + off) : 0u;
+    pz[i] = ok ? __ldg(ap + rbase + off) : 0u;
+    v[i] = ok ? __ldg(av + rbase + off) : 0u;
+  }
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i)
+    if (wbase + i * 32 + lane < tile_n) rk[i] = atomicAdd(&S.hist[(k[i] >> shift) & (nd - 1)], 1u);
+  __syncthreads();
+  const uint32_t c = tid < (int)nd ? S.hist[tid] : 0u;
+  uint32_t toff = 0;
+  if (tid < (int)nd && c) toff = atomicAdd(cntB + ((d1 << w) | tid), c);
+  uint32_t tot;
+  const uint32_t ts = block_exclusive_scan<kMsdThreads, uint32_t>(c, S.scan, &tot);
+  if (tid < (int)nd) S.tstart[tid] = ts;
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const uint32_t off = wbase + i * 32 + lane;
+    if (off < tile_n) {
+      const uint32_t p = S.tstart[(k[i] >> shift) & (nd - 1)] + rk[i];
+      S.keys[p] = k[i];
+      S.pos[p] = pz[i];
+      S.vals[p] = v[i];
+    }
+  }
+  if (tid < (int)nd) S.gdst[tid] = tid * capB + toff - ts;
+  __syncthreads();
+  const uint64_t obase = (uint64_t)(d1 << w) * capB;
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const uint32_t idx = i * kMsdThreads + tid;
+    if (idx < tile_n) {
+      const uint32_t key = S.keys[idx];
+      const uint32_t d2 = (key >> shift) & (nd - 1);
+      const uint32_t g = S.gdst[d2] + idx;
+      if (g < (d2 + 1) * capB) {  // past the end: that sub-bucket is regathered
+        bk[obase + g] = key;
+        bp[obase + g] = S.pos[idx];
+        bv[obase + g] = S.vals[idx];
+      }
+    }
+  }
 }
 
 #ifndef SORT_BIN_BITS
@@ -840,9 +923,23 @@ __device__ __forceinline__ uint32_t half16(const uint32_t* w, uint32_t bin) {
   return (w[bin >> 1] >> ((bin & 1u) * 16u)) & 0xFFFFu;
 }
 constexpr uint32_t kBinMax = 64;           // larger bins: stable LSD fallback
-constexpr int kBinsPerWarp = kBins / (kBktThreads / 32);  // bins of one warp's sort range
-constexpr int kOetK = 12;  // records per lane in the odd-even transposition sort (even)
-static_assert(kOetK % 2 == 0 && kBinsPerWarp % 32 == 0, "odd-even layout");
+
+// Geometry of the rank pass. One level (one-wave b): bucket g = top digit g,
+// regions of kBktCap at g * kBktCap, start = the counts of the buckets below.
+// Two levels (larger b): bucket g = (top digit d1, next w
+// bits d2) = (g >> w, g & (2^w - 1)), regions of capB at g * capB written by
+// msd2_scatter_kernel; start = the counts of the top digits below d1 plus
+// those of the sub-buckets of d1 below d2. pos_bits: positions are < 2^pos_bits
+// (21 one-wave, 27 two-level); the rest of the position word carries the
+// record's rank in its bin.
+struct BucketGeo {
+  const uint32_t* cntA;  // [256] top-digit counts
+  const uint32_t* cntB;  // [256 << w] sub-bucket counts (two levels) or nullptr
+  uint32_t w;            // sub-digit bits (0: one level)
+  uint32_t capA;         // top-digit region capacity (two levels: overflow test)
+  uint32_t capB;         // region capacity of the buckets this pass reads
+  uint32_t pos_bits;
+};
 
 struct RankSmem {
   uint2 kv[2][kBktCap];  // (key, position)
@@ -860,7 +957,7 @@ struct RankSmem {
 };
 
 __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
-    const uint32_t* __restrict__ cnt, uint32_t* __restrict__ ak, uint32_t* __restrict__ ap,
+    BucketGeo G, uint32_t* __restrict__ ak, uint32_t* __restrict__ ap,
     const uint32_t* __restrict__ av, RawBatch in, uint64_t b, uint32_t* __restrict__ tk,
     uint32_t* __restrict__ tv,
     uint32_t* __restrict__ out_keys, uint32_t* __restrict__ out_vals, uint32_t* __restrict__ out_f1,
@@ -881,9 +978,13 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
   // the bucket's region (msd_scatter_kernel): all loads issued before the
   // start scan so the two latencies overlap (the region holds kBktCap words:
   // every load is in bounds)
-  ak += (uint64_t)d * kBktCap;
-  ap += (uint64_t)d * kBktCap;
-  av += (uint64_t)d * kBktCap;
+  const uint32_t w = G.w;
+  const uint32_t d1 = d >> w, d2 = d & ((1u << w) - 1u);
+  // sub-bucket bits below the top digit and the bin field under them
+  const int bin_shift = 24 - (int)w - kBinBits;
+  ak += (uint64_t)d * G.capB;
+  ap += (uint64_t)d * G.capB;
+  av += (uint64_t)d * G.capB;
   uint32_t kx[kBktItems], ky[kBktItems], kv[kBktItems];
 #pragma unroll
   for (int i = 0; i < kBktItems; ++i) {
@@ -891,19 +992,39 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
     ky[i] = __ldg(ap + i * kBktThreads + tid);
     kv[i] = __ldg(av + i * kBktThreads + tid);
   }
-  {  // output start = records in the buckets below d
-    const uint32_t c = tid < kRadix ? __ldg(cnt + tid) : 0u;
+  {  // output start = records in the top digits below d1 (+ the sub-buckets
+     // of d1 below d2)
+    const uint32_t c = tid < kRadix ? __ldg(G.cntA + tid) : 0u;
     uint32_t tot;
     const uint32_t ex = block_exclusive_scan<kBktThreads, uint32_t>(c, S.scan, &tot);
-    if (tid == (int)d) {
+    if (tid == (int)d1) {
       S.start_d = ex;
       S.size_d = c;
     }
     __syncthreads();
+    if (G.cntB != nullptr) {
+      const uint32_t cb = tid < (1 << w) ? __ldg(G.cntB + ((d1 << w) | tid)) : 0u;
+      const uint32_t exb = block_exclusive_scan<kBktThreads, uint32_t>(cb, S.scan, &tot);
+      __syncthreads();
+      if (tid == (int)d2) {
+        if (S.size_d <= G.capA) {
+          S.start_d += exb;
+          S.size_d = cb;
+        } else if (d2 != 0) {
+          S.size_d = 0;  // top digit over capacity: sub-bucket 0 regathers all of it
+        }
+      }
+      __syncthreads();
+    }
   }
   const uint32_t start = S.start_d, size = S.size_d;
   if (size == 0) return;
-  if (size > (uint32_t)kBktCap) {
+  // over capacity: the whole top digit (one level, or its region overflowed)
+  // or this sub-bucket is regathered from the raw batch
+  const bool whole_digit = G.cntB == nullptr || __ldg(G.cntA + d1) > G.capA;
+  const uint32_t sel_shift = whole_digit ? 24u : 24u - w;
+  const uint32_t sel_val = whole_digit ? d1 : d;
+  if (size > (uint32_t)kBktCap || (!whole_digit && size > G.capB)) {
     // oversized bucket (skewed keys): its region holds only the first
     // kBktCap records, so regather it in input order from the raw batch
     // (stable compaction) into tk/tv[start ..), then the chunked LSD of the
@@ -927,7 +1048,7 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
           const uint32_t op = (inb && in.mode == kModeMixed) ? (uint32_t)__ldg(in.ops + p) : 0u;
           bool bad;
           encode_loaded(in, p, rk, rv, op, key[i], val[i], bad);
-          sel[i] = (key[i] >> 24) == d;
+          sel[i] = (key[i] >> sel_shift) == sel_val;
         }
         mine += __popc(__ballot_sync(kFull, sel[i]));
       }
@@ -1004,16 +1125,19 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
   //      is kept in the position word's free top bits (positions of
   //      one-wave batches are < 2^21; the rank matters only below kBinMax) ----
   static_assert((uint64_t)kSortTile * 148 < (1ull << 21), "positions fit in 21 bits");
+  const uint32_t rank_max = (1u << (32 - G.pos_bits)) - 1u;  // 2047 / 31
+  const uint32_t pos_mask = (1u << G.pos_bits) - 1u;
+  const uint32_t bin_max = min(kBinMax, rank_max);
   for (int i = tid; i < kBins / 2; i += kBktThreads) S.u.b.cnt[i] = 0;
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < kBktItems; ++i) {
     const uint32_t p = i * kBktThreads + tid;
     if (p < size) {
-      const uint32_t bin = (kx[i] >> kBinShift) & (kBins - 1);
+      const uint32_t bin = (kx[i] >> bin_shift) & (kBins - 1);
       const uint32_t sh = (bin & 1u) * 16u;
       const uint32_t r = (atomicAdd(&S.u.b.cnt[bin >> 1], 1u << sh) >> sh) & 0xFFFFu;
-      ky[i] |= min(r, 2047u) << 21;
+      ky[i] |= min(r, rank_max) << G.pos_bits;
     }
   }
   __syncthreads();
@@ -1034,7 +1158,7 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
     S.u.b.start[(tid * kPer + j) >> 1] = run | ((run + c[j]) << 16);
     run += c[j] + c[j + 1];
   }
-  const bool skew = __syncthreads_or(mx > kBinMax);
+  const bool skew = __syncthreads_or(mx > bin_max);
   RPB(2);
   int res = 0;
   if (!skew) {
@@ -1047,8 +1171,9 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
     for (int i = 0; i < kBktItems; ++i) {
       const uint32_t p = i * kBktThreads + tid;
       if (p < size) {
-        const uint32_t g = half16(S.u.b.start, (kx[i] >> kBinShift) & (kBins - 1)) + (ky[i] >> 21);
-        w64[g] = ((unsigned long long)kx[i] << 32) | (ky[i] & 0x1FFFFFu);
+        const uint32_t g = half16(S.u.b.start, (kx[i] >> bin_shift) & (kBins - 1)) +
+                           (ky[i] >> G.pos_bits);
+        w64[g] = ((unsigned long long)kx[i] << 32) | (ky[i] & pos_mask);
         gval[g] = kv[i];
       }
     }
@@ -1066,7 +1191,7 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
       if (g < size) {
         const unsigned long long me = w64[g];
         const uint32_t key = (uint32_t)(me >> 32);
-        const uint32_t bin = (key >> kBinShift) & (kBins - 1);
+        const uint32_t bin = (key >> bin_shift) & (kBins - 1);
         const uint32_t lo = half16(S.u.b.start, bin), hi = lo + half16(S.u.b.cnt, bin);
         uint32_t r = 0;
         for (uint32_t j = lo; j < hi; ++j) r += w64[j] < me;
@@ -1081,16 +1206,17 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
     RPB(6);
     return;
   } else {
-    // skewed bin: stable LSD on the position, then on the key (3 digits each;
-    // one-wave batches have positions < 2^24)
+    // skewed bin: stable LSD on the position (pos_bits: 3 or 4 digits), then
+    // on the key's low 3 digits (the bits above are the bucket's)
     if (tid == 0) atomicOr(overflow, 1u);
 #pragma unroll
     for (int i = 0; i < kBktItems; ++i) {  // (position, key) from the registers
       const uint32_t p = i * kBktThreads + tid;
-      if (p < size) S.kv[0][p] = make_uint2(ky[i] & 0x1FFFFFu, kx[i]);
+      if (p < size) S.kv[0][p] = make_uint2(ky[i] & pos_mask, kx[i]);
     }
     __syncthreads();
-    for (int pass = 0; pass < 3; ++pass) {
+    const int pos_passes = ((int)G.pos_bits + kRadixBits - 1) / kRadixBits;
+    for (int pass = 0; pass < pos_passes; ++pass) {
       local_subpass_kv<kBktThreads, kBktItems>(S.kv[res], size, S.kv[res ^ 1], pass * kRadixBits,
                                                S.u.L);
       res ^= 1;
@@ -1163,6 +1289,9 @@ static cudaError_t sort_attrs() {
     e = cudaFuncSetAttribute(msd_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(MsdSmem));
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(msd2_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(MsdSmem));
+    if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(bucket_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(RankSmem));
     if (e != cudaSuccess) return e;
@@ -1171,10 +1300,32 @@ static cudaError_t sort_attrs() {
   return cudaSuccess;
 }
 
-// words of each sort ping-pong buffer for batches of b records: the MSD +
-// rank mode scatters into 256 fixed regions of kBktCap records
+// Two-level MSD sort: above one wave of tiles and up to
+// 2^27 records (positions in 27 bits). w sub-digit bits give sub-buckets of
+// about 2048-4096 records; top-digit regions hold b/256 + 8 sigma + 1024.
+constexpr uint64_t kTwoLevelMaxB = 1ull << 27;
+static uint32_t sort2_w(uint64_t b) {
+  uint32_t w = 1;
+  while (w < 8 && ((uint64_t)kRadix << (w + 12)) < b) ++w;
+  return w;
+}
+static uint32_t sort2_capA(uint64_t b) {
+  const double m = (double)b / kRadix;
+  const uint64_t c = (uint64_t)(m + 8.0 * std::sqrt(m)) + 1024;
+  return (uint32_t)((c + 3) & ~3ull);
+}
+
+// words of each sort ping-pong buffer for batches of b records: the one-wave
+// MSD + rank mode scatters into 256 fixed regions of kBktCap records, the
+// two-level mode into 256 regions of capA and (256 << w) of kBktCap
 uint64_t sort_tmp_words(uint64_t b) {
-  return b > (uint64_t)kSmallCap ? std::max<uint64_t>(b, (uint64_t)kRadix * kBktCap) : b;
+  if (b <= (uint64_t)kSmallCap) return b;
+  uint64_t w = std::max<uint64_t>(b, (uint64_t)kRadix * kBktCap);
+  if (b <= kTwoLevelMaxB) {
+    w = std::max<uint64_t>(w, (uint64_t)kRadix * sort2_capA(b));
+    w = std::max<uint64_t>(w, ((uint64_t)kRadix << sort2_w(b)) * kBktCap);
+  }
+  return w;
 }
 
 cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals,
@@ -1221,13 +1372,15 @@ cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals
     hk.begin(hk.ctx, LSM_K_SORT_PASS, s);
     e = launch_pdl(msd_scatter_kernel, (unsigned)((b + kMsdTile - 1) / kMsdTile), kMsdThreads,
                    sizeof(MsdSmem), s, in, b,
-                   S.tmp_keys[0], S.tmp_vals[0], S.tmp_v3, cnt, cnt_next, S.err);
+                   S.tmp_keys[0], S.tmp_vals[0], S.tmp_v3, cnt, cnt_next, S.err,
+                   (uint32_t)kBktCap, (uint32_t*)nullptr, 0u);
     // bytes: keys + ops + values read (9 B), (key, position, value) written (12 B)
     hk.end(hk.ctx, LSM_K_SORT_PASS, (double)b * 21.0, s, 1);
     if (e != cudaSuccess) return e;
     hk.begin(hk.ctx, LSM_K_SORT_PASS, s);
-    e = launch_pdl(bucket_rank_kernel, (unsigned)kRadix, kBktThreads, sizeof(RankSmem), s,
-                   (const uint32_t*)cnt, S.tmp_keys[0], S.tmp_vals[0], (const uint32_t*)S.tmp_v3,
+    const BucketGeo G{cnt, nullptr, 0u, (uint32_t)kBktCap, (uint32_t)kBktCap, 21u};
+    e = launch_pdl(bucket_rank_kernel, (unsigned)kRadix, kBktThreads, sizeof(RankSmem), s, G,
+                   S.tmp_keys[0], S.tmp_vals[0], (const uint32_t*)S.tmp_v3,
                    in, b, S.tmp_keys[1],
                    S.tmp_vals[1], out_keys, out_vals, out_f1, S.overflow_dev);
     // bytes: (key, position, value) read (12 B), (key, value) written (8 B)
@@ -1235,7 +1388,39 @@ cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals
     return e;
   }
 
-  // (3) 4-pass LSD onesweep (multi-wave batches or skewed key sets)
+  // (2') two-level MSD + rank (multi-wave batches up to 2^27 records): top
+  //      digit scatter, sub-digit scatter per top-digit region, rank pass per
+  //      sub-bucket
+  if (b <= kTwoLevelMaxB && !S.lsd_only && S.tmp_v4 != nullptr && S.msd_cntB != nullptr) {
+    const uint32_t w = sort2_w(b), capA = sort2_capA(b);
+    uint32_t* cnt = S.msd_cnt + (S.msd_parity ? kRadix : 0);
+    uint32_t* cnt_next = S.msd_cnt + (S.msd_parity ? 0 : kRadix);
+    S.msd_parity ^= 1;
+    hk.begin(hk.ctx, LSM_K_SORT_PASS, s);
+    e = launch_pdl(msd_scatter_kernel, (unsigned)((b + kMsdTile - 1) / kMsdTile), kMsdThreads,
+                   sizeof(MsdSmem), s, in, b, S.tmp_keys[0], S.tmp_vals[0], S.tmp_v3, cnt,
+                   cnt_next, S.err, capA, S.msd_cntB, (uint32_t)kRadix << w);
+    hk.end(hk.ctx, LSM_K_SORT_PASS, (double)b * 21.0, s, 1);
+    if (e != cudaSuccess) return e;
+    hk.begin(hk.ctx, LSM_K_SORT_PASS, s);
+    e = launch_pdl(msd2_scatter_kernel, dim3((capA + kMsdTile - 1) / kMsdTile, kRadix),
+                   kMsdThreads, sizeof(MsdSmem), s, (const uint32_t*)S.tmp_keys[0],
+                   (const uint32_t*)S.tmp_vals[0], (const uint32_t*)S.tmp_v3,
+                   (const uint32_t*)cnt, capA, w, S.tmp_keys[1], S.tmp_vals[1], S.tmp_v4,
+                   S.msd_cntB, (uint32_t)kBktCap);
+    // bytes: (key, position, value) read and written (24 B)
+    hk.end(hk.ctx, LSM_K_SORT_PASS, (double)b * 24.0, s, 1);
+    if (e != cudaSuccess) return e;
+    hk.begin(hk.ctx, LSM_K_SORT_PASS, s);
+    const BucketGeo G{cnt, S.msd_cntB, w, capA, (uint32_t)kBktCap, 27u};
+    e = launch_pdl(bucket_rank_kernel, (unsigned)(kRadix << w), kBktThreads, sizeof(RankSmem), s,
+                   G, S.tmp_keys[1], S.tmp_vals[1], (const uint32_t*)S.tmp_v4, in, b,
+                   S.tmp_keys[0], S.tmp_vals[0], out_keys, out_vals, out_f1, S.overflow_dev);
+    hk.end(hk.ctx, LSM_K_SORT_PASS, (double)b * 20.0, s, 1);
+    return e;
+  }
+
+  // (3) 4-pass LSD onesweep (larger batches or skewed key sets)
   if (use_ctr) {  // multi-wave: digit bases from an upfront histogram
     uint64_t hgrid = (b + 4 * kHistThreads - 1) / (4 * kHistThreads);
     if (hgrid < 1) hgrid = 1;

@@ -170,8 +170,7 @@ def test_multi_tile_sort_and_merge(b):
 
 
 def test_multi_wave_sort():
-    # b > 148 sort tiles: histogram kernel + tile counter + group look-back
-    # over more than one window of groups
+    # b > 148 sort tiles: the two-level MSD + rank sort
     _run_schedule((1 << 21) + 4097, 3, 99, frac4=1, nlook=20_000, nrange=1000)
 
 
@@ -398,12 +397,13 @@ def test_launch_counter_counts_kernels():
     assert mid.launch_count - n2 == 2
     mid.update(to_device(km), to_device(vm), to_device(dm))
     assert mid.launch_count - n2 == 2 + 3  # sort (2) + one merge
-    # multi-wave batch: histogram kernel + 4 passes
+    # multi-wave batch: two-level MSD (top-digit scatter, sub-digit scatter,
+    # rank pass)
     big = pkg.GpuLSM(2_000_000)
     kb, vb, db = synth.updates(2, 0, 2_000_000)
     n1 = big.launch_count
     big.update(to_device(kb), to_device(vb), to_device(db))
-    assert big.launch_count - n1 == 5
+    assert big.launch_count - n1 == 3
 
 
 @pytest.mark.slow
@@ -842,3 +842,39 @@ def test_torch_caching_allocator_hook():
     gv_, gf_ = g.lookup(to_device(q))
     assert np.array_equal(gf_.cpu().numpy(), of) and np.array_equal(to_numpy_u32(gv_), ov)
     g.close()
+
+
+@pytest.mark.slow
+def test_two_level_sort_top_digit_overflow():
+    # b = 2^21 + 5 takes the two-level MSD sort; 30 % of the keys share top
+    # digit 7 (k >> 23 == 7), far over its region: that digit is regathered
+    # from the raw batch and sorted by the chunked LSD -- bit-exact vs S1
+    b = (1 << 21) + 5
+
+    def keyfn(h0, h5):
+        uni = synth.mulhi(h0, synth.D)
+        hot = np.uint64(7 << 23) + (h0 & np.uint64((1 << 23) - 1))
+        return np.where(h5 % np.uint64(10) < np.uint64(3), hot, uni)
+    _run_custom_keys(b, 3, 4242, keyfn)
+
+
+@pytest.mark.slow
+def test_two_level_sort_sub_bucket_overflow():
+    # b = 2^22 (w = 2 sub-digit bits): 6000 keys fall into sub-bucket (top
+    # digit 9, sub-digit 1) and no other key has top digit 9, so only that
+    # sub-bucket exceeds its 5632-record region
+    b = 1 << 22
+
+    def keyfn(h0, h5):
+        uni = synth.mulhi(h0, synth.D)
+        uni = np.where((uni >> np.uint64(23)) == np.uint64(9), uni ^ np.uint64(1 << 27), uni)
+        hot = np.uint64((9 << 23) | (1 << 21)) + (h0 & np.uint64((1 << 21) - 1))
+        return np.where(h5 % np.uint64(b) < np.uint64(6000), hot, uni)
+    _run_custom_keys(b, 2, 4343, keyfn)
+
+
+@pytest.mark.slow
+def test_two_level_sort_duplicates():
+    # duplicate-heavy keys at b = 2^21 + 77: position tie-breaks with 27-bit
+    # positions in the two-level rank pass (first insert wins, R4)
+    _run_schedule((1 << 21) + 77, 3, 4444, frac4=1, alphabet=500_000, nlook=20_000, nrange=1000)
