@@ -878,3 +878,12 @@ def test_two_level_sort_duplicates():
     # duplicate-heavy keys at b = 2^21 + 77: position tie-breaks with 27-bit
     # positions in the two-level rank pass (first insert wins, R4)
     _run_schedule((1 << 21) + 77, 3, 4444, frac4=1, alphabet=500_000, nlook=20_000, nrange=1000)
+
+
+@pytest.mark.slow
+def test_multi_wave_lsd_after_skew():
+    # b = 2^21 + 4097 with keys < 3000: the first batch's single top digit
+    # overflows the two-level sort (one CTA regathers and LSD-sorts it), which
+    # moves the handle to the multi-wave onesweep LSD (tile counter, group
+    # look-back) for the later batches -- all bit-exact vs S1
+    _run_schedule((1 << 21) + 4097, 3, 4545, frac4=1, alphabet=3000, nlook=3000, nrange=300)
