@@ -470,14 +470,17 @@ template <int NL, bool NEED_VAL, typename Emit>
 __device__ __forceinline__ uint32_t walk_slices(const LevelTable& T, uint64_t* pos, uint32_t z,
                                                 int L, Emit emit) {
   constexpr int CAP = NL > 0 ? NL : LSM_MAX_LEVELS;
+  // raw key variable of each level's head (its status bit included, so the
+  // run head's validity needs no reload); kSentRaw past the slice
+  constexpr uint32_t kSentRaw = 0xFFFFFFFFu;
   uint32_t head[CAP];
 #pragma unroll
   for (int j = 0; j < CAP; ++j) {
     if (j < L) {
-      head[j] = kSent;
+      head[j] = kSentRaw;
       if (pos[j] < T.n[j]) {
-        const uint32_t k = __ldg(T.keys[j] + pos[j]) >> 1;
-        if (k <= z) head[j] = k;
+        const uint32_t k = __ldg(T.keys[j] + pos[j]);
+        if ((k >> 1) <= z) head[j] = k;
       }
     }
   }
@@ -490,30 +493,30 @@ __device__ __forceinline__ uint32_t walk_slices(const LevelTable& T, uint64_t* p
     uint32_t m = kSent;
 #pragma unroll
     for (int j = 0; j < CAP; ++j)
-      if (j < L) m = min(m, head[j]);
+      if (j < L && head[j] != kSentRaw) m = min(m, head[j] >> 1);
     if (m == kSent) break;
     bool first = true, valid = false;
     uint32_t val = 0;
 #pragma unroll
     for (int j = 0; j < CAP; ++j) {
-      if (j < L && head[j] == m) {
+      if (j < L && head[j] != kSentRaw && (head[j] >> 1) == m) {
         const uint32_t* K = T.keys[j];
         const uint64_t n = T.n[j];
         uint64_t p = pos[j];
         if (first) {  // newest record of key m: run head in the lowest level
           first = false;
-          valid = (__ldg(K + p) & 1u) != 0;
+          valid = (head[j] & 1u) != 0;
           if (NEED_VAL && valid) val = ldg_pol(T.vals[j] + p, l2_policy_stream());
         }
         // skip the rest of this level's run of key m (stale copies)
-        uint32_t nk = kSent;
+        uint32_t nk = kSentRaw;
         while (++p < n) {
-          nk = __ldg(K + p) >> 1;
-          if (nk != m) break;
-          nk = kSent;
+          nk = __ldg(K + p);
+          if ((nk >> 1) != m) break;
+          nk = kSentRaw;
         }
         pos[j] = p;
-        head[j] = nk <= z ? nk : kSent;
+        head[j] = (nk != kSentRaw && (nk >> 1) <= z) ? nk : kSentRaw;
       }
     }
     if (valid) {
