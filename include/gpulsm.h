@@ -64,7 +64,8 @@ typedef enum {
   LSM_ERR_CAPACITY = 4,     /* lsm_range output larger than `capacity`       */
   LSM_ERR_OOM = 5,          /* device allocation failed                      */
   LSM_ERR_CUDA = 6,         /* CUDA runtime error (launch/sync)              */
-  LSM_ERR_NO_DEVICE = 7     /* no CUDA device / not an sm_100 device         */
+  LSM_ERR_NO_DEVICE = 7,    /* no CUDA device / not an sm_100 device         */
+  LSM_ERR_NCCL = 8          /* an NCCL call of the router failed             */
 } lsm_status;
 
 #define LSM_MAX_KEY 0x7FFFFFFEu   /* user keys in [0, 2^31-2]                 */
@@ -293,6 +294,28 @@ lsm_status lsm_shard_bucket(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_
 lsm_status lsm_shard_bucket_records(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals,
                                     const uint8_t* d_ops, uint64_t n, uint32_t nshards,
                                     uint32_t* d_records_out, uint32_t* d_counts_out, void* stream);
+
+/* ---- Native update router over NCCL ----
+ * One router per rank, bound to that rank's local handle. Every update of a
+ * global batch: lsm_shard_bucket_records (encode + group by owner) -> an NCCL
+ * exchange of the P counts -> (one call later, once the counts are on the
+ * host) one grouped ncclSend/ncclRecv of the encoded records -> the owner's
+ * lsm_update_records (split by key hash when it exceeds b_local). All device
+ * work is enqueued on the caller's stream; the host waits only for the
+ * previous batch's bucket kernel and count exchange. Queries, cleanup and
+ * every read of the local handle must be preceded by lsm_router_flush.
+ * lsm_nccl_unique_id writes the 128-byte NCCL id (rank 0 creates it, the
+ * caller broadcasts it); lsm_router_create is collective over the P ranks. */
+typedef struct lsm_router lsm_router_t;
+lsm_status lsm_nccl_unique_id(void* id_out /* 128 bytes */);
+lsm_status lsm_router_create(lsm_t* local, uint32_t nranks, uint32_t rank, const void* nccl_id,
+                             uint64_t b_in, uint64_t b_local, lsm_router_t** out);
+/* This rank's slice (n <= b_in updates) of one global batch; all ranks call it together. */
+lsm_status lsm_router_update(lsm_router_t* r, const uint32_t* d_keys, const uint32_t* d_vals,
+                             const uint8_t* d_is_delete, uint64_t n, void* stream);
+lsm_status lsm_router_flush(lsm_router_t* r, void* stream);
+lsm_status lsm_router_stats(const lsm_router_t* r, uint64_t* batches_out, uint64_t* splits_out);
+lsm_status lsm_router_destroy(lsm_router_t* r);
 
 /* out[perm[i]] = in[i] for i < n: routes lookup results back to the query
  * order a lsm_shard_bucket permutation came from. d_found_* may be NULL.   */

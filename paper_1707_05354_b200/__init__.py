@@ -70,6 +70,13 @@ SIGNATURES = {
                           _vp, _vp, _vp], _st),
     "lsm_shard_bucket_records": ([_vp, _vp, _vp, _vp, _u64, ctypes.c_uint32, _vp, _vp, _vp], _st),
     "lsm_shard_scatter": ([_vp, _vp, _vp, _vp, _u64, _vp, _vp, _vp], _st),
+    "lsm_nccl_unique_id": ([_vp], _st),
+    "lsm_router_create": ([_vp, ctypes.c_uint32, ctypes.c_uint32, _vp, _u64, _u64,
+                           ctypes.POINTER(_vp)], _st),
+    "lsm_router_update": ([_vp, _vp, _vp, _vp, _u64, _vp], _st),
+    "lsm_router_flush": ([_vp, _vp], _st),
+    "lsm_router_stats": ([_vp, ctypes.POINTER(_u64), ctypes.POINTER(_u64)], _st),
+    "lsm_router_destroy": ([_vp], _st),
     "lsm_shard_clip": ([_vp, _vp, _vp, _u64, ctypes.c_uint32, ctypes.c_uint32, _vp, _vp, _vp], _st),
     "lsm_shard_sum": ([_vp, _vp, ctypes.c_uint32, _u64, _vp, _vp], _st),
     "lsm_shard_pick": ([_vp, _vp, _vp, _vp, ctypes.c_uint32, _u64, ctypes.c_int, _vp, _vp, _vp,
@@ -190,6 +197,55 @@ def _torch_allocator(device_index):
 
     fa, ff = _ALLOC_FN(alloc), _FREE_FN(free)
     return LsmAllocator(fa, ff, None), (fa, ff)
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id for NativeRouter (created on one rank, broadcast)."""
+    lib = load_library()
+    buf = ctypes.create_string_buffer(128)
+    _check(lib.lsm_nccl_unique_id(buf), "lsm_nccl_unique_id")
+    return buf.raw
+
+
+class NativeRouter:
+    """The native update router of the key-range sharded LSM (router.cu): bucket
+    kernel + NCCL count exchange + one grouped NCCL exchange of encoded records
+    + local insert, all enqueued from C++ on the caller's stream."""
+
+    def __init__(self, local: "GpuLSM", nranks: int, rank: int, nccl_id: bytes, b_in: int,
+                 b_local: int):
+        self._lib = load_library()
+        self.local = local
+        h = ctypes.c_void_p()
+        idb = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        _check(self._lib.lsm_router_create(local.h, int(nranks), int(rank), idb, int(b_in),
+                                           int(b_local), ctypes.byref(h)), "lsm_router_create")
+        self.h = h
+
+    def update(self, keys, vals=None, is_delete=None, stream=None):
+        _check(self._lib.lsm_router_update(self.h, _dev(keys, 4, "keys"), _dev(vals, 4, "vals"),
+                                           _dev(is_delete, 1, "is_delete"), keys.numel(),
+                                           _stream_ptr(stream)), "lsm_router_update")
+
+    def flush(self, stream=None):
+        _check(self._lib.lsm_router_flush(self.h, _stream_ptr(stream)), "lsm_router_flush")
+
+    def stats(self):
+        b, sp = _u64(0), _u64(0)
+        _check(self._lib.lsm_router_stats(self.h, ctypes.byref(b), ctypes.byref(sp)),
+               "lsm_router_stats")
+        return int(b.value), int(sp.value)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._lib.lsm_router_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class GpuLSM:

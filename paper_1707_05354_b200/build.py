@@ -15,13 +15,32 @@ INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libgpulsm.so")
 BUILD = os.path.join(HERE, "_build")
 
-SOURCES = ["sort.cu", "merge.cu", "query.cu", "scan.cu", "index.cu", "cleanup.cu", "shard.cu", "lsm.cu"]
+SOURCES = ["sort.cu", "merge.cu", "query.cu", "scan.cu", "index.cu", "cleanup.cu", "shard.cu", "lsm.cu",
+           "router.cu"]
+
+
+def _nccl_dirs():
+    """(include dir, lib dir) of the NCCL that torch loads (the nvidia-nccl
+    wheel), else the system one. The native router links it by soname, so at
+    run time it shares the library torch.distributed already loaded."""
+    try:
+        import nvidia.nccl
+        base = list(nvidia.nccl.__path__)[0]
+        inc, lib = os.path.join(base, "include"), os.path.join(base, "lib")
+        if os.path.exists(os.path.join(inc, "nccl.h")) and os.path.exists(os.path.join(lib, "libnccl.so.2")):
+            return inc, lib
+    except ImportError:
+        pass
+    return "/usr/include", "/usr/lib/x86_64-linux-gnu"
+
+
+NCCL_INC, NCCL_LIB = _nccl_dirs()
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
     "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-    "-I", INCLUDE, "-I", CSRC,
+    "-I", INCLUDE, "-I", CSRC, "-I", NCCL_INC,
 ]
 
 
@@ -66,7 +85,9 @@ def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB
         raise RuntimeError(f"nvcc failed for {failed}")
     tmp = lib + ".tmp"
     subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
-                           "-Xcompiler", "-fPIC", "--cudart", "static", *objs, "-o", tmp])
+                           "-Xcompiler", "-fPIC", "--cudart", "static", *objs,
+                           "-L", NCCL_LIB, "-l:libnccl.so.2", "-Xlinker", f"-rpath={NCCL_LIB}",
+                           "-o", tmp])
     os.replace(tmp, lib)
     return lib
 

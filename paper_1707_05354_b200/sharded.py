@@ -152,7 +152,7 @@ class ShardedLSM:
     """One LSM per rank, keys partitioned by range, routed by all-to-all."""
 
     def __init__(self, b_global: int, group=None, backend=None, slack_sigma: float = 8.0,
-                 reserve_batches: int = 0, pipelined=None):
+                 reserve_batches: int = 0, pipelined=None, native=None):
         self.group = group
         self.P = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -165,13 +165,22 @@ class ShardedLSM:
         self.backend = backend if backend is not None else GpuShardBackend(
             self.b_local, reserve_batches=reserve_batches)
         self.batches = 0
-        self.overflow_splits = 0
+        self._py_splits = 0
         # GPU: the per-batch count exchange runs on a side stream over its own
         # communicator, so the host waits only for the bucket kernel and that
         # exchange -- never for the previous batch's local insert, which keeps
         # the device busy while the next batch is routed
         gpu = isinstance(self.backend, GpuShardBackend)
         self._pipelined = gpu if pipelined is None else bool(pipelined)
+        # GPU + NCCL: the per-batch update path runs natively (router.cu):
+        # same protocol, no Python or torch.distributed per batch
+        self._native = None
+        if gpu and native is not False and dist.get_backend(group) == "nccl":
+            from . import NativeRouter, nccl_unique_id
+            obj = [nccl_unique_id() if self.rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            self._native = NativeRouter(self.backend.lsm, self.P, self.rank, obj[0], self.b_in,
+                                        self.b_local)
         self._pending = None
         self._routed = 0
         if self._pipelined:
@@ -180,6 +189,11 @@ class ShardedLSM:
             # host-side completion of the bucket kernel + count exchange: a CUDA
             # event on GPUs; CPU backends (the gloo tests) complete synchronously
             self._event = torch.cuda.Event if gpu else _DoneEvent
+
+    @property
+    def overflow_splits(self) -> int:
+        """Local batches split by key hash for exceeding b_local."""
+        return self._py_splits + (self._native.stats()[1] if self._native is not None else 0)
 
     # ---- collectives (bytes only) ----
     def _a2a(self, send, send_counts, recv_counts, dtype):
@@ -206,6 +220,10 @@ class ShardedLSM:
         exchange and the local insert of the PREVIOUS batch -- whose counts
         are already on the host -- follow, so the host never waits for device
         work in flight."""
+        if self._native is not None:
+            self._native.update(keys, vals, is_delete)
+            self.batches += 1
+            return
         rec, cnt = self.backend.bucket_records(keys, vals, is_delete, self.P)
         if not self._pipelined:
             send, recv = self._exchange_counts(cnt)
@@ -230,6 +248,9 @@ class ShardedLSM:
 
     def flush(self):
         """Insert the batch routed by the last update() (no-op otherwise)."""
+        if self._native is not None:
+            self._native.flush()
+            return
         if not self._pipelined or self._pending is None:
             return
         rec, ev, slot = self._pending
@@ -261,7 +282,7 @@ class ShardedLSM:
             return
         # oversized local batch: 64 hash buckets of the original key (equal
         # keys stay together), packed in order into sub-batches <= b_local
-        self.overflow_splits += 1
+        self._py_splits += 1
         r2, c2 = self.backend.split_records(rr, 64)
         counts = self.backend.host_list(c2)
         if max(counts) > self.b_local:
@@ -501,5 +522,7 @@ def run_sharded_bench(args, dist_mod, rank, world, local_rank, clock_cls=None, p
         }
         print(json.dumps(line), flush=True)
     dist_mod.barrier()
+    if sh._native is not None:
+        sh._native.close()
     dist_mod.destroy_process_group()
     return 0

@@ -112,7 +112,10 @@ def _free_port():
     return p
 
 
-def test_sharded_router_single_gpu_nccl():
+@pytest.mark.parametrize("native", [True, False])
+def test_sharded_router_single_gpu_nccl(native):
+    # native=True: the per-batch update path in router.cu (NCCL from C++);
+    # False: the Python router (torch.distributed all-to-alls)
     import torch.distributed as dist
     from paper_1707_05354_b200.sharded import ShardedLSM
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -120,7 +123,8 @@ def test_sharded_router_single_gpu_nccl():
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     try:
         b = 1 << 14
-        sh = ShardedLSM(b)
+        sh = ShardedLSM(b, native=native)
+        assert (sh._native is not None) == native
         o = oracle.OracleDict(b)
         for j in range(9):
             k, v, d = synth.updates(5, j * b, b, delete_frac4=1, alphabet=50_000)
@@ -143,5 +147,36 @@ def test_sharded_router_single_gpu_nccl():
         ooff, ok, ov2 = o.range(k1, k2)
         assert np.array_equal(ro.cpu().numpy().astype(np.uint64), ooff)
         assert np.array_equal(to_numpy_u32(rk), ok) and np.array_equal(to_numpy_u32(rv), ov2)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_native_router_oversize_split():
+    # b_local < b_in: every received batch exceeds the local batch size and is
+    # split by a hash of the original key (equal keys stay together) into
+    # sub-batches inserted in order -- lookups and counts equal to O1
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        b_in, b_local = 1 << 14, 3 << 12
+        local = pkg.GpuLSM(b_local)
+        rt = pkg.NativeRouter(local, 1, 0, pkg.nccl_unique_id(), b_in, b_local)
+        o = oracle.OracleDict(b_in)
+        for j in range(5):
+            k, v, d = synth.updates(8, j * b_in, b_in, delete_frac4=1, alphabet=40_000)
+            rt.update(to_device(k), to_device(v), to_device(d))
+            o.apply_batch(k, v, d)
+        rt.flush()
+        assert rt.stats() == (5, 5)
+        q = synth.lookup_queries(9, 20_000, 5 * b_in, alphabet=40_000)
+        qv, qf = local.lookup(to_device(q))
+        ov, of = o.lookup(q)
+        assert np.array_equal(qf.cpu().numpy(), of) and np.array_equal(to_numpy_u32(qv), ov)
+        k1, k2 = synth.range_queries(10, 3000, 5 * b_in, 12, domain=40_002)
+        assert np.array_equal(to_numpy_u32(local.count(to_device(k1), to_device(k2))),
+                              o.count(k1, k2))
+        rt.close()
     finally:
         dist.destroy_process_group()
