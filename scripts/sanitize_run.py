@@ -46,7 +46,7 @@ run(1000, 7, multi=True)          # multi-batch insertion
 run(8192, 4, L=2000)              # one level, long slices: warp-cooperative walk
 run(20_000, 3, alphabet=3000)     # oversized bucket: regather + chunked LSD
 if os.environ.get("SAN_BIG"):
-    run(1 << 21, 2)                   # multi-wave 4-pass LSD sort
+    run(1_100_000, 2)                 # above one wave: the two-level MSD + rank sort
 g = pkg.GpuLSM(256)
 k, v, d = synth.updates(3, 0, 2000, delete_frac4=1, alphabet=700)
 g.bulk_build(to_device(k), to_device(v), to_device(d)); g.sync()
