@@ -748,10 +748,16 @@ def run_native(args):
     lv_pre, lv_post = levels_searched
     pairs = recs[-1][1] + recs[-1][2]
     model = {
+        # encode + sort: §8(d)'s 70 B/update (the onesweep-LSD figure; the
+        # MSD + rank implementation moves 41 B of it)
+        "sort_pass": 70.0 * R * B,
         "lookup": NQ * (2 * 9 + 32 * (lv_pre + lv_post) + 2 * 32 * hit),
         "count": NQ * (2 * 12 + 64 * (lv_pre + lv_post) + 2 * 4 * L_RANGE),
         "range": NQ * (2 * 20 + 64 * (lv_pre + lv_post) + 2 * 12 * L_RANGE) + 8 * pairs,
     }
+    # cleanup (count + write + placebo fill; the merges are in "merge"):
+    # read 8n, write 8r'b
+    model["cleanup"] = 8.0 * R * B + 8.0 * lsm.r * B
     for c, bytes_per_step in model.items():
         if c in prof:
             prof[c]["alg_bytes"] = bytes_per_step * args.steps
@@ -806,9 +812,11 @@ def run_native(args):
                           "steps right after the timed ones (the timed steps run without them: "
                           "per-launch events split programmatic dependent launch)",
                 "share_of_step_kernel_time": prof[dom]["ms"] / step_kernel_ms if step_kernel_ms else None,
-                "byte_model": ("SURVEY §8(d): lookup 9+32*levels+32*hit, count 12+64*levels+4*L, "
-                               "range 20+64*levels+12*L+8*valid B/query (E[candidates]=L, R15); "
-                               "sort/merge/cleanup: the implemented bytes (DESIGN.md §4)"),
+                "byte_model": ("SURVEY §8(d) per-unit figures: sort 70 B/update (the MSD + rank "
+                               "implementation moves 41 B), merge 16 B per output record, lookup "
+                               "9+32*levels+32*hit, count 12+64*levels+4*L, range "
+                               "20+64*levels+12*L+8*valid B/query (E[candidates]=L, R15), cleanup "
+                               "8n + 8r'b"),
                 "levels_searched": {"before_cleanup": levels_searched[0],
                                     "after_cleanup": levels_searched[1]}}
     per_class = {c: {"ms_per_step": p["ms"] / args.steps,
