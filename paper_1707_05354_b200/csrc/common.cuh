@@ -253,7 +253,7 @@ struct SortScratch {
   uint32_t* tmp_vals[2];
   uint32_t* tmp_v3;       // values carried by the MSD scatter (sort_tmp_words(b) words)
   uint32_t* tmp_v4;       // values of the second MSD level (sort_tmp_words(b) words)
-  uint32_t* msd_cntB;     // [256 << 8] sub-bucket counts of the two-level MSD sort
+  uint32_t* msd_cntB;     // [kMsdCntBWords] sub-bucket counts of the two-level MSD sort
   uint64_t tiles_cap;     // status capacity in tiles
   int parity;             // which hist half this sort uses
   uint32_t epoch;         // sort counter -> look-back word epochs
@@ -261,12 +261,16 @@ struct SortScratch {
   uint32_t* overflow_dev; // mapped host word: a bucket overflowed shared memory
   volatile uint32_t* overflow_host;
   bool lsd_only;          // skewed keys seen: use the 4-pass LSD path
-  uint32_t* msd_cnt;      // [2][256] bucket counts of the MSD + rank mode (double-buffered)
+  uint32_t* msd_cnt;      // [2][kMsdCntWords] bucket counts of the MSD + rank mode (double-buffered)
   uint32_t* msd_bar;      // [2] its grid-barrier words
   int msd_parity;
 };
 // words of the sort metadata head (before the look-back status words)
-constexpr uint64_t kSortMetaHead = 3 * 4 * 256 + 16 + 2 * 256 + 2 * 256 + 16;
+// hist[2][4][256] | bases[4][256] | tile_ctr/err/done (16) | bkt[2][256] |
+// msd_cnt[2][512] | msd_bar (16)
+constexpr uint64_t kSortMetaHead = 3 * 4 * 256 + 16 + 2 * 256 + 2 * 512 + 16;
+constexpr uint32_t kMsdCntWords = 512;          // one msd_cnt half (>= MSD digits)
+constexpr uint32_t kMsdCntBWords = 512u << 8;   // msd_cntB (two-level sub-bucket counts)
 
 // one fat tile per SM: 1024 threads x 7 records (b = 2^20 -> 147 tiles)
 constexpr int kSortThreads = 1024;
@@ -275,7 +279,8 @@ constexpr int kSortTile = kSortThreads * kSortItems;
 constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;
 constexpr int kPasses = 4;
-static_assert(kSortMetaHead == 3 * kPasses * kRadix + 16 + 4 * kRadix + 16, "sort meta layout");
+static_assert(kSortMetaHead == 3 * kPasses * kRadix + 16 + 2 * kRadix + 2 * kMsdCntWords + 16,
+              "sort meta layout");
 
 inline uint64_t sort_tiles(uint64_t b) { return (b + kSortTile - 1) / kSortTile; }
 inline uint64_t sort_groups(uint64_t b) { return (sort_tiles(b) + 31) / 32; }

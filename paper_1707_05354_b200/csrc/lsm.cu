@@ -290,7 +290,7 @@ cudaError_t ensure_sort_scratch(lsm* h, cudaStream_t s) {
     h->sort.done_ctr = h->sort.tile_ctr + 5;
     h->sort.bkt = h->sort_meta + 3 * kPasses * kRadix + 16;
     h->sort.msd_cnt = h->sort.bkt + 2 * kRadix;
-    h->sort.msd_bar = h->sort.msd_cnt + 2 * kRadix;
+    h->sort.msd_bar = h->sort.msd_cnt + 2 * kMsdCntWords;
     h->sort.msd_parity = 0;
     h->sort.status = h->sort_meta + head;
     // overflow flag of the MSD + local sort: a mapped host word, so the host
@@ -314,7 +314,7 @@ cudaError_t ensure_sort_scratch(lsm* h, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     e = pool_alloc(h, (void**)&h->sort.tmp_v4, sort_tmp_words(h->b) * 4, s);
     if (e != cudaSuccess) return e;
-    e = pool_alloc(h, (void**)&h->sort.msd_cntB, (256u << 8) * 4, s);
+    e = pool_alloc(h, (void**)&h->sort.msd_cntB, (uint64_t)kMsdCntBWords * 4, s);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -353,7 +353,7 @@ cudaError_t ensure_bulk_scratch(lsm* h, uint64_t cap, cudaStream_t s) {
   B.done_ctr = B.tile_ctr + 5;
   B.bkt = h->bulk_meta + 3 * kPasses * kRadix + 16;
   B.msd_cnt = B.bkt + 2 * kRadix;
-  B.msd_bar = B.msd_cnt + 2 * kRadix;
+  B.msd_bar = B.msd_cnt + 2 * kMsdCntWords;
   B.msd_parity = 0;
   B.status = h->bulk_meta + head;
   B.overflow_dev = h->sort.overflow_dev;
@@ -370,7 +370,7 @@ cudaError_t ensure_bulk_scratch(lsm* h, uint64_t cap, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   e = pool_alloc(h, (void**)&B.tmp_v4, sort_tmp_words(cap) * 4, s);
   if (e != cudaSuccess) return e;
-  e = pool_alloc(h, (void**)&B.msd_cntB, (256u << 8) * 4, s);
+  e = pool_alloc(h, (void**)&B.msd_cntB, (uint64_t)kMsdCntBWords * 4, s);
   if (e != cudaSuccess) return e;
   h->bulk_cap = cap;
   return cudaSuccess;

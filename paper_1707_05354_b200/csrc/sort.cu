@@ -673,11 +673,23 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_sort_kernel(
   }
 }
 
+// MSD digit of the MSD + rank mode: the top MSD_BITS bits of the key variable
+// (8: 256 buckets of ~4096 records at b = 2^20, two 512-thread bucket CTAs per
+// SM; 9: 512 buckets of ~2048, four 256-thread CTAs per SM -- measured 22.97
+// vs 22.13 us per 2^20 sort: the bucket pass gains 1 us, the scatter loses 1)
+#ifndef MSD_BITS
+#define MSD_BITS 8
+#endif
+constexpr int kMsdBits = MSD_BITS;
+constexpr int kMsdDigits = 1 << kMsdBits;
+constexpr int kMsdShift = 32 - kMsdBits;
+static_assert(kMsdDigits <= (int)kMsdCntWords, "msd counter layout");
 // bucket pass of the MSD + rank mode: CTA d sorts bucket d (all records whose
 // top digit is d)
-constexpr int kBktThreads = 512;
-constexpr int kBktItems = 11;
-constexpr int kBktCap = kBktThreads * kBktItems;  // 5632
+constexpr int kBktThreads = kMsdBits == 9 ? 256 : 512;
+constexpr int kBktCtasPerSm = kMsdBits == 9 ? 4 : 2;
+constexpr int kBktItems = kMsdBits == 9 ? 10 : 11;
+constexpr int kBktCap = kBktThreads * kBktItems;  // 2560 / 5632
 
 // ---------------------------------------------------------------------------
 // MSD + rank mode (default for one-wave batches). The batch
@@ -723,9 +735,9 @@ struct MsdSmem {
   uint32_t keys[kMsdTile];
   uint32_t pos[kMsdTile];
   uint32_t vals[kMsdTile];
-  uint32_t hist[kRadix];    // tile digit counts (atomic ranks)
-  uint32_t tstart[kRadix];  // tile-local digit starts
-  uint32_t gdst[kRadix];    // global destination - tile-local start
+  uint32_t hist[kMsdDigits];    // tile digit counts (atomic ranks)
+  uint32_t tstart[kMsdDigits];  // tile-local digit starts
+  uint32_t gdst[kMsdDigits];    // global destination - tile-local start
   uint32_t scan[kMsdThreads / 32 + 1];
 };
 
@@ -737,12 +749,12 @@ __global__ void __launch_bounds__(kMsdThreads, MSD_MINB) msd_scatter_kernel(
   extern __shared__ __align__(16) uint8_t msd_smem[];
   MsdSmem& S = *reinterpret_cast<MsdSmem*>(msd_smem);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid < kRadix) S.hist[tid] = 0;
+  if (tid < kMsdDigits) S.hist[tid] = 0;
   pdl_wait();
   pdl_trigger();
   // the next sort's counters (the previous sort finished: pdl_wait), and the
   // sub-bucket counters of a two-level sort (used only after this kernel)
-  if (blockIdx.x == 0 && tid < kRadix) cnt_next[tid] = 0;
+  if (blockIdx.x == 0 && tid < kMsdDigits) cnt_next[tid] = 0;
   for (uint32_t i = blockIdx.x * kMsdThreads + tid; i < nzero; i += gridDim.x * kMsdThreads)
     zero_words[i] = 0;
   __syncthreads();
@@ -787,23 +799,23 @@ __global__ void __launch_bounds__(kMsdThreads, MSD_MINB) msd_scatter_kernel(
   MSDP(1);
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i)
-    if (wbase + i * 32 + lane < tile_n) rk[i] = atomicAdd(&S.hist[k[i] >> 24], 1u);
+    if (wbase + i * 32 + lane < tile_n) rk[i] = atomicAdd(&S.hist[k[i] >> kMsdShift], 1u);
   __syncthreads();
   MSDP(2);
-  const uint32_t c = tid < kRadix ? S.hist[tid] : 0u;
+  const uint32_t c = tid < kMsdDigits ? S.hist[tid] : 0u;
   // the tile's slot in each bucket: the L2 atomic's round trip overlaps the
   // scan and the staging below (its result is used only after them)
   uint32_t toff = 0;
-  if (tid < kRadix && c) toff = atomicAdd(cnt + tid, c);
+  if (tid < kMsdDigits && c) toff = atomicAdd(cnt + tid, c);
   uint32_t tot;
   const uint32_t ts = block_exclusive_scan<kMsdThreads, uint32_t>(c, S.scan, &tot);
-  if (tid < kRadix) S.tstart[tid] = ts;
+  if (tid < kMsdDigits) S.tstart[tid] = ts;
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const uint32_t off = wbase + i * 32 + lane;
     if (off < tile_n) {
-      const uint32_t p = S.tstart[k[i] >> 24] + rk[i];
+      const uint32_t p = S.tstart[k[i] >> kMsdShift] + rk[i];
       S.keys[p] = k[i];
       S.pos[p] = (uint32_t)(tile_base + off);
       S.vals[p] = v[i];
@@ -814,14 +826,14 @@ __global__ void __launch_bounds__(kMsdThreads, MSD_MINB) msd_scatter_kernel(
   // for another. Records past the region's end are dropped: that bucket is
   // oversized, and the bucket pass regathers it from the raw batch.
   MSDP(3);
-  if (tid < kRadix) S.gdst[tid] = tid * region_cap + toff - ts;
+  if (tid < kMsdDigits) S.gdst[tid] = tid * region_cap + toff - ts;
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const uint32_t idx = i * kMsdThreads + tid;
     if (idx < tile_n) {
       const uint32_t key = S.keys[idx];
-      const uint32_t d = key >> 24;
+      const uint32_t d = key >> kMsdShift;
       const uint32_t g = S.gdst[d] + idx;
       if (g < (d + 1) * region_cap) {
         out_keys[g] = key;
@@ -860,7 +872,7 @@ __global__ void __launch_bounds__(kMsdThreads, 1) msd2_scatter_kernel(
   const uint32_t tile_n = min((uint32_t)kMsdTile, nA - tile_base);
   const uint64_t rbase = (uint64_t)d1 * capA + tile_base;
   const uint32_t wbase = warp * (32 * kSortItems);
-  const uint32_t shift = 24 - w;
+  const uint32_t shift = kMsdShift - w;
   uint32_t k[kSortItems], pz[kSortItems], v[kSortItems], rk[kSortItems];
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
@@ -911,11 +923,10 @@ __global__ void __launch_bounds__(kMsdThreads, 1) msd2_scatter_kernel(
 }
 
 #ifndef SORT_BIN_BITS
-#define SORT_BIN_BITS 11
+#define SORT_BIN_BITS (MSD_BITS == 9 ? 10 : 11)
 #endif
 constexpr int kBinBits = SORT_BIN_BITS;
 constexpr int kBins = 1 << kBinBits;
-constexpr int kBinShift = 24 - kBinBits;  // bins = key bits [24 - kBinBits, 24)
 // bin counts and starts are 16-bit halves of 32-bit words (a bucket holds at
 // most kBktCap < 2^16 records), so 4096 bins fit where 2048 words would
 static_assert(kBktCap < 65536 && (kBins / kBktThreads) % 2 == 0, "16-bit bin halves");
@@ -956,7 +967,7 @@ struct RankSmem {
   uint32_t start_d, size_d;
 };
 
-__global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
+__global__ void __launch_bounds__(kBktThreads, kBktCtasPerSm) bucket_rank_kernel(
     BucketGeo G, uint32_t* __restrict__ ak, uint32_t* __restrict__ ap,
     const uint32_t* __restrict__ av, RawBatch in, uint64_t b, uint32_t* __restrict__ tk,
     uint32_t* __restrict__ tv,
@@ -981,7 +992,7 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
   const uint32_t w = G.w;
   const uint32_t d1 = d >> w, d2 = d & ((1u << w) - 1u);
   // sub-bucket bits below the top digit and the bin field under them
-  const int bin_shift = 24 - (int)w - kBinBits;
+  const int bin_shift = kMsdShift - (int)w - kBinBits;
   ak += (uint64_t)d * G.capB;
   ap += (uint64_t)d * G.capB;
   av += (uint64_t)d * G.capB;
@@ -994,12 +1005,24 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
   }
   {  // output start = records in the top digits below d1 (+ the sub-buckets
      // of d1 below d2)
-    const uint32_t c = tid < kRadix ? __ldg(G.cntA + tid) : 0u;
+    // kMsdDigits counts over kBktThreads threads: kDpt consecutive per thread
+    constexpr int kDpt = kMsdDigits / kBktThreads > 0 ? kMsdDigits / kBktThreads : 1;
+    uint32_t cs[kDpt], csum = 0;
+#pragma unroll
+    for (int q = 0; q < kDpt; ++q) {
+      const int dd = tid * kDpt + q;
+      cs[q] = dd < kMsdDigits ? __ldg(G.cntA + dd) : 0u;
+      csum += cs[q];
+    }
     uint32_t tot;
-    const uint32_t ex = block_exclusive_scan<kBktThreads, uint32_t>(c, S.scan, &tot);
-    if (tid == (int)d1) {
-      S.start_d = ex;
-      S.size_d = c;
+    uint32_t ex = block_exclusive_scan<kBktThreads, uint32_t>(csum, S.scan, &tot);
+#pragma unroll
+    for (int q = 0; q < kDpt; ++q) {
+      if (tid * kDpt + q == (int)d1) {
+        S.start_d = ex;
+        S.size_d = cs[q];
+      }
+      ex += cs[q];
     }
     __syncthreads();
     if (G.cntB != nullptr) {
@@ -1022,7 +1045,7 @@ __global__ void __launch_bounds__(kBktThreads, 2) bucket_rank_kernel(
   // over capacity: the whole top digit (one level, or its region overflowed)
   // or this sub-bucket is regathered from the raw batch
   const bool whole_digit = G.cntB == nullptr || __ldg(G.cntA + d1) > G.capA;
-  const uint32_t sel_shift = whole_digit ? 24u : 24u - w;
+  const uint32_t sel_shift = whole_digit ? (uint32_t)kMsdShift : (uint32_t)kMsdShift - w;
   const uint32_t sel_val = whole_digit ? d1 : d;
   if (size > (uint32_t)kBktCap || (!whole_digit && size > G.capB)) {
     // oversized bucket (skewed keys): its region holds only the first
@@ -1306,11 +1329,13 @@ static cudaError_t sort_attrs() {
 constexpr uint64_t kTwoLevelMaxB = 1ull << 27;
 static uint32_t sort2_w(uint64_t b) {
   uint32_t w = 1;
-  while (w < 8 && ((uint64_t)kRadix << (w + 12)) < b) ++w;
+  // sub-buckets of at most ~kBktThreads * 8 records on average
+  constexpr int kTargetBits = kBktThreads == 256 ? 11 : 12;
+  while (w < 8 && ((uint64_t)kMsdDigits << (w + kTargetBits)) < b) ++w;
   return w;
 }
 static uint32_t sort2_capA(uint64_t b) {
-  const double m = (double)b / kRadix;
+  const double m = (double)b / kMsdDigits;
   const uint64_t c = (uint64_t)(m + 8.0 * std::sqrt(m)) + 1024;
   return (uint32_t)((c + 3) & ~3ull);
 }
@@ -1320,10 +1345,10 @@ static uint32_t sort2_capA(uint64_t b) {
 // two-level mode into 256 regions of capA and (256 << w) of kBktCap
 uint64_t sort_tmp_words(uint64_t b) {
   if (b <= (uint64_t)kSmallCap) return b;
-  uint64_t w = std::max<uint64_t>(b, (uint64_t)kRadix * kBktCap);
+  uint64_t w = std::max<uint64_t>(b, (uint64_t)kMsdDigits * kBktCap);
   if (b <= kTwoLevelMaxB) {
-    w = std::max<uint64_t>(w, (uint64_t)kRadix * sort2_capA(b));
-    w = std::max<uint64_t>(w, ((uint64_t)kRadix << sort2_w(b)) * kBktCap);
+    w = std::max<uint64_t>(w, (uint64_t)kMsdDigits * sort2_capA(b));
+    w = std::max<uint64_t>(w, ((uint64_t)kMsdDigits << sort2_w(b)) * kBktCap);
   }
   return w;
 }
@@ -1366,8 +1391,8 @@ cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals
   // (2) MSD + rank: the scatter puts every record into its top-digit bucket,
   //     the bucket pass sorts each bucket in shared memory (one CTA each)
   if (!use_ctr && !S.lsd_only) {
-    uint32_t* cnt = S.msd_cnt + (S.msd_parity ? kRadix : 0);
-    uint32_t* cnt_next = S.msd_cnt + (S.msd_parity ? 0 : kRadix);
+    uint32_t* cnt = S.msd_cnt + (S.msd_parity ? kMsdCntWords : 0);
+    uint32_t* cnt_next = S.msd_cnt + (S.msd_parity ? 0 : kMsdCntWords);
     S.msd_parity ^= 1;
     hk.begin(hk.ctx, LSM_K_SORT_PASS, s);
     e = launch_pdl(msd_scatter_kernel, (unsigned)((b + kMsdTile - 1) / kMsdTile), kMsdThreads,
@@ -1379,7 +1404,7 @@ cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals
     if (e != cudaSuccess) return e;
     hk.begin(hk.ctx, LSM_K_SORT_PASS, s);
     const BucketGeo G{cnt, nullptr, 0u, (uint32_t)kBktCap, (uint32_t)kBktCap, 21u};
-    e = launch_pdl(bucket_rank_kernel, (unsigned)kRadix, kBktThreads, sizeof(RankSmem), s, G,
+    e = launch_pdl(bucket_rank_kernel, (unsigned)kMsdDigits, kBktThreads, sizeof(RankSmem), s, G,
                    S.tmp_keys[0], S.tmp_vals[0], (const uint32_t*)S.tmp_v3,
                    in, b, S.tmp_keys[1],
                    S.tmp_vals[1], out_keys, out_vals, out_f1, S.overflow_dev);
@@ -1393,17 +1418,17 @@ cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals
   //      sub-bucket
   if (b <= kTwoLevelMaxB && !S.lsd_only && S.tmp_v4 != nullptr && S.msd_cntB != nullptr) {
     const uint32_t w = sort2_w(b), capA = sort2_capA(b);
-    uint32_t* cnt = S.msd_cnt + (S.msd_parity ? kRadix : 0);
-    uint32_t* cnt_next = S.msd_cnt + (S.msd_parity ? 0 : kRadix);
+    uint32_t* cnt = S.msd_cnt + (S.msd_parity ? kMsdCntWords : 0);
+    uint32_t* cnt_next = S.msd_cnt + (S.msd_parity ? 0 : kMsdCntWords);
     S.msd_parity ^= 1;
     hk.begin(hk.ctx, LSM_K_SORT_PASS, s);
     e = launch_pdl(msd_scatter_kernel, (unsigned)((b + kMsdTile - 1) / kMsdTile), kMsdThreads,
                    sizeof(MsdSmem), s, in, b, S.tmp_keys[0], S.tmp_vals[0], S.tmp_v3, cnt,
-                   cnt_next, S.err, capA, S.msd_cntB, (uint32_t)kRadix << w);
+                   cnt_next, S.err, capA, S.msd_cntB, (uint32_t)kMsdDigits << w);
     hk.end(hk.ctx, LSM_K_SORT_PASS, (double)b * 21.0, s, 1);
     if (e != cudaSuccess) return e;
     hk.begin(hk.ctx, LSM_K_SORT_PASS, s);
-    e = launch_pdl(msd2_scatter_kernel, dim3((capA + kMsdTile - 1) / kMsdTile, kRadix),
+    e = launch_pdl(msd2_scatter_kernel, dim3((capA + kMsdTile - 1) / kMsdTile, kMsdDigits),
                    kMsdThreads, sizeof(MsdSmem), s, (const uint32_t*)S.tmp_keys[0],
                    (const uint32_t*)S.tmp_vals[0], (const uint32_t*)S.tmp_v3,
                    (const uint32_t*)cnt, capA, w, S.tmp_keys[1], S.tmp_vals[1], S.tmp_v4,
@@ -1413,7 +1438,7 @@ cudaError_t launch_sort_batch(const uint32_t* raw_keys, const uint32_t* raw_vals
     if (e != cudaSuccess) return e;
     hk.begin(hk.ctx, LSM_K_SORT_PASS, s);
     const BucketGeo G{cnt, S.msd_cntB, w, capA, (uint32_t)kBktCap, 27u};
-    e = launch_pdl(bucket_rank_kernel, (unsigned)(kRadix << w), kBktThreads, sizeof(RankSmem), s,
+    e = launch_pdl(bucket_rank_kernel, (unsigned)(kMsdDigits << w), kBktThreads, sizeof(RankSmem), s,
                    G, S.tmp_keys[1], S.tmp_vals[1], (const uint32_t*)S.tmp_v4, in, b,
                    S.tmp_keys[0], S.tmp_vals[0], out_keys, out_vals, out_f1, S.overflow_dev);
     hk.end(hk.ctx, LSM_K_SORT_PASS, (double)b * 20.0, s, 1);

@@ -41,7 +41,7 @@ int main(int argc, char** argv) {
   SortScratch S{};
   S.hist = meta; S.bases = meta + 2 * kPasses * kRadix; S.tile_ctr = meta + 3 * kPasses * kRadix;
   S.err = S.tile_ctr + 4; S.done_ctr = S.tile_ctr + 5;
-  S.bkt = meta + 3 * kPasses * kRadix + 16; S.msd_cnt = S.bkt + 2 * kRadix; S.msd_bar = S.msd_cnt + 2 * kRadix;
+  S.bkt = meta + 3 * kPasses * kRadix + 16; S.msd_cnt = S.bkt + 2 * kRadix; S.msd_bar = S.msd_cnt + 2 * kMsdCntWords;
   S.status = meta + kSortMetaHead; S.tiles_cap = sort_tiles(b);
   uint32_t* hp; cudaHostAlloc((void**)&hp, 64, cudaHostAllocMapped); *hp = 0;
   cudaHostGetDevicePointer((void**)&S.overflow_dev, hp, 0); S.overflow_host = hp;
@@ -77,7 +77,7 @@ int main(int argc, char** argv) {
   const char* bn[7] = {"bkt entry", "bkt loaded+binned", "bkt bins scanned", "bkt grouped", "bkt ranked", "bkt values gathered", "bkt written"};
   for (int ph = 0; ph < 7; ++ph) {
     std::vector<double> x;
-    for (int c = 0; c < 256; ++c) { unsigned long long s = P[5ull * 4096 * 8 + c * 8 + ph]; if (s) x.push_back((double)(s - t0) / 1e3); }
+    for (int c = 0; c < 4096; ++c) { unsigned long long s = P[5ull * 4096 * 8 + c * 8 + ph]; if (s) x.push_back((double)(s - t0) / 1e3); }
     dist(bn[ph], x);
   }
   printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
