@@ -53,6 +53,11 @@ constexpr int kMergeTile = kConsumers * kMergeItems;  // 3840
 #ifndef MERGE_CTAS
 #define MERGE_CTAS 3
 #endif
+// merges of up to MERGE_SINGLE_WAVES waves of tiles run the one-tile-per-CTA
+// variant (no persistent ring to fill)
+#ifndef MERGE_SINGLE_WAVES
+#define MERGE_SINGLE_WAVES 1
+#endif
 constexpr int kStages = MERGE_STAGES;
 constexpr int kMergeCtasPerSm = MERGE_CTAS;
 constexpr int kBufElems = kMergeTile + 16;  // A + B windows incl. alignment slack
@@ -436,7 +441,7 @@ cudaError_t launch_merge(const uint32_t* ak, const uint32_t* av, uint64_t na,
   const uint64_t ntiles = (total + kMergeTile - 1) / kMergeTile;
   hk.begin(hk.ctx, LSM_K_MERGE, s);
   cudaError_t e;
-  if (ntiles <= g_single_cap) {
+  if (ntiles <= g_single_cap * (uint64_t)MERGE_SINGLE_WAVES) {
     // small merge: one tile per CTA, all resident at once
     e = launch_pdl(merge_kernel_t<1>, (unsigned)ntiles, kMergeThreads, sizeof(MergeSmemT<1>), s,
                    ak, av, na, bk, bv, nb, ok, ov, ntiles, out_f1);
