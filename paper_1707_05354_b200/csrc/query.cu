@@ -612,10 +612,93 @@ __device__ __forceinline__ uint32_t walk_window(const LevelTable& T, uint64_t* p
   return cnt;
 }
 
+// The same result record by record, branch-light, for 2..8 levels whose
+// lengths fit 32 bits (walk_levels checks): per level the raw key variable of
+// the head and of the next record (loaded one step ahead) and a 32-bit
+// index. A step takes the smallest head key m, reads the status of the newest
+// level holding m (the run head of m there) if m is
+// a new key, and advances every level whose head has key m by ONE record;
+// the rest of a level's run of m comes up in later steps as the same key and
+// is skipped by the m != prev test. Heads past the slice (key > z), past the
+// level, or placebos (key 2^31-1, tombstones below every user key, R5) hold
+// kSentRaw = 0xFFFFFFFF, above every stored key variable. (ncu, C4 at 7 levels
+// and L = 1024: the per-key walk above spent ~270 instructions per step.)
+template <int NL, bool NEED_VAL, typename Emit>
+__device__ __forceinline__ uint32_t walk_flat(const LevelTable& T, const uint64_t* pos, uint32_t z,
+                                              Emit emit) {
+  constexpr uint32_t kSentRaw = 0xFFFFFFFFu;
+  // a stored key variable v is in the slice iff v <= zlim (and v < placebo)
+  const uint32_t zlim = z >= 0x7FFFFFFFu ? 0xFFFFFFFDu : 2u * z + 1u;
+  uint32_t h[NL], nx[NL], p[NL];
+  auto ld = [&](int j, uint32_t q) -> uint32_t {
+    const uint32_t v = q < (uint32_t)T.n[j] ? __ldg(T.keys[j] + q) : kSentRaw;
+    return v <= zlim ? v : kSentRaw;
+  };
+#pragma unroll
+  for (int j = 0; j < NL; ++j) {
+    p[j] = (uint32_t)pos[j];
+    h[j] = ld(j, p[j]);
+    nx[j] = ld(j, p[j] + 1);
+  }
+  uint32_t cnt = 0, prev = 0xFFFFFFFFu;
+  bool pend = false;
+  uint32_t pk = 0, pv = 0;
+  while (true) {
+    uint32_t mk = h[0];
+#pragma unroll
+    for (int j = 1; j < NL; ++j) mk = min(mk, h[j]);
+    if (mk == kSentRaw) break;
+    const uint32_t m = mk >> 1;
+    // newest level holding m: the lowest j with h[j] >> 1 == m
+    uint32_t st = 0, vj = 0, vp = 0;
+#pragma unroll
+    for (int j = NL - 1; j >= 0; --j)
+      if ((h[j] >> 1) == m) {
+        st = h[j];
+        vj = (uint32_t)j;
+        vp = p[j];
+      }
+    const bool valid = (st & 1u) && m != prev;
+    prev = m;
+    if (NEED_VAL && valid) {
+      const uint32_t* V = T.vals[0];
+#pragma unroll
+      for (int j = 1; j < NL; ++j)
+        if (vj == (uint32_t)j) V = T.vals[j];
+      const uint32_t val = ldg_pol(V + vp, l2_policy_stream());
+      if (pend) emit(cnt - 1, pk, pv);
+      pend = true;
+      pk = m;
+      pv = val;
+    }
+    cnt += valid;
+#pragma unroll
+    for (int j = 0; j < NL; ++j)
+      if ((h[j] >> 1) == m) {
+        h[j] = nx[j];
+        ++p[j];
+        nx[j] = nx[j] == kSentRaw ? kSentRaw : ld(j, p[j] + 1);
+      }
+  }
+  if (NEED_VAL && pend) emit(cnt - 1, pk, pv);
+  return cnt;
+}
+
+// every level's length fits the 32-bit indices of walk_flat
+__device__ __forceinline__ bool flat_ok(const LevelTable& T, int L) {
+  bool ok = true;
+  for (int j = 0; j < L; ++j) ok &= T.n[j] < 0xFFFFFFFFull;
+  return ok;
+}
+
 // dispatch: the windowed walk for 2..4 levels, the plain walk otherwise
 template <int NL, bool NEED_VAL, typename Emit>
 __device__ __forceinline__ uint32_t walk_levels(const LevelTable& T, uint64_t* pos, uint32_t z,
                                                 int L, Emit emit) {
+#if !defined(GPULSM_WALK_OLD)
+  if constexpr (NL >= 2 && NL <= 8)
+    if (flat_ok(T, NL)) return walk_flat<NL, NEED_VAL>(T, pos, z, emit);
+#endif
 #if !defined(GPULSM_NO_WINDOW)
   if constexpr (NL >= 2 && NL <= 4) return walk_window<NL, NEED_VAL>(T, pos, z, emit);
 #endif

@@ -237,6 +237,36 @@ def test_long_ranges_single_level(alphabet):
         assert_queries_equal(g, o1, q, k1, k2, f"long ranges L={L}")
 
 
+@pytest.mark.parametrize("r", [3, 6, 15, 27, 63, 127, 255, 511])
+@pytest.mark.parametrize("alphabet", [None, 30_000])
+def test_long_ranges_multi_level(r, alphabet):
+    # 2..9 occupied levels and ranges of ~100..10^4 resident records: a lane's
+    # walk stops after its key cap and the warp finishes the query in rounds
+    # over shared memory (warp_merge_long) -- chunks cut at a common key,
+    # validity against newer levels, slots from per-level valid ranks; the
+    # duplicate-heavy alphabet gives stale runs longer than a chunk (the
+    # one-step fallback) and tombstones; a partial last batch puts a placebo
+    # run into the slices of ranges ending at 2^32-1 (R5, R8). r = 511 takes
+    # the >8-level kernels.
+    b = 1024
+    g = GpuAdapter(b)
+    o1 = oracle.OracleDict(b)
+    seed = 71 + r
+    for j in range(r):
+        n = b if j + 1 < r else b - 77
+        k, v, d = synth.updates(seed, j * b, n, delete_frac4=1, alphabet=alphabet)
+        g.update(k, v, d)
+        o1.apply_batch(k, v, d)
+    assert g.r == r
+    dom = synth.D if alphabet is None else alphabet + 2
+    for L in (100, 1000, 10_000):
+        k1, k2 = synth.range_queries(seed + L, 300 if L < 10_000 else 60, r * b, L, domain=dom)
+        k2[::7] = 0xFFFFFFFF  # to the top of the 32-bit query space
+        k1[::11] = 0
+        q = synth.lookup_queries(seed, 1000, r * b, alphabet)
+        assert_queries_equal(g, o1, q, k1, k2, f"r={r} long ranges L={L}")
+
+
 def test_one_wave_boundary_sort():
     # exactly 148 tiles (largest one-wave batch) and one record more
     for b in (148 * 7168, 148 * 7168 + 1):
