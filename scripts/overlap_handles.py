@@ -36,6 +36,8 @@ def run(handles, streams):
         sl = slice(j * b, (j + 1) * b)
         for h, s in zip(handles, streams):
             h.update(K[sl], V[sl], D[sl], stream=s)
+    for h, s in zip(handles, streams):
+        h.sync(stream=s)  # joins the handle's merge stream (host wait)
     ej = torch.cuda.Event()
     ej.record(s2)
     s1.wait_event(ej)
