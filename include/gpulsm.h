@@ -16,14 +16,6 @@
  *  - The handle owns the level storage and all scratch. It is bound to the
  *    device current at lsm_create; every call switches to that device and
  *    restores the caller's current device before returning.
- *  - Updates (lsm_update and its variants) read their inputs on `stream` (the
- *    sort) and run the merge cascade on the handle's internal merge stream,
- *    after that sort, so the sort of the next batch overlaps the merges of
- *    this one. Every other call that reads or rewrites the levels (queries,
- *    cleanup, clear, reserve, bulk_build, update_batches, sync) first makes
- *    its `stream` wait for the cascades enqueued so far; lsm_level_view
- *    waits for them on the host. The inputs of an update may be reused once
- *    `stream` has passed the call.
  *  - Mutations (insert/delete/update/bulk_build/update_batches/cleanup/clear)
  *    need exclusive access ("updates and queries are performed in separate
  *    phases"): the caller orders them against every query
@@ -149,10 +141,9 @@ lsm_status lsm_clear(lsm_t* h, void* stream);
  * scatter by the top 8 bits (key, input position and value carried) plus
  * a shared-memory rank of each bucket by (key variable, input position);
  * above that (or after a skewed key set)
- * a 4-pass onesweep LSD -- into a ring of three sorted-batch buffers (level 0
- * itself when r is even) -- then, on the merge stream, the binary-counter
- * cascade of stable merges on key>>1, batch first on ties (PAPER.md:621-622,
- * R1), writing level ffz(r).
+ * a 4-pass onesweep LSD -- then the binary-counter cascade of stable merges
+ * on key>>1, batch first on ties (R1), writing level
+ * ffz(r).
  * Errors: LSM_ERR_BATCH_SIZE, LSM_ERR_INVALID_ARG, LSM_ERR_OOM,
  * LSM_ERR_CUDA; out-of-domain keys set the sticky LSM_ERR_KEY_DOMAIN.      */
 lsm_status lsm_update(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals,
@@ -381,9 +372,7 @@ lsm_status lsm_num_batches(const lsm_t* h, uint64_t* r_out);
  * still occupied (they form one sorted array). */
 lsm_status lsm_query_levels(lsm_t* h, uint32_t* n_out);
 /* Device view of level i: key variables ((k<<1)|status) and values, n =
- * b*2^i if full else 0 (pointers NULL). Valid until the next mutation.
- * Waits on the host for the cascades enqueued so far (the sort of a batch
- * that became level 0 is ordered on the update's stream).                  */
+ * b*2^i if full else 0 (pointers NULL). Valid until the next mutation.     */
 lsm_status lsm_level_view(const lsm_t* h, uint32_t i, const uint32_t** d_keys,
                           const uint32_t** d_vals, uint64_t* n);
 /* Synchronise `stream` and return (then clear) the sticky device error

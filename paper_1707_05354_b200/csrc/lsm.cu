@@ -61,24 +61,7 @@ struct lsm {
   Buffer home[LSM_MAX_LEVELS];
   uint32_t* home_idx[LSM_MAX_LEVELS] = {};  // index storage of each home level
   Buffer ping[2];         // merge ping-pong scratch
-  Buffer sortout;         // sorted batch of the GPU SA mode
-  // Sorted batches (overlapped update): a ring of three
-  // buffers on the caller's stream; batch j's sorted output is either the
-  // first merge input of its cascade (t >= 1) or level 0 (t = 0, with its F1
-  // index in ring_idx). The cascades run on the handle's merge stream, so the
-  // sort of batch j+1 overlaps the merges of batch j; a ring buffer is reused
-  // by the sort three batches later once the merge that read it has finished
-  // (ring_ev).
-  Buffer ring[3];
-  uint32_t* ring_idx[3] = {};
-  cudaEvent_t ring_ev[3] = {};
-  bool ring_wait[3] = {};
-  int ring_cur = 0;
-  int level0_ring = -1;                 // ring slot holding level 0, or -1
-  cudaStream_t mst = nullptr;           // merge stream (cascades)
-  cudaEvent_t m_done = nullptr;         // recorded after the last cascade
-  cudaEvent_t m_sorted = nullptr;       // the sort a cascade waits for
-  bool m_used = false;
+  Buffer sortout;         // sorted batch when t >= 1
   SortScratch sort{};
   uint32_t* sort_meta = nullptr;
   uint64_t sort_meta_words = 0;
@@ -533,31 +516,6 @@ lsm_status take_sticky(lsm* h, cudaStream_t s) {
   return LSM_ERR_KEY_DOMAIN;
 }
 
-// Order stream s after every cascade enqueued on the merge stream (all
-// calls that read or rewrite the levels do this first).
-cudaError_t join_merges(lsm* h, cudaStream_t s) {
-  if (!h->m_used) return cudaSuccess;
-  return cudaStreamWaitEvent(s, h->m_done, 0);
-}
-
-cudaError_t ensure_merge_stream(lsm* h) {
-  if (h->mst) return cudaSuccess;
-  cudaError_t e = cudaStreamCreateWithFlags(&h->mst, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->m_done, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->m_sorted, cudaEventDisableTiming);
-  for (int k = 0; k < 3 && e == cudaSuccess; ++k)
-    e = cudaEventCreateWithFlags(&h->ring_ev[k], cudaEventDisableTiming);
-  return e;
-}
-
-// ring slot k: a sorted batch of b records + room for its fence-key index
-cudaError_t ring_ensure(lsm* h, int k, cudaStream_t s) {
-  cudaError_t e = buf_ensure(h, h->ring[k], h->b, s);
-  if (e == cudaSuccess && h->ring_idx[k] == nullptr)
-    e = pool_alloc(h, (void**)&h->ring_idx[k], idx_words(h->b) * 4, s);
-  return e;
-}
-
 }  // namespace
 
 extern "C" {
@@ -628,10 +586,6 @@ lsm_status lsm_destroy(lsm_t* h) {
   buf_free(h, h->ping[0], nullptr);
   buf_free(h, h->ping[1], nullptr);
   buf_free(h, h->sortout, nullptr);
-  for (int k = 0; k < 3; ++k) {
-    buf_free(h, h->ring[k], nullptr);
-    if (h->ring_idx[k]) pool_free(h, h->ring_idx[k], nullptr);
-  }
   if (h->sort_meta) pool_free(h, h->sort_meta, nullptr);
   for (int k = 0; k < 2; ++k) {
     if (h->sort.tmp_keys[k]) pool_free(h, h->sort.tmp_keys[k], nullptr);
@@ -662,11 +616,6 @@ lsm_status lsm_destroy(lsm_t* h) {
     if (h->st_free[k]) cudaEventDestroy(h->st_free[k]);
   }
   if (h->st_stream) cudaStreamDestroy(h->st_stream);
-  for (int k = 0; k < 3; ++k)
-    if (h->ring_ev[k]) cudaEventDestroy(h->ring_ev[k]);
-  if (h->m_done) cudaEventDestroy(h->m_done);
-  if (h->m_sorted) cudaEventDestroy(h->m_sorted);
-  if (h->mst) cudaStreamDestroy(h->mst);
   if (h->h_pinned) cudaFreeHost(h->h_pinned);
   if (h->sort.overflow_host) cudaFreeHost((void*)h->sort.overflow_host);
   if (h->idx_ev) cudaEventDestroy(h->idx_ev);
@@ -683,7 +632,6 @@ lsm_status lsm_reserve(lsm_t* h, uint64_t max_batches, void* stream) {
   if (!h) return LSM_ERR_INVALID_ARG;
   ENTER(h);
   cudaStream_t s = S(stream);
-  CK(join_merges(h, s));
   CK(ensure_sort_scratch(h, s));
   if (h->sa) {
     CK(sa_buf_ensure(h, h->sa_buf[0], max_batches * h->b, s));
@@ -697,7 +645,7 @@ lsm_status lsm_reserve(lsm_t* h, uint64_t max_batches, void* stream) {
     CK(buf_ensure(h, h->home[i], h->b << i, s));
     CK(home_idx_ensure(h, i, s));
   }
-  for (int k = 0; k < 3; ++k) CK(ring_ensure(h, k, s));
+  CK(buf_ensure(h, h->sortout, h->b, s));
   if (top >= 1) {
     CK(buf_ensure(h, h->ping[0], h->b << (top - 1), s));
     CK(buf_ensure(h, h->ping[1], h->b << (top - 1), s));
@@ -712,12 +660,10 @@ lsm_status lsm_clear(lsm_t* h, void* stream) {
     h->r = 0;
     return LSM_OK;
   }
-  CK(join_merges(h, S(stream)));
   cv_drop(h, S(stream));
   for (int i = 0; i < LSM_MAX_LEVELS; ++i)
     if ((h->r >> i) & 1ull) level_release(h, i, S(stream));
   h->r = 0;
-  h->level0_ring = -1;
   return LSM_OK;
 }
 
@@ -728,6 +674,7 @@ static lsm_status prepare_insert(lsm_t* h, int t, cudaStream_t s) {
   const uint64_t b = h->b;
   CK(buf_ensure(h, h->home[t], b << t, s));
   CK(home_idx_ensure(h, t, s));
+  if (t > 0) CK(buf_ensure(h, h->sortout, b, s));
   if (t >= 2) {
     CK(buf_ensure(h, h->ping[0], b << (t - 1), s));
     CK(buf_ensure(h, h->ping[1], b << (t - 1), s));
@@ -747,11 +694,6 @@ static lsm_status cascade(lsm_t* h, const uint32_t* ck, const uint32_t* cv, int 
     const uint64_t ni = b << i;
     CK(launch_merge(ck, cv, ni, h->level[i].keys, h->level[i].vals, ni, ok, ov,
                     i == t - 1 ? h->home_idx[t] : nullptr, s, hk));
-    if (i == 0 && h->level0_ring >= 0) {  // the ring slot of level 0 is free again
-      CK(cudaEventRecord(h->ring_ev[h->level0_ring], s));
-      h->ring_wait[h->level0_ring] = true;
-      h->level0_ring = -1;
-    }
     level_release(h, i, s);  // level i <- empty
     ck = ok;
     cv = ov;
@@ -849,45 +791,16 @@ static lsm_status do_update(lsm_t* h, const uint32_t* keys, const uint32_t* vals
   if (t >= LSM_MAX_LEVELS) return LSM_ERR_INVALID_ARG;
   LaunchHooks hk = hooks(h);
   CK(ensure_sort_scratch(h, s));
-  CK(ensure_merge_stream(h));
   lsm_status st = prepare_insert(h, t, s);
   if (st != LSM_OK) return st;
-  // sort (A1+A2) on the caller's stream into the next ring slot (with its F1
-  // when it becomes level 0); the slot's previous batch has been merged
-  const int k = h->ring_cur;
-  h->ring_cur = (k + 1) % 3;
-  CK(ring_ensure(h, k, s));
-  if (h->ring_wait[k]) {
-    CK(cudaStreamWaitEvent(s, h->ring_ev[k], 0));
-    h->ring_wait[k] = false;
-  }
-  Buffer& R = h->ring[k];
-  CK(launch_sort_batch(keys, vals, ops, mode, n, b, h->sort, R.keys, R.vals,
-                       t == 0 ? h->ring_idx[k] : nullptr, s, hk));
-  if (t == 0) {  // level 0 <- the sorted batch
-    Level& L0 = h->level[0];
-    L0.keys = R.keys;
-    L0.vals = R.vals;
-    L0.owner = nullptr;
-    L0.idx = h->ring_idx[k];
-    L0.idx_owned = false;
-    L0.idx_ready = false;
-    h->level0_ring = k;
-    h->r += 1;
-  } else {
-    // cascade (A3) on the merge stream, after this sort; the batch's slot is
-    // free once the first merge has read it
-    cudaStream_t m = h->mst;
-    CK(cudaEventRecord(h->m_sorted, s));
-    CK(cudaStreamWaitEvent(m, h->m_sorted, 0));
-    st = cascade(h, R.keys, R.vals, t, m, hk);
-    if (st != LSM_OK) return st;
-    CK(cudaEventRecord(h->ring_ev[k], m));
-    h->ring_wait[k] = true;
-    commit_insert(h, t);
-    CK(cudaEventRecord(h->m_done, m));
-    h->m_used = true;
-  }
+  // sort (A1+A2): straight into level 0 (with its F1) when t == 0
+  uint32_t* sk = (t == 0) ? h->home[0].keys : h->sortout.keys;
+  uint32_t* sv = (t == 0) ? h->home[0].vals : h->sortout.vals;
+  CK(launch_sort_batch(keys, vals, ops, mode, n, b, h->sort, sk, sv,
+                       t == 0 ? h->home_idx[0] : nullptr, s, hk));
+  st = cascade(h, sk, sv, t, s, hk);
+  if (st != LSM_OK) return st;
+  commit_insert(h, t);
   if (h->cv_owner && !cv_valid(h)) cv_drop(h, s);  // a view was merged away
   return LSM_OK;
 }
@@ -927,7 +840,6 @@ lsm_status lsm_bulk_build(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_va
   const uint64_t k = (n + b - 1) / b;
   if (k >= (1ull << LSM_MAX_LEVELS) || k * b > (1ull << 32)) return LSM_ERR_INVALID_ARG;
   cudaStream_t s = S(stream);
-  CK(join_merges(h, s));
   LaunchHooks hk = hooks(h);
   const int mode = d_is_delete ? kModeMixed : kModeInsert;
   if (h->sa) {  // one sort straight into the array (with its F1)
@@ -988,7 +900,6 @@ lsm_status lsm_update_batches(lsm_t* h, const uint32_t* d_keys, const uint32_t* 
   const uint64_t k = (n + b - 1) / b;
   if (h->r + k >= (1ull << LSM_MAX_LEVELS)) return LSM_ERR_INVALID_ARG;
   cudaStream_t s = S(stream);
-  CK(join_merges(h, s));  // the cascades below run on s
   LaunchHooks hk = hooks(h);
   const int mode = d_is_delete ? kModeMixed : kModeInsert;
   CK(ensure_sort_scratch(h, s));
@@ -1007,7 +918,6 @@ lsm_status lsm_update_batches(lsm_t* h, const uint32_t* d_keys, const uint32_t* 
     const uint32_t* ck = h->stage.keys + j * b;
     const uint32_t* cv = h->stage.vals + j * b;
     if (t == 0) {  // level 0 <- the sorted batch, and its fence keys
-      h->level0_ring = -1;
       CK(cudaMemcpyAsync(h->home[0].keys, ck, b * 4, cudaMemcpyDeviceToDevice, s));
       CK(cudaMemcpyAsync(h->home[0].vals, cv, b * 4, cudaMemcpyDeviceToDevice, s));
       CK(launch_build_f1(h->home[0].keys, b, h->home_idx[0], s, hk));
@@ -1060,7 +970,6 @@ lsm_status lsm_lookup(lsm_t* h, const uint32_t* d_q, uint64_t nq, uint32_t* d_va
   ENTER(h);
   if (nq == 0) return LSM_OK;
   if (!d_q || !d_vals_out) return LSM_ERR_INVALID_ARG;
-  CK(join_merges(h, S(stream)));
   CK(ensure_index(h, S(stream), hooks(h)));
   LevelTable T = level_table(h);
   CK(launch_lookup(T, d_q, nq, d_vals_out, d_found_out, S(stream), hooks(h)));
@@ -1085,7 +994,6 @@ lsm_status lsm_lookup_host(lsm_t* h, const uint32_t* h_q, uint64_t nq, uint32_t*
     uint32_t* dv = reinterpret_cast<uint32_t*>(base + align_up(nq * 4, 256));
     uint8_t* df = base + 2 * align_up(nq * 4, 256);
     CK(cudaMemcpyAsync(dq, h_q, nq * 4, cudaMemcpyHostToDevice, s));
-    CK(join_merges(h, s));
     CK(ensure_index(h, s, hooks(h)));
     LevelTable T = level_table(h);
     CK(launch_lookup(T, dq, nq, dv, df, s, hooks(h)));
@@ -1104,7 +1012,6 @@ static lsm_status order_query(lsm_t* h, const uint32_t* d_q, uint64_t nq, bool s
   ENTER(h);
   if (nq == 0) return LSM_OK;
   if (!d_q || !d_keys_out || !d_vals_out) return LSM_ERR_INVALID_ARG;
-  CK(join_merges(h, S(stream)));
   CK(ensure_index(h, S(stream), hooks(h)));
   LevelTable T = level_table(h);
   CK(launch_order(T, d_q, nq, succ, d_keys_out, d_vals_out, d_found_out, S(stream), hooks(h)));
@@ -1127,7 +1034,6 @@ lsm_status lsm_count(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2, uint6
   ENTER(h);
   if (nq == 0) return LSM_OK;
   if (!d_k1 || !d_k2 || !d_counts_out) return LSM_ERR_INVALID_ARG;
-  CK(join_merges(h, S(stream)));
   CK(ensure_index(h, S(stream), hooks(h)));
   LevelTable T = level_table(h);
   CK(launch_count(T, d_k1, d_k2, nq, d_counts_out, S(stream), hooks(h), LSM_K_COUNT));
@@ -1148,7 +1054,6 @@ lsm_status lsm_range(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2, uint6
       CK(cudaMemsetAsync(d_offsets_out, 0, 8, s));
     } else {
       LaunchHooks hk = hooks(h);
-      CK(join_merges(h, s));
       CK(ensure_index(h, s, hk));
       LevelTable T = level_table(h);
       // per-call look-back scratch (stream-ordered pool), so concurrent
@@ -1191,7 +1096,6 @@ lsm_status lsm_cleanup(lsm_t* h, void* stream) {
   if (!h) return LSM_ERR_INVALID_ARG;
   ENTER(h);
   cudaStream_t s = S(stream);
-  CK(join_merges(h, s));
   LaunchHooks hk = hooks(h);
   const uint64_t b = h->b;
   std::vector<int> occ;
@@ -1257,7 +1161,6 @@ lsm_status lsm_cleanup(lsm_t* h, void* stream) {
   //    r' (R12), no copy
   cv_drop(h, s);
   for (int i : occ) level_release(h, i, s);
-  h->level0_ring = -1;  // a ring slot read by the merges above is free (stream order)
   uint64_t off = 0;
   int refs = 0;
   for (int i = 0; i < LSM_MAX_LEVELS; ++i) {
@@ -1431,8 +1334,6 @@ lsm_status lsm_level_view(const lsm_t* h, uint32_t i, const uint32_t** d_keys,
     *n = occ ? h->r * h->b : 0;
     return LSM_OK;
   }
-  // the pointers are final once the cascades enqueued so far have run
-  if (h->m_used && cudaEventSynchronize(h->m_done) != cudaSuccess) return LSM_ERR_CUDA;
   if ((h->r >> i) & 1ull) {
     *d_keys = h->level[i].keys;
     *d_vals = h->level[i].vals;
@@ -1449,7 +1350,6 @@ lsm_status lsm_sync(lsm_t* h, void* stream) {
   if (!h) return LSM_ERR_INVALID_ARG;
   ENTER(h);
   cudaStream_t s = S(stream);
-  CK(join_merges(h, s));
   CK(cudaStreamSynchronize(s));
   const lsm_status st = take_sticky(h, s);
   if (st != LSM_OK) return st;
