@@ -4,7 +4,10 @@
 // range: a global batch's slice on this rank is encoded and grouped by owner
 // (lsm_shard_bucket_records), the P counts are exchanged, and one call later
 // -- the counts are on the host by then -- the records go to their owners in
-// one grouped ncclSend/ncclRecv and are inserted with lsm_update_records.
+// one grouped ncclSend/ncclRecv and are inserted with lsm_update_records. The
+// rank's own chunk and count never cross the network (a device copy; at P = 1
+// the bucket kernel writes the count into mapped host memory and the grouped
+// records are inserted in place: no NCCL call, no copy).
 // Records arrive in source-rank order = global batch order, so the in-batch
 // rules (first insert wins, a delete wins) hold globally.
 // The same protocol as paper_1707_05354_b200/sharded.py's Python router
@@ -29,7 +32,9 @@ namespace {
 struct RouterBuf {
   uint32_t* rec = nullptr;  // [b_in][2] encoded records grouped by owner
   uint32_t* cnt = nullptr;  // [2P]: send counts | receive counts (device)
-  uint32_t* h_cnt = nullptr;  // pinned copy of cnt
+  uint32_t* h_cnt = nullptr;  // pinned copy of cnt (mapped: at P = 1 the bucket
+                              // kernel writes the count straight into it)
+  uint32_t* h_cnt_dev = nullptr;  // device alias of h_cnt
   cudaEvent_t ev = nullptr;
 };
 
@@ -128,25 +133,40 @@ lsm_status deliver(lsm_router* r, int k, cudaStream_t s) {
   RCK(cu(cudaEventSynchronize(B.ev)));
   double t1 = r->timing ? now_us() : 0.0;
   r->t_wait += t1 - t0;
-  const uint32_t P = r->P;
+  const uint32_t P = r->P, me = r->rank;
+  B.h_cnt[P + me] = B.h_cnt[me];  // the rank's own chunk never crosses the network
   std::vector<uint64_t> soff(P + 1, 0), roff(P + 1, 0);
   for (uint32_t p = 0; p < P; ++p) {
     soff[p + 1] = soff[p] + B.h_cnt[p];
     roff[p + 1] = roff[p] + B.h_cnt[P + p];
   }
   const uint64_t n = roff[P];
-  RCK(ensure_recv(r, n));
-  RCK(nc(ncclGroupStart()));
-  for (uint32_t p = 0; p < P; ++p) {
-    RCK(nc(ncclSend(B.rec + 2 * soff[p], 2 * (soff[p + 1] - soff[p]), ncclUint32, (int)p, r->comm, s)));
-    RCK(nc(ncclRecv(r->recv + 2 * roff[p], 2 * (roff[p + 1] - roff[p]), ncclUint32, (int)p, r->comm, s)));
+  const uint32_t* in = B.rec;  // P = 1: the grouped records are the local batch
+  if (P > 1) {
+    RCK(ensure_recv(r, n));
+    // chunks land in source-rank order (= global batch order); the own chunk
+    // by a device copy, the others in one NCCL group
+    RCK(nc(ncclGroupStart()));
+    for (uint32_t p = 0; p < P; ++p) {
+      if (p == me) continue;
+      RCK(nc(ncclSend(B.rec + 2 * soff[p], 2 * (soff[p + 1] - soff[p]), ncclUint32, (int)p, r->comm, s)));
+      RCK(nc(ncclRecv(r->recv + 2 * roff[p], 2 * (roff[p + 1] - roff[p]), ncclUint32, (int)p, r->comm, s)));
+    }
+    RCK(nc(ncclGroupEnd()));
+    if (soff[me + 1] > soff[me])
+      RCK(cu(cudaMemcpyAsync(r->recv + 2 * roff[me], B.rec + 2 * soff[me],
+                             8 * (soff[me + 1] - soff[me]), cudaMemcpyDeviceToDevice, s)));
+    in = r->recv;
   }
-  RCK(nc(ncclGroupEnd()));
   double t2 = r->timing ? now_us() : 0.0;
   r->t_xchg += t2 - t1;
   ++r->batches;
   if (n == 0) return LSM_OK;
-  lsm_status st = n <= r->b_local ? lsm_update_records(r->local, r->recv, n, s) : insert_split(r, n, s);
+  if (n > r->b_local && in != r->recv) {  // the oversize split works in the receive buffer
+    RCK(ensure_recv(r, n));
+    RCK(cu(cudaMemcpyAsync(r->recv, in, 8 * n, cudaMemcpyDeviceToDevice, s)));
+  }
+  lsm_status st = n <= r->b_local ? lsm_update_records(r->local, in, n, s) : insert_split(r, n, s);
   if (r->timing) r->t_insert += now_us() - t2;
   return st;
 }
@@ -185,7 +205,8 @@ lsm_status lsm_router_create(lsm_t* local, uint32_t nranks, uint32_t rank, const
     RouterBuf& B = r->buf[k];
     st = cu(cudaMalloc((void**)&B.rec, b_in * 8));
     if (st == LSM_OK) st = cu(cudaMalloc((void**)&B.cnt, 2 * nranks * 4));
-    if (st == LSM_OK) st = cu(cudaMallocHost((void**)&B.h_cnt, 2 * nranks * 4));
+    if (st == LSM_OK) st = cu(cudaHostAlloc((void**)&B.h_cnt, 2 * nranks * 4, cudaHostAllocMapped));
+    if (st == LSM_OK) st = cu(cudaHostGetDevicePointer((void**)&B.h_cnt_dev, B.h_cnt, 0));
     if (st == LSM_OK) st = cu(cudaEventCreateWithFlags(&B.ev, cudaEventDisableTiming));
   }
   if (st == LSM_OK) st = ensure_recv(r, b_local);
@@ -208,16 +229,20 @@ lsm_status lsm_router_update(lsm_router_t* r, const uint32_t* d_keys, const uint
   const uint32_t P = r->P;
   // encode + group by owner, then the count exchange (send | receive counts)
   double t0 = r->timing ? now_us() : 0.0;
-  RCK(lsm_shard_bucket_records(r->local, d_keys, d_vals, d_is_delete, n, P, B.rec, B.cnt, s));
+  RCK(lsm_shard_bucket_records(r->local, d_keys, d_vals, d_is_delete, n, P, B.rec,
+                               P > 1 ? B.cnt : B.h_cnt_dev, s));
   double t1 = r->timing ? now_us() : 0.0;
   r->t_bucket += t1 - t0;
-  RCK(nc(ncclGroupStart()));
-  for (uint32_t p = 0; p < P; ++p) {
-    RCK(nc(ncclSend(B.cnt + p, 1, ncclUint32, (int)p, r->comm, s)));
-    RCK(nc(ncclRecv(B.cnt + P + p, 1, ncclUint32, (int)p, r->comm, s)));
+  if (P > 1) {  // the own count is not exchanged (deliver copies it)
+    RCK(nc(ncclGroupStart()));
+    for (uint32_t p = 0; p < P; ++p) {
+      if (p == r->rank) continue;
+      RCK(nc(ncclSend(B.cnt + p, 1, ncclUint32, (int)p, r->comm, s)));
+      RCK(nc(ncclRecv(B.cnt + P + p, 1, ncclUint32, (int)p, r->comm, s)));
+    }
+    RCK(nc(ncclGroupEnd()));
   }
-  RCK(nc(ncclGroupEnd()));
-  RCK(cu(cudaMemcpyAsync(B.h_cnt, B.cnt, 2 * P * 4, cudaMemcpyDeviceToHost, s)));
+  if (P > 1) RCK(cu(cudaMemcpyAsync(B.h_cnt, B.cnt, 2 * P * 4, cudaMemcpyDeviceToHost, s)));
   RCK(cu(cudaEventRecord(B.ev, s)));
   if (r->timing) r->t_count += now_us() - t1;
   // the previous batch: its counts are (or soon will be) on the host

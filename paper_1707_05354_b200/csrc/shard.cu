@@ -42,12 +42,19 @@ __global__ void __launch_bounds__(kBThreads) bucket_count_kernel(const uint32_t*
                                                                  uint64_t ntiles) {
   __shared__ uint32_t c[kMaxShards];
   for (int i = threadIdx.x; i < (int)P; i += kBThreads) c[i] = 0;
+  pdl_wait();
+  pdl_trigger();
   __syncthreads();
   const uint64_t base = (uint64_t)blockIdx.x * kBTile;
-  for (int i = threadIdx.x; i < kBTile; i += kBThreads) {
-    const uint64_t p = base + i;
-    if (p < n) atomicAdd(&c[owner_of(__ldg(keys + p), P, mode)], 1u);
+  uint32_t k[kBItems];
+#pragma unroll
+  for (int i = 0; i < kBItems; ++i) {  // all loads in flight before the first atomic
+    const uint64_t p = base + i * kBThreads + threadIdx.x;
+    k[i] = p < n ? __ldg(keys + p) : 0u;
   }
+#pragma unroll
+  for (int i = 0; i < kBItems; ++i)
+    if (base + i * kBThreads + threadIdx.x < n) atomicAdd(&c[owner_of(k[i], P, mode)], 1u);
   __syncthreads();
   // layout: tcounts[owner * ntiles + tile] (owner-major for the scan)
   for (int i = threadIdx.x; i < (int)P; i += kBThreads) tcounts[(uint64_t)i * ntiles + blockIdx.x] = c[i];
@@ -60,6 +67,8 @@ __global__ void __launch_bounds__(1024) bucket_scan_kernel(uint32_t* __restrict_
                                                            uint64_t ntiles,
                                                            uint32_t* __restrict__ counts_out) {
   __shared__ uint32_t tmp[1024 / 32 + 1];
+  pdl_wait();
+  pdl_trigger();
   uint32_t carry = 0;
   for (uint64_t base = 0; base < total_words; base += 1024) {
     const uint64_t i = base + threadIdx.x;
@@ -88,15 +97,26 @@ __global__ void __launch_bounds__(kBThreads) bucket_scatter_kernel(
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = kBThreads / 32;
   for (int i = tid; i < NW * kMaxShards; i += kBThreads) (&wcnt[0][0])[i] = 0;
+  pdl_wait();
+  pdl_trigger();
   __syncthreads();
   const uint64_t base = (uint64_t)blockIdx.x * kBTile;
-  uint32_t own[kBItems], rk[kBItems];
+  uint32_t own[kBItems], rk[kBItems], kk[kBItems], vv[kBItems], oo[kBItems];
   const uint32_t lt = lanemask_lt();
+  // every load of the tile in flight first (keys, values, ops), then the ranks
+#pragma unroll
+  for (int i = 0; i < kBItems; ++i) {
+    const uint64_t p = base + warp * (32 * kBItems) + i * 32 + lane;
+    const bool in = p < n;
+    kk[i] = in ? __ldg(keys + p) : 0u;
+    vv[i] = (in && vals != nullptr) ? __ldg(vals + p) : 0u;
+    oo[i] = (in && ops != nullptr) ? (uint32_t)__ldg(ops + p) : 0u;
+  }
   // warp w handles items base + w*256 + i*32 + lane (stable order)
 #pragma unroll
   for (int i = 0; i < kBItems; ++i) {
     const uint64_t p = base + warp * (32 * kBItems) + i * 32 + lane;
-    const uint32_t o = p < n ? owner_of(__ldg(keys + p), P, mode) : 0xFFFFFFFFu;
+    const uint32_t o = p < n ? owner_of(kk[i], P, mode) : 0xFFFFFFFFu;
     own[i] = o;
     const uint32_t peers = __match_any_sync(kFull, o);
     rk[i] = __popc(peers & lt);
@@ -127,20 +147,20 @@ __global__ void __launch_bounds__(kBThreads) bucket_scatter_kernel(
         // encoded record for the owner's local insert (A1):
         // key variable (k << 1 | regular), value 0 for a tombstone (R6), an
         // out-of-domain key as a placebo + the sticky error (R5)
-        const uint32_t k = __ldg(keys + p);
-        const bool del = ops != nullptr && __ldg(ops + p) != 0;
+        const uint32_t k = kk[i];
+        const bool del = oo[i] != 0;
         uint2 r;
         if (k > kMaxKey) {
           r = make_uint2(kPlacebo, 0u);
           atomicOr(err, 1u);
         } else {
-          r = make_uint2((k << 1) | (del ? 0u : 1u), (del || vals == nullptr) ? 0u : __ldg(vals + p));
+          r = make_uint2((k << 1) | (del ? 0u : 1u), del ? 0u : vv[i]);
         }
         rec_out[dst] = r;
       } else {
-        keys_out[dst] = __ldg(keys + p);
-        if (vals) vals_out[dst] = __ldg(vals + p);
-        if (ops) ops_out[dst] = __ldg(ops + p);
+        keys_out[dst] = kk[i];
+        if (vals) vals_out[dst] = vv[i];
+        if (ops) ops_out[dst] = (uint8_t)oo[i];
       }
       if (perm_out) perm_out[dst] = (uint32_t)p;
     }
@@ -287,15 +307,21 @@ cudaError_t launch_bucket(const uint32_t* keys, const uint32_t* vals, const uint
                           const LaunchHooks& hk, uint32_t* rec_out, uint32_t* err) {
   const uint64_t ntiles = (n + kBTile - 1) / kBTile;
   hk.begin(hk.ctx, LSM_K_OTHER, s);
+  // programmatic dependent launches: each kernel waits for its predecessor's
+  // results (griddepcontrol.wait) after its launch overlapped that tail
+  cudaError_t e = cudaSuccess;
   if (ntiles > 0)
-    bucket_count_kernel<<<(unsigned)ntiles, kBThreads, 0, s>>>(keys, n, P, mode, scratch, ntiles);
-  bucket_scan_kernel<<<1, 1024, 0, s>>>(scratch, (uint64_t)P * ntiles, P, ntiles, counts_out);
-  if (ntiles > 0)
-    bucket_scatter_kernel<<<(unsigned)ntiles, kBThreads, 0, s>>>(
-        keys, vals, ops, n, P, mode, scratch, ntiles, keys_out, vals_out, ops_out, perm_out,
-        reinterpret_cast<uint2*>(rec_out), err);
+    e = launch_pdl(bucket_count_kernel, (unsigned)ntiles, kBThreads, 0, s, keys, n, P, mode,
+                   scratch, ntiles);
+  if (e == cudaSuccess)
+    e = launch_pdl(bucket_scan_kernel, 1u, 1024u, 0, s, scratch, (uint64_t)P * ntiles, P, ntiles,
+                   counts_out);
+  if (e == cudaSuccess && ntiles > 0)
+    e = launch_pdl(bucket_scatter_kernel, (unsigned)ntiles, kBThreads, 0, s, keys, vals, ops, n, P,
+                   mode, (const uint32_t*)scratch, ntiles, keys_out, vals_out, ops_out, perm_out,
+                   reinterpret_cast<uint2*>(rec_out), err);
   hk.end(hk.ctx, LSM_K_OTHER, (double)n * 18.0, s, 3);
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_scatter_back(const uint32_t* perm, const uint32_t* vin, const uint8_t* fin,
