@@ -323,31 +323,44 @@ lsm_status lsm_shard_scatter(lsm_t* h, const uint32_t* d_perm, const uint32_t* d
                              const uint8_t* d_found_in, uint64_t n, uint32_t* d_vals_out,
                              uint8_t* d_found_out, void* stream);
 
-/* Intersect each [k1, k2] with the key interval [lo, hi] (a shard's range);
- * an empty result is written as (1, 0), which every query treats as empty
- * (R9).                                                                    */
-lsm_status lsm_shard_clip(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2, uint64_t n,
-                          uint32_t lo, uint32_t hi, uint32_t* d_k1_out, uint32_t* d_k2_out,
-                          void* stream);
+/* Owner-routed count and range (every operation is key-local,
+ * PAPER.md:94-110). Shard o owns the original keys [ceil(o*2^31/P),
+ * ceil((o+1)*2^31/P) - 1] (the last shard also every query word above the
+ * domain, R8). Query q = [k1, k2] with k1 <= k2 covers the shards
+ * owner(k1)..owner(k2); its PIECES are its intersections with them, in shard
+ * (= key) order; k1 > k2 has none (R9). Writes d_pstart_out[nq+1] (query q's
+ * pieces are [pstart[q], pstart[q+1]), u32) and the pieces' bounds
+ * d_pk1_out / d_pk2_out; *npieces_out = the number of pieces. Syncs the
+ * stream (the host sizes the exchange); LSM_ERR_CAPACITY (pieces not
+ * written) if npieces > capacity.                                          */
+lsm_status lsm_shard_route_ranges(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2,
+                                  uint64_t nq, uint32_t nshards, uint32_t* d_pstart_out,
+                                  uint32_t* d_pk1_out, uint32_t* d_pk2_out, uint64_t capacity,
+                                  uint64_t* npieces_out, void* stream);
 
-/* out[i] = sum_{p < parts} in[p * n + i] (u32): totals of per-shard counts. */
-lsm_status lsm_shard_sum(lsm_t* h, const uint32_t* d_in, uint32_t parts, uint64_t n,
-                         uint32_t* d_out, void* stream);
+/* Count of each query = the sum of its pieces' counts. d_counts_in[i] is the
+ * count of the piece in bucket slot i, d_perm[i] its piece index (the
+ * permutation of lsm_shard_bucket over the pieces); d_pstart as written by
+ * lsm_shard_route_ranges. Writes d_counts_out[nq] (u32).                   */
+lsm_status lsm_shard_piece_sum(lsm_t* h, const uint32_t* d_counts_in, const uint32_t* d_perm,
+                               const uint32_t* d_pstart, uint64_t nq, uint64_t npieces,
+                               uint32_t* d_counts_out, void* stream);
 
-/* Range assembly at a query's origin rank (the concatenation
- * in shard order of SURVEY §8(e)): shard s returned, for this rank's nq
- * queries, its offsets slice d_offs[s*nq + q] (u64, in the sender's own
- * numbering, i.e. not rebased) and a block of d_block_len[s] (key, value)
- * pairs; the P blocks are concatenated in shard order in d_keys_in /
- * d_vals_in. Writes d_offsets_out[nq+1] and each query's pairs, shard 0's
- * first (shards own ascending key intervals, so the result is sorted by key,
- * PAPER.md:736); pairs are written while < capacity. Syncs the stream;
+/* Range answers at the origin rank: the bucket slots [c_0 + .. + c_{o-1},
+ * + c_o) (c = d_chunk_counts[nshards], u32) went to shard o, which returned
+ * d_offs[i] (u64, the start of slot i's pairs in shard o's own output
+ * numbering) and one block of d_block_len[o] (key, value) pairs; the blocks
+ * are concatenated in shard order in d_keys_in / d_vals_in. Writes
+ * d_offsets_out[nq+1] and every query's pairs, its pieces in shard order
+ * (sorted by key), while < capacity. Syncs the stream;
  * *total_out = number of pairs; LSM_ERR_CAPACITY if it exceeds capacity.   */
-lsm_status lsm_shard_range_assemble(lsm_t* h, const uint64_t* d_offs, const uint64_t* d_block_len,
-                                   uint32_t parts, uint64_t nq, const uint32_t* d_keys_in,
-                                   const uint32_t* d_vals_in, uint64_t* d_offsets_out,
-                                   uint32_t* d_keys_out, uint32_t* d_vals_out, uint64_t capacity,
-                                   uint64_t* total_out, void* stream);
+lsm_status lsm_shard_piece_assemble(lsm_t* h, const uint64_t* d_offs, const uint64_t* d_block_len,
+                                    const uint32_t* d_chunk_counts, uint32_t nshards,
+                                    const uint32_t* d_perm, const uint32_t* d_pstart, uint64_t nq,
+                                    uint64_t npieces, const uint32_t* d_keys_in,
+                                    const uint32_t* d_vals_in, uint64_t* d_offsets_out,
+                                    uint32_t* d_keys_out, uint32_t* d_vals_out, uint64_t capacity,
+                                    uint64_t* total_out, void* stream);
 
 /* Successor / predecessor across shards (R23): d_keys,
  * d_vals, d_found hold `parts` shards' local answers for the same n queries

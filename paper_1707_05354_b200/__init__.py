@@ -77,12 +77,13 @@ SIGNATURES = {
     "lsm_router_flush": ([_vp, _vp], _st),
     "lsm_router_stats": ([_vp, ctypes.POINTER(_u64), ctypes.POINTER(_u64)], _st),
     "lsm_router_destroy": ([_vp], _st),
-    "lsm_shard_clip": ([_vp, _vp, _vp, _u64, ctypes.c_uint32, ctypes.c_uint32, _vp, _vp, _vp], _st),
-    "lsm_shard_sum": ([_vp, _vp, ctypes.c_uint32, _u64, _vp, _vp], _st),
+    "lsm_shard_route_ranges": ([_vp, _vp, _vp, _u64, ctypes.c_uint32, _vp, _vp, _vp, _u64,
+                                ctypes.POINTER(_u64), _vp], _st),
+    "lsm_shard_piece_sum": ([_vp, _vp, _vp, _vp, _u64, _u64, _vp, _vp], _st),
+    "lsm_shard_piece_assemble": ([_vp, _vp, _vp, _vp, ctypes.c_uint32, _vp, _vp, _u64, _u64, _vp,
+                                  _vp, _vp, _vp, _vp, _u64, ctypes.POINTER(_u64), _vp], _st),
     "lsm_shard_pick": ([_vp, _vp, _vp, _vp, ctypes.c_uint32, _u64, ctypes.c_int, _vp, _vp, _vp,
                         _vp], _st),
-    "lsm_shard_range_assemble": ([_vp, _vp, _vp, ctypes.c_uint32, _u64, _vp, _vp, _vp, _vp, _vp,
-                                  _u64, ctypes.POINTER(_u64), _vp], _st),
 }
 
 
@@ -507,45 +508,64 @@ class GpuLSM:
                "lsm_shard_pick")
         return ko, vo, fo
 
-    def shard_range_assemble(self, offs, block_len, parts, nq, keys_in, vals_in, stream=None):
-        """Assemble this rank's range results from the shards' parts:
-        offs int64 [parts*nq] (each shard's offsets slice), block_len int64
-        [parts], the pair blocks concatenated in shard order. Returns
-        (offsets[nq+1] int64, keys, vals)."""
-        torch = _torch()
-        dev = offs.device
-        cap = int(keys_in.numel())
-        offsets = torch.empty(nq + 1, dtype=torch.int64, device=dev)
-        keys = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
-        vals = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
-        total = _u64(0)
-        _check(self._lib.lsm_shard_range_assemble(
-            self.h, _dev(offs, 8, "offs"), _dev(block_len, 8, "block_len"), int(parts), int(nq),
-            _dev(keys_in, 4, "keys_in"), _dev(vals_in, 4, "vals_in"), _dev(offsets, 8, "offsets"),
-            _dev(keys, 4, "keys"), _dev(vals, 4, "vals"), cap, ctypes.byref(total),
-            _stream_ptr(stream)), "lsm_shard_range_assemble")
-        t = int(total.value)
-        return offsets, keys[:t], vals[:t]
-
     def shard_scatter(self, perm, vals_in, found_in, vals_out, found_out, stream=None):
         _check(self._lib.lsm_shard_scatter(self.h, _dev(perm), _dev(vals_in), _dev(found_in, 1),
                                            perm.numel(), _dev(vals_out), _dev(found_out, 1),
                                            _stream_ptr(stream)), "lsm_shard_scatter")
 
-    def shard_clip(self, k1, k2, lo, hi, stream=None):
+    def shard_route_ranges(self, k1, k2, nshards, stream=None):
+        """Pieces of the (k1, k2) queries on the shards they cover -> (pk1, pk2,
+        pstart[nq+1] int32 (query q's pieces are [pstart[q], pstart[q+1])))."""
         torch = _torch()
-        o1 = torch.empty_like(k1)
-        o2 = torch.empty_like(k2)
-        _check(self._lib.lsm_shard_clip(self.h, _dev(k1), _dev(k2), k1.numel(), int(lo), int(hi),
-                                        _dev(o1), _dev(o2), _stream_ptr(stream)), "lsm_shard_clip")
-        return o1, o2
+        nq = k1.numel()
+        dev = k1.device
+        pstart = torch.empty(nq + 1, dtype=torch.int32, device=dev)
+        cap = nq + 1024
+        while True:
+            pk1 = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+            pk2 = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+            npc = _u64(0)
+            st = self._lib.lsm_shard_route_ranges(
+                self.h, _dev(k1, 4, "k1"), _dev(k2, 4, "k2"), nq, int(nshards), _dev(pstart),
+                _dev(pk1), _dev(pk2), cap, ctypes.byref(npc), _stream_ptr(stream))
+            if st == LSM_ERR_CAPACITY and int(npc.value) > cap:
+                cap = int(npc.value)
+                continue
+            _check(st, "lsm_shard_route_ranges")
+            n = int(npc.value)
+            return pk1[:n], pk2[:n], pstart
 
-    def shard_sum(self, parts_tensor, parts, n, stream=None):
+    def shard_piece_sum(self, counts_in, perm, pstart, nq, stream=None):
+        """Per-query sums of piece counts (counts_in in bucket order)."""
         torch = _torch()
-        out = torch.empty(n, dtype=torch.int32, device=parts_tensor.device)
-        _check(self._lib.lsm_shard_sum(self.h, _dev(parts_tensor), int(parts), int(n), _dev(out),
-                                       _stream_ptr(stream)), "lsm_shard_sum")
+        out = torch.empty(nq, dtype=torch.int32, device=pstart.device)
+        _check(self._lib.lsm_shard_piece_sum(self.h, _dev(counts_in), _dev(perm), _dev(pstart),
+                                             int(nq), int(perm.numel()), _dev(out),
+                                             _stream_ptr(stream)), "lsm_shard_piece_sum")
         return out
+
+    def shard_piece_assemble(self, offs, block_len, chunk_counts, nshards, perm, pstart, nq,
+                             keys_in, vals_in, stream=None):
+        """Range answers from the shards' piece results: offs int64
+        [npieces] (bucket order, each shard's own numbering), block_len int64
+        [nshards], chunk_counts int32 [nshards] (pieces sent to each shard), the
+        pair blocks concatenated in shard order -> (offsets[nq+1] int64, keys, vals)."""
+        torch = _torch()
+        dev = pstart.device
+        cap = int(keys_in.numel())
+        offsets = torch.empty(nq + 1, dtype=torch.int64, device=dev)
+        keys = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+        vals = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+        total = _u64(0)
+        _check(self._lib.lsm_shard_piece_assemble(
+            self.h, _dev(offs, 8, "offs"), _dev(block_len, 8, "block_len"),
+            _dev(chunk_counts, 4, "chunk_counts"), int(nshards), _dev(perm, 4, "perm"),
+            _dev(pstart, 4, "pstart"), int(nq), int(perm.numel()), _dev(keys_in, 4, "keys_in"),
+            _dev(vals_in, 4, "vals_in"), _dev(offsets, 8, "offsets"), _dev(keys, 4, "keys"),
+            _dev(vals, 4, "vals"), cap, ctypes.byref(total), _stream_ptr(stream)),
+            "lsm_shard_piece_assemble")
+        t = int(total.value)
+        return offsets, keys[:t], vals[:t]
 
     @property
     def launch_count(self) -> int:

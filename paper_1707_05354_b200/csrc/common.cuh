@@ -405,19 +405,30 @@ cudaError_t launch_bucket(const uint32_t* keys, const uint32_t* vals, const uint
 cudaError_t launch_scatter_back(const uint32_t* perm, const uint32_t* vin, const uint8_t* fin,
                                 uint64_t n, uint32_t* vout, uint8_t* fout, cudaStream_t s,
                                 const LaunchHooks& hk);
-cudaError_t launch_clip(const uint32_t* k1, const uint32_t* k2, uint64_t n, uint32_t lo,
-                        uint32_t hi, uint32_t* o1, uint32_t* o2, cudaStream_t s,
-                        const LaunchHooks& hk);
-cudaError_t launch_range_assemble(const uint64_t* offs, const uint64_t* blen, uint32_t P,
-                                  uint64_t nq, const uint32_t* kin, const uint32_t* vin,
-                                  uint64_t* offsets, uint32_t* kout, uint32_t* vout,
-                                  uint64_t capacity, uint32_t* totals, uint64_t* sums,
-                                  cudaStream_t s, const LaunchHooks& hk);
+// owner-routed count / range: pieces of each query on the
+// shards it covers (route_*), per-query sums of piece counts, and the range
+// answers concatenated in piece (= key) order at the origin (piece_assemble).
+uint64_t route_scratch_words(uint64_t nq);
+cudaError_t launch_route_count(const uint32_t* k1, const uint32_t* k2, uint64_t nq, uint32_t P,
+                               uint64_t* scratch, uint64_t* npc_dev, cudaStream_t s,
+                               const LaunchHooks& hk);
+cudaError_t launch_route_write(const uint32_t* k1, const uint32_t* k2, uint64_t nq, uint32_t P,
+                               const uint64_t* scratch, uint64_t npc, uint32_t* pstart,
+                               uint32_t* pk1, uint32_t* pk2, cudaStream_t s, const LaunchHooks& hk);
+cudaError_t launch_piece_sum(const uint32_t* cnt, const uint32_t* perm, const uint32_t* pstart,
+                             uint64_t nq, uint64_t npc, uint32_t* tmp, uint32_t* out,
+                             cudaStream_t s, const LaunchHooks& hk);
+uint64_t piece_scratch_words(uint64_t npc);
+cudaError_t launch_piece_assemble(const uint64_t* offs, const uint64_t* blen,
+                                  const uint32_t* chunk_cnt, uint32_t P, const uint32_t* perm,
+                                  const uint32_t* pstart, uint64_t nq, uint64_t npc,
+                                  const uint32_t* kin, const uint32_t* vin, uint64_t* offsets,
+                                  uint32_t* kout, uint32_t* vout, uint64_t capacity,
+                                  uint64_t* scratch, cudaStream_t s, const LaunchHooks& hk);
 cudaError_t launch_pick(const uint32_t* kin, const uint32_t* vin, const uint8_t* fin,
                         uint32_t parts, uint64_t n, int last, uint32_t* kout, uint32_t* vout,
                         uint8_t* fout, cudaStream_t s, const LaunchHooks& hk);
-cudaError_t launch_sum_parts(const uint32_t* in, uint32_t parts, uint64_t n, uint32_t* out,
-                             cudaStream_t s, const LaunchHooks& hk);
+
 
 cudaError_t launch_fill_placebo(uint32_t* ck, uint32_t* cv, uint64_t from, uint64_t to,
                                 cudaStream_t s, const LaunchHooks& hk);

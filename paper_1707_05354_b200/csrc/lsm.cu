@@ -1239,57 +1239,83 @@ lsm_status lsm_shard_scatter(lsm_t* h, const uint32_t* d_perm, const uint32_t* d
   return LSM_OK;
 }
 
-lsm_status lsm_shard_clip(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2, uint64_t n,
-                          uint32_t lo, uint32_t hi, uint32_t* d_k1_out, uint32_t* d_k2_out,
-                          void* stream) {
-  if (!h) return LSM_ERR_INVALID_ARG;
-  ENTER(h);
-  if (n == 0) return LSM_OK;
-  if (!d_k1 || !d_k2 || !d_k1_out || !d_k2_out) return LSM_ERR_INVALID_ARG;
-  CK(launch_clip(d_k1, d_k2, n, lo, hi, d_k1_out, d_k2_out, S(stream), hooks(h)));
-  return LSM_OK;
-}
-
-lsm_status lsm_shard_sum(lsm_t* h, const uint32_t* d_in, uint32_t parts, uint64_t n,
-                         uint32_t* d_out, void* stream) {
-  if (!h || parts == 0) return LSM_ERR_INVALID_ARG;
-  ENTER(h);
-  if (n == 0) return LSM_OK;
-  if (!d_in || !d_out) return LSM_ERR_INVALID_ARG;
-  CK(launch_sum_parts(d_in, parts, n, d_out, S(stream), hooks(h)));
-  return LSM_OK;
-}
-
-lsm_status lsm_shard_range_assemble(lsm_t* h, const uint64_t* d_offs, const uint64_t* d_block_len,
-                                   uint32_t parts, uint64_t nq, const uint32_t* d_keys_in,
-                                   const uint32_t* d_vals_in, uint64_t* d_offsets_out,
-                                   uint32_t* d_keys_out, uint32_t* d_vals_out, uint64_t capacity,
-                                   uint64_t* total_out, void* stream) {
-  if (!h || parts == 0 || !total_out || !d_offsets_out) return LSM_ERR_INVALID_ARG;
+lsm_status lsm_shard_route_ranges(lsm_t* h, const uint32_t* d_k1, const uint32_t* d_k2,
+                                  uint64_t nq, uint32_t nshards, uint32_t* d_pstart_out,
+                                  uint32_t* d_pk1_out, uint32_t* d_pk2_out, uint64_t capacity,
+                                  uint64_t* npieces_out, void* stream) {
+  if (!h || nshards == 0 || nshards > 64 || !npieces_out || !d_pstart_out) return LSM_ERR_INVALID_ARG;
   ENTER(h);
   cudaStream_t s = S(stream);
+  *npieces_out = 0;
   if (nq == 0) {
-    CK(cudaMemsetAsync(d_offsets_out, 0, 8, s));
-    *total_out = 0;
+    CK(cudaMemsetAsync(d_pstart_out, 0, 4, s));
     return LSM_OK;
   }
-  if (!d_offs || !d_block_len) return LSM_ERR_INVALID_ARG;
+  if (!d_k1 || !d_k2 || nq >= 0xFFFFFFFFull) return LSM_ERR_INVALID_ARG;
+  CallScratch sc(h, s);
+  CK(sc.get(route_scratch_words(nq) * 8));
+  uint64_t* scr = static_cast<uint64_t*>(sc.p);
+  uint64_t* npc_dev = scr + route_scratch_words(nq) - 1;
+  CK(launch_route_count(d_k1, d_k2, nq, nshards, scr, npc_dev, s, hooks(h)));
+  CK(cudaMemcpyAsync(h->h_pinned, npc_dev, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const uint64_t npc = h->h_pinned[0];
+  *npieces_out = npc;
+  if (npc >= 0xFFFFFFFFull) return LSM_ERR_INVALID_ARG;
+  if (npc > capacity) return LSM_ERR_CAPACITY;
+  if (npc > 0 && (!d_pk1_out || !d_pk2_out)) return LSM_ERR_INVALID_ARG;
+  CK(launch_route_write(d_k1, d_k2, nq, nshards, scr, npc, d_pstart_out, d_pk1_out, d_pk2_out, s,
+                        hooks(h)));
+  return LSM_OK;
+}
+
+lsm_status lsm_shard_piece_sum(lsm_t* h, const uint32_t* d_counts_in, const uint32_t* d_perm,
+                               const uint32_t* d_pstart, uint64_t nq, uint64_t npieces,
+                               uint32_t* d_counts_out, void* stream) {
+  if (!h) return LSM_ERR_INVALID_ARG;
+  ENTER(h);
+  if (nq == 0) return LSM_OK;
+  if (!d_pstart || !d_counts_out || (npieces > 0 && (!d_counts_in || !d_perm)))
+    return LSM_ERR_INVALID_ARG;
+  cudaStream_t s = S(stream);
+  CallScratch sc(h, s);
+  CK(sc.get(npieces * 4 + 16));
+  CK(launch_piece_sum(d_counts_in, d_perm, d_pstart, nq, npieces, static_cast<uint32_t*>(sc.p),
+                      d_counts_out, s, hooks(h)));
+  return LSM_OK;
+}
+
+lsm_status lsm_shard_piece_assemble(lsm_t* h, const uint64_t* d_offs, const uint64_t* d_block_len,
+                                    const uint32_t* d_chunk_counts, uint32_t nshards,
+                                    const uint32_t* d_perm, const uint32_t* d_pstart, uint64_t nq,
+                                    uint64_t npieces, const uint32_t* d_keys_in,
+                                    const uint32_t* d_vals_in, uint64_t* d_offsets_out,
+                                    uint32_t* d_keys_out, uint32_t* d_vals_out, uint64_t capacity,
+                                    uint64_t* total_out, void* stream) {
+  if (!h || nshards == 0 || nshards > 64 || !total_out || !d_offsets_out) return LSM_ERR_INVALID_ARG;
+  ENTER(h);
+  cudaStream_t s = S(stream);
+  *total_out = 0;
+  if (nq == 0) {
+    CK(cudaMemsetAsync(d_offsets_out, 0, 8, s));
+    return LSM_OK;
+  }
+  if (!d_pstart || (npieces > 0 && (!d_offs || !d_block_len || !d_chunk_counts || !d_perm)))
+    return LSM_ERR_INVALID_ARG;
   if (capacity > 0 && (!d_keys_out || !d_vals_out || !d_keys_in || !d_vals_in))
     return LSM_ERR_INVALID_ARG;
-  const uint64_t tb = align_up(nq * 4, 256);
   {
     CallScratch sc(h, s);
-    CK(sc.get(tb + scan_scratch_words(nq) * 8));
-    uint8_t* qb = static_cast<uint8_t*>(sc.p);
-    CK(launch_range_assemble(d_offs, d_block_len, parts, nq, d_keys_in, d_vals_in, d_offsets_out,
-                             d_keys_out, d_vals_out, capacity, reinterpret_cast<uint32_t*>(qb),
-                             reinterpret_cast<uint64_t*>(qb + tb), s, hooks(h)));
+    CK(sc.get(piece_scratch_words(npieces) * 8));
+    CK(launch_piece_assemble(d_offs, d_block_len, d_chunk_counts, nshards, d_perm, d_pstart, nq,
+                             npieces, d_keys_in, d_vals_in, d_offsets_out, d_keys_out, d_vals_out,
+                             capacity, static_cast<uint64_t*>(sc.p), s, hooks(h)));
   }
   uint64_t total = 0;
   CK(cudaMemcpyAsync(&total, d_offsets_out + nq, 8, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   *total_out = total;
-  return *total_out > capacity ? LSM_ERR_CAPACITY : LSM_OK;
+  return total > capacity ? LSM_ERR_CAPACITY : LSM_OK;
 }
 
 lsm_status lsm_shard_pick(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals,

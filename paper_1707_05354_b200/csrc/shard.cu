@@ -10,7 +10,10 @@
 //    scatter (in-tile ranks from warp ballots, one per owner). Also writes the
 //    permutation (source index of every output slot) for results routed back.
 //  * scatter_back: out[perm[i]] = in[i] for lookup results.
-//  * clip: intersect [k1, k2] with a shard's key range (empty stays empty).
+//  * route / piece_*: owner-routed count and range -- a query is cut into
+//    its pieces on the shards it covers, each piece goes to its owner only,
+//    and the answers are summed (count) or concatenated in shard order
+//    (range) at the origin.
 
 #include <algorithm>
 
@@ -179,75 +182,6 @@ __global__ void scatter_back_kernel(const uint32_t* __restrict__ perm,
   }
 }
 
-__global__ void clip_kernel(const uint32_t* __restrict__ k1, const uint32_t* __restrict__ k2,
-                            uint64_t n, uint32_t lo, uint32_t hi, uint32_t* __restrict__ o1,
-                            uint32_t* __restrict__ o2) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t a = __ldg(k1 + i), z = __ldg(k2 + i);
-    if (a > z || z < lo || a > hi) {  // empty stays empty: (1, 0)
-      a = 1;
-      z = 0;
-    } else {
-      a = max(a, lo);
-      z = min(z, hi);
-    }
-    o1[i] = a;
-    o2[i] = z;
-  }
-}
-
-// Range assembly at the query's origin: shard s sent, for
-// each of this rank's nq queries, its offsets slice offs[s][q] (u64, the
-// sender's numbering) and one block of pairs (block_len[s] of them, blocks
-// concatenated in shard order). count[s][q] = offs[s][q+1] - offs[s][q]
-// (the block end for the last query).
-__device__ __forceinline__ uint64_t part_count(const uint64_t* offs, const uint64_t* blen,
-                                               uint32_t s, uint64_t q, uint64_t nq) {
-  const uint64_t* o = offs + (uint64_t)s * nq;
-  const uint64_t end = q + 1 < nq ? o[q + 1] : o[0] + blen[s];
-  return end - o[q];
-}
-
-__global__ void range_totals_kernel(const uint64_t* __restrict__ offs,
-                                    const uint64_t* __restrict__ blen, uint32_t P, uint64_t nq,
-                                    uint32_t* __restrict__ totals) {
-  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq;
-       q += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t t = 0;
-    for (uint32_t s = 0; s < P; ++s) t += part_count(offs, blen, s, q, nq);
-    totals[q] = (uint32_t)t;
-  }
-}
-
-// pairs of (shard s, query q) -> out[offsets[q] + (pairs of shards < s)],
-// shard order = key order, so each query's pairs stay sorted
-__global__ void range_scatter_kernel(const uint64_t* __restrict__ offs,
-                                     const uint64_t* __restrict__ blen, uint32_t P, uint64_t nq,
-                                     const uint32_t* __restrict__ kin,
-                                     const uint32_t* __restrict__ vin,
-                                     const uint64_t* __restrict__ offsets,
-                                     uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
-                                     uint64_t capacity) {
-  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq;
-       q += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t dst = offsets[q], base = 0;
-    for (uint32_t s = 0; s < P; ++s) {
-      const uint64_t* o = offs + (uint64_t)s * nq;
-      const uint64_t c = part_count(offs, blen, s, q, nq);
-      const uint64_t src = base + (o[q] - o[0]);
-      for (uint64_t i = 0; i < c; ++i) {
-        if (dst + i < capacity) {
-          kout[dst + i] = kin[src + i];
-          vout[dst + i] = vin[src + i];
-        }
-      }
-      dst += c;
-      base += blen[s];
-    }
-  }
-}
-
 // successor / predecessor across shards: the answer is the first shard (in
 // shard = key order) with an answer for a successor, the last one for a
 // predecessor (shards own ascending key intervals)
@@ -274,27 +208,137 @@ __global__ void pick_kernel(const uint32_t* __restrict__ kin, const uint32_t* __
   }
 }
 
-__global__ void sum_parts_kernel(const uint32_t* __restrict__ in, uint32_t parts, uint64_t n,
-                                 uint32_t* __restrict__ out) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+// ---- owner-routed count / range ----
+// A query [k1, k2] (k1 <= k2) covers the shards owner(k1) .. owner(k2); its
+// PIECES are its intersections with those shards' key intervals, in shard (=
+// key) order, so the concatenation of its pieces' answers is its answer
+// (every dictionary operation is key-local). Pieces are
+// numbered query by query: query q's pieces are [pstart[q], pstart[q+1]).
+__device__ __forceinline__ uint32_t shard_lo(uint32_t o, uint32_t P) {
+  return (uint32_t)(((uint64_t)o * 0x80000000ull + P - 1) / P);  // ceil(o * 2^31 / P)
+}
+__device__ __forceinline__ uint32_t shard_hi(uint32_t o, uint32_t P) {
+  return o + 1 < P ? shard_lo(o + 1, P) - 1u : 0xFFFFFFFFu;
+}
+
+__global__ void route_count_kernel(const uint32_t* __restrict__ k1, const uint32_t* __restrict__ k2,
+                                   uint64_t nq, uint32_t P, uint32_t* __restrict__ npieces) {
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t a = __ldg(k1 + q), z = __ldg(k2 + q);
+    npieces[q] = a > z ? 0u : owner_of(z, P, 0) - owner_of(a, P, 0) + 1u;
+  }
+}
+
+__global__ void route_write_kernel(const uint32_t* __restrict__ k1, const uint32_t* __restrict__ k2,
+                                   uint64_t nq, uint32_t P, const uint64_t* __restrict__ pofs,
+                                   uint64_t npc, uint32_t* __restrict__ pstart,
+                                   uint32_t* __restrict__ pk1, uint32_t* __restrict__ pk2) {
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t a = __ldg(k1 + q), z = __ldg(k2 + q);
+    const uint64_t d = pofs[q];
+    pstart[q] = (uint32_t)d;
+    if (q == nq - 1) pstart[nq] = (uint32_t)npc;
+    if (a > z) continue;
+    const uint32_t o1 = owner_of(a, P, 0), o2 = owner_of(z, P, 0);
+    for (uint32_t o = o1; o <= o2; ++o) {
+      pk1[d + (o - o1)] = max(a, shard_lo(o, P));
+      pk2[d + (o - o1)] = min(z, shard_hi(o, P));
+    }
+  }
+}
+
+// count of query q = sum of its pieces' counts; cnt[i] is the count of the
+// piece in bucket slot i (perm[i] = its piece index)
+__global__ void piece_unpermute_kernel(const uint32_t* __restrict__ cnt,
+                                       const uint32_t* __restrict__ perm, uint64_t npc,
+                                       uint32_t* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npc;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[__ldg(perm + i)] = __ldg(cnt + i);
+}
+
+__global__ void piece_sum_kernel(const uint32_t* __restrict__ pc, const uint32_t* __restrict__ pstart,
+                                 uint64_t nq, uint32_t* __restrict__ out) {
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t c = 0;
+    for (uint32_t i = __ldg(pstart + q); i < __ldg(pstart + q + 1); ++i) c += __ldg(pc + i);
+    out[q] = c;
+  }
+}
+
+// Range answers at the origin. Bucket slot i belongs to owner chunk c (the
+// slots [cstart[c], cstart[c+1]) went to owner c); owner c returned the
+// start offset offs[i] of every piece in ITS output numbering and one block
+// of blen[c] pairs for this rank (blocks concatenated in owner order). Per
+// piece (by piece index): its pair count and its source in the blocks.
+__global__ void piece_locate_kernel(const uint64_t* __restrict__ offs,
+                                    const uint64_t* __restrict__ blen,
+                                    const uint32_t* __restrict__ chunk_cnt, uint32_t P,
+                                    const uint32_t* __restrict__ perm, uint64_t npc,
+                                    uint32_t* __restrict__ pc, uint64_t* __restrict__ psrc) {
+  __shared__ uint64_t cstart[kMaxShards + 1], bstart[kMaxShards + 1];
+  if (threadIdx.x == 0) {
+    uint64_t c = 0, bsum = 0;
+    for (uint32_t o = 0; o < P; ++o) {
+      cstart[o] = c;
+      bstart[o] = bsum;
+      c += chunk_cnt[o];
+      bsum += blen[o];
+    }
+    cstart[P] = c;
+    bstart[P] = bsum;
+  }
+  __syncthreads();
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npc;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t s = 0;
-    for (uint32_t p = 0; p < parts; ++p) s += __ldg(in + (uint64_t)p * n + i);
-    out[i] = s;
+    uint32_t c = 0;
+    while (c + 1 < P && i >= cstart[c + 1]) ++c;
+    const uint64_t first = offs[cstart[c]];
+    const uint64_t end = i + 1 < cstart[c + 1] ? offs[i + 1] : first + blen[c];
+    const uint32_t d = __ldg(perm + i);
+    pc[d] = (uint32_t)(end - offs[i]);
+    psrc[d] = bstart[c] + (offs[i] - first);
+  }
+}
+
+__global__ void piece_offsets_kernel(const uint64_t* __restrict__ pdst,
+                                     const uint32_t* __restrict__ pstart, uint64_t nq,
+                                     uint64_t npc, const uint64_t* __restrict__ total,
+                                     uint64_t* __restrict__ offsets) {
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q <= nq;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t p = __ldg(pstart + q);
+    offsets[q] = p < npc ? pdst[p] : *total;
+  }
+}
+
+// one warp per piece: its pairs from the owner's block to the query's slot
+// (a query's pieces are consecutive in piece order = key order)
+__global__ void piece_copy_kernel(const uint32_t* __restrict__ pc, const uint64_t* __restrict__ psrc,
+                                  const uint64_t* __restrict__ pdst, uint64_t npc,
+                                  const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                  uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
+                                  uint64_t capacity) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t w0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const uint64_t nw = (uint64_t)gridDim.x * blockDim.x / 32;
+  for (uint64_t j = w0; j < npc; j += nw) {
+    const uint32_t c = __ldg(pc + j);
+    const uint64_t src = psrc[j], dst = pdst[j];
+    for (uint32_t t = lane; t < c; t += 32) {
+      if (dst + t < capacity) {
+        kout[dst + t] = __ldg(kin + src + t);
+        vout[dst + t] = __ldg(vin + src + t);
+      }
+    }
   }
 }
 
 }  // namespace
 
-cudaError_t launch_sum_parts(const uint32_t* in, uint32_t parts, uint64_t n, uint32_t* out,
-                             cudaStream_t s, const LaunchHooks& hk) {
-  if (n == 0) return cudaSuccess;
-  unsigned grid = (unsigned)((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
-  hk.begin(hk.ctx, LSM_K_OTHER, s);
-  sum_parts_kernel<<<grid, 256, 0, s>>>(in, parts, n, out);
-  hk.end(hk.ctx, LSM_K_OTHER, (double)n * 4.0 * (parts + 1), s, 1);
-  return cudaGetLastError();
-}
 
 uint64_t bucket_scratch_words(uint64_t n, uint32_t P) {
   return (uint64_t)P * ((n + kBTile - 1) / kBTile) + 1;
@@ -335,34 +379,7 @@ cudaError_t launch_scatter_back(const uint32_t* perm, const uint32_t* vin, const
   return cudaGetLastError();
 }
 
-cudaError_t launch_clip(const uint32_t* k1, const uint32_t* k2, uint64_t n, uint32_t lo,
-                        uint32_t hi, uint32_t* o1, uint32_t* o2, cudaStream_t s,
-                        const LaunchHooks& hk) {
-  if (n == 0) return cudaSuccess;
-  unsigned grid = (unsigned)((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
-  hk.begin(hk.ctx, LSM_K_OTHER, s);
-  clip_kernel<<<grid, 256, 0, s>>>(k1, k2, n, lo, hi, o1, o2);
-  hk.end(hk.ctx, LSM_K_OTHER, (double)n * 16.0, s, 1);
-  return cudaGetLastError();
-}
 
-cudaError_t launch_range_assemble(const uint64_t* offs, const uint64_t* blen, uint32_t P,
-                                  uint64_t nq, const uint32_t* kin, const uint32_t* vin,
-                                  uint64_t* offsets, uint32_t* kout, uint32_t* vout,
-                                  uint64_t capacity, uint32_t* totals, uint64_t* sums,
-                                  cudaStream_t s, const LaunchHooks& hk) {
-  const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nq + 255) / 256, 148 * 8));
-  hk.begin(hk.ctx, LSM_K_OTHER, s);
-  range_totals_kernel<<<g, 256, 0, s>>>(offs, blen, P, nq, totals);
-  hk.end(hk.ctx, LSM_K_OTHER, (double)nq * (8.0 * P + 4.0), s, 1);
-  cudaError_t e = launch_scan(totals, nq, offsets, sums, s, hk);
-  if (e != cudaSuccess) return e;
-  hk.begin(hk.ctx, LSM_K_OTHER, s);
-  range_scatter_kernel<<<g, 256, 0, s>>>(offs, blen, P, nq, kin, vin, offsets, kout, vout,
-                                         capacity);
-  hk.end(hk.ctx, LSM_K_OTHER, (double)nq * (8.0 * P + 8.0), s, 1);
-  return cudaGetLastError();
-}
 
 cudaError_t launch_pick(const uint32_t* kin, const uint32_t* vin, const uint8_t* fin,
                         uint32_t parts, uint64_t n, int last, uint32_t* kout, uint32_t* vout,
@@ -372,6 +389,83 @@ cudaError_t launch_pick(const uint32_t* kin, const uint32_t* vin, const uint8_t*
   pick_kernel<<<g, 256, 0, s>>>(kin, vin, fin, parts, n, last, kout, vout, fout);
   hk.end(hk.ctx, LSM_K_OTHER, (double)n * (9.0 * parts + 9.0), s, 1);
   return cudaGetLastError();
+}
+
+static unsigned small_grid(uint64_t n) {
+  return (unsigned)((n + 255) / 256 < 148 * 16 ? std::max<uint64_t>(1, (n + 255) / 256) : 148 * 16);
+}
+
+uint64_t route_scratch_words(uint64_t nq) {
+  return (nq * 4 + 7) / 8 + (nq + 1) + scan_scratch_words(nq) + 1;
+}
+
+cudaError_t launch_route_count(const uint32_t* k1, const uint32_t* k2, uint64_t nq, uint32_t P,
+                               uint64_t* scratch, uint64_t* npc_dev, cudaStream_t s,
+                               const LaunchHooks& hk) {
+  uint32_t* np = reinterpret_cast<uint32_t*>(scratch);
+  uint64_t* pofs = scratch + (nq * 4 + 7) / 8;  // nq + 1 words
+  uint64_t* sc = pofs + nq + 1;
+  hk.begin(hk.ctx, LSM_K_OTHER, s);
+  route_count_kernel<<<small_grid(nq), 256, 0, s>>>(k1, k2, nq, P, np);
+  cudaError_t e = launch_scan(np, nq, pofs, sc, s, hk);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(npc_dev, pofs + nq, 8, cudaMemcpyDeviceToDevice, s);
+  hk.end(hk.ctx, LSM_K_OTHER, (double)nq * 8.0, s, 1);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t launch_route_write(const uint32_t* k1, const uint32_t* k2, uint64_t nq, uint32_t P,
+                               const uint64_t* scratch, uint64_t npc, uint32_t* pstart,
+                               uint32_t* pk1, uint32_t* pk2, cudaStream_t s, const LaunchHooks& hk) {
+  const uint64_t* pofs = scratch + (nq * 4 + 7) / 8;
+  hk.begin(hk.ctx, LSM_K_OTHER, s);
+  route_write_kernel<<<small_grid(nq), 256, 0, s>>>(k1, k2, nq, P, pofs, npc, pstart, pk1, pk2);
+  hk.end(hk.ctx, LSM_K_OTHER, (double)nq * 12.0 + npc * 8.0, s, 1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_piece_sum(const uint32_t* cnt, const uint32_t* perm, const uint32_t* pstart,
+                             uint64_t nq, uint64_t npc, uint32_t* tmp, uint32_t* out,
+                             cudaStream_t s, const LaunchHooks& hk) {
+  hk.begin(hk.ctx, LSM_K_OTHER, s);
+  if (npc > 0) piece_unpermute_kernel<<<small_grid(npc), 256, 0, s>>>(cnt, perm, npc, tmp);
+  piece_sum_kernel<<<small_grid(nq), 256, 0, s>>>(tmp, pstart, nq, out);
+  hk.end(hk.ctx, LSM_K_OTHER, (double)npc * 12.0 + nq * 12.0, s, 2);
+  return cudaGetLastError();
+}
+
+uint64_t piece_scratch_words(uint64_t npc) {
+  return (npc * 4 + 7) / 8 + 2 * npc + scan_scratch_words(npc) + 2;
+}
+
+cudaError_t launch_piece_assemble(const uint64_t* offs, const uint64_t* blen,
+                                  const uint32_t* chunk_cnt, uint32_t P, const uint32_t* perm,
+                                  const uint32_t* pstart, uint64_t nq, uint64_t npc,
+                                  const uint32_t* kin, const uint32_t* vin, uint64_t* offsets,
+                                  uint32_t* kout, uint32_t* vout, uint64_t capacity,
+                                  uint64_t* scratch, cudaStream_t s, const LaunchHooks& hk) {
+  uint32_t* pc = reinterpret_cast<uint32_t*>(scratch);
+  uint64_t* psrc = scratch + (npc * 4 + 7) / 8;
+  uint64_t* pdst = psrc + npc;
+  uint64_t* sc = pdst + npc + 1;
+  hk.begin(hk.ctx, LSM_K_OTHER, s);
+  cudaError_t e = cudaSuccess;
+  if (npc > 0) {
+    piece_locate_kernel<<<small_grid(npc), 256, 0, s>>>(offs, blen, chunk_cnt, P, perm, npc, pc,
+                                                         psrc);
+    e = launch_scan(pc, npc, pdst, sc, s, hk);
+  } else {
+    e = cudaMemsetAsync(pdst, 0, 8, s);
+  }
+  if (e == cudaSuccess) {
+    piece_offsets_kernel<<<small_grid(nq + 1), 256, 0, s>>>(pdst, pstart, nq, npc, pdst + npc,
+                                                             offsets);
+    if (npc > 0)
+      piece_copy_kernel<<<small_grid(npc * 32), 256, 0, s>>>(pc, psrc, pdst, npc, kin, vin, kout,
+                                                              vout, capacity);
+  }
+  hk.end(hk.ctx, LSM_K_OTHER, (double)npc * 28.0 + nq * 12.0, s, 4);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace gpulsm

@@ -22,16 +22,18 @@ Lookups: bucket the queries (keeping the permutation), all-to-all them to
 their owners, look up locally, all-to-all the (value, found) results back
 and scatter them to the original positions (lsm_shard_scatter).
 
-Counts: every rank gathers all ranks' (k1, k2), clips them to its own key
-interval (lsm_shard_clip), counts locally, and the per-shard partial counts
-go back to each query's origin with an all-to-all and are summed there
-(lsm_shard_sum): a range that spans shards is the sum of its pieces.
-
-Ranges: the same gather + clip, one local range over all ranks' queries, then
-each origin receives from every shard its offsets slice and its block of
-pairs (an all-to-all-v after an exchange of the block lengths) and
-lsm_shard_range_assemble concatenates each query's pieces in shard order --
-key order, since shards own ascending key intervals.
+Counts and ranges are routed by owner: lsm_shard_route_ranges cuts each
+query [k1, k2] into its PIECES, its intersections with the key intervals of
+the shards it covers (one piece for a range inside one shard), numbered query
+by query in shard = key order; the pieces are bucketed by owner (keeping the
+permutation) and go to their owners only, in one all-to-all. Each owner
+counts (or ranges) the pieces it received locally. Counts come back with the
+reverse all-to-all and lsm_shard_piece_sum adds up each query's pieces. For
+ranges each owner returns, per origin, the start offset of every piece and
+one block of pairs (an all-to-all-v after an exchange of the block lengths),
+and lsm_shard_piece_assemble writes each query's pieces one after another in
+shard order -- key order, since shards own ascending key intervals. Every
+rank handles only the pieces it owns: O(nq) work per rank, not O(P nq).
 
 Successor / predecessor: all-gather the queries, every shard answers all of
 them locally (its keys lie in its own interval, so no clipping), the answers
@@ -93,11 +95,11 @@ class GpuShardBackend:
         self.lsm.shard_scatter(perm, vals, found, vo, fo)
         return vo, fo
 
-    def clip(self, k1, k2, lo, hi):
-        return self.lsm.shard_clip(k1, k2, lo, hi)
+    def route_ranges(self, k1, k2, P):
+        return self.lsm.shard_route_ranges(k1, k2, P)
 
-    def sum_parts(self, t, P, n):
-        return self.lsm.shard_sum(t, P, n)
+    def piece_sum(self, counts, perm, pstart, nq):
+        return self.lsm.shard_piece_sum(counts, perm, pstart, nq)
 
     def update(self, k, v, o):
         self.lsm.update(k, v, o)
@@ -128,8 +130,13 @@ class GpuShardBackend:
     def range(self, k1, k2):
         return self.lsm.range(k1, k2)
 
-    def range_assemble(self, offs, block_len, P, nq, keys, vals):
-        return self.lsm.shard_range_assemble(offs, block_len, P, nq, keys, vals)
+    def piece_assemble(self, offs, block_len, chunk_counts, P, perm, pstart, nq, keys, vals):
+        return self.lsm.shard_piece_assemble(offs, block_len, chunk_counts, P, perm, pstart, nq,
+                                             keys, vals)
+
+    def gather(self, t, idx):
+        """t[idx] for a handful of host indices (the exchange's block bounds)."""
+        return self.host_list(t[torch.tensor(idx, dtype=torch.int64, device=t.device)])
 
     def order(self, q, succ):
         return self.lsm.successor(q) if succ else self.lsm.predecessor(q)
@@ -309,19 +316,24 @@ class ShardedLSM:
         bf = self._a2a(f, recv, send, torch.uint8)
         return self.backend.scatter(perm, bv, bf)
 
+    def _route(self, k1, k2):
+        """Pieces of this rank's queries, bucketed by owner and delivered:
+        (pstart, perm, chunk counts (device), send, recv, received k1, k2)."""
+        pk1, pk2, pstart = self.backend.route_ranges(k1, k2, self.P)
+        bk1, bk2, _, perm, cnt = self.backend.bucket(pk1, pk2, None, self.P, 0, True)
+        send, recv = self._exchange_counts(cnt)
+        rk1 = self._a2a(bk1, send, recv, torch.int32)
+        rk2 = self._a2a(bk2, send, recv, torch.int32)
+        return pstart, perm, cnt, send, recv, rk1, rk2
+
     def count(self, k1, k2):
-        """Counts for this rank's (k1, k2) queries; every rank passes the same
-        number of queries."""
+        """Counts for this rank's (k1, k2) queries (owner-routed pieces)."""
         self.flush()
         nq = k1.numel()
-        all1 = self.backend.empty(nq * self.P, torch.int32)
-        all2 = self.backend.empty(nq * self.P, torch.int32)
-        dist.all_gather_into_tensor(all1, k1, group=self.group)
-        dist.all_gather_into_tensor(all2, k2, group=self.group)
-        c1, c2 = self.backend.clip(all1, all2, self.lo, self.hi)
-        partial = self.backend.count(c1, c2)
-        recv = self._a2a(partial, [nq] * self.P, [nq] * self.P, torch.int32)
-        return self.backend.sum_parts(recv, self.P, nq)
+        pstart, perm, _, send, recv, rk1, rk2 = self._route(k1, k2)
+        c = self.backend.count(rk1, rk2)
+        back = self._a2a(c, recv, send, torch.int32)
+        return self.backend.piece_sum(back, perm, pstart, nq)
 
     def _order(self, q, succ):
         self.flush()
@@ -345,28 +357,26 @@ class ShardedLSM:
 
     def range(self, k1, k2):
         """Ranges for this rank's (k1, k2) queries: (offsets[nq+1], keys, vals)
-        with each query's pairs in key order; every rank passes the same number
-        of queries."""
+        with each query's pairs in key order (owner-routed pieces)."""
         self.flush()
         nq = k1.numel()
         P = self.P
-        all1 = self.backend.empty(nq * P, torch.int32)
-        all2 = self.backend.empty(nq * P, torch.int32)
-        dist.all_gather_into_tensor(all1, k1, group=self.group)
-        dist.all_gather_into_tensor(all2, k2, group=self.group)
-        c1, c2 = self.backend.clip(all1, all2, self.lo, self.hi)
-        off, rk, rv = self.backend.range(c1, c2)  # queries of origin o at [o*nq, (o+1)*nq)
-        bnd = self.backend.host_list(off[0:P * nq + 1:nq])
-        send = [bnd[o + 1] - bnd[o] for o in range(P)]
+        pstart, perm, cnt, send, recv, rk1, rk2 = self._route(k1, k2)
+        off, rk, rv = self.backend.range(rk1, rk2)  # pieces of origin o: [rb[o], rb[o+1])
+        rb = [0]
+        for c in recv:
+            rb.append(rb[-1] + c)
+        bnd = self.backend.gather(off, rb)
+        blk = [bnd[o + 1] - bnd[o] for o in range(P)]  # pairs back to each origin
         sl = self.backend.empty(P, torch.int64)
-        sl.copy_(torch.tensor(send, dtype=torch.int64))
+        sl.copy_(torch.tensor(blk, dtype=torch.int64))
         rl = self.backend.empty(P, torch.int64)
         dist.all_to_all_single(rl, sl, group=self.group)
-        recv = self.backend.host_list(rl)
-        roffs = self._a2a(off[:P * nq].contiguous(), [nq] * P, [nq] * P, torch.int64)
-        rkk = self._a2a(rk[bnd[0]:bnd[P]].contiguous(), send, recv, torch.int32)
-        rvv = self._a2a(rv[bnd[0]:bnd[P]].contiguous(), send, recv, torch.int32)
-        return self.backend.range_assemble(roffs, rl, P, nq, rkk, rvv)
+        rlist = self.backend.host_list(rl)
+        roffs = self._a2a(off[:rb[P]].contiguous(), recv, send, torch.int64)
+        rkk = self._a2a(rk[bnd[0]:bnd[P]].contiguous(), blk, rlist, torch.int32)
+        rvv = self._a2a(rv[bnd[0]:bnd[P]].contiguous(), blk, rlist, torch.int32)
+        return self.backend.piece_assemble(roffs, rl, cnt, P, perm, pstart, nq, rkk, rvv)
 
 
 def run_sharded_bench(args, dist_mod, rank, world, local_rank, clock_cls=None, peaks_fn=None):

@@ -44,7 +44,7 @@ def test_bucket_kernel_is_a_stable_partition(P, mode, n):
     assert np.array_equal(pb.cpu().numpy().astype(np.int64), perm)
 
 
-def test_scatter_clip_sum_kernels():
+def test_scatter_kernel():
     g = pkg.GpuLSM(16)
     n = 100_000
     perm = np.random.default_rng(1).permutation(n).astype(np.int32)
@@ -58,50 +58,68 @@ def test_scatter_clip_sum_kernels():
     ef = np.empty(n, np.uint8)
     ef[perm] = found
     assert np.array_equal(to_numpy_u32(vo), ev) and np.array_equal(fo.cpu().numpy(), ef)
-    k1 = synth.uniform_u32(2, 1, n)
-    k2 = synth.uniform_u32(2, 2, n)
-    lo, hi = 1 << 29, (1 << 30) - 1
-    c1, c2 = g.shard_clip(to_device(k1), to_device(k2), lo, hi)
-    a, z = k1.astype(np.int64), k2.astype(np.int64)
-    empty = (a > z) | (z < lo) | (a > hi)
-    assert np.array_equal(to_numpy_u32(c1), np.where(empty, 1, np.maximum(a, lo)).astype(np.uint32))
-    assert np.array_equal(to_numpy_u32(c2), np.where(empty, 0, np.minimum(z, hi)).astype(np.uint32))
-    parts = (synth.uniform_u32(4, 1, 3 * n) >> 8).astype(np.uint32)
-    s = g.shard_sum(to_device(parts), 3, n)
-    assert np.array_equal(to_numpy_u32(s), parts.reshape(3, n).sum(axis=0).astype(np.uint32))
 
 
-def test_range_assemble_kernel():
-    # lsm_shard_range_assemble vs a numpy definition: P = 3 shards' parts for
-    # nq queries, offsets slices in the senders' numbering, blocks in shard
-    # order; each query's pieces concatenated shard 0 first.
+def _routing_queries(n, seed):
+    # short ranges, ranges across shard boundaries, the whole query space,
+    # empty ones (k1 > k2), keys above the domain (R8)
+    k1 = synth.uniform_u32(seed, 1, n)
+    w = (synth.uniform_u32(seed, 2, n) >> np.uint32(20 + seed % 3 * 3)).astype(np.uint64)
+    k2 = np.minimum(k1.astype(np.uint64) + w, 0xFFFFFFFF).astype(np.uint32)
+    k1[::13] = 0
+    k2[::17] = 0xFFFFFFFF
+    sel = np.arange(5, n, 19)
+    sel = sel[k1[sel] > 0]
+    k2[sel] = k1[sel] - 1  # empty: k1 > k2
+    return k1, k2
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 8, 64])
+def test_route_and_piece_kernels(P):
+    # lsm_shard_route_ranges / piece_sum / piece_assemble vs the numpy
+    # stand-ins of the gloo tests' CPU backend (an independent implementation)
+    from tests.test_sharded_gloo import CpuTestBackend
+    cpu = CpuTestBackend(16)
     g = pkg.GpuLSM(16)
-    rng = np.random.default_rng(4)
-    P, nq = 3, 5000
-    cnt = rng.integers(0, 6, (P, nq))
-    cnt[:, 7] = 0  # a query with nothing anywhere
-    offs = np.zeros((P, nq), np.int64)
-    blen = cnt.sum(axis=1)
-    for s_ in range(P):
-        start = int(rng.integers(0, 1000))  # sender numbering need not start at 0
-        offs[s_] = start + np.concatenate([[0], np.cumsum(cnt[s_])[:-1]])
+    n = 3000
+    k1, k2 = _routing_queries(n, P)
+    t1 = torch.from_numpy(k1.view(np.int32).copy())
+    t2 = torch.from_numpy(k2.view(np.int32).copy())
+    pk1, pk2, pstart = g.shard_route_ranges(t1.cuda(), t2.cuda(), P)
+    ck1, ck2, cps = cpu.route_ranges(t1, t2, P)
+    assert np.array_equal(pstart.cpu().numpy(), cps.numpy())
+    assert np.array_equal(pk1.cpu().numpy(), ck1.numpy())
+    assert np.array_equal(pk2.cpu().numpy(), ck2.numpy())
+    npc = pk1.numel()
+    assert npc > n // 2
+    # pieces bucketed by owner; made-up per-piece answers from the owners
+    _, _, _, perm, cnt = g.shard_bucket(pk1, P, vals=pk2, want_perm=True)
+    rng = np.random.default_rng(P)
+    pc = rng.integers(0, 7, npc).astype(np.int32)  # answers in bucket order
+    s = g.shard_piece_sum(torch.from_numpy(pc).cuda(), perm, pstart, n)
+    es = cpu.piece_sum(torch.from_numpy(pc), perm.cpu(), cps, n)
+    assert np.array_equal(s.cpu().numpy(), es.numpy())
+    # each owner numbers its output from an arbitrary start
+    chunk = cnt.cpu().numpy().astype(np.int64)
+    cstart = np.concatenate([[0], np.cumsum(chunk)])
+    offs = np.zeros(npc, np.int64)
+    blen = np.zeros(P, np.int64)
+    for c in range(P):
+        seg = pc[cstart[c]:cstart[c + 1]].astype(np.int64)
+        if len(seg):
+            offs[cstart[c]:cstart[c + 1]] = int(rng.integers(0, 1000)) + np.concatenate(
+                [[0], np.cumsum(seg)[:-1]])
+        blen[c] = seg.sum()
     tot = int(blen.sum())
     keys = rng.integers(0, 1 << 31, tot).astype(np.uint32)
     vals = np.arange(tot, dtype=np.uint32)
-    o, k, v = g.shard_range_assemble(torch.from_numpy(offs.reshape(-1)).cuda(),
-                                     torch.from_numpy(blen.astype(np.int64)).cuda(), P, nq,
-                                     to_device(keys), to_device(vals))
-    eoff = np.concatenate([[0], np.cumsum(cnt.sum(axis=0))])
-    base = np.concatenate([[0], np.cumsum(blen)])
-    ek, ev = [], []
-    for q in range(nq):
-        for s_ in range(P):
-            src = base[s_] + offs[s_, q] - offs[s_, 0]
-            ek.append(keys[src:src + cnt[s_, q]])
-            ev.append(vals[src:src + cnt[s_, q]])
-    assert np.array_equal(o.cpu().numpy(), eoff)
-    assert np.array_equal(to_numpy_u32(k), np.concatenate(ek))
-    assert np.array_equal(to_numpy_u32(v), np.concatenate(ev))
+    args = [torch.from_numpy(offs), torch.from_numpy(blen), cnt.cpu(), P, perm.cpu(), cps, n,
+            torch.from_numpy(keys.view(np.int32)), torch.from_numpy(vals.view(np.int32))]
+    eo, ek, ev = cpu.piece_assemble(*args)
+    o, k, v = g.shard_piece_assemble(*[a.cuda() if isinstance(a, torch.Tensor) else a for a in args])
+    assert np.array_equal(o.cpu().numpy(), eo.numpy())
+    assert np.array_equal(k.cpu().numpy(), ek.numpy())
+    assert np.array_equal(v.cpu().numpy(), ev.numpy())
 
 
 def _free_port():

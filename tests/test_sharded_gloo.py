@@ -63,17 +63,64 @@ class CpuTestBackend:
         fo[perm.long()] = found
         return vo, fo
 
-    def clip(self, k1, k2, lo, hi):
+    # owner-routed count / range: numpy stand-ins of lsm_shard_route_ranges,
+    # lsm_shard_piece_sum and lsm_shard_piece_assemble
+    @staticmethod
+    def _bounds(P, o):
+        lo = -(-o * (1 << 31) // P)
+        hi = (-(-(o + 1) * (1 << 31) // P) - 1) if o + 1 < P else 0xFFFFFFFF
+        return lo, hi
+
+    def route_ranges(self, k1, k2, P):
         a = k1.numpy().view(np.uint32).astype(np.int64)
         z = k2.numpy().view(np.uint32).astype(np.int64)
-        empty = (a > z) | (z < lo) | (a > hi)
-        a2 = np.where(empty, 1, np.maximum(a, lo))
-        z2 = np.where(empty, 0, np.minimum(z, hi))
-        return (torch.from_numpy(a2.astype(np.uint32).view(np.int32)),
-                torch.from_numpy(z2.astype(np.uint32).view(np.int32)))
+        pk1, pk2, pstart = [], [], [0]
+        for x, y in zip(a, z):
+            if x <= y:
+                o1 = int(self.owner(np.array([x]), P, 0)[0])
+                o2 = int(self.owner(np.array([y]), P, 0)[0])
+                for o in range(o1, o2 + 1):
+                    lo, hi = self._bounds(P, o)
+                    pk1.append(max(x, lo))
+                    pk2.append(min(y, hi))
+            pstart.append(len(pk1))
+        t = lambda v: torch.from_numpy(np.array(v, np.int64).astype(np.uint32).view(np.int32))  # noqa: E731
+        return t(pk1), t(pk2), torch.from_numpy(np.array(pstart, np.int32))
 
-    def sum_parts(self, t, P, n):
-        return torch.from_numpy(t.numpy().reshape(P, n).sum(axis=0).astype(np.int32))
+    def piece_sum(self, counts, perm, pstart, nq):
+        pc = np.zeros(perm.numel(), np.int64)
+        pc[perm.numpy()] = counts.numpy()
+        ps = pstart.numpy()
+        return torch.from_numpy(np.array([pc[ps[q]:ps[q + 1]].sum() for q in range(nq)], np.int32))
+
+    def gather(self, t, idx):
+        return [int(t[i]) for i in idx]
+
+    def piece_assemble(self, offs, block_len, chunk_counts, P, perm, pstart, nq, keys, vals):
+        o = offs.numpy().astype(np.int64)
+        bl = block_len.numpy().astype(np.int64)
+        cc = chunk_counts.numpy().astype(np.int64)
+        cstart = np.concatenate([[0], np.cumsum(cc)])
+        bstart = np.concatenate([[0], np.cumsum(bl)])
+        npc = perm.numel()
+        pc = np.zeros(npc, np.int64)
+        src = np.zeros(npc, np.int64)
+        pm = perm.numpy()
+        for c in range(P):
+            for i in range(cstart[c], cstart[c + 1]):
+                end = o[i + 1] if i + 1 < cstart[c + 1] else o[cstart[c]] + bl[c]
+                pc[pm[i]] = end - o[i]
+                src[pm[i]] = bstart[c] + o[i] - o[cstart[c]]
+        dst = np.concatenate([[0], np.cumsum(pc)])
+        ps = pstart.numpy()
+        offsets = dst[ps].astype(np.int64)
+        kn, vn = keys.numpy(), vals.numpy()
+        ko = np.empty(int(dst[-1]), np.int32)
+        vo = np.empty(int(dst[-1]), np.int32)
+        for j in range(npc):
+            ko[dst[j]:dst[j] + pc[j]] = kn[src[j]:src[j] + pc[j]]
+            vo[dst[j]:dst[j] + pc[j]] = vn[src[j]:src[j] + pc[j]]
+        return torch.from_numpy(offsets), torch.from_numpy(ko), torch.from_numpy(vo)
 
     def clear(self):
         import oracle
@@ -145,30 +192,6 @@ class CpuTestBackend:
             fo[take] = 1
         return torch.from_numpy(ko), torch.from_numpy(vo), torch.from_numpy(fo)
 
-    def range_assemble(self, offs, block_len, P, nq, keys, vals):
-        # numpy stand-in of lsm_shard_range_assemble
-        o = offs.numpy().reshape(P, nq)
-        bl = block_len.numpy()
-        base = np.concatenate([[0], np.cumsum(bl)])
-        cnt = np.zeros((P, nq), np.int64)
-        for s_ in range(P):
-            ends = np.append(o[s_, 1:], o[s_, 0] + bl[s_])
-            cnt[s_] = ends - o[s_]
-        tot = cnt.sum(axis=0)
-        offsets = np.concatenate([[0], np.cumsum(tot)]).astype(np.int64)
-        ko = np.empty(int(offsets[-1]), np.int32)
-        vo = np.empty(int(offsets[-1]), np.int32)
-        kn, vn = keys.numpy(), vals.numpy()
-        for q in range(nq):
-            d = offsets[q]
-            for s_ in range(P):
-                src = base[s_] + o[s_, q] - o[s_, 0]
-                c = cnt[s_, q]
-                ko[d:d + c] = kn[src:src + c]
-                vo[d:d + c] = vn[src:src + c]
-                d += c
-        return torch.from_numpy(offsets), torch.from_numpy(ko), torch.from_numpy(vo)
-
 
 def _free_port():
     s = socket.socket()
@@ -205,8 +228,9 @@ def _worker(rank, world, port, scenario, out_q):
         qv, qf = sh.lookup(torch.from_numpy(q.view(np.int32).copy()))
         k1, k2 = synth.range_queries(9 + rank, 300, nbatch * b_global, 16, domain=dom)
         # ranges that straddle the shard boundary and the whole domain
-        k1 = np.concatenate([k1, np.array([0, (1 << 30) - 5, 0], np.uint32)])
-        k2 = np.concatenate([k2, np.array([0xFFFFFFFF, (1 << 30) + 5, 3], np.uint32)])
+        # (and an empty one, k1 > k2: no pieces, R9)
+        k1 = np.concatenate([k1, np.array([0, (1 << 30) - 5, 0, 9], np.uint32)])
+        k2 = np.concatenate([k2, np.array([0xFFFFFFFF, (1 << 30) + 5, 3, 4], np.uint32)])
         c = sh.count(torch.from_numpy(k1.view(np.int32).copy()), torch.from_numpy(k2.view(np.int32).copy()))
         ro, rk, rv = sh.range(torch.from_numpy(k1.view(np.int32).copy()),
                               torch.from_numpy(k2.view(np.int32).copy()))
