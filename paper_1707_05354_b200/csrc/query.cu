@@ -20,8 +20,8 @@
 // block, takes the block's global base by a decoupled look-back (the paper's
 // stage-2 scan) and walks again to write pairs sorted by key.
 // Walk variants: walk_one (one level, 8 records per step; slices past 128
-// records continued by the whole warp, warp_walk_long), walk_window (2-4
-// levels, 4-record look-ahead), walk_slices (general).
+// records continued by the whole warp, warp_walk_long), walk_flat (2-8
+// levels, record by record, one-ahead loads), walk_slices (general).
 //
 // Searches: the paper's bottleneck is "the random memory
 // accesses required in all binary searches". Every lower_bound
@@ -535,83 +535,6 @@ __device__ __forceinline__ uint32_t walk_slices(const LevelTable& T, uint64_t* p
   return cnt;
 }
 
-// The same walk for a few levels (NL <= 4) with a 4-record look-ahead window
-// of raw key variables per level: advancing a level shifts its window and
-// issues the load of the record 4 ahead, so the walk's compare chain runs on
-// registers instead of waiting one load latency per record, and the status
-// bit of a run head comes from the window (no reload). Same visiting order
-// and the same results as walk_slices (ncu: the per-record dependent loads
-// were ~40 % of the 3-level range kernel's stall samples).
-template <int NL, bool NEED_VAL, typename Emit>
-__device__ __forceinline__ uint32_t walk_window(const LevelTable& T, uint64_t* pos, uint32_t z,
-                                                Emit emit) {
-  uint32_t w0[NL], w1[NL], w2[NL], w3[NL];
-  auto ld = [&](int j, uint64_t p) -> uint32_t {
-    return p < T.n[j] ? __ldg(T.keys[j] + p) : 0xFFFFFFFFu;
-  };
-#pragma unroll
-  for (int j = 0; j < NL; ++j) {
-    const uint64_t p = pos[j];
-    w0[j] = ld(j, p);
-    w1[j] = ld(j, p + 1);
-    w2[j] = ld(j, p + 2);
-    w3[j] = ld(j, p + 3);
-#if !defined(GPULSM_NO_WALK_PREFETCH)
-    // the refills past the first 8-record sector come from L2; pull the next
-    // sector into L1 now so a refill issued 3 records ahead finds it there
-    if (p + 8 < T.n[j])
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(T.keys[j] + ((p + 8) & ~7ull)));
-#endif
-  }
-  // head of level j: its original key, or kSent past the slice (> z or >= n)
-  auto head = [&](int j) -> uint32_t {
-    const uint32_t k = w0[j] >> 1;
-    return (pos[j] < T.n[j] && k <= z) ? k : kSent;
-  };
-  uint32_t cnt = 0;
-  bool pend = false;
-  uint32_t pk = 0, pv = 0;
-  while (true) {
-    uint32_t m = kSent;
-#pragma unroll
-    for (int j = 0; j < NL; ++j) m = min(m, head(j));
-    if (m == kSent) break;
-    bool first = true, valid = false;
-    uint32_t val = 0;
-#pragma unroll
-    for (int j = 0; j < NL; ++j) {
-      if (head(j) == m) {
-        if (first) {  // newest record of key m: run head in the lowest level
-          first = false;
-          valid = (w0[j] & 1u) != 0;
-          if (NEED_VAL && valid) val = ldg_pol(T.vals[j] + pos[j], l2_policy_stream());
-        }
-        // skip this level's run of key m (stale copies): shift the window
-        do {
-          w0[j] = w1[j];
-          w1[j] = w2[j];
-          w2[j] = w3[j];
-          pos[j] += 1;
-          w3[j] = ld(j, pos[j] + 3);
-        } while (pos[j] < T.n[j] && (w0[j] >> 1) == m);
-      }
-    }
-    if (valid) {
-      if (NEED_VAL) {
-        if (pend) emit(cnt - 1, pk, pv);
-        pend = true;
-        pk = m;
-        pv = val;
-      } else {
-        emit(cnt, m, val);
-      }
-      ++cnt;
-    }
-  }
-  if (NEED_VAL && pend) emit(cnt - 1, pk, pv);
-  return cnt;
-}
-
 // The same result record by record, branch-light, for 2..8 levels whose
 // lengths fit 32 bits (walk_levels checks): per level the raw key variable of
 // the head and of the next record (loaded one step ahead) and a 32-bit
@@ -691,17 +614,13 @@ __device__ __forceinline__ bool flat_ok(const LevelTable& T, int L) {
   return ok;
 }
 
-// dispatch: the windowed walk for 2..4 levels, the plain walk otherwise
+// dispatch: the record-by-record walk for 2..8 levels of < 2^32 records, the
+// per-key walk otherwise
 template <int NL, bool NEED_VAL, typename Emit>
 __device__ __forceinline__ uint32_t walk_levels(const LevelTable& T, uint64_t* pos, uint32_t z,
                                                 int L, Emit emit) {
-#if !defined(GPULSM_WALK_OLD)
   if constexpr (NL >= 2 && NL <= 8)
     if (flat_ok(T, NL)) return walk_flat<NL, NEED_VAL>(T, pos, z, emit);
-#endif
-#if !defined(GPULSM_NO_WINDOW)
-  if constexpr (NL >= 2 && NL <= 4) return walk_window<NL, NEED_VAL>(T, pos, z, emit);
-#endif
   return walk_slices<NL, NEED_VAL>(T, pos, z, L, emit);
 }
 
@@ -783,12 +702,15 @@ __device__ __forceinline__ uint32_t walk_one(const uint32_t* __restrict__ K,
 // the first record past z or n (ballot), and valid records get their output
 // slot from a warp exclusive scan -- coalesced, streaming at HBM rates instead
 // of one thread walking the slice. g is 8-aligned (walk_one's next group);
-// prev = the original key before K[g]. Returns the valid records found; put(k,
-// key, val) receives the k-th of them (k from 0).
+// prev = the original key before K[g]; records before `start` (the slice's
+// first record, inside g's group when the warp takes a query from its start)
+// are skipped. Returns the valid records found; put(k, key, val) receives the
+// k-th of them (k from 0).
 template <bool NEED_VAL, typename Put>
 __device__ __forceinline__ uint32_t warp_walk_long(const uint32_t* __restrict__ K,
                                                    const uint32_t* __restrict__ V, uint64_t n,
-                                                   uint64_t g, uint32_t prev, uint32_t z, Put put) {
+                                                   uint64_t g, uint32_t prev, uint32_t z, Put put,
+                                                   uint64_t start = 0) {
   const uint32_t lane = lane_id();
   uint32_t added = 0;
   const uint64_t vpol = l2_policy_stream();
@@ -806,11 +728,14 @@ __device__ __forceinline__ uint32_t warp_walk_long(const uint32_t* __restrict__ 
     for (int s = 0; s < kUnr; ++s) {
       const uint64_t p0 = g + 128ull * s + 4ull * lane;
       const uint32_t kk[4] = {k4s[s].x, k4s[s].y, k4s[s].z, k4s[s].w};
-      // in-slice flags, then the first out-of-slice record of the warp
-      uint32_t in = 0;
+      // in-slice flags (records before `start` count as in: they precede the
+      // slice), then the first out-of-slice record of the warp
+      uint32_t in = 0, pre = 0;
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (p0 + i < n && (kk[i] >> 1) <= z) in |= 1u << i;
+      for (int i = 0; i < 4; ++i) {
+        if (p0 + i < start) pre |= 1u << i;
+        if (p0 + i < start || (p0 + i < n && (kk[i] >> 1) <= z)) in |= 1u << i;
+      }
       const uint32_t stop_mask = __ballot_sync(kFull, in != 0xFu);
       const uint32_t first_stop = stop_mask ? (uint32_t)(__ffs(stop_mask) - 1) : 32u;
       // records before the first out-of-slice record are in the slice
@@ -819,6 +744,7 @@ __device__ __forceinline__ uint32_t warp_walk_long(const uint32_t* __restrict__ 
       else if (lane == first_stop) live = ((in + 1u) ^ in) >> 1;  // bits below the first zero
       const uint32_t pk = __shfl_up_sync(kFull, kk[3] >> 1, 1);
       uint32_t before = lane == 0 ? prev : pk;
+      live &= ~pre;
       uint32_t valid = 0;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -1157,6 +1083,10 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) order_kernel(
 #define RB_TASKS 2
 #endif
 constexpr int kRBTasks = RB_TASKS;                // 32-query tasks per warp per block
+#ifndef RANGE_WARP_MIN
+#define RANGE_WARP_MIN 32
+#endif
+constexpr int kWarpFromStart = RANGE_WARP_MIN;    // pairs above which the warp writes a query
 constexpr int kRBQueries = kQThreads * kRBTasks;  // 1024
 
 template <int NL>
@@ -1247,15 +1177,27 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) range_block_kernel(
         }
       };
       if (NL == 1 && (reinterpret_cast<uintptr_t>(T.keys[0]) & 15) == 0) {
-        // whole warp: serial walk per lane, long slices continued together
-        uint64_t res = kNoResume;
+        // whole warp: serial walk per lane, long slices continued together;
+        // a query known (phase 1) to hold more than kWarpFromStart pairs goes
+        // to the warp from its first record (coalesced loads and stores
+        // instead of one lane's walk)
+        uint64_t res = kNoResume, st = 0;
         uint32_t rprev = 0, c0 = 0;
-        if (has) c0 = walk_one<true>(T.keys[0], T.vals[0], T.n[0], pos[0], z, put, &res, &rprev);
+        const uint32_t cq = act ? nxt - sOff[li] : 0u;
+        if (has) {
+          if (cq > (uint32_t)kWarpFromStart) {
+            res = pos[0] & ~7ull;
+            st = pos[0];
+            rprev = 0xFFFFFFFFu;
+          } else {
+            c0 = walk_one<true>(T.keys[0], T.vals[0], T.n[0], pos[0], z, put, &res, &rprev);
+          }
+        }
         uint32_t longm = __ballot_sync(kFull, res != kNoResume);
         while (longm) {
           const int l = __ffs(longm) - 1;
           longm &= longm - 1;
-          const uint64_t gl = __shfl_sync(kFull, res, l);
+          const uint64_t gl = __shfl_sync(kFull, res, l), sl = __shfl_sync(kFull, st, l);
           const uint32_t pl = __shfl_sync(kFull, rprev, l), zl = __shfl_sync(kFull, z, l);
           const uint64_t obl = __shfl_sync(kFull, ob, l) + __shfl_sync(kFull, c0, l);
           warp_walk_long<true>(T.keys[0], T.vals[0], T.n[0], gl, pl, zl,
@@ -1265,7 +1207,7 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) range_block_kernel(
                                    __stcs(keys_out + o, key);
                                    __stcs(vals_out + o, val);
                                  }
-                               });
+                               }, sl);
         }
       } else if (has) {
         walk_levels<NL, true>(T, pos, z, NL, put);

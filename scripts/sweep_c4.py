@@ -25,11 +25,17 @@ from paper_1707_05354_b200 import to_device  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--out", default=None)
 ap.add_argument("--quick", action="store_true", help="r in {96, 127} and L in {8, 128, 1024}")
+ap.add_argument("--rs", default=None, help="comma-separated r values (overrides the default set)")
+ap.add_argument("--ls", default=None, help="comma-separated L values")
 a = ap.parse_args()
 
 b = 1 << 20
 RS = [96, 127] if a.quick else [96, 112, 120, 124, 126, 127, 128]
 LS = [8, 128, 1024] if a.quick else [8, 16, 32, 64, 128, 256, 512, 1024]
+if a.rs:
+    RS = [int(x) for x in a.rs.split(",")]
+if a.ls:
+    LS = [int(x) for x in a.ls.split(",")]
 seed = synth.SEED_BASE + 3
 torch.cuda.set_device(0)
 lsm = pkg.GpuLSM(b, reserve_batches=max(RS))
