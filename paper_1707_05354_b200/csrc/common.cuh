@@ -22,7 +22,11 @@ constexpr uint32_t kFull = 0xFFFFFFFFu;
 // F3[j] = F2[32j] = K[8192j] (full key variables). A lower_bound then reads
 // F3 (shared memory), one 128-byte line of F2, one of F1 and one 32-byte
 // sector of K instead of log2(n) dependent probes.
-constexpr int kF1Step = 8;
+#ifndef F1_STEP
+#define F1_STEP 8
+#endif
+constexpr int kF1Step = F1_STEP;  // 8 or 16 (query.cu's group counts)
+static_assert(kF1Step == 8 || kF1Step == 16, "F1_STEP");
 constexpr int kFanout = 32;
 inline __host__ __device__ uint64_t idx_f1_len(uint64_t n) { return (n + kF1Step - 1) / kF1Step; }
 inline __host__ __device__ uint64_t idx_f2_len(uint64_t n) { return (idx_f1_len(n) + kFanout - 1) / kFanout; }

@@ -201,21 +201,22 @@ __device__ __forceinline__ uint32_t grp_line_count(const uint32_t* __restrict__ 
   return res;
 }
 
-// For every lane: records of the 8-record group K[8*gi ..) (within n) below
-// x. 16-byte aligned K: 2 lanes x 16 B per query, 16 queries per load;
-// otherwise 8 lanes x 4 B, 4 queries per load.
+// For every lane: records of the kF1Step-record group K[kF1Step*gi ..)
+// (within n) below x. 16-byte aligned K: kF1Step/4 lanes x 16 B per query;
+// otherwise kF1Step lanes x 4 B per query.
+constexpr uint32_t kGL = kF1Step / 4;  // lanes per query, aligned groups
 __device__ __forceinline__ uint32_t grp_group_count(const uint32_t* __restrict__ K, uint64_t n,
                                                     uint32_t gi, uint32_t x2, uint64_t strm) {
   const uint32_t lane = lane_id();
   uint32_t res = 0;
   if ((reinterpret_cast<uintptr_t>(K) & 15) == 0) {
-    const uint32_t hf = lane & 1;
+    const uint32_t e = lane & (kGL - 1);
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const uint32_t src = (lane & ~1u) | r;  // round r: lanes 2P, 2P+1 serve lane 2P+r
+    for (int r = 0; r < (int)kGL; ++r) {
+      const uint32_t src = (lane & ~(kGL - 1)) | r;  // round r: the lanes of a group serve its lane r
       const uint32_t gj = __shfl_sync(kFull, gi, src);
       const uint32_t xj = __shfl_sync(kFull, x2, src);
-      const uint64_t base = (uint64_t)gj * kF1Step + 4 * hf;
+      const uint64_t base = (uint64_t)gj * kF1Step + 4 * e;
       uint4 v = ldg_v4_pol(K + base, strm);  // +16 words of slack
       if (base + 4 > n) {  // the level's last group
         if (base + 0 >= n) v.x = 0xFFFFFFFFu;
@@ -224,21 +225,24 @@ __device__ __forceinline__ uint32_t grp_group_count(const uint32_t* __restrict__
         v.w = 0xFFFFFFFFu;
       }
       uint32_t c = (v.x < xj) + (v.y < xj) + (v.z < xj) + (v.w < xj);
-      c += __shfl_xor_sync(kFull, c, 1);
-      if (hf == (uint32_t)r) res = c;
+#pragma unroll
+      for (uint32_t o = 1; o < kGL; o <<= 1) c += __shfl_xor_sync(kFull, c, o);
+      if (e == (uint32_t)r) res = c;
     }
   } else {
-    const uint32_t sub = lane >> 3, e = lane & 7;
+    constexpr uint32_t kQPR = 32 / kF1Step;  // queries per round
+    const uint32_t sub = lane / kF1Step, e = lane % kF1Step;
+    const uint32_t seg = kF1Step == 32 ? 0xFFFFFFFFu : (1u << kF1Step) - 1u;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const uint32_t src = 4 * r + sub;
+    for (int r = 0; r < kF1Step; ++r) {
+      const uint32_t src = kQPR * r + sub;
       const uint32_t gj = __shfl_sync(kFull, gi, src);
       const uint32_t xj = __shfl_sync(kFull, x2, src);
       const uint64_t idx = (uint64_t)gj * kF1Step + e;
       const bool below = idx < n && __ldg(K + idx) < xj;
       const uint32_t m = __ballot_sync(kFull, below);
-      const uint32_t t = __popc((m >> (8 * (lane & 3))) & 0xFFu);
-      if ((lane >> 2) == (uint32_t)r) res = t;
+      const uint32_t t = __popc((m >> (kF1Step * (lane % kQPR))) & seg);
+      if (lane / kQPR == (uint32_t)r) res = t;
     }
   }
   return res;
@@ -336,13 +340,13 @@ __device__ __forceinline__ void warp_lower_bound_n(const LevelTable& T, const ui
   bool aligned = true;
 #pragma unroll
   for (int j = 0; j < NL; ++j) aligned &= (reinterpret_cast<uintptr_t>(T.keys[j]) & 15) == 0;
-  if (aligned) {  // the groups of all levels together: 2 lanes x 16 B per query
-    const uint32_t lane = lane_id(), hf = lane & 1;
+  if (aligned) {  // the groups of all levels together: kGL lanes x 16 B per query
+    const uint32_t lane = lane_id(), hf = lane & (kGL - 1);
 #pragma unroll
     for (int j = 0; j < NL; ++j) c[j] = 0;
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const uint32_t src = (lane & ~1u) | r;
+    for (int r = 0; r < (int)kGL; ++r) {
+      const uint32_t src = (lane & ~(kGL - 1)) | r;
       const uint32_t xj = __shfl_sync(kFull, x2, src);
       uint4 v[NL];
       uint64_t base[NL];
@@ -362,7 +366,8 @@ __device__ __forceinline__ void warp_lower_bound_n(const LevelTable& T, const ui
           v[j].w = 0xFFFFFFFFu;
         }
         uint32_t t = (v[j].x < xj) + (v[j].y < xj) + (v[j].z < xj) + (v[j].w < xj);
-        t += __shfl_xor_sync(kFull, t, 1);
+#pragma unroll
+        for (uint32_t o = 1; o < kGL; o <<= 1) t += __shfl_xor_sync(kFull, t, o);
         if (hf == (uint32_t)r) c[j] = t;
       }
     }
