@@ -22,6 +22,7 @@ from .brute import BruteDict  # noqa: F401
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "lsm_oracle.cpp")
+_SRCS = [_SRC, os.path.join(_HERE, "exhaustive.cpp")]
 _LIB = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
@@ -31,9 +32,10 @@ u8p = ctypes.POINTER(ctypes.c_uint8)
 
 
 def build(force: bool = False) -> str:
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB) or any(os.path.getmtime(_LIB) < os.path.getmtime(f)
+                                                 for f in _SRCS):
         subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-pthread",
-                               "-o", _LIB, _SRC])
+                               "-o", _LIB, *_SRCS])
     return _LIB
 
 
@@ -45,6 +47,8 @@ def lib():
         vp, u64 = ctypes.c_void_p, ctypes.c_uint64
         sig = {
             "o1_create": ([u64], vp), "o1_destroy": ([vp], None),
+            "oracle_exhaustive": ([ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+                                   ctypes.c_uint32], ctypes.c_int64),
             "o1_apply_batch": ([vp, u32p, u32p, u8p, u64], None),
             "o1_lookup": ([vp, u32p, u64, u32p, u8p], None),
             "o1_count": ([vp, u32p, u32p, u64, u32p], None),
@@ -356,3 +360,16 @@ class ShardedOracleDict:
 
     def __len__(self):
         return int(lib().o1mt_size(self.h))
+
+
+def exhaustive(b: int, nbatch: int, alphabet: int, threads: int = 0) -> int:
+    """Every schedule of nbatch batches of b updates over `alphabet` keys x
+    {insert, delete}: O0 (history scan) vs O1 vs S1 (oracle/exhaustive.cpp).
+    Returns the number of schedules; raises on the first disagreement."""
+    threads = threads or os.cpu_count() or 1
+    r = int(lib().oracle_exhaustive(b, nbatch, alphabet, threads))
+    if r < 0:
+        raise AssertionError(f"oracle disagreement at schedule {-r - 1} (b={b}, nbatch={nbatch}, "
+                             f"alphabet={alphabet})")
+    return r
+

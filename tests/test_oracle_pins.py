@@ -261,6 +261,20 @@ def test_o1_vs_brute_exhaustive_tiny():
         assert np.array_equal(sf2, of) and np.array_equal(sv2[sf2 == 1], ov[of == 1])
 
 
+@pytest.mark.parametrize("b,nbatch,alphabet", [(4, 2, 3), (2, 3, 3), (1, 6, 3), (3, 3, 2)])
+def test_oracle_exhaustive_schedules(b, nbatch, alphabet):
+    # EVERY schedule of nbatch batches of b updates over
+    # `alphabet` keys x {insert, delete} ((2A)^(b*nbatch): 6^8 = 1,679,616 for
+    # b = 4 and two batches) through three implementations sharing no logic --
+    # O0, a literal history scan of the batch rules, O1 and
+    # S1 -- compared on lookups after every batch, count / range of every
+    # interval and successor / predecessor after the last, and lookups after
+    # cleanup (oracle/exhaustive.cpp). A mutant O0 (last insert wins instead of
+    # the first, R4) fails at schedule 0.
+    n = oracle.exhaustive(b, nbatch, alphabet)
+    assert n == (2 * alphabet) ** (b * nbatch)
+
+
 @pytest.mark.parametrize("seed", range(6))
 def test_random_schedules_with_brute(seed):
     _random_schedule_check(b=4, nbatch=12, alphabet=10, seed=seed, frac4=2, brute=True)
