@@ -267,6 +267,54 @@ def test_long_ranges_multi_level(r, alphabet):
         assert_queries_equal(g, o1, q, k1, k2, f"r={r} long ranges L={L}")
 
 
+def _tiny_schedules(b, nbatch, A, sample=None, seed=0):
+    import itertools
+    C = 2 * A
+    total = C ** (b * nbatch)
+    idx = range(total) if sample is None else np.random.default_rng(seed).choice(total, sample,
+                                                                                 replace=False)
+    for i in idx:
+        x = int(i)
+        digits = []
+        for _ in range(b * nbatch):
+            digits.append(x % C)
+            x //= C
+        yield digits
+
+
+@pytest.mark.parametrize("b,nbatch,sample", [(2, 2, None), (4, 2, 1500), (2, 3, 1500), (1, 5, 800)])
+def test_tiny_schedules_exhaustive_vs_o1(b, nbatch, sample):
+    # every (or a seeded sample of the) schedule(s) of nbatch batches of b
+    # updates over 3 keys x {insert, delete} (the shapes of the oracle's
+    # exhaustive pins): levels bit-exact vs S1, and lookups of every key,
+    # count / range of every interval vs O1 (one handle, cleared per schedule)
+    A = 3
+    g = GpuAdapter(b)
+    q = np.arange(A + 1, dtype=np.uint32)
+    k1 = np.array([a for a in range(A + 1) for z in range(a, A + 1)] + [2], np.uint32)
+    k2 = np.array([z for a in range(A + 1) for z in range(a, A + 1)] + [1], np.uint32)
+    for digits in _tiny_schedules(b, nbatch, A, sample, seed=b * 10 + nbatch):
+        g.lsm.clear()
+        s1 = oracle.ShadowLSM(b)
+        o1 = oracle.OracleDict(b)
+        for j in range(nbatch):
+            part = digits[j * b:(j + 1) * b]
+            keys = np.array([c // 2 for c in part], np.uint32)
+            dels = np.array([c % 2 for c in part], np.uint8)
+            vals = np.arange(j * b + 1, (j + 1) * b + 1, dtype=np.uint32)
+            g.update(keys, vals, dels)
+            s1.update(keys, vals, dels)
+            o1.apply_batch(keys, vals, dels)
+        assert_levels_equal(g, s1, f"schedule {digits}")
+        gv, gf = g.lookup(q)
+        ov, of = o1.lookup(q)
+        assert np.array_equal(gf, of) and np.array_equal(gv[gf == 1], ov[of == 1]), digits
+        assert np.array_equal(g.count(k1, k2), o1.count(k1, k2)), digits
+        goff, gk, gvv = g.range(k1, k2)
+        ooff, ok, ovv = o1.range(k1, k2)
+        assert np.array_equal(goff, ooff) and np.array_equal(gk, ok) and np.array_equal(gvv, ovv), digits
+
+
 def test_one_wave_boundary_sort():
     # exactly 148 tiles (largest one-wave batch) and one record more
     for b in (148 * 7168, 148 * 7168 + 1):
