@@ -362,15 +362,22 @@ lsm_status lsm_shard_piece_assemble(lsm_t* h, const uint64_t* d_offs, const uint
                                     uint32_t* d_keys_out, uint32_t* d_vals_out, uint64_t capacity,
                                     uint64_t* total_out, void* stream);
 
-/* Successor / predecessor across shards (R23): d_keys,
- * d_vals, d_found hold `parts` shards' local answers for the same n queries
- * ([part][n], shard order = ascending key intervals). Per query: the first
- * shard with an answer (last = 0: successor) or the last one (last = 1:
- * predecessor); ⊥ (LSM_NOT_FOUND, found 0) if none. d_found_out may be NULL. */
-lsm_status lsm_shard_pick(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals,
-                          const uint8_t* d_found, uint32_t parts, uint64_t n, int last,
-                          uint32_t* d_keys_out, uint32_t* d_vals_out, uint8_t* d_found_out,
-                          void* stream);
+/* Successor / predecessor, owner-routed (R23): each query went
+ * to the shard owning its key (lsm_shard_bucket, permutation d_perm: bucket
+ * slot i -> query index; the slots [c_0 + .. + c_{o-1}, + c_o) went to shard o,
+ * c = d_chunk_counts[nshards]) and came back with that shard's local answer
+ * (d_keys / d_vals / d_found, bucket order). d_ext_* hold every shard's
+ * extreme live key: its smallest (last = 0, successor) or its largest
+ * (last = 1, predecessor), found = 0 for an empty shard. A query its owner
+ * could not answer takes the extreme of the first later (successor) or last
+ * earlier (predecessor) shard that has one, else ⊥ (LSM_NOT_FOUND, found 0).
+ * Writes the answers in query order; d_found_out may be NULL.             */
+lsm_status lsm_shard_order_resolve(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals,
+                                   const uint8_t* d_found, const uint32_t* d_chunk_counts,
+                                   const uint32_t* d_ext_keys, const uint32_t* d_ext_vals,
+                                   const uint8_t* d_ext_found, uint32_t nshards, int last,
+                                   const uint32_t* d_perm, uint64_t n, uint32_t* d_keys_out,
+                                   uint32_t* d_vals_out, uint8_t* d_found_out, void* stream);
 
 /* ------------------------------------------------------------------------ */
 /* Introspection                                                             */

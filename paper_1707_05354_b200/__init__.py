@@ -82,8 +82,8 @@ SIGNATURES = {
     "lsm_shard_piece_sum": ([_vp, _vp, _vp, _vp, _u64, _u64, _vp, _vp], _st),
     "lsm_shard_piece_assemble": ([_vp, _vp, _vp, _vp, ctypes.c_uint32, _vp, _vp, _u64, _u64, _vp,
                                   _vp, _vp, _vp, _vp, _u64, ctypes.POINTER(_u64), _vp], _st),
-    "lsm_shard_pick": ([_vp, _vp, _vp, _vp, ctypes.c_uint32, _u64, ctypes.c_int, _vp, _vp, _vp,
-                        _vp], _st),
+    "lsm_shard_order_resolve": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_uint32,
+                                 ctypes.c_int, _vp, _u64, _vp, _vp, _vp, _vp], _st),
 }
 
 
@@ -495,17 +495,21 @@ class GpuLSM:
                                                   _stream_ptr(stream)), "lsm_shard_bucket_records")
         return rec, cnt
 
-    def shard_pick(self, keys, vals, found, parts, n, last, stream=None):
-        """First (last=False) / last (last=True) shard answer per query."""
+    def shard_order_resolve(self, keys, vals, found, chunk_counts, ext_keys, ext_vals,
+                            ext_found, nshards, last, perm, stream=None):
+        """Owner-routed successor (last=False) / predecessor (last=True) answers in
+        query order (see lsm_shard_order_resolve)."""
         torch = _torch()
-        ko = torch.empty(n, dtype=torch.int32, device=keys.device)
-        vo = torch.empty(n, dtype=torch.int32, device=keys.device)
-        fo = torch.empty(n, dtype=torch.uint8, device=keys.device)
-        _check(self._lib.lsm_shard_pick(self.h, _dev(keys, 4, "keys"), _dev(vals, 4, "vals"),
-                                        _dev(found, 1, "found"), int(parts), int(n), int(bool(last)),
-                                        _dev(ko, 4, "keys_out"), _dev(vo, 4, "vals_out"),
-                                        _dev(fo, 1, "found_out"), _stream_ptr(stream)),
-               "lsm_shard_pick")
+        n = perm.numel()
+        ko = torch.empty(n, dtype=torch.int32, device=perm.device)
+        vo = torch.empty(n, dtype=torch.int32, device=perm.device)
+        fo = torch.empty(n, dtype=torch.uint8, device=perm.device)
+        _check(self._lib.lsm_shard_order_resolve(
+            self.h, _dev(keys, 4, "keys"), _dev(vals, 4, "vals"), _dev(found, 1, "found"),
+            _dev(chunk_counts, 4, "chunk_counts"), _dev(ext_keys, 4, "ext_keys"),
+            _dev(ext_vals, 4, "ext_vals"), _dev(ext_found, 1, "ext_found"), int(nshards),
+            int(bool(last)), _dev(perm, 4, "perm"), n, _dev(ko), _dev(vo), _dev(fo, 1),
+            _stream_ptr(stream)), "lsm_shard_order_resolve")
         return ko, vo, fo
 
     def shard_scatter(self, perm, vals_in, found_in, vals_out, found_out, stream=None):

@@ -429,9 +429,11 @@ cudaError_t launch_piece_assemble(const uint64_t* offs, const uint64_t* blen,
                                   const uint32_t* kin, const uint32_t* vin, uint64_t* offsets,
                                   uint32_t* kout, uint32_t* vout, uint64_t capacity,
                                   uint64_t* scratch, cudaStream_t s, const LaunchHooks& hk);
-cudaError_t launch_pick(const uint32_t* kin, const uint32_t* vin, const uint8_t* fin,
-                        uint32_t parts, uint64_t n, int last, uint32_t* kout, uint32_t* vout,
-                        uint8_t* fout, cudaStream_t s, const LaunchHooks& hk);
+cudaError_t launch_order_resolve(const uint32_t* kin, const uint32_t* vin, const uint8_t* fin,
+                                const uint32_t* chunk_cnt, const uint32_t* ek, const uint32_t* ev,
+                                const uint8_t* ef, uint32_t P, int last, const uint32_t* perm,
+                                uint64_t n, uint32_t* kout, uint32_t* vout, uint8_t* fout,
+                                cudaStream_t s, const LaunchHooks& hk);
 
 
 cudaError_t launch_fill_placebo(uint32_t* ck, uint32_t* cv, uint64_t from, uint64_t to,

@@ -1318,16 +1318,21 @@ lsm_status lsm_shard_piece_assemble(lsm_t* h, const uint64_t* d_offs, const uint
   return total > capacity ? LSM_ERR_CAPACITY : LSM_OK;
 }
 
-lsm_status lsm_shard_pick(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals,
-                          const uint8_t* d_found, uint32_t parts, uint64_t n, int last,
-                          uint32_t* d_keys_out, uint32_t* d_vals_out, uint8_t* d_found_out,
-                          void* stream) {
-  if (!h || parts == 0) return LSM_ERR_INVALID_ARG;
+lsm_status lsm_shard_order_resolve(lsm_t* h, const uint32_t* d_keys, const uint32_t* d_vals,
+                                   const uint8_t* d_found, const uint32_t* d_chunk_counts,
+                                   const uint32_t* d_ext_keys, const uint32_t* d_ext_vals,
+                                   const uint8_t* d_ext_found, uint32_t nshards, int last,
+                                   const uint32_t* d_perm, uint64_t n, uint32_t* d_keys_out,
+                                   uint32_t* d_vals_out, uint8_t* d_found_out, void* stream) {
+  if (!h || nshards == 0 || nshards > 64) return LSM_ERR_INVALID_ARG;
   ENTER(h);
   if (n == 0) return LSM_OK;
-  if (!d_keys || !d_vals || !d_found || !d_keys_out || !d_vals_out) return LSM_ERR_INVALID_ARG;
-  CK(launch_pick(d_keys, d_vals, d_found, parts, n, last, d_keys_out, d_vals_out, d_found_out,
-                 S(stream), hooks(h)));
+  if (!d_keys || !d_vals || !d_found || !d_chunk_counts || !d_ext_keys || !d_ext_vals ||
+      !d_ext_found || !d_perm || !d_keys_out || !d_vals_out)
+    return LSM_ERR_INVALID_ARG;
+  CK(launch_order_resolve(d_keys, d_vals, d_found, d_chunk_counts, d_ext_keys, d_ext_vals,
+                          d_ext_found, nshards, last, d_perm, n, d_keys_out, d_vals_out,
+                          d_found_out, S(stream), hooks(h)));
   return LSM_OK;
 }
 

@@ -182,29 +182,63 @@ __global__ void scatter_back_kernel(const uint32_t* __restrict__ perm,
   }
 }
 
-// successor / predecessor across shards: the answer is the first shard (in
-// shard = key order) with an answer for a successor, the last one for a
-// predecessor (shards own ascending key intervals)
-__global__ void pick_kernel(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
-                            const uint8_t* __restrict__ fin, uint32_t parts, uint64_t n, int last,
-                            uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
-                            uint8_t* __restrict__ fout) {
+// successor / predecessor, owner-routed: bucket slot i (in
+// owner chunk c) holds owner c's local answer for its query; a query its
+// owner cannot answer takes the extreme live key of the next shard that has
+// one -- the smallest of the first later shard for a successor, the largest
+// of the last earlier shard for a predecessor (shards own ascending key
+// intervals, so every key there is above / below the query). Answers go to
+// the query's slot perm[i].
+__global__ void order_resolve_kernel(const uint32_t* __restrict__ kin,
+                                     const uint32_t* __restrict__ vin,
+                                     const uint8_t* __restrict__ fin,
+                                     const uint32_t* __restrict__ chunk_cnt,
+                                     const uint32_t* __restrict__ ek, const uint32_t* __restrict__ ev,
+                                     const uint8_t* __restrict__ ef, uint32_t P, int last,
+                                     const uint32_t* __restrict__ perm, uint64_t n,
+                                     uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
+                                     uint8_t* __restrict__ fout) {
+  __shared__ uint64_t cstart[kMaxShards + 1];
+  if (threadIdx.x == 0) {
+    uint64_t c = 0;
+    for (uint32_t o = 0; o < P; ++o) {
+      cstart[o] = c;
+      c += chunk_cnt[o];
+    }
+    cstart[P] = c;
+  }
+  __syncthreads();
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t c = 0;
+    while (c + 1 < P && i >= cstart[c + 1]) ++c;
     uint32_t k = 0xFFFFFFFFu, v = 0xFFFFFFFFu;
     uint8_t f = 0;
-    for (uint32_t p = 0; p < parts; ++p) {
-      const uint32_t s = last ? parts - 1 - p : p;
-      if (fin[(uint64_t)s * n + i]) {
-        k = kin[(uint64_t)s * n + i];
-        v = vin[(uint64_t)s * n + i];
-        f = 1;
-        break;
-      }
+    if (fin[i]) {
+      k = kin[i];
+      v = vin[i];
+      f = 1;
+    } else if (!last) {
+      for (uint32_t t = c + 1; t < P; ++t)
+        if (ef[t]) {
+          k = ek[t];
+          v = ev[t];
+          f = 1;
+          break;
+        }
+    } else {
+      for (uint32_t t = c; t-- > 0;)
+        if (ef[t]) {
+          k = ek[t];
+          v = ev[t];
+          f = 1;
+          break;
+        }
     }
-    kout[i] = k;
-    vout[i] = v;
-    if (fout) fout[i] = f;
+    const uint32_t d = __ldg(perm + i);
+    kout[d] = k;
+    vout[d] = v;
+    if (fout) fout[d] = f;
   }
 }
 
@@ -381,13 +415,16 @@ cudaError_t launch_scatter_back(const uint32_t* perm, const uint32_t* vin, const
 
 
 
-cudaError_t launch_pick(const uint32_t* kin, const uint32_t* vin, const uint8_t* fin,
-                        uint32_t parts, uint64_t n, int last, uint32_t* kout, uint32_t* vout,
-                        uint8_t* fout, cudaStream_t s, const LaunchHooks& hk) {
+cudaError_t launch_order_resolve(const uint32_t* kin, const uint32_t* vin, const uint8_t* fin,
+                                const uint32_t* chunk_cnt, const uint32_t* ek, const uint32_t* ev,
+                                const uint8_t* ef, uint32_t P, int last, const uint32_t* perm,
+                                uint64_t n, uint32_t* kout, uint32_t* vout, uint8_t* fout,
+                                cudaStream_t s, const LaunchHooks& hk) {
   const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, 148 * 8));
   hk.begin(hk.ctx, LSM_K_OTHER, s);
-  pick_kernel<<<g, 256, 0, s>>>(kin, vin, fin, parts, n, last, kout, vout, fout);
-  hk.end(hk.ctx, LSM_K_OTHER, (double)n * (9.0 * parts + 9.0), s, 1);
+  order_resolve_kernel<<<g, 256, 0, s>>>(kin, vin, fin, chunk_cnt, ek, ev, ef, P, last, perm, n,
+                                         kout, vout, fout);
+  hk.end(hk.ctx, LSM_K_OTHER, (double)n * 22.0, s, 1);
   return cudaGetLastError();
 }
 

@@ -35,10 +35,12 @@ and lsm_shard_piece_assemble writes each query's pieces one after another in
 shard order -- key order, since shards own ascending key intervals. Every
 rank handles only the pieces it owns: O(nq) work per rank, not O(P nq).
 
-Successor / predecessor: all-gather the queries, every shard answers all of
-them locally (its keys lie in its own interval, so no clipping), the answers
-go back to the origins and lsm_shard_pick keeps the first shard's answer
-(successor) or the last one's (predecessor).
+Successor / predecessor are routed by owner too: each query goes to the shard
+owning its key and is answered there; every shard also publishes its extreme
+live key (its smallest for successors, its largest for predecessors; one
+all-gather of P entries), and lsm_shard_order_resolve gives a query its owner
+could not answer the extreme of the first later (successor) or last earlier
+(predecessor) shard that has one -- shards own ascending key intervals.
 
 All data-path arithmetic runs in libgpulsm kernels; torch.distributed only
 moves bytes. The backend is pluggable so the routing logic can be tested on
@@ -141,8 +143,12 @@ class GpuShardBackend:
     def order(self, q, succ):
         return self.lsm.successor(q) if succ else self.lsm.predecessor(q)
 
-    def pick(self, k, v, f, P, n, last):
-        return self.lsm.shard_pick(k, v, f, P, n, last)
+    def order_resolve(self, k, v, f, chunk_counts, ek, ev, ef, P, last, perm):
+        return self.lsm.shard_order_resolve(k, v, f, chunk_counts, ek, ev, ef, P, last, perm)
+
+    def extreme_probe(self, succ):
+        """The one query whose local answer is this shard's extreme live key."""
+        return torch.tensor([0 if succ else -1], dtype=torch.int32, device=self.device)
 
 
 class _DoneEvent:
@@ -337,15 +343,23 @@ class ShardedLSM:
 
     def _order(self, q, succ):
         self.flush()
-        nq = q.numel()
         P = self.P
-        allq = self.backend.empty(nq * P, torch.int32)
-        dist.all_gather_into_tensor(allq, q, group=self.group)
-        k, v, f = self.backend.order(allq, succ)  # local answers: keys of this shard only
-        rk = self._a2a(k, [nq] * P, [nq] * P, torch.int32)
-        rv = self._a2a(v, [nq] * P, [nq] * P, torch.int32)
-        rf = self._a2a(f, [nq] * P, [nq] * P, torch.uint8)
-        return self.backend.pick(rk, rv, rf, P, nq, not succ)
+        k, _, _, perm, cnt = self.backend.bucket(q, None, None, P, 0, True)
+        send, recv = self._exchange_counts(cnt)
+        rq = self._a2a(k, send, recv, torch.int32)
+        lk, lv, lf = self.backend.order(rq, succ)  # answers inside the owner's interval
+        bk = self._a2a(lk, recv, send, torch.int32)
+        bv = self._a2a(lv, recv, send, torch.int32)
+        bf = self._a2a(lf, recv, send, torch.uint8)
+        # every shard's smallest (successor) / largest (predecessor) live key
+        ek, ev, ef = self.backend.order(self.backend.extreme_probe(succ), succ)
+        ak = self.backend.empty(P, torch.int32)
+        av = self.backend.empty(P, torch.int32)
+        af = self.backend.empty(P, torch.uint8)
+        dist.all_gather_into_tensor(ak, ek, group=self.group)
+        dist.all_gather_into_tensor(av, ev, group=self.group)
+        dist.all_gather_into_tensor(af, ef, group=self.group)
+        return self.backend.order_resolve(bk, bv, bf, cnt, ak, av, af, P, not succ, perm)
 
     def successor(self, q):
         """Smallest live key >= q per query (R23): (keys, vals, found)."""

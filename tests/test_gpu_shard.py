@@ -122,6 +122,32 @@ def test_route_and_piece_kernels(P):
     assert np.array_equal(v.cpu().numpy(), ev.numpy())
 
 
+@pytest.mark.parametrize("P", [1, 3, 8])
+def test_order_resolve_kernel(P):
+    # lsm_shard_order_resolve vs the numpy stand-in of the gloo tests: owners'
+    # local answers in bucket order, empty shards, queries no shard can answer
+    from tests.test_sharded_gloo import CpuTestBackend
+    cpu = CpuTestBackend(16)
+    g = pkg.GpuLSM(16)
+    rng = np.random.default_rng(P)
+    n = 5000
+    chunk = rng.multinomial(n, [1.0 / P] * P).astype(np.int32)
+    k = rng.integers(0, 1 << 31, n).astype(np.int32)
+    v = rng.integers(0, 1 << 31, n).astype(np.int32)
+    f = (rng.random(n) < 0.6).astype(np.uint8)
+    ek = rng.integers(0, 1 << 31, P).astype(np.int32)
+    ev = rng.integers(0, 1 << 31, P).astype(np.int32)
+    ef = (rng.random(P) < 0.5).astype(np.uint8)
+    perm = rng.permutation(n).astype(np.int32)
+    for last in (False, True):
+        args = [torch.from_numpy(x) for x in (k, v, f, chunk, ek, ev, ef)] + [P, last,
+                                                                         torch.from_numpy(perm)]
+        eo = cpu.order_resolve(*args)
+        go = g.shard_order_resolve(*[a.cuda() if isinstance(a, torch.Tensor) else a for a in args])
+        for x, y in zip(go, eo):
+            assert np.array_equal(x.cpu().numpy(), y.numpy()), (P, last)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))

@@ -178,6 +178,148 @@ class CpuTestBackend:
         return (torch.from_numpy(k.view(np.int32).copy()), torch.from_numpy(v.view(np.int32).copy()),
                 torch.from_numpy(f.copy()))
 
+    # owner-routed successor / predecessor: numpy stand-in of
+    # lsm_shard_order_resolve
+    def extreme_probe(self, succ):
+        return torch.tensor([0 if succ else -1], dtype=torch.int32)
+
+    def order_resolve(self, k, v, f, chunk_counts, ek, ev, ef, P, last, perm):
+        n = perm.numel()
+        cc = np.concatenate([[0], np.cumsum(chunk_counts.numpy().astype(np.int64))])
+        kk, vv, ff = k.numpy(), v.numpy(), f.numpy()
+        ekn, evn, efn = ek.numpy(), ev.numpy(), ef.numpy()
+        ko = np.full(n, -1, np.int32)
+        vo = np.full(n, -1, np.int32)
+        fo = np.zeros(n, np.uint8)
+        pm = perm.numpy()
+        for c in range(P):
+            for i in range(cc[c], cc[c + 1]):
+                d = pm[i]
+                if ff[i]:
+                    ko[d], vo[d], fo[d] = kk[i], vv[i], 1
+                    continue
+                order = range(c - 1, -1, -1) if last else range(c + 1, P)
+                for t in order:
+                    if efn[t]:
+                        ko[d], vo[d], fo[d] = ekn[t], evn[t], 1
+                        break
+        return torch.from_numpy(ko), torch.from_numpy(vo), torch.from_numpy(fo)
+
+    # owner-routed count / range: numpy stand-ins of lsm_shard_route_ranges,
+    # lsm_shard_piece_sum and lsm_shard_piece_assemble
+    @staticmethod
+    def _bounds(P, o):
+        lo = -(-o * (1 << 31) // P)
+        hi = (-(-(o + 1) * (1 << 31) // P) - 1) if o + 1 < P else 0xFFFFFFFF
+        return lo, hi
+
+    def route_ranges(self, k1, k2, P):
+        a = k1.numpy().view(np.uint32).astype(np.int64)
+        z = k2.numpy().view(np.uint32).astype(np.int64)
+        pk1, pk2, pstart = [], [], [0]
+        for x, y in zip(a, z):
+            if x <= y:
+                o1 = int(self.owner(np.array([x]), P, 0)[0])
+                o2 = int(self.owner(np.array([y]), P, 0)[0])
+                for o in range(o1, o2 + 1):
+                    lo, hi = self._bounds(P, o)
+                    pk1.append(max(x, lo))
+                    pk2.append(min(y, hi))
+            pstart.append(len(pk1))
+        t = lambda v: torch.from_numpy(np.array(v, np.int64).astype(np.uint32).view(np.int32))  # noqa: E731
+        return t(pk1), t(pk2), torch.from_numpy(np.array(pstart, np.int32))
+
+    def piece_sum(self, counts, perm, pstart, nq):
+        pc = np.zeros(perm.numel(), np.int64)
+        pc[perm.numpy()] = counts.numpy()
+        ps = pstart.numpy()
+        return torch.from_numpy(np.array([pc[ps[q]:ps[q + 1]].sum() for q in range(nq)], np.int32))
+
+    def gather(self, t, idx):
+        return [int(t[i]) for i in idx]
+
+    def piece_assemble(self, offs, block_len, chunk_counts, P, perm, pstart, nq, keys, vals):
+        o = offs.numpy().astype(np.int64)
+        bl = block_len.numpy().astype(np.int64)
+        cc = chunk_counts.numpy().astype(np.int64)
+        cstart = np.concatenate([[0], np.cumsum(cc)])
+        bstart = np.concatenate([[0], np.cumsum(bl)])
+        npc = perm.numel()
+        pc = np.zeros(npc, np.int64)
+        src = np.zeros(npc, np.int64)
+        pm = perm.numpy()
+        for c in range(P):
+            for i in range(cstart[c], cstart[c + 1]):
+                end = o[i + 1] if i + 1 < cstart[c + 1] else o[cstart[c]] + bl[c]
+                pc[pm[i]] = end - o[i]
+                src[pm[i]] = bstart[c] + o[i] - o[cstart[c]]
+        dst = np.concatenate([[0], np.cumsum(pc)])
+        ps = pstart.numpy()
+        offsets = dst[ps].astype(np.int64)
+        kn, vn = keys.numpy(), vals.numpy()
+        ko = np.empty(int(dst[-1]), np.int32)
+        vo = np.empty(int(dst[-1]), np.int32)
+        for j in range(npc):
+            ko[dst[j]:dst[j] + pc[j]] = kn[src[j]:src[j] + pc[j]]
+            vo[dst[j]:dst[j] + pc[j]] = vn[src[j]:src[j] + pc[j]]
+        return torch.from_numpy(offsets), torch.from_numpy(ko), torch.from_numpy(vo)
+
+    def clear(self):
+        import oracle
+        self.store = oracle.OracleDict(self.b_local)
+
+    def update(self, k, v, o):
+        assert k.numel() <= self.b_local
+        self.batch_sizes.append(k.numel())
+        self.store.apply_batch(k.numpy().view(np.uint32), v.numpy().view(np.uint32), o.numpy())
+
+    # encoded records (key variable << 1 | regular, value): the GPU router's format
+    def bucket_records(self, keys, vals, ops, P, out=None, counts=None):
+        n = keys.numel()
+        v = vals if vals is not None else torch.zeros(n, dtype=torch.int32)
+        o = ops if ops is not None else torch.zeros(n, dtype=torch.uint8)
+        kb, vb, ob, _, cnt = self.bucket(keys, v, o, P, 0, False)
+        k = kb.numpy().view(np.uint32).astype(np.uint64)
+        dele = ob.numpy() != 0
+        bad = k > 0x7FFFFFFE
+        kv = np.where(bad, 0xFFFFFFFE, (k << np.uint64(1)) | np.where(dele, 0, 1).astype(np.uint64))
+        vv = np.where(dele | bad, 0, vb.numpy().view(np.uint32))
+        rec = np.stack([kv.astype(np.uint32), vv.astype(np.uint32)], axis=1).view(np.int32)
+        return torch.from_numpy(np.ascontiguousarray(rec)), cnt
+
+    def update_records(self, rec):
+        r = rec.numpy().view(np.uint32)
+        kv, vv = r[:, 0], r[:, 1]
+        self.update(torch.from_numpy((kv >> 1).view(np.int32).copy()),
+                    torch.from_numpy(vv.view(np.int32).copy()),
+                    torch.from_numpy(((kv & 1) == 0).astype(np.uint8)))
+
+    def split_records(self, rec, nparts):
+        r = rec.numpy().view(np.uint32)
+        o = self.owner(r[:, 0] >> 1, nparts, 1)
+        perm = np.argsort(o, kind="stable")
+        counts = np.bincount(o, minlength=nparts).astype(np.int32)
+        return torch.from_numpy(np.ascontiguousarray(r[perm]).view(np.int32)), torch.from_numpy(counts)
+
+    def lookup(self, q):
+        v, f = self.store.lookup(q.numpy().view(np.uint32))
+        return torch.from_numpy(v.view(np.int32).copy()), torch.from_numpy(f.copy())
+
+    def count(self, k1, k2):
+        c = self.store.count(k1.numpy().view(np.uint32), k2.numpy().view(np.uint32))
+        return torch.from_numpy(c.view(np.int32).copy())
+
+    def range(self, k1, k2):
+        off, k, v = self.store.range(k1.numpy().view(np.uint32), k2.numpy().view(np.uint32))
+        return (torch.from_numpy(off.astype(np.int64)), torch.from_numpy(k.view(np.int32).copy()),
+                torch.from_numpy(v.view(np.int32).copy()))
+
+    def order(self, q, succ):
+        fn = self.store.successor if succ else self.store.predecessor
+        k, v, f = fn(q.numpy().view(np.uint32))
+        return (torch.from_numpy(k.view(np.int32).copy()), torch.from_numpy(v.view(np.int32).copy()),
+                torch.from_numpy(f.copy()))
+
     def pick(self, k, v, f, P, n, last):
         kk = k.numpy().reshape(P, n)
         vv = v.numpy().reshape(P, n)
