@@ -540,10 +540,13 @@ __device__ __forceinline__ uint32_t walk_slices(const LevelTable& T, uint64_t* p
   return cnt;
 }
 
+#ifndef WALK_AHEAD2
+#define WALK_AHEAD2 1
+#endif
 // The same result record by record, branch-light, for 2..8 levels whose
 // lengths fit 32 bits (walk_levels checks): per level the raw key variable of
-// the head and of the next record (loaded one step ahead) and a 32-bit
-// index. A step takes the smallest head key m, reads the status of the newest
+// the head and of the next two records (loads issued two advances ahead;
+// WALK_AHEAD2=0: one) and a 32-bit index. A step takes the smallest head key m, reads the status of the newest
 // level holding m (the run head of m there) if m is
 // a new key, and advances every level whose head has key m by ONE record;
 // the rest of a level's run of m comes up in later steps as the same key and
@@ -558,6 +561,9 @@ __device__ __forceinline__ uint32_t walk_flat(const LevelTable& T, const uint64_
   // a stored key variable v is in the slice iff v <= zlim (and v < placebo)
   const uint32_t zlim = z >= 0x7FFFFFFFu ? 0xFFFFFFFDu : 2u * z + 1u;
   uint32_t h[NL], nx[NL], p[NL];
+#if WALK_AHEAD2
+  uint32_t nx2[NL];
+#endif
   auto ld = [&](int j, uint32_t q) -> uint32_t {
     const uint32_t v = q < (uint32_t)T.n[j] ? __ldg(T.keys[j] + q) : kSentRaw;
     return v <= zlim ? v : kSentRaw;
@@ -567,6 +573,9 @@ __device__ __forceinline__ uint32_t walk_flat(const LevelTable& T, const uint64_
     p[j] = (uint32_t)pos[j];
     h[j] = ld(j, p[j]);
     nx[j] = ld(j, p[j] + 1);
+#if WALK_AHEAD2
+    nx2[j] = ld(j, p[j] + 2);
+#endif
   }
   uint32_t cnt = 0, prev = 0xFFFFFFFFu;
   bool pend = false;
@@ -605,7 +614,12 @@ __device__ __forceinline__ uint32_t walk_flat(const LevelTable& T, const uint64_
       if ((h[j] >> 1) == m) {
         h[j] = nx[j];
         ++p[j];
+#if WALK_AHEAD2
+        nx[j] = nx2[j];
+        nx2[j] = nx2[j] == kSentRaw ? kSentRaw : ld(j, p[j] + 2);
+#else
         nx[j] = nx[j] == kSentRaw ? kSentRaw : ld(j, p[j] + 1);
+#endif
       }
   }
   if (NEED_VAL && pend) emit(cnt - 1, pk, pv);
