@@ -133,6 +133,45 @@ __device__ __forceinline__ void consumers_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
 }
 
+#ifndef MERGE_GUESS
+#define MERGE_GUESS 1
+#endif
+// One round of the merge-path search probed around a GUESS of the split
+// instead of across [lo, hi]: for runs drawn from similar key distributions
+// the split of diagonal d lies near d * na / (na + nb), within a few sqrt(d);
+// 32 probes w apart (w ~ sqrt(d) / 8) bracket it and leave a span of w, or --
+// the guess missed -- still cut [lo, hi] at the window's edge. The predicate
+// is monotone, so the result is exact either way; only the number of
+// dependent rounds changes.
+__device__ __forceinline__ void merge_path_guess(const uint32_t* __restrict__ ak,
+                                                 const uint32_t* __restrict__ bk, uint64_t d,
+                                                 uint64_t na, uint64_t nb, uint64_t& lo,
+                                                 uint64_t& hi) {
+#if MERGE_GUESS
+  if (hi - lo <= 4096) return;
+  const uint32_t lane = lane_id();
+  const double fr = (double)na / (double)(na + nb);
+  const uint64_t g = (uint64_t)((double)d * fr);
+  const uint64_t w0 = (uint64_t)(sqrt((double)d) * 0.125);
+  const uint64_t w = w0 > 0 ? w0 : 1;
+  // probes at g + (lane - 16) * w, clamped into [lo, hi)
+  const int64_t raw = (int64_t)g + ((int64_t)lane - 16) * (int64_t)w;
+  const int64_t lo_s = (int64_t)lo, hi_s = (int64_t)hi - 1;
+  const uint64_t p = (uint64_t)(raw < lo_s ? lo_s : (raw > hi_s ? hi_s : raw));
+  const bool t = (__ldg(ak + p) >> 1) <= (__ldg(bk + (d - 1 - p)) >> 1);
+  const uint32_t m = __ballot_sync(kFull, t);
+  // t is monotone in p (true below the split): the split lies after the last
+  // true probe and at or before the first false one
+  const int c = __popc(m);
+  const uint64_t plo = __shfl_sync(kFull, p, c > 0 ? c - 1 : 0);
+  const uint64_t phi = __shfl_sync(kFull, p, c < 32 ? c : 31);
+  if (c > 0 && plo + 1 > lo) lo = plo + 1;
+  if (c < 32 && phi < hi) hi = phi;
+#else
+  (void)ak; (void)bk; (void)d; (void)na; (void)nb; (void)lo; (void)hi;
+#endif
+}
+
 // First i in [lo, hi] with !((A[i]>>1) <= (B[d-1-i]>>1)): the number of A
 // records among the first d outputs (A first on ties). Whole warp.
 __device__ __forceinline__ uint64_t warp_merge_path(const uint32_t* __restrict__ ak,
@@ -255,11 +294,16 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel_t(
     uint64_t a = 0, a_first_end = 0;
     const uint64_t d_first_end = min(d + (uint64_t)kMergeTile, total);
     if (STAGES == 1) {  // one tile: its start and end splits searched together
-      warp_merge_path2(ak, bk, d, d > nb ? d - nb : 0, d < na ? d : na, d_first_end,
-                       d_first_end > nb ? d_first_end - nb : 0, d_first_end < na ? d_first_end : na,
-                       a, a_first_end);
+      uint64_t lo0 = d > nb ? d - nb : 0, hi0 = d < na ? d : na;
+      uint64_t lo1 = d_first_end > nb ? d_first_end - nb : 0,
+               hi1 = d_first_end < na ? d_first_end : na;
+      merge_path_guess(ak, bk, d, na, nb, lo0, hi0);
+      merge_path_guess(ak, bk, d_first_end, na, nb, lo1, hi1);
+      warp_merge_path2(ak, bk, d, lo0, hi0, d_first_end, lo1, hi1, a, a_first_end);
     } else {
-      a = warp_merge_path(ak, bk, d, d > nb ? d - nb : 0, d < na ? d : na);
+      uint64_t lo0 = d > nb ? d - nb : 0, hi0 = d < na ? d : na;
+      merge_path_guess(ak, bk, d, na, nb, lo0, hi0);
+      a = warp_merge_path(ak, bk, d, lo0, hi0);
     }
     if (lane == 0) MPROBE(2);
     for (uint64_t t = t_begin, k = 0; t < t_end; ++t, ++k) {
