@@ -136,6 +136,9 @@ __device__ __forceinline__ void consumers_sync() {
 #ifndef MERGE_GUESS
 #define MERGE_GUESS 1
 #endif
+#ifndef MERGE_GUESS_TILE
+#define MERGE_GUESS_TILE 1
+#endif
 // One round of the merge-path search probed around a GUESS of the split
 // instead of across [lo, hi]: for runs drawn from similar key distributions
 // the split of diagonal d lies near d * na / (na + nb), within a few sqrt(d);
@@ -143,17 +146,12 @@ __device__ __forceinline__ void consumers_sync() {
 // the guess missed -- still cut [lo, hi] at the window's edge. The predicate
 // is monotone, so the result is exact either way; only the number of
 // dependent rounds changes.
-__device__ __forceinline__ void merge_path_guess(const uint32_t* __restrict__ ak,
-                                                 const uint32_t* __restrict__ bk, uint64_t d,
-                                                 uint64_t na, uint64_t nb, uint64_t& lo,
-                                                 uint64_t& hi) {
+__device__ __forceinline__ void merge_path_guess_at(const uint32_t* __restrict__ ak,
+                                                    const uint32_t* __restrict__ bk, uint64_t d,
+                                                    uint64_t g, uint64_t w, uint64_t& lo,
+                                                    uint64_t& hi) {
 #if MERGE_GUESS
-  if (hi - lo <= 4096) return;
   const uint32_t lane = lane_id();
-  const double fr = (double)na / (double)(na + nb);
-  const uint64_t g = (uint64_t)((double)d * fr);
-  const uint64_t w0 = (uint64_t)(sqrt((double)d) * 0.125);
-  const uint64_t w = w0 > 0 ? w0 : 1;
   // probes at g + (lane - 16) * w, clamped into [lo, hi)
   const int64_t raw = (int64_t)g + ((int64_t)lane - 16) * (int64_t)w;
   const int64_t lo_s = (int64_t)lo, hi_s = (int64_t)hi - 1;
@@ -168,8 +166,19 @@ __device__ __forceinline__ void merge_path_guess(const uint32_t* __restrict__ ak
   if (c > 0 && plo + 1 > lo) lo = plo + 1;
   if (c < 32 && phi < hi) hi = phi;
 #else
-  (void)ak; (void)bk; (void)d; (void)na; (void)nb; (void)lo; (void)hi;
+  (void)ak; (void)bk; (void)d; (void)g; (void)w; (void)lo; (void)hi;
 #endif
+}
+
+// the first split of a CTA: guess d * na / (na + nb), probes ~sqrt(d) / 8 apart
+__device__ __forceinline__ void merge_path_guess(const uint32_t* __restrict__ ak,
+                                                 const uint32_t* __restrict__ bk, uint64_t d,
+                                                 uint64_t na, uint64_t nb, uint64_t& lo,
+                                                 uint64_t& hi) {
+  if (hi - lo <= 4096) return;
+  const double fr = (double)na / (double)(na + nb);
+  const uint64_t w0 = (uint64_t)(sqrt((double)d) * 0.125);
+  merge_path_guess_at(ak, bk, d, (uint64_t)((double)d * fr), w0 > 0 ? w0 : 1, lo, hi);
 }
 
 // First i in [lo, hi] with !((A[i]>>1) <= (B[d-1-i]>>1)): the number of A
@@ -311,6 +320,14 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel_t(
       uint64_t lo = d_end > nb ? d_end - nb : 0;
       lo = max(lo, a);
       uint64_t hi = min(a + (d_end - d), na);
+#if MERGE_GUESS_TILE
+      // the next split, guessed from the previous one: a + tile * na / (na + nb),
+      // probes 4 apart (the tile's split spreads ~sqrt(tile) / 2 around it)
+      if (!(STAGES == 1 && k == 0) && hi - lo > 128)
+        merge_path_guess_at(ak, bk, d_end,
+                            a + (uint64_t)((double)(d_end - d) * ((double)na / (double)(na + nb))),
+                            4, lo, hi);
+#endif
       const uint64_t a_end = (STAGES == 1 && k == 0) ? a_first_end : warp_merge_path(ak, bk, d_end, lo, hi);
       if (lane == 0 && k == 0) MPROBE(3);
       const int s = (int)(k % kStages);
