@@ -967,6 +967,17 @@ struct RankSmem {
   uint32_t start_d, size_d;
 };
 
+#ifndef BKT_VEC
+#define BKT_VEC 1
+#endif
+// the rank pass's loads of its region: kBktV4 groups of four consecutive
+// records per thread as 16-byte loads, then one record per load
+constexpr int kBktV4 = BKT_VEC ? (kBktItems / 4 < 2 ? kBktItems / 4 : 2) : 0;
+__device__ __forceinline__ uint32_t bkt_item(int i, uint32_t tid) {
+  if (i < 4 * kBktV4) return (uint32_t)(i / 4) * 4 * kBktThreads + 4 * tid + (uint32_t)(i % 4);
+  return (uint32_t)(4 * kBktV4) * kBktThreads + (uint32_t)(i - 4 * kBktV4) * kBktThreads + tid;
+}
+
 __global__ void __launch_bounds__(kBktThreads, kBktCtasPerSm) bucket_rank_kernel(
     BucketGeo G, uint32_t* __restrict__ ak, uint32_t* __restrict__ ap,
     const uint32_t* __restrict__ av, RawBatch in, uint64_t b, uint32_t* __restrict__ tk,
@@ -997,12 +1008,35 @@ __global__ void __launch_bounds__(kBktThreads, kBktCtasPerSm) bucket_rank_kernel
   ap += (uint64_t)d * G.capB;
   av += (uint64_t)d * G.capB;
   uint32_t kx[kBktItems], ky[kBktItems], kv[kBktItems];
+#if BKT_VEC
+  // records [0, kBktV4 * 4 * kBktThreads) as 16-byte loads (four consecutive
+  // records per thread and load), the rest one word per load; bkt_item(i)
+  // is item i's record index in the region
+#pragma unroll
+  for (int v = 0; v < kBktV4; ++v) {
+    const uint32_t r0 = (uint32_t)v * 4 * kBktThreads + 4 * tid;
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(ak + r0));
+    const uint4 b = __ldg(reinterpret_cast<const uint4*>(ap + r0));
+    const uint4 c = __ldg(reinterpret_cast<const uint4*>(av + r0));
+    kx[4 * v] = a.x; kx[4 * v + 1] = a.y; kx[4 * v + 2] = a.z; kx[4 * v + 3] = a.w;
+    ky[4 * v] = b.x; ky[4 * v + 1] = b.y; ky[4 * v + 2] = b.z; ky[4 * v + 3] = b.w;
+    kv[4 * v] = c.x; kv[4 * v + 1] = c.y; kv[4 * v + 2] = c.z; kv[4 * v + 3] = c.w;
+  }
+#pragma unroll
+  for (int i = 4 * kBktV4; i < kBktItems; ++i) {
+    const uint32_t r = bkt_item(i, tid);
+    kx[i] = __ldg(ak + r);
+    ky[i] = __ldg(ap + r);
+    kv[i] = __ldg(av + r);
+  }
+#else
 #pragma unroll
   for (int i = 0; i < kBktItems; ++i) {
     kx[i] = __ldg(ak + i * kBktThreads + tid);
     ky[i] = __ldg(ap + i * kBktThreads + tid);
     kv[i] = __ldg(av + i * kBktThreads + tid);
   }
+#endif
   {  // output start = records in the top digits below d1 (+ the sub-buckets
      // of d1 below d2)
     // kMsdDigits counts over kBktThreads threads: kDpt consecutive per thread
@@ -1155,7 +1189,7 @@ __global__ void __launch_bounds__(kBktThreads, kBktCtasPerSm) bucket_rank_kernel
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < kBktItems; ++i) {
-    const uint32_t p = i * kBktThreads + tid;
+    const uint32_t p = bkt_item(i, tid);
     if (p < size) {
       const uint32_t bin = (kx[i] >> bin_shift) & (kBins - 1);
       const uint32_t sh = (bin & 1u) * 16u;
@@ -1192,7 +1226,7 @@ __global__ void __launch_bounds__(kBktThreads, kBktCtasPerSm) bucket_rank_kernel
     uint32_t* __restrict__ gval = reinterpret_cast<uint32_t*>(S.kv[0]);
 #pragma unroll
     for (int i = 0; i < kBktItems; ++i) {
-      const uint32_t p = i * kBktThreads + tid;
+      const uint32_t p = bkt_item(i, tid);
       if (p < size) {
         const uint32_t g = half16(S.u.b.start, (kx[i] >> bin_shift) & (kBins - 1)) +
                            (ky[i] >> G.pos_bits);
@@ -1234,7 +1268,7 @@ __global__ void __launch_bounds__(kBktThreads, kBktCtasPerSm) bucket_rank_kernel
     if (tid == 0) atomicOr(overflow, 1u);
 #pragma unroll
     for (int i = 0; i < kBktItems; ++i) {  // (position, key) from the registers
-      const uint32_t p = i * kBktThreads + tid;
+      const uint32_t p = bkt_item(i, tid);
       if (p < size) S.kv[0][p] = make_uint2(ky[i] & pos_mask, kx[i]);
     }
     __syncthreads();
