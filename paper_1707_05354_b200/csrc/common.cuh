@@ -18,12 +18,12 @@ constexpr uint32_t kFull = 0xFFFFFFFFu;
 
 // Fence-key index of a level (the
 // paper's future-work direction PAPER.md:1043-1046 without COLA's
-// inter-level pointers): F1[j] = K[8j], F2[j] = F1[32j] = K[256j],
-// F3[j] = F2[32j] = K[8192j] (full key variables). A lower_bound then reads
+// inter-level pointers): F1[j] = K[16j], F2[j] = F1[32j] = K[512j],
+// F3[j] = F2[32j] = K[16384j] (full key variables; F1_STEP = 8 halves them). A lower_bound then reads
 // F3 (shared memory), one 128-byte line of F2, one of F1 and one 32-byte
 // sector of K instead of log2(n) dependent probes.
 #ifndef F1_STEP
-#define F1_STEP 8
+#define F1_STEP 16
 #endif
 constexpr int kF1Step = F1_STEP;  // 8 or 16 (query.cu's group counts)
 static_assert(kF1Step == 8 || kF1Step == 16, "F1_STEP");

@@ -204,7 +204,26 @@ __device__ __forceinline__ uint32_t grp_line_count(const uint32_t* __restrict__ 
 // For every lane: records of the kF1Step-record group K[kF1Step*gi ..)
 // (within n) below x. 16-byte aligned K: kF1Step/4 lanes x 16 B per query;
 // otherwise kF1Step lanes x 4 B per query.
-constexpr uint32_t kGL = kF1Step / 4;  // lanes per query, aligned groups
+constexpr uint32_t kGL = 2;                  // lanes per query, aligned groups
+constexpr uint32_t kKPL = kF1Step / kGL;     // keys per lane: 4 or 8
+// entries of K[base .. base + kKPL) below x2 (16-byte loads, padded past n)
+__device__ __forceinline__ uint32_t lane_group_count(const uint32_t* __restrict__ K, uint64_t n,
+                                                     uint64_t base, uint32_t x2, uint64_t pol) {
+  uint32_t c = 0;
+#pragma unroll
+  for (uint32_t u = 0; u < kKPL / 4; ++u) {
+    const uint64_t b4 = base + 4 * u;
+    uint4 v = ldg_v4_pol(K + b4, pol);  // +16 words of slack
+    if (b4 + 4 > n) {  // the level's last group
+      if (b4 + 0 >= n) v.x = 0xFFFFFFFFu;
+      if (b4 + 1 >= n) v.y = 0xFFFFFFFFu;
+      if (b4 + 2 >= n) v.z = 0xFFFFFFFFu;
+      v.w = 0xFFFFFFFFu;
+    }
+    c += (v.x < x2) + (v.y < x2) + (v.z < x2) + (v.w < x2);
+  }
+  return c;
+}
 __device__ __forceinline__ uint32_t grp_group_count(const uint32_t* __restrict__ K, uint64_t n,
                                                     uint32_t gi, uint32_t x2, uint64_t strm) {
   const uint32_t lane = lane_id();
@@ -216,15 +235,7 @@ __device__ __forceinline__ uint32_t grp_group_count(const uint32_t* __restrict__
       const uint32_t src = (lane & ~(kGL - 1)) | r;  // round r: the lanes of a group serve its lane r
       const uint32_t gj = __shfl_sync(kFull, gi, src);
       const uint32_t xj = __shfl_sync(kFull, x2, src);
-      const uint64_t base = (uint64_t)gj * kF1Step + 4 * e;
-      uint4 v = ldg_v4_pol(K + base, strm);  // +16 words of slack
-      if (base + 4 > n) {  // the level's last group
-        if (base + 0 >= n) v.x = 0xFFFFFFFFu;
-        if (base + 1 >= n) v.y = 0xFFFFFFFFu;
-        if (base + 2 >= n) v.z = 0xFFFFFFFFu;
-        v.w = 0xFFFFFFFFu;
-      }
-      uint32_t c = (v.x < xj) + (v.y < xj) + (v.z < xj) + (v.w < xj);
+      uint32_t c = lane_group_count(K, n, (uint64_t)gj * kF1Step + kKPL * e, xj, strm);
 #pragma unroll
       for (uint32_t o = 1; o < kGL; o <<= 1) c += __shfl_xor_sync(kFull, c, o);
       if (e == (uint32_t)r) res = c;
@@ -348,24 +359,15 @@ __device__ __forceinline__ void warp_lower_bound_n(const LevelTable& T, const ui
     for (int r = 0; r < (int)kGL; ++r) {
       const uint32_t src = (lane & ~(kGL - 1)) | r;
       const uint32_t xj = __shfl_sync(kFull, x2, src);
-      uint4 v[NL];
-      uint64_t base[NL];
+      uint32_t t0[NL];
 #pragma unroll
       for (int j = 0; j < NL; ++j) {
         const uint32_t gj = __shfl_sync(kFull, l[j], src);
-        base[j] = (uint64_t)gj * kF1Step + 4 * hf;
-        v[j] = ldg_v4_pol(T.keys[j] + base[j], kpol);  // +16 words of slack
+        t0[j] = lane_group_count(T.keys[j], T.n[j], (uint64_t)gj * kF1Step + kKPL * hf, xj, kpol);
       }
 #pragma unroll
       for (int j = 0; j < NL; ++j) {
-        const uint64_t n = T.n[j];
-        if (base[j] + 4 > n) {  // the level's last group
-          if (base[j] + 0 >= n) v[j].x = 0xFFFFFFFFu;
-          if (base[j] + 1 >= n) v[j].y = 0xFFFFFFFFu;
-          if (base[j] + 2 >= n) v[j].z = 0xFFFFFFFFu;
-          v[j].w = 0xFFFFFFFFu;
-        }
-        uint32_t t = (v[j].x < xj) + (v[j].y < xj) + (v[j].z < xj) + (v[j].w < xj);
+        uint32_t t = t0[j];
 #pragma unroll
         for (uint32_t o = 1; o < kGL; o <<= 1) t += __shfl_xor_sync(kFull, t, o);
         if (hf == (uint32_t)r) c[j] = t;
