@@ -25,8 +25,8 @@ constexpr uint32_t kFull = 0xFFFFFFFFu;
 #ifndef F1_STEP
 #define F1_STEP 16
 #endif
-constexpr int kF1Step = F1_STEP;  // 8 or 16 (query.cu's group counts)
-static_assert(kF1Step == 8 || kF1Step == 16, "F1_STEP");
+constexpr int kF1Step = F1_STEP;  // 8, 16 or 32 (query.cu's group counts)
+static_assert(kF1Step == 8 || kF1Step == 16 || kF1Step == 32, "F1_STEP");
 constexpr int kFanout = 32;
 inline __host__ __device__ uint64_t idx_f1_len(uint64_t n) { return (n + kF1Step - 1) / kF1Step; }
 inline __host__ __device__ uint64_t idx_f2_len(uint64_t n) { return (idx_f1_len(n) + kFanout - 1) / kFanout; }
