@@ -40,6 +40,20 @@ namespace gpulsm {
 
 namespace {
 
+#ifndef GPULSM_QIN_STREAM
+#define GPULSM_QIN_STREAM 1
+#endif
+// lookup / count inputs are read once: evict-first, so the 64-128 MB of keys
+// of a query batch do not push the levels' fence-key index out of L2 (the
+// range kernels keep the default: their writing pass re-reads k2)
+__device__ __forceinline__ uint32_t ldq(const uint32_t* p) {
+#if GPULSM_QIN_STREAM
+  return ldg_pol(p, l2_policy_stream());
+#else
+  return __ldg(p);
+#endif
+}
+
 constexpr int kQThreads = 512;
 constexpr int kQCtasPerSm = 2;
 constexpr uint32_t kSent = 0xFFFFFFFFu;  // > any original key (<= 2^31-1)
@@ -400,7 +414,7 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) lookup_kernel(
   for (uint64_t base = gw * 32; base < nq; base += nw * 32) {
     const uint64_t i = base + lane;
     const bool act = i < nq;
-    const uint32_t x = act ? __ldg(q + i) : 0u;
+    const uint32_t x = act ? ldq(q + i) : 0u;
     bool done = !act;
     uint32_t v = LSM_NOT_FOUND;
     uint8_t f = 0;
@@ -441,7 +455,7 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) lookup_n_kernel(
   for (uint64_t base = gw * 32; base < nq; base += nw * 32) {
     const uint64_t i = base + lane;
     const bool act = i < nq;
-    const uint32_t x = act ? __ldg(q + i) : 0u;
+    const uint32_t x = act ? ldq(q + i) : 0u;
     uint64_t p[NL];
     warp_lower_bound_n<NL>(T, sF3, x, strm, p);
     uint32_t kk[NL];
@@ -864,7 +878,7 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) count_kernel(
   for (uint64_t base = gw * 32; base < nq; base += nw * 32) {
     const uint64_t i = base + lane;
     const bool act = i < nq;
-    const uint32_t a = act ? __ldg(k1 + i) : 1u, z = act ? __ldg(k2 + i) : 0u;
+    const uint32_t a = act ? ldq(k1 + i) : 1u, z = act ? ldq(k2 + i) : 0u;
     uint64_t pos[CAP];
     bounds<NL>(T, sF3, a, a > z, pos, L, l2_policy_stream());
     uint32_t c;
@@ -1020,7 +1034,7 @@ __global__ void __launch_bounds__(kQThreads, kQCtasPerSm) order_kernel(
   for (uint64_t wb = gw * 32; wb < nq; wb += nw * 32) {  // warp-uniform loop
     const uint64_t i = wb + lane;
     const bool act = i < nq;
-    const uint32_t x = act ? __ldg(q + i) : 0u;
+    const uint32_t x = act ? ldq(q + i) : 0u;
     uint64_t pos[CAP];
     uint32_t head[CAP];  // successor: key (kSent = none); predecessor: key + 1 (0 = none)
 #pragma unroll
