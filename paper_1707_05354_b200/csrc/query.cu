@@ -27,7 +27,7 @@
 // accesses required in all binary searches". Every lower_bound
 // here goes through the level's fence-key index (common.cuh): a binary search
 // of F3 in shared memory, then one 128-byte line of F2, one of F1 and one
-// 32-byte sector of K. Each warp serves 32 queries and searches
+// 64-byte group of K (16 keys, F1_STEP). Each warp serves 32 queries and searches
 // cooperatively: for each of its 32 queries the warp loads the whole line in
 // one coalesced load and a ballot counts the fences below the query, so a
 // step issues 32 independent line loads per warp.
@@ -169,7 +169,7 @@ __device__ __forceinline__ uint32_t line_count(const uint32_t* __restrict__ a, u
 }
 
 // Lane-private lower_bound on the original key through the fence index:
-// F3 tree (shared memory) -> F2 line -> F1 line -> 8-record group of K.
+// F3 tree (shared memory) -> F2 line -> F1 line -> kF1Step-record group of K.
 // Used where lanes diverge (the successor/predecessor run skips).
 __device__ __forceinline__ uint64_t idx_lower_bound(const LvView& L, uint32_t x) {
   if (x > 0x7FFFFFFFu) return L.n;  // above every original key (R8)
@@ -304,7 +304,7 @@ __device__ __noinline__ uint64_t warp_lower_bound(const LvView L, uint32_t x, ui
 
 // ---- the same lower_bound in NL levels at once (2 <= NL <= 4) ----
 // The searches of different levels are independent, so each step (F3 tree,
-// F2 line, F1 line, 8-record group) is taken for all levels before the next:
+// F2 line, F1 line, kF1Step-record group) is taken for all levels before the next:
 // the line loads of all levels are in flight together and a query pays ~4
 // memory round trips instead of 4 per level (ncu: the post-cleanup 3-level
 // lookup ran at ~55 % of the random-read ceiling, latency-bound).
